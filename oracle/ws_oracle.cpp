@@ -1,0 +1,426 @@
+// oracle/ws_oracle.cpp -- plain, slow CPU oracle of the Warpspeed estimator.
+//
+// TEST INFRASTRUCTURE ONLY (see ws_oracle.h).  Nothing here is shared with
+// the CUDA path.  Each function names the passage of PAPER.md (P:line) or the
+// reading of SURVEY.md section 8(c) (Qnn) it writes out.  The structure
+// follows SURVEY.md 8(c) "Specification of the integer core" steps O1..O10.
+//
+// Deliberately naive: every (thread, instruction) address of every scope is
+// generated and inserted into std::set; counts are set sizes; overlaps are
+// std::set_intersection sizes.
+#include "ws_oracle.h"
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <iterator>
+#include <map>
+#include <set>
+#include <thread>
+#include <utility>
+#include <vector>
+
+namespace {
+
+typedef std::array<int64_t, 3> V3;
+typedef std::pair<int64_t, int64_t> Key;  // (field, sector or line): fields never alias
+
+int64_t floordiv(int64_t a, int64_t b) {  // floor(a / b), b > 0  ("floor divide")
+  int64_t q = a / b;
+  if ((a % b) != 0 && (a < 0)) q -= 1;
+  return q;
+}
+int64_t floormod(int64_t a, int64_t b) { return a - floordiv(a, b) * b; }
+int64_t ceildiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- O4: address map
+// A = align + elem * sum_d pitch[d] * cell[d]   (P:157-161 with the base pointer
+// replaced by the field alignment; worked example P:540-545).
+int64_t address(const wso_field& f, const V3& cell) {
+  return f.align_bytes + f.elem_bytes * (f.pitch[0] * cell[0] + f.pitch[1] * cell[1] + f.pitch[2] * cell[2]);
+}
+
+// ---------------------------------------------------------------- O5 pieces
+// Number of distinct 32 B sectors among addresses (CL32Visitor).
+int64_t unique_sectors(const std::vector<int64_t>& a, int64_t sector_bytes) {
+  std::set<int64_t> s;
+  for (int64_t x : a) s.insert(floordiv(x, sector_bytes));
+  return (int64_t)s.size();
+}
+
+// Wavefronts of one half-warp instruction (Listing lst:griditeration
+// BankConflictVisitor P:408-417 with the far-address rule P:393-395; Q2-Q4):
+//   U = sorted unique bank words (A div bank_bytes)
+//   split U greedily into clusters; a new cluster starts at u when
+//   (u - cluster_start) * bank_bytes >= pair_window_bytes
+//   cycles = sum over clusters of max over banks of |{u in cluster : u mod n_banks = bank}|
+int64_t halfwarp_wavefronts(const std::vector<int64_t>& a, const wso_gpu& g) {
+  std::set<int64_t> U;
+  for (int64_t x : a) U.insert(floordiv(x, g.bank_bytes));
+  int64_t cycles = 0;
+  std::vector<int64_t> banks(g.n_banks, 0);
+  bool open = false;
+  int64_t start = 0;
+  for (int64_t u : U) {
+    if (open && (u - start) * g.bank_bytes >= g.pair_window_bytes) {
+      cycles += *std::max_element(banks.begin(), banks.end());
+      std::fill(banks.begin(), banks.end(), 0);
+      open = false;
+    }
+    if (!open) { start = u; open = true; }
+    banks[floormod(u, g.n_banks)] += 1;
+  }
+  if (open) cycles += *std::max_element(banks.begin(), banks.end());
+  return cycles;
+}
+
+// Gompertz-form hit rate R(O) = a * exp(-b * exp(-c * O))
+double hit_rate(const double abc[3], double O) { return abc[0] * std::exp(-abc[1] * std::exp(-abc[2] * O)); }
+
+int64_t log2_exact(int64_t v) {
+  int64_t l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return ((int64_t(1) << l) == v) ? l : -1;
+}
+
+// ---------------------------------------------------------------- O1: validation
+int64_t check_kernel(const wso_kernel& K) {
+  if (K.n_fields < 1 || K.n_fields > 64 || K.n_accesses < 1 || K.n_accesses > 128) return WSO_EINVAL;
+  for (int64_t i = 0; i < K.n_fields; ++i) {
+    const wso_field& f = K.fields[i];
+    if (log2_exact(f.elem_bytes) < 0 || f.elem_bytes > 32) return WSO_EINVAL;
+    for (int d = 0; d < 3; ++d)
+      if (f.extent[d] < 1) return WSO_EINVAL;
+    // x contiguous, rows and planes disjoint (row-major, padding allowed)
+    if (f.pitch[0] != 1 || f.pitch[1] < f.extent[0] || f.pitch[2] < f.pitch[1] * f.extent[1]) return WSO_EINVAL;
+  }
+  for (int d = 0; d < 3; ++d)
+    if (K.dom_lo[d] < 0 || K.dom_hi[d] <= K.dom_lo[d]) return WSO_EINVAL;
+  for (int64_t i = 0; i < K.n_accesses; ++i) {
+    const wso_access& a = K.accesses[i];
+    if (a.field < 0 || a.field >= K.n_fields || (a.is_store != 0 && a.is_store != 1)) return WSO_EINVAL;
+    const wso_field& f = K.fields[a.field];
+    for (int d = 0; d < 3; ++d)  // every active cell + offset stays inside the field
+      if (K.dom_lo[d] + a.off[d] < 0 || K.dom_hi[d] - 1 + a.off[d] >= f.extent[d]) return WSO_EBOUNDS;
+  }
+  return WSO_OK;
+}
+
+// ---------------------------------------------------------------- O3: instruction table
+// One instruction per distinct (field, kind, kappa + o) over the fold cube
+// kappa in [0,f) and the accesses o of that field and kind (Q7).
+struct Instr {
+  int64_t field, is_store;
+  V3 r;
+  std::vector<V3> kappas;  // {kappa in [0,f) : r - kappa is an access offset of (field, kind)}
+};
+
+struct Plan {
+  V3 b, f, lo, hi, G;
+  int64_t T, N, k, W, s, n_sets, Ly0, Lz0;
+  std::vector<Instr> instr;
+};
+
+bool in_offsets(const wso_kernel& K, int64_t field, int64_t is_store, const V3& o) {
+  for (int64_t i = 0; i < K.n_accesses; ++i) {
+    const wso_access& a = K.accesses[i];
+    if (a.field == field && a.is_store == is_store && a.off[0] == o[0] && a.off[1] == o[1] && a.off[2] == o[2])
+      return true;
+  }
+  return false;
+}
+
+// Block id -> block coordinates in X-Y-Z scheduling order.
+V3 block_coord(const Plan& p, int64_t B) { return V3{B % p.G[0], (B / p.G[0]) % p.G[1], B / (p.G[0] * p.G[1])}; }
+// Thread index -> thread coordinates, tid = tx + bx*(ty + by*tz).
+V3 thread_coord(const Plan& p, int64_t t) { return V3{t % p.b[0], (t / p.b[0]) % p.b[1], t / (p.b[0] * p.b[1])}; }
+// Base cell of a thread: lo + (blockcoord * b + threadcoord) * f; it computes cells base + kappa.
+V3 base_cell(const Plan& p, int64_t B, int64_t t) {
+  V3 bc = block_coord(p, B), tc = thread_coord(p, t), c;
+  for (int d = 0; d < 3; ++d) c[d] = p.lo[d] + (bc[d] * p.b[d] + tc[d]) * p.f[d];
+  return c;
+}
+bool active(const Plan& p, const V3& cell) {  // guard clipping by the domain
+  for (int d = 0; d < 3; ++d)
+    if (cell[d] >= p.hi[d]) return false;
+  return true;
+}
+// Thread issues instruction r iff some active folded cell base+kappa has
+// r - kappa among the accesses of that field and kind (Q27).  The kappas with
+// r - kappa an access offset are listed once per instruction (I.kappas).
+bool issues(const Plan& p, const V3& base, const Instr& I) {
+  for (const V3& kap : I.kappas)
+    if (active(p, V3{base[0] + kap[0], base[1] + kap[1], base[2] + kap[2]})) return true;
+  return false;
+}
+int64_t instr_address(const wso_kernel& K, const V3& base, const Instr& I) {
+  V3 cell{base[0] + I.r[0], base[1] + I.r[1], base[2] + I.r[2]};
+  return address(K.fields[I.field], cell);
+}
+
+// ---------------------------------------------------------------- O2: geometry
+int64_t make_plan(const wso_kernel& K, const wso_gpu& g, const wso_config& c, Plan& p, wso_result& r) {
+  for (int d = 0; d < 3; ++d) {
+    if (c.block[d] < 1 || c.fold[d] < 1) return WSO_EINVAL;
+    p.b[d] = c.block[d];
+    p.f[d] = c.fold[d];
+    p.lo[d] = K.dom_lo[d];
+    p.hi[d] = K.dom_hi[d];
+  }
+  for (int64_t i = 0; i < K.n_fields; ++i)
+    if (K.fields[i].elem_bytes > g.sector_bytes) return WSO_EINVAL;
+  p.T = p.b[0] * p.b[1] * p.b[2];
+  if (p.T > g.max_thr_blk) return WSO_ELIMIT;
+  if (p.f[0] * p.f[1] * p.f[2] > 64) return WSO_ELIMIT;
+  for (int d = 0; d < 3; ++d) p.G[d] = ceildiv(p.hi[d] - p.lo[d], p.b[d] * p.f[d]);
+  p.N = p.G[0] * p.G[1] * p.G[2];
+  // Resident blocks per SM (Q10): threads, blocks and registers,
+  // allocated at warp granularity.
+  if (c.blocks_per_sm > 0) {
+    p.k = c.blocks_per_sm;
+  } else {
+    int64_t Ta = ceildiv(p.T, 32) * 32;
+    p.k = std::min(g.max_thr_sm / Ta, g.max_blk_sm);
+    if (K.regs_per_thread > 0) p.k = std::min(p.k, g.regs_sm / (K.regs_per_thread * Ta));
+  }
+  if (p.k < 1) return WSO_ELIMIT;
+  // Wave: W resident blocks; representative wave centred on the grid's
+  // central block (Q11).
+  p.W = std::min(p.N, g.n_sm * p.k);
+  int64_t cen = p.G[0] / 2 + p.G[0] * (p.G[1] / 2 + p.G[1] * (p.G[2] / 2));
+  p.s = std::min(std::max(cen - p.W / 2, int64_t(0)), p.N - p.W);
+  p.n_sets = std::min(g.n_sm, p.W);
+  // Layer thread sets: everything scheduled since the wave's y-neighbour block
+  // row / z-neighbour block layer (Q13).
+  p.Ly0 = std::max(int64_t(0), p.s - p.G[0]);
+  p.Lz0 = std::max(int64_t(0), p.s - p.G[0] * p.G[1]);
+  // O3: instruction table
+  for (int64_t fi = 0; fi < K.n_fields; ++fi)
+    for (int64_t st = 0; st < 2; ++st) {
+      std::set<V3> R;
+      for (int64_t i = 0; i < K.n_accesses; ++i) {
+        const wso_access& a = K.accesses[i];
+        if (a.field != fi || a.is_store != st) continue;
+        for (int64_t kz = 0; kz < p.f[2]; ++kz)
+          for (int64_t ky = 0; ky < p.f[1]; ++ky)
+            for (int64_t kx = 0; kx < p.f[0]; ++kx) R.insert(V3{kx + a.off[0], ky + a.off[1], kz + a.off[2]});
+      }
+      for (const V3& rr : R) {
+        Instr I{fi, st, rr, {}};
+        for (int64_t kz = 0; kz < p.f[2]; ++kz)
+          for (int64_t ky = 0; ky < p.f[1]; ++ky)
+            for (int64_t kx = 0; kx < p.f[0]; ++kx)
+              if (in_offsets(K, fi, st, V3{rr[0] - kx, rr[1] - ky, rr[2] - kz})) I.kappas.push_back(V3{kx, ky, kz});
+        p.instr.push_back(I);
+      }
+    }
+  if (p.instr.size() > 1024) return WSO_ELIMIT;
+  r.grid[0] = p.G[0];
+  r.grid[1] = p.G[1];
+  r.grid[2] = p.G[2];
+  r.k = p.k;
+  r.wave_blocks = p.W;
+  r.n_smsets = p.n_sets;
+  r.wave_first_block = p.s;
+  r.n_instr = (int64_t)p.instr.size();
+  return WSO_OK;
+}
+
+size_t intersection_size(const std::set<Key>& a, const std::set<Key>& b) {
+  std::vector<Key> out;
+  std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
+  return out.size();
+}
+
+// F_L: every sector touched by any instruction (loads and stores) of the
+// blocks [B0, B1) (Q15: L2 is write-back, stored data can be hit).
+std::set<Key> layer_footprint(const wso_kernel& K, const wso_gpu& g, const Plan& p, int64_t B0, int64_t B1) {
+  std::set<Key> F;
+  for (int64_t B = B0; B < B1; ++B)
+    for (int64_t t = 0; t < p.T; ++t) {
+      V3 base = base_cell(p, B, t);
+      for (const Instr& I : p.instr)
+        if (issues(p, base, I)) F.insert(Key(I.field, floordiv(instr_address(K, base, I), g.sector_bytes)));
+    }
+  return F;
+}
+
+int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso_result& r) {
+  r = wso_result();
+  int64_t st = check_kernel(K);
+  Plan p;
+  if (st == WSO_OK) st = make_plan(K, g, c, p, r);
+  if (st != WSO_OK) {
+    wso_result z = wso_result();
+    z.status = st;
+    r = z;
+    return st;
+  }
+  const int64_t sec_per_line = g.line_bytes / g.sector_bytes;
+
+  // ------------------------------------------------------------ O5-O7 over the wave
+  int64_t wf = 0, req_ld = 0, req_st = 0, lup = 0;
+  std::vector<std::set<Key>> SMsec(p.n_sets), SMlin(p.n_sets);
+  std::set<Key> WLD, WST, WLIN;
+  const int64_t n_warps = ceildiv(p.T, 32);
+  for (int64_t B = p.s; B < p.s + p.W; ++B) {
+    const int64_t j = (B - p.s) % g.n_sm;  // round-robin SM assignment (Q9)
+    for (int64_t t = 0; t < p.T; ++t) {   // active cells = lattice updates of the wave
+      V3 base = base_cell(p, B, t);
+      for (int64_t kz = 0; kz < p.f[2]; ++kz)
+        for (int64_t ky = 0; ky < p.f[1]; ++ky)
+          for (int64_t kx = 0; kx < p.f[0]; ++kx)
+            if (active(p, V3{base[0] + kx, base[1] + ky, base[2] + kz})) ++lup;
+    }
+    for (int64_t w = 0; w < n_warps; ++w) {
+      for (const Instr& I : p.instr) {
+        // warp instruction: unique sectors over issuing lanes (Q5);
+        // stores are written through and counted per instruction
+        std::vector<int64_t> A;
+        for (int64_t lane = 0; lane < 32; ++lane) {
+          int64_t t = w * 32 + lane;
+          if (t >= p.T) break;
+          V3 base = base_cell(p, B, t);
+          if (issues(p, base, I)) A.push_back(instr_address(K, base, I));
+        }
+        if (I.is_store) req_st += unique_sectors(A, g.sector_bytes);
+        else req_ld += unique_sectors(A, g.sector_bytes);
+        // half-warps: wavefronts (Q6: loads and stores)
+        for (int64_t h = 0; h < 32 / g.half_warp; ++h) {
+          std::vector<int64_t> H;
+          for (int64_t lane = h * g.half_warp; lane < (h + 1) * g.half_warp; ++lane) {
+            int64_t t = w * 32 + lane;
+            if (t >= p.T) break;
+            V3 base = base_cell(p, B, t);
+            if (issues(p, base, I)) H.push_back(instr_address(K, base, I));
+          }
+          wf += halfwarp_wavefronts(H, g);
+        }
+        for (int64_t a : A) {
+          Key ks(I.field, floordiv(a, g.sector_bytes)), kl(I.field, floordiv(a, g.line_bytes));
+          if (!I.is_store) {
+            SMsec[j].insert(ks);  // L1: SM-resident set (Q8)
+            SMlin[j].insert(kl);  // 128 B allocation granularity (Q18: loads only)
+            WLD.insert(ks);       // wave load footprint
+          } else {
+            WST.insert(ks);       // wave store footprint
+          }
+          WLIN.insert(kl);
+        }
+      }
+    }
+  }
+  int64_t sm_sec = 0, sm_lin = 0;
+  for (int64_t j = 0; j < p.n_sets; ++j) {
+    sm_sec += (int64_t)SMsec[j].size();
+    sm_lin += (int64_t)SMlin[j].size();
+  }
+
+  // ------------------------------------------------------------ O8 layer sets
+  std::set<Key> Fy = layer_footprint(K, g, p, p.Ly0, p.s);
+  std::set<Key> Fz = layer_footprint(K, g, p, p.Lz0, p.s);
+  std::set<Key> Fy_lines, Fz_lines;
+  for (const Key& k : Fy) Fy_lines.insert(Key(k.first, floordiv(k.second, sec_per_line)));
+  for (const Key& k : Fz) Fz_lines.insert(Key(k.first, floordiv(k.second, sec_per_line)));
+
+  r.lup_wave = lup;
+  r.l1_wavefronts = wf;
+  r.l1_req_ld_sectors = req_ld;
+  r.l1_req_st_sectors = req_st;
+  r.sm_ld_sectors = sm_sec;
+  r.sm_ld_lines = sm_lin;
+  r.wave_ld_sectors = (int64_t)WLD.size();
+  r.wave_st_sectors = (int64_t)WST.size();
+  r.wave_lines = (int64_t)WLIN.size();
+  r.ly_lines = (int64_t)Fy_lines.size();
+  r.lz_lines = (int64_t)Fz_lines.size();
+  r.ov_y = (int64_t)intersection_size(WLD, Fy);
+  r.ov_z = (int64_t)intersection_size(WLD, Fz);
+  r.addr_evals = (p.W + (p.s - p.Lz0)) * p.T * (int64_t)p.instr.size();
+
+  // ------------------------------------------------------------ O9 model (FP64)
+  // Volumes in sectors; x sector_bytes gives bytes.
+  const double SB = (double)g.sector_bytes, LB = (double)g.line_bytes;
+  const double n = (double)lup;
+  // L1 level: Eq.4 O = V_alloc / V_cache with V_alloc the mean SM-set line
+  // footprint; Eq.2/3/5: V_down = V_comp + (1 - R) * (V_up - V_comp).
+  r.O_l1 = ((double)sm_lin * LB / (double)p.n_sets) / (double)g.l1_bytes;
+  r.R_l1 = hit_rate(g.hit_abc[0], r.O_l1);
+  double v_red_l1 = std::max(0.0, (double)req_ld - (double)sm_sec);
+  double l2l1_ld = (double)sm_sec + (1.0 - r.R_l1) * v_red_l1;
+  double l1l2_st = (double)req_st;  // write-through
+  // L2 level: effective capacity of one section (Q31)
+  double l2eff = (double)g.l2_bytes / (double)g.l2_sections;
+  r.O_y = (double)Fy_lines.size() * LB / l2eff;
+  r.O_z = (double)Fz_lines.size() * LB / l2eff;
+  r.R_y = hit_rate(g.hit_abc[1], r.O_y);
+  r.R_z = hit_rate(g.hit_abc[2], r.O_z);
+  double hits = r.R_y * (double)r.ov_y + r.R_z * (double)(r.ov_z - r.ov_y);  // Q16
+  // stores: redundant partial stores missing in L2 are read back (Q19)
+  double red_st = std::max(0.0, (double)req_st - (double)r.wave_st_sectors);
+  r.O_st = (double)r.wave_lines * LB / l2eff;
+  r.R_st = hit_rate(g.hit_abc[3], r.O_st);
+  double cap_st = (1.0 - r.R_st) * red_st;
+  double dram_ld = (double)r.wave_ld_sectors - hits + cap_st;
+  double dram_st = (double)r.wave_st_sectors;
+  // per lattice update
+  r.l1_cyc_per_lup = (double)wf / n;
+  r.l2_ld_Bpl = SB * l2l1_ld / n;
+  r.l2_st_Bpl = SB * l1l2_st / n;
+  r.dram_ld_Bpl = SB * dram_ld / n;
+  r.dram_st_Bpl = SB * dram_st / n;
+  // limiters (Q1): seconds per lattice update
+  r.t_l1 = (double)wf / (n * (double)g.n_sm * g.clock_hz);
+  r.t_l2 = SB * (l2l1_ld + l1l2_st) / (n * g.l2_bw);
+  r.t_dram = SB * (dram_ld + dram_st) / (n * g.dram_bw);
+  double t = std::max(r.t_l1, std::max(r.t_l2, r.t_dram));
+  // limiter: argmax, ties resolved DRAM > L2 > L1 (Q29)
+  r.limiter = (r.t_dram >= t) ? 2 : (r.t_l2 >= t) ? 1 : 0;
+  double cells = 1.0;
+  for (int d = 0; d < 3; ++d) cells *= (double)(p.hi[d] - p.lo[d]);
+  r.t_pred = t * cells;
+  r.status = WSO_OK;
+  return WSO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t wso_check_kernel(const wso_kernel* k) { return check_kernel(*k); }
+
+int64_t wso_estimate(const wso_kernel* k, const wso_gpu* g, const wso_config* c, wso_result* r) {
+  return estimate(*k, *g, *c, *r);
+}
+
+void wso_estimate_batch(const wso_kernel* k, const wso_gpu* g, const wso_config* c, int64_t n, wso_result* r,
+                        int64_t n_threads) {
+  if (n_threads < 1) n_threads = 1;
+  std::atomic<int64_t> next(0);
+  auto work = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      estimate(*k, *g, c[i], r[i]);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int64_t i = 1; i < n_threads; ++i) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
+
+int64_t wso_address(const wso_field* f, const int64_t cell[3]) { return address(*f, V3{cell[0], cell[1], cell[2]}); }
+
+int64_t wso_unique_sectors(const int64_t* a, int64_t n, int64_t sector_bytes) {
+  return unique_sectors(std::vector<int64_t>(a, a + n), sector_bytes);
+}
+
+int64_t wso_halfwarp_wavefronts(const int64_t* a, int64_t n, const wso_gpu* g) {
+  return halfwarp_wavefronts(std::vector<int64_t>(a, a + n), *g);
+}
+
+double wso_hit_rate(const double abc[3], double O) { return hit_rate(abc, O); }
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+"""Independent brute-force re-implementation used to PIN the oracle.
+
+Written separately from oracle/ws_oracle.cpp and structured differently, so a
+plausible slip in either (wrong pitch index, transposed operand, wrong block
+ordering, dropped term) shows up as a mismatch:
+
+* footprints are computed the paper's way ("numpy meshgrid ... unique"),
+  over *cells* rather than (thread, instruction) pairs: the footprint of a set
+  of threads is {addr(c + o) : c an active cell of those threads, o an offset
+  of the field/kind} -- every active cell c = base+kappa issues instruction
+  r = kappa + o, so the two definitions name the same set;
+* a sectored, fully-associative LRU cache replays the trace
+  (SPEC.md cachesim-oracle) for the capacity pins.
+
+Only small grids (the whole thing is numpy over every cell of a block range).
+"""
+from __future__ import annotations
+
+import itertools
+from collections import OrderedDict
+
+import numpy as np
+
+
+def geometry(kernel, gpu, cfg):
+    (bx, by, bz), (fx, fy, fz), kov = cfg
+    lo = np.array(kernel["dom_lo"], dtype=np.int64)
+    hi = np.array(kernel["dom_hi"], dtype=np.int64)
+    b = np.array([bx, by, bz], dtype=np.int64)
+    f = np.array([fx, fy, fz], dtype=np.int64)
+    T = int(bx * by * bz)
+    G = -(-(hi - lo) // (b * f))
+    N = int(np.prod(G))
+    if kov:
+        k = kov
+    else:
+        Ta = -(-T // 32) * 32
+        k = min(gpu["max_thr_sm"] // Ta, gpu["max_blk_sm"])
+        if kernel["regs"]:
+            k = min(k, gpu["regs_sm"] // (kernel["regs"] * Ta))
+    W = min(N, gpu["n_sm"] * k)
+    cx, cy, cz = G[0] // 2, G[1] // 2, G[2] // 2
+    centre = int(cx + G[0] * (cy + G[1] * cz))
+    s = min(max(centre - W // 2, 0), N - W)
+    return dict(lo=lo, hi=hi, b=b, f=f, T=T, G=G, N=N, k=k, W=W, s=s,
+                Ly=(max(0, s - int(G[0])), s), Lz=(max(0, s - int(G[0] * G[1])), s))
+
+
+def block_cells(geo, blocks):
+    """Active cells (n,3) of the given block ids (numpy meshgrid over the box)."""
+    out = []
+    G, b, f, lo, hi = geo["G"], geo["b"], geo["f"], geo["lo"], geo["hi"]
+    for B in blocks:
+        bc = np.array([B % G[0], (B // G[0]) % G[1], B // (G[0] * G[1])], dtype=np.int64)
+        start = lo + bc * b * f
+        stop = np.minimum(start + b * f, hi)
+        xs, ys, zs = [np.arange(start[d], stop[d]) for d in range(3)]
+        Z, Y, X = np.meshgrid(zs, ys, xs, indexing="ij")
+        out.append(np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1))
+    if not out:
+        return np.zeros((0, 3), dtype=np.int64)
+    return np.concatenate(out)
+
+
+def addresses(field, cells):
+    p = np.array(field["pitch"], dtype=np.int64)
+    return field["align"] + field["elem"] * (cells @ p)
+
+
+def footprint(kernel, cells, kinds, shift):
+    """Set of (field, addr >> shift) over cells + offsets of the given kinds."""
+    keys = set()
+    for fi, fld in enumerate(kernel["fields"]):
+        offs = [o for (f, st, o) in kernel["accesses"] if f == fi and st in kinds]
+        if not offs or len(cells) == 0:
+            continue
+        allc = np.concatenate([cells + np.array(o, dtype=np.int64) for o in offs])
+        a = np.unique(addresses(fld, allc) >> shift)
+        keys.update((fi, int(v)) for v in a)
+    return keys
+
+
+def set_counts(kernel, gpu, cfg):
+    """Union scopes a4-a6 by cell enumeration (the oracle does (thread, instr))."""
+    geo = geometry(kernel, gpu, cfg)
+    ls = int(np.log2(gpu["sector_bytes"]))
+    ll = int(np.log2(gpu["line_bytes"]))
+    s, W, nsm = geo["s"], geo["W"], gpu["n_sm"]
+    wave = list(range(s, s + W))
+    wcells = block_cells(geo, wave)
+    WLD = footprint(kernel, wcells, (0,), ls)
+    WST = footprint(kernel, wcells, (1,), ls)
+    WLIN = footprint(kernel, wcells, (0, 1), ll)
+    sm_sec = sm_lin = 0
+    for j in range(min(nsm, W)):
+        cells = block_cells(geo, wave[j::nsm])
+        sm_sec += len(footprint(kernel, cells, (0,), ls))
+        sm_lin += len(footprint(kernel, cells, (0,), ll))
+    FY = footprint(kernel, block_cells(geo, range(*geo["Ly"])), (0, 1), ls)
+    FZ = footprint(kernel, block_cells(geo, range(*geo["Lz"])), (0, 1), ls)
+    d = ll - ls
+    return dict(lup_wave=len(wcells), sm_ld_sectors=sm_sec, sm_ld_lines=sm_lin,
+                wave_ld_sectors=len(WLD), wave_st_sectors=len(WST), wave_lines=len(WLIN),
+                ly_lines=len({(f, v >> d) for f, v in FY}), lz_lines=len({(f, v >> d) for f, v in FZ}),
+                ov_y=len(WLD & FY), ov_z=len(WLD & FZ), k=geo["k"], wave_blocks=W,
+                wave_first_block=s, grid=tuple(int(g) for g in geo["G"]))
+
+
+# ------------------------------------------------------------- per-thread traces
+def thread_trace(kernel, geo, B, t):
+    """(field, kind, cell - base, addr) issued by one thread, in instruction order (deduplicated
+    per thread, i.e. register reuse under folding)."""
+    G, b, f, lo, hi = geo["G"], geo["b"], geo["f"], geo["lo"], geo["hi"]
+    bc = np.array([B % G[0], (B // G[0]) % G[1], B // (G[0] * G[1])])
+    tc = np.array([t % b[0], (t // b[0]) % b[1], t // (b[0] * b[1])])
+    base = lo + (bc * b + tc) * f
+    out = []
+    for fi, fld in enumerate(kernel["fields"]):
+        for st in (0, 1):
+            offs = [o for (ff, s_, o) in kernel["accesses"] if ff == fi and s_ == st]
+            seen = set()
+            for kap in itertools.product(range(f[0]), range(f[1]), range(f[2])):
+                c = base + np.array(kap)
+                if np.any(c >= hi):
+                    continue
+                for o in offs:
+                    cell = tuple(int(v) for v in c + np.array(o))
+                    if cell in seen:
+                        continue
+                    seen.add(cell)
+                    rel = tuple(int(v) for v in np.array(cell) - base)
+                    out.append((fi, st, rel, int(addresses(fld, np.array([cell]))[0])))
+    return out
+
+
+def l1_counts(kernel, gpu, cfg):
+    """a3 via per-warp dictionaries keyed by instruction identity (field, kind, cell - thread base)."""
+    geo = geometry(kernel, gpu, cfg)
+    T = geo["T"]
+    SB, BB, NB, HW, PW = (gpu["sector_bytes"], gpu["bank_bytes"], gpu["n_banks"],
+                          gpu["half_warp"], gpu["pair_window_bytes"])
+    req = [0, 0]
+    wf = 0
+    for B in range(geo["s"], geo["s"] + geo["W"]):
+        for w in range(-(-T // 32)):
+            lanes = [t for t in range(32 * w, min(32 * w + 32, T))]
+            # instruction key: (field, kind, relative cell) -> lane -> addr
+            per_instr = {}
+            for t in lanes:
+                for (fi, st, rel, a) in thread_trace(kernel, geo, B, t):
+                    per_instr.setdefault((fi, st, rel), {})[t] = a
+            for (fi, st, rel), lane_addr in per_instr.items():
+                req[st] += len({a // SB for a in lane_addr.values()})
+                for h in range(32 // HW):
+                    words = sorted({a // BB for t, a in lane_addr.items() if h * HW <= t - 32 * w < (h + 1) * HW})
+                    clusters, cur = [], []
+                    for u in words:
+                        if cur and (u - cur[0]) * BB >= PW:
+                            clusters.append(cur)
+                            cur = []
+                        cur.append(u)
+                    if cur:
+                        clusters.append(cur)
+                    for c in clusters:
+                        cnt = [0] * NB
+                        for u in c:
+                            cnt[u % NB] += 1
+                        wf += max(cnt)
+    return dict(l1_wavefronts=wf, l1_req_ld_sectors=req[0], l1_req_st_sectors=req[1])
+
+
+class SectoredLRU:
+    """Fully-associative LRU over lines, 32 B valid bits per sector."""
+
+    def __init__(self, capacity_bytes, line_bytes=128, sector_bytes=32):
+        self.cap = max(1, capacity_bytes // line_bytes)
+        self.lb, self.sb = line_bytes, sector_bytes
+        self.lines = OrderedDict()
+        self.misses = 0
+        self.requests = 0
+
+    def access(self, key_sector):
+        field, sec = key_sector
+        line = (field, sec // (self.lb // self.sb))
+        self.requests += 1
+        if line in self.lines:
+            self.lines.move_to_end(line)
+            if sec in self.lines[line]:
+                return
+            self.lines[line].add(sec)
+            self.misses += 1
+            return
+        self.misses += 1
+        self.lines[line] = {sec}
+        if len(self.lines) > self.cap:
+            self.lines.popitem(last=False)
+
+
+def replay_blocks(kernel, gpu, cfg, blocks, cache, kinds=(0,), count_from=None):
+    """Replay every thread of `blocks` in schedule order through `cache`.
+    Returns misses incurred by blocks >= count_from (all if None)."""
+    geo = geometry(kernel, gpu, cfg)
+    SB = gpu["sector_bytes"]
+    base_miss = None
+    for B in blocks:
+        if count_from is not None and B == count_from:
+            base_miss = cache.misses
+        for t in range(geo["T"]):
+            for (fi, st, _rel, a) in thread_trace(kernel, geo, B, t):
+                if st in kinds:
+                    cache.access((fi, a // SB))
+    return cache.misses - (base_miss or 0)

@@ -1,0 +1,385 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Each test names the passage it pins.  None of these expected values comes
+from the CUDA path; they are the paper's printed numbers
+(tests/golden/paper_values.json), closed forms derived in DESIGN.md, or an
+independent brute-force implementation (tests/indep_model.py).
+"""
+import json
+import math
+import os
+
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+import indep_model as M
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+# --------------------------------------------------------------------- a2: address map
+def test_address_map_paper_example():
+    """A[tidx][tidy+1] on a 100-wide array with a -1 element alignment."""
+    g = GOLD["address_map_example"]
+    fld = {"extent": (100, 10, 1), "pitch": (1, 100, 1000),
+           "align": g["align_elems"] * g["elem"], "elem": g["elem"]}
+    for tx, ty, idx in g["cases"]:
+        a = O.address(fld, (tx, ty + 1, 0))
+        assert a // 32 == idx, (tx, ty)
+
+
+def test_address_map_pystencils_expression():
+    """src_W = src + (tx + bx*BX + 1) + (ty + by*BY)*w (element units)."""
+    w = 37
+    fld = {"extent": (w, 20, 3), "pitch": (1, w, w * 20), "align": 0, "elem": 1}
+    BX, BY = 8, 4
+    for tx, bx, ty, by in [(0, 0, 0, 0), (3, 2, 1, 3), (7, 1, 3, 0)]:
+        expect = (tx + bx * BX + 1) + (ty + by * BY) * w
+        assert O.address(fld, (tx + bx * BX + 1, ty + by * BY, 0)) == expect
+
+
+# --------------------------------------------------------------------- a3: sectors
+def _one_load_kernel(n, align, fold=(1, 1, 1)):
+    fld = {"extent": (n * fold[0] + 8, 2, 2), "pitch": (1, n * fold[0] + 8, 2 * (n * fold[0] + 8)),
+           "align": align, "elem": 8}
+    return {"name": "oneload", "fields": [fld], "accesses": [(0, 0, (0, 0, 0))],
+            "dom_lo": (0, 0, 0), "dom_hi": (n * fold[0], 1, 1), "regs": 0, "flops": 0.0}
+
+
+def test_sectors_32_contiguous_doubles():
+    """P:474-475 + BJ north_star: 32 contiguous doubles, 256 B aligned -> 8 sectors, 2 lines;
+    shifted by 8 B -> 9 sectors, 3 lines."""
+    g = W.gpu_v100()
+    r = O.estimate(_one_load_kernel(32, 0), g, ((32, 1, 1), (1, 1, 1), 1))
+    assert (r["l1_req_ld_sectors"], r["wave_ld_sectors"], r["sm_ld_sectors"], r["sm_ld_lines"]) == (8, 8, 8, 2)
+    r = O.estimate(_one_load_kernel(32, 8), g, ((32, 1, 1), (1, 1, 1), 1))
+    assert (r["l1_req_ld_sectors"], r["wave_ld_sectors"], r["sm_ld_lines"]) == (9, 9, 3)
+
+
+def test_sectors_strided_warp():
+    """Stride-2 doubles (x fold 2): each warp instruction spans 16 sectors (P:389 pattern)."""
+    g = W.gpu_v100()
+    r = O.estimate(_one_load_kernel(32, 0, fold=(2, 1, 1)), g, ((32, 1, 1), (2, 1, 1), 1))
+    assert r["n_instr"] == 2
+    assert r["l1_req_ld_sectors"] == 2 * 16
+    assert r["wave_ld_sectors"] == 16          # the union is the 64 contiguous doubles
+    assert r["l1_wavefronts"] == 2 * 2 * 2     # 2 instr x 2 half-warps x 2 wavefronts
+
+
+def test_unique_sectors_helper():
+    assert O.unique_sectors([8 * i for i in range(32)]) == 8
+    assert O.unique_sectors([8 + 8 * i for i in range(32)]) == 9
+    assert O.unique_sectors([16 * i for i in range(32)]) == 16
+    assert O.unique_sectors([128 * i for i in range(32)]) == 32
+
+
+# --------------------------------------------------------------------- a3: wavefronts
+def test_halfwarp_wavefronts_paper_examples():
+    """strides 1/2/16 doubles -> 1/2/16 cycles per half warp."""
+    g = W.gpu_a100()
+    for stride, cyc in GOLD["halfwarp_wavefronts"]["stride_elems_to_cycles"]:
+        assert O.halfwarp_wavefronts([8 * stride * i for i in range(16)], g) == cyc
+
+
+def test_halfwarp_far_pairing():
+    """non-conflicting addresses > 1024 B apart cannot pair: two 8-double runs
+    4096 B apart -> 2 wavefronts; inside the window they pair -> 1."""
+    g = W.gpu_a100()
+    a = [8 * i for i in range(8)] + [4096 + 64 + 8 * i for i in range(8)]
+    assert O.halfwarp_wavefronts(a, g) == 2
+    b = [8 * i for i in range(8)] + [64 + 8 * i for i in range(8)]
+    assert O.halfwarp_wavefronts(b, g) == 1
+    # duplicates are one address (unique words, Listing 1 'unique(addresses)')
+    assert O.halfwarp_wavefronts([0] * 16, g) == 1
+    assert O.halfwarp_wavefronts([], g) == 0
+
+
+def test_wavefronts_listing1_when_span_below_window():
+    """Within a 1024 B span the rule is exactly Listing 1: max over banks of unique words."""
+    import random
+    g = W.gpu_a100()
+    rng = random.Random(5)
+    for _ in range(200):
+        words = [rng.randrange(0, 128) for _ in range(16)]
+        a = [8 * u for u in words]
+        cnt = [0] * 16
+        for u in set(words):
+            cnt[u % 16] += 1
+        assert O.halfwarp_wavefronts(a, g) == max(cnt)
+
+
+def _k25_small(nx=64, ny=32, nz=32):
+    return W.stencil_star(nx, ny, nz, 4, regs=64)
+
+
+def test_l1_cycles_25pt_closed_form():
+    """bx >= 16 -> one wavefront per half-warp instruction: 26 instr x 2 = 52 cycles
+    per warp-wide LUP (1.625/LUP); 2z folding: 44 instr / 2 LUP -> 1.375/LUP; bx < 16 with a
+    row pitch >= 1024 B: 16/bx wavefronts per half-warp instruction."""
+    k = _k25_small(256, 16, 16)   # row pitch 264*8 = 2112 B >= 1024 B
+    g = W.gpu_a100()
+    r = O.estimate(k, g, ((32, 4, 2), (1, 1, 1), 1))
+    assert r["n_instr"] == 26
+    assert r["l1_cyc_per_lup"] == pytest.approx(1.625, abs=0)
+    r = O.estimate(k, g, ((32, 4, 2), (1, 1, 2), 1))
+    assert r["n_instr"] == 44
+    assert r["l1_cyc_per_lup"] == pytest.approx(1.375, abs=0)
+    for bx in (8, 4, 2, 1):
+        r = O.estimate(k, g, ((bx, 16, 2), (1, 1, 1), 1))
+        assert r["l1_cyc_per_lup"] == pytest.approx(26 * 2 * (16 // bx) / 32, abs=0), bx
+
+
+# --------------------------------------------------------------------- a5/a6 closed forms
+XS = 256  # row width of the series domain
+
+
+def _series_setup(d, ry, rz):
+    """domain 256x32x64, 16 SMs, k=1 -> 16-block waves of (256,1,1)
+    blocks folded d-deep in z: a wave d layers deep spanning full rows."""
+    k = W.stencil_star(XS, 32, 64, 4, regs=0)
+    g = W.gpu_a100()
+    g["n_sm"] = 16
+    g["hit_abc"][1] = [ry, 0.0, 0.0]     # R_y == ry for every O
+    g["hit_abc"][2] = [rz, 0.0, 0.0]     # R_z == rz
+    return k, g, ((XS, 1, 1), (1, 1, d), 1)
+
+
+@pytest.mark.parametrize("d,vol", GOLD["wave_depth_series"]["depth_to_BperLup"])
+def test_wave_depth_series(d, vol):
+    """without z-layer reuse a d-deep wave loads (d+8)/d values per LUP:
+    72/40/24/16/(12)/10 B/Lup.  Exact value here: 8(d+8)/d + 8*8/XS (the x-halo of
+    the XS-wide rows, 8 extra elements per row never reused; rows are whole sectors)."""
+    k, g, c = _series_setup(d, 1.0, 0.0)
+    r = O.estimate(k, g, c)
+    assert vol == pytest.approx(8 * (d + 8) / d)
+    assert r["dram_ld_Bpl"] == pytest.approx(vol + 64 / XS, rel=1e-12)
+    assert r["dram_st_Bpl"] == pytest.approx(8.0, rel=1e-12)
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8, 16, 32])
+def test_layer_condition_floor(d):
+    """with full z-layer reuse the stencil needs one load and one store per
+    point: 8 B/Lup (+ the same 64/XS B/Lup x-halo)."""
+    k, g, c = _series_setup(d, 1.0, 1.0)
+    r = O.estimate(k, g, c)
+    assert r["dram_ld_Bpl"] == pytest.approx(GOLD["stencil_floor"]["load_BperLup"] + 64 / XS, rel=1e-12)
+    assert r["dram_st_Bpl"] == pytest.approx(GOLD["stencil_floor"]["store_BperLup"], rel=1e-12)
+    # no reuse at all: (d+8)/d values plus the y-halo of the 16-row wave
+    k, g, c = _series_setup(d, 0.0, 0.0)
+    r0 = O.estimate(k, g, c)
+    assert r0["dram_ld_Bpl"] > r["dram_ld_Bpl"]
+
+
+def test_lbm15_floors():
+    """D3Q15 streaming moves 15 doubles in and 15 out per LUP (240 B/Lup);
+    with perfect reuse the phase field adds >= 8 B/Lup load; every config loads >= 128 B/Lup
+    and stores >= 128 B/Lup (15 PDFs + FD result)."""
+    k = W.lbm15(24)
+    g = W.gpu_a100()
+    g["n_sm"] = 8
+    for i in range(4):
+        g["hit_abc"][i] = [1.0, 0.0, 0.0]
+    for c in [((8, 2, 2), (1, 1, 1), 1), ((32, 1, 1), (1, 1, 1), 1), ((1, 8, 4), (1, 1, 1), 1)]:
+        r = O.estimate(k, g, c)
+        assert r["dram_ld_Bpl"] >= 128.0 - 1e-9
+        assert r["dram_st_Bpl"] >= 128.0 - 1e-9
+        assert r["dram_ld_Bpl"] + r["dram_st_Bpl"] >= GOLD["d3q15_streaming"]["pdf_BperLup_read_plus_write"]
+
+
+# --------------------------------------------------------------------- a7 arithmetic
+def test_gompertz_form():
+    """R(O) = a exp(-b exp(-cO)); R(0) = a e^{-b}; SURVEY Q17 default anchors."""
+    assert O.hit_rate([0.9, 2.0, -1.0], 0.0) == pytest.approx(0.9 * math.exp(-2.0), rel=1e-15)
+    L1, L2y, L2z, L2st = W.HIT_ABC_DEFAULT
+    assert O.hit_rate(L1, 1.0) == pytest.approx(0.90, abs=2e-3)
+    assert O.hit_rate(L1, 2.0) == pytest.approx(0.20, abs=2e-3)
+    assert O.hit_rate(L2z, 2.0) == pytest.approx(0.05, abs=2e-3)
+    assert O.hit_rate(L2st, 1.0) == pytest.approx(0.95, abs=2e-3)
+    # monotone decreasing ("With increasing oversubscription ... towards zero")
+    for abc in W.HIT_ABC_DEFAULT:
+        vals = [O.hit_rate(abc, o / 4) for o in range(40)]
+        assert all(a >= b for a, b in zip(vals, vals[1:]))
+        assert vals[-1] < 0.01
+
+
+def test_model_homogeneity():
+    """scaling every bandwidth and the clock by s scales predicted time by 1/s."""
+    k = W.k7(16)
+    g = W.gpu_v100()
+    c = ((32, 2, 2), (1, 1, 1), 0)
+    r1 = O.estimate(k, g, c)
+    g2 = dict(g)
+    s = 3.0
+    g2["dram_bw"], g2["l2_bw"], g2["clock_hz"] = g["dram_bw"] * s, g["l2_bw"] * s, g["clock_hz"] * s
+    r2 = O.estimate(k, g2, c)
+    assert r2["t_pred"] == pytest.approx(r1["t_pred"] / s, rel=1e-12)
+    assert r2["limiter"] == r1["limiter"]
+
+
+def test_model_eq5_and_limiter_arithmetic():
+    """Eq. 5 and the max-limiter (Q1) recomputed from the integer fields."""
+    k = W.k7(24)
+    g = W.gpu_v100()
+    for c in W.space_k7()[:15]:
+        r = O.estimate(k, g, c)
+        n = r["lup_wave"]
+        v_red = max(0, r["l1_req_ld_sectors"] - r["sm_ld_sectors"])
+        l2l1 = r["sm_ld_sectors"] + (1 - r["R_l1"]) * v_red
+        assert r["l2_ld_Bpl"] == pytest.approx(32 * l2l1 / n, rel=1e-12)
+        t = max(r["t_l1"], r["t_l2"], r["t_dram"])
+        assert r["t_pred"] == pytest.approx(t * 24 ** 3, rel=1e-12)
+        assert [r["t_l1"], r["t_l2"], r["t_dram"]][r["limiter"]] == t
+
+
+# --------------------------------------------------------------------- a1 combinatorics
+def test_sweep_sizes():
+    s = GOLD["sweep_constraint"]
+    assert len(W.block_shapes(1024)) == s["n_shapes_1024"]
+    assert len(W.block_shapes(512)) == s["n_shapes_512"]
+    assert len(W.space_stencil_paper()) == s["n_shapes_1024"] * s["n_folds"]
+
+
+def test_sequential_layer_condition_numbers():
+    """P:762, P:996 in MiB."""
+    s = GOLD["sequential_layer_condition"]
+    assert 640 * 512 * 8 * 3 == s["bytes_640x512x3"] == int(s["MiB"] * 2 ** 20)
+    assert int(math.sqrt(10 * 2 ** 20 / (9 * 8))) == s["xy_limit_9_layers_10MiB"]
+
+
+def test_wave_size_a100():
+    """108 SMs, 2048 threads/SM, 1024-thread blocks, no register limit -> 216-block wave."""
+    k = W.k25(128)
+    k["regs"] = 0
+    r = O.estimate(k, W.gpu_a100(), ((32, 32, 1), (1, 1, 1), 0))
+    assert r["k"] == 2
+    assert r["wave_blocks"] == 216
+
+
+def test_config_errors():
+    """ABI conventions: T > max_thr_blk -> ELIMIT, fold 0 -> EINVAL."""
+    k = W.k7(16)
+    g = W.gpu_v100()
+    assert O.estimate(k, g, ((32, 8, 8), (1, 1, 1), 0))["status"] == 2
+    assert O.estimate(k, g, ((32, 1, 1), (0, 1, 1), 0))["status"] == 1
+    bad = W.k7(16)
+    bad["accesses"] = bad["accesses"] + [(0, 0, (2, 0, 0))]
+    assert O.check_kernel(bad) == 3
+
+
+# --------------------------------------------------------------------- independent brute force
+SMALL_CASES = [
+    (W.k7(12), W.gpu_v100(), ((32, 2, 1), (1, 1, 1), 0)),
+    (W.stencil_star(20, 10, 12, 4, regs=64), dict(W.gpu_a100(), n_sm=6), ((8, 4, 2), (1, 1, 2), 1)),
+    (W.stencil_star(20, 10, 12, 4, regs=64), dict(W.gpu_a100(), n_sm=5), ((4, 2, 4), (1, 2, 1), 2)),
+    (W.lbm15(6), dict(W.gpu_a100(), n_sm=3), ((4, 2, 2), (1, 1, 1), 1)),
+]
+
+
+@pytest.mark.parametrize("case", range(len(SMALL_CASES)))
+def test_oracle_vs_independent_sets(case):
+    k, g, c = SMALL_CASES[case]
+    r = O.estimate(k, g, c)
+    m = M.set_counts(k, g, c)
+    for key, v in m.items():
+        assert r[key] == v, key
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_oracle_vs_independent_random(seed):
+    k, g, c = W.random_kernel(seed, max_dom=9), W.random_gpu(seed), W.random_config(seed)
+    r = O.estimate(k, g, c)
+    if r["status"] != 0:
+        pytest.skip("config rejected")
+    m = M.set_counts(k, g, c)
+    for key, v in m.items():
+        assert r[key] == v, key
+    l1 = M.l1_counts(k, g, c)
+    for key, v in l1.items():
+        assert r[key] == v, key
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_oracle_vs_independent_l1(case):
+    k, g, c = SMALL_CASES[case]
+    r = O.estimate(k, g, c)
+    l1 = M.l1_counts(k, g, c)
+    for key, v in l1.items():
+        assert r[key] == v, key
+
+
+def test_lru_infinite_capacity_pins():
+    """SURVEY 8c pins for a4-a6 via a trace-driven sectored LRU:
+    cold misses of the wave = wave_ld_sectors; replaying the L_z then the wave,
+    misses inside the wave = wave_ld_sectors - ov_z; with L_y: - ov_y."""
+    k = W.stencil_star(16, 8, 12, 4, regs=64)
+    g = dict(W.gpu_a100(), n_sm=4)
+    c = ((8, 2, 2), (1, 1, 1), 1)
+    r = O.estimate(k, g, c)
+    geo = M.geometry(k, g, c)
+    s, Wb = geo["s"], geo["W"]
+    big = 1 << 40
+    assert M.replay_blocks(k, g, c, range(s, s + Wb), M.SectoredLRU(big)) == r["wave_ld_sectors"]
+    assert M.replay_blocks(k, g, c, range(s, s + Wb), M.SectoredLRU(big), kinds=(1,)) == r["wave_st_sectors"]
+    lz0, ly0 = geo["Lz"][0], geo["Ly"][0]
+    # stores of the layer set must also be cached (write-back L2, Q15): replay loads and stores
+    # of the layer blocks, loads of the wave
+    cache = M.SectoredLRU(big)
+    M.replay_blocks(k, g, c, range(lz0, s), cache, kinds=(0, 1))
+    before = cache.misses
+    M.replay_blocks(k, g, c, range(s, s + Wb), cache, kinds=(0,))
+    assert cache.misses - before == r["wave_ld_sectors"] - r["ov_z"]
+    cache = M.SectoredLRU(big)
+    M.replay_blocks(k, g, c, range(ly0, s), cache, kinds=(0, 1))
+    before = cache.misses
+    M.replay_blocks(k, g, c, range(s, s + Wb), cache, kinds=(0,))
+    assert cache.misses - before == r["wave_ld_sectors"] - r["ov_y"]
+    # per SM set with infinite capacity: misses = sm_ld_sectors
+    tot = 0
+    for j in range(r["n_smsets"]):
+        tot += M.replay_blocks(k, g, c, list(range(s, s + Wb))[j::g["n_sm"]], M.SectoredLRU(big))
+    assert tot == r["sm_ld_sectors"]
+
+
+def test_lru_capacity_monotone():
+    """Finite capacity: misses never decrease as capacity shrinks (S:536 invariant) and are
+    bounded below by the compulsory footprint."""
+    k = W.stencil_star(16, 8, 8, 4, regs=64)
+    g = dict(W.gpu_a100(), n_sm=4)
+    c = ((8, 2, 2), (1, 1, 1), 1)
+    r = O.estimate(k, g, c)
+    geo = M.geometry(k, g, c)
+    blocks = range(geo["s"], geo["s"] + geo["W"])
+    prev = None
+    for cap in [1 << 30, 64 * 1024, 16 * 1024, 4 * 1024, 1024]:
+        m = M.replay_blocks(k, g, c, blocks, M.SectoredLRU(cap))
+        assert m >= r["wave_ld_sectors"]
+        if prev is not None:
+            assert m >= prev
+        prev = m
+
+
+# --------------------------------------------------------------------- invariants
+@pytest.mark.parametrize("seed", range(20, 40))
+def test_invariants_random(seed):
+    k, g, c = W.random_kernel(seed), W.random_gpu(seed), W.random_config(seed)
+    r = O.estimate(k, g, c)
+    if r["status"] != 0:
+        return
+    assert r["sm_ld_lines"] <= r["sm_ld_sectors"] <= 4 * r["sm_ld_lines"]
+    assert r["wave_ld_sectors"] <= r["sm_ld_sectors"] <= r["l1_req_ld_sectors"]
+    assert r["wave_st_sectors"] <= r["l1_req_st_sectors"]
+    assert r["ov_y"] <= r["ov_z"] <= r["wave_ld_sectors"]
+    assert r["ly_lines"] <= r["lz_lines"]
+    # shifting every field by 128 B changes nothing (sectors/lines/banks are 128 B periodic)
+    k2 = dict(k, fields=[dict(f, align=f["align"] + 128) for f in k["fields"]])
+    r2 = O.estimate(k2, g, c)
+    for key in M.set_counts.__code__.co_varnames[:0] or ["l1_wavefronts", "l1_req_ld_sectors", "sm_ld_sectors",
+                                                          "wave_ld_sectors", "wave_lines", "lz_lines", "ov_z"]:
+        assert r2[key] == r[key]
+    # access order permutation
+    k3 = dict(k, accesses=list(reversed(k["accesses"])))
+    r3 = O.estimate(k3, g, c)
+    for key in ["l1_wavefronts", "l1_req_ld_sectors", "l1_req_st_sectors", "sm_ld_lines", "wave_ld_sectors",
+                "wave_st_sectors", "ly_lines", "lz_lines", "ov_y", "ov_z", "t_pred"]:
+        assert r3[key] == r[key]
