@@ -1,0 +1,171 @@
+/* include/ws.h -- C ABI of libwsb200.so, the B200-native hot path of the
+ * Warpspeed data-volume estimator (Ernst et al., arXiv 2204.14242,
+ * "Analytical Performance Estimation during Code Generation on Modern GPUs").
+ *
+ * The estimator takes, per the paper's statement of the problem (PAPER.md
+ * P:163-166), only address expressions (here: per-field constant relative
+ * cell offsets), a launch configuration (block, folding; grid is
+ * derived), field sizes and field alignments, plus
+ * hardware parameters (Table tab:av100).  For every configuration
+ * it counts distinct 32 B sectors / 128 B lines at the warp-instruction, SM-
+ * resident-set, wave and layer-set scopes, evaluates the capacity
+ * model (Eqs. 1-5) and the max-limiter performance model
+ * (P:262-281), and ranks the configurations.  Exact semantics:
+ * DESIGN.md ("Readings") and SURVEY.md section 8.
+ *
+ * Conventions (all functions):
+ *  - Every function returns ws_status; WS_OK = 0.  On a call-level error the
+ *    message is available from ws_last_error(ctx) until the next call on ctx.
+ *  - The caller owns every array passed in or out; the library never keeps a
+ *    pointer to caller memory after a call returns (describe calls deep-copy).
+ *  - Per-configuration problems never fail a batch: they set ws_result.status
+ *    (WS_EINVAL, WS_ELIMIT, WS_EUNKNOWN_ID) and leave that record's numbers 0.
+ *  - A context is bound to one CUDA device and one stream and is not
+ *    thread-safe.  Results are byte-identical for identical inputs.
+ *  - There is no CPU fallback: a context cannot be created without a CUDA
+ *    device (WS_ECUDA).
+ */
+#ifndef WS_H
+#define WS_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  WS_OK = 0,
+  WS_EINVAL = 1,      /* malformed argument / descriptor                                    */
+  WS_ELIMIT = 2,      /* a documented limit is exceeded (threads/block, occupancy k = 0, ...) */
+  WS_EBOUNDS = 3,     /* an access of an active cell leaves its field              */
+  WS_ENOMEM = 4,      /* device or host allocation failed                                   */
+  WS_ECUDA = 5,       /* CUDA runtime error (no device, launch failure, ...)                */
+  WS_EUNKNOWN_ID = 6  /* kernel_id / gpu_id not described in this context                   */
+} ws_status;
+
+typedef struct ws_ctx ws_ctx;
+
+/* Create a context on CUDA device `cuda_device`; work is issued on
+ * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream). */
+ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out);
+void ws_destroy(ws_ctx* ctx);
+const char* ws_last_error(const ws_ctx* ctx);
+/* Change the stream later work is issued on (e.g. torch's current stream). */
+ws_status ws_set_stream(ws_ctx* ctx, void* cuda_stream);
+
+/* ------------------------------------------------------------------ kernels
+ * Field: a row-major array, x fastest.  Byte address of element (x,y,z):
+ *   align_bytes + elem_bytes * (x*pitch[0] + y*pitch[1] + z*pitch[2])
+ * (P:157-161 with the unknown base pointer replaced by the alignment).
+ * Requirements: pitch[0] == 1, pitch[1] >= extent[0], pitch[2] >= pitch[1]*extent[1]
+ * (rows and planes never overlap); elem_bytes in {1,2,4,8,16,32}.  */
+typedef struct {
+  int64_t extent[3];
+  int64_t pitch[3];
+  int64_t align_bytes;   /* may be negative (P:540 example uses -8) */
+  uint32_t elem_bytes;
+  uint32_t pad;
+} ws_field;
+
+/* One access `field[cell + off]` (relative field access). */
+typedef struct {
+  uint32_t field;
+  uint32_t is_store;     /* 0 = load, 1 = store */
+  int32_t off[3];
+} ws_access;
+
+typedef struct {
+  uint32_t n_fields;           /* 1..64  */
+  uint32_t n_accesses;         /* 1..128 */
+  const ws_field* fields;
+  const ws_access* accesses;
+  int64_t dom_lo[3], dom_hi[3];/* iteration domain (field-index coords); guard clipping P:171-172 */
+  uint32_t regs_per_thread;    /* 0 = ignore the register limit on occupancy (Q10) */
+  uint32_t pad;
+  double flops_per_lup;        /* carried, not a limiter */
+} ws_kernel;
+
+/* Deep-copies the description.  Errors: WS_EINVAL (counts, layout, elem,
+ * empty domain), WS_EBOUNDS (dom +- offsets leaves a field), WS_ELIMIT (a
+ * field has more than 16 distinct x-offset runs).  *kernel_id receives a new id. */
+ws_status ws_describe_kernel(ws_ctx* ctx, const ws_kernel* k, uint32_t* kernel_id);
+
+/* ------------------------------------------------------------------ hardware
+ * Table tab:av100 plus the cache geometry of P:373-395. */
+typedef struct {
+  uint32_t n_sm;
+  uint32_t max_thr_sm, max_blk_sm, max_thr_blk, regs_sm;   /* occupancy limits (Q10) */
+  uint32_t sector_bytes;       /* 32  (power of two, >= every elem_bytes used)  */
+  uint32_t line_bytes;         /* 128 (power of two, multiple of sector_bytes)   */
+  uint32_t n_banks;            /* 16  (power of two)                            */
+  uint32_t bank_bytes;         /* 8   (power of two)                            */
+  uint32_t half_warp;          /* 16  (power of two dividing 32)                */
+  uint32_t pair_window_bytes;  /* 1024                                  */
+  uint32_t l2_sections;        /* 2 for the split A100 L2: L2_eff = l2_bytes / l2_sections */
+  uint64_t l1_bytes, l2_bytes;
+  double clock_hz, dram_bw, l2_bw;   /* Hz, bytes/s, bytes/s */
+  double hit_abc[4][3];        /* R(O) = a exp(-b exp(-c O)) for L1, L2-over-y, L2-over-z, L2-store */
+} ws_gpu;
+
+/* Deep-copies.  Errors: WS_EINVAL (zero / non-power-of-two geometry, ...). */
+ws_status ws_describe_gpu(ws_ctx* ctx, const ws_gpu* g, uint32_t* gpu_id);
+
+/* ------------------------------------------------------------------ configurations */
+typedef struct {
+  uint32_t kernel_id, gpu_id;
+  uint32_t block[3];           /* threads per block (X,Y,Z)            */
+  uint32_t fold[3];            /* thread folding factors; prod <= 64       */
+  uint32_t blocks_per_sm;      /* 0 = derive the occupancy k (Q10)                */
+  uint32_t pad;
+} ws_config;                   /* 40 bytes */
+
+typedef struct {
+  int32_t status;              /* WS_OK or the per-config error                   */
+  uint32_t limiter;            /* 0 = L1, 1 = L2, 2 = DRAM                        */
+  uint32_t grid[3];            /* blocks per dimension                            */
+  uint32_t k;                  /* resident blocks per SM                          */
+  uint32_t wave_blocks;        /* W                                               */
+  uint32_t n_smsets;           /* min(n_sm, W)                                    */
+  uint32_t n_instr;            /* instructions per thread after folding dedupe    */
+  uint32_t rank;               /* filled by ws_rank                               */
+  uint64_t wave_first_block;   /* s                                               */
+  uint64_t lup_wave;           /* active cells (lattice updates) of the wave      */
+  uint64_t l1_wavefronts;      /* a3: sum of half-warp wavefronts (loads+stores)  */
+  uint64_t l1_req_ld_sectors;  /* a3: per-warp-instruction unique load sectors    */
+  uint64_t l1_req_st_sectors;  /* a3: per-warp-instruction unique store sectors   */
+  uint64_t sm_ld_sectors;      /* a4: sum over SM sets of unique load sectors     */
+  uint64_t sm_ld_lines;        /* a4: sum over SM sets of unique load lines       */
+  uint64_t wave_ld_sectors;    /* a5 */
+  uint64_t wave_st_sectors;    /* a5 */
+  uint64_t wave_lines;         /* a5: lines of all wave accesses                  */
+  uint64_t ly_lines, lz_lines; /* a6: lines of the layer sets                     */
+  uint64_t ov_y, ov_z;         /* a6: |wave load sectors  intersect  layer sectors| */
+  uint64_t addr_evals;         /* (W + |L_z|) * T * n_instr: plain-definition work units */
+  double O_l1, R_l1, O_y, R_y, O_z, R_z, O_st, R_st;
+  double l1_cyc_per_lup, l2_ld_Bpl, l2_st_Bpl, dram_ld_Bpl, dram_st_Bpl;
+  double t_l1, t_l2, t_dram;   /* seconds per lattice update                      */
+  double t_pred;               /* seconds for the whole domain                    */
+} ws_result;                   /* 296 bytes */
+
+/* Host pointers; synchronous.  Copies cfgs to the device, runs the whole
+ * device path, copies n results back. */
+ws_status ws_estimate(ws_ctx* ctx, const ws_config* cfgs, size_t n, ws_result* out);
+
+/* Device pointers (cfgs: n ws_config, out: n ws_result in device memory);
+ * enqueued on the context stream, returns without synchronising. */
+ws_status ws_estimate_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_result* d_out);
+
+/* Rank by (t_pred ascending, index ascending); failed configs rank last.
+ * Fills res[i].rank and top_idx[0..min(k,n)) with the indices of the best.
+ * ws_rank: host pointers, synchronous.  ws_rank_async: device pointers, no sync. */
+ws_status ws_rank(ws_ctx* ctx, ws_result* res, size_t n, size_t k, uint32_t* top_idx);
+ws_status ws_rank_async(ws_ctx* ctx, ws_result* d_res, size_t n, size_t k, uint32_t* d_top_idx);
+
+/* Number of kernel launches the last ws_estimate[_async] / ws_rank[_async]
+ * call enqueued (for the bench's gpu_launches count). */
+uint32_t ws_last_launch_count(const ws_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

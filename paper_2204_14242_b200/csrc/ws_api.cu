@@ -1,0 +1,371 @@
+// ws_api.cu -- host side of libwsb200.so: the C ABI of include/ws.h.
+// Validates and deep-copies descriptors, owns device scratch, enqueues the
+// device path (ws_kernels.cu) on the context stream.  No arithmetic of the
+// estimator runs here: every step a1-a8 is a kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ws_internal.cuh"
+
+using namespace wsb;
+
+struct ws_ctx {
+  int device = 0;
+  int n_sm_dev = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::vector<DKernel> hk;
+  std::vector<DGpu> hg;
+  std::vector<int64_t> chunk_bound;  // per kernel: max row chunks of one configuration
+  DKernel* dk = nullptr;
+  DGpu* dg = nullptr;
+  size_t cap_k = 0, cap_g = 0;
+  bool dirty = false;
+  void* scratch = nullptr;
+  size_t scratch_cap = 0;
+  void* io = nullptr;  // host-path staging for configs + results
+  size_t io_cap = 0;
+  uint32_t last_launches = 0;
+};
+
+namespace {
+
+ws_status fail(ws_ctx* c, ws_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+ws_status cuda_fail(ws_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, WS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+int lg2(uint64_t v) {  // exact log2 or -1
+  if (v == 0 || (v & (v - 1))) return -1;
+  int l = 0;
+  while ((1ull << l) < v) ++l;
+  return l;
+}
+
+ws_status upload(ws_ctx* c) {
+  if (!c->dirty) return WS_OK;
+  cudaError_t e;
+  if (c->hk.size() > c->cap_k) {
+    if (c->dk) cudaFree(c->dk);
+    c->cap_k = std::max<size_t>(c->hk.size() * 2, 4);
+    if ((e = cudaMalloc(&c->dk, c->cap_k * sizeof(DKernel))) != cudaSuccess) return cuda_fail(c, e, "cudaMalloc kernels");
+  }
+  if (c->hg.size() > c->cap_g) {
+    if (c->dg) cudaFree(c->dg);
+    c->cap_g = std::max<size_t>(c->hg.size() * 2, 4);
+    if ((e = cudaMalloc(&c->dg, c->cap_g * sizeof(DGpu))) != cudaSuccess) return cuda_fail(c, e, "cudaMalloc gpus");
+  }
+  if (!c->hk.empty() &&
+      (e = cudaMemcpyAsync(c->dk, c->hk.data(), c->hk.size() * sizeof(DKernel), cudaMemcpyHostToDevice, c->stream)) !=
+          cudaSuccess)
+    return cuda_fail(c, e, "upload kernels");
+  if (!c->hg.empty() &&
+      (e = cudaMemcpyAsync(c->dg, c->hg.data(), c->hg.size() * sizeof(DGpu), cudaMemcpyHostToDevice, c->stream)) !=
+          cudaSuccess)
+    return cuda_fail(c, e, "upload gpus");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "upload sync");
+  c->dirty = false;
+  return WS_OK;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
+  int64_t cb = 1;
+  for (int64_t v : c->chunk_bound) cb = std::max(cb, v);
+  const size_t max_chunks = n * (size_t)cb;
+  size_t off = 0;
+  const size_t o_plans = off;   off = align_up(off + n * sizeof(DPlan));
+  const size_t o_instr = off;   off = align_up(off + n * (size_t)kMaxInstr * sizeof(DInstr));
+  const size_t o_row = off;     off = align_up(off + n * (size_t)kMaxFields * sizeof(DRowInfo));
+  const size_t o_acc = off;     off = align_up(off + n * (size_t)A_N * sizeof(unsigned long long));
+  const size_t o_pre = off;     off = align_up(off + (n + 1) * sizeof(DPrefix));
+  const size_t o_chunk = off;   off = align_up(off + max_chunks * (size_t)kNQ * 3 * sizeof(long long));
+  if (off > c->scratch_cap) {
+    if (c->scratch) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_cap = 0;
+    cudaError_t e = cudaMalloc(&c->scratch, off);
+    if (e != cudaSuccess) return fail(c, WS_ENOMEM, std::string("device scratch: ") + cudaGetErrorString(e));
+    c->scratch_cap = off;
+  }
+  char* b = (char*)c->scratch;
+  s.plans = (DPlan*)(b + o_plans);
+  s.instr = (DInstr*)(b + o_instr);
+  s.rowinfo = (DRowInfo*)(b + o_row);
+  s.acc = (unsigned long long*)(b + o_acc);
+  s.prefix = (DPrefix*)(b + o_pre);
+  s.chunkres = (long long*)(b + o_chunk);
+  s.max_chunks = (int64_t)max_chunks;
+  return WS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out) {
+  if (!out) return WS_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) return WS_ECUDA;  // no CPU fallback
+  if (cuda_device < 0 || cuda_device >= ndev) return WS_EINVAL;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return WS_ECUDA;
+  ws_ctx* c = new (std::nothrow) ws_ctx();
+  if (!c) return WS_ENOMEM;
+  c->device = cuda_device;
+  c->stream = (cudaStream_t)cuda_stream;
+  cudaDeviceGetAttribute(&c->n_sm_dev, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (c->n_sm_dev <= 0) c->n_sm_dev = 148;
+  *out = c;
+  return WS_OK;
+}
+
+void ws_destroy(ws_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->dk) cudaFree(c->dk);
+  if (c->dg) cudaFree(c->dg);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->io) cudaFree(c->io);
+  delete c;
+}
+
+const char* ws_last_error(const ws_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+ws_status ws_set_stream(ws_ctx* c, void* s) {
+  if (!c) return WS_EINVAL;
+  c->stream = (cudaStream_t)s;
+  return WS_OK;
+}
+
+uint32_t ws_last_launch_count(const ws_ctx* c) { return c ? c->last_launches : 0; }
+
+ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
+  if (!c || !k || !id) return fail(c, WS_EINVAL, "null argument");
+  if (k->n_fields < 1 || k->n_fields > (uint32_t)kMaxFields || k->n_accesses < 1 || k->n_accesses > (uint32_t)kMaxAcc ||
+      !k->fields || !k->accesses)
+    return fail(c, WS_EINVAL, "n_fields must be 1..64 and n_accesses 1..128");
+  DKernel D;
+  memset(&D, 0, sizeof(D));
+  D.n_fields = (int)k->n_fields;
+  D.n_acc = (int)k->n_accesses;
+  D.regs = (int)k->regs_per_thread;
+  D.flops = k->flops_per_lup;
+  D.cells = 1.0;
+  for (int d = 0; d < 3; ++d) {
+    if (k->dom_lo[d] < 0 || k->dom_hi[d] <= k->dom_lo[d]) return fail(c, WS_EINVAL, "empty or negative domain");
+    D.lo[d] = k->dom_lo[d];
+    D.hi[d] = k->dom_hi[d];
+    D.cells *= (double)(k->dom_hi[d] - k->dom_lo[d]);
+  }
+  for (uint32_t i = 0; i < k->n_fields; ++i) {
+    const ws_field& F = k->fields[i];
+    DField& G = D.f[i];
+    const int le = lg2(F.elem_bytes);
+    if (le < 0 || F.elem_bytes > 32) return fail(c, WS_EINVAL, "elem_bytes must be a power of two <= 32");
+    for (int d = 0; d < 3; ++d)
+      if (F.extent[d] < 1) return fail(c, WS_EINVAL, "field extent < 1");
+    if (F.pitch[0] != 1 || F.pitch[1] < F.extent[0] || F.pitch[2] < F.pitch[1] * F.extent[1])
+      return fail(c, WS_EINVAL, "layout: need pitch[0]==1, pitch[1]>=extent[0], pitch[2]>=pitch[1]*extent[1]");
+    for (int d = 0; d < 3; ++d) {
+      G.ext[d] = F.extent[d];
+      G.pitch[d] = F.pitch[d];
+    }
+    G.align = F.align_bytes;
+    G.lg_elem = le;
+  }
+  for (uint32_t i = 0; i < k->n_accesses; ++i) {
+    const ws_access& A = k->accesses[i];
+    if (A.field >= k->n_fields || A.is_store > 1) return fail(c, WS_EINVAL, "access: bad field index or kind");
+    const ws_field& F = k->fields[A.field];
+    for (int d = 0; d < 3; ++d)
+      if (k->dom_lo[d] + A.off[d] < 0 || k->dom_hi[d] - 1 + A.off[d] >= F.extent[d])
+        return fail(c, WS_EBOUNDS, "access leaves its field for an active cell");
+    D.acc[i] = A;
+  }
+  // groups: (field, kind, oy, oz) -> maximal runs of consecutive ox
+  int ng = 0;
+  int64_t chunks = 0;
+  for (int fi = 0; fi < D.n_fields; ++fi) {
+    DField& G = D.f[fi];
+    G.g_begin = ng;
+    std::vector<std::pair<int, int>> runs;
+    G.oy_min = G.oz_min = G.ld_oy_min = G.ld_oz_min = 1 << 30;
+    G.oy_max = G.oz_max = G.ld_oy_max = G.ld_oz_max = -(1 << 30);
+    for (int kind = 0; kind < 2; ++kind) {
+      std::map<std::pair<int, int>, std::set<int>> byrow;
+      for (int i = 0; i < D.n_acc; ++i)
+        if ((int)D.acc[i].field == fi && (int)D.acc[i].is_store == kind)
+          byrow[{D.acc[i].off[1], D.acc[i].off[2]}].insert(D.acc[i].off[0]);
+      for (auto& kv : byrow) {
+        std::vector<int> xs(kv.second.begin(), kv.second.end());
+        size_t a = 0;
+        while (a < xs.size()) {
+          size_t b = a;
+          while (b + 1 < xs.size() && xs[b + 1] == xs[b] + 1) ++b;
+          std::pair<int, int> run(xs[a], xs[b]);
+          int ri = -1;
+          for (size_t q = 0; q < runs.size(); ++q)
+            if (runs[q] == run) ri = (int)q;
+          if (ri < 0) {
+            if ((int)runs.size() >= kMaxRuns) return fail(c, WS_ELIMIT, "more than 16 distinct x-offset runs in a field");
+            ri = (int)runs.size();
+            runs.push_back(run);
+          }
+          DGroup gr;
+          gr.field = fi;
+          gr.kind = kind;
+          gr.oy = kv.first.first;
+          gr.oz = kv.first.second;
+          gr.run = ri;
+          gr.pad = 0;
+          D.g[ng++] = gr;
+          G.oy_min = std::min(G.oy_min, gr.oy);
+          G.oy_max = std::max(G.oy_max, gr.oy);
+          G.oz_min = std::min(G.oz_min, gr.oz);
+          G.oz_max = std::max(G.oz_max, gr.oz);
+          if (kind == 0) {
+            G.n_ld_groups++;
+            G.ld_oy_min = std::min(G.ld_oy_min, gr.oy);
+            G.ld_oy_max = std::max(G.ld_oy_max, gr.oy);
+            G.ld_oz_min = std::min(G.ld_oz_min, gr.oz);
+            G.ld_oz_max = std::max(G.ld_oz_max, gr.oz);
+          }
+          G.kinds |= 1 << kind;
+          a = b + 1;
+        }
+      }
+    }
+    G.g_end = ng;
+    G.n_runs = (int)runs.size();
+    for (size_t q = 0; q < runs.size(); ++q) {
+      G.run_lo[q] = runs[q].first;
+      G.run_hi[q] = runs[q].second;
+    }
+    if (G.g_end > G.g_begin) chunks += (G.ext[1] * G.ext[2] + kRowsPerChunk - 1) / kRowsPerChunk;
+  }
+  D.n_groups = ng;
+  c->hk.push_back(D);
+  c->chunk_bound.push_back(chunks);
+  c->dirty = true;
+  *id = (uint32_t)(c->hk.size() - 1);
+  return WS_OK;
+}
+
+ws_status ws_describe_gpu(ws_ctx* c, const ws_gpu* g, uint32_t* id) {
+  if (!c || !g || !id) return fail(c, WS_EINVAL, "null argument");
+  DGpu D;
+  memset(&D, 0, sizeof(D));
+  D.g = *g;
+  D.lg_sector = lg2(g->sector_bytes);
+  D.lg_line = lg2(g->line_bytes);
+  D.lg_bank = lg2(g->bank_bytes);
+  D.lg_hw = lg2(g->half_warp);
+  D.lg_nbanks = lg2(g->n_banks);
+  if (g->n_sm < 1 || g->max_thr_sm < 1 || g->max_blk_sm < 1 || g->max_thr_blk < 1 || g->regs_sm < 1)
+    return fail(c, WS_EINVAL, "occupancy limits must be >= 1");
+  if (D.lg_sector < 0 || D.lg_line < 0 || D.lg_line < D.lg_sector || D.lg_bank < 0 || D.lg_hw < 0 || g->half_warp > 32 ||
+      D.lg_nbanks < 0 || g->n_banks > 256)
+    return fail(c, WS_EINVAL, "sector/line/bank/half-warp geometry must be powers of two (line >= sector, half_warp <= 32)");
+  if (g->pair_window_bytes < 1 || g->l2_sections < 1 || g->l1_bytes < 1 || g->l2_bytes < 1)
+    return fail(c, WS_EINVAL, "cache sizes / window must be >= 1");
+  if (!(g->clock_hz > 0) || !(g->dram_bw > 0) || !(g->l2_bw > 0)) return fail(c, WS_EINVAL, "rates must be > 0");
+  c->hg.push_back(D);
+  c->dirty = true;
+  *id = (uint32_t)(c->hg.size() - 1);
+  return WS_OK;
+}
+
+ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out) {
+  if (!c) return WS_EINVAL;
+  if (n == 0) return WS_OK;
+  if (!d_cfgs || !d_out) return fail(c, WS_EINVAL, "null argument");
+  if (n > (size_t)(1 << 24)) return fail(c, WS_ELIMIT, "batch larger than 2^24 configurations");
+  if (c->hk.empty() || c->hg.empty()) return fail(c, WS_EUNKNOWN_ID, "describe a kernel and a gpu first");
+  cudaSetDevice(c->device);
+  ws_status s = upload(c);
+  if (s != WS_OK) return s;
+  Scratch S;
+  if ((s = ensure_scratch(c, n, S)) != WS_OK) return s;
+  int e = launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, c->stream,
+                          c->n_sm_dev, &c->last_launches);
+  if (e) return cuda_fail(c, (cudaError_t)e, "launch");
+  return WS_OK;
+}
+
+ws_status ws_estimate(ws_ctx* c, const ws_config* cfgs, size_t n, ws_result* out) {
+  if (!c) return WS_EINVAL;
+  if (n == 0) return WS_OK;
+  if (!cfgs || !out) return fail(c, WS_EINVAL, "null argument");
+  cudaSetDevice(c->device);
+  const size_t need = align_up(n * sizeof(ws_config)) + n * sizeof(ws_result);
+  cudaError_t e;
+  if (need > c->io_cap) {
+    if (c->io) cudaFree(c->io);
+    c->io = nullptr;
+    c->io_cap = 0;
+    if ((e = cudaMalloc(&c->io, need)) != cudaSuccess) return fail(c, WS_ENOMEM, "device io buffer");
+    c->io_cap = need;
+  }
+  ws_config* dc = (ws_config*)c->io;
+  ws_result* dr = (ws_result*)((char*)c->io + align_up(n * sizeof(ws_config)));
+  if ((e = cudaMemcpyAsync(dc, cfgs, n * sizeof(ws_config), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "H2D configs");
+  ws_status s = ws_estimate_async(c, dc, n, dr);
+  if (s != WS_OK) return s;
+  if ((e = cudaMemcpyAsync(out, dr, n * sizeof(ws_result), cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "D2H results");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "estimate");
+  return WS_OK;
+}
+
+ws_status ws_rank_async(ws_ctx* c, ws_result* d_res, size_t n, size_t k, uint32_t* d_top) {
+  if (!c) return WS_EINVAL;
+  if (n == 0) return WS_OK;
+  if (!d_res) return fail(c, WS_EINVAL, "null argument");
+  cudaSetDevice(c->device);
+  int e = launch_rank(d_res, (int)n, (int)std::min(k, n), d_top, c->stream, &c->last_launches);
+  if (e) return cuda_fail(c, (cudaError_t)e, "rank launch");
+  return WS_OK;
+}
+
+ws_status ws_rank(ws_ctx* c, ws_result* res, size_t n, size_t k, uint32_t* top) {
+  if (!c) return WS_EINVAL;
+  if (n == 0) return WS_OK;
+  if (!res) return fail(c, WS_EINVAL, "null argument");
+  cudaSetDevice(c->device);
+  k = std::min(k, n);
+  void* buf = nullptr;
+  cudaError_t e;
+  const size_t bytes = align_up(n * sizeof(ws_result)) + (k + 1) * sizeof(uint32_t);
+  if ((e = cudaMalloc(&buf, bytes)) != cudaSuccess) return fail(c, WS_ENOMEM, "rank buffer");
+  ws_result* dr = (ws_result*)buf;
+  uint32_t* dt = (uint32_t*)((char*)buf + align_up(n * sizeof(ws_result)));
+  ws_status s = WS_OK;
+  if ((e = cudaMemcpyAsync(dr, res, n * sizeof(ws_result), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess) {
+    s = cuda_fail(c, e, "H2D results");
+  } else if ((s = ws_rank_async(c, dr, n, k, k ? dt : nullptr)) == WS_OK) {
+    if ((e = cudaMemcpyAsync(res, dr, n * sizeof(ws_result), cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+      s = cuda_fail(c, e, "D2H results");
+    else if (k && top && (e = cudaMemcpyAsync(top, dt, k * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+      s = cuda_fail(c, e, "D2H top");
+    else if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess)
+      s = cuda_fail(c, e, "rank");
+  }
+  cudaFree(buf);
+  return s;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// ws_internal.cuh -- device-side descriptors shared by ws_api.cu and ws_kernels.cu
+// (library-internal; the oracle never sees this file).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "ws.h"
+
+namespace wsb {
+
+constexpr int kMaxFields = 64;
+constexpr int kMaxAcc = 128;
+constexpr int kMaxRuns = 16;       // distinct x-offset runs per field (bitmask width of k_rows)
+constexpr int kMaxInstr = 1024;    // instructions per thread after fold dedupe
+constexpr int kMaxFoldCube = 64;   // prod(fold)
+constexpr int kRowThreads = 256;
+constexpr int kRowsPerThread = 4;
+constexpr int kRowsPerChunk = kRowThreads * kRowsPerThread;
+constexpr int kNQ = 9;             // union triples per row chunk (see k_rows)
+
+// x-offset run: all accesses of one (field, kind, oy, oz) whose ox values form a
+// maximal run of consecutive integers [lo, hi] ("group").  The union of a
+// row interval [x0,x1) shifted by every ox of a run is [x0+lo, x1+hi).
+struct DField {
+  int64_t ext[3], pitch[3], align;
+  int32_t lg_elem, kinds;          // kinds: bit0 = has loads, bit1 = has stores
+  int32_t g_begin, g_end;          // this field's groups in DKernel::g
+  int32_t n_runs, n_ld_groups;
+  int32_t oy_min, oy_max, oz_min, oz_max;  // over all groups of the field
+  int32_t ld_oy_min, ld_oy_max, ld_oz_min, ld_oz_max;  // over load groups
+  int32_t run_lo[kMaxRuns], run_hi[kMaxRuns];
+};
+
+struct DGroup {
+  int32_t field, kind, oy, oz, run, pad;
+};
+
+struct DKernel {
+  int32_t n_fields, n_acc, n_groups, regs;
+  int64_t lo[3], hi[3];
+  double flops, cells;
+  DField f[kMaxFields];
+  ws_access acc[kMaxAcc];
+  DGroup g[kMaxAcc];
+};
+
+struct DGpu {
+  ws_gpu g;
+  int32_t lg_sector, lg_line, lg_bank, lg_hw, lg_nbanks, pad;
+};
+
+// One per-thread instruction after fold dedupe:
+// address = C + (pitch . base) << lg_elem ; issued iff kmask & active_kappas != 0.
+struct DInstr {
+  int64_t C;
+  uint64_t kmask;
+  int32_t field, kind, lg_elem, pad;
+};
+
+// Row box (field-index rows (y,z), z-major) of the wave + layer-set footprint of one field.
+struct DRowInfo {
+  int64_t y0, ny, z0, nz, chunk_begin, n_chunks;
+};
+
+struct DPlan {
+  int32_t status, kid, gid, n_instr;
+  int32_t b[3], f[3];
+  int32_t T, nwarps, k, fcube;
+  int64_t lo[3], hi[3], G[3], BF[3];
+  int64_t N, W, s, nsets, Ly0, Lz0;
+  int64_t n_warp_items, n_set_items, n_chunks, n_fields;
+  uint64_t addr_evals;
+};
+
+// per-config accumulator slots (u64, atomically added by the worker kernels)
+enum {
+  A_LUP = 0, A_WF, A_REQ_LD, A_REQ_ST, A_SM_SEC, A_SM_LIN,
+  A_WLD, A_WST, A_WLIN, A_LY, A_LZ, A_OVY, A_OVZ, A_N = 16
+};
+
+struct DPrefix {
+  int64_t warp, set, chunk, fold;
+};
+
+// ---------------------------------------------------------------- launchers (ws_kernels.cu)
+struct Scratch {
+  DPlan* plans;
+  DInstr* instr;
+  DRowInfo* rowinfo;
+  unsigned long long* acc;
+  DPrefix* prefix;            // n + 1 entries
+  long long* chunkres;        // max_chunks * kNQ * 3
+  int64_t max_chunks;
+};
+
+int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
+                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches);
+int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches);
+
+}  // namespace wsb

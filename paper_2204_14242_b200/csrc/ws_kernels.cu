@@ -1,0 +1,959 @@
+// ws_kernels.cu -- sm_100a kernels of the Warpspeed hot path.
+//
+//   k_plan   (a1)  one CTA per configuration: geometry, wave, SM sets, layer sets,
+//                  fold-deduplicated instruction table, row boxes, work counts.
+//   k_scan         exclusive prefix of the per-config work counts (one CTA).
+//   k_warp   (a2+a3) one warp per (config, wave warp): addresses of every lane and
+//                  instruction, unique sectors per warp instruction (lanes are
+//                  address-sorted, so a shuffle against the previous issuing lane
+//                  dedupes), half-warp wavefronts (__match_any_sync bank histogram
+//                  per 1024 B cluster), lattice updates.
+//   k_smset  (a4)  one CTA per (config, SM-resident block set): unique load
+//                  sectors/lines of the set's footprint, row by row.
+//   k_rows   (a5+a6) one CTA per (config, field, chunk of 1024 address rows):
+//                  unique sectors/lines of the wave, the layer sets and their unions,
+//                  row by row, as ordered (first, last, count) triples.
+//   k_fold         ordered fold of the chunk triples -> per-config counts.
+//   k_model  (a7)  FP64 Eqs. 1-5 + max-limiter.
+//   k_rank   (a8)  rank by (t_pred, index).
+//
+// Exactness: every count is an exact set cardinality.  Footprints of a set of
+// threads are computed as unions of element intervals per address row: the
+// footprint of blocks R for field phi is {addr(c+o) : c active cell of R,
+// o an offset of phi} (every active cell c = base+kappa issues instruction
+// r = kappa+o).  Rows are element-
+// disjoint and address-ordered (validated layout), so the sector union of a
+// sorted list of element intervals is sum(len) - #(adjacent pairs sharing a
+// sector); the (first, last, count) triple is a monoid under that rule.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "ws_internal.cuh"
+
+namespace wsb {
+
+#define FULL 0xffffffffu
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ long long shfl64(long long v, int src) {
+  int lo = __shfl_sync(FULL, (int)(v & 0xffffffffll), src);
+  int hi = __shfl_sync(FULL, (int)(v >> 32), src);
+  return ((long long)hi << 32) | (unsigned int)lo;
+}
+__device__ __forceinline__ long long shfl64_down(long long v, int d) {
+  int lo = __shfl_down_sync(FULL, (int)(v & 0xffffffffll), d);
+  int hi = __shfl_down_sync(FULL, (int)(v >> 32), d);
+  return ((long long)hi << 32) | (unsigned int)lo;
+}
+
+struct Tri {
+  long long f, l, c;  // first, last, count; c == 0: empty
+};
+__device__ __forceinline__ Tri tri_empty() { return Tri{0, 0, 0}; }
+// append the sorted range [s0, s1] (s0 >= last element appended so far)
+__device__ __forceinline__ void tri_add(Tri& t, long long s0, long long s1) {
+  if (t.c == 0) {
+    t.f = s0;
+    t.c = s1 - s0 + 1;
+  } else {
+    t.c += s1 - s0 + 1 - (t.l == s0 ? 1 : 0);
+  }
+  t.l = s1;
+}
+__device__ __forceinline__ Tri tri_combine(const Tri& a, const Tri& b) {
+  if (a.c == 0) return b;
+  if (b.c == 0) return a;
+  return Tri{a.f, b.l, a.c + b.c - (a.l == b.f ? 1 : 0)};
+}
+
+// Ordered CTA reduction of NQ triples per thread (thread order = row order).
+// Result valid in thread 0.  `sm` holds (blockDim/32)*NQ triples.
+template <int NQ>
+__device__ void cta_ordered_reduce(Tri (&t)[NQ], Tri* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
+      if (lane + o < 32) t[q] = tri_combine(t[q], x);
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) sm[warp * NQ + q] = t[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      Tri a = sm[q];
+      for (int w = 1; w < nw; ++w) a = tri_combine(a, sm[w * NQ + q]);
+      t[q] = a;
+    }
+  }
+  __syncthreads();
+}
+
+// Union of the element intervals produced by `gen` (each [xs, xe), xs < xe) in one
+// address row whose element 0 is at byte R0; appends the union's sectors/lines in
+// increasing order to *ts / *tl.  Repeated extension: no sorting, no storage.
+template <class Gen>
+__device__ __forceinline__ void row_union(const Gen& gen, long long R0, int lg_elem, int lg_sec, int lg_line, Tri* ts,
+                                          Tri* tl) {
+  const long long INF = LLONG_MAX;
+  long long start = INF;
+  gen([&](long long xs, long long xe) { start = xs < start ? xs : start; });
+  while (start != INF) {
+    long long end = start, nxt;
+    bool grew;
+    do {
+      grew = false;
+      nxt = INF;
+      gen([&](long long xs, long long xe) {
+        if (xs <= end) {
+          if (xe > end) {
+            end = xe;
+            grew = true;
+          }
+        } else if (xs < nxt) {
+          nxt = xs;
+        }
+      });
+    } while (grew);
+    const long long a0 = R0 + (start << lg_elem), a1 = R0 + ((end - 1) << lg_elem);
+    if (ts) tri_add(*ts, a0 >> lg_sec, a1 >> lg_sec);
+    if (tl) tri_add(*tl, a0 >> lg_line, a1 >> lg_line);
+    start = nxt;
+  }
+}
+
+template <int MEMBER>
+__device__ __forceinline__ int find_config(const DPrefix* pre, int n, long long item) {
+  // largest c in [0, n) with pre[c].member <= item (pre is an exclusive prefix)
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    const long long v = MEMBER == 0 ? pre[mid].warp : MEMBER == 1 ? pre[mid].set : MEMBER == 2 ? pre[mid].chunk : pre[mid].fold;
+    if (v <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------ a1: plan
+__device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, const DGpu* gs, int ng, DPlan& P) {
+  P = DPlan();
+  P.kid = (int)cf.kernel_id;
+  P.gid = (int)cf.gpu_id;
+  if (cf.kernel_id >= (uint32_t)nk || cf.gpu_id >= (uint32_t)ng) {
+    P.status = WS_EUNKNOWN_ID;
+    return;
+  }
+  const DKernel& K = ks[cf.kernel_id];
+  const DGpu& G = gs[cf.gpu_id];
+  for (int d = 0; d < 3; ++d) {
+    if (cf.block[d] < 1 || cf.fold[d] < 1) {
+      P.status = WS_EINVAL;
+      return;
+    }
+  }
+  for (int i = 0; i < K.n_fields; ++i)
+    if (K.f[i].lg_elem > G.lg_sector) {
+      P.status = WS_EINVAL;
+      return;
+    }
+  const long long T = (long long)cf.block[0] * cf.block[1] * cf.block[2];
+  if (T > (long long)G.g.max_thr_blk) {
+    P.status = WS_ELIMIT;
+    return;
+  }
+  const long long fc = (long long)cf.fold[0] * cf.fold[1] * cf.fold[2];
+  if (fc > kMaxFoldCube) {
+    P.status = WS_ELIMIT;
+    return;
+  }
+  long long k;
+  const long long Ta = (T + 31) / 32 * 32;
+  if (cf.blocks_per_sm > 0) {
+    k = cf.blocks_per_sm;
+  } else {
+    k = (long long)G.g.max_thr_sm / Ta;
+    if ((long long)G.g.max_blk_sm < k) k = G.g.max_blk_sm;
+    if (K.regs > 0) {
+      long long kr = (long long)G.g.regs_sm / ((long long)K.regs * Ta);
+      if (kr < k) k = kr;
+    }
+  }
+  if (k < 1) {
+    P.status = WS_ELIMIT;
+    return;
+  }
+  for (int d = 0; d < 3; ++d) {
+    P.b[d] = (int)cf.block[d];
+    P.f[d] = (int)cf.fold[d];
+    P.lo[d] = K.lo[d];
+    P.hi[d] = K.hi[d];
+    P.BF[d] = (long long)cf.block[d] * cf.fold[d];
+    P.G[d] = (K.hi[d] - K.lo[d] + P.BF[d] - 1) / P.BF[d];
+  }
+  P.T = (int)T;
+  P.fcube = (int)fc;
+  P.nwarps = (int)((T + 31) / 32);
+  P.k = (int)k;
+  P.N = P.G[0] * P.G[1] * P.G[2];
+  const long long cap = (long long)G.g.n_sm * k;
+  P.W = P.N < cap ? P.N : cap;
+  const long long cen = P.G[0] / 2 + P.G[0] * (P.G[1] / 2 + P.G[1] * (P.G[2] / 2));
+  long long s = cen - P.W / 2;
+  if (s < 0) s = 0;
+  if (s > P.N - P.W) s = P.N - P.W;
+  P.s = s;
+  P.nsets = (long long)G.g.n_sm < P.W ? (long long)G.g.n_sm : P.W;
+  P.Ly0 = s - P.G[0] > 0 ? s - P.G[0] : 0;
+  P.Lz0 = s - P.G[0] * P.G[1] > 0 ? s - P.G[0] * P.G[1] : 0;
+  P.status = WS_OK;
+}
+
+__device__ __forceinline__ void decode_kappa(int q, const int* f, int& kx, int& ky, int& kz) {
+  kx = q % f[0];
+  ky = (q / f[0]) % f[1];
+  kz = q / (f[0] * f[1]);
+}
+
+__global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs, int n,
+                                              const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
+                                              int ng, DPlan* __restrict__ plans, DInstr* __restrict__ instr,
+                                              DRowInfo* __restrict__ rowinfo, unsigned long long* __restrict__ acc) {
+  const int c = blockIdx.x;
+  const int tid = threadIdx.x;
+  __shared__ DPlan P;
+  __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
+  __shared__ int s_part[128];
+  __shared__ int s_total;
+  if (tid < A_N) acc[(long long)c * A_N + tid] = 0ull;
+  if (tid == 0) {
+    ws_config cf = cfgs[c];
+    plan_geometry(cf, ks, nk, gs, ng, P);
+  }
+  __syncthreads();
+  if (P.status != WS_OK) {
+    if (tid == 0) plans[c] = P;
+    return;
+  }
+  const DKernel& K = ks[P.kid];
+  const int fc = P.fcube;
+  const int np = K.n_acc * fc;
+  // ---- O3: fold-deduplicated instruction table.  Pair p = (access a, kappa q) gives
+  // instruction (field, kind, kappa + o_a); keep the first occurrence of each key.
+  for (int p = tid; p < np; p += blockDim.x) {
+    const int a = p / fc, q = p % fc;
+    int kx, ky, kz;
+    decode_kappa(q, P.f, kx, ky, kz);
+    const ws_access A = K.acc[a];
+    const int rx = kx + A.off[0], ry = ky + A.off[1], rz = kz + A.off[2];
+    unsigned char first = 1;
+    for (int p2 = 0; p2 < p && first; ++p2) {
+      const int a2 = p2 / fc, q2 = p2 % fc;
+      const ws_access B = K.acc[a2];
+      if (B.field != A.field || B.is_store != A.is_store) continue;
+      int jx, jy, jz;
+      decode_kappa(q2, P.f, jx, jy, jz);
+      if (jx + B.off[0] == rx && jy + B.off[1] == ry && jz + B.off[2] == rz) first = 0;
+    }
+    s_first[p] = first;
+  }
+  __syncthreads();
+  // block-wide exclusive prefix of s_first (contiguous segments per thread)
+  const int seg = (np + blockDim.x - 1) / blockDim.x;
+  int mysum = 0;
+  for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) mysum += s_first[p];
+  s_part[tid] = mysum;
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      int v = s_part[i];
+      s_part[i] = run;
+      run += v;
+    }
+    s_total = run;
+  }
+  __syncthreads();
+  if (s_total > kMaxInstr) {
+    if (tid == 0) {
+      DPlan Q = P;
+      Q.status = WS_ELIMIT;
+      plans[c] = Q;
+    }
+    return;
+  }
+  {
+    int pos = s_part[tid];
+    for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) {
+      if (!s_first[p]) continue;
+      const int a = p / fc, q = p % fc;
+      int kx, ky, kz;
+      decode_kappa(q, P.f, kx, ky, kz);
+      const ws_access A = K.acc[a];
+      const int r[3] = {kx + A.off[0], ky + A.off[1], kz + A.off[2]};
+      // kappas whose folded cell uses this instruction: r - kappa2 is an access offset (Q27)
+      unsigned long long km = 0;
+      for (int q2 = 0; q2 < fc; ++q2) {
+        int jx, jy, jz;
+        decode_kappa(q2, P.f, jx, jy, jz);
+        const int o0 = r[0] - jx, o1 = r[1] - jy, o2 = r[2] - jz;
+        for (int a2 = 0; a2 < K.n_acc; ++a2) {
+          const ws_access B = K.acc[a2];
+          if (B.field == A.field && B.is_store == A.is_store && B.off[0] == o0 && B.off[1] == o1 && B.off[2] == o2) {
+            km |= 1ull << q2;
+            break;
+          }
+        }
+      }
+      const DField& F = K.f[A.field];
+      DInstr e;
+      e.C = F.align + ((r[0] * F.pitch[0] + r[1] * F.pitch[1] + r[2] * F.pitch[2]) << F.lg_elem);
+      e.kmask = km;
+      e.field = (int)A.field;
+      e.kind = (int)A.is_store;
+      e.lg_elem = F.lg_elem;
+      e.pad = 0;
+      instr[(long long)c * kMaxInstr + pos] = e;
+      ++pos;
+    }
+  }
+  // ---- row boxes of the wave + layer-set footprint, per field
+  for (int fi = tid; fi < K.n_fields; fi += blockDim.x) {
+    const DField& F = K.f[fi];
+    const long long rA = P.Lz0 / P.G[0], rB = (P.s + P.W - 1) / P.G[0];
+    const long long byA = rA % P.G[1], bzA = rA / P.G[1], byB = rB % P.G[1], bzB = rB / P.G[1];
+    long long ylo, yhi;
+    if (bzA == bzB) {
+      ylo = P.lo[1] + byA * P.BF[1];
+      yhi = P.lo[1] + (byB + 1) * P.BF[1];
+      if (yhi > P.hi[1]) yhi = P.hi[1];
+    } else {
+      ylo = P.lo[1];
+      yhi = P.hi[1];
+    }
+    long long zlo = P.lo[2] + bzA * P.BF[2], zhi = P.lo[2] + (bzB + 1) * P.BF[2];
+    if (zhi > P.hi[2]) zhi = P.hi[2];
+    long long y0 = ylo + F.oy_min, y1 = yhi + F.oy_max, z0 = zlo + F.oz_min, z1 = zhi + F.oz_max;
+    if (y0 < 0) y0 = 0;
+    if (z0 < 0) z0 = 0;
+    if (y1 > F.ext[1]) y1 = F.ext[1];
+    if (z1 > F.ext[2]) z1 = F.ext[2];
+    DRowInfo ri;
+    ri.y0 = y0;
+    ri.ny = y1 > y0 ? y1 - y0 : 0;
+    ri.z0 = z0;
+    ri.nz = z1 > z0 ? z1 - z0 : 0;
+    if (F.g_end == F.g_begin) ri.ny = ri.nz = 0;
+    const long long rows = ri.ny * ri.nz;
+    ri.n_chunks = (rows + kRowsPerChunk - 1) / kRowsPerChunk;
+    ri.chunk_begin = 0;
+    rowinfo[(long long)c * kMaxFields + fi] = ri;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long cb = 0;
+    for (int fi = 0; fi < K.n_fields; ++fi) {
+      DRowInfo& ri = rowinfo[(long long)c * kMaxFields + fi];
+      ri.chunk_begin = cb;
+      cb += ri.n_chunks;
+    }
+    DPlan Q = P;
+    Q.n_instr = s_total;
+    Q.n_warp_items = P.W * P.nwarps;
+    Q.n_set_items = P.nsets;
+    Q.n_chunks = cb;
+    Q.n_fields = K.n_fields;
+    Q.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
+    plans[c] = Q;
+  }
+}
+
+// ------------------------------------------------------------------ scan of work counts
+__global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre) {
+  __shared__ long long s[4][1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int seg = (n + nt - 1) / nt;
+  long long a[4] = {0, 0, 0, 0};
+  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
+    const DPlan& P = plans[c];
+    if (P.status != WS_OK) continue;
+    a[0] += P.n_warp_items;
+    a[1] += P.n_set_items;
+    a[2] += P.n_chunks;
+    a[3] += P.n_fields;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s[j][tid] = a[j];
+  __syncthreads();
+  if (tid < 4) {
+    long long run = 0;
+    for (int i = 0; i < nt; ++i) {
+      long long v = s[tid][i];
+      s[tid][i] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  long long r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) r[j] = s[j][tid];
+  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
+    pre[c] = DPrefix{r[0], r[1], r[2], r[3]};
+    const DPlan& P = plans[c];
+    if (P.status != WS_OK) continue;
+    r[0] += P.n_warp_items;
+    r[1] += P.n_set_items;
+    r[2] += P.n_chunks;
+    r[3] += P.n_fields;
+  }
+  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3]};
+}
+
+// ------------------------------------------------------------------ a2 + a3: warp instructions
+__global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                              const DInstr* __restrict__ instr, const DKernel* __restrict__ ks,
+                                              const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc) {
+  const long long total = pre[n].warp;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
+    const int c = find_config<0>(pre, n, item);
+    const DPlan& P = plans[c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    const long long wi = item - pre[c].warp;
+    const long long B = P.s + wi / P.nwarps;
+    const int w = (int)(wi % P.nwarps);
+    const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
+    const int t = w * 32 + lane;
+    const bool valid = t < P.T;
+    const int tc[3] = {t % P.b[0], (t / P.b[0]) % P.b[1], t / (P.b[0] * P.b[1])};
+    long long base[3];
+    long long lim[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      base[d] = P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d];
+      lim[d] = P.hi[d] - base[d];
+    }
+    // active folded cells of this lane (guard clipping)
+    unsigned long long act = 0;
+    if (valid && lim[0] > 0 && lim[1] > 0 && lim[2] > 0) {
+      if (lim[0] >= P.f[0] && lim[1] >= P.f[1] && lim[2] >= P.f[2]) {
+        act = P.fcube == 64 ? ~0ull : ((1ull << P.fcube) - 1ull);
+      } else {
+        for (int q = 0; q < P.fcube; ++q) {
+          int kx, ky, kz;
+          decode_kappa(q, P.f, kx, ky, kz);
+          if (kx < lim[0] && ky < lim[1] && kz < lim[2]) act |= 1ull << q;
+        }
+      }
+    }
+    const int lg_sec = G.lg_sector, lg_bank = G.lg_bank, lg_hw = G.lg_hw;
+    const long long bank_bytes = G.g.bank_bytes, window = G.g.pair_window_bytes;
+    const int nbm = (int)G.g.n_banks - 1;
+    const unsigned hbits = (lg_hw == 5 ? FULL : ((1u << (1 << lg_hw)) - 1u)) << ((lane >> lg_hw) << lg_hw);
+    const bool hleader = (lane & ((1 << lg_hw) - 1)) == 0;
+    long long req_ld = 0, req_st = 0, wf = 0;
+    int cur_field = -1;
+    long long plane = 0;
+    const DInstr* tab = instr + (long long)c * kMaxInstr;
+    for (int i = 0; i < P.n_instr; ++i) {
+      const DInstr e = tab[i];
+      const bool iss = (e.kmask & act) != 0ull;
+      const unsigned m = __ballot_sync(FULL, iss);
+      if (m == 0u) continue;
+      if (e.field != cur_field) {
+        cur_field = e.field;
+        const DField& F = K.f[e.field];
+        plane = base[0] + F.pitch[1] * base[1] + F.pitch[2] * base[2];
+      }
+      const long long A = e.C + (plane << e.lg_elem);
+      // unique sectors of the warp instruction (lanes are address-sorted)
+      const long long sec = A >> lg_sec;
+      const unsigned pm = m & lt_mask;
+      const long long psec = shfl64(sec, pm ? 31 - __clz(pm) : lane);
+      const bool us = iss && (pm == 0u || psec != sec);
+      const int cnt = __popc(__ballot_sync(FULL, us));
+      if (e.kind) req_st += cnt;
+      else req_ld += cnt;
+      // half-warp wavefronts: unique bank words, 1024 B clusters, bank max
+      const long long word = A >> lg_bank;
+      const unsigned mh = m & hbits;
+      const unsigned pmh = mh & lt_mask;
+      const long long pword = shfl64(word, pmh ? 31 - __clz(pmh) : lane);
+      const bool uw = iss && (pmh == 0u || pword != word);
+      unsigned rem = __ballot_sync(FULL, uw) & hbits;
+      while (__any_sync(FULL, rem != 0u)) {
+        const int first = rem ? __ffs(rem) - 1 : lane;
+        const long long cs = shfl64(word, first);
+        const bool inC = ((rem >> lane) & 1u) && ((word - cs) * bank_bytes < window);
+        const unsigned cm = __ballot_sync(FULL, inC) & hbits;
+        const int bank = (int)(word & nbm);
+        const unsigned key = inC ? (unsigned)(bank | ((lane >> lg_hw) << 8)) : (0x10000u | (unsigned)lane);
+        const unsigned peers = __match_any_sync(FULL, key);
+        int cb = inC ? __popc(peers) : 0;
+        for (int o = (1 << lg_hw) >> 1; o >= 1; o >>= 1) cb = max(cb, __shfl_xor_sync(FULL, cb, o));
+        if (hleader && rem != 0u) wf += cb;
+        rem &= ~cm;
+      }
+    }
+    // lattice updates of this warp
+    long long lup = valid ? __popcll(act) : 0;
+    long long wfl = wf;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      lup += shfl64_down(lup, o);
+      wfl += shfl64_down(wfl, o);
+    }
+    if (lane == 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      if (lup) atomicAdd(a + A_LUP, (unsigned long long)lup);
+      if (wfl) atomicAdd(a + A_WF, (unsigned long long)wfl);
+      if (req_ld) atomicAdd(a + A_REQ_LD, (unsigned long long)req_ld);
+      if (req_st) atomicAdd(a + A_REQ_ST, (unsigned long long)req_st);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a4: SM-resident block sets
+__global__ void __launch_bounds__(kRowThreads) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
+                                                       int n, const DKernel* __restrict__ ks,
+                                                       const DGpu* __restrict__ gs,
+                                                       unsigned long long* __restrict__ acc) {
+  __shared__ DGroup s_g[kMaxAcc];
+  __shared__ int s_ng;
+  __shared__ long long s_box[4];
+  __shared__ Tri s_red[(kRowThreads / 32) * 2];
+  const long long total = pre[n].set;
+  const int tid = threadIdx.x;
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_config<1>(pre, n, item);
+    const DPlan& P = plans[c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    const long long j = item - pre[c].set;
+    const long long nsm = G.g.n_sm;
+    const long long S0 = P.s + j;
+    const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
+    const int lg_sec = G.lg_sector, lg_line = G.lg_line;
+    unsigned long long sum_s = 0, sum_l = 0;
+    for (int fi = 0; fi < K.n_fields; ++fi) {
+      const DField& F = K.f[fi];
+      if (!(F.kinds & 1)) continue;
+      __syncthreads();
+      if (tid == 0) {
+        int ng = 0;
+        for (int g = F.g_begin; g < F.g_end; ++g)
+          if (K.g[g].kind == 0) s_g[ng++] = K.g[g];
+        s_ng = ng;
+        // bounding row box of the members' cells, widened by the load offsets
+        long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
+        for (long long m = 0; m < kj; ++m) {
+          const long long Bm = S0 + m * nsm;
+          const long long by = (Bm / P.G[0]) % P.G[1], bz = Bm / (P.G[0] * P.G[1]);
+          long long a = P.lo[1] + by * P.BF[1], b = a + P.BF[1];
+          if (b > P.hi[1]) b = P.hi[1];
+          ylo = a < ylo ? a : ylo;
+          yhi = b > yhi ? b : yhi;
+          a = P.lo[2] + bz * P.BF[2];
+          b = a + P.BF[2];
+          if (b > P.hi[2]) b = P.hi[2];
+          zlo = a < zlo ? a : zlo;
+          zhi = b > zhi ? b : zhi;
+        }
+        long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
+        if (y0 < 0) y0 = 0;
+        if (z0 < 0) z0 = 0;
+        if (y1 > F.ext[1]) y1 = F.ext[1];
+        if (z1 > F.ext[2]) z1 = F.ext[2];
+        s_box[0] = y0;
+        s_box[1] = y1 > y0 ? y1 - y0 : 0;
+        s_box[2] = z0;
+        s_box[3] = z1 > z0 ? z1 - z0 : 0;
+      }
+      __syncthreads();
+      const int ng = s_ng;
+      const long long y0 = s_box[0], ny = s_box[1], z0 = s_box[2], nz = s_box[3];
+      const long long rows = ny * nz;
+      Tri carry_s = tri_empty(), carry_l = tri_empty();
+      for (long long base = 0; base < rows; base += (long long)kRowThreads * kRowsPerThread) {
+        Tri t[2] = {tri_empty(), tri_empty()};
+        for (int u = 0; u < kRowsPerThread; ++u) {
+          const long long i = base + (long long)tid * kRowsPerThread + u;
+          if (i >= rows) break;
+          const long long z = z0 + i / ny, y = y0 + i % ny;
+          const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << F.lg_elem);
+          auto gen = [&](auto&& cb) {
+            for (int g = 0; g < ng; ++g) {
+              const DGroup gr = s_g[g];
+              const long long yy = y - gr.oy, zz = z - gr.oz;
+              if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
+              const long long r = (yy - P.lo[1]) / P.BF[1] + P.G[1] * ((zz - P.lo[2]) / P.BF[2]);
+              const long long rs = r * P.G[0];
+              const long long num2 = rs + P.G[0] - 1 - S0;
+              if (num2 < 0) continue;
+              long long m1 = num2 / nsm;
+              if (m1 > kj - 1) m1 = kj - 1;
+              const long long num = rs - S0;
+              const long long m0 = num <= 0 ? 0 : (num + nsm - 1) / nsm;
+              for (long long m = m0; m <= m1; ++m) {
+                const long long bxi = S0 + m * nsm - rs;
+                const long long x0 = P.lo[0] + bxi * P.BF[0];
+                long long x1 = x0 + P.BF[0];
+                if (x1 > P.hi[0]) x1 = P.hi[0];
+                cb(x0 + F.run_lo[gr.run], x1 + F.run_hi[gr.run]);
+              }
+            }
+          };
+          row_union(gen, R0, F.lg_elem, lg_sec, lg_line, &t[0], &t[1]);
+        }
+        cta_ordered_reduce<2>(t, s_red);
+        if (tid == 0) {
+          carry_s = tri_combine(carry_s, t[0]);
+          carry_l = tri_combine(carry_l, t[1]);
+        }
+      }
+      if (tid == 0) {
+        sum_s += (unsigned long long)carry_s.c;
+        sum_l += (unsigned long long)carry_l.c;
+      }
+    }
+    if (tid == 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      atomicAdd(a + A_SM_SEC, sum_s);
+      atomicAdd(a + A_SM_LIN, sum_l);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ a5 + a6: wave and layer sets
+// ranges: 0 = wave [s, s+W), 1 = L_y [Ly0, s), 2 = L_z [Lz0, s), 3 = L_y + wave, 4 = L_z + wave
+struct RangeInfo {
+  long long ra, rl;      // first / last block-row touched
+  long long iv[4][2];    // x cell intervals: FULL, SUFFIX, PREFIX, MIDDLE
+  int nonempty, pad;
+};
+
+__device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
+  if (!R.nonempty || r < R.ra || r > R.rl) return -1;
+  if (R.ra == R.rl) return 3;
+  if (r == R.ra) return 1;
+  if (r == R.rl) return 2;
+  return 0;
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
+                                                      int n, const DKernel* __restrict__ ks,
+                                                      const DGpu* __restrict__ gs, const DRowInfo* __restrict__ rowinfo,
+                                                      long long* __restrict__ chunkres) {
+  __shared__ DGroup s_g[kMaxAcc];
+  __shared__ RangeInfo s_r[5];
+  __shared__ Tri s_red[(kRowThreads / 32) * kNQ];
+  const long long total = pre[n].chunk;
+  const int tid = threadIdx.x;
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_config<2>(pre, n, item);
+    const DPlan& P = plans[c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    const long long ci = item - pre[c].chunk;
+    int fi = 0;
+    for (int f2 = 0; f2 < K.n_fields; ++f2) {
+      const DRowInfo& r2 = rowinfo[(long long)c * kMaxFields + f2];
+      if (ci >= r2.chunk_begin && ci < r2.chunk_begin + r2.n_chunks) {
+        fi = f2;
+        break;
+      }
+    }
+    const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
+    const DField& F = K.f[fi];
+    const int ng = F.g_end - F.g_begin;
+    __syncthreads();
+    for (int g = tid; g < ng; g += blockDim.x) s_g[g] = K.g[F.g_begin + g];
+    if (tid < 5) {
+      long long a, b;
+      if (tid == 0) { a = P.s; b = P.s + P.W; }
+      else if (tid == 1) { a = P.Ly0; b = P.s; }
+      else if (tid == 2) { a = P.Lz0; b = P.s; }
+      else if (tid == 3) { a = P.Ly0; b = P.s + P.W; }
+      else { a = P.Lz0; b = P.s + P.W; }
+      RangeInfo R;
+      R.nonempty = a < b;
+      R.pad = 0;
+      const long long Gx = P.G[0], lx = P.lo[0], hx = P.hi[0], bf = P.BF[0];
+      long long xa = 0, xl = Gx;
+      if (a < b) {
+        R.ra = a / Gx;
+        xa = a % Gx;
+        R.rl = (b - 1) / Gx;
+        xl = (b - 1) % Gx + 1;
+      } else {
+        R.ra = R.rl = 0;
+      }
+      const long long xs_a = lx + xa * bf;
+      long long xe_l = lx + xl * bf;
+      if (xe_l > hx) xe_l = hx;
+      R.iv[0][0] = lx;   R.iv[0][1] = hx;
+      R.iv[1][0] = xs_a; R.iv[1][1] = hx;
+      R.iv[2][0] = lx;   R.iv[2][1] = xe_l;
+      R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
+      s_r[tid] = R;
+    }
+    __syncthreads();
+    const int lg_sec = G.lg_sector, lg_line = G.lg_line;
+    const long long ny = RI.ny, rows = RI.ny * RI.nz;
+    const long long chunk_in_field = ci - RI.chunk_begin;
+    Tri t[kNQ];
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
+    for (int u = 0; u < kRowsPerThread; ++u) {
+      const long long i = chunk_in_field * kRowsPerChunk + (long long)tid * kRowsPerThread + u;
+      if (i >= rows) break;
+      const long long z = RI.z0 + i / ny, y = RI.y0 + i % ny;
+      const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << F.lg_elem);
+      unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
+      for (int g = 0; g < ng; ++g) {
+        const DGroup gr = s_g[g];
+        const long long yy = y - gr.oy, zz = z - gr.oz;
+        if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
+        const long long r = (yy - P.lo[1]) / P.BF[1] + P.G[1] * ((zz - P.lo[2]) / P.BF[2]);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const int ty = classify(s_r[q], r);
+          if (ty >= 0) {
+            const unsigned long long bit = 1ull << (ty * 16 + gr.run);
+            if (gr.kind) mS[q] |= bit;
+            else mL[q] |= bit;
+          }
+        }
+      }
+      // a generator over (range, candidate-mask) pairs
+      auto make_gen = [&](int q1, unsigned long long m1, int q2, unsigned long long m2) {
+        return [&, q1, m1, q2, m2](auto&& cb) {
+          unsigned long long m = m1;
+          while (m) {
+            const int b = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int ty = b >> 4, run = b & 15;
+            cb(s_r[q1].iv[ty][0] + F.run_lo[run], s_r[q1].iv[ty][1] + F.run_hi[run]);
+          }
+          m = m2;
+          while (m) {
+            const int b = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int ty = b >> 4, run = b & 15;
+            cb(s_r[q2].iv[ty][0] + F.run_lo[run], s_r[q2].iv[ty][1] + F.run_hi[run]);
+          }
+        };
+      };
+      const int le = F.lg_elem;
+      row_union(make_gen(0, mL[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[0], nullptr);              // WLD
+      row_union(make_gen(0, mS[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[1], nullptr);              // WST
+      row_union(make_gen(0, mL[0] | mS[0], 0, 0ull), R0, le, lg_sec, lg_line, nullptr, &t[2]);      // WLIN
+      row_union(make_gen(1, mL[1] | mS[1], 1, 0ull), R0, le, lg_sec, lg_line, &t[3], &t[4]);        // F_Ly
+      row_union(make_gen(2, mL[2] | mS[2], 2, 0ull), R0, le, lg_sec, lg_line, &t[5], &t[6]);        // F_Lz
+      row_union(make_gen(3, mL[3], 1, mS[1]), R0, le, lg_sec, lg_line, &t[7], nullptr);             // WLD u F_Ly
+      row_union(make_gen(4, mL[4], 2, mS[2]), R0, le, lg_sec, lg_line, &t[8], nullptr);             // WLD u F_Lz
+    }
+    cta_ordered_reduce<kNQ>(t, s_red);
+    if (tid == 0) {
+      long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        out[q * 3 + 0] = t[q].f;
+        out[q * 3 + 1] = t[q].l;
+        out[q * 3 + 2] = t[q].c;
+      }
+    }
+  }
+}
+
+// ordered fold of the chunk triples of one (config, field); one warp per item
+__global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                              const DRowInfo* __restrict__ rowinfo,
+                                              const long long* __restrict__ chunkres,
+                                              unsigned long long* __restrict__ acc) {
+  const long long total = pre[n].fold;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
+    const int c = find_config<3>(pre, n, item);
+    const int fi = (int)(item - pre[c].fold);
+    const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
+    const long long nch = RI.n_chunks;
+    const long long per = (nch + 31) / 32;
+    Tri t[kNQ];
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
+    for (long long k = lane * per; k < nch && k < (lane + 1) * per; ++k) {
+      const long long* in = chunkres + (pre[c].chunk + RI.chunk_begin + k) * (kNQ * 3);
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) t[q] = tri_combine(t[q], Tri{in[q * 3], in[q * 3 + 1], in[q * 3 + 2]});
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
+        if (lane + o < 32) t[q] = tri_combine(t[q], x);
+      }
+    }
+    if (lane == 0 && nch > 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      atomicAdd(a + A_WLD, (unsigned long long)t[0].c);
+      atomicAdd(a + A_WST, (unsigned long long)t[1].c);
+      atomicAdd(a + A_WLIN, (unsigned long long)t[2].c);
+      atomicAdd(a + A_LY, (unsigned long long)t[4].c);
+      atomicAdd(a + A_LZ, (unsigned long long)t[6].c);
+      // |WLD n F_L| = |WLD| + |F_L| - |WLD u F_L|  (per field; fields never alias)
+      atomicAdd(a + A_OVY, (unsigned long long)(t[0].c + t[3].c - t[7].c));
+      atomicAdd(a + A_OVZ, (unsigned long long)(t[0].c + t[5].c - t[8].c));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a7: model (FP64)
+__device__ __forceinline__ double gompertz(const double* abc, double O) { return abc[0] * exp(-abc[1] * exp(-abc[2] * O)); }
+
+__global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, int n, const DKernel* __restrict__ ks,
+                                               const DGpu* __restrict__ gs, const unsigned long long* __restrict__ acc,
+                                               ws_result* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const DPlan& P = plans[c];
+  ws_result R;
+  memset(&R, 0, sizeof(R));
+  R.status = P.status;
+  if (P.status != WS_OK) {
+    out[c] = R;
+    return;
+  }
+  const DKernel& K = ks[P.kid];
+  const DGpu& G = gs[P.gid];
+  const unsigned long long* a = acc + (long long)c * A_N;
+  for (int d = 0; d < 3; ++d) R.grid[d] = (uint32_t)P.G[d];
+  R.k = (uint32_t)P.k;
+  R.wave_blocks = (uint32_t)P.W;
+  R.n_smsets = (uint32_t)P.nsets;
+  R.n_instr = (uint32_t)P.n_instr;
+  R.wave_first_block = (uint64_t)P.s;
+  R.lup_wave = a[A_LUP];
+  R.l1_wavefronts = a[A_WF];
+  R.l1_req_ld_sectors = a[A_REQ_LD];
+  R.l1_req_st_sectors = a[A_REQ_ST];
+  R.sm_ld_sectors = a[A_SM_SEC];
+  R.sm_ld_lines = a[A_SM_LIN];
+  R.wave_ld_sectors = a[A_WLD];
+  R.wave_st_sectors = a[A_WST];
+  R.wave_lines = a[A_WLIN];
+  R.ly_lines = a[A_LY];
+  R.lz_lines = a[A_LZ];
+  R.ov_y = a[A_OVY];
+  R.ov_z = a[A_OVZ];
+  R.addr_evals = P.addr_evals;
+  const double sector = (double)G.g.sector_bytes, line = (double)G.g.line_bytes;
+  const double lup = (double)R.lup_wave;
+  // L1: capacity on the mean SM-set allocation (Eq. 4) and Eq. 5 on the redundant loads
+  R.O_l1 = ((double)R.sm_ld_lines * line / (double)P.nsets) / (double)G.g.l1_bytes;
+  R.R_l1 = gompertz(G.g.hit_abc[0], R.O_l1);
+  const double red1 = (double)R.l1_req_ld_sectors > (double)R.sm_ld_sectors
+                          ? (double)R.l1_req_ld_sectors - (double)R.sm_ld_sectors : 0.0;
+  const double v_l2l1_ld = (double)R.sm_ld_sectors + (1.0 - R.R_l1) * red1;
+  const double v_l1l2_st = (double)R.l1_req_st_sectors;
+  // L2: split-L2 effective capacity; layer-set overlaps (Q13-Q16)
+  const double l2_eff = (double)G.g.l2_bytes / (double)G.g.l2_sections;
+  R.O_y = (double)R.ly_lines * line / l2_eff;
+  R.O_z = (double)R.lz_lines * line / l2_eff;
+  R.R_y = gompertz(G.g.hit_abc[1], R.O_y);
+  R.R_z = gompertz(G.g.hit_abc[2], R.O_z);
+  const double hit = R.R_y * (double)R.ov_y + R.R_z * (double)(R.ov_z - R.ov_y);
+  const double red_st = (double)R.l1_req_st_sectors > (double)R.wave_st_sectors
+                            ? (double)R.l1_req_st_sectors - (double)R.wave_st_sectors : 0.0;
+  R.O_st = (double)R.wave_lines * line / l2_eff;
+  R.R_st = gompertz(G.g.hit_abc[3], R.O_st);
+  const double v_dram_ld = (double)R.wave_ld_sectors - hit + (1.0 - R.R_st) * red_st;
+  const double v_dram_st = (double)R.wave_st_sectors;
+  R.l1_cyc_per_lup = (double)R.l1_wavefronts / lup;
+  R.l2_ld_Bpl = sector * v_l2l1_ld / lup;
+  R.l2_st_Bpl = sector * v_l1l2_st / lup;
+  R.dram_ld_Bpl = sector * v_dram_ld / lup;
+  R.dram_st_Bpl = sector * v_dram_st / lup;
+  R.t_l1 = (double)R.l1_wavefronts / (lup * (double)G.g.n_sm * G.g.clock_hz);
+  R.t_l2 = sector * (v_l2l1_ld + v_l1l2_st) / (lup * G.g.l2_bw);
+  R.t_dram = sector * (v_dram_ld + v_dram_st) / (lup * G.g.dram_bw);
+  const double tm = fmax(R.t_l1, fmax(R.t_l2, R.t_dram));
+  R.limiter = R.t_dram >= tm ? 2u : (R.t_l2 >= tm ? 1u : 0u);
+  R.t_pred = tm * K.cells;
+  out[c] = R;
+}
+
+// ------------------------------------------------------------------ a8: rank
+__global__ void __launch_bounds__(256) k_rank(ws_result* __restrict__ res, int n, int k, uint32_t* __restrict__ top) {
+  __shared__ double s_key[256];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  double ki = INF;
+  if (i < n) ki = res[i].status == WS_OK ? res[i].t_pred : INF;
+  unsigned int rank = 0;
+  for (int base = 0; base < n; base += 256) {
+    const int j = base + threadIdx.x;
+    s_key[threadIdx.x] = j < n ? (res[j].status == WS_OK ? res[j].t_pred : INF) : INF;
+    __syncthreads();
+    const int lim = n - base < 256 ? n - base : 256;
+    for (int jj = 0; jj < lim; ++jj) {
+      const double kj = s_key[jj];
+      const int j2 = base + jj;
+      rank += (kj < ki || (kj == ki && j2 < i)) ? 1u : 0u;
+    }
+    __syncthreads();
+  }
+  if (i < n) {
+    res[i].rank = rank;
+    if ((int)rank < k && top) top[rank] = (uint32_t)i;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
+                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches) {
+  uint32_t L = 0;
+  k_plan<<<n, 128, 0, st>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc);
+  ++L;
+  k_scan<<<1, 1024, 0, st>>>(s.plans, n, s.prefix);
+  ++L;
+  const int persist = n_sm_dev * 8;
+  k_warp<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc);
+  ++L;
+  k_smset<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc);
+  ++L;
+  k_rows<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres);
+  ++L;
+  k_fold<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, s.rowinfo, s.chunkres, s.acc);
+  ++L;
+  k_model<<<(n + 127) / 128, 128, 0, st>>>(s.plans, n, d_k, d_g, s.acc, d_out);
+  ++L;
+  if (launches) *launches = L;
+  return check_launch();
+}
+
+int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches) {
+  k_rank<<<(n + 255) / 256, 256, 0, st>>>(d_res, n, k, d_top);
+  if (launches) *launches = 1;
+  return check_launch();
+}
+
+}  // namespace wsb

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element,
+on the same seeded inputs (integers bit-exact, doubles within 1e-9 relative)."""
+import os
+import random
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+from parity_util import check_ranking, compare
+
+pytestmark = pytest.mark.gpu
+
+NT = max(1, min(32, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2204_14242_b200 import Context
+    return Context(0)
+
+
+def run_gpu(ctx, kernel, gpu, configs):
+    from paper_2204_14242_b200 import config_array, result_dicts
+    kid = ctx.describe_kernel(kernel)
+    gid = ctx.describe_gpu(gpu)
+    res = ctx.estimate(config_array(kid, gid, configs))
+    return result_dicts(res), res
+
+
+def assert_parity(ctx, kernel, gpu, configs, label):
+    g, _ = run_gpu(ctx, kernel, gpu, configs)
+    o = O.estimate_batch(kernel, gpu, configs, NT)
+    errs = []
+    for i, (a, b) in enumerate(zip(g, o)):
+        errs += compare(a, b, f"{label}[{i}] {configs[i]}")
+    assert not errs, "\n".join(errs[:40])
+    return g, o
+
+
+def test_configs0_k7_v100(ctx):
+    """BJ configs[0]: 7pt 64^3, 16 shapes on V100 (incl. the invalid 2048-thread block)."""
+    g, o = assert_parity(ctx, W.k7(64), W.gpu_v100(), W.space_k7(), "cfg0")
+    assert sum(r["status"] != 0 for r in g) == 1
+
+
+def test_small_cases(ctx):
+    cases = [
+        (W.k7(12), W.gpu_v100(), [((32, 2, 1), (1, 1, 1), 0), ((32, 8, 8), (1, 1, 1), 0)]),
+        (W.stencil_star(20, 10, 12, 4, regs=64), dict(W.gpu_a100(), n_sm=6),
+         [((8, 4, 2), (1, 1, 2), 1), ((4, 2, 4), (1, 2, 1), 2), ((1, 1, 1), (1, 1, 1), 1)]),
+        (W.lbm15(6), dict(W.gpu_a100(), n_sm=3), [((4, 2, 2), (1, 1, 1), 1), ((2, 2, 2), (2, 1, 1), 0)]),
+    ]
+    for i, (k, gp, cf) in enumerate(cases):
+        assert_parity(ctx, k, gp, cf, f"small{i}")
+
+
+def test_stencil25_paper_space_64(ctx):
+    """Full 168-config paper space on a 64^3 grid, A100 parameters."""
+    assert_parity(ctx, W.k25(64), W.gpu_a100(), W.space_stencil_paper(), "k25_64")
+
+
+def test_stencil25_ragged(ctx):
+    """Ragged domain (not divisible by any block), several tiles and a tail."""
+    k = W.stencil_star(75, 37, 29, 4, regs=64)
+    g = dict(W.gpu_a100(), n_sm=20)
+    cf = [((32, 4, 2), (1, 1, 1), 0), ((16, 2, 8), (1, 1, 2), 0), ((64, 1, 4), (1, 2, 1), 0),
+          ((1, 16, 4), (1, 1, 1), 0), ((128, 2, 1), (1, 1, 1), 0), ((1024, 1, 1), (1, 1, 1), 0)]
+    assert_parity(ctx, k, g, cf, "ragged")
+
+
+def test_lbm_spaces_small(ctx):
+    """LBM15 / LBM27 (Q23) on 40^3 with 16 SMs: 49 shapes."""
+    g = dict(W.gpu_a100(), n_sm=16)
+    assert_parity(ctx, W.lbm15(40), g, W.space_lbm(), "lbm15")
+    sub = W.space_lbm()[::4]
+    assert_parity(ctx, W.lbm27(24), dict(W.gpu_a100(), n_sm=8), sub, "lbm27")
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_kernels(ctx, seed):
+    k, gp = W.random_kernel(seed), W.random_gpu(seed)
+    rng = random.Random(seed)
+    cf = [W.random_config(seed * 10 + j) for j in range(4)]
+    assert_parity(ctx, k, gp, cf, f"rand{seed}")
+
+
+def test_edge_cases(ctx):
+    # single block grid: wave = whole grid, empty layer sets
+    k = W.stencil_star(8, 8, 8, 1, regs=0)
+    assert_parity(ctx, k, W.gpu_v100(), [((8, 8, 8), (1, 1, 1), 0), ((16, 16, 4), (1, 1, 2), 0)], "single")
+    # negative alignment (P:540 uses -1 element), 4- and 16-byte elements
+    k2 = W.stencil_star(16, 8, 8, 1, regs=0)
+    k2["fields"][0] = dict(k2["fields"][0], align=-8)
+    k2["fields"][1] = dict(k2["fields"][1], align=-120, elem=8)
+    assert_parity(ctx, k2, dict(W.gpu_v100(), n_sm=4), [((8, 2, 2), (1, 1, 1), 0), ((4, 4, 1), (2, 1, 1), 1)], "neg")
+    k3 = W.stencil_star(16, 8, 8, 1, regs=0)
+    k3["fields"][0] = dict(k3["fields"][0], elem=4, align=4)
+    k3["fields"][1] = dict(k3["fields"][1], elem=16, align=16)
+    assert_parity(ctx, k3, dict(W.gpu_v100(), n_sm=4), [((8, 2, 2), (1, 1, 1), 0), ((32, 1, 1), (1, 1, 1), 1)], "elem")
+    # per-config errors: zero block, fold cube > 64, T > max threads, k override
+    assert_parity(ctx, k, W.gpu_v100(),
+                  [((0, 1, 1), (1, 1, 1), 0), ((8, 8, 8), (8, 8, 2), 0), ((64, 32, 1), (1, 1, 1), 0),
+                   ((8, 1, 1), (1, 1, 1), 3)], "errors")
+
+
+def test_unknown_ids_and_empty_batch(ctx):
+    from paper_2204_14242_b200 import config_array, result_dicts
+    kid = ctx.describe_kernel(W.k7(8))
+    gid = ctx.describe_gpu(W.gpu_v100())
+    a = config_array(kid, gid, [((32, 1, 1), (1, 1, 1), 0)] * 2)
+    a[1]["kernel_id"] = 999
+    r = result_dicts(ctx.estimate(a))
+    assert r[0]["status"] == 0 and r[1]["status"] == 6 and r[1]["t_pred"] == 0.0
+    assert len(ctx.estimate(a[:0])) == 0
+
+
+def test_rank_parity_and_determinism(ctx):
+    k, gp, cf = W.k25(64), W.gpu_a100(), W.space_stencil_paper()
+    g, res = run_gpu(ctx, k, gp, cf)
+    _, res2 = run_gpu(ctx, k, gp, cf)
+    assert res.tobytes() == res2.tobytes()
+    o = O.estimate_batch(k, gp, cf, NT)
+    top = ctx.rank(res, 10)
+    ranks = [int(r) for r in res["rank"]]
+    check_ranking(ranks, o)
+    assert [int(t) for t in top] == sorted(range(len(cf)), key=lambda i: ranks[i])[:10]
+
+
+def test_describe_errors(ctx):
+    from paper_2204_14242_b200 import WSError
+    bad = W.k7(8)
+    bad["accesses"] = bad["accesses"] + [(0, 0, (3, 0, 0))]
+    with pytest.raises(WSError) as e:
+        ctx.describe_kernel(bad)
+    assert e.value.status == 3
+    bad2 = W.k7(8)
+    bad2["fields"][0] = dict(bad2["fields"][0], pitch=(1, 5, 100))
+    with pytest.raises(WSError) as e:
+        ctx.describe_kernel(bad2)
+    assert e.value.status == 1
+    g = W.gpu_v100()
+    g["sector_bytes"] = 24
+    with pytest.raises(WSError):
+        ctx.describe_gpu(g)
+
+
+# ----------------------------------------------------------------- full size (bench launch configuration)
+def test_full_size_configs1_sampled(ctx):
+    """BJ configs[1]: 25pt 512^3 A100, the whole 168-config batch in one launch (as bench.py
+    times it); sampled configurations recomputed one by one by the oracle."""
+    k, gp, cf = W.k25(512), W.gpu_a100(), W.space_stencil_paper()
+    g, _ = run_gpu(ctx, k, gp, cf)
+    assert all(r["status"] == 0 for r in g)
+    # samples with small layer sets so the oracle finishes in seconds each (plus one deep one)
+    idx = [i for i, c in enumerate(cf) if c[0] in ((1024, 1, 1), (512, 2, 1), (32, 32, 1), (256, 4, 1))
+           and c[1] == (1, 1, 1)]
+    idx += [i for i, c in enumerate(cf) if c[0] == (64, 4, 4) and c[1] == (1, 1, 2)]
+    o = O.estimate_batch(k, gp, [cf[i] for i in idx], NT)
+    errs = []
+    for j, i in enumerate(idx):
+        errs += compare(g[i], o[j], f"full[{i}] {cf[i]}")
+    assert not errs, "\n".join(errs)
+    # properties that hold at any size
+    for r in g:
+        assert r["sm_ld_lines"] <= r["sm_ld_sectors"] <= 4 * r["sm_ld_lines"]
+        assert r["wave_ld_sectors"] <= r["sm_ld_sectors"] <= r["l1_req_ld_sectors"]
+        assert r["ov_y"] <= r["ov_z"] <= r["wave_ld_sectors"]
+        assert r["dram_ld_Bpl"] >= 8.0 - 1e-9 and r["dram_st_Bpl"] >= 8.0 - 1e-9
+
+
+def test_full_size_lbm15_sampled(ctx):
+    """BJ configs[2]: LBM15 256^3 A100 (49 shapes) in one launch; two sampled configs."""
+    k, gp, cf = W.lbm15(256), W.gpu_a100(), W.space_lbm()
+    g, _ = run_gpu(ctx, k, gp, cf)
+    idx = [i for i, c in enumerate(cf) if c[0] in ((512, 1, 1), (64, 8, 1))]
+    o = O.estimate_batch(k, gp, [cf[i] for i in idx], NT)
+    errs = []
+    for j, i in enumerate(idx):
+        errs += compare(g[i], o[j], f"lbm[{i}] {cf[i]}")
+    assert not errs, "\n".join(errs)
+    for r in g:
+        assert r["dram_ld_Bpl"] >= 120.0 and r["dram_ld_Bpl"] + r["dram_st_Bpl"] >= 240.0
