@@ -1,0 +1,378 @@
+#!/usr/bin/env python3
+"""bench.py -- configs estimated/s of the B200-native Warpspeed hot path.
+
+Workload (BASELINE.json configs[1]): range-4 3D-25pt double stencil on 512^3,
+the paper's full block-shape x thread-folding space (56 shapes x {none, 2y, 2z}
+= 168 configurations), A100 parameters with the split-L2 halving.
+One step = the whole hot path (a1-a8: plan, warp-instruction, SM-set, wave and
+layer-set scopes, model, ranking) over that batch.  At N GPUs every rank
+evaluates the same 168-config space on its own hardware parameter set
+(architecture exploration, BJ configs[3]: rank 0 = A100, then B200-like, V100
+and a hypothetical grid), the results are all-gathered over NCCL and every rank
+ranks the gathered set: per-GPU work is fixed -> "scaling": "weak".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+Rank 0 prints one JSON line.  `--impl reference` times the plain CPU oracle
+(oracle/) on the host cores instead (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "configs estimated/sec (8×B200, device-timed) + bit-exact volume match vs CPU"
+UNIT = "configs/s"
+WORKLOAD = ("BJ configs[1]: 3D-25pt r4 double stencil, grid 512^3, 168 configs "
+            "(56 block shapes x {none,2y,2z} folding), A100 parameters (split L2)")
+TOPK = 10
+# algorithmic integer lane-ops per work unit
+OPS_PER_UNIT = {"k_warp": 12, "k_wclass": 12, "k_smset": 24, "k_sclass": 24, "k_rows": 24, "k_plan": 8}
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    return p
+
+
+def alu_peak_gops(sm_max_mhz):
+    """Issue-limited integer lane-op peak: 148 SMs x 4 SMSPs x 1 warp-instruction/clk x 32 lanes."""
+    return 148 * 4 * 32 * sm_max_mhz * 1e6 / 1e9
+
+
+def hw_sets(world):
+    pk = peaks()
+    sets = [W.gpu_a100(), W.gpu_b200_like(pk.get("hbm_gbs", 6546.2)), W.gpu_v100()]
+    for l1 in (128, 256):
+        for l2 in (20, 40, 64):
+            for nsm in (108, 148):
+                sets.append(W.gpu_hypothetical(l1, l2, nsm))
+    while len(sets) < world:
+        sets.append(W.gpu_hypothetical(192, 32 + len(sets), 132))
+    return sets[:max(1, world)]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc, self.t = device, [], None, None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, tag):
+        self.marks.append((tag, time.time()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(2)
+
+    def summary(self, t0, t1):
+        inside = [r for t, r in self.rows if t0 <= t <= t1]
+        note = "samples inside the timed region"
+        if len(inside) < 3:
+            inside = [r for _, r in self.rows]
+            note = "timed region shorter than the sampling interval: samples over warm-up + timed region"
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "note": "nvidia-smi unavailable"}
+        sm = [float(r[0]) for r in inside if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in inside if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in inside for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(inside), "note": note}
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
+def oracle_sample(kernel, gpu, cfgs, threads):
+    """Plain CPU oracle over a bounded sample of the workload, scaled to configs/s of the whole
+    space by the oracle's own work measure (addr_evals, the plain definition's address evaluations).
+    Sample: the shallow configurations (block z = 1, no z fold) -- about 1-3 s of CPU work each."""
+    from oracle import oracle as O
+    plans = [O.plan(kernel, gpu, c) for c in cfgs]
+    mean_evals = statistics.mean(p["addr_evals"] for p in plans if p["status"] == 0)
+    sample = [c for c in cfgs if c[0][2] == 1 and c[1] == (1, 1, 1)]
+    t0 = time.perf_counter()
+    res = O.estimate_batch(kernel, gpu, sample, threads)
+    dt = time.perf_counter() - t0
+    ev = sum(r["addr_evals"] for r in res)
+    rate = ev / dt
+    return {"value": rate / mean_evals, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": (f"{len(sample)} of {len(cfgs)} configs (block z=1, no fold) on {threads} host threads: "
+                       f"{dt:.2f} s wall, {ev:.3e} address evaluations -> {rate:.3e} evals/s, scaled by the "
+                       f"space's mean {mean_evals:.3e} evals/config"),
+            "sample_configs_per_s": len(sample) / dt, "evals_per_s": rate, "wall_s": dt}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    kernel, gpu, cfgs = W.k25(512), W.gpu_a100(), W.space_stencil_paper()
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+    O.build()
+    plans = [O.plan(kernel, gpu, c) for c in cfgs]
+    mean_evals = statistics.mean(p["addr_evals"] for p in plans if p["status"] == 0)
+    shallow = [c for c in cfgs if c[0][2] == 1 and c[1] == (1, 1, 1)]
+    per_step = shallow[:max(1, min(len(shallow), threads))]
+    for _ in range(args.warmup):
+        O.estimate_batch(kernel, gpu, per_step[:1], 1)
+    tot_dt, tot_ev, tot_n = 0.0, 0, 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = O.estimate_batch(kernel, gpu, per_step, threads)
+        tot_dt += time.perf_counter() - t0
+        tot_ev += sum(r["addr_evals"] for r in res)
+        tot_n += len(per_step)
+    rate = tot_ev / tot_dt
+    value = rate / mean_evals
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": len(cfgs), "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": (f"each step: {len(per_step)} shallow configs (block z=1, no fold) of the 168 on "
+                                    f"{threads} threads; throughput {rate:.3e} address evals/s scaled by the space's "
+                                    f"mean {mean_evals:.3e} evals/config")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ native arm
+def run_native(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2204_14242_b200 import Context, config_array, result_dicts
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    ctx = Context(local, stream.cuda_stream)
+    kernel = W.k25(512)
+    gpu = hw_sets(world)[rank]
+    space = W.space_stencil_paper()
+    kid, gid = ctx.describe_kernel(kernel), ctx.describe_gpu(gpu)
+    host_cfg = config_array(kid, gid, space)
+    n = len(host_cfg)
+    rb = RESULT_DTYPE.itemsize
+    d_cfg = torch.from_numpy(host_cfg.view(np.uint8).copy()).to(dev)
+    d_out = torch.empty(n * rb, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * n * rb, dtype=torch.uint8, device=dev) if world > 1 else d_out
+    d_top = torch.empty(TOPK, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step():
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d_out)
+        ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
+
+    launches_per_step = None
+    for _ in range(max(args.warmup, 0)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+    est_launches = ctx.last_launch_count()
+    launches_per_step = est_launches + 1
+    work = ctx.work_read()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    ctx.profile_enable(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_wall0 = time.time()
+    for i in range(args.steps):
+        flush.zero_()                       # L2 flushed between timed steps (outside the events)
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    if world > 1:
+        dist.barrier()
+    ctx.profile_enable(False)
+    prof = ctx.profile_read()
+    ms_total = sum(a.elapsed_time(b) for a, b in evs)
+    time.sleep(0.2)
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n * args.steps / (ms_max / 1e3)
+
+    # correctness guard on the timed output (no silently empty work)
+    res = np.frombuffer(gathered.cpu().numpy().tobytes(), dtype=RESULT_DTYPE)
+    assert (res["status"] == 0).all() and (res["lup_wave"] > 0).all()
+    addr_evals = int(res["addr_evals"][:n].sum())
+
+    # ---- e2e through the public API with host buffers
+    e2e = e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb)
+
+    # ---- roofline of the dominant kernel
+    kern = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(kern, key=lambda k: kern[k][0])
+    dom_ms = kern[dom][0] / kern[dom][1]
+    pk = peaks()
+    sm_max = pk.get("sm_max_mhz", 1965.0)
+    peak = alu_peak_gops(sm_max)
+    units = work.get(dom, 0)
+    ops = units * OPS_PER_UNIT.get(dom, 0)
+    achieved = ops / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom)
+    except Exception:
+        pass
+    share = {k: round(v[0] / sum(x[0] for x in kern.values()), 4) for k, v in kern.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(kernel, gpu, space, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (analytic kernel descriptions shaped like the paper's; no datasets or weights)",
+            "config": {"workload": WORKLOAD, "global_batch": world * n, "per_gpu_batch": n,
+                       "hardware_sets": [hw_sets(world)[r]["name"] for r in range(world)],
+                       "parallelism": f"dp{world} over configurations (one NCCL all-gather of results)",
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+            "addresses_per_s_equiv": world * addr_evals * args.steps / (ms_max / 1e3),
+            "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "Gop/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "units_per_launch": units, "ops_per_unit": OPS_PER_UNIT.get(dom),
+                         "avg_launch_ms": dom_ms,
+                         "peak_note": f"148 SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (issue-limited int lane-ops)"},
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+            "kernel_share": share,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb):
+    """Same metric end to end: pinned host configs -> device -> whole path -> results + top-k
+    back in pinned host memory, every step."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+    h_cfg = torch.from_numpy(host_cfg.view(np.uint8).copy()).pin_memory()
+    h_res = torch.empty(world * n * rb, dtype=torch.uint8).pin_memory()
+    h_top = torch.empty(TOPK, dtype=torch.int32).pin_memory()
+    d_cfg = torch.empty_like(h_cfg, device=dev)
+    d_out = torch.empty(n * rb, dtype=torch.uint8, device=dev)
+    gathered = torch.empty(world * n * rb, dtype=torch.uint8, device=dev) if world > 1 else d_out
+    d_top = torch.empty(TOPK, dtype=torch.int32, device=dev)
+
+    def one():
+        d_cfg.copy_(h_cfg, non_blocking=True)
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d_out)
+        ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
+        h_res.copy_(gathered, non_blocking=True)
+        h_top.copy_(d_top, non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    res = np.frombuffer(h_res.numpy().tobytes(), dtype=RESULT_DTYPE)
+    assert (res["status"] == 0).all()
+    return {"value": world * n * args.steps / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h_cfg.numel()), "d2h_bytes_per_step": int(h_res.numel() + h_top.numel() * 4),
+            "api": "pinned host configs -> ws_estimate_async -> [all-gather] -> ws_rank_async -> pinned host results"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_native(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,22 @@ ws_status ws_rank_async(ws_ctx* ctx, ws_result* d_res, size_t n, size_t k, uint3
  * call enqueued (for the bench's gpu_launches count). */
 uint32_t ws_last_launch_count(const ws_ctx* ctx);
 
+/* Tracing.  While enabled, CUDA events are recorded on the context stream
+ * around every kernel the library launches.  ws_profile_read synchronises on
+ * them, writes the summed device milliseconds per kernel (in the order of
+ * ws_kernel_name(0..)) and the number of launches per kernel, resets the
+ * accumulators and returns the number of kernel kinds in *n_kinds. */
+ws_status ws_profile_enable(ws_ctx* ctx, int on);
+ws_status ws_profile_read(ws_ctx* ctx, double* ms, uint64_t* launches, uint32_t cap, uint32_t* n_kinds);
+const char* ws_kernel_name(uint32_t i);   /* NULL past the last kind */
+
+/* Algorithmic work units each kernel kind processed in the last
+ * ws_estimate[_async] call (synchronises).  Units:
+ * k_warp / k_wclass: lane-instructions evaluated (32 per warp and instruction,
+ * 32 per warp only classified); k_smset / k_sclass / k_rows: (address row,
+ * offset group) evaluations; k_plan: (access, fold cell) pairs. */
+ws_status ws_work_read(ws_ctx* ctx, uint64_t* units, uint32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,8 @@ def lib():
         L.wso_estimate_batch.argtypes = [C.POINTER(Kernel), C.POINTER(Gpu), C.POINTER(Config), I64,
                                          C.POINTER(Result), I64]
         L.wso_estimate_batch.restype = None
+        L.wso_plan.argtypes = [C.POINTER(Kernel), C.POINTER(Gpu), C.POINTER(Config), C.POINTER(Result)]
+        L.wso_plan.restype = I64
         L.wso_check_kernel.argtypes = [C.POINTER(Kernel)]
         L.wso_check_kernel.restype = I64
         L.wso_address.argtypes = [C.POINTER(Field), C.POINTER(I64)]
@@ -167,6 +169,13 @@ def estimate_batch(kernel, gpu, configs, n_threads=1):
     R = (Result * len(configs))()
     lib().wso_estimate_batch(C.byref(K), C.byref(G), X, len(configs), R, n_threads)
     return [result_dict(R[i]) for i in range(len(configs))]
+
+
+def plan(kernel, gpu, config):
+    """Geometry + addr_evals only (no enumeration)."""
+    K, G, X, R = make_kernel(kernel), make_gpu(gpu), make_config(config), Result()
+    lib().wso_plan(C.byref(K), C.byref(G), C.byref(X), C.byref(R))
+    return result_dict(R)
 
 
 def check_kernel(kernel):

@@ -390,6 +390,16 @@ extern "C" {
 
 int64_t wso_check_kernel(const wso_kernel* k) { return check_kernel(*k); }
 
+int64_t wso_plan(const wso_kernel* k, const wso_gpu* g, const wso_config* c, wso_result* r) {
+  *r = wso_result();
+  int64_t st = check_kernel(*k);
+  Plan p;
+  if (st == WSO_OK) st = make_plan(*k, *g, *c, p, *r);
+  r->status = st;
+  if (st == WSO_OK) r->addr_evals = (p.W + (p.s - p.Lz0)) * p.T * (int64_t)p.instr.size();
+  return st;
+}
+
 int64_t wso_estimate(const wso_kernel* k, const wso_gpu* g, const wso_config* c, wso_result* r) {
   return estimate(*k, *g, *c, *r);
 }

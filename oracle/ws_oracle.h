@@ -73,6 +73,9 @@ int64_t wso_check_kernel(const wso_kernel* k);
 /* One configuration, single-threaded. Returns status (also in r->status). */
 int64_t wso_estimate(const wso_kernel* k, const wso_gpu* g, const wso_config* c, wso_result* r);
 
+/* Geometry only (O1-O3): status, grid, k, W, s, n_instr and addr_evals, no enumeration. */
+int64_t wso_plan(const wso_kernel* k, const wso_gpu* g, const wso_config* c, wso_result* r);
+
 /* n configurations on up to n_threads host threads (one config per thread). */
 void wso_estimate_batch(const wso_kernel* k, const wso_gpu* g, const wso_config* c,
                         int64_t n, wso_result* r, int64_t n_threads);

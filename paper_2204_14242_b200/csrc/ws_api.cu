@@ -35,6 +35,33 @@ struct ws_ctx {
   void* io = nullptr;  // host-path staging for configs + results
   size_t io_cap = 0;
   uint32_t last_launches = 0;
+  unsigned long long* last_work = nullptr;
+  // tracing
+  bool profiling = false;
+  struct Rec {
+    int first_kind, n;
+    std::vector<cudaEvent_t> ev;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> free_ev;
+  cudaEvent_t* take_events(int first_kind, int nk) {
+    Rec r;
+    r.first_kind = first_kind;
+    r.n = nk;
+    for (int i = 0; i <= nk; ++i) {
+      cudaEvent_t e;
+      if (!free_ev.empty()) {
+        e = free_ev.back();
+        free_ev.pop_back();
+      } else if (cudaEventCreate(&e) != cudaSuccess) {
+        for (cudaEvent_t x : r.ev) free_ev.push_back(x);
+        return nullptr;
+      }
+      r.ev.push_back(e);
+    }
+    pending.push_back(std::move(r));
+    return pending.back().ev.data();
+  }
 };
 
 namespace {
@@ -92,6 +119,11 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   const size_t o_acc = off;     off = align_up(off + n * (size_t)A_N * sizeof(unsigned long long));
   const size_t o_pre = off;     off = align_up(off + (n + 1) * sizeof(DPrefix));
   const size_t o_chunk = off;   off = align_up(off + max_chunks * (size_t)kNQ * 3 * sizeof(long long));
+  const size_t o_wcnt = off;    off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned int));
+  const size_t o_wrep = off;    off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
+  const size_t o_scnt = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned int));
+  const size_t o_srep = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
+  const size_t o_work = off;    off = align_up(off + 16 * sizeof(unsigned long long));
   if (off > c->scratch_cap) {
     if (c->scratch) cudaFree(c->scratch);
     c->scratch = nullptr;
@@ -108,6 +140,12 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   s.prefix = (DPrefix*)(b + o_pre);
   s.chunkres = (long long*)(b + o_chunk);
   s.max_chunks = (int64_t)max_chunks;
+  s.wcnt = (unsigned int*)(b + o_wcnt);
+  s.wrep = (unsigned long long*)(b + o_wrep);
+  s.scnt = (unsigned int*)(b + o_scnt);
+  s.srep = (unsigned long long*)(b + o_srep);
+  s.work = (unsigned long long*)(b + o_work);
+  c->last_work = s.work;
   return WS_OK;
 }
 
@@ -139,6 +177,9 @@ void ws_destroy(ws_ctx* c) {
   if (c->dg) cudaFree(c->dg);
   if (c->scratch) cudaFree(c->scratch);
   if (c->io) cudaFree(c->io);
+  for (auto& r : c->pending)
+    for (cudaEvent_t e : r.ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->free_ev) cudaEventDestroy(e);
   delete c;
 }
 
@@ -151,6 +192,56 @@ ws_status ws_set_stream(ws_ctx* c, void* s) {
 }
 
 uint32_t ws_last_launch_count(const ws_ctx* c) { return c ? c->last_launches : 0; }
+
+static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_scan", "k_warp", "k_wclass", "k_smset",
+                                           "k_sclass", "k_rows", "k_fold", "k_model",  "k_rank"};
+
+const char* ws_kernel_name(uint32_t i) { return i < (uint32_t)K_NKINDS ? kKindNames[i] : nullptr; }
+
+ws_status ws_profile_enable(ws_ctx* c, int on) {
+  if (!c) return WS_EINVAL;
+  c->profiling = on != 0;
+  return WS_OK;
+}
+
+ws_status ws_profile_read(ws_ctx* c, double* ms, uint64_t* launches, uint32_t cap, uint32_t* n_kinds) {
+  if (!c) return WS_EINVAL;
+  cudaSetDevice(c->device);
+  std::vector<double> acc(K_NKINDS, 0.0);
+  std::vector<uint64_t> cnt(K_NKINDS, 0);
+  ws_status st = WS_OK;
+  for (auto& r : c->pending) {
+    for (int i = 0; i < r.n; ++i) {
+      float t = 0.f;
+      cudaError_t e = cudaEventSynchronize(r.ev[i + 1]);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]);
+      if (e != cudaSuccess) st = cuda_fail(c, e, "profile read");
+      acc[r.first_kind + i] += t;
+      cnt[r.first_kind + i] += 1;
+    }
+    for (cudaEvent_t e : r.ev) c->free_ev.push_back(e);
+  }
+  c->pending.clear();
+  for (uint32_t i = 0; i < cap && i < (uint32_t)K_NKINDS; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (launches) launches[i] = cnt[i];
+  }
+  if (n_kinds) *n_kinds = K_NKINDS;
+  return st;
+}
+
+ws_status ws_work_read(ws_ctx* c, uint64_t* units, uint32_t cap) {
+  if (!c || !units) return WS_EINVAL;
+  cudaSetDevice(c->device);
+  unsigned long long h[16] = {0};
+  if (c->last_work) {
+    cudaError_t e = cudaMemcpyAsync(h, c->last_work, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "work read");
+  }
+  for (uint32_t i = 0; i < cap && i < 16; ++i) units[i] = h[i];
+  return WS_OK;
+}
 
 ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
   if (!c || !k || !id) return fail(c, WS_EINVAL, "null argument");
@@ -299,8 +390,9 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   if (s != WS_OK) return s;
   Scratch S;
   if ((s = ensure_scratch(c, n, S)) != WS_OK) return s;
+  cudaEvent_t* ev = c->profiling ? c->take_events(K_PLAN, kEstimateKernels) : nullptr;
   int e = launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, c->stream,
-                          c->n_sm_dev, &c->last_launches);
+                          c->n_sm_dev, &c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "launch");
   return WS_OK;
 }
@@ -336,7 +428,8 @@ ws_status ws_rank_async(ws_ctx* c, ws_result* d_res, size_t n, size_t k, uint32_
   if (n == 0) return WS_OK;
   if (!d_res) return fail(c, WS_EINVAL, "null argument");
   cudaSetDevice(c->device);
-  int e = launch_rank(d_res, (int)n, (int)std::min(k, n), d_top, c->stream, &c->last_launches);
+  cudaEvent_t* ev = c->profiling ? c->take_events(K_RANK, 1) : nullptr;
+  int e = launch_rank(d_res, (int)n, (int)std::min(k, n), d_top, c->stream, &c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "rank launch");
   return WS_OK;
 }

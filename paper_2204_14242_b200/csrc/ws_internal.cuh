@@ -68,7 +68,11 @@ struct DPlan {
   int32_t T, nwarps, k, fcube;
   int64_t lo[3], hi[3], G[3], BF[3];
   int64_t N, W, s, nsets, Ly0, Lz0;
-  int64_t n_warp_items, n_set_items, n_chunks, n_fields;
+  // translation classes: 0 = disabled
+  int32_t wcls_R, scls_R;        // residue slots per warp index / per SM set
+  int64_t cls_pitch[3];          // the common pitch of every field when classes are enabled
+  int32_t cls_lg_elem, pad2;
+  int64_t n_warp_items, n_wclass_items, n_set_items, n_sclass_items, n_chunks, n_fields;
   uint64_t addr_evals;
 };
 
@@ -79,8 +83,11 @@ enum {
 };
 
 struct DPrefix {
-  int64_t warp, set, chunk, fold;
+  int64_t warp, wclass, set, sclass, chunk, fold;
 };
+constexpr int kNPrefix = 6;
+constexpr int kWSlots = 32 * 64;   // per config: warp index (<32) x residue (<64)
+constexpr int kSSlots = 64;        // per config: residue (<64)
 
 // ---------------------------------------------------------------- launchers (ws_kernels.cu)
 struct Scratch {
@@ -91,10 +98,23 @@ struct Scratch {
   DPrefix* prefix;            // n + 1 entries
   long long* chunkres;        // max_chunks * kNQ * 3
   int64_t max_chunks;
+  unsigned int* wcnt;         // n * kWSlots
+  unsigned long long* wrep;   // n * kWSlots
+  unsigned int* scnt;         // n * kSSlots
+  unsigned long long* srep;   // n * kSSlots
+  unsigned long long* work;   // K_NKINDS algorithmic work units of the last call (ws_work_read)
 };
 
+// kernel kinds, in launch order (ws_kernel_name)
+enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_MODEL, K_RANK, K_NKINDS };
+constexpr int kEstimateKernels = 9;
+
+// ev: nullptr, or kEstimateKernels+1 events recorded before each launch and after the last
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
-                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches);
-int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches);
+                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches,
+                    cudaEvent_t* ev);
+// ev: nullptr or 2 events
+int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches,
+                cudaEvent_t* ev);
 
 }  // namespace wsb

@@ -135,7 +135,12 @@ __device__ __forceinline__ int find_config(const DPrefix* pre, int n, long long 
   int lo = 0, hi = n - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
-    const long long v = MEMBER == 0 ? pre[mid].warp : MEMBER == 1 ? pre[mid].set : MEMBER == 2 ? pre[mid].chunk : pre[mid].fold;
+    const long long v = MEMBER == 0   ? pre[mid].warp
+                        : MEMBER == 1 ? pre[mid].wclass
+                        : MEMBER == 2 ? pre[mid].set
+                        : MEMBER == 3 ? pre[mid].sclass
+                        : MEMBER == 4 ? pre[mid].chunk
+                                      : pre[mid].fold;
     if (v <= item) lo = mid;
     else hi = mid - 1;
   }
@@ -213,6 +218,18 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   P.nsets = (long long)G.g.n_sm < P.W ? (long long)G.g.n_sm : P.W;
   P.Ly0 = s - P.G[0] > 0 ? s - P.G[0] : 0;
   P.Lz0 = s - P.G[0] * P.G[1] > 0 ? s - P.G[0] * P.G[1] : 0;
+  // translation classes need one pitch and one element size for every field
+  bool same = true;
+  for (int i = 1; i < K.n_fields; ++i)
+    for (int d = 0; d < 3; ++d)
+      if (K.f[i].pitch[d] != K.f[0].pitch[d] || K.f[i].lg_elem != K.f[0].lg_elem) same = false;
+  const long long M = (long long)G.g.sector_bytes > (long long)G.g.bank_bytes * G.g.n_banks
+                          ? (long long)G.g.sector_bytes : (long long)G.g.bank_bytes * G.g.n_banks;
+  const long long Rw = M >> K.f[0].lg_elem, Rs = (long long)G.g.line_bytes >> K.f[0].lg_elem;
+  P.wcls_R = (same && Rw >= 1 && Rw <= 64 && P.nwarps <= 32) ? (int)Rw : 0;
+  P.scls_R = (same && Rs >= 1 && Rs <= 64) ? (int)Rs : 0;
+  for (int d = 0; d < 3; ++d) P.cls_pitch[d] = K.f[0].pitch[d];
+  P.cls_lg_elem = K.f[0].lg_elem;
   P.status = WS_OK;
 }
 
@@ -225,10 +242,13 @@ __device__ __forceinline__ void decode_kappa(int q, const int* f, int& kx, int& 
 __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs, int n,
                                               const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
                                               int ng, DPlan* __restrict__ plans, DInstr* __restrict__ instr,
-                                              DRowInfo* __restrict__ rowinfo, unsigned long long* __restrict__ acc) {
+                                              DRowInfo* __restrict__ rowinfo, unsigned long long* __restrict__ acc,
+                                              unsigned int* __restrict__ wcnt, unsigned int* __restrict__ scnt) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
   __shared__ DPlan P;
+  for (int i = tid; i < kWSlots; i += blockDim.x) wcnt[(long long)c * kWSlots + i] = 0u;
+  if (tid < kSSlots) scnt[(long long)c * kSSlots + tid] = 0u;
   __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
   __shared__ int s_part[128];
   __shared__ int s_total;
@@ -367,7 +387,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     DPlan Q = P;
     Q.n_instr = s_total;
     Q.n_warp_items = P.W * P.nwarps;
+    Q.n_wclass_items = (long long)P.nwarps * P.wcls_R;
     Q.n_set_items = P.nsets;
+    Q.n_sclass_items = P.scls_R;
     Q.n_chunks = cb;
     Q.n_fields = K.n_fields;
     Q.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
@@ -376,23 +398,36 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
 }
 
 // ------------------------------------------------------------------ scan of work counts
-__global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre) {
-  __shared__ long long s[4][1024];
+__device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
+  switch (j) {
+    case 0: return P.n_warp_items;
+    case 1: return P.n_wclass_items;
+    case 2: return P.n_set_items;
+    case 3: return P.n_sclass_items;
+    case 4: return P.n_chunks;
+    default: return P.n_fields;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
+                                               unsigned long long* __restrict__ work) {
+  __shared__ long long s[kNPrefix][1024];
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid < 16) work[tid] = 0ull;
   const int seg = (n + nt - 1) / nt;
-  long long a[4] = {0, 0, 0, 0};
+  long long a[kNPrefix];
+#pragma unroll
+  for (int j = 0; j < kNPrefix; ++j) a[j] = 0;
   for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
     const DPlan& P = plans[c];
     if (P.status != WS_OK) continue;
-    a[0] += P.n_warp_items;
-    a[1] += P.n_set_items;
-    a[2] += P.n_chunks;
-    a[3] += P.n_fields;
+#pragma unroll
+    for (int j = 0; j < kNPrefix; ++j) a[j] += plan_count(P, j);
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) s[j][tid] = a[j];
+  for (int j = 0; j < kNPrefix; ++j) s[j][tid] = a[j];
   __syncthreads();
-  if (tid < 4) {
+  if (tid < kNPrefix) {
     long long run = 0;
     for (int i = 0; i < nt; ++i) {
       long long v = s[tid][i];
@@ -401,133 +436,308 @@ __global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, 
     }
   }
   __syncthreads();
-  long long r[4];
+  long long r[kNPrefix];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) r[j] = s[j][tid];
+  for (int j = 0; j < kNPrefix; ++j) r[j] = s[j][tid];
   for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
-    pre[c] = DPrefix{r[0], r[1], r[2], r[3]};
+    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5]};
     const DPlan& P = plans[c];
     if (P.status != WS_OK) continue;
-    r[0] += P.n_warp_items;
-    r[1] += P.n_set_items;
-    r[2] += P.n_chunks;
-    r[3] += P.n_fields;
+#pragma unroll
+    for (int j = 0; j < kNPrefix; ++j) r[j] += plan_count(P, j);
   }
-  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3]};
+  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5]};
 }
 
 // ------------------------------------------------------------------ a2 + a3: warp instructions
+struct Lane {
+  long long base[3];
+  unsigned long long act;  // active folded cells (guard clipping)
+  bool valid;              // thread index < T
+};
+
+__device__ __forceinline__ unsigned long long full_cube(int fc) { return fc == 64 ? ~0ull : ((1ull << fc) - 1ull); }
+
+__device__ __forceinline__ Lane lane_setup(const DPlan& P, long long B, int w, int lane) {
+  Lane L;
+  const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
+  const int t = w * 32 + lane;
+  L.valid = t < P.T;
+  const int tc[3] = {t % P.b[0], (t / P.b[0]) % P.b[1], t / (P.b[0] * P.b[1])};
+  long long lim[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    L.base[d] = P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d];
+    lim[d] = P.hi[d] - L.base[d];
+  }
+  L.act = 0;
+  if (L.valid && lim[0] > 0 && lim[1] > 0 && lim[2] > 0) {
+    if (lim[0] >= P.f[0] && lim[1] >= P.f[1] && lim[2] >= P.f[2]) {
+      L.act = full_cube(P.fcube);
+    } else {
+      for (int q = 0; q < P.fcube; ++q) {
+        int kx, ky, kz;
+        decode_kappa(q, P.f, kx, ky, kz);
+        if (kx < lim[0] && ky < lim[1] && kz < lim[2]) L.act |= 1ull << q;
+      }
+    }
+  }
+  return L;
+}
+
+// Every instruction of one warp: unique sectors per warp instruction (the
+// issuing lanes are address-sorted, so comparing with the previous issuing lane
+// dedupes) and half-warp wavefronts (unique bank words, greedy 1024 B
+// clusters, max bank multiplicity via __match_any_sync).  Returns warp totals in lane 0.
+__device__ void eval_warp(const DPlan& P, const DKernel& K, const DGpu& G, const DInstr* __restrict__ tab,
+                          const Lane& L, int lane, long long& lup, long long& wf_out, long long& req_ld,
+                          long long& req_st) {
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int lg_sec = G.lg_sector, lg_bank = G.lg_bank, lg_hw = G.lg_hw;
+  const long long bank_bytes = G.g.bank_bytes, window = G.g.pair_window_bytes;
+  const int nbm = (int)G.g.n_banks - 1;
+  const unsigned hbits = (lg_hw == 5 ? FULL : ((1u << (1 << lg_hw)) - 1u)) << ((lane >> lg_hw) << lg_hw);
+  const bool hleader = (lane & ((1 << lg_hw) - 1)) == 0;
+  long long wf = 0;
+  req_ld = req_st = 0;
+  int cur_field = -1;
+  long long plane = 0;
+  for (int i = 0; i < P.n_instr; ++i) {
+    const DInstr e = tab[i];
+    const bool iss = (e.kmask & L.act) != 0ull;
+    const unsigned m = __ballot_sync(FULL, iss);
+    if (m == 0u) continue;
+    if (e.field != cur_field) {
+      cur_field = e.field;
+      const DField& F = K.f[e.field];
+      plane = L.base[0] + F.pitch[1] * L.base[1] + F.pitch[2] * L.base[2];
+    }
+    const long long A = e.C + (plane << e.lg_elem);
+    const long long sec = A >> lg_sec;
+    const unsigned pm = m & lt_mask;
+    const long long psec = shfl64(sec, pm ? 31 - __clz(pm) : lane);
+    const bool us = iss && (pm == 0u || psec != sec);
+    const int cnt = __popc(__ballot_sync(FULL, us));
+    if (e.kind) req_st += cnt;
+    else req_ld += cnt;
+    const long long word = A >> lg_bank;
+    const unsigned mh = m & hbits;
+    const unsigned pmh = mh & lt_mask;
+    const long long pword = shfl64(word, pmh ? 31 - __clz(pmh) : lane);
+    const bool uw = iss && (pmh == 0u || pword != word);
+    unsigned rem = __ballot_sync(FULL, uw) & hbits;
+    while (__any_sync(FULL, rem != 0u)) {
+      const int first = rem ? __ffs(rem) - 1 : lane;
+      const long long cs = shfl64(word, first);
+      const bool inC = ((rem >> lane) & 1u) && ((word - cs) * bank_bytes < window);
+      const unsigned cm = __ballot_sync(FULL, inC) & hbits;
+      const int bank = (int)(word & nbm);
+      const unsigned key = inC ? (unsigned)(bank | ((lane >> lg_hw) << 8)) : (0x10000u | (unsigned)lane);
+      const unsigned peers = __match_any_sync(FULL, key);
+      int cb = inC ? __popc(peers) : 0;
+      for (int o = (1 << lg_hw) >> 1; o >= 1; o >>= 1) cb = max(cb, __shfl_xor_sync(FULL, cb, o));
+      if (hleader && rem != 0u) wf += cb;
+      rem &= ~cm;
+    }
+  }
+  lup = L.valid ? __popcll(L.act) : 0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    lup += shfl64_down(lup, o);
+    wf += shfl64_down(wf, o);
+  }
+  wf_out = wf;
+}
+
+__device__ __forceinline__ void add_warp_stats(unsigned long long* a, long long mult, long long lup, long long wf,
+                                               long long rl, long long rs) {
+  if (lup) atomicAdd(a + A_LUP, (unsigned long long)(lup * mult));
+  if (wf) atomicAdd(a + A_WF, (unsigned long long)(wf * mult));
+  if (rl) atomicAdd(a + A_REQ_LD, (unsigned long long)(rl * mult));
+  if (rs) atomicAdd(a + A_REQ_ST, (unsigned long long)(rs * mult));
+}
+
+// Pass 1: every wave warp.  A warp whose valid lanes are all fully active is a pure
+// translate of every other such warp with the same warp index and the same base
+// address residue mod M = max(sector, bank_bytes*n_banks) (DESIGN.md "Translation
+// classes"): it is only counted into its class.  Every other warp is evaluated here.
 __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                               const DInstr* __restrict__ instr, const DKernel* __restrict__ ks,
-                                              const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc) {
+                                              const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
+                                              unsigned int* __restrict__ wcnt, unsigned long long* __restrict__ wrep,
+                                              unsigned long long* __restrict__ work) {
   const long long total = pre[n].warp;
+  unsigned long long my_units = 0;
   const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
     const int c = find_config<0>(pre, n, item);
     const DPlan& P = plans[c];
-    const DKernel& K = ks[P.kid];
-    const DGpu& G = gs[P.gid];
     const long long wi = item - pre[c].warp;
     const long long B = P.s + wi / P.nwarps;
     const int w = (int)(wi % P.nwarps);
-    const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
-    const int t = w * 32 + lane;
-    const bool valid = t < P.T;
-    const int tc[3] = {t % P.b[0], (t / P.b[0]) % P.b[1], t / (P.b[0] * P.b[1])};
-    long long base[3];
-    long long lim[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      base[d] = P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d];
-      lim[d] = P.hi[d] - base[d];
+    const Lane L = lane_setup(P, B, w, lane);
+    if (P.wcls_R > 0 && __all_sync(FULL, !L.valid || L.act == full_cube(P.fcube))) {
+      if (lane == 0) {
+        const long long pl = L.base[0] + P.cls_pitch[1] * L.base[1] + P.cls_pitch[2] * L.base[2];
+        const int res = (int)(pl & (P.wcls_R - 1));  // (pl << lg_elem) mod M, in elements
+        const long long slot = (long long)c * kWSlots + w * 64 + res;
+        atomicAdd(wcnt + slot, 1u);
+        atomicExch(wrep + slot, (unsigned long long)B);
+      }
+      my_units += 32;
+      continue;
     }
-    // active folded cells of this lane (guard clipping)
-    unsigned long long act = 0;
-    if (valid && lim[0] > 0 && lim[1] > 0 && lim[2] > 0) {
-      if (lim[0] >= P.f[0] && lim[1] >= P.f[1] && lim[2] >= P.f[2]) {
-        act = P.fcube == 64 ? ~0ull : ((1ull << P.fcube) - 1ull);
-      } else {
-        for (int q = 0; q < P.fcube; ++q) {
-          int kx, ky, kz;
-          decode_kappa(q, P.f, kx, ky, kz);
-          if (kx < lim[0] && ky < lim[1] && kz < lim[2]) act |= 1ull << q;
-        }
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    long long lup, wf, rl, rs;
+    eval_warp(P, K, G, instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
+    if (lane == 0) add_warp_stats(acc + (long long)c * A_N, 1, lup, wf, rl, rs);
+    my_units += 32ull * (unsigned long long)P.n_instr;
+  }
+  if (lane == 0 && my_units) atomicAdd(work + K_WARP, my_units);
+}
+
+// Pass 2: one representative warp per non-empty class, counted class-size times.
+__global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                                const DInstr* __restrict__ instr, const DKernel* __restrict__ ks,
+                                                const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
+                                                const unsigned int* __restrict__ wcnt,
+                                                const unsigned long long* __restrict__ wrep,
+                                                unsigned long long* __restrict__ work) {
+  const long long total = pre[n].wclass;
+  unsigned long long my_units = 0;
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
+    const int c = find_config<1>(pre, n, item);
+    const DPlan& P = plans[c];
+    const long long si = item - pre[c].wclass;
+    const int w = (int)(si / P.wcls_R), res = (int)(si % P.wcls_R);
+    const long long slot = (long long)c * kWSlots + w * 64 + res;
+    const unsigned int cnt = wcnt[slot];
+    if (cnt == 0u) continue;
+    const long long B = (long long)wrep[slot];
+    const Lane L = lane_setup(P, B, w, lane);
+    long long lup, wf, rl, rs;
+    eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
+    if (lane == 0) add_warp_stats(acc + (long long)c * A_N, cnt, lup, wf, rl, rs);
+    my_units += 32ull * (unsigned long long)P.n_instr;
+  }
+  if (lane == 0 && my_units) atomicAdd(work + K_WCLASS, my_units);
+}
+
+// ------------------------------------------------------------------ a4: SM-resident block sets
+// Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
+// dispatch, Q9), row by row; every thread of the CTA participates, totals in thread 0.
+__device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
+                           DGroup* s_g, int* s_ng, long long* s_box, Tri* s_red, unsigned long long& sum_s,
+                           unsigned long long& sum_l, unsigned long long& units) {
+  const int tid = threadIdx.x;
+  const int lg_sec = G.lg_sector, lg_line = G.lg_line;
+  sum_s = sum_l = 0;
+  units = 0;
+  for (int fi = 0; fi < K.n_fields; ++fi) {
+    const DField& F = K.f[fi];
+    if (!(F.kinds & 1)) continue;
+    __syncthreads();
+    if (tid == 0) {
+      int ng = 0;
+      for (int g = F.g_begin; g < F.g_end; ++g)
+        if (K.g[g].kind == 0) s_g[ng++] = K.g[g];
+      *s_ng = ng;
+      // bounding row box of the members' cells, widened by the load offsets
+      long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
+      for (long long m = 0; m < kj; ++m) {
+        const long long Bm = S0 + m * nsm;
+        const long long by = (Bm / P.G[0]) % P.G[1], bz = Bm / (P.G[0] * P.G[1]);
+        long long a = P.lo[1] + by * P.BF[1], b = a + P.BF[1];
+        if (b > P.hi[1]) b = P.hi[1];
+        ylo = a < ylo ? a : ylo;
+        yhi = b > yhi ? b : yhi;
+        a = P.lo[2] + bz * P.BF[2];
+        b = a + P.BF[2];
+        if (b > P.hi[2]) b = P.hi[2];
+        zlo = a < zlo ? a : zlo;
+        zhi = b > zhi ? b : zhi;
+      }
+      long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
+      if (y0 < 0) y0 = 0;
+      if (z0 < 0) z0 = 0;
+      if (y1 > F.ext[1]) y1 = F.ext[1];
+      if (z1 > F.ext[2]) z1 = F.ext[2];
+      s_box[0] = y0;
+      s_box[1] = y1 > y0 ? y1 - y0 : 0;
+      s_box[2] = z0;
+      s_box[3] = z1 > z0 ? z1 - z0 : 0;
+    }
+    __syncthreads();
+    const int ng = *s_ng;
+    const long long y0 = s_box[0], ny = s_box[1], z0 = s_box[2], nz = s_box[3];
+    const long long rows = ny * nz;
+    units += (unsigned long long)(rows * ng);
+    Tri carry_s = tri_empty(), carry_l = tri_empty();
+    for (long long base = 0; base < rows; base += (long long)kRowThreads * kRowsPerThread) {
+      Tri t[2] = {tri_empty(), tri_empty()};
+      for (int u = 0; u < kRowsPerThread; ++u) {
+        const long long i = base + (long long)tid * kRowsPerThread + u;
+        if (i >= rows) break;
+        const long long z = z0 + i / ny, y = y0 + i % ny;
+        const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << F.lg_elem);
+        auto gen = [&](auto&& cb) {
+          for (int g = 0; g < ng; ++g) {
+            const DGroup gr = s_g[g];
+            const long long yy = y - gr.oy, zz = z - gr.oz;
+            if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
+            const long long r = (yy - P.lo[1]) / P.BF[1] + P.G[1] * ((zz - P.lo[2]) / P.BF[2]);
+            const long long rs = r * P.G[0];
+            const long long num2 = rs + P.G[0] - 1 - S0;
+            if (num2 < 0) continue;
+            long long m1 = num2 / nsm;
+            if (m1 > kj - 1) m1 = kj - 1;
+            const long long num = rs - S0;
+            const long long m0 = num <= 0 ? 0 : (num + nsm - 1) / nsm;
+            for (long long m = m0; m <= m1; ++m) {
+              const long long bxi = S0 + m * nsm - rs;
+              const long long x0 = P.lo[0] + bxi * P.BF[0];
+              long long x1 = x0 + P.BF[0];
+              if (x1 > P.hi[0]) x1 = P.hi[0];
+              cb(x0 + F.run_lo[gr.run], x1 + F.run_hi[gr.run]);
+            }
+          }
+        };
+        row_union(gen, R0, F.lg_elem, lg_sec, lg_line, &t[0], &t[1]);
+      }
+      cta_ordered_reduce<2>(t, s_red);
+      if (tid == 0) {
+        carry_s = tri_combine(carry_s, t[0]);
+        carry_l = tri_combine(carry_l, t[1]);
       }
     }
-    const int lg_sec = G.lg_sector, lg_bank = G.lg_bank, lg_hw = G.lg_hw;
-    const long long bank_bytes = G.g.bank_bytes, window = G.g.pair_window_bytes;
-    const int nbm = (int)G.g.n_banks - 1;
-    const unsigned hbits = (lg_hw == 5 ? FULL : ((1u << (1 << lg_hw)) - 1u)) << ((lane >> lg_hw) << lg_hw);
-    const bool hleader = (lane & ((1 << lg_hw) - 1)) == 0;
-    long long req_ld = 0, req_st = 0, wf = 0;
-    int cur_field = -1;
-    long long plane = 0;
-    const DInstr* tab = instr + (long long)c * kMaxInstr;
-    for (int i = 0; i < P.n_instr; ++i) {
-      const DInstr e = tab[i];
-      const bool iss = (e.kmask & act) != 0ull;
-      const unsigned m = __ballot_sync(FULL, iss);
-      if (m == 0u) continue;
-      if (e.field != cur_field) {
-        cur_field = e.field;
-        const DField& F = K.f[e.field];
-        plane = base[0] + F.pitch[1] * base[1] + F.pitch[2] * base[2];
-      }
-      const long long A = e.C + (plane << e.lg_elem);
-      // unique sectors of the warp instruction (lanes are address-sorted)
-      const long long sec = A >> lg_sec;
-      const unsigned pm = m & lt_mask;
-      const long long psec = shfl64(sec, pm ? 31 - __clz(pm) : lane);
-      const bool us = iss && (pm == 0u || psec != sec);
-      const int cnt = __popc(__ballot_sync(FULL, us));
-      if (e.kind) req_st += cnt;
-      else req_ld += cnt;
-      // half-warp wavefronts: unique bank words, 1024 B clusters, bank max
-      const long long word = A >> lg_bank;
-      const unsigned mh = m & hbits;
-      const unsigned pmh = mh & lt_mask;
-      const long long pword = shfl64(word, pmh ? 31 - __clz(pmh) : lane);
-      const bool uw = iss && (pmh == 0u || pword != word);
-      unsigned rem = __ballot_sync(FULL, uw) & hbits;
-      while (__any_sync(FULL, rem != 0u)) {
-        const int first = rem ? __ffs(rem) - 1 : lane;
-        const long long cs = shfl64(word, first);
-        const bool inC = ((rem >> lane) & 1u) && ((word - cs) * bank_bytes < window);
-        const unsigned cm = __ballot_sync(FULL, inC) & hbits;
-        const int bank = (int)(word & nbm);
-        const unsigned key = inC ? (unsigned)(bank | ((lane >> lg_hw) << 8)) : (0x10000u | (unsigned)lane);
-        const unsigned peers = __match_any_sync(FULL, key);
-        int cb = inC ? __popc(peers) : 0;
-        for (int o = (1 << lg_hw) >> 1; o >= 1; o >>= 1) cb = max(cb, __shfl_xor_sync(FULL, cb, o));
-        if (hleader && rem != 0u) wf += cb;
-        rem &= ~cm;
-      }
-    }
-    // lattice updates of this warp
-    long long lup = valid ? __popcll(act) : 0;
-    long long wfl = wf;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      lup += shfl64_down(lup, o);
-      wfl += shfl64_down(wfl, o);
-    }
-    if (lane == 0) {
-      unsigned long long* a = acc + (long long)c * A_N;
-      if (lup) atomicAdd(a + A_LUP, (unsigned long long)lup);
-      if (wfl) atomicAdd(a + A_WF, (unsigned long long)wfl);
-      if (req_ld) atomicAdd(a + A_REQ_LD, (unsigned long long)req_ld);
-      if (req_st) atomicAdd(a + A_REQ_ST, (unsigned long long)req_st);
+    if (tid == 0) {
+      sum_s += (unsigned long long)carry_s.c;
+      sum_l += (unsigned long long)carry_l.c;
     }
   }
 }
 
-// ------------------------------------------------------------------ a4: SM-resident block sets
+__device__ __forceinline__ bool block_interior(const DPlan& P, long long B) {
+  const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    if ((bc[d] + 1) * P.BF[d] > P.hi[d] - P.lo[d]) return false;
+  return true;
+}
+
+// Pass 1: single-block SM sets of fully interior blocks go to their translation class
+// (residue of the block's first cell address mod line_bytes); the rest are evaluated here.
 __global__ void __launch_bounds__(kRowThreads) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
                                                        int n, const DKernel* __restrict__ ks,
                                                        const DGpu* __restrict__ gs,
-                                                       unsigned long long* __restrict__ acc) {
+                                                       unsigned long long* __restrict__ acc,
+                                                       unsigned int* __restrict__ scnt,
+                                                       unsigned long long* __restrict__ srep,
+                                                       unsigned long long* __restrict__ work) {
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
@@ -535,101 +745,65 @@ __global__ void __launch_bounds__(kRowThreads) k_smset(const DPlan* __restrict__
   const long long total = pre[n].set;
   const int tid = threadIdx.x;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const int c = find_config<1>(pre, n, item);
+    const int c = find_config<2>(pre, n, item);
     const DPlan& P = plans[c];
-    const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
     const long long j = item - pre[c].set;
     const long long nsm = G.g.n_sm;
     const long long S0 = P.s + j;
     const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-    const int lg_sec = G.lg_sector, lg_line = G.lg_line;
-    unsigned long long sum_s = 0, sum_l = 0;
-    for (int fi = 0; fi < K.n_fields; ++fi) {
-      const DField& F = K.f[fi];
-      if (!(F.kinds & 1)) continue;
-      __syncthreads();
+    if (P.scls_R > 0 && kj == 1 && block_interior(P, S0)) {
       if (tid == 0) {
-        int ng = 0;
-        for (int g = F.g_begin; g < F.g_end; ++g)
-          if (K.g[g].kind == 0) s_g[ng++] = K.g[g];
-        s_ng = ng;
-        // bounding row box of the members' cells, widened by the load offsets
-        long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
-        for (long long m = 0; m < kj; ++m) {
-          const long long Bm = S0 + m * nsm;
-          const long long by = (Bm / P.G[0]) % P.G[1], bz = Bm / (P.G[0] * P.G[1]);
-          long long a = P.lo[1] + by * P.BF[1], b = a + P.BF[1];
-          if (b > P.hi[1]) b = P.hi[1];
-          ylo = a < ylo ? a : ylo;
-          yhi = b > yhi ? b : yhi;
-          a = P.lo[2] + bz * P.BF[2];
-          b = a + P.BF[2];
-          if (b > P.hi[2]) b = P.hi[2];
-          zlo = a < zlo ? a : zlo;
-          zhi = b > zhi ? b : zhi;
-        }
-        long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
-        if (y0 < 0) y0 = 0;
-        if (z0 < 0) z0 = 0;
-        if (y1 > F.ext[1]) y1 = F.ext[1];
-        if (z1 > F.ext[2]) z1 = F.ext[2];
-        s_box[0] = y0;
-        s_box[1] = y1 > y0 ? y1 - y0 : 0;
-        s_box[2] = z0;
-        s_box[3] = z1 > z0 ? z1 - z0 : 0;
+        const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
+        long long pl = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+        const long long slot = (long long)c * kSSlots + (pl & (P.scls_R - 1));
+        atomicAdd(scnt + slot, 1u);
+        atomicExch(srep + slot, (unsigned long long)S0);
       }
-      __syncthreads();
-      const int ng = s_ng;
-      const long long y0 = s_box[0], ny = s_box[1], z0 = s_box[2], nz = s_box[3];
-      const long long rows = ny * nz;
-      Tri carry_s = tri_empty(), carry_l = tri_empty();
-      for (long long base = 0; base < rows; base += (long long)kRowThreads * kRowsPerThread) {
-        Tri t[2] = {tri_empty(), tri_empty()};
-        for (int u = 0; u < kRowsPerThread; ++u) {
-          const long long i = base + (long long)tid * kRowsPerThread + u;
-          if (i >= rows) break;
-          const long long z = z0 + i / ny, y = y0 + i % ny;
-          const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << F.lg_elem);
-          auto gen = [&](auto&& cb) {
-            for (int g = 0; g < ng; ++g) {
-              const DGroup gr = s_g[g];
-              const long long yy = y - gr.oy, zz = z - gr.oz;
-              if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
-              const long long r = (yy - P.lo[1]) / P.BF[1] + P.G[1] * ((zz - P.lo[2]) / P.BF[2]);
-              const long long rs = r * P.G[0];
-              const long long num2 = rs + P.G[0] - 1 - S0;
-              if (num2 < 0) continue;
-              long long m1 = num2 / nsm;
-              if (m1 > kj - 1) m1 = kj - 1;
-              const long long num = rs - S0;
-              const long long m0 = num <= 0 ? 0 : (num + nsm - 1) / nsm;
-              for (long long m = m0; m <= m1; ++m) {
-                const long long bxi = S0 + m * nsm - rs;
-                const long long x0 = P.lo[0] + bxi * P.BF[0];
-                long long x1 = x0 + P.BF[0];
-                if (x1 > P.hi[0]) x1 = P.hi[0];
-                cb(x0 + F.run_lo[gr.run], x1 + F.run_hi[gr.run]);
-              }
-            }
-          };
-          row_union(gen, R0, F.lg_elem, lg_sec, lg_line, &t[0], &t[1]);
-        }
-        cta_ordered_reduce<2>(t, s_red);
-        if (tid == 0) {
-          carry_s = tri_combine(carry_s, t[0]);
-          carry_l = tri_combine(carry_l, t[1]);
-        }
-      }
-      if (tid == 0) {
-        sum_s += (unsigned long long)carry_s.c;
-        sum_l += (unsigned long long)carry_l.c;
-      }
+      continue;
     }
+    unsigned long long ss, sl, un;
+    smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_red, ss, sl, un);
     if (tid == 0) {
       unsigned long long* a = acc + (long long)c * A_N;
-      atomicAdd(a + A_SM_SEC, sum_s);
-      atomicAdd(a + A_SM_LIN, sum_l);
+      atomicAdd(a + A_SM_SEC, ss);
+      atomicAdd(a + A_SM_LIN, sl);
+      atomicAdd(work + K_SMSET, un);
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2: one representative block per non-empty SM-set class, counted class-size times.
+__global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict__ plans,
+                                                        const DPrefix* __restrict__ pre, int n,
+                                                        const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                                        unsigned long long* __restrict__ acc,
+                                                        const unsigned int* __restrict__ scnt,
+                                                        const unsigned long long* __restrict__ srep,
+                                                        unsigned long long* __restrict__ work) {
+  __shared__ DGroup s_g[kMaxAcc];
+  __shared__ int s_ng;
+  __shared__ long long s_box[4];
+  __shared__ Tri s_red[(kRowThreads / 32) * 2];
+  const long long total = pre[n].sclass;
+  const int tid = threadIdx.x;
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_config<3>(pre, n, item);
+    const DPlan& P = plans[c];
+    const long long slot = (long long)c * kSSlots + (item - pre[c].sclass);
+    const unsigned int cnt = scnt[slot];
+    if (cnt == 0u) continue;
+    const DGpu& G = gs[P.gid];
+    unsigned long long ss, sl, un;
+    smset_eval(P, ks[P.kid], G, (long long)srep[slot], 1, G.g.n_sm, s_g, &s_ng, s_box, s_red, ss, sl, un);
+    if (tid == 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      atomicAdd(a + A_SM_SEC, ss * cnt);
+      atomicAdd(a + A_SM_LIN, sl * cnt);
+      atomicAdd(work + K_SCLASS, un);
     }
     __syncthreads();
   }
@@ -654,14 +828,15 @@ __device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
 __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
                                                       int n, const DKernel* __restrict__ ks,
                                                       const DGpu* __restrict__ gs, const DRowInfo* __restrict__ rowinfo,
-                                                      long long* __restrict__ chunkres) {
+                                                      long long* __restrict__ chunkres,
+                                                      unsigned long long* __restrict__ work) {
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ RangeInfo s_r[5];
   __shared__ Tri s_red[(kRowThreads / 32) * kNQ];
   const long long total = pre[n].chunk;
   const int tid = threadIdx.x;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const int c = find_config<2>(pre, n, item);
+    const int c = find_config<4>(pre, n, item);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
@@ -766,6 +941,9 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ 
     }
     cta_ordered_reduce<kNQ>(t, s_red);
     if (tid == 0) {
+      long long nr = rows - chunk_in_field * kRowsPerChunk;
+      if (nr > kRowsPerChunk) nr = kRowsPerChunk;
+      atomicAdd(work + K_ROWS, (unsigned long long)(nr * ng));
       long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) {
@@ -786,7 +964,7 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
   const int lane = threadIdx.x & 31;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
-    const int c = find_config<3>(pre, n, item);
+    const int c = find_config<5>(pre, n, item);
     const int fi = (int)(item - pre[c].fold);
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
@@ -929,29 +1107,52 @@ static int check_launch() {
 }
 
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
-                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches) {
+                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches,
+                    cudaEvent_t* ev) {
   uint32_t L = 0;
-  k_plan<<<n, 128, 0, st>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc);
-  ++L;
-  k_scan<<<1, 1024, 0, st>>>(s.plans, n, s.prefix);
-  ++L;
+  int mk = 0;
+  auto mark = [&]() {
+    if (ev) cudaEventRecord(ev[mk], st);
+    ++mk;
+  };
   const int persist = n_sm_dev * 8;
-  k_warp<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc);
+  mark();
+  k_plan<<<n, 128, 0, st>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt);
   ++L;
-  k_smset<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc);
+  mark();
+  k_scan<<<1, 1024, 0, st>>>(s.plans, n, s.prefix, s.work);
   ++L;
-  k_rows<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres);
+  mark();
+  k_warp<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.work);
   ++L;
+  mark();
+  k_wclass<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.work);
+  ++L;
+  mark();
+  k_smset<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.scnt, s.srep, s.work);
+  ++L;
+  mark();
+  k_sclass<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.scnt, s.srep, s.work);
+  ++L;
+  mark();
+  k_rows<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
+  ++L;
+  mark();
   k_fold<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, s.rowinfo, s.chunkres, s.acc);
   ++L;
+  mark();
   k_model<<<(n + 127) / 128, 128, 0, st>>>(s.plans, n, d_k, d_g, s.acc, d_out);
   ++L;
+  mark();
   if (launches) *launches = L;
   return check_launch();
 }
 
-int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches) {
+int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches,
+                cudaEvent_t* ev) {
+  if (ev) cudaEventRecord(ev[0], st);
   k_rank<<<(n + 255) / 256, 256, 0, st>>>(d_res, n, k, d_top);
+  if (ev) cudaEventRecord(ev[1], st);
   if (launches) *launches = 1;
   return check_launch();
 }

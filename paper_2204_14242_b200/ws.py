@@ -64,7 +64,8 @@ CONFIG_DTYPE = np.dtype(ws_config)
 RESULT_DTYPE = np.dtype(ws_result)
 
 EXPORTS = ["ws_create", "ws_destroy", "ws_last_error", "ws_set_stream", "ws_describe_kernel", "ws_describe_gpu",
-           "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count"]
+           "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count",
+           "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read"]
 
 _lib = None
 
@@ -93,8 +94,13 @@ def load_library(path: str = LIB_PATH):
     L.ws_rank_async.argtypes = [P, P, C.c_size_t, C.c_size_t, P]
     L.ws_last_launch_count.argtypes = [P]
     L.ws_last_launch_count.restype = U32
+    L.ws_profile_enable.argtypes = [P, C.c_int]
+    L.ws_profile_read.argtypes = [P, C.POINTER(F64), C.POINTER(U64), U32, C.POINTER(U32)]
+    L.ws_work_read.argtypes = [P, C.POINTER(U64), U32]
+    L.ws_kernel_name.argtypes = [U32]
+    L.ws_kernel_name.restype = C.c_char_p
     for n in EXPORTS:
-        if n not in ("ws_destroy", "ws_last_error", "ws_last_launch_count"):
+        if n not in ("ws_destroy", "ws_last_error", "ws_last_launch_count", "ws_kernel_name"):
             getattr(L, n).restype = C.c_int
     _lib = L
     return L
@@ -227,3 +233,27 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(self.L.ws_last_launch_count(self.h))
+
+    def profile_enable(self, on: bool = True):
+        self._check(self.L.ws_profile_enable(self.h, int(on)))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (summed device ms, launches)} since the last read (synchronises)."""
+        ms = (F64 * 16)()
+        cnt = (U64 * 16)()
+        nk = U32()
+        self._check(self.L.ws_profile_read(self.h, ms, cnt, 16, C.byref(nk)))
+        return {self.L.ws_kernel_name(i).decode(): (ms[i], int(cnt[i])) for i in range(nk.value)}
+
+    def work_read(self) -> dict:
+        """{kernel name: algorithmic work units of the last estimate call} (synchronises)."""
+        u = (U64 * 16)()
+        self._check(self.L.ws_work_read(self.h, u, 16))
+        out, i = {}, 0
+        while True:
+            nm = self.L.ws_kernel_name(i)
+            if nm is None:
+                break
+            out[nm.decode()] = int(u[i])
+            i += 1
+        return out

@@ -1,0 +1,34 @@
+"""Per-kernel device times of one workload (development probe)."""
+import sys, os, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import workloads as W
+from paper_2204_14242_b200 import Context, config_array, result_dicts
+
+def run(name, k, g, cfgs, reps=5):
+    ctx = Context(0, torch.cuda.current_stream().cuda_stream)
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
+    a = config_array(kid, gid, cfgs)
+    n = len(a)
+    dc = torch.from_numpy(a.view(np.uint8)).cuda()
+    do = torch.empty(n * 296, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
+    torch.cuda.synchronize()
+    ctx.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
+    e1.record(); torch.cuda.synchronize()
+    prof = ctx.profile_read()
+    tot = e0.elapsed_time(e1) / reps
+    print(f"{name}: n={n} step {tot:.3f} ms -> {n/tot*1e3:.0f} configs/s")
+    for kname, (ms, cnt) in prof.items():
+        if cnt: print(f"   {kname:8s} {ms/cnt:9.4f} ms")
+
+run("configs1 K25 512^3 A100 168", W.k25(512), W.gpu_a100(), W.space_stencil_paper())
+run("configs2 LBM15 256^3 A100 49", W.lbm15(256), W.gpu_a100(), W.space_lbm())
+run("configs2 LBM27 256^3 A100 49", W.lbm27(256), W.gpu_a100(), W.space_lbm())
+run("configs0 K7 64^3 V100 16", W.k7(64), W.gpu_v100(), W.space_k7())
+run("extended K25 512^3 A100", W.k25(512), W.gpu_a100(), W.space_extended(), reps=2)
