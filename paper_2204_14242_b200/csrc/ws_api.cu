@@ -124,6 +124,9 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   const size_t o_scnt = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned int));
   const size_t o_srep = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
   const size_t o_work = off;    off = align_up(off + 16 * sizeof(unsigned long long));
+  const size_t o_lists = off;   off = align_up(off + 4 * sizeof(unsigned long long));
+  const size_t o_wlist = off;   off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
+  const size_t o_slist = off;   off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
   if (off > c->scratch_cap) {
     if (c->scratch) cudaFree(c->scratch);
     c->scratch = nullptr;
@@ -145,6 +148,9 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   s.scnt = (unsigned int*)(b + o_scnt);
   s.srep = (unsigned long long*)(b + o_srep);
   s.work = (unsigned long long*)(b + o_work);
+  s.lists = (unsigned long long*)(b + o_lists);
+  s.wlist = (unsigned long long*)(b + o_wlist);
+  s.slist = (unsigned long long*)(b + o_slist);
   c->last_work = s.work;
   return WS_OK;
 }

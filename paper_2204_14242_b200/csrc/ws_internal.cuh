@@ -62,6 +62,12 @@ struct DRowInfo {
   int64_t y0, ny, z0, nz, chunk_begin, n_chunks;
 };
 
+// n / d for 0 <= n < 2^31 by multiply-high (Granlund-Montgomery round-up method):
+// q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
+struct FDiv {
+  uint32_t m, l;
+};
+
 struct DPlan {
   int32_t status, kid, gid, n_instr;
   int32_t b[3], f[3];
@@ -74,6 +80,8 @@ struct DPlan {
   int32_t cls_lg_elem, pad2;
   int64_t n_warp_items, n_wclass_items, n_set_items, n_sclass_items, n_chunks, n_fields;
   uint64_t addr_evals;
+  FDiv fd_BF[3];                 // division by BF[d] (cell -> block coordinate)
+  int64_t part[3];               // extent of a partial last block per dim (0 = none)
 };
 
 // per-config accumulator slots (u64, atomically added by the worker kernels)
@@ -86,8 +94,8 @@ struct DPrefix {
   int64_t warp, wclass, set, sclass, chunk, fold;
 };
 constexpr int kNPrefix = 6;
-constexpr int kWSlots = 32 * 64;   // per config: warp index (<32) x residue (<64)
-constexpr int kSSlots = 64;        // per config: residue (<64)
+constexpr int kWSlots = 32 * 64 * 8;  // per config: warp index (<32) x residue (<64) x clip pattern (<8)
+constexpr int kSSlots = 64 * 8;       // per config: residue (<64) x clip pattern (<8)
 
 // ---------------------------------------------------------------- launchers (ws_kernels.cu)
 struct Scratch {
@@ -103,6 +111,9 @@ struct Scratch {
   unsigned int* scnt;         // n * kSSlots
   unsigned long long* srep;   // n * kSSlots
   unsigned long long* work;   // K_NKINDS algorithmic work units of the last call (ws_work_read)
+  unsigned long long* lists;  // [0] = # warp classes, [1] = # SM-set classes (zeroed by k_scan)
+  unsigned long long* wlist;  // n * kWSlots entries (config << 32 | slot)
+  unsigned long long* slist;  // n * kSSlots entries
 };
 
 // kernel kinds, in launch order (ws_kernel_name)

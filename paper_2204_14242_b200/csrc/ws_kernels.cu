@@ -48,6 +48,19 @@ __device__ __forceinline__ long long shfl64_down(long long v, int d) {
   return ((long long)hi << 32) | (unsigned int)lo;
 }
 
+__device__ __forceinline__ FDiv make_fdiv(unsigned long long d) {
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  FDiv f;
+  f.l = l;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1ull);
+  return f;
+}
+// n / d for 0 <= n < 2^31
+__device__ __forceinline__ long long fdiv(long long n, FDiv f) {
+  return (long long)((__umulhi((unsigned)n, f.m) + (unsigned)n) >> f.l);
+}
+
 struct Tri {
   long long f, l, c;  // first, last, count; c == 0: empty
 };
@@ -218,6 +231,11 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   P.nsets = (long long)G.g.n_sm < P.W ? (long long)G.g.n_sm : P.W;
   P.Ly0 = s - P.G[0] > 0 ? s - P.G[0] : 0;
   P.Lz0 = s - P.G[0] * P.G[1] > 0 ? s - P.G[0] * P.G[1] : 0;
+  for (int d = 0; d < 3; ++d) {
+    P.fd_BF[d] = make_fdiv((unsigned long long)P.BF[d]);
+    const long long last = (K.hi[d] - K.lo[d]) - (P.G[d] - 1) * P.BF[d];
+    P.part[d] = last < P.BF[d] ? last : 0;
+  }
   // translation classes need one pitch and one element size for every field
   bool same = true;
   for (int i = 1; i < K.n_fields; ++i)
@@ -247,8 +265,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
   __shared__ DPlan P;
-  for (int i = tid; i < kWSlots; i += blockDim.x) wcnt[(long long)c * kWSlots + i] = 0u;
-  if (tid < kSSlots) scnt[(long long)c * kSSlots + tid] = 0u;
+
   __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
   __shared__ int s_part[128];
   __shared__ int s_total;
@@ -387,9 +404,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     DPlan Q = P;
     Q.n_instr = s_total;
     Q.n_warp_items = P.W * P.nwarps;
-    Q.n_wclass_items = (long long)P.nwarps * P.wcls_R;
+    Q.n_wclass_items = 0;
     Q.n_set_items = P.nsets;
-    Q.n_sclass_items = P.scls_R;
+    Q.n_sclass_items = 0;
     Q.n_chunks = cb;
     Q.n_fields = K.n_fields;
     Q.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
@@ -410,10 +427,12 @@ __device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
 }
 
 __global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
-                                               unsigned long long* __restrict__ work) {
+                                               unsigned long long* __restrict__ work,
+                                               unsigned long long* __restrict__ lists) {
   __shared__ long long s[kNPrefix][1024];
   const int tid = threadIdx.x, nt = blockDim.x;
   if (tid < 16) work[tid] = 0ull;
+  if (tid < 4) lists[tid] = 0ull;
   const int seg = (n + nt - 1) / nt;
   long long a[kNPrefix];
 #pragma unroll
@@ -488,43 +507,62 @@ __device__ __forceinline__ Lane lane_setup(const DPlan& P, long long B, int w, i
 // Every instruction of one warp: unique sectors per warp instruction (the
 // issuing lanes are address-sorted, so comparing with the previous issuing lane
 // dedupes) and half-warp wavefronts (unique bank words, greedy 1024 B
-// clusters, max bank multiplicity via __match_any_sync).  Returns warp totals in lane 0.
+// clusters, max bank multiplicity).  Wavefronts, loop-free when every run of
+// unique words between gaps >= the pair window spans less than the window (then
+// the greedy clusters are exactly those runs): sum over clusters of the max bank
+// multiplicity = number of distinct (cluster, rank-within-bank) pairs.  Otherwise
+// the greedy split is walked cluster by cluster.  Returns warp totals in lane 0.
 __device__ void eval_warp(const DPlan& P, const DKernel& K, const DGpu& G, const DInstr* __restrict__ tab,
                           const Lane& L, int lane, long long& lup, long long& wf_out, long long& req_ld,
                           long long& req_st) {
-  const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned lt_mask = (1u << lane) - 1u, le_mask = lt_mask | (1u << lane);
   const int lg_sec = G.lg_sector, lg_bank = G.lg_bank, lg_hw = G.lg_hw;
   const long long bank_bytes = G.g.bank_bytes, window = G.g.pair_window_bytes;
   const int nbm = (int)G.g.n_banks - 1;
   const unsigned hbits = (lg_hw == 5 ? FULL : ((1u << (1 << lg_hw)) - 1u)) << ((lane >> lg_hw) << lg_hw);
   const bool hleader = (lane & ((1 << lg_hw) - 1)) == 0;
-  long long wf = 0;
+  long long wf_u = 0, wf_l = 0;  // warp-uniform part / per half-warp-leader part
   req_ld = req_st = 0;
   int cur_field = -1;
   long long plane = 0;
-  for (int i = 0; i < P.n_instr; ++i) {
-    const DInstr e = tab[i];
-    const bool iss = (e.kmask & L.act) != 0ull;
+  const int ni = P.n_instr;
+  DInstr e = tab[0];
+  for (int i = 0; i < ni; ++i) {
+    const DInstr cur = e;
+    if (i + 1 < ni) e = tab[i + 1];
+    const bool iss = (cur.kmask & L.act) != 0ull;
     const unsigned m = __ballot_sync(FULL, iss);
     if (m == 0u) continue;
-    if (e.field != cur_field) {
-      cur_field = e.field;
-      const DField& F = K.f[e.field];
+    if (cur.field != cur_field) {
+      cur_field = cur.field;
+      const DField& F = K.f[cur.field];
       plane = L.base[0] + F.pitch[1] * L.base[1] + F.pitch[2] * L.base[2];
     }
-    const long long A = e.C + (plane << e.lg_elem);
+    const long long A = cur.C + (plane << cur.lg_elem);
     const long long sec = A >> lg_sec;
     const unsigned pm = m & lt_mask;
     const long long psec = shfl64(sec, pm ? 31 - __clz(pm) : lane);
     const bool us = iss && (pm == 0u || psec != sec);
     const int cnt = __popc(__ballot_sync(FULL, us));
-    if (e.kind) req_st += cnt;
+    if (cur.kind) req_st += cnt;
     else req_ld += cnt;
     const long long word = A >> lg_bank;
-    const unsigned mh = m & hbits;
-    const unsigned pmh = mh & lt_mask;
+    const unsigned pmh = m & hbits & lt_mask;
     const long long pword = shfl64(word, pmh ? 31 - __clz(pmh) : lane);
     const bool uw = iss && (pmh == 0u || pword != word);
+    const bool bnd = uw && (pmh == 0u || (word - pword) * bank_bytes >= window);
+    const unsigned bm = __ballot_sync(FULL, bnd) & hbits & le_mask;
+    const int sl = bm ? 31 - __clz(bm) : lane;
+    const long long sword = shfl64(word, sl);
+    const bool longseg = uw && (word - sword) * bank_bytes >= window;
+    if (!__any_sync(FULL, longseg)) {
+      const int bank = (int)(word & nbm);
+      const unsigned peers = __match_any_sync(FULL, uw ? (unsigned)(bank | (sl << 8)) : (0x10000u | (unsigned)lane));
+      const int rank = __popc(peers & le_mask);
+      const unsigned p2 = __match_any_sync(FULL, uw ? (unsigned)(rank | (sl << 8)) : (0x10000u | (unsigned)lane));
+      wf_u += __popc(__ballot_sync(FULL, uw && (p2 & lt_mask) == 0u));
+      continue;
+    }
     unsigned rem = __ballot_sync(FULL, uw) & hbits;
     while (__any_sync(FULL, rem != 0u)) {
       const int first = rem ? __ffs(rem) - 1 : lane;
@@ -536,7 +574,7 @@ __device__ void eval_warp(const DPlan& P, const DKernel& K, const DGpu& G, const
       const unsigned peers = __match_any_sync(FULL, key);
       int cb = inC ? __popc(peers) : 0;
       for (int o = (1 << lg_hw) >> 1; o >= 1; o >>= 1) cb = max(cb, __shfl_xor_sync(FULL, cb, o));
-      if (hleader && rem != 0u) wf += cb;
+      if (hleader && rem != 0u) wf_l += cb;
       rem &= ~cm;
     }
   }
@@ -544,9 +582,9 @@ __device__ void eval_warp(const DPlan& P, const DKernel& K, const DGpu& G, const
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
     lup += shfl64_down(lup, o);
-    wf += shfl64_down(wf, o);
+    wf_l += shfl64_down(wf_l, o);
   }
-  wf_out = wf;
+  wf_out = wf_l + wf_u;
 }
 
 __device__ __forceinline__ void add_warp_stats(unsigned long long* a, long long mult, long long lup, long long wf,
@@ -557,18 +595,31 @@ __device__ __forceinline__ void add_warp_stats(unsigned long long* a, long long 
   if (rs) atomicAdd(a + A_REQ_ST, (unsigned long long)(rs * mult));
 }
 
-// Pass 1: every wave warp.  A warp whose valid lanes are all fully active is a pure
-// translate of every other such warp with the same warp index and the same base
-// address residue mod M = max(sector, bank_bytes*n_banks) (DESIGN.md "Translation
-// classes"): it is only counted into its class.  Every other warp is evaluated here.
+// clip pattern of a block: bit d set when it is the partial last block along d
+__device__ __forceinline__ int clip_pattern(const DPlan& P, const long long* bc) {
+  int pat = 0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    if (P.part[d] != 0 && bc[d] == P.G[d] - 1) pat |= 1 << d;
+  return pat;
+}
+
+// Pass 1 over every wave warp.  Two warps with the same warp index, the same clip
+// pattern of their block (hence identical lane activity) and the same base address
+// residue mod M = max(sector, bank_bytes*n_banks) are translates by a multiple of M:
+// identical sector, bank and cluster statistics.
+// With classes enabled the warp is only counted into its class (first member
+// appends the class to a compact list); otherwise it is evaluated here.
 __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                               const DInstr* __restrict__ instr, const DKernel* __restrict__ ks,
                                               const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
                                               unsigned int* __restrict__ wcnt, unsigned long long* __restrict__ wrep,
+                                              unsigned long long* __restrict__ lists,
+                                              unsigned long long* __restrict__ wlist,
                                               unsigned long long* __restrict__ work) {
   const long long total = pre[n].warp;
-  unsigned long long my_units = 0;
   const int lane = threadIdx.x & 31;
+  unsigned long long my_units = 0;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
     const int c = find_config<0>(pre, n, item);
@@ -576,48 +627,57 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
     const long long wi = item - pre[c].warp;
     const long long B = P.s + wi / P.nwarps;
     const int w = (int)(wi % P.nwarps);
-    const Lane L = lane_setup(P, B, w, lane);
-    if (P.wcls_R > 0 && __all_sync(FULL, !L.valid || L.act == full_cube(P.fcube))) {
+    if (P.wcls_R > 0) {
       if (lane == 0) {
-        const long long pl = L.base[0] + P.cls_pitch[1] * L.base[1] + P.cls_pitch[2] * L.base[2];
-        const int res = (int)(pl & (P.wcls_R - 1));  // (pl << lg_elem) mod M, in elements
-        const long long slot = (long long)c * kWSlots + w * 64 + res;
-        atomicAdd(wcnt + slot, 1u);
-        atomicExch(wrep + slot, (unsigned long long)B);
+        const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
+        const int t0 = w * 32;
+        const long long tc[3] = {t0 % P.b[0], (t0 / P.b[0]) % P.b[1], t0 / (P.b[0] * P.b[1])};
+        long long pl = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d]);
+        const int res = (int)(pl & (P.wcls_R - 1));  // (pl * elem) mod M, in elements
+        const unsigned slot = (unsigned)(((w * 64 + res) << 3) | clip_pattern(P, bc));
+        const long long gslot = (long long)c * kWSlots + slot;
+        if (atomicAdd(wcnt + gslot, 1u) == 0u) {
+          wrep[gslot] = (unsigned long long)B;
+          const unsigned long long idx = atomicAdd(lists + 0, 1ull);
+          wlist[idx] = ((unsigned long long)c << 32) | slot;
+        }
       }
       my_units += 32;
       continue;
     }
-    const DKernel& K = ks[P.kid];
-    const DGpu& G = gs[P.gid];
+    const Lane L = lane_setup(P, B, w, lane);
     long long lup, wf, rl, rs;
-    eval_warp(P, K, G, instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
+    eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
     if (lane == 0) add_warp_stats(acc + (long long)c * A_N, 1, lup, wf, rl, rs);
     my_units += 32ull * (unsigned long long)P.n_instr;
   }
   if (lane == 0 && my_units) atomicAdd(work + K_WARP, my_units);
 }
 
-// Pass 2: one representative warp per non-empty class, counted class-size times.
-__global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
-                                                const DInstr* __restrict__ instr, const DKernel* __restrict__ ks,
-                                                const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
+// Pass 2: one representative warp per class, counted class-size times.
+__global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans, const DInstr* __restrict__ instr,
+                                                const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                                unsigned long long* __restrict__ acc,
                                                 const unsigned int* __restrict__ wcnt,
                                                 const unsigned long long* __restrict__ wrep,
+                                                const unsigned long long* __restrict__ lists,
+                                                const unsigned long long* __restrict__ wlist,
                                                 unsigned long long* __restrict__ work) {
-  const long long total = pre[n].wclass;
-  unsigned long long my_units = 0;
+  const long long total = (long long)lists[0];
   const int lane = threadIdx.x & 31;
+  unsigned long long my_units = 0;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
-    const int c = find_config<1>(pre, n, item);
+    const unsigned long long ent = wlist[item];
+    const int c = (int)(ent >> 32);
+    const unsigned slot = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
-    const long long si = item - pre[c].wclass;
-    const int w = (int)(si / P.wcls_R), res = (int)(si % P.wcls_R);
-    const long long slot = (long long)c * kWSlots + w * 64 + res;
-    const unsigned int cnt = wcnt[slot];
-    if (cnt == 0u) continue;
-    const long long B = (long long)wrep[slot];
+    const long long gslot = (long long)c * kWSlots + slot;
+    const unsigned int cnt = wcnt[gslot];
+    const long long B = (long long)wrep[gslot];
+    const int w = (int)(slot >> 9);
     const Lane L = lane_setup(P, B, w, lane);
     long long lup, wf, rl, rs;
     eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
@@ -628,15 +688,37 @@ __global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans,
 }
 
 // ------------------------------------------------------------------ a4: SM-resident block sets
+struct SmBox {
+  long long x0, x1, y0, y1, z0, z1;  // active cell box of one member block (clipped to the domain)
+};
+constexpr int kMaxMembers = 32;
+
 // Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
-// dispatch, Q9), row by row; every thread of the CTA participates, totals in thread 0.
+// dispatch, Q9), row by row.  A row (y,z) of field phi holds element x iff some member's
+// box contains (x - ox, y - oy, z - oz) for a load offset o: per (row, offset group) the
+// member boxes are tested with compares only and the candidate intervals (member, x-run)
+// collected in a bitmask (<= 4 members) for the union.  Every thread of the CTA
+// participates; totals in thread 0.
 __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
-                           DGroup* s_g, int* s_ng, long long* s_box, Tri* s_red, unsigned long long& sum_s,
-                           unsigned long long& sum_l, unsigned long long& units) {
+                           DGroup* s_g, int* s_ng, long long* s_box, SmBox* s_mb, Tri* s_red,
+                           unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
   const int tid = threadIdx.x;
   const int lg_sec = G.lg_sector, lg_line = G.lg_line;
   sum_s = sum_l = 0;
   units = 0;
+  const int nm = (int)(kj < kMaxMembers ? kj : kMaxMembers);
+  __syncthreads();
+  for (int m = tid; m < nm; m += blockDim.x) {
+    const long long Bm = S0 + (long long)m * nsm;
+    const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+    long long lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = P.lo[d] + bc[d] * P.BF[d];
+      hi[d] = lo[d] + P.BF[d];
+      if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
+    }
+    s_mb[m] = SmBox{lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]};
+  }
   for (int fi = 0; fi < K.n_fields; ++fi) {
     const DField& F = K.f[fi];
     if (!(F.kinds & 1)) continue;
@@ -646,20 +728,12 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
       for (int g = F.g_begin; g < F.g_end; ++g)
         if (K.g[g].kind == 0) s_g[ng++] = K.g[g];
       *s_ng = ng;
-      // bounding row box of the members' cells, widened by the load offsets
       long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
-      for (long long m = 0; m < kj; ++m) {
-        const long long Bm = S0 + m * nsm;
-        const long long by = (Bm / P.G[0]) % P.G[1], bz = Bm / (P.G[0] * P.G[1]);
-        long long a = P.lo[1] + by * P.BF[1], b = a + P.BF[1];
-        if (b > P.hi[1]) b = P.hi[1];
-        ylo = a < ylo ? a : ylo;
-        yhi = b > yhi ? b : yhi;
-        a = P.lo[2] + bz * P.BF[2];
-        b = a + P.BF[2];
-        if (b > P.hi[2]) b = P.hi[2];
-        zlo = a < zlo ? a : zlo;
-        zhi = b > zhi ? b : zhi;
+      for (int m = 0; m < nm; ++m) {
+        ylo = min(ylo, s_mb[m].y0);
+        yhi = max(yhi, s_mb[m].y1);
+        zlo = min(zlo, s_mb[m].z0);
+        zhi = max(zhi, s_mb[m].z1);
       }
       long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
       if (y0 < 0) y0 = 0;
@@ -676,6 +750,8 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
     const long long y0 = s_box[0], ny = s_box[1], z0 = s_box[2], nz = s_box[3];
     const long long rows = ny * nz;
     units += (unsigned long long)(rows * ng);
+    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
+    const int le = F.lg_elem;
     Tri carry_s = tri_empty(), carry_l = tri_empty();
     for (long long base = 0; base < rows; base += (long long)kRowThreads * kRowsPerThread) {
       Tri t[2] = {tri_empty(), tri_empty()};
@@ -683,30 +759,41 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
         const long long i = base + (long long)tid * kRowsPerThread + u;
         if (i >= rows) break;
         const long long z = z0 + i / ny, y = y0 + i % ny;
-        const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << F.lg_elem);
-        auto gen = [&](auto&& cb) {
+        const long long R0 = align + ((py * y + pz * z) << le);
+        if (nm <= 4) {
+          unsigned long long mk = 0;
           for (int g = 0; g < ng; ++g) {
             const DGroup gr = s_g[g];
             const long long yy = y - gr.oy, zz = z - gr.oz;
-            if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
-            const long long r = (yy - P.lo[1]) / P.BF[1] + P.G[1] * ((zz - P.lo[2]) / P.BF[2]);
-            const long long rs = r * P.G[0];
-            const long long num2 = rs + P.G[0] - 1 - S0;
-            if (num2 < 0) continue;
-            long long m1 = num2 / nsm;
-            if (m1 > kj - 1) m1 = kj - 1;
-            const long long num = rs - S0;
-            const long long m0 = num <= 0 ? 0 : (num + nsm - 1) / nsm;
-            for (long long m = m0; m <= m1; ++m) {
-              const long long bxi = S0 + m * nsm - rs;
-              const long long x0 = P.lo[0] + bxi * P.BF[0];
-              long long x1 = x0 + P.BF[0];
-              if (x1 > P.hi[0]) x1 = P.hi[0];
-              cb(x0 + F.run_lo[gr.run], x1 + F.run_hi[gr.run]);
+            for (int m = 0; m < nm; ++m) {
+              const SmBox& bx = s_mb[m];
+              if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1) mk |= 1ull << (m * 16 + gr.run);
             }
           }
-        };
-        row_union(gen, R0, F.lg_elem, lg_sec, lg_line, &t[0], &t[1]);
+          auto gen = [&](auto&& cb) {
+            unsigned long long q = mk;
+            while (q) {
+              const int b = __ffsll((long long)q) - 1;
+              q &= q - 1;
+              const SmBox& bx = s_mb[b >> 4];
+              cb(bx.x0 + F.run_lo[b & 15], bx.x1 + F.run_hi[b & 15]);
+            }
+          };
+          row_union(gen, R0, le, lg_sec, lg_line, &t[0], &t[1]);
+        } else {
+          auto gen = [&](auto&& cb) {
+            for (int g = 0; g < ng; ++g) {
+              const DGroup gr = s_g[g];
+              const long long yy = y - gr.oy, zz = z - gr.oz;
+              for (int m = 0; m < nm; ++m) {
+                const SmBox& bx = s_mb[m];
+                if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
+                  cb(bx.x0 + F.run_lo[gr.run], bx.x1 + F.run_hi[gr.run]);
+              }
+            }
+          };
+          row_union(gen, R0, le, lg_sec, lg_line, &t[0], &t[1]);
+        }
       }
       cta_ordered_reduce<2>(t, s_red);
       if (tid == 0) {
@@ -721,26 +808,23 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
   }
 }
 
-__device__ __forceinline__ bool block_interior(const DPlan& P, long long B) {
-  const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-    if ((bc[d] + 1) * P.BF[d] > P.hi[d] - P.lo[d]) return false;
-  return true;
-}
-
-// Pass 1: single-block SM sets of fully interior blocks go to their translation class
-// (residue of the block's first cell address mod line_bytes); the rest are evaluated here.
+// Pass 1: single-block SM sets go to their translation class: clip pattern of the block x
+// residue of its first cell's address mod line_bytes (identical active-cell boxes that are
+// translates by a multiple of the line size have identical sector and line counts).
+// Multi-block sets are evaluated here.
 __global__ void __launch_bounds__(kRowThreads) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
                                                        int n, const DKernel* __restrict__ ks,
                                                        const DGpu* __restrict__ gs,
                                                        unsigned long long* __restrict__ acc,
                                                        unsigned int* __restrict__ scnt,
                                                        unsigned long long* __restrict__ srep,
+                                                       unsigned long long* __restrict__ lists,
+                                                       unsigned long long* __restrict__ slist,
                                                        unsigned long long* __restrict__ work) {
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
+  __shared__ SmBox s_mb[kMaxMembers];
   __shared__ Tri s_red[(kRowThreads / 32) * 2];
   const long long total = pre[n].set;
   const int tid = threadIdx.x;
@@ -752,60 +836,65 @@ __global__ void __launch_bounds__(kRowThreads) k_smset(const DPlan* __restrict__
     const long long nsm = G.g.n_sm;
     const long long S0 = P.s + j;
     const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-    if (P.scls_R > 0 && kj == 1 && block_interior(P, S0)) {
+    if (P.scls_R > 0 && kj == 1) {
       if (tid == 0) {
         const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
         long long pl = 0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-        const long long slot = (long long)c * kSSlots + (pl & (P.scls_R - 1));
-        atomicAdd(scnt + slot, 1u);
-        atomicExch(srep + slot, (unsigned long long)S0);
+        const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+        const long long gslot = (long long)c * kSSlots + slot;
+        if (atomicAdd(scnt + gslot, 1u) == 0u) {
+          srep[gslot] = (unsigned long long)S0;
+          const unsigned long long idx = atomicAdd(lists + 1, 1ull);
+          slist[idx] = ((unsigned long long)c << 32) | slot;
+        }
       }
       continue;
     }
     unsigned long long ss, sl, un;
-    smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_red, ss, sl, un);
+    smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
     if (tid == 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_SM_SEC, ss);
       atomicAdd(a + A_SM_LIN, sl);
       atomicAdd(work + K_SMSET, un);
     }
-    __syncthreads();
   }
 }
 
-// Pass 2: one representative block per non-empty SM-set class, counted class-size times.
-__global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict__ plans,
-                                                        const DPrefix* __restrict__ pre, int n,
-                                                        const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+// Pass 2: one representative block per SM-set class, counted class-size times.
+__global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                                        const DGpu* __restrict__ gs,
                                                         unsigned long long* __restrict__ acc,
                                                         const unsigned int* __restrict__ scnt,
                                                         const unsigned long long* __restrict__ srep,
+                                                        const unsigned long long* __restrict__ lists,
+                                                        const unsigned long long* __restrict__ slist,
                                                         unsigned long long* __restrict__ work) {
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
+  __shared__ SmBox s_mb[kMaxMembers];
   __shared__ Tri s_red[(kRowThreads / 32) * 2];
-  const long long total = pre[n].sclass;
+  const long long total = (long long)lists[1];
   const int tid = threadIdx.x;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const int c = find_config<3>(pre, n, item);
+    const unsigned long long ent = slist[item];
+    const int c = (int)(ent >> 32);
+    const unsigned slot = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
-    const long long slot = (long long)c * kSSlots + (item - pre[c].sclass);
-    const unsigned int cnt = scnt[slot];
-    if (cnt == 0u) continue;
+    const long long gslot = (long long)c * kSSlots + slot;
+    const unsigned int cnt = scnt[gslot];
     const DGpu& G = gs[P.gid];
     unsigned long long ss, sl, un;
-    smset_eval(P, ks[P.kid], G, (long long)srep[slot], 1, G.g.n_sm, s_g, &s_ng, s_box, s_red, ss, sl, un);
+    smset_eval(P, ks[P.kid], G, (long long)srep[gslot], 1, G.g.n_sm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
     if (tid == 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_SM_SEC, ss * cnt);
       atomicAdd(a + A_SM_LIN, sl * cnt);
       atomicAdd(work + K_SCLASS, un);
     }
-    __syncthreads();
   }
 }
 
@@ -887,6 +976,9 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ 
     const int lg_sec = G.lg_sector, lg_line = G.lg_line;
     const long long ny = RI.ny, rows = RI.ny * RI.nz;
     const long long chunk_in_field = ci - RI.chunk_begin;
+    const long long lo1 = P.lo[1], hi1 = P.hi[1], lo2 = P.lo[2], hi2 = P.hi[2], Gy = P.G[1];
+    const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
+    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
@@ -894,13 +986,13 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ 
       const long long i = chunk_in_field * kRowsPerChunk + (long long)tid * kRowsPerThread + u;
       if (i >= rows) break;
       const long long z = RI.z0 + i / ny, y = RI.y0 + i % ny;
-      const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << F.lg_elem);
+      const long long R0 = align + ((py * y + pz * z) << F.lg_elem);
       unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
       for (int g = 0; g < ng; ++g) {
         const DGroup gr = s_g[g];
         const long long yy = y - gr.oy, zz = z - gr.oz;
-        if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
-        const long long r = (yy - P.lo[1]) / P.BF[1] + P.G[1] * ((zz - P.lo[2]) / P.BF[2]);
+        if (yy < lo1 || yy >= hi1 || zz < lo2 || zz >= hi2) continue;
+        const long long r = fdiv(yy - lo1, fdy) + Gy * fdiv(zz - lo2, fdz);
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
           const int ty = classify(s_r[q], r);
@@ -1116,23 +1208,27 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     ++mk;
   };
   const int persist = n_sm_dev * 8;
+  cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), st);
+  cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), st);
   mark();
   k_plan<<<n, 128, 0, st>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt);
   ++L;
   mark();
-  k_scan<<<1, 1024, 0, st>>>(s.plans, n, s.prefix, s.work);
+  k_scan<<<1, 1024, 0, st>>>(s.plans, n, s.prefix, s.work, s.lists);
   ++L;
   mark();
-  k_warp<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.work);
+  k_warp<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
+                                   s.work);
   ++L;
   mark();
-  k_wclass<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.work);
+  k_wclass<<<persist, 256, 0, st>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
   ++L;
   mark();
-  k_smset<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.scnt, s.srep, s.work);
+  k_smset<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist,
+                                            s.work);
   ++L;
   mark();
-  k_sclass<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.scnt, s.srep, s.work);
+  k_sclass<<<persist, kRowThreads, 0, st>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.work);
   ++L;
   mark();
   k_rows<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
