@@ -114,10 +114,23 @@ __device__ void cta_ordered_reduce(Tri (&t)[NQ], Tri* sm) {
 // increasing order to *ts / *tl.  Repeated extension: no sorting, no storage.
 template <class Gen>
 __device__ __forceinline__ void row_union(const Gen& gen, long long R0, int lg_elem, int lg_sec, int lg_line, Tri* ts,
-                                          Tri* tl) {
+                                          Tri* tl, Tri* ts2 = nullptr) {
   const long long INF = LLONG_MAX;
-  long long start = INF;
-  gen([&](long long xs, long long xe) { start = xs < start ? xs : start; });
+  long long start = INF, mx_s = LLONG_MIN, mn_e = INF, mx_e = LLONG_MIN;
+  gen([&](long long xs, long long xe) {
+    start = xs < start ? xs : start;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  if (start == INF) return;
+  if (mx_s <= mn_e) {  // every interval reaches the point mx_s: one component [start, mx_e)
+    const long long a0 = R0 + (start << lg_elem), a1 = R0 + ((mx_e - 1) << lg_elem);
+    if (ts) tri_add(*ts, a0 >> lg_sec, a1 >> lg_sec);
+    if (ts2) tri_add(*ts2, a0 >> lg_sec, a1 >> lg_sec);
+    if (tl) tri_add(*tl, a0 >> lg_line, a1 >> lg_line);
+    return;
+  }
   while (start != INF) {
     long long end = start, nxt;
     bool grew;
@@ -137,6 +150,7 @@ __device__ __forceinline__ void row_union(const Gen& gen, long long R0, int lg_e
     } while (grew);
     const long long a0 = R0 + (start << lg_elem), a1 = R0 + ((end - 1) << lg_elem);
     if (ts) tri_add(*ts, a0 >> lg_sec, a1 >> lg_sec);
+    if (ts2) tri_add(*ts2, a0 >> lg_sec, a1 >> lg_sec);
     if (tl) tri_add(*tl, a0 >> lg_line, a1 >> lg_line);
     start = nxt;
   }
@@ -621,14 +635,22 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
   const int lane = threadIdx.x & 31;
   unsigned long long my_units = 0;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
-    const int c = find_config<0>(pre, n, item);
-    const DPlan& P = plans[c];
-    const long long wi = item - pre[c].warp;
-    const long long B = P.s + wi / P.nwarps;
-    const int w = (int)(wi % P.nwarps);
-    if (P.wcls_R > 0) {
-      if (lane == 0) {
+  // each lane classifies one wave warp; warps of configs without classes are then
+  // evaluated cooperatively by the whole warp
+  for (long long base = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < total; base += nw * 32) {
+    const long long item = base + lane;
+    const bool have = item < total;
+    int c = 0;
+    bool direct = false;
+    unsigned long long key = ~0ull;
+    long long B = 0;
+    if (have) {
+      c = find_config<0>(pre, n, item);
+      const DPlan& P = plans[c];
+      const long long wi = item - pre[c].warp;
+      B = P.s + wi / P.nwarps;
+      const int w = (int)(wi % P.nwarps);
+      if (P.wcls_R > 0) {
         const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
         const int t0 = w * 32;
         const long long tc[3] = {t0 % P.b[0], (t0 / P.b[0]) % P.b[1], t0 / (P.b[0] * P.b[1])};
@@ -637,22 +659,44 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
         for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d]);
         const int res = (int)(pl & (P.wcls_R - 1));  // (pl * elem) mod M, in elements
         const unsigned slot = (unsigned)(((w * 64 + res) << 3) | clip_pattern(P, bc));
-        const long long gslot = (long long)c * kWSlots + slot;
-        if (atomicAdd(wcnt + gslot, 1u) == 0u) {
-          wrep[gslot] = (unsigned long long)B;
-          const unsigned long long idx = atomicAdd(lists + 0, 1ull);
-          wlist[idx] = ((unsigned long long)c << 32) | slot;
-        }
+        key = ((unsigned long long)c << 32) | slot;
+        my_units += 32;
+      } else {
+        direct = true;
       }
-      my_units += 32;
-      continue;
     }
-    const Lane L = lane_setup(P, B, w, lane);
-    long long lup, wf, rl, rs;
-    eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
-    if (lane == 0) add_warp_stats(acc + (long long)c * A_N, 1, lup, wf, rl, rs);
-    my_units += 32ull * (unsigned long long)P.n_instr;
+    // one atomic per distinct class among the lanes
+    const unsigned peers = __match_any_sync(FULL, key);
+    if (key != ~0ull && (peers & ((1u << lane) - 1u)) == 0u) {
+      const int cc = (int)(key >> 32);
+      const unsigned slot = (unsigned)(key & 0xffffffffu);
+      const long long gslot = (long long)cc * kWSlots + slot;
+      if (atomicAdd(wcnt + gslot, (unsigned)__popc(peers)) == 0u) {
+        wrep[gslot] = (unsigned long long)B;
+        const unsigned long long idx = atomicAdd(lists + 0, 1ull);
+        wlist[idx] = key;
+      }
+    }
+    unsigned dm = __ballot_sync(FULL, direct);
+    while (dm) {
+      const int src = __ffs(dm) - 1;
+      dm &= dm - 1;
+      const long long it = shfl64(item, src);
+      const int cc = __shfl_sync(FULL, c, src);
+      const DPlan& P = plans[cc];
+      const long long wi = it - pre[cc].warp;
+      const Lane L = lane_setup(P, P.s + wi / P.nwarps, (int)(wi % P.nwarps), lane);
+      long long lup, wf, rl, rs;
+      eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)cc * kMaxInstr, L, lane, lup, wf, rl, rs);
+      if (lane == 0) {
+        add_warp_stats(acc + (long long)cc * A_N, 1, lup, wf, rl, rs);
+        my_units += 32ull * (unsigned long long)P.n_instr;
+      }
+    }
   }
+  // per-warp total of the units counted by the lanes
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) my_units += __shfl_down_sync(FULL, my_units, o);
   if (lane == 0 && my_units) atomicAdd(work + K_WARP, my_units);
 }
 
@@ -1023,13 +1067,27 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ 
         };
       };
       const int le = F.lg_elem;
-      row_union(make_gen(0, mL[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[0], nullptr);              // WLD
-      row_union(make_gen(0, mS[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[1], nullptr);              // WST
-      row_union(make_gen(0, mL[0] | mS[0], 0, 0ull), R0, le, lg_sec, lg_line, nullptr, &t[2]);      // WLIN
-      row_union(make_gen(1, mL[1] | mS[1], 1, 0ull), R0, le, lg_sec, lg_line, &t[3], &t[4]);        // F_Ly
-      row_union(make_gen(2, mL[2] | mS[2], 2, 0ull), R0, le, lg_sec, lg_line, &t[5], &t[6]);        // F_Lz
-      row_union(make_gen(3, mL[3], 1, mS[1]), R0, le, lg_sec, lg_line, &t[7], nullptr);             // WLD u F_Ly
-      row_union(make_gen(4, mL[4], 2, mS[2]), R0, le, lg_sec, lg_line, &t[8], nullptr);             // WLD u F_Lz
+      // WLD (+ WLIN when the field has no stores in the wave), WST (+ WLIN when no loads)
+      if (mS[0] == 0ull) {
+        row_union(make_gen(0, mL[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[0], &t[2]);
+      } else if (mL[0] == 0ull) {
+        row_union(make_gen(0, mS[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[1], &t[2]);
+      } else {
+        row_union(make_gen(0, mL[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[0], nullptr);
+        row_union(make_gen(0, mS[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[1], nullptr);
+        row_union(make_gen(0, mL[0] | mS[0], 0, 0ull), R0, le, lg_sec, lg_line, nullptr, &t[2]);
+      }
+      // F_Ly, F_Lz (sectors + lines) and WLD u F_Ly, WLD u F_Lz: the unions equal F_L
+      // in rows where the wave loads nothing from this field
+      if (mL[0] != 0ull) {
+        row_union(make_gen(1, mL[1] | mS[1], 1, 0ull), R0, le, lg_sec, lg_line, &t[3], &t[4]);
+        row_union(make_gen(2, mL[2] | mS[2], 2, 0ull), R0, le, lg_sec, lg_line, &t[5], &t[6]);
+        row_union(make_gen(3, mL[3], 1, mS[1]), R0, le, lg_sec, lg_line, &t[7], nullptr);
+        row_union(make_gen(4, mL[4], 2, mS[2]), R0, le, lg_sec, lg_line, &t[8], nullptr);
+      } else {
+        row_union(make_gen(1, mL[1] | mS[1], 1, 0ull), R0, le, lg_sec, lg_line, &t[3], &t[4], &t[7]);
+        row_union(make_gen(2, mL[2] | mS[2], 2, 0ull), R0, le, lg_sec, lg_line, &t[5], &t[6], &t[8]);
+      }
     }
     cta_ordered_reduce<kNQ>(t, s_red);
     if (tid == 0) {
