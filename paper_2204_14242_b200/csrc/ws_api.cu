@@ -127,6 +127,9 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   const size_t o_lists = off;   off = align_up(off + 4 * sizeof(unsigned long long));
   const size_t o_wlist = off;   off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
   const size_t o_slist = off;   off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
+  size_t max_nsm = 1;
+  for (const DGpu& g : c->hg) max_nsm = std::max<size_t>(max_nsm, g.g.n_sm);
+  const size_t o_dlist = off;   off = align_up(off + n * max_nsm * sizeof(unsigned long long));
   if (off > c->scratch_cap) {
     if (c->scratch) cudaFree(c->scratch);
     c->scratch = nullptr;
@@ -151,6 +154,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   s.lists = (unsigned long long*)(b + o_lists);
   s.wlist = (unsigned long long*)(b + o_wlist);
   s.slist = (unsigned long long*)(b + o_slist);
+  s.dlist = (unsigned long long*)(b + o_dlist);
   c->last_work = s.work;
   return WS_OK;
 }
@@ -351,7 +355,7 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
       G.run_lo[q] = runs[q].first;
       G.run_hi[q] = runs[q].second;
     }
-    if (G.g_end > G.g_begin) chunks += (G.ext[1] * G.ext[2] + kRowsPerChunk - 1) / kRowsPerChunk;
+    if (G.g_end > G.g_begin) chunks += G.ext[2];  // k_rows chunks are >= 1 z-plane each
   }
   D.n_groups = ng;
   c->hk.push_back(D);

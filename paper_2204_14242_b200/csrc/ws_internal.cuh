@@ -58,9 +58,11 @@ struct DInstr {
 };
 
 // Row box (field-index rows (y,z), z-major) of the wave + layer-set footprint of one field.
+// A chunk is `ppc` consecutive z-planes of the box (k_rows: one warp per chunk).
 struct DRowInfo {
-  int64_t y0, ny, z0, nz, chunk_begin, n_chunks;
+  int64_t y0, ny, z0, nz, chunk_begin, n_chunks, ppc, pad;
 };
+constexpr int kPlaneRows = 8192;   // target rows per k_rows chunk
 
 // n / d for 0 <= n < 2^31 by multiply-high (Granlund-Montgomery round-up method):
 // q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
@@ -111,9 +113,10 @@ struct Scratch {
   unsigned int* scnt;         // n * kSSlots
   unsigned long long* srep;   // n * kSSlots
   unsigned long long* work;   // K_NKINDS algorithmic work units of the last call (ws_work_read)
-  unsigned long long* lists;  // [0] = # warp classes, [1] = # SM-set classes (zeroed by k_scan)
+  unsigned long long* lists;  // [0] # warp classes, [1] # SM-set classes, [2] # direct SM sets (zeroed by k_scan)
   unsigned long long* wlist;  // n * kWSlots entries (config << 32 | slot)
   unsigned long long* slist;  // n * kSSlots entries
+  unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm entries
 };
 
 // kernel kinds, in launch order (ws_kernel_name)

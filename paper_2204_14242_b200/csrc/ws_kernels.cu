@@ -255,8 +255,11 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   for (int i = 1; i < K.n_fields; ++i)
     for (int d = 0; d < 3; ++d)
       if (K.f[i].pitch[d] != K.f[0].pitch[d] || K.f[i].lg_elem != K.f[0].lg_elem) same = false;
-  const long long M = (long long)G.g.sector_bytes > (long long)G.g.bank_bytes * G.g.n_banks
-                          ? (long long)G.g.sector_bytes : (long long)G.g.bank_bytes * G.g.n_banks;
+  // sector counts are invariant under translation by multiples of sector_bytes; bank words
+  // shift uniformly under multiples of bank_bytes, which only relabels the banks cyclically
+  // (the max multiplicity and the cluster split are unchanged): M = lcm = max (powers of two)
+  const long long M = (long long)G.g.sector_bytes > (long long)G.g.bank_bytes ? (long long)G.g.sector_bytes
+                                                                              : (long long)G.g.bank_bytes;
   const long long Rw = M >> K.f[0].lg_elem, Rs = (long long)G.g.line_bytes >> K.f[0].lg_elem;
   P.wcls_R = (same && Rw >= 1 && Rw <= 64 && P.nwarps <= 32) ? (int)Rw : 0;
   P.scls_R = (same && Rs >= 1 && Rs <= 64) ? (int)Rs : 0;
@@ -402,8 +405,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     ri.z0 = z0;
     ri.nz = z1 > z0 ? z1 - z0 : 0;
     if (F.g_end == F.g_begin) ri.ny = ri.nz = 0;
-    const long long rows = ri.ny * ri.nz;
-    ri.n_chunks = (rows + kRowsPerChunk - 1) / kRowsPerChunk;
+    ri.ppc = 1;
+    ri.n_chunks = ri.ny > 0 ? ri.nz : 0;
+    ri.pad = 0;
     ri.chunk_begin = 0;
     rowinfo[(long long)c * kMaxFields + fi] = ri;
   }
@@ -489,6 +493,8 @@ struct Lane {
   bool valid;              // thread index < T
 };
 
+__device__ __forceinline__ unsigned bm_all(bool p) { return __ballot_sync(FULL, p); }
+
 __device__ __forceinline__ unsigned long long full_cube(int fc) { return fc == 64 ? ~0ull : ((1ull << fc) - 1ull); }
 
 __device__ __forceinline__ Lane lane_setup(const DPlan& P, long long B, int w, int lane) {
@@ -570,6 +576,11 @@ __device__ void eval_warp(const DPlan& P, const DKernel& K, const DGpu& G, const
     const long long sword = shfl64(word, sl);
     const bool longseg = uw && (word - sword) * bank_bytes >= window;
     if (!__any_sync(FULL, longseg)) {
+      // a cluster spanning fewer than n_banks words has every bank at most once
+      if (!__any_sync(FULL, uw && (word - sword) > (long long)nbm)) {
+        wf_u += __popc(bm_all(bnd));
+        continue;
+      }
       const int bank = (int)(word & nbm);
       const unsigned peers = __match_any_sync(FULL, uw ? (unsigned)(bank | (sl << 8)) : (0x10000u | (unsigned)lane));
       const int rank = __popc(peers & le_mask);
@@ -852,62 +863,44 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
   }
 }
 
-// Pass 1: single-block SM sets go to their translation class: clip pattern of the block x
-// residue of its first cell's address mod line_bytes (identical active-cell boxes that are
-// translates by a multiple of the line size have identical sector and line counts).
-// Multi-block sets are evaluated here.
-__global__ void __launch_bounds__(kRowThreads) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
-                                                       int n, const DKernel* __restrict__ ks,
-                                                       const DGpu* __restrict__ gs,
-                                                       unsigned long long* __restrict__ acc,
-                                                       unsigned int* __restrict__ scnt,
-                                                       unsigned long long* __restrict__ srep,
-                                                       unsigned long long* __restrict__ lists,
-                                                       unsigned long long* __restrict__ slist,
-                                                       unsigned long long* __restrict__ work) {
-  __shared__ DGroup s_g[kMaxAcc];
-  __shared__ int s_ng;
-  __shared__ long long s_box[4];
-  __shared__ SmBox s_mb[kMaxMembers];
-  __shared__ Tri s_red[(kRowThreads / 32) * 2];
+// Pass 1 (one thread per SM set): single-block sets go to their translation class: clip
+// pattern of the block x residue of its first cell's address mod line_bytes (identical
+// active-cell boxes that are translates by a multiple of the line size have identical
+// sector and line counts).  Multi-block sets are appended to the direct list.
+__global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                               const DGpu* __restrict__ gs, unsigned int* __restrict__ scnt,
+                                               unsigned long long* __restrict__ srep,
+                                               unsigned long long* __restrict__ lists,
+                                               unsigned long long* __restrict__ slist,
+                                               unsigned long long* __restrict__ dlist) {
   const long long total = pre[n].set;
-  const int tid = threadIdx.x;
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+  for (long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x; item < total;
+       item += (long long)gridDim.x * blockDim.x) {
     const int c = find_config<2>(pre, n, item);
     const DPlan& P = plans[c];
-    const DGpu& G = gs[P.gid];
     const long long j = item - pre[c].set;
-    const long long nsm = G.g.n_sm;
+    const long long nsm = gs[P.gid].g.n_sm;
     const long long S0 = P.s + j;
     const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
     if (P.scls_R > 0 && kj == 1) {
-      if (tid == 0) {
-        const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
-        long long pl = 0;
+      const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
+      long long pl = 0;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-        const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
-        const long long gslot = (long long)c * kSSlots + slot;
-        if (atomicAdd(scnt + gslot, 1u) == 0u) {
-          srep[gslot] = (unsigned long long)S0;
-          const unsigned long long idx = atomicAdd(lists + 1, 1ull);
-          slist[idx] = ((unsigned long long)c << 32) | slot;
-        }
+      for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+      const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+      const long long gslot = (long long)c * kSSlots + slot;
+      if (atomicAdd(scnt + gslot, 1u) == 0u) {
+        srep[gslot] = (unsigned long long)S0;
+        slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
       }
-      continue;
-    }
-    unsigned long long ss, sl, un;
-    smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
-    if (tid == 0) {
-      unsigned long long* a = acc + (long long)c * A_N;
-      atomicAdd(a + A_SM_SEC, ss);
-      atomicAdd(a + A_SM_LIN, sl);
-      atomicAdd(work + K_SMSET, un);
+    } else {
+      dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
     }
   }
 }
 
-// Pass 2: one representative block per SM-set class, counted class-size times.
+// Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
+// directly evaluated multi-block SM sets.
 __global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
                                                         const DGpu* __restrict__ gs,
                                                         unsigned long long* __restrict__ acc,
@@ -915,29 +908,42 @@ __global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict_
                                                         const unsigned long long* __restrict__ srep,
                                                         const unsigned long long* __restrict__ lists,
                                                         const unsigned long long* __restrict__ slist,
+                                                        const unsigned long long* __restrict__ dlist,
                                                         unsigned long long* __restrict__ work) {
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ Tri s_red[(kRowThreads / 32) * 2];
-  const long long total = (long long)lists[1];
+  const long long ncls = (long long)lists[1];
+  const long long total = ncls + (long long)lists[2];
   const int tid = threadIdx.x;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const unsigned long long ent = slist[item];
+    const bool cls = item < ncls;
+    const unsigned long long ent = cls ? slist[item] : dlist[item - ncls];
     const int c = (int)(ent >> 32);
-    const unsigned slot = (unsigned)(ent & 0xffffffffu);
+    const unsigned low = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
-    const long long gslot = (long long)c * kSSlots + slot;
-    const unsigned int cnt = scnt[gslot];
     const DGpu& G = gs[P.gid];
+    const long long nsm = G.g.n_sm;
+    unsigned long long mult = 1;
+    long long S0, kj;
+    if (cls) {
+      const long long gslot = (long long)c * kSSlots + low;
+      mult = scnt[gslot];
+      S0 = (long long)srep[gslot];
+      kj = 1;
+    } else {
+      S0 = P.s + low;
+      kj = (P.W - (long long)low + nsm - 1) / nsm;
+    }
     unsigned long long ss, sl, un;
-    smset_eval(P, ks[P.kid], G, (long long)srep[gslot], 1, G.g.n_sm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
+    smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
     if (tid == 0) {
       unsigned long long* a = acc + (long long)c * A_N;
-      atomicAdd(a + A_SM_SEC, ss * cnt);
-      atomicAdd(a + A_SM_LIN, sl * cnt);
-      atomicAdd(work + K_SCLASS, un);
+      atomicAdd(a + A_SM_SEC, ss * mult);
+      atomicAdd(a + A_SM_LIN, sl * mult);
+      atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     }
   }
 }
@@ -958,17 +964,116 @@ __device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
   return 0;
 }
 
-__global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre,
-                                                      int n, const DKernel* __restrict__ ks,
-                                                      const DGpu* __restrict__ gs, const DRowInfo* __restrict__ rowinfo,
-                                                      long long* __restrict__ chunkres,
-                                                      unsigned long long* __restrict__ work) {
-  __shared__ DGroup s_g[kMaxAcc];
-  __shared__ RangeInfo s_r[5];
-  __shared__ Tri s_red[(kRowThreads / 32) * kNQ];
+// Smallest power of two k <= 16 with k * plane_pitch_bytes a multiple of line_bytes (0: none):
+// planes that far apart are translates by whole lines.
+__device__ __forceinline__ int plane_period(long long pz, int le, int ll) {
+  const long long pb = pz << le;
+  const long long tz = pb == 0 ? 63 : __ffsll(pb) - 1;
+  const long long need = ll > tz ? ll - tz : 0;
+  return need <= 4 ? (1 << need) : 0;
+}
+
+// Cached union of one row: a single component [x0, x1) (x0 >= x1: empty) or `multi`.
+struct UC {
+  long long x0, x1;
+  int single;
+};
+
+template <class Gen>
+__device__ __forceinline__ void row_union_c(const Gen& gen, long long R0, int le, int ls, int ll, Tri* ts, Tri* tl,
+                                            Tri* ts2, UC& uc) {
+  const long long INF = LLONG_MAX;
+  long long start = INF, mx_s = LLONG_MIN, mn_e = INF, mx_e = LLONG_MIN;
+  gen([&](long long xs, long long xe) {
+    start = xs < start ? xs : start;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  if (start == INF) {
+    uc = UC{0, 0, 1};
+    return;
+  }
+  if (mx_s <= mn_e) {
+    uc = UC{start, mx_e, 1};
+    const long long a0 = R0 + (start << le), a1 = R0 + ((mx_e - 1) << le);
+    if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
+    if (ts2) tri_add(*ts2, a0 >> ls, a1 >> ls);
+    if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
+    return;
+  }
+  uc.single = 0;
+  row_union(gen, R0, le, ls, ll, ts, tl, ts2);
+}
+
+template <class Gen>
+__device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, long long R0, int le, int ls, int ll,
+                                                 Tri* ts, Tri* tl, Tri* ts2, UC& uc) {
+  if (first) {
+    row_union_c(gen, R0, le, ls, ll, ts, tl, ts2, uc);
+  } else if (uc.single) {
+    if (uc.x0 < uc.x1) {
+      const long long a0 = R0 + (uc.x0 << le), a1 = R0 + ((uc.x1 - 1) << le);
+      if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
+      if (ts2) tri_add(*ts2, a0 >> ls, a1 >> ls);
+      if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
+    }
+  } else {
+    row_union(gen, R0, le, ls, ll, ts, tl, ts2);
+  }
+}
+
+template <int NQ>
+__device__ __forceinline__ void warp_ordered_reduce(Tri (&t)[NQ]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
+      if (lane + o < 32) t[q] = tri_combine(t[q], x);
+    }
+  }
+}
+
+constexpr int kRowWarps = 8;
+constexpr int kRowsPerLane = kRowsPerChunk / 32;
+
+struct WarpRowCtx {
+  RangeInfo r[5];
+  long long bnd[20];  // sorted distinct block rows where some range's classification zone starts
+  int nb, pad;
+};
+
+// One union of a row: candidates (range q1, mask m1) u (range q2, mask m2); targets are
+// indices into the chunk triples (-1 = none).
+struct USpec {
+  unsigned long long m1, m2;
+  int q1, q2, ts, tl, ts2, pad;
+};
+
+// One warp per chunk of 1024 address rows of one (config, field).  The chunk is cut into
+// runs of consecutive rows whose candidate masks are identical: a row's masks change only
+// where some offset group's region row enters another classification zone (the 5 ranges'
+// first / second / last / after-last block rows) or leaves / enters the domain, or at a
+// z-plane end.  Per run the masks are computed once (lanes split the offset groups), the
+// unions once (every lane), then the lanes take the run's rows 32 at a time: row y
+// contributes count(y) - [last(y) == first(y+1)], which it can evaluate alone because row
+// y+1 of the run has the same union shifted by one row pitch.  The run's count is a plain
+// warp sum; its first / last sector come from its first / last row; runs are folded in order.
+__global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict__ plans,
+                                                         const DPrefix* __restrict__ pre, int n,
+                                                         const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                                         const DRowInfo* __restrict__ rowinfo,
+                                                         long long* __restrict__ chunkres,
+                                                         unsigned long long* __restrict__ work) {
+  __shared__ WarpRowCtx s_ctx[kRowWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpRowCtx& X = s_ctx[wid];
   const long long total = pre[n].chunk;
-  const int tid = threadIdx.x;
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+  const long long nwg = (long long)gridDim.x * kRowWarps;
+  unsigned long long my_rows = 0;
+  for (long long item = (long long)blockIdx.x * kRowWarps + wid; item < total; item += nwg) {
     const int c = find_config<4>(pre, n, item);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
@@ -984,15 +1089,14 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ 
     }
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const DField& F = K.f[fi];
-    const int ng = F.g_end - F.g_begin;
-    __syncthreads();
-    for (int g = tid; g < ng; g += blockDim.x) s_g[g] = K.g[F.g_begin + g];
-    if (tid < 5) {
+    const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
+    __syncwarp();
+    if (lane < 5) {
       long long a, b;
-      if (tid == 0) { a = P.s; b = P.s + P.W; }
-      else if (tid == 1) { a = P.Ly0; b = P.s; }
-      else if (tid == 2) { a = P.Lz0; b = P.s; }
-      else if (tid == 3) { a = P.Ly0; b = P.s + P.W; }
+      if (lane == 0) { a = P.s; b = P.s + P.W; }
+      else if (lane == 1) { a = P.Ly0; b = P.s; }
+      else if (lane == 2) { a = P.Lz0; b = P.s; }
+      else if (lane == 3) { a = P.Ly0; b = P.s + P.W; }
       else { a = P.Lz0; b = P.s + P.W; }
       RangeInfo R;
       R.nonempty = a < b;
@@ -1014,99 +1118,223 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(const DPlan* __restrict__ 
       R.iv[1][0] = xs_a; R.iv[1][1] = hx;
       R.iv[2][0] = lx;   R.iv[2][1] = xe_l;
       R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
-      s_r[tid] = R;
+      X.r[lane] = R;
     }
-    __syncthreads();
-    const int lg_sec = G.lg_sector, lg_line = G.lg_line;
-    const long long ny = RI.ny, rows = RI.ny * RI.nz;
-    const long long chunk_in_field = ci - RI.chunk_begin;
-    const long long lo1 = P.lo[1], hi1 = P.hi[1], lo2 = P.lo[2], hi2 = P.hi[2], Gy = P.G[1];
-    const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
-    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
-    Tri t[kNQ];
-#pragma unroll
-    for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
-    for (int u = 0; u < kRowsPerThread; ++u) {
-      const long long i = chunk_in_field * kRowsPerChunk + (long long)tid * kRowsPerThread + u;
-      if (i >= rows) break;
-      const long long z = RI.z0 + i / ny, y = RI.y0 + i % ny;
-      const long long R0 = align + ((py * y + pz * z) << F.lg_elem);
-      unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
-      for (int g = 0; g < ng; ++g) {
-        const DGroup gr = s_g[g];
-        const long long yy = y - gr.oy, zz = z - gr.oz;
-        if (yy < lo1 || yy >= hi1 || zz < lo2 || zz >= hi2) continue;
-        const long long r = fdiv(yy - lo1, fdy) + Gy * fdiv(zz - lo2, fdz);
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-          const int ty = classify(s_r[q], r);
-          if (ty >= 0) {
-            const unsigned long long bit = 1ull << (ty * 16 + gr.run);
-            if (gr.kind) mS[q] |= bit;
-            else mL[q] |= bit;
-          }
+    __syncwarp();
+    if (lane == 0) {
+      int nb = 0;
+      for (int q = 0; q < 5; ++q) {
+        if (!X.r[q].nonempty) continue;
+        const long long cand[4] = {X.r[q].ra, X.r[q].ra + 1, X.r[q].rl, X.r[q].rl + 1};
+        for (int k = 0; k < 4; ++k) {
+          const long long v = cand[k];
+          int pos = 0;
+          while (pos < nb && X.bnd[pos] < v) ++pos;
+          if (pos < nb && X.bnd[pos] == v) continue;
+          for (int m = nb; m > pos; --m) X.bnd[m] = X.bnd[m - 1];
+          X.bnd[pos] = v;
+          ++nb;
         }
       }
-      // a generator over (range, candidate-mask) pairs
-      auto make_gen = [&](int q1, unsigned long long m1, int q2, unsigned long long m2) {
-        return [&, q1, m1, q2, m2](auto&& cb) {
-          unsigned long long m = m1;
-          while (m) {
-            const int b = __ffsll((long long)m) - 1;
-            m &= m - 1;
-            const int ty = b >> 4, run = b & 15;
-            cb(s_r[q1].iv[ty][0] + F.run_lo[run], s_r[q1].iv[ty][1] + F.run_hi[run]);
-          }
-          m = m2;
-          while (m) {
-            const int b = __ffsll((long long)m) - 1;
-            m &= m - 1;
-            const int ty = b >> 4, run = b & 15;
-            cb(s_r[q2].iv[ty][0] + F.run_lo[run], s_r[q2].iv[ty][1] + F.run_hi[run]);
-          }
-        };
-      };
-      const int le = F.lg_elem;
-      // WLD (+ WLIN when the field has no stores in the wave), WST (+ WLIN when no loads)
-      if (mS[0] == 0ull) {
-        row_union(make_gen(0, mL[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[0], &t[2]);
-      } else if (mL[0] == 0ull) {
-        row_union(make_gen(0, mS[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[1], &t[2]);
-      } else {
-        row_union(make_gen(0, mL[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[0], nullptr);
-        row_union(make_gen(0, mS[0], 0, 0ull), R0, le, lg_sec, lg_line, &t[1], nullptr);
-        row_union(make_gen(0, mL[0] | mS[0], 0, 0ull), R0, le, lg_sec, lg_line, nullptr, &t[2]);
-      }
-      // F_Ly, F_Lz (sectors + lines) and WLD u F_Ly, WLD u F_Lz: the unions equal F_L
-      // in rows where the wave loads nothing from this field
-      if (mL[0] != 0ull) {
-        row_union(make_gen(1, mL[1] | mS[1], 1, 0ull), R0, le, lg_sec, lg_line, &t[3], &t[4]);
-        row_union(make_gen(2, mL[2] | mS[2], 2, 0ull), R0, le, lg_sec, lg_line, &t[5], &t[6]);
-        row_union(make_gen(3, mL[3], 1, mS[1]), R0, le, lg_sec, lg_line, &t[7], nullptr);
-        row_union(make_gen(4, mL[4], 2, mS[2]), R0, le, lg_sec, lg_line, &t[8], nullptr);
-      } else {
-        row_union(make_gen(1, mL[1] | mS[1], 1, 0ull), R0, le, lg_sec, lg_line, &t[3], &t[4], &t[7]);
-        row_union(make_gen(2, mL[2] | mS[2], 2, 0ull), R0, le, lg_sec, lg_line, &t[5], &t[6], &t[8]);
-      }
+      X.nb = nb;
     }
-    cta_ordered_reduce<kNQ>(t, s_red);
-    if (tid == 0) {
-      long long nr = rows - chunk_in_field * kRowsPerChunk;
-      if (nr > kRowsPerChunk) nr = kRowsPerChunk;
-      atomicAdd(work + K_ROWS, (unsigned long long)(nr * ng));
-      long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
+    __syncwarp();
+    const int nb = X.nb;
+    const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
+    const long long ny = RI.ny, rows = RI.ny * RI.nz;
+    const long long lo1 = P.lo[1], hi1 = P.hi[1], lo2 = P.lo[2], hi2 = P.hi[2], Gy = P.G[1], BF1 = P.BF[1];
+    const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
+    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
+    const long long pystep = py << le;
+    Tri carry[kNQ];
 #pragma unroll
-      for (int q = 0; q < kNQ; ++q) {
-        out[q * 3 + 0] = t[q].f;
-        out[q * 3 + 1] = t[q].l;
-        out[q * 3 + 2] = t[q].c;
+    for (int q = 0; q < kNQ; ++q) carry[q] = tri_empty();
+    // planes of this chunk
+    const long long zc0 = RI.z0 + (ci - RI.chunk_begin) * RI.ppc;
+    long long zc1 = zc0 + RI.ppc;
+    if (zc1 > RI.z0 + RI.nz) zc1 = RI.z0 + RI.nz;
+    // plane reuse period: smallest power of two k with k*pz*elem a multiple of line_bytes
+    const int per = plane_period(pz, le, ll);
+    for (long long z = zc0; z < zc1; ++z) {
+      // identical row structure to plane z - per when every offset group falls in the same
+      // block layer (or outside the domain) in both planes: k_fold derives it by translation
+      if (per > 0 && z - per >= RI.z0) {
+        bool same = true;
+        for (int g = lane; g < ng; g += 32) {
+          const long long za = z - K.g[g0 + g].oz, zb = za - per;
+          const long long ka = (za < lo2 || za >= hi2) ? -1 : fdiv(za - lo2, fdz);
+          const long long kb = (zb < lo2 || zb >= hi2) ? -1 : fdiv(zb - lo2, fdz);
+          same = same && ka == kb;
+        }
+        if (__all_sync(FULL, same)) {
+          if (lane == 0) {
+            long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
+            out[2] = -1;  // derived plane marker (counts are never negative)
+          }
+          continue;
+        }
+      }
+      Tri pt[kNQ];
+      my_rows += (unsigned long long)(lane == 0 ? ny : 0);
+      {
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q) pt[q] = tri_empty();
+        long long y = RI.y0;
+        const long long yend = RI.y0 + ny;
+        while (y < yend) {  // warp-uniform
+          long long y_stop = yend;
+          // ---- masks of row (y, z) and the run end: lanes split the offset groups
+          unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
+          for (int g = lane; g < ng; g += 32) {
+            const DGroup gr = K.g[g0 + g];
+            const long long zz = z - gr.oz;
+            if (zz < lo2 || zz >= hi2) continue;
+            const long long yy = y - gr.oy;
+            if (yy < lo1) {
+              if (y + (lo1 - yy) < y_stop) y_stop = y + (lo1 - yy);
+              continue;
+            }
+            if (yy >= hi1) continue;
+            const long long C = Gy * fdiv(zz - lo2, fdz);
+            const long long r = fdiv(yy - lo1, fdy) + C;
+    #pragma unroll
+            for (int q = 0; q < 5; ++q) {
+              const int ty = classify(X.r[q], r);
+              if (ty >= 0) {
+                const unsigned long long bit = 1ull << (ty * 16 + gr.run);
+                if (gr.kind) mS[q] |= bit;
+                else mL[q] |= bit;
+              }
+            }
+            long long yn = hi1;
+            for (int k = 0; k < nb; ++k) {
+              const long long bk = X.bnd[k];
+              if (bk > r) {
+                if (bk - C < Gy) {
+                  const long long v = lo1 + (bk - C) * BF1;
+                  yn = v < hi1 ? v : hi1;
+                }
+                break;
+              }
+            }
+            if (yn + gr.oy < y_stop) y_stop = yn + gr.oy;
+          }
+    #pragma unroll
+          for (int q = 0; q < 5; ++q) {
+            mL[q] = ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(mL[q] >> 32)) << 32) |
+                    __reduce_or_sync(FULL, (unsigned)mL[q]);
+            mS[q] = ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(mS[q] >> 32)) << 32) |
+                    __reduce_or_sync(FULL, (unsigned)mS[q]);
+          }
+          y_stop = y + __reduce_min_sync(FULL, (unsigned)(y_stop - y));
+          const long long run = y_stop - y;
+          // ---- the run's unions (uniform)
+          USpec U[7];
+          int nu = 0;
+          const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
+          if (noS) {
+            U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, 2, -1, 0};
+          } else if (noL) {
+            U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, 2, -1, 0};
+          } else {
+            U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, -1, -1, 0};
+            U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, -1, -1, 0};
+            U[nu++] = USpec{mL[0] | mS[0], 0ull, 0, 0, -1, 2, -1, 0};
+          }
+          if (!noL) {
+            U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, -1, 0};
+            U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, -1, 0};
+            U[nu++] = USpec{mL[3], mS[1], 3, 1, 7, -1, -1, 0};
+            U[nu++] = USpec{mL[4], mS[2], 4, 2, 8, -1, -1, 0};
+          } else {
+            U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, 7, 0};
+            U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, 8, 0};
+          }
+          const long long R0f = align + ((py * y + pz * z) << le);
+          const long long R0l = R0f + (run - 1) * pystep;
+          for (int u = 0; u < nu; ++u) {
+            const USpec sp = U[u];
+            auto gen = [&](auto&& cb) {
+              unsigned long long m = sp.m1;
+              while (m) {
+                const int b = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const int ty = b >> 4, rr = b & 15;
+                cb(X.r[sp.q1].iv[ty][0] + F.run_lo[rr], X.r[sp.q1].iv[ty][1] + F.run_hi[rr]);
+              }
+              m = sp.m2;
+              while (m) {
+                const int b = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const int ty = b >> 4, rr = b & 15;
+                cb(X.r[sp.q2].iv[ty][0] + F.run_lo[rr], X.r[sp.q2].iv[ty][1] + F.run_hi[rr]);
+              }
+            };
+            long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
+            gen([&](long long xs, long long xe) {
+              mn_s = xs < mn_s ? xs : mn_s;
+              mx_s = xs > mx_s ? xs : mx_s;
+              mn_e = xe < mn_e ? xe : mn_e;
+              mx_e = xe > mx_e ? xe : mx_e;
+            });
+            if (mn_s == LLONG_MAX) continue;  // empty union in every row of the run
+            const bool single = mx_s <= mn_e;
+            const long long d0 = mn_s << le, d1 = (mx_e - 1) << le;
+            // per-lane rows of the run: count(y) - [last(y) == first(y+1)]
+            long long cs = 0, cl = 0;
+            for (long long r = lane; r < run; r += 32) {
+              const long long R0 = R0f + r * pystep;
+              const long long a0 = R0 + d0, a1 = R0 + d1, an = a0 + pystep;
+              const bool more = r + 1 < run;
+              if (single) {
+                if (sp.ts >= 0) cs += ((a1 >> ls) - (a0 >> ls) + 1) - (more && (a1 >> ls) == (an >> ls) ? 1 : 0);
+                if (sp.tl >= 0) cl += ((a1 >> ll) - (a0 >> ll) + 1) - (more && (a1 >> ll) == (an >> ll) ? 1 : 0);
+              } else {
+                Tri ts = tri_empty(), tl = tri_empty();
+                row_union(gen, R0, le, ls, ll, sp.ts >= 0 ? &ts : nullptr, sp.tl >= 0 ? &tl : nullptr);
+                if (sp.ts >= 0) cs += ts.c - (more && (a1 >> ls) == (an >> ls) ? 1 : 0);
+                if (sp.tl >= 0) cl += tl.c - (more && (a1 >> ll) == (an >> ll) ? 1 : 0);
+              }
+            }
+            // run triples (warp sums; counts of one run fit 32 bits)
+            if (sp.ts >= 0) {
+              const long long sum = (long long)__reduce_add_sync(FULL, (unsigned)cs);
+              const Tri tr{(R0f + d0) >> ls, (R0l + d1) >> ls, sum};
+              pt[sp.ts] = tri_combine(pt[sp.ts], tr);
+              if (sp.ts2 >= 0) pt[sp.ts2] = tri_combine(pt[sp.ts2], tr);
+            }
+            if (sp.tl >= 0) {
+              const long long sum = (long long)__reduce_add_sync(FULL, (unsigned)cl);
+              const Tri tr{(R0f + d0) >> ll, (R0l + d1) >> ll, sum};
+              pt[sp.tl] = tri_combine(pt[sp.tl], tr);
+            }
+          }
+          y += run;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) carry[q] = tri_combine(carry[q], pt[q]);
+      if (lane == 0) {
+        long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q) {
+          out[q * 3 + 0] = carry[q].f;
+          out[q * 3 + 1] = carry[q].l;
+          out[q * 3 + 2] = carry[q].c;
+        }
       }
     }
   }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) my_rows += __shfl_down_sync(FULL, my_rows, o);
+  if (lane == 0 && my_rows) atomicAdd(work + K_ROWS, my_rows);
 }
 
-// ordered fold of the chunk triples of one (config, field); one warp per item
+// Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
+// plane (marker count -1) takes the triple of plane z - k*per (the nearest computed one)
+// translated by k*per plane pitches (whole lines).
 __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                              const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                               const DRowInfo* __restrict__ rowinfo,
                                               const long long* __restrict__ chunkres,
                                               unsigned long long* __restrict__ acc) {
@@ -1116,16 +1344,30 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
     const int c = find_config<5>(pre, n, item);
     const int fi = (int)(item - pre[c].fold);
+    const DPlan& P = plans[c];
+    const DField& F = ks[P.kid].f[fi];
+    const DGpu& G = gs[P.gid];
+    const int ls = G.lg_sector, ll = G.lg_line;
+    const int per = plane_period(F.pitch[2], F.lg_elem, ll);
+    const long long pbytes = F.pitch[2] << F.lg_elem;
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
-    const long long per = (nch + 31) / 32;
+    const long long per_l = (nch + 31) / 32;
+    const long long* base = chunkres + (pre[c].chunk + RI.chunk_begin) * (kNQ * 3);
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
-    for (long long k = lane * per; k < nch && k < (lane + 1) * per; ++k) {
-      const long long* in = chunkres + (pre[c].chunk + RI.chunk_begin + k) * (kNQ * 3);
+    for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
+      long long src = k;
+      while (base[src * (kNQ * 3) + 2] == -1) src -= per;  // per > 0 whenever a marker exists
+      const long long* in = base + src * (kNQ * 3);
+      const long long dbytes = (k - src) * pbytes;
 #pragma unroll
-      for (int q = 0; q < kNQ; ++q) t[q] = tri_combine(t[q], Tri{in[q * 3], in[q * 3 + 1], in[q * 3 + 2]});
+      for (int q = 0; q < kNQ; ++q) {
+        const long long d = dbytes >> ((q == 2 || q == 4 || q == 6) ? ll : ls);
+        const long long cq = in[q * 3 + 2];
+        t[q] = tri_combine(t[q], cq ? Tri{in[q * 3] + d, in[q * 3 + 1] + d, cq} : tri_empty());
+      }
     }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1282,17 +1524,17 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_wclass<<<persist, 256, 0, st>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
   ++L;
   mark();
-  k_smset<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist,
-                                            s.work);
+  k_smset<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
   ++L;
   mark();
-  k_sclass<<<persist, kRowThreads, 0, st>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.work);
+  k_sclass<<<persist, kRowThreads, 0, st>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist,
+                                             s.work);
   ++L;
   mark();
-  k_rows<<<persist, kRowThreads, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
+  k_rows<<<persist, kRowWarps * 32, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
   ++L;
   mark();
-  k_fold<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, s.rowinfo, s.chunkres, s.acc);
+  k_fold<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
   ++L;
   mark();
   k_model<<<(n + 127) / 128, 128, 0, st>>>(s.plans, n, d_k, d_g, s.acc, d_out);
