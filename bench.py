@@ -38,7 +38,7 @@ WORKLOAD = ("BJ configs[1]: 3D-25pt r4 double stencil, grid 512^3, 168 configs "
             "(56 block shapes x {none,2y,2z} folding), A100 parameters (split L2)")
 TOPK = 10
 # algorithmic integer lane-ops per work unit
-OPS_PER_UNIT = {"k_warp": 12, "k_wclass": 12, "k_smset": 24, "k_sclass": 24, "k_rows": 42, "k_plan": 8}
+OPS_PER_UNIT = {"k_warp": 12, "k_wclass": 12, "k_smset": 16, "k_sclass": 16, "k_rows": 42, "k_plan": 8}
 
 
 def peaks():

@@ -61,6 +61,15 @@ __device__ __forceinline__ long long fdiv(long long n, FDiv f) {
   return (long long)((__umulhi((unsigned)n, f.m) + (unsigned)n) >> f.l);
 }
 
+// Smallest power of two k <= 16 with k * plane_pitch_bytes a multiple of line_bytes (0: none):
+// planes that far apart are translates by whole lines.
+__device__ __forceinline__ int plane_period(long long pz, int le, int ll) {
+  const long long pb = pz << le;
+  const long long tz = pb == 0 ? 63 : __ffsll(pb) - 1;
+  const long long need = ll > tz ? ll - tz : 0;
+  return need <= 4 ? (1 << need) : 0;
+}
+
 struct Tri {
   long long f, l, c;  // first, last, count; c == 0: empty
 };
@@ -107,6 +116,19 @@ __device__ void cta_ordered_reduce(Tri (&t)[NQ], Tri* sm) {
     }
   }
   __syncthreads();
+}
+
+template <int NQ>
+__device__ __forceinline__ void warp_ordered_reduce(Tri (&t)[NQ]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
+      if (lane + o < 32) t[q] = tri_combine(t[q], x);
+    }
+  }
 }
 
 // Union of the element intervals produced by `gen` (each [xs, xe), xs < xe) in one
@@ -748,6 +770,7 @@ struct SmBox {
 };
 constexpr int kMaxMembers = 32;
 
+// (flat-row variant, used for single-block class representatives: small boxes, no plane reuse)
 // Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
 // dispatch, Q9), row by row.  A row (y,z) of field phi holds element x iff some member's
 // box contains (x - ox, y - oy, z - oz) for a load offset o: per (row, offset group) the
@@ -804,7 +827,7 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
     const int ng = *s_ng;
     const long long y0 = s_box[0], ny = s_box[1], z0 = s_box[2], nz = s_box[3];
     const long long rows = ny * nz;
-    units += (unsigned long long)(rows * ng);
+    units += (unsigned long long)rows;
     const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
     const int le = F.lg_elem;
     Tri carry_s = tri_empty(), carry_l = tri_empty();
@@ -863,6 +886,160 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
   }
 }
 
+constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
+
+// Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
+// dispatch, Q9) by one CTA.  Row (y,z) of field phi holds element x iff some member box
+// contains (x - ox, y - oy, z - oz) for a load offset o.  Per z-plane: if every
+// (group, member) z-membership equals that of plane z - per, the plane is the translate of
+// that plane by whole lines (derived); otherwise a warp computes it, lanes taking rows
+// (per row: compares against the member boxes into a candidate mask, union, triple), with an
+// ordered warp reduction.  Thread 0 folds the plane triples in z order.
+__device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
+                          SmBox* mb, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */,
+                          unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwp = blockDim.x >> 5;
+  const int ls = G.lg_sector, ll = G.lg_line;
+  const int nm = (int)(kj < kMaxMembers ? kj : kMaxMembers);
+  sum_s = sum_l = 0;
+  units = 0;
+  __syncthreads();
+  if (tid < nm) {
+    const long long Bm = S0 + (long long)tid * nsm;
+    const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+    long long lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = P.lo[d] + bc[d] * P.BF[d];
+      hi[d] = lo[d] + P.BF[d];
+      if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
+    }
+    mb[tid] = SmBox{lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]};
+  }
+  __syncthreads();
+  long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
+  for (int m = 0; m < nm; ++m) {
+    ylo = min(ylo, mb[m].y0);
+    yhi = max(yhi, mb[m].y1);
+    zlo = min(zlo, mb[m].z0);
+    zhi = max(zhi, mb[m].z1);
+  }
+  for (int fi = 0; fi < K.n_fields; ++fi) {
+    const DField& F = K.f[fi];
+    if (!(F.kinds & 1)) continue;
+    const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
+    const int le = F.lg_elem;
+    long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
+    if (y0 < 0) y0 = 0;
+    if (z0 < 0) z0 = 0;
+    if (y1 > F.ext[1]) y1 = F.ext[1];
+    if (z1 > F.ext[2]) z1 = F.ext[2];
+    if (y1 <= y0 || z1 <= z0) continue;
+    const long long ny = y1 - y0;
+    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
+    const long long pbytes = pz << le;
+    const int per = plane_period(pz, le, ll);
+    const int npairs = ng * nm;
+    Tri cs_all = tri_empty(), cl_all = tri_empty();
+    for (long long zs = z0; zs < z1; zs += kMaxPlanes) {
+      const int np = (int)(z1 - zs < kMaxPlanes ? z1 - zs : kMaxPlanes);
+      // (a) derived planes (relative to plane z - per of the whole box)
+      for (int p = wid; p < np; p += nwp) {
+        const long long z = zs + p;
+        bool same = per > 0 && z - per >= zs;  // derive only within this segment
+        if (same) {
+          for (int k = lane; k < npairs; k += 32) {
+            const DGroup gr = K.g[g0 + k / nm];
+            if (gr.kind != 0) continue;
+            const SmBox& bx = mb[k % nm];
+            const long long za = z - gr.oz, zb = za - per;
+            same = same && ((za >= bx.z0 && za < bx.z1) == (zb >= bx.z0 && zb < bx.z1));
+          }
+        }
+        same = __all_sync(FULL, same);
+        if (lane == 0) pder[p] = same ? 1 : 0;
+      }
+      __syncthreads();
+      // (b) computed planes: one warp per plane, lanes over rows
+      for (int p = wid; p < np; p += nwp) {
+        if (pder[p]) continue;
+        const long long z = zs + p;
+        Tri carry_s = tri_empty(), carry_l = tri_empty();
+        for (long long yb = 0; yb < ny; yb += 32) {
+          Tri t[2] = {tri_empty(), tri_empty()};
+          const long long y = y0 + yb + lane;
+          if (y < y1) {
+            const long long R0 = align + ((py * y + pz * z) << le);
+            if (nm <= 4) {
+              unsigned long long mk = 0;
+              for (int g = 0; g < ng; ++g) {
+                const DGroup gr = K.g[g0 + g];
+                if (gr.kind != 0) continue;
+                const long long yy = y - gr.oy, zz = z - gr.oz;
+                for (int m = 0; m < nm; ++m) {
+                  const SmBox& bx = mb[m];
+                  if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1) mk |= 1ull << (m * 16 + gr.run);
+                }
+              }
+              auto gen = [&](auto&& cb) {
+                unsigned long long q = mk;
+                while (q) {
+                  const int bb = __ffsll((long long)q) - 1;
+                  q &= q - 1;
+                  const SmBox& bx = mb[bb >> 4];
+                  cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
+                }
+              };
+              row_union(gen, R0, le, ls, ll, &t[0], &t[1]);
+            } else {
+              auto gen = [&](auto&& cb) {
+                for (int g = 0; g < ng; ++g) {
+                  const DGroup gr = K.g[g0 + g];
+                  if (gr.kind != 0) continue;
+                  const long long yy = y - gr.oy, zz = z - gr.oz;
+                  for (int m = 0; m < nm; ++m) {
+                    const SmBox& bx = mb[m];
+                    if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
+                      cb(bx.x0 + F.run_lo[gr.run], bx.x1 + F.run_hi[gr.run]);
+                  }
+                }
+              };
+              row_union(gen, R0, le, ls, ll, &t[0], &t[1]);
+            }
+          }
+          warp_ordered_reduce<2>(t);
+          carry_s = tri_combine(carry_s, Tri{shfl64(t[0].f, 0), shfl64(t[0].l, 0), shfl64(t[0].c, 0)});
+          carry_l = tri_combine(carry_l, Tri{shfl64(t[1].f, 0), shfl64(t[1].l, 0), shfl64(t[1].c, 0)});
+        }
+        if (lane == 0) {
+          pt[2 * p] = carry_s;
+          pt[2 * p + 1] = carry_l;
+          units += (unsigned long long)ny;
+        }
+      }
+      __syncthreads();
+      // (c) ordered fold with derivation (plane z - per is resolved before z)
+      if (tid == 0) {
+        for (int p = 0; p < np; ++p) {
+          if (pder[p]) {
+            const int q = p - per;  // >= 0: derived planes have their source in this segment
+            const Tri a = pt[2 * q], b = pt[2 * q + 1];
+            const long long dsh = (long long)per * pbytes;
+            pt[2 * p] = a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty();
+            pt[2 * p + 1] = b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty();
+          }
+          cs_all = tri_combine(cs_all, pt[2 * p]);
+          cl_all = tri_combine(cl_all, pt[2 * p + 1]);
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      sum_s += (unsigned long long)cs_all.c;
+      sum_l += (unsigned long long)cl_all.c;
+    }
+  }
+}
+
 // Pass 1 (one thread per SM set): single-block sets go to their translation class: clip
 // pattern of the block x residue of its first cell's address mod line_bytes (identical
 // active-cell boxes that are translates by a multiple of the line size have identical
@@ -901,23 +1078,23 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
 
 // Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
 // directly evaluated multi-block SM sets.
-__global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
-                                                        const DGpu* __restrict__ gs,
-                                                        unsigned long long* __restrict__ acc,
-                                                        const unsigned int* __restrict__ scnt,
-                                                        const unsigned long long* __restrict__ srep,
-                                                        const unsigned long long* __restrict__ lists,
-                                                        const unsigned long long* __restrict__ slist,
-                                                        const unsigned long long* __restrict__ dlist,
-                                                        unsigned long long* __restrict__ work) {
+__global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                                const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
+                                                const unsigned int* __restrict__ scnt,
+                                                const unsigned long long* __restrict__ srep,
+                                                const unsigned long long* __restrict__ lists,
+                                                const unsigned long long* __restrict__ slist,
+                                                const unsigned long long* __restrict__ dlist,
+                                                unsigned long long* __restrict__ work) {
+  __shared__ SmBox s_mb[kMaxMembers];
+  __shared__ Tri s_pt[2 * kMaxPlanes];
+  __shared__ unsigned char s_der[kMaxPlanes];
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
-  __shared__ SmBox s_mb[kMaxMembers];
   __shared__ Tri s_red[(kRowThreads / 32) * 2];
   const long long ncls = (long long)lists[1];
   const long long total = ncls + (long long)lists[2];
-  const int tid = threadIdx.x;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
     const bool cls = item < ncls;
     const unsigned long long ent = cls ? slist[item] : dlist[item - ncls];
@@ -938,12 +1115,18 @@ __global__ void __launch_bounds__(kRowThreads) k_sclass(const DPlan* __restrict_
       kj = (P.W - (long long)low + nsm - 1) / nsm;
     }
     unsigned long long ss, sl, un;
-    smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
-    if (tid == 0) {
+    if (kj == 1) {
+      smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
+      if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
+    } else {
+      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_pt, s_der, ss, sl, un);
+      // every warp's lane 0 counted its planes' rows
+      if ((threadIdx.x & 31) == 0 && un) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
+    }
+    if (threadIdx.x == 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_SM_SEC, ss * mult);
       atomicAdd(a + A_SM_LIN, sl * mult);
-      atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     }
   }
 }
@@ -962,15 +1145,6 @@ __device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
   if (r == R.ra) return 1;
   if (r == R.rl) return 2;
   return 0;
-}
-
-// Smallest power of two k <= 16 with k * plane_pitch_bytes a multiple of line_bytes (0: none):
-// planes that far apart are translates by whole lines.
-__device__ __forceinline__ int plane_period(long long pz, int le, int ll) {
-  const long long pb = pz << le;
-  const long long tz = pb == 0 ? 63 : __ffsll(pb) - 1;
-  const long long need = ll > tz ? ll - tz : 0;
-  return need <= 4 ? (1 << need) : 0;
 }
 
 // Cached union of one row: a single component [x0, x1) (x0 >= x1: empty) or `multi`.
@@ -1020,19 +1194,6 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
     }
   } else {
     row_union(gen, R0, le, ls, ll, ts, tl, ts2);
-  }
-}
-
-template <int NQ>
-__device__ __forceinline__ void warp_ordered_reduce(Tri (&t)[NQ]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
-      if (lane + o < 32) t[q] = tri_combine(t[q], x);
-    }
   }
 }
 
@@ -1527,8 +1688,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_smset<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
   ++L;
   mark();
-  k_sclass<<<persist, kRowThreads, 0, st>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist,
-                                             s.work);
+  k_sclass<<<persist, 256, 0, st>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
   ++L;
   mark();
   k_rows<<<persist, kRowWarps * 32, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
