@@ -64,6 +64,14 @@ struct DRowInfo {
 };
 constexpr int kPlaneRows = 8192;   // target rows per k_rows chunk
 
+// One contiguous block-id range [a, b) seen per block row: first / last block row touched and the
+// four cell x-intervals it can cover in a row (FULL, SUFFIX, PREFIX, MIDDLE).
+struct RangeInfo {
+  int64_t ra, rl;
+  int64_t iv[4][2];
+  int32_t nonempty, pad;
+};
+
 // n / d for 0 <= n < 2^31 by multiply-high (Granlund-Montgomery round-up method):
 // q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
 struct FDiv {
@@ -84,6 +92,11 @@ struct DPlan {
   uint64_t addr_evals;
   FDiv fd_BF[3];                 // division by BF[d] (cell -> block coordinate)
   int64_t part[3];               // extent of a partial last block per dim (0 = none)
+  // k_rows: ranges 0 = wave, 1 = L_y, 2 = L_z, 3 = L_y + wave, 4 = L_z + wave, and the sorted
+  // distinct block rows where some range's classification zone starts
+  RangeInfo rng[5];
+  int64_t bnd[20];
+  int32_t nb, pad3;
 };
 
 // per-config accumulator slots (u64, atomically added by the worker kernels)

@@ -285,6 +285,47 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   const long long Rw = M >> K.f[0].lg_elem, Rs = (long long)G.g.line_bytes >> K.f[0].lg_elem;
   P.wcls_R = (same && Rw >= 1 && Rw <= 64 && P.nwarps <= 32) ? (int)Rw : 0;
   P.scls_R = (same && Rs >= 1 && Rs <= 64) ? (int)Rs : 0;
+  // k_rows ranges and zone boundaries
+  P.nb = 0;
+  for (int q = 0; q < 5; ++q) {
+    long long a, b;
+    if (q == 0) { a = P.s; b = P.s + P.W; }
+    else if (q == 1) { a = P.Ly0; b = P.s; }
+    else if (q == 2) { a = P.Lz0; b = P.s; }
+    else if (q == 3) { a = P.Ly0; b = P.s + P.W; }
+    else { a = P.Lz0; b = P.s + P.W; }
+    RangeInfo& R = P.rng[q];
+    R.nonempty = a < b;
+    R.pad = 0;
+    const long long Gx = P.G[0], lx = P.lo[0], hx = P.hi[0], bf = P.BF[0];
+    long long xa = 0, xl = Gx;
+    if (a < b) {
+      R.ra = a / Gx;
+      xa = a % Gx;
+      R.rl = (b - 1) / Gx;
+      xl = (b - 1) % Gx + 1;
+    } else {
+      R.ra = R.rl = 0;
+    }
+    const long long xs_a = lx + xa * bf;
+    long long xe_l = lx + xl * bf;
+    if (xe_l > hx) xe_l = hx;
+    R.iv[0][0] = lx;   R.iv[0][1] = hx;
+    R.iv[1][0] = xs_a; R.iv[1][1] = hx;
+    R.iv[2][0] = lx;   R.iv[2][1] = xe_l;
+    R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
+    if (!R.nonempty) continue;
+    const long long cand[4] = {R.ra, R.ra + 1, R.rl, R.rl + 1};
+    for (int k = 0; k < 4; ++k) {
+      const long long v = cand[k];
+      int pos = 0;
+      while (pos < P.nb && P.bnd[pos] < v) ++pos;
+      if (pos < P.nb && P.bnd[pos] == v) continue;
+      for (int m = P.nb; m > pos; --m) P.bnd[m] = P.bnd[m - 1];
+      P.bnd[pos] = v;
+      ++P.nb;
+    }
+  }
   for (int d = 0; d < 3; ++d) P.cls_pitch[d] = K.f[0].pitch[d];
   P.cls_lg_elem = K.f[0].lg_elem;
   P.status = WS_OK;
@@ -1133,11 +1174,6 @@ __global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans,
 
 // ------------------------------------------------------------------ a5 + a6: wave and layer sets
 // ranges: 0 = wave [s, s+W), 1 = L_y [Ly0, s), 2 = L_z [Lz0, s), 3 = L_y + wave, 4 = L_z + wave
-struct RangeInfo {
-  long long ra, rl;      // first / last block-row touched
-  long long iv[4][2];    // x cell intervals: FULL, SUFFIX, PREFIX, MIDDLE
-  int nonempty, pad;
-};
 
 __device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
   if (!R.nonempty || r < R.ra || r > R.rl) return -1;
@@ -1252,52 +1288,12 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict
     const DField& F = K.f[fi];
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
     __syncwarp();
-    if (lane < 5) {
-      long long a, b;
-      if (lane == 0) { a = P.s; b = P.s + P.W; }
-      else if (lane == 1) { a = P.Ly0; b = P.s; }
-      else if (lane == 2) { a = P.Lz0; b = P.s; }
-      else if (lane == 3) { a = P.Ly0; b = P.s + P.W; }
-      else { a = P.Lz0; b = P.s + P.W; }
-      RangeInfo R;
-      R.nonempty = a < b;
-      R.pad = 0;
-      const long long Gx = P.G[0], lx = P.lo[0], hx = P.hi[0], bf = P.BF[0];
-      long long xa = 0, xl = Gx;
-      if (a < b) {
-        R.ra = a / Gx;
-        xa = a % Gx;
-        R.rl = (b - 1) / Gx;
-        xl = (b - 1) % Gx + 1;
-      } else {
-        R.ra = R.rl = 0;
-      }
-      const long long xs_a = lx + xa * bf;
-      long long xe_l = lx + xl * bf;
-      if (xe_l > hx) xe_l = hx;
-      R.iv[0][0] = lx;   R.iv[0][1] = hx;
-      R.iv[1][0] = xs_a; R.iv[1][1] = hx;
-      R.iv[2][0] = lx;   R.iv[2][1] = xe_l;
-      R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
-      X.r[lane] = R;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      int nb = 0;
-      for (int q = 0; q < 5; ++q) {
-        if (!X.r[q].nonempty) continue;
-        const long long cand[4] = {X.r[q].ra, X.r[q].ra + 1, X.r[q].rl, X.r[q].rl + 1};
-        for (int k = 0; k < 4; ++k) {
-          const long long v = cand[k];
-          int pos = 0;
-          while (pos < nb && X.bnd[pos] < v) ++pos;
-          if (pos < nb && X.bnd[pos] == v) continue;
-          for (int m = nb; m > pos; --m) X.bnd[m] = X.bnd[m - 1];
-          X.bnd[pos] = v;
-          ++nb;
-        }
-      }
-      X.nb = nb;
+    {  // ranges and zone boundaries of this config (k_plan) -> warp smem
+      const long long* src = reinterpret_cast<const long long*>(&P.rng[0]);
+      long long* dst = reinterpret_cast<long long*>(&X);
+      constexpr int nw64 = (int)((sizeof(RangeInfo) * 5 + sizeof(long long) * 20) / 8);
+      for (int k = lane; k < nw64; k += 32) dst[k] = src[k];
+      if (lane == 0) X.nb = P.nb;
     }
     __syncwarp();
     const int nb = X.nb;
@@ -1317,21 +1313,28 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict
     // plane reuse period: smallest power of two k with k*pz*elem a multiple of line_bytes
     const int per = plane_period(pz, le, ll);
     for (long long z = zc0; z < zc1; ++z) {
-      // identical row structure to plane z - per when every offset group falls in the same
-      // block layer (or outside the domain) in both planes: k_fold derives it by translation
-      if (per > 0 && z - per >= RI.z0) {
-        bool same = true;
+      // Planes whose every offset group falls in the same block layer (or the same side outside
+      // the domain) have identical row structure.  The segment of such planes containing z
+      // starts at the latest layer / domain edge crossed by some group; its plane congruent to
+      // z mod per is the representative, of which z is the translate by whole lines.
+      if (per > 0) {
+        long long seg = RI.z0;
         for (int g = lane; g < ng; g += 32) {
-          const long long za = z - K.g[g0 + g].oz, zb = za - per;
-          const long long ka = (za < lo2 || za >= hi2) ? -1 : fdiv(za - lo2, fdz);
-          const long long kb = (zb < lo2 || zb >= hi2) ? -1 : fdiv(zb - lo2, fdz);
-          same = same && ka == kb;
+          const long long oz = K.g[g0 + g].oz, zz = z - oz;
+          long long st;
+          if (zz < lo2) st = LLONG_MIN;
+          else if (zz >= hi2) st = hi2 + oz;
+          else st = lo2 + fdiv(zz - lo2, fdz) * P.BF[2] + oz;
+          seg = st > seg ? st : seg;
         }
-        if (__all_sync(FULL, same)) {
-          if (lane == 0) {
-            long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
-            out[2] = -1;  // derived plane marker (counts are never negative)
-          }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const long long v = shfl64(seg, (lane + o) & 31);
+          seg = v > seg ? v : seg;
+        }
+        const long long rep = seg + ((z - seg) % per);
+        if (rep != z) {
+          if (lane == 0) chunkres[(pre[c].chunk + ci) * (kNQ * 3) + 2] = -(rep - RI.z0) - 2;
           continue;
         }
       }
@@ -1492,8 +1495,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict
 }
 
 // Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
-// plane (marker count -1) takes the triple of plane z - k*per (the nearest computed one)
-// translated by k*per plane pitches (whole lines).
+// plane (count slot = -(representative index) - 2) takes its representative's triple
+// translated by the plane distance (a multiple of the reuse period: whole lines).
 __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                               const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                               const DRowInfo* __restrict__ rowinfo,
@@ -1509,7 +1512,6 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
     const DField& F = ks[P.kid].f[fi];
     const DGpu& G = gs[P.gid];
     const int ls = G.lg_sector, ll = G.lg_line;
-    const int per = plane_period(F.pitch[2], F.lg_elem, ll);
     const long long pbytes = F.pitch[2] << F.lg_elem;
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
@@ -1520,7 +1522,8 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
     for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
       long long src = k;
-      while (base[src * (kNQ * 3) + 2] == -1) src -= per;  // per > 0 whenever a marker exists
+      const long long mk = base[k * (kNQ * 3) + 2];
+      if (mk < 0) src = -mk - 2;  // derived plane: representative plane index
       const long long* in = base + src * (kNQ * 3);
       const long long dbytes = (k - src) * pbytes;
 #pragma unroll
