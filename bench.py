@@ -204,10 +204,14 @@ def run_native(args, rank, world, local):
     d_top = torch.empty(TOPK, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    from paper_2204_14242_b200 import dist as D
+    shards = [[r * n + j for j in range(n)] for r in range(world)]   # rank r: its hardware set
+
     def step():
+        nonlocal gathered
         ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
         if world > 1:
-            dist.all_gather_into_tensor(gathered, d_out)
+            gathered = D.gather_records(d_out.view(n, rb), shards).view(-1)
         ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
 
     launches_per_step = None

@@ -185,3 +185,53 @@ def test_full_size_lbm15_sampled(ctx):
     assert not errs, "\n".join(errs)
     for r in g:
         assert r["dram_ld_Bpl"] >= 120.0 and r["dram_ld_Bpl"] + r["dram_st_Bpl"] >= 240.0
+
+
+def test_sharded_single_rank_matches(ctx):
+    """dist.estimate_sharded on one rank = the direct batch (record bytes identical)."""
+    import torch
+    from paper_2204_14242_b200 import config_array, dist as D
+    k, gp = W.k25(64), W.gpu_a100()
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(gp)
+    a = config_array(kid, gid, W.space_stencil_paper())
+    ref = ctx.estimate(a)
+    ctx.rank(ref, 10)
+    res, top = D.estimate_sharded(ctx, a, k_top=10)
+    torch.cuda.synchronize()
+    assert res.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_medium_domains(ctx, seed):
+    """Medium domains (24-56 cells per dim) with deep / folded blocks and occupancy > 1:
+    exercises the derived planes, multi-block SM sets and multi-component row unions."""
+    rng = random.Random(1000 + seed)
+    k = W.random_kernel(500 + seed, max_fields=2, max_acc=10, max_dom=56)
+    gp = dict(W.random_gpu(seed), n_sm=rng.choice([4, 6, 9, 16]))
+    cf = []
+    for _ in range(5):
+        b = (rng.choice([1, 2, 4, 8, 16, 32]), rng.choice([1, 2, 4, 8]), rng.choice([1, 2, 4, 8, 16]))
+        while b[0] * b[1] * b[2] > 256:
+            b = (b[0], b[1], max(1, b[2] // 2))
+        f = (rng.choice([1, 1, 2]), rng.choice([1, 2]), rng.choice([1, 2, 4]))
+        cf.append((b, f, rng.choice([0, 1, 2, 3])))
+    assert_parity(ctx, k, gp, cf, f"med{seed}")
+
+
+def test_grid_sweep_sizes_sampled(ctx):
+    """BJ configs[4]: the 25pt space at 32^3 and 96^3 (every config; oracle in seconds)."""
+    for n in (32, 96):
+        cf = W.space_stencil_paper()[::3]
+        assert_parity(ctx, W.k25(n), W.gpu_a100(), cf, f"sweep{n}")
+
+
+def test_full_size_lbm27_sampled(ctx):
+    """BJ configs[2] LBM27 (58 arrays) 256^3: whole space in one launch, one sampled config."""
+    k, gp, cf = W.lbm27(256), W.gpu_a100(), W.space_lbm()
+    g, _ = run_gpu(ctx, k, gp, cf)
+    idx = [i for i, c in enumerate(cf) if c[0] == (64, 8, 1)]
+    o = O.estimate_batch(k, gp, [cf[i] for i in idx], NT)
+    errs = []
+    for j, i in enumerate(idx):
+        errs += compare(g[i], o[j], f"lbm27[{i}] {cf[i]}")
+    assert not errs, "\n".join(errs)
