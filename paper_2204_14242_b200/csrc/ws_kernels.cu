@@ -1236,10 +1236,15 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
 constexpr int kRowWarps = 8;
 constexpr int kRowsPerLane = kRowsPerChunk / 32;
 
+constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
+constexpr int kRunMax = 16;     // runs are split every kRunMax rows (lane work balance)
+
 struct WarpRowCtx {
   RangeInfo r[5];
   long long bnd[20];  // sorted distinct block rows where some range's classification zone starts
   int nb, pad;
+  unsigned bm[kSegRows / 32];                   // run-start bitmap of the current segment
+  short rs[kSegRows + 2];                       // run starts (ascending) + end
 };
 
 // One union of a row: candidates (range q1, mask m1) u (range q2, mask m2); targets are
@@ -1340,141 +1345,150 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict
       }
       Tri pt[kNQ];
       my_rows += (unsigned long long)(lane == 0 ? ny : 0);
-      {
 #pragma unroll
-        for (int q = 0; q < kNQ; ++q) pt[q] = tri_empty();
-        long long y = RI.y0;
-        const long long yend = RI.y0 + ny;
-        while (y < yend) {  // warp-uniform
-          long long y_stop = yend;
-          // ---- masks of row (y, z) and the run end: lanes split the offset groups
-          unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
-          for (int g = lane; g < ng; g += 32) {
-            const DGroup gr = K.g[g0 + g];
-            const long long zz = z - gr.oz;
-            if (zz < lo2 || zz >= hi2) continue;
-            const long long yy = y - gr.oy;
-            if (yy < lo1) {
-              if (y + (lo1 - yy) < y_stop) y_stop = y + (lo1 - yy);
-              continue;
-            }
-            if (yy >= hi1) continue;
-            const long long C = Gy * fdiv(zz - lo2, fdz);
-            const long long r = fdiv(yy - lo1, fdy) + C;
-    #pragma unroll
-            for (int q = 0; q < 5; ++q) {
-              const int ty = classify(X.r[q], r);
-              if (ty >= 0) {
-                const unsigned long long bit = 1ull << (ty * 16 + gr.run);
-                if (gr.kind) mS[q] |= bit;
-                else mL[q] |= bit;
-              }
-            }
-            long long yn = hi1;
-            for (int k = 0; k < nb; ++k) {
-              const long long bk = X.bnd[k];
-              if (bk > r) {
-                if (bk - C < Gy) {
-                  const long long v = lo1 + (bk - C) * BF1;
-                  yn = v < hi1 ? v : hi1;
-                }
-                break;
-              }
-            }
-            if (yn + gr.oy < y_stop) y_stop = yn + gr.oy;
+      for (int q = 0; q < kNQ; ++q) pt[q] = tri_empty();
+      for (long long ys = RI.y0; ys < RI.y0 + ny; ys += kSegRows) {
+        const int nseg = (int)(RI.y0 + ny - ys < kSegRows ? RI.y0 + ny - ys : kSegRows);
+        const int nwd = (nseg + 31) >> 5;
+        // (1) breakpoint bitmap over the segment's rows: a run starts where some offset group's
+        //     region row enters another classification zone or the domain, and every kRunMax rows
+        for (int w = lane; w < nwd; w += 32) X.bm[w] = 0u;
+        __syncwarp();
+        for (int i = lane * kRunMax; i < nseg; i += 32 * kRunMax) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
+        for (int g = lane; g < ng; g += 32) {
+          const DGroup gr = K.g[g0 + g];
+          const long long zz = z - gr.oz;
+          if (zz < lo2 || zz >= hi2) continue;
+          const long long C = Gy * fdiv(zz - lo2, fdz);
+          auto mark = [&](long long yb) {
+            const long long i = yb - ys;
+            if (i > 0 && i < nseg) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
+          };
+          mark(lo1 + gr.oy);
+          mark(hi1 + gr.oy);
+          for (int k = 0; k < nb; ++k) {
+            const long long d = X.bnd[k] - C;
+            if (d > 0 && d < Gy) mark(lo1 + d * BF1 + gr.oy);
           }
-    #pragma unroll
-          for (int q = 0; q < 5; ++q) {
-            mL[q] = ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(mL[q] >> 32)) << 32) |
-                    __reduce_or_sync(FULL, (unsigned)mL[q]);
-            mS[q] = ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(mS[q] >> 32)) << 32) |
-                    __reduce_or_sync(FULL, (unsigned)mS[q]);
-          }
-          y_stop = y + __reduce_min_sync(FULL, (unsigned)(y_stop - y));
-          const long long run = y_stop - y;
-          // ---- the run's unions (uniform)
-          USpec U[7];
-          int nu = 0;
-          const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
-          if (noS) {
-            U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, 2, -1, 0};
-          } else if (noL) {
-            U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, 2, -1, 0};
-          } else {
-            U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, -1, -1, 0};
-            U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, -1, -1, 0};
-            U[nu++] = USpec{mL[0] | mS[0], 0ull, 0, 0, -1, 2, -1, 0};
-          }
-          if (!noL) {
-            U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, -1, 0};
-            U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, -1, 0};
-            U[nu++] = USpec{mL[3], mS[1], 3, 1, 7, -1, -1, 0};
-            U[nu++] = USpec{mL[4], mS[2], 4, 2, 8, -1, -1, 0};
-          } else {
-            U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, 7, 0};
-            U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, 8, 0};
-          }
-          const long long R0f = align + ((py * y + pz * z) << le);
-          const long long R0l = R0f + (run - 1) * pystep;
-          for (int u = 0; u < nu; ++u) {
-            const USpec sp = U[u];
-            auto gen = [&](auto&& cb) {
-              unsigned long long m = sp.m1;
-              while (m) {
-                const int b = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const int ty = b >> 4, rr = b & 15;
-                cb(X.r[sp.q1].iv[ty][0] + F.run_lo[rr], X.r[sp.q1].iv[ty][1] + F.run_hi[rr]);
-              }
-              m = sp.m2;
-              while (m) {
-                const int b = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const int ty = b >> 4, rr = b & 15;
-                cb(X.r[sp.q2].iv[ty][0] + F.run_lo[rr], X.r[sp.q2].iv[ty][1] + F.run_hi[rr]);
-              }
-            };
-            long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
-            gen([&](long long xs, long long xe) {
-              mn_s = xs < mn_s ? xs : mn_s;
-              mx_s = xs > mx_s ? xs : mx_s;
-              mn_e = xe < mn_e ? xe : mn_e;
-              mx_e = xe > mx_e ? xe : mx_e;
-            });
-            if (mn_s == LLONG_MAX) continue;  // empty union in every row of the run
-            const bool single = mx_s <= mn_e;
-            const long long d0 = mn_s << le, d1 = (mx_e - 1) << le;
-            // per-lane rows of the run: count(y) - [last(y) == first(y+1)]
-            long long cs = 0, cl = 0;
-            for (long long r = lane; r < run; r += 32) {
-              const long long R0 = R0f + r * pystep;
-              const long long a0 = R0 + d0, a1 = R0 + d1, an = a0 + pystep;
-              const bool more = r + 1 < run;
-              if (single) {
-                if (sp.ts >= 0) cs += ((a1 >> ls) - (a0 >> ls) + 1) - (more && (a1 >> ls) == (an >> ls) ? 1 : 0);
-                if (sp.tl >= 0) cl += ((a1 >> ll) - (a0 >> ll) + 1) - (more && (a1 >> ll) == (an >> ll) ? 1 : 0);
-              } else {
-                Tri ts = tri_empty(), tl = tri_empty();
-                row_union(gen, R0, le, ls, ll, sp.ts >= 0 ? &ts : nullptr, sp.tl >= 0 ? &tl : nullptr);
-                if (sp.ts >= 0) cs += ts.c - (more && (a1 >> ls) == (an >> ls) ? 1 : 0);
-                if (sp.tl >= 0) cl += tl.c - (more && (a1 >> ll) == (an >> ll) ? 1 : 0);
-              }
-            }
-            // run triples (warp sums; counts of one run fit 32 bits)
-            if (sp.ts >= 0) {
-              const long long sum = (long long)__reduce_add_sync(FULL, (unsigned)cs);
-              const Tri tr{(R0f + d0) >> ls, (R0l + d1) >> ls, sum};
-              pt[sp.ts] = tri_combine(pt[sp.ts], tr);
-              if (sp.ts2 >= 0) pt[sp.ts2] = tri_combine(pt[sp.ts2], tr);
-            }
-            if (sp.tl >= 0) {
-              const long long sum = (long long)__reduce_add_sync(FULL, (unsigned)cl);
-              const Tri tr{(R0f + d0) >> ll, (R0l + d1) >> ll, sum};
-              pt[sp.tl] = tri_combine(pt[sp.tl], tr);
-            }
-          }
-          y += run;
         }
+        __syncwarp();
+        // (2) compact the run starts (ascending) into X.rs
+        const int wpl = (nwd + 31) >> 5;
+        int cnt = 0;
+        for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(X.bm[w]);
+        int pos = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(FULL, pos, o);
+          if (lane >= o) pos += v;
+        }
+        const int nruns = __shfl_sync(FULL, pos, 31);
+        pos -= cnt;
+        for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
+          unsigned bits = X.bm[w];
+          while (bits) {
+            const int bt = __ffs(bits) - 1;
+            bits &= bits - 1;
+            X.rs[pos++] = (short)(w * 32 + bt);
+          }
+        }
+        if (lane == 0) X.rs[nruns] = (short)nseg;
+        __syncwarp();
+        // (3) one run per lane: masks of its first row, unions, rows emitted in order
+        for (int rb = 0; rb < nruns; rb += 32) {
+          Tri t[kNQ];
+#pragma unroll
+          for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
+          const int j = rb + lane;
+          if (j < nruns) {
+            const long long y = ys + X.rs[j];
+            const int run = X.rs[j + 1] - X.rs[j];
+            unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
+            for (int g = 0; g < ng; ++g) {
+              const DGroup gr = K.g[g0 + g];
+              const long long zz = z - gr.oz, yy = y - gr.oy;
+              if (zz < lo2 || zz >= hi2 || yy < lo1 || yy >= hi1) continue;
+              const long long r = fdiv(yy - lo1, fdy) + Gy * fdiv(zz - lo2, fdz);
+#pragma unroll
+              for (int q = 0; q < 5; ++q) {
+                const int ty = classify(X.r[q], r);
+                if (ty >= 0) {
+                  const unsigned long long bit = 1ull << (ty * 16 + gr.run);
+                  if (gr.kind) mS[q] |= bit;
+                  else mL[q] |= bit;
+                }
+              }
+            }
+            USpec U[7];
+            int nu = 0;
+            const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
+            if (noS) {
+              U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, 2, -1, 0};
+            } else if (noL) {
+              U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, 2, -1, 0};
+            } else {
+              U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, -1, -1, 0};
+              U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, -1, -1, 0};
+              U[nu++] = USpec{mL[0] | mS[0], 0ull, 0, 0, -1, 2, -1, 0};
+            }
+            if (!noL) {
+              U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, -1, 0};
+              U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, -1, 0};
+              U[nu++] = USpec{mL[3], mS[1], 3, 1, 7, -1, -1, 0};
+              U[nu++] = USpec{mL[4], mS[2], 4, 2, 8, -1, -1, 0};
+            } else {
+              U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, 7, 0};
+              U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, 8, 0};
+            }
+            const long long R0f = align + ((py * y + pz * z) << le);
+            for (int u = 0; u < nu; ++u) {
+              const USpec sp = U[u];
+              auto gen = [&](auto&& cb) {
+                unsigned long long m = sp.m1;
+                while (m) {
+                  const int bb = __ffsll((long long)m) - 1;
+                  m &= m - 1;
+                  const int ty = bb >> 4, rr = bb & 15;
+                  cb(X.r[sp.q1].iv[ty][0] + F.run_lo[rr], X.r[sp.q1].iv[ty][1] + F.run_hi[rr]);
+                }
+                m = sp.m2;
+                while (m) {
+                  const int bb = __ffsll((long long)m) - 1;
+                  m &= m - 1;
+                  const int ty = bb >> 4, rr = bb & 15;
+                  cb(X.r[sp.q2].iv[ty][0] + F.run_lo[rr], X.r[sp.q2].iv[ty][1] + F.run_hi[rr]);
+                }
+              };
+              long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
+              gen([&](long long xs, long long xe) {
+                mn_s = xs < mn_s ? xs : mn_s;
+                mx_s = xs > mx_s ? xs : mx_s;
+                mn_e = xe < mn_e ? xe : mn_e;
+                mx_e = xe > mx_e ? xe : mx_e;
+              });
+              if (mn_s == LLONG_MAX) continue;
+              Tri* ts = sp.ts >= 0 ? &t[sp.ts] : nullptr;
+              Tri* tl = sp.tl >= 0 ? &t[sp.tl] : nullptr;
+              Tri* ts2 = sp.ts2 >= 0 ? &t[sp.ts2] : nullptr;
+              if (mx_s <= mn_e) {
+                const long long d0 = mn_s << le, d1 = (mx_e - 1) << le;
+                for (int r = 0; r < run; ++r) {
+                  const long long R0 = R0f + r * pystep;
+                  if (ts) tri_add(*ts, (R0 + d0) >> ls, (R0 + d1) >> ls);
+                  if (ts2) tri_add(*ts2, (R0 + d0) >> ls, (R0 + d1) >> ls);
+                  if (tl) tri_add(*tl, (R0 + d0) >> ll, (R0 + d1) >> ll);
+                }
+              } else {
+                for (int r = 0; r < run; ++r) row_union(gen, R0f + r * pystep, le, ls, ll, ts, tl, ts2);
+              }
+            }
+          }
+          warp_ordered_reduce<kNQ>(t);
+#pragma unroll
+          for (int q = 0; q < kNQ; ++q)
+            pt[q] = tri_combine(pt[q], Tri{shfl64(t[q].f, 0), shfl64(t[q].l, 0), shfl64(t[q].c, 0)});
+        }
+        __syncwarp();
       }
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) carry[q] = tri_combine(carry[q], pt[q]);
