@@ -44,11 +44,15 @@ struct ws_ctx {
   };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> free_ev;
+  // aux streams + fork/join events for the concurrent worker chains
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+  // 2 events (start, end) per kernel kind, kinds [first_kind, first_kind + nk)
   cudaEvent_t* take_events(int first_kind, int nk) {
     Rec r;
     r.first_kind = first_kind;
     r.n = nk;
-    for (int i = 0; i <= nk; ++i) {
+    for (int i = 0; i < 2 * nk; ++i) {
       cudaEvent_t e;
       if (!free_ev.empty()) {
         e = free_ev.back();
@@ -176,6 +180,14 @@ ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out) {
   c->stream = (cudaStream_t)cuda_stream;
   cudaDeviceGetAttribute(&c->n_sm_dev, cudaDevAttrMultiProcessorCount, cuda_device);
   if (c->n_sm_dev <= 0) c->n_sm_dev = 148;
+  if (cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->join[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->join[1], cudaEventDisableTiming) != cudaSuccess) {
+    ws_destroy(c);
+    return WS_ECUDA;
+  }
   *out = c;
   return WS_OK;
 }
@@ -190,6 +202,11 @@ void ws_destroy(ws_ctx* c) {
   for (auto& r : c->pending)
     for (cudaEvent_t e : r.ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->free_ev) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->aux[i]) cudaStreamDestroy(c->aux[i]);
+    if (c->join[i]) cudaEventDestroy(c->join[i]);
+  }
+  if (c->fork) cudaEventDestroy(c->fork);
   delete c;
 }
 
@@ -223,8 +240,8 @@ ws_status ws_profile_read(ws_ctx* c, double* ms, uint64_t* launches, uint32_t ca
   for (auto& r : c->pending) {
     for (int i = 0; i < r.n; ++i) {
       float t = 0.f;
-      cudaError_t e = cudaEventSynchronize(r.ev[i + 1]);
-      if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.ev[i], r.ev[i + 1]);
+      cudaError_t e = cudaEventSynchronize(r.ev[2 * i + 1]);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.ev[2 * i], r.ev[2 * i + 1]);
       if (e != cudaSuccess) st = cuda_fail(c, e, "profile read");
       acc[r.first_kind + i] += t;
       cnt[r.first_kind + i] += 1;
@@ -401,7 +418,14 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   Scratch S;
   if ((s = ensure_scratch(c, n, S)) != WS_OK) return s;
   cudaEvent_t* ev = c->profiling ? c->take_events(K_PLAN, kEstimateKernels) : nullptr;
-  int e = launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, c->stream,
+  Streams st;
+  st.main = c->stream;
+  st.aux[0] = c->aux[0];
+  st.aux[1] = c->aux[1];
+  st.fork = c->fork;
+  st.join[0] = c->join[0];
+  st.join[1] = c->join[1];
+  int e = launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st,
                           c->n_sm_dev, &c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "launch");
   return WS_OK;

@@ -136,11 +136,17 @@ struct Scratch {
 enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_MODEL, K_RANK, K_NKINDS };
 constexpr int kEstimateKernels = 9;
 
-// ev: nullptr, or kEstimateKernels+1 events recorded before each launch and after the last
+// Streams and fork/join events of one context: the three worker chains (warp scope, SM-set
+// scope, row scope) run concurrently after k_scan.
+struct Streams {
+  cudaStream_t main, aux[2];
+  cudaEvent_t fork, join[2];
+};
+// ev: nullptr, or 2 events per kernel (start, end) in K_* order, recorded on the kernel's stream
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
-                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches,
+                    const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
                     cudaEvent_t* ev);
-// ev: nullptr or 2 events
+// ev: nullptr or 2 events (start, end)
 int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches,
                 cudaEvent_t* ev);
 

@@ -1677,46 +1677,57 @@ static int check_launch() {
 }
 
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
-                    const Scratch& s, ws_result* d_out, cudaStream_t st, int n_sm_dev, uint32_t* launches,
+                    const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
                     cudaEvent_t* ev) {
   uint32_t L = 0;
-  int mk = 0;
-  auto mark = [&]() {
-    if (ev) cudaEventRecord(ev[mk], st);
-    ++mk;
+  auto beg = [&](int kind, cudaStream_t q) {
+    if (ev) cudaEventRecord(ev[2 * kind], q);
+  };
+  auto end = [&](int kind, cudaStream_t q) {
+    if (ev) cudaEventRecord(ev[2 * kind + 1], q);
+    ++L;
   };
   const int persist = n_sm_dev * 8;
-  cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), st);
-  cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), st);
-  mark();
-  k_plan<<<n, 128, 0, st>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt);
-  ++L;
-  mark();
-  k_scan<<<1, 1024, 0, st>>>(s.plans, n, s.prefix, s.work, s.lists);
-  ++L;
-  mark();
-  k_warp<<<persist, 256, 0, st>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
-                                   s.work);
-  ++L;
-  mark();
-  k_wclass<<<persist, 256, 0, st>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
-  ++L;
-  mark();
-  k_smset<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
-  ++L;
-  mark();
-  k_sclass<<<persist, 256, 0, st>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
-  ++L;
-  mark();
-  k_rows<<<persist, kRowWarps * 32, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
-  ++L;
-  mark();
-  k_fold<<<n_sm_dev * 2, 256, 0, st>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
-  ++L;
-  mark();
-  k_model<<<(n + 127) / 128, 128, 0, st>>>(s.plans, n, d_k, d_g, s.acc, d_out);
-  ++L;
-  mark();
+  cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
+  cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), m);
+  cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), m);
+  beg(K_PLAN, m);
+  k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt);
+  end(K_PLAN, m);
+  beg(K_SCAN, m);
+  k_scan<<<1, 1024, 0, m>>>(s.plans, n, s.prefix, s.work, s.lists);
+  end(K_SCAN, m);
+  // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on main
+  cudaEventRecord(st.fork, m);
+  cudaStreamWaitEvent(a, st.fork, 0);
+  cudaStreamWaitEvent(b, st.fork, 0);
+  beg(K_ROWS, b);
+  k_rows<<<persist, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
+  end(K_ROWS, b);
+  beg(K_FOLD, b);
+  k_fold<<<n_sm_dev * 2, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
+  end(K_FOLD, b);
+  beg(K_SMSET, a);
+  k_smset<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, s.prefix, n, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
+  end(K_SMSET, a);
+  beg(K_SCLASS, a);
+  k_sclass<<<persist, 256, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
+  end(K_SCLASS, a);
+  beg(K_WARP, m);
+  k_warp<<<persist, 256, 0, m>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
+                                 s.work);
+  end(K_WARP, m);
+  beg(K_WCLASS, m);
+  k_wclass<<<persist, 256, 0, m>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
+  end(K_WCLASS, m);
+  // join
+  cudaEventRecord(st.join[0], a);
+  cudaEventRecord(st.join[1], b);
+  cudaStreamWaitEvent(m, st.join[0], 0);
+  cudaStreamWaitEvent(m, st.join[1], 0);
+  beg(K_MODEL, m);
+  k_model<<<(n + 127) / 128, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out);
+  end(K_MODEL, m);
   if (launches) *launches = L;
   return check_launch();
 }
