@@ -1234,7 +1234,6 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
 }
 
 constexpr int kRowWarps = 8;
-constexpr int kRowsPerLane = kRowsPerChunk / 32;
 
 constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
 constexpr int kRunMax = 16;     // runs are split every kRunMax rows (lane work balance)
@@ -1246,6 +1245,56 @@ struct WarpRowCtx {
   unsigned bm[kSegRows / 32];                   // run-start bitmap of the current segment
   short rs[kSegRows + 2];                       // run starts (ascending) + end
 };
+
+// Union of the candidates (range q1, mask m1) u (range q2, mask m2) in `run` consecutive rows
+// starting at byte R0f, appended to the compile-time targets t[TS] (sectors), t[TL] (lines),
+// t[TS2] (sectors again); -1 = none.
+template <int TS, int TL, int TS2, class Ctx>
+__device__ __forceinline__ void row_emit(Tri (&t)[kNQ], const Ctx& X, const DField& F, unsigned long long m1, int q1,
+                                         unsigned long long m2, int q2, long long R0f, long long pystep, int run,
+                                         int le, int ls, int ll) {
+  auto gen = [&](auto&& cb) {
+    unsigned long long m = m1;
+    while (m) {
+      const int bb = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const int ty = bb >> 4, rr = bb & 15;
+      cb(X.r[q1].iv[ty][0] + F.run_lo[rr], X.r[q1].iv[ty][1] + F.run_hi[rr]);
+    }
+    m = m2;
+    while (m) {
+      const int bb = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const int ty = bb >> 4, rr = bb & 15;
+      cb(X.r[q2].iv[ty][0] + F.run_lo[rr], X.r[q2].iv[ty][1] + F.run_hi[rr]);
+    }
+  };
+  long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
+  gen([&](long long xs, long long xe) {
+    mn_s = xs < mn_s ? xs : mn_s;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  if (mn_s == LLONG_MAX) return;
+  if (mx_s <= mn_e) {
+    const long long d0 = mn_s << le, d1 = (mx_e - 1) << le;
+    for (int r = 0; r < run; ++r) {
+      const long long a0 = R0f + r * pystep + d0, a1 = R0f + r * pystep + d1;
+      if (TS >= 0) tri_add(t[TS >= 0 ? TS : 0], a0 >> ls, a1 >> ls);
+      if (TS2 >= 0) tri_add(t[TS2 >= 0 ? TS2 : 0], a0 >> ls, a1 >> ls);
+      if (TL >= 0) tri_add(t[TL >= 0 ? TL : 0], a0 >> ll, a1 >> ll);
+    }
+  } else {
+    for (int r = 0; r < run; ++r) {
+      Tri rs = tri_empty(), rl = tri_empty();
+      row_union(gen, R0f + r * pystep, le, ls, ll, &rs, &rl, nullptr);
+      if (TS >= 0) t[TS >= 0 ? TS : 0] = tri_combine(t[TS >= 0 ? TS : 0], rs);
+      if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = tri_combine(t[TS2 >= 0 ? TS2 : 0], rs);
+      if (TL >= 0) t[TL >= 0 ? TL : 0] = tri_combine(t[TL >= 0 ? TL : 0], rl);
+    }
+  }
+}
 
 // One union of a row: candidates (range q1, mask m1) u (range q2, mask m2); targets are
 // indices into the chunk triples (-1 = none).
@@ -1263,7 +1312,7 @@ struct USpec {
 // contributes count(y) - [last(y) == first(y+1)], which it can evaluate alone because row
 // y+1 of the run has the same union shifted by one row pitch.  The run's count is a plain
 // warp sum; its first / last sector come from its first / last row; runs are folded in order.
-__global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict__ plans,
+__global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restrict__ plans,
                                                          const DPrefix* __restrict__ pre, int n,
                                                          const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                                          const DRowInfo* __restrict__ rowinfo,
@@ -1303,7 +1352,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict
     __syncwarp();
     const int nb = X.nb;
     const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
-    const long long ny = RI.ny, rows = RI.ny * RI.nz;
+    const long long ny = RI.ny;
     const long long lo1 = P.lo[1], hi1 = P.hi[1], lo2 = P.lo[2], hi2 = P.hi[2], Gy = P.G[1], BF1 = P.BF[1];
     const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
     const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
@@ -1419,68 +1468,26 @@ __global__ void __launch_bounds__(kRowWarps * 32) k_rows(const DPlan* __restrict
                 }
               }
             }
-            USpec U[7];
-            int nu = 0;
+            const long long R0f = align + ((py * y + pz * z) << le);
             const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
+            // unions with compile-time targets (the triples stay in registers)
             if (noS) {
-              U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, 2, -1, 0};
+              row_emit<0, 2, -1>(t, X, F, mL[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
             } else if (noL) {
-              U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, 2, -1, 0};
+              row_emit<1, 2, -1>(t, X, F, mS[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
             } else {
-              U[nu++] = USpec{mL[0], 0ull, 0, 0, 0, -1, -1, 0};
-              U[nu++] = USpec{mS[0], 0ull, 0, 0, 1, -1, -1, 0};
-              U[nu++] = USpec{mL[0] | mS[0], 0ull, 0, 0, -1, 2, -1, 0};
+              row_emit<0, -1, -1>(t, X, F, mL[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
+              row_emit<1, -1, -1>(t, X, F, mS[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
+              row_emit<-1, 2, -1>(t, X, F, mL[0] | mS[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
             }
             if (!noL) {
-              U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, -1, 0};
-              U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, -1, 0};
-              U[nu++] = USpec{mL[3], mS[1], 3, 1, 7, -1, -1, 0};
-              U[nu++] = USpec{mL[4], mS[2], 4, 2, 8, -1, -1, 0};
+              row_emit<3, 4, -1>(t, X, F, mL[1] | mS[1], 1, 0ull, 1, R0f, pystep, run, le, ls, ll);
+              row_emit<5, 6, -1>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0f, pystep, run, le, ls, ll);
+              row_emit<7, -1, -1>(t, X, F, mL[3], 3, mS[1], 1, R0f, pystep, run, le, ls, ll);
+              row_emit<8, -1, -1>(t, X, F, mL[4], 4, mS[2], 2, R0f, pystep, run, le, ls, ll);
             } else {
-              U[nu++] = USpec{mL[1] | mS[1], 0ull, 1, 1, 3, 4, 7, 0};
-              U[nu++] = USpec{mL[2] | mS[2], 0ull, 2, 2, 5, 6, 8, 0};
-            }
-            const long long R0f = align + ((py * y + pz * z) << le);
-            for (int u = 0; u < nu; ++u) {
-              const USpec sp = U[u];
-              auto gen = [&](auto&& cb) {
-                unsigned long long m = sp.m1;
-                while (m) {
-                  const int bb = __ffsll((long long)m) - 1;
-                  m &= m - 1;
-                  const int ty = bb >> 4, rr = bb & 15;
-                  cb(X.r[sp.q1].iv[ty][0] + F.run_lo[rr], X.r[sp.q1].iv[ty][1] + F.run_hi[rr]);
-                }
-                m = sp.m2;
-                while (m) {
-                  const int bb = __ffsll((long long)m) - 1;
-                  m &= m - 1;
-                  const int ty = bb >> 4, rr = bb & 15;
-                  cb(X.r[sp.q2].iv[ty][0] + F.run_lo[rr], X.r[sp.q2].iv[ty][1] + F.run_hi[rr]);
-                }
-              };
-              long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
-              gen([&](long long xs, long long xe) {
-                mn_s = xs < mn_s ? xs : mn_s;
-                mx_s = xs > mx_s ? xs : mx_s;
-                mn_e = xe < mn_e ? xe : mn_e;
-                mx_e = xe > mx_e ? xe : mx_e;
-              });
-              if (mn_s == LLONG_MAX) continue;
-              Tri* ts = sp.ts >= 0 ? &t[sp.ts] : nullptr;
-              Tri* tl = sp.tl >= 0 ? &t[sp.tl] : nullptr;
-              Tri* ts2 = sp.ts2 >= 0 ? &t[sp.ts2] : nullptr;
-              if (mx_s <= mn_e) {
-                const long long d0 = mn_s << le, d1 = (mx_e - 1) << le;
-                for (int r = 0; r < run; ++r) {
-                  const long long R0 = R0f + r * pystep;
-                  if (ts) tri_add(*ts, (R0 + d0) >> ls, (R0 + d1) >> ls);
-                  if (ts2) tri_add(*ts2, (R0 + d0) >> ls, (R0 + d1) >> ls);
-                  if (tl) tri_add(*tl, (R0 + d0) >> ll, (R0 + d1) >> ll);
-                }
-              } else {
-                for (int r = 0; r < run; ++r) row_union(gen, R0f + r * pystep, le, ls, ll, ts, tl, ts2);
-              }
+              row_emit<3, 4, 7>(t, X, F, mL[1] | mS[1], 1, 0ull, 1, R0f, pystep, run, le, ls, ll);
+              row_emit<5, 6, 8>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0f, pystep, run, le, ls, ll);
             }
           }
           warp_ordered_reduce<kNQ>(t);
