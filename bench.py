@@ -38,7 +38,7 @@ WORKLOAD = ("BJ configs[1]: 3D-25pt r4 double stencil, grid 512^3, 168 configs "
             "(56 block shapes x {none,2y,2z} folding), A100 parameters (split L2)")
 TOPK = 10
 # algorithmic integer lane-ops per work unit
-OPS_PER_UNIT = {"k_warp": 12, "k_wclass": 12, "k_smset": 16, "k_sclass": 16, "k_rows": 42, "k_plan": 8}
+OPS_PER_UNIT = {"k_warp": 12, "k_wclass": 12, "k_smset": 16, "k_sclass": 16, "k_rows": 1, "k_plan": 8}
 
 
 def peaks():
@@ -364,7 +364,7 @@ def e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--no-cpu-baseline", action="store_true")

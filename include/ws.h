@@ -177,8 +177,9 @@ const char* ws_kernel_name(uint32_t i);   /* NULL past the last kind */
 /* Algorithmic work units each kernel kind processed in the last
  * ws_estimate[_async] call (synchronises).  Units:
  * k_warp / k_wclass: lane-instructions evaluated (32 per warp and instruction,
- * 32 per warp only classified); k_smset / k_sclass / k_rows: (address row,
- * offset group) evaluations; k_plan: (access, fold cell) pairs. */
+ * 32 per warp only classified); k_smset / k_sclass: address rows evaluated;
+ * k_rows: algorithmic integer operations (weighted per offset group, run and row);
+ * k_plan: unused (0). */
 ws_status ws_work_read(ws_ctx* ctx, uint64_t* units, uint32_t cap);
 
 #ifdef __cplusplus

@@ -1393,7 +1393,6 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
         }
       }
       Tri pt[kNQ];
-      my_rows += (unsigned long long)(lane == 0 ? ny : 0);
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) pt[q] = tri_empty();
       for (long long ys = RI.y0; ys < RI.y0 + ny; ys += kSegRows) {
@@ -1404,6 +1403,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
         for (int w = lane; w < nwd; w += 32) X.bm[w] = 0u;
         __syncwarp();
         for (int i = lane * kRunMax; i < nseg; i += 32 * kRunMax) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
+        my_rows += (unsigned long long)(lane < ng ? 8 * (nb + 2) : 0);  // breakpoint marks
         for (int g = lane; g < ng; g += 32) {
           const DGroup gr = K.g[g0 + g];
           const long long zz = z - gr.oz;
@@ -1452,6 +1452,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
           if (j < nruns) {
             const long long y = ys + X.rs[j];
             const int run = X.rs[j + 1] - X.rs[j];
+            // algorithmic int ops of this run: classification of every
+            // offset group (domain 4, two multiply-high divisions 6, block row 2, five range
+            // classifications 15, mask update 3) and 9 triple appends per row (8 each)
+            my_rows += (unsigned long long)(30 * ng + 72 * run);
             unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
             for (int g = 0; g < ng; ++g) {
               const DGroup gr = K.g[g0 + g];
