@@ -1236,7 +1236,7 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
 constexpr int kRowWarps = 8;
 
 constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
-constexpr int kRunMax = 16;     // runs are split every kRunMax rows (lane work balance)
+constexpr int kRunMax = 256;    // runs are split every kRunMax rows (lane work balance)
 
 struct WarpRowCtx {
   RangeInfo r[5];
@@ -1245,6 +1245,35 @@ struct WarpRowCtx {
   unsigned bm[kSegRows / 32];                   // run-start bitmap of the current segment
   short rs[kSegRows + 2];                       // run starts (ascending) + end
 };
+
+// Triple of `run` consecutive rows that are translates of each other by `step` bytes;
+// row(r) returns row r's own triple in units of 2^sh bytes.  Rows r and r+P (P =
+// 2^sh / gcd(step, 2^sh)) differ by exactly D = P*step >> sh units, so the run is nb full
+// periods (each the translate of rows [0,P) by D) plus the translate of rows [0, rem):
+// only the first P rows are evaluated.
+template <class RowFn>
+__device__ __forceinline__ Tri run_triple(const RowFn& row, long long step, int run, int sh) {
+  const int tz = step == 0 ? 63 : __ffsll(step) - 1;
+  const int P = sh > tz ? 1 << (sh - tz) : 1;
+  if (run <= 2 * P) {
+    Tri acc = tri_empty();
+    for (int r = 0; r < run; ++r) acc = tri_combine(acc, row(r));
+    return acc;
+  }
+  const int nb = run / P, rem = run % P;
+  const long long D = ((long long)P * step) >> sh;
+  Tri blk = tri_empty(), remb = tri_empty();
+  for (int i = 0; i < P; ++i) {
+    const Tri rt = row(i);
+    blk = tri_combine(blk, rt);
+    if (i < rem) remb = tri_combine(remb, rt);
+  }
+  if (blk.c == 0) return blk;  // every row empty
+  const long long adj = blk.l == blk.f + D ? 1 : 0;
+  Tri acc{blk.f, blk.l + (long long)(nb - 1) * D, (long long)nb * blk.c - (long long)(nb - 1) * adj};
+  if (remb.c) acc = tri_combine(acc, Tri{remb.f + (long long)nb * D, remb.l + (long long)nb * D, remb.c});
+  return acc;
+}
 
 // Union of the candidates (range q1, mask m1) u (range q2, mask m2) in `run` consecutive rows
 // starting at byte R0f, appended to the compile-time targets t[TS] (sectors), t[TL] (lines),
@@ -1277,22 +1306,37 @@ __device__ __forceinline__ void row_emit(Tri (&t)[kNQ], const Ctx& X, const DFie
     mx_e = xe > mx_e ? xe : mx_e;
   });
   if (mn_s == LLONG_MAX) return;
-  if (mx_s <= mn_e) {
-    const long long d0 = mn_s << le, d1 = (mx_e - 1) << le;
-    for (int r = 0; r < run; ++r) {
-      const long long a0 = R0f + r * pystep + d0, a1 = R0f + r * pystep + d1;
-      if (TS >= 0) tri_add(t[TS >= 0 ? TS : 0], a0 >> ls, a1 >> ls);
-      if (TS2 >= 0) tri_add(t[TS2 >= 0 ? TS2 : 0], a0 >> ls, a1 >> ls);
-      if (TL >= 0) tri_add(t[TL >= 0 ? TL : 0], a0 >> ll, a1 >> ll);
+  if (mx_s <= mn_e) {  // one interval per row
+    const long long a0 = R0f + (mn_s << le), a1 = R0f + ((mx_e - 1) << le);
+    auto rs = [&](int r) {
+      return Tri{(a0 + r * pystep) >> ls, (a1 + r * pystep) >> ls, ((a1 + r * pystep) >> ls) - ((a0 + r * pystep) >> ls) + 1};
+    };
+    auto rl = [&](int r) {
+      return Tri{(a0 + r * pystep) >> ll, (a1 + r * pystep) >> ll, ((a1 + r * pystep) >> ll) - ((a0 + r * pystep) >> ll) + 1};
+    };
+    if (TS >= 0 || TS2 >= 0) {
+      const Tri rt = run_triple(rs, pystep, run, ls);
+      if (TS >= 0) t[TS >= 0 ? TS : 0] = tri_combine(t[TS >= 0 ? TS : 0], rt);
+      if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = tri_combine(t[TS2 >= 0 ? TS2 : 0], rt);
     }
-  } else {
-    for (int r = 0; r < run; ++r) {
-      Tri rs = tri_empty(), rl = tri_empty();
-      row_union(gen, R0f + r * pystep, le, ls, ll, &rs, &rl, nullptr);
-      if (TS >= 0) t[TS >= 0 ? TS : 0] = tri_combine(t[TS >= 0 ? TS : 0], rs);
-      if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = tri_combine(t[TS2 >= 0 ? TS2 : 0], rs);
-      if (TL >= 0) t[TL >= 0 ? TL : 0] = tri_combine(t[TL >= 0 ? TL : 0], rl);
+    if (TL >= 0) t[TL >= 0 ? TL : 0] = tri_combine(t[TL >= 0 ? TL : 0], run_triple(rl, pystep, run, ll));
+  } else {  // several intervals per row (same components in every row of the run)
+    auto rs = [&](int r) {
+      Tri x = tri_empty();
+      row_union(gen, R0f + r * pystep, le, ls, ll, &x, nullptr);
+      return x;
+    };
+    auto rl = [&](int r) {
+      Tri x = tri_empty();
+      row_union(gen, R0f + r * pystep, le, ls, ll, nullptr, &x);
+      return x;
+    };
+    if (TS >= 0 || TS2 >= 0) {
+      const Tri rt = run_triple(rs, pystep, run, ls);
+      if (TS >= 0) t[TS >= 0 ? TS : 0] = tri_combine(t[TS >= 0 ? TS : 0], rt);
+      if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = tri_combine(t[TS2 >= 0 ? TS2 : 0], rt);
     }
+    if (TL >= 0) t[TL >= 0 ? TL : 0] = tri_combine(t[TL >= 0 ? TL : 0], run_triple(rl, pystep, run, ll));
   }
 }
 
