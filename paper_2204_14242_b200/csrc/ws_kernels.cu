@@ -178,6 +178,35 @@ __device__ __forceinline__ void row_union(const Gen& gen, long long R0, int lg_e
   }
 }
 
+// Triple of `run` consecutive rows that are translates of each other by `step` bytes;
+// row(r) returns row r's own triple in units of 2^sh bytes.  Rows r and r+P (P =
+// 2^sh / gcd(step, 2^sh)) differ by exactly D = P*step >> sh units, so the run is nb full
+// periods (each the translate of rows [0,P) by D) plus the translate of rows [0, rem):
+// only the first P rows are evaluated.
+template <class RowFn>
+__device__ __forceinline__ Tri run_triple(const RowFn& row, long long step, int run, int sh) {
+  const int tz = step == 0 ? 63 : __ffsll(step) - 1;
+  const int P = sh > tz ? 1 << (sh - tz) : 1;
+  if (run <= 2 * P) {
+    Tri acc = tri_empty();
+    for (int r = 0; r < run; ++r) acc = tri_combine(acc, row(r));
+    return acc;
+  }
+  const int nb = run / P, rem = run % P;
+  const long long D = ((long long)P * step) >> sh;
+  Tri blk = tri_empty(), remb = tri_empty();
+  for (int i = 0; i < P; ++i) {
+    const Tri rt = row(i);
+    blk = tri_combine(blk, rt);
+    if (i < rem) remb = tri_combine(remb, rt);
+  }
+  if (blk.c == 0) return blk;  // every row empty
+  const long long adj = blk.l == blk.f + D ? 1 : 0;
+  Tri acc{blk.f, blk.l + (long long)(nb - 1) * D, (long long)nb * blk.c - (long long)(nb - 1) * adj};
+  if (remb.c) acc = tri_combine(acc, Tri{remb.f + (long long)nb * D, remb.l + (long long)nb * D, remb.c});
+  return acc;
+}
+
 template <int MEMBER>
 __device__ __forceinline__ int find_config(const DPrefix* pre, int n, long long item) {
   // largest c in [0, n) with pre[c].member <= item (pre is an exclusive prefix)
@@ -928,6 +957,7 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
 }
 
 constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
+constexpr int kSegRowsS = 1024;  // rows of a plane per SM-set run segment
 
 // Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
 // dispatch, Q9) by one CTA.  Row (y,z) of field phi holds element x iff some member box
@@ -936,8 +966,13 @@ constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
 // that plane by whole lines (derived); otherwise a warp computes it, lanes taking rows
 // (per row: compares against the member boxes into a candidate mask, union, triple), with an
 // ordered warp reduction.  Thread 0 folds the plane triples in z order.
+struct SmWarp {
+  unsigned bm[kSegRowsS / 32];
+  short rs[kSegRowsS + 2];
+};
+
 __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
-                          SmBox* mb, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */,
+                          SmBox* mb, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */, SmWarp* sw,
                           unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwp = blockDim.x >> 5;
   const int ls = G.lg_sector, ll = G.lg_line;
@@ -977,7 +1012,7 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
     if (y1 <= y0 || z1 <= z0) continue;
     const long long ny = y1 - y0;
     const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
-    const long long pbytes = pz << le;
+    const long long pbytes = pz << le, pystep = py << le;
     const int per = plane_period(pz, le, ll);
     const int npairs = ng * nm;
     Tri cs_all = tri_empty(), cl_all = tri_empty();
@@ -1000,60 +1035,127 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
         if (lane == 0) pder[p] = same ? 1 : 0;
       }
       __syncthreads();
-      // (b) computed planes: one warp per plane, lanes over rows
+      // (b) computed planes: one warp per plane.  A row's candidates change only where some
+      //     y - oy crosses a member's y edge: lanes mark these breakpoints, then take one run
+      //     each (candidates of its first row, union, closed-form run triple).
       for (int p = wid; p < np; p += nwp) {
         if (pder[p]) continue;
         const long long z = zs + p;
-        Tri carry_s = tri_empty(), carry_l = tri_empty();
-        for (long long yb = 0; yb < ny; yb += 32) {
-          Tri t[2] = {tri_empty(), tri_empty()};
-          const long long y = y0 + yb + lane;
-          if (y < y1) {
-            const long long R0 = align + ((py * y + pz * z) << le);
-            if (nm <= 4) {
-              unsigned long long mk = 0;
+        SmWarp& Wp = sw[wid];
+        Tri ps = tri_empty(), pl = tri_empty();
+        for (long long ys = y0; ys < y1; ys += kSegRowsS) {
+          const int nseg = (int)(y1 - ys < kSegRowsS ? y1 - ys : kSegRowsS);
+          const int nwd = (nseg + 31) >> 5;
+          for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
+          __syncwarp();
+          if (lane == 0) atomicOr(&Wp.bm[0], 1u);
+          for (int k = lane; k < npairs; k += 32) {
+            const DGroup gr = K.g[g0 + k / nm];
+            if (gr.kind != 0) continue;
+            const SmBox& bx = mb[k % nm];
+            const long long zz = z - gr.oz;
+            if (zz < bx.z0 || zz >= bx.z1) continue;
+            const long long e0 = bx.y0 + gr.oy - ys, e1 = bx.y1 + gr.oy - ys;
+            if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
+            if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
+          }
+          __syncwarp();
+          const int wpl = (nwd + 31) >> 5;
+          int cnt = 0;
+          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(Wp.bm[w]);
+          int pos = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, pos, o);
+            if (lane >= o) pos += v;
+          }
+          const int nruns = __shfl_sync(FULL, pos, 31);
+          pos -= cnt;
+          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
+            unsigned bits = Wp.bm[w];
+            while (bits) {
+              const int bt = __ffs(bits) - 1;
+              bits &= bits - 1;
+              Wp.rs[pos++] = (short)(w * 32 + bt);
+            }
+          }
+          if (lane == 0) Wp.rs[nruns] = (short)nseg;
+          __syncwarp();
+          for (int rb = 0; rb < nruns; rb += 32) {
+            Tri t[2] = {tri_empty(), tri_empty()};
+            const int j = rb + lane;
+            if (j < nruns) {
+              const long long y = ys + Wp.rs[j];
+              const int run = Wp.rs[j + 1] - Wp.rs[j];
+              const long long R0f = align + ((py * y + pz * z) << le);
+              unsigned long long mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
               for (int g = 0; g < ng; ++g) {
                 const DGroup gr = K.g[g0 + g];
                 if (gr.kind != 0) continue;
                 const long long yy = y - gr.oy, zz = z - gr.oz;
+#pragma unroll 4
                 for (int m = 0; m < nm; ++m) {
                   const SmBox& bx = mb[m];
-                  if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1) mk |= 1ull << (m * 16 + gr.run);
+                  if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
+                    mk[m >> 2] |= 1ull << ((m & 3) * 16 + gr.run);
                 }
               }
               auto gen = [&](auto&& cb) {
-                unsigned long long q = mk;
-                while (q) {
-                  const int bb = __ffsll((long long)q) - 1;
-                  q &= q - 1;
-                  const SmBox& bx = mb[bb >> 4];
-                  cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
-                }
-              };
-              row_union(gen, R0, le, ls, ll, &t[0], &t[1]);
-            } else {
-              auto gen = [&](auto&& cb) {
-                for (int g = 0; g < ng; ++g) {
-                  const DGroup gr = K.g[g0 + g];
-                  if (gr.kind != 0) continue;
-                  const long long yy = y - gr.oy, zz = z - gr.oz;
-                  for (int m = 0; m < nm; ++m) {
-                    const SmBox& bx = mb[m];
-                    if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
-                      cb(bx.x0 + F.run_lo[gr.run], bx.x1 + F.run_hi[gr.run]);
+                for (int w = 0; w < ((nm + 3) >> 2); ++w) {
+                  unsigned long long q = mk[w];
+                  while (q) {
+                    const int bb = __ffsll((long long)q) - 1;
+                    q &= q - 1;
+                    const SmBox& bx = mb[w * 4 + (bb >> 4)];
+                    cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
                   }
                 }
               };
-              row_union(gen, R0, le, ls, ll, &t[0], &t[1]);
+              long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
+              gen([&](long long xs, long long xe) {
+                mn_s = xs < mn_s ? xs : mn_s;
+                mx_s = xs > mx_s ? xs : mx_s;
+                mn_e = xe < mn_e ? xe : mn_e;
+                mx_e = xe > mx_e ? xe : mx_e;
+              });
+              if (mn_s != LLONG_MAX) {
+                if (mx_s <= mn_e) {
+                  const long long a0 = R0f + (mn_s << le), a1 = R0f + ((mx_e - 1) << le);
+                  auto rs_ = [&](int r) {
+                    const long long s0 = (a0 + r * pystep) >> ls, s1 = (a1 + r * pystep) >> ls;
+                    return Tri{s0, s1, s1 - s0 + 1};
+                  };
+                  auto rl_ = [&](int r) {
+                    const long long s0 = (a0 + r * pystep) >> ll, s1 = (a1 + r * pystep) >> ll;
+                    return Tri{s0, s1, s1 - s0 + 1};
+                  };
+                  t[0] = run_triple(rs_, pystep, run, ls);
+                  t[1] = run_triple(rl_, pystep, run, ll);
+                } else {
+                  auto rs_ = [&](int r) {
+                    Tri x = tri_empty();
+                    row_union(gen, R0f + r * pystep, le, ls, ll, &x, nullptr);
+                    return x;
+                  };
+                  auto rl_ = [&](int r) {
+                    Tri x = tri_empty();
+                    row_union(gen, R0f + r * pystep, le, ls, ll, nullptr, &x);
+                    return x;
+                  };
+                  t[0] = run_triple(rs_, pystep, run, ls);
+                  t[1] = run_triple(rl_, pystep, run, ll);
+                }
+              }
             }
+            warp_ordered_reduce<2>(t);
+            ps = tri_combine(ps, Tri{shfl64(t[0].f, 0), shfl64(t[0].l, 0), shfl64(t[0].c, 0)});
+            pl = tri_combine(pl, Tri{shfl64(t[1].f, 0), shfl64(t[1].l, 0), shfl64(t[1].c, 0)});
           }
-          warp_ordered_reduce<2>(t);
-          carry_s = tri_combine(carry_s, Tri{shfl64(t[0].f, 0), shfl64(t[0].l, 0), shfl64(t[0].c, 0)});
-          carry_l = tri_combine(carry_l, Tri{shfl64(t[1].f, 0), shfl64(t[1].l, 0), shfl64(t[1].c, 0)});
+          __syncwarp();
         }
         if (lane == 0) {
-          pt[2 * p] = carry_s;
-          pt[2 * p + 1] = carry_l;
+          pt[2 * p] = ps;
+          pt[2 * p + 1] = pl;
           units += (unsigned long long)ny;
         }
       }
@@ -1130,6 +1232,7 @@ __global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans,
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ Tri s_pt[2 * kMaxPlanes];
   __shared__ unsigned char s_der[kMaxPlanes];
+  __shared__ SmWarp s_sw[8];
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
@@ -1156,11 +1259,11 @@ __global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans,
       kj = (P.W - (long long)low + nsm - 1) / nsm;
     }
     unsigned long long ss, sl, un;
-    if (kj == 1) {
+    if (kj == 1) {  // one block: small box, flat rows over the whole CTA
       smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
       if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
-    } else {
-      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_pt, s_der, ss, sl, un);
+    } else {        // several blocks: plane derivation + runs
+      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_pt, s_der, s_sw, ss, sl, un);
       // every warp's lane 0 counted its planes' rows
       if ((threadIdx.x & 31) == 0 && un) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     }
@@ -1245,35 +1348,6 @@ struct WarpRowCtx {
   unsigned bm[kSegRows / 32];                   // run-start bitmap of the current segment
   short rs[kSegRows + 2];                       // run starts (ascending) + end
 };
-
-// Triple of `run` consecutive rows that are translates of each other by `step` bytes;
-// row(r) returns row r's own triple in units of 2^sh bytes.  Rows r and r+P (P =
-// 2^sh / gcd(step, 2^sh)) differ by exactly D = P*step >> sh units, so the run is nb full
-// periods (each the translate of rows [0,P) by D) plus the translate of rows [0, rem):
-// only the first P rows are evaluated.
-template <class RowFn>
-__device__ __forceinline__ Tri run_triple(const RowFn& row, long long step, int run, int sh) {
-  const int tz = step == 0 ? 63 : __ffsll(step) - 1;
-  const int P = sh > tz ? 1 << (sh - tz) : 1;
-  if (run <= 2 * P) {
-    Tri acc = tri_empty();
-    for (int r = 0; r < run; ++r) acc = tri_combine(acc, row(r));
-    return acc;
-  }
-  const int nb = run / P, rem = run % P;
-  const long long D = ((long long)P * step) >> sh;
-  Tri blk = tri_empty(), remb = tri_empty();
-  for (int i = 0; i < P; ++i) {
-    const Tri rt = row(i);
-    blk = tri_combine(blk, rt);
-    if (i < rem) remb = tri_combine(remb, rt);
-  }
-  if (blk.c == 0) return blk;  // every row empty
-  const long long adj = blk.l == blk.f + D ? 1 : 0;
-  Tri acc{blk.f, blk.l + (long long)(nb - 1) * D, (long long)nb * blk.c - (long long)(nb - 1) * adj};
-  if (remb.c) acc = tri_combine(acc, Tri{remb.f + (long long)nb * D, remb.l + (long long)nb * D, remb.c});
-  return acc;
-}
 
 // Union of the candidates (range q1, mask m1) u (range q2, mask m2) in `run` consecutive rows
 // starting at byte R0f, appended to the compile-time targets t[TS] (sectors), t[TL] (lines),
