@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -420,8 +421,10 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   cudaEvent_t* ev = c->profiling ? c->take_events(K_PLAN, kEstimateKernels) : nullptr;
   Streams st;
   st.main = c->stream;
-  st.aux[0] = c->aux[0];
-  st.aux[1] = c->aux[1];
+  // WS_SERIAL=1 (diagnostics): every chain on the context stream -> uncontended kernel times
+  static const bool serial = getenv("WS_SERIAL") && getenv("WS_SERIAL")[0] == '1';
+  st.aux[0] = serial ? c->stream : c->aux[0];
+  st.aux[1] = serial ? c->stream : c->aux[1];
   st.fork = c->fork;
   st.join[0] = c->join[0];
   st.join[1] = c->join[1];
