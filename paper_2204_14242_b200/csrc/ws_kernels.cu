@@ -1337,6 +1337,7 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
 }
 
 constexpr int kRowWarps = 8;
+constexpr int kItemBlock = 1;   // consecutive planes per warp iteration in k_rows (computed planes cluster: keep 1)
 
 constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
 constexpr int kRunMax = 256;    // runs are split every kRunMax rows (lane work balance)
@@ -1442,8 +1443,15 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
   const long long total = pre[n].chunk;
   const long long nwg = (long long)gridDim.x * kRowWarps;
   unsigned long long my_rows = 0;
-  for (long long item = (long long)blockIdx.x * kRowWarps + wid; item < total; item += nwg) {
-    const int c = find_config<4>(pre, n, item);
+  // each warp takes blocks of kItemBlock consecutive planes: one config search per block, the
+  // config's ranges copied to shared memory only when a plane has to be computed
+  for (long long base = ((long long)blockIdx.x * kRowWarps + wid) * kItemBlock; base < total;
+       base += nwg * kItemBlock) {
+   const long long bend = base + kItemBlock < total ? base + kItemBlock : total;
+   int c = find_config<4>(pre, n, base);
+   int ranges_c = -1;
+   for (long long item = base; item < bend; ++item) {
+    while (c + 1 < n && pre[c + 1].chunk <= item) ++c;
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
@@ -1459,16 +1467,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const DField& F = K.f[fi];
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
-    __syncwarp();
-    {  // ranges and zone boundaries of this config (k_plan) -> warp smem
-      const long long* src = reinterpret_cast<const long long*>(&P.rng[0]);
-      long long* dst = reinterpret_cast<long long*>(&X);
-      constexpr int nw64 = (int)((sizeof(RangeInfo) * 5 + sizeof(long long) * 20) / 8);
-      for (int k = lane; k < nw64; k += 32) dst[k] = src[k];
-      if (lane == 0) X.nb = P.nb;
-    }
-    __syncwarp();
-    const int nb = X.nb;
+    const int nb = P.nb;
     const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
     const long long ny = RI.ny;
     const long long lo1 = P.lo[1], hi1 = P.hi[1], lo2 = P.lo[2], hi2 = P.hi[2], Gy = P.G[1], BF1 = P.BF[1];
@@ -1509,6 +1508,15 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
           if (lane == 0) chunkres[(pre[c].chunk + ci) * (kNQ * 3) + 2] = -(rep - RI.z0) - 2;
           continue;
         }
+      }
+      if (ranges_c != c) {  // ranges and zone boundaries of this config (k_plan) -> warp smem
+        __syncwarp();
+        const long long* src = reinterpret_cast<const long long*>(&P.rng[0]);
+        long long* dst = reinterpret_cast<long long*>(&X);
+        constexpr int nw64 = (int)((sizeof(RangeInfo) * 5 + sizeof(long long) * 20) / 8);
+        for (int k = lane; k < nw64; k += 32) dst[k] = src[k];
+        __syncwarp();
+        ranges_c = c;
       }
       Tri pt[kNQ];
 #pragma unroll
@@ -1631,6 +1639,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
         }
       }
     }
+   }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) my_rows += __shfl_down_sync(FULL, my_rows, o);
