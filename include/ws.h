@@ -58,7 +58,8 @@ ws_status ws_set_stream(ws_ctx* ctx, void* cuda_stream);
  *   align_bytes + elem_bytes * (x*pitch[0] + y*pitch[1] + z*pitch[2])
  * (P:157-161 with the unknown base pointer replaced by the alignment).
  * Requirements: pitch[0] == 1, pitch[1] >= extent[0], pitch[2] >= pitch[1]*extent[1]
- * (rows and planes never overlap); elem_bytes in {1,2,4,8,16,32}.  */
+ * (rows and planes never overlap); elem_bytes in {1,2,4,8,16,32}; one z-plane
+ * (pitch[2] * elem_bytes) smaller than 2 GiB (WS_ELIMIT).  */
 typedef struct {
   int64_t extent[3];
   int64_t pitch[3];
@@ -87,7 +88,8 @@ typedef struct {
 
 /* Deep-copies the description.  Errors: WS_EINVAL (counts, layout, elem,
  * empty domain), WS_EBOUNDS (dom +- offsets leaves a field), WS_ELIMIT (a
- * field has more than 16 distinct x-offset runs).  *kernel_id receives a new id. */
+ * field has more than 16 distinct x-offset runs, or a z-plane >= 2 GiB).
+ * *kernel_id receives a new id. */
 ws_status ws_describe_kernel(ws_ctx* ctx, const ws_kernel* k, uint32_t* kernel_id);
 
 /* ------------------------------------------------------------------ hardware

@@ -298,6 +298,8 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
       if (F.extent[d] < 1) return fail(c, WS_EINVAL, "field extent < 1");
     if (F.pitch[0] != 1 || F.pitch[1] < F.extent[0] || F.pitch[2] < F.pitch[1] * F.extent[1])
       return fail(c, WS_EINVAL, "layout: need pitch[0]==1, pitch[1]>=extent[0], pitch[2]>=pitch[1]*extent[1]");
+    if ((F.pitch[2] * (int64_t)F.elem_bytes) >= (int64_t(1) << 31) || F.extent[2] >= (int64_t(1) << 31))
+      return fail(c, WS_ELIMIT, "a z-plane of a field must be smaller than 2 GiB");
     for (int d = 0; d < 3; ++d) {
       G.ext[d] = F.extent[d];
       G.pitch[d] = F.pitch[d];

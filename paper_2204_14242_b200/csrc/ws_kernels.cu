@@ -1337,26 +1337,140 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
 }
 
 constexpr int kRowWarps = 8;
-constexpr int kItemBlock = 1;   // consecutive planes per warp iteration in k_rows (computed planes cluster: keep 1)
 
 constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
 constexpr int kRunMax = 256;    // runs are split every kRunMax rows (lane work balance)
 
-struct WarpRowCtx {
-  RangeInfo r[5];
-  long long bnd[20];  // sorted distinct block rows where some range's classification zone starts
-  int nb, pad;
-  unsigned bm[kSegRows / 32];                   // run-start bitmap of the current segment
-  short rs[kSegRows + 2];                       // run starts (ascending) + end
+// ---- 32-bit plane-relative arithmetic for k_rows ---------------------------------------------
+// Every address of one z-plane of a field is R0p + rel with R0p the address of the plane's first
+// box row and 0 <= rel < 2^31 (describe-time limit: pitch[2] * elem_bytes < 2^31).  Sectors and
+// lines are counted relative to B = floor(R0p / line_bytes) * line_bytes, a multiple of both unit
+// sizes: unit(R0p + rel) = (B >> sh) + ((off0 + rel) >> sh) with off0 = R0p - B < line_bytes.
+struct T32 {
+  int f, l, c;  // first, last, count; c == 0: empty
+};
+__device__ __forceinline__ T32 t32_empty() { return T32{0, 0, 0}; }
+__device__ __forceinline__ void t32_add(T32& t, int s0, int s1) {
+  if (t.c == 0) {
+    t.f = s0;
+    t.c = s1 - s0 + 1;
+  } else {
+    t.c += s1 - s0 + 1 - (t.l == s0 ? 1 : 0);
+  }
+  t.l = s1;
+}
+__device__ __forceinline__ T32 t32_combine(const T32& a, const T32& b) {
+  if (a.c == 0) return b;
+  if (b.c == 0) return a;
+  return T32{a.f, b.l, a.c + b.c - (a.l == b.f ? 1 : 0)};
+}
+
+// union of the intervals [xs, xe) produced by gen, in the row starting at plane offset R
+template <class Gen>
+__device__ __forceinline__ void row_union32(const Gen& gen, int R, int le, int sh, T32& t) {
+  const int INF = 0x7fffffff;
+  int start = INF, mx_s = -INF, mn_e = INF, mx_e = -INF;
+  gen([&](int xs, int xe) {
+    start = xs < start ? xs : start;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  if (start == INF) return;
+  if (mx_s <= mn_e) {
+    t32_add(t, (R + (start << le)) >> sh, (R + ((mx_e - 1) << le)) >> sh);
+    return;
+  }
+  while (start != INF) {
+    int end = start, nxt;
+    bool grew;
+    do {
+      grew = false;
+      nxt = INF;
+      gen([&](int xs, int xe) {
+        if (xs <= end) {
+          if (xe > end) {
+            end = xe;
+            grew = true;
+          }
+        } else if (xs < nxt) {
+          nxt = xs;
+        }
+      });
+    } while (grew);
+    t32_add(t, (R + (start << le)) >> sh, (R + ((end - 1) << le)) >> sh);
+    start = nxt;
+  }
+}
+
+// run_triple (above) in 32-bit: rows r and r+P are translates by D = P*step >> sh units
+template <class RowFn>
+__device__ __forceinline__ T32 run_triple32(const RowFn& row, int step, int run, int sh) {
+  const int tz = step == 0 ? 31 : __ffs(step) - 1;
+  const int P = sh > tz ? 1 << (sh - tz) : 1;
+  if (run <= 2 * P) {
+    T32 acc = t32_empty();
+    for (int r = 0; r < run; ++r) acc = t32_combine(acc, row(r));
+    return acc;
+  }
+  const int nb = run / P, rem = run % P;
+  const int D = (P * step) >> sh;
+  T32 blk = t32_empty(), remb = t32_empty();
+  for (int i = 0; i < P; ++i) {
+    const T32 rt = row(i);
+    blk = t32_combine(blk, rt);
+    if (i < rem) remb = t32_combine(remb, rt);
+  }
+  if (blk.c == 0) return blk;
+  const int adj = blk.l == blk.f + D ? 1 : 0;
+  T32 acc{blk.f, blk.l + (nb - 1) * D, nb * blk.c - (nb - 1) * adj};
+  if (remb.c) acc = t32_combine(acc, T32{remb.f + nb * D, remb.l + nb * D, remb.c});
+  return acc;
+}
+
+struct RI32 {
+  int ra, rl;
+  int iv[4][2];
+  int nonempty, pad;
 };
 
-// Union of the candidates (range q1, mask m1) u (range q2, mask m2) in `run` consecutive rows
-// starting at byte R0f, appended to the compile-time targets t[TS] (sectors), t[TL] (lines),
-// t[TS2] (sectors again); -1 = none.
-template <int TS, int TL, int TS2, class Ctx>
-__device__ __forceinline__ void row_emit(Tri (&t)[kNQ], const Ctx& X, const DField& F, unsigned long long m1, int q1,
-                                         unsigned long long m2, int q2, long long R0f, long long pystep, int run,
-                                         int le, int ls, int ll) {
+__device__ __forceinline__ int classify32(const RI32& R, int r) {
+  if (!R.nonempty || r < R.ra || r > R.rl) return -1;
+  if (R.ra == R.rl) return 3;
+  if (r == R.ra) return 1;
+  if (r == R.rl) return 2;
+  return 0;
+}
+
+struct WarpRowCtx {
+  RI32 r[5];
+  int bnd[20];  // sorted distinct block rows where some range's classification zone starts
+  int nb, pad;
+  unsigned bm[kSegRows / 32];  // run-start bitmap of the current segment
+  short rs[kSegRows + 2];      // run starts (ascending) + end
+};
+
+template <int NQ>
+__device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const T32 x{__shfl_down_sync(FULL, t[q].f, o), __shfl_down_sync(FULL, t[q].l, o),
+                  __shfl_down_sync(FULL, t[q].c, o)};
+      if (lane + o < 32) t[q] = t32_combine(t[q], x);
+    }
+  }
+}
+
+// Union of the candidates (range q1, mask m1) u (range q2, mask m2) over `run` consecutive rows
+// (row 0 at plane offset R0, rows `step` bytes apart), appended to the compile-time targets
+// t[TS] (sectors), t[TL] (lines), t[TS2] (sectors again); -1 = none.
+template <int TS, int TL, int TS2>
+__device__ __forceinline__ void row_emit32(T32 (&t)[kNQ], const WarpRowCtx& X, const DField& F, unsigned long long m1,
+                                           int q1, unsigned long long m2, int q2, int R0, int step, int run, int le,
+                                           int ls, int ll) {
   auto gen = [&](auto&& cb) {
     unsigned long long m = m1;
     while (m) {
@@ -1373,85 +1487,76 @@ __device__ __forceinline__ void row_emit(Tri (&t)[kNQ], const Ctx& X, const DFie
       cb(X.r[q2].iv[ty][0] + F.run_lo[rr], X.r[q2].iv[ty][1] + F.run_hi[rr]);
     }
   };
-  long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
-  gen([&](long long xs, long long xe) {
+  const int INF = 0x7fffffff;
+  int mn_s = INF, mx_s = -INF, mn_e = INF, mx_e = -INF;
+  gen([&](int xs, int xe) {
     mn_s = xs < mn_s ? xs : mn_s;
     mx_s = xs > mx_s ? xs : mx_s;
     mn_e = xe < mn_e ? xe : mn_e;
     mx_e = xe > mx_e ? xe : mx_e;
   });
-  if (mn_s == LLONG_MAX) return;
+  if (mn_s == INF) return;
+  T32 ts = t32_empty(), tl = t32_empty();
   if (mx_s <= mn_e) {  // one interval per row
-    const long long a0 = R0f + (mn_s << le), a1 = R0f + ((mx_e - 1) << le);
-    auto rs = [&](int r) {
-      return Tri{(a0 + r * pystep) >> ls, (a1 + r * pystep) >> ls, ((a1 + r * pystep) >> ls) - ((a0 + r * pystep) >> ls) + 1};
-    };
-    auto rl = [&](int r) {
-      return Tri{(a0 + r * pystep) >> ll, (a1 + r * pystep) >> ll, ((a1 + r * pystep) >> ll) - ((a0 + r * pystep) >> ll) + 1};
-    };
-    if (TS >= 0 || TS2 >= 0) {
-      const Tri rt = run_triple(rs, pystep, run, ls);
-      if (TS >= 0) t[TS >= 0 ? TS : 0] = tri_combine(t[TS >= 0 ? TS : 0], rt);
-      if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = tri_combine(t[TS2 >= 0 ? TS2 : 0], rt);
-    }
-    if (TL >= 0) t[TL >= 0 ? TL : 0] = tri_combine(t[TL >= 0 ? TL : 0], run_triple(rl, pystep, run, ll));
-  } else {  // several intervals per row (same components in every row of the run)
-    auto rs = [&](int r) {
-      Tri x = tri_empty();
-      row_union(gen, R0f + r * pystep, le, ls, ll, &x, nullptr);
-      return x;
-    };
-    auto rl = [&](int r) {
-      Tri x = tri_empty();
-      row_union(gen, R0f + r * pystep, le, ls, ll, nullptr, &x);
-      return x;
-    };
-    if (TS >= 0 || TS2 >= 0) {
-      const Tri rt = run_triple(rs, pystep, run, ls);
-      if (TS >= 0) t[TS >= 0 ? TS : 0] = tri_combine(t[TS >= 0 ? TS : 0], rt);
-      if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = tri_combine(t[TS2 >= 0 ? TS2 : 0], rt);
-    }
-    if (TL >= 0) t[TL >= 0 ? TL : 0] = tri_combine(t[TL >= 0 ? TL : 0], run_triple(rl, pystep, run, ll));
+    const int a0 = R0 + (mn_s << le), a1 = R0 + ((mx_e - 1) << le);
+    if (TS >= 0 || TS2 >= 0)
+      ts = run_triple32([&](int r) {
+        const int s0 = (a0 + r * step) >> ls, s1 = (a1 + r * step) >> ls;
+        return T32{s0, s1, s1 - s0 + 1};
+      }, step, run, ls);
+    if (TL >= 0)
+      tl = run_triple32([&](int r) {
+        const int s0 = (a0 + r * step) >> ll, s1 = (a1 + r * step) >> ll;
+        return T32{s0, s1, s1 - s0 + 1};
+      }, step, run, ll);
+  } else {  // several intervals per row (the same components in every row of the run)
+    if (TS >= 0 || TS2 >= 0)
+      ts = run_triple32([&](int r) {
+        T32 x = t32_empty();
+        row_union32(gen, R0 + r * step, le, ls, x);
+        return x;
+      }, step, run, ls);
+    if (TL >= 0)
+      tl = run_triple32([&](int r) {
+        T32 x = t32_empty();
+        row_union32(gen, R0 + r * step, le, ll, x);
+        return x;
+      }, step, run, ll);
   }
+  if (TS >= 0) t[TS >= 0 ? TS : 0] = t32_combine(t[TS >= 0 ? TS : 0], ts);
+  if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = t32_combine(t[TS2 >= 0 ? TS2 : 0], ts);
+  if (TL >= 0) t[TL >= 0 ? TL : 0] = t32_combine(t[TL >= 0 ? TL : 0], tl);
 }
 
-// One union of a row: candidates (range q1, mask m1) u (range q2, mask m2); targets are
-// indices into the chunk triples (-1 = none).
-struct USpec {
-  unsigned long long m1, m2;
-  int q1, q2, ts, tl, ts2, pad;
-};
+__device__ __forceinline__ int fdiv32(int n, FDiv f) { return (int)((__umulhi((unsigned)n, f.m) + (unsigned)n) >> f.l); }
 
-// One warp per chunk of 1024 address rows of one (config, field).  The chunk is cut into
-// runs of consecutive rows whose candidate masks are identical: a row's masks change only
-// where some offset group's region row enters another classification zone (the 5 ranges'
-// first / second / last / after-last block rows) or leaves / enters the domain, or at a
-// z-plane end.  Per run the masks are computed once (lanes split the offset groups), the
-// unions once (every lane), then the lanes take the run's rows 32 at a time: row y
-// contributes count(y) - [last(y) == first(y+1)], which it can evaluate alone because row
-// y+1 of the run has the same union shifted by one row pitch.  The run's count is a plain
-// warp sum; its first / last sector come from its first / last row; runs are folded in order.
+// One warp per (config, field, z-plane) of the row box of the wave + layer-set footprint.
+//  * Plane derivation: a plane whose every offset group falls in the same block layer (or the
+//    same side outside the domain) as its representative (start of that zone segment, aligned
+//    to the reuse period per) is that plane's translate by whole lines: only marked here,
+//    translated by k_fold.
+//  * Computed planes: a row's candidate masks change only where some offset group's region row
+//    enters another classification zone (the 5 ranges' first / second / last / after-last block
+//    rows) or the domain.  Lanes mark these breakpoints in a bitmap, compact the run starts, then
+//    take one run each: masks of its first row, the <= 7 unions, the run's triple in closed form
+//    (rows of a run are translates).  An ordered warp reduction of the lanes' 9 triples gives the
+//    plane's contribution.  All of it in 32-bit plane-relative arithmetic.
 __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restrict__ plans,
-                                                         const DPrefix* __restrict__ pre, int n,
-                                                         const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
-                                                         const DRowInfo* __restrict__ rowinfo,
-                                                         long long* __restrict__ chunkres,
-                                                         unsigned long long* __restrict__ work) {
+                                                            const DPrefix* __restrict__ pre, int n,
+                                                            const DKernel* __restrict__ ks,
+                                                            const DGpu* __restrict__ gs,
+                                                            const DRowInfo* __restrict__ rowinfo,
+                                                            long long* __restrict__ chunkres,
+                                                            unsigned long long* __restrict__ work) {
   __shared__ WarpRowCtx s_ctx[kRowWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRowCtx& X = s_ctx[wid];
   const long long total = pre[n].chunk;
   const long long nwg = (long long)gridDim.x * kRowWarps;
-  unsigned long long my_rows = 0;
-  // each warp takes blocks of kItemBlock consecutive planes: one config search per block, the
-  // config's ranges copied to shared memory only when a plane has to be computed
-  for (long long base = ((long long)blockIdx.x * kRowWarps + wid) * kItemBlock; base < total;
-       base += nwg * kItemBlock) {
-   const long long bend = base + kItemBlock < total ? base + kItemBlock : total;
-   int c = find_config<4>(pre, n, base);
-   int ranges_c = -1;
-   for (long long item = base; item < bend; ++item) {
-    while (c + 1 < n && pre[c + 1].chunk <= item) ++c;
+  unsigned long long my_ops = 0;
+  int ranges_c = -1;
+  for (long long item = (long long)blockIdx.x * kRowWarps + wid; item < total; item += nwg) {
+    const int c = find_config<4>(pre, n, item);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
@@ -1467,183 +1572,173 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const DField& F = K.f[fi];
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
-    const int nb = P.nb;
     const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
-    const long long ny = RI.ny;
-    const long long lo1 = P.lo[1], hi1 = P.hi[1], lo2 = P.lo[2], hi2 = P.hi[2], Gy = P.G[1], BF1 = P.BF[1];
+    const int lo1 = (int)P.lo[1], hi1 = (int)P.hi[1], lo2 = (int)P.lo[2], hi2 = (int)P.hi[2];
+    const int Gy = (int)P.G[1], BF1 = (int)P.BF[1], BF2 = (int)P.BF[2];
     const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
-    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
-    const long long pystep = py << le;
-    Tri carry[kNQ];
-#pragma unroll
-    for (int q = 0; q < kNQ; ++q) carry[q] = tri_empty();
-    // planes of this chunk
-    const long long zc0 = RI.z0 + (ci - RI.chunk_begin) * RI.ppc;
-    long long zc1 = zc0 + RI.ppc;
-    if (zc1 > RI.z0 + RI.nz) zc1 = RI.z0 + RI.nz;
-    // plane reuse period: smallest power of two k with k*pz*elem a multiple of line_bytes
+    const int y0 = (int)RI.y0, ny = (int)RI.ny;
+    const int z = (int)(RI.z0 + (ci - RI.chunk_begin));  // one plane per chunk (ppc == 1)
+    const long long py = F.pitch[1], pz = F.pitch[2];
     const int per = plane_period(pz, le, ll);
-    for (long long z = zc0; z < zc1; ++z) {
-      // Planes whose every offset group falls in the same block layer (or the same side outside
-      // the domain) have identical row structure.  The segment of such planes containing z
-      // starts at the latest layer / domain edge crossed by some group; its plane congruent to
-      // z mod per is the representative, of which z is the translate by whole lines.
-      if (per > 0) {
-        long long seg = RI.z0;
-        for (int g = lane; g < ng; g += 32) {
-          const long long oz = K.g[g0 + g].oz, zz = z - oz;
-          long long st;
-          if (zz < lo2) st = LLONG_MIN;
-          else if (zz >= hi2) st = hi2 + oz;
-          else st = lo2 + fdiv(zz - lo2, fdz) * P.BF[2] + oz;
-          seg = st > seg ? st : seg;
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          const long long v = shfl64(seg, (lane + o) & 31);
-          seg = v > seg ? v : seg;
-        }
-        const long long rep = seg + ((z - seg) % per);
-        if (rep != z) {
-          if (lane == 0) chunkres[(pre[c].chunk + ci) * (kNQ * 3) + 2] = -(rep - RI.z0) - 2;
-          continue;
-        }
+    if (per > 0) {
+      int seg = (int)RI.z0;
+      for (int g = lane; g < ng; g += 32) {
+        const int oz = K.g[g0 + g].oz, zz = z - oz;
+        int st;
+        if (zz < lo2) st = -0x7fffffff;
+        else if (zz >= hi2) st = hi2 + oz;
+        else st = lo2 + fdiv32(zz - lo2, fdz) * BF2 + oz;
+        seg = st > seg ? st : seg;
       }
-      if (ranges_c != c) {  // ranges and zone boundaries of this config (k_plan) -> warp smem
-        __syncwarp();
-        const long long* src = reinterpret_cast<const long long*>(&P.rng[0]);
-        long long* dst = reinterpret_cast<long long*>(&X);
-        constexpr int nw64 = (int)((sizeof(RangeInfo) * 5 + sizeof(long long) * 20) / 8);
-        for (int k = lane; k < nw64; k += 32) dst[k] = src[k];
-        __syncwarp();
-        ranges_c = c;
-      }
-      Tri pt[kNQ];
-#pragma unroll
-      for (int q = 0; q < kNQ; ++q) pt[q] = tri_empty();
-      for (long long ys = RI.y0; ys < RI.y0 + ny; ys += kSegRows) {
-        const int nseg = (int)(RI.y0 + ny - ys < kSegRows ? RI.y0 + ny - ys : kSegRows);
-        const int nwd = (nseg + 31) >> 5;
-        // (1) breakpoint bitmap over the segment's rows: a run starts where some offset group's
-        //     region row enters another classification zone or the domain, and every kRunMax rows
-        for (int w = lane; w < nwd; w += 32) X.bm[w] = 0u;
-        __syncwarp();
-        for (int i = lane * kRunMax; i < nseg; i += 32 * kRunMax) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
-        my_rows += (unsigned long long)(lane < ng ? 8 * (nb + 2) : 0);  // breakpoint marks
-        for (int g = lane; g < ng; g += 32) {
-          const DGroup gr = K.g[g0 + g];
-          const long long zz = z - gr.oz;
-          if (zz < lo2 || zz >= hi2) continue;
-          const long long C = Gy * fdiv(zz - lo2, fdz);
-          auto mark = [&](long long yb) {
-            const long long i = yb - ys;
-            if (i > 0 && i < nseg) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
-          };
-          mark(lo1 + gr.oy);
-          mark(hi1 + gr.oy);
-          for (int k = 0; k < nb; ++k) {
-            const long long d = X.bnd[k] - C;
-            if (d > 0 && d < Gy) mark(lo1 + d * BF1 + gr.oy);
-          }
-        }
-        __syncwarp();
-        // (2) compact the run starts (ascending) into X.rs
-        const int wpl = (nwd + 31) >> 5;
-        int cnt = 0;
-        for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(X.bm[w]);
-        int pos = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(FULL, pos, o);
-          if (lane >= o) pos += v;
-        }
-        const int nruns = __shfl_sync(FULL, pos, 31);
-        pos -= cnt;
-        for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
-          unsigned bits = X.bm[w];
-          while (bits) {
-            const int bt = __ffs(bits) - 1;
-            bits &= bits - 1;
-            X.rs[pos++] = (short)(w * 32 + bt);
-          }
-        }
-        if (lane == 0) X.rs[nruns] = (short)nseg;
-        __syncwarp();
-        // (3) one run per lane: masks of its first row, unions, rows emitted in order
-        for (int rb = 0; rb < nruns; rb += 32) {
-          Tri t[kNQ];
-#pragma unroll
-          for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
-          const int j = rb + lane;
-          if (j < nruns) {
-            const long long y = ys + X.rs[j];
-            const int run = X.rs[j + 1] - X.rs[j];
-            // algorithmic int ops of this run: classification of every
-            // offset group (domain 4, two multiply-high divisions 6, block row 2, five range
-            // classifications 15, mask update 3) and 9 triple appends per row (8 each)
-            my_rows += (unsigned long long)(30 * ng + 72 * run);
-            unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
-            for (int g = 0; g < ng; ++g) {
-              const DGroup gr = K.g[g0 + g];
-              const long long zz = z - gr.oz, yy = y - gr.oy;
-              if (zz < lo2 || zz >= hi2 || yy < lo1 || yy >= hi1) continue;
-              const long long r = fdiv(yy - lo1, fdy) + Gy * fdiv(zz - lo2, fdz);
-#pragma unroll
-              for (int q = 0; q < 5; ++q) {
-                const int ty = classify(X.r[q], r);
-                if (ty >= 0) {
-                  const unsigned long long bit = 1ull << (ty * 16 + gr.run);
-                  if (gr.kind) mS[q] |= bit;
-                  else mL[q] |= bit;
-                }
-              }
-            }
-            const long long R0f = align + ((py * y + pz * z) << le);
-            const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
-            // unions with compile-time targets (the triples stay in registers)
-            if (noS) {
-              row_emit<0, 2, -1>(t, X, F, mL[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
-            } else if (noL) {
-              row_emit<1, 2, -1>(t, X, F, mS[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
-            } else {
-              row_emit<0, -1, -1>(t, X, F, mL[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
-              row_emit<1, -1, -1>(t, X, F, mS[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
-              row_emit<-1, 2, -1>(t, X, F, mL[0] | mS[0], 0, 0ull, 0, R0f, pystep, run, le, ls, ll);
-            }
-            if (!noL) {
-              row_emit<3, 4, -1>(t, X, F, mL[1] | mS[1], 1, 0ull, 1, R0f, pystep, run, le, ls, ll);
-              row_emit<5, 6, -1>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0f, pystep, run, le, ls, ll);
-              row_emit<7, -1, -1>(t, X, F, mL[3], 3, mS[1], 1, R0f, pystep, run, le, ls, ll);
-              row_emit<8, -1, -1>(t, X, F, mL[4], 4, mS[2], 2, R0f, pystep, run, le, ls, ll);
-            } else {
-              row_emit<3, 4, 7>(t, X, F, mL[1] | mS[1], 1, 0ull, 1, R0f, pystep, run, le, ls, ll);
-              row_emit<5, 6, 8>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0f, pystep, run, le, ls, ll);
-            }
-          }
-          warp_ordered_reduce<kNQ>(t);
-#pragma unroll
-          for (int q = 0; q < kNQ; ++q)
-            pt[q] = tri_combine(pt[q], Tri{shfl64(t[q].f, 0), shfl64(t[q].l, 0), shfl64(t[q].c, 0)});
-        }
-        __syncwarp();
-      }
-#pragma unroll
-      for (int q = 0; q < kNQ; ++q) carry[q] = tri_combine(carry[q], pt[q]);
-      if (lane == 0) {
-        long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
-#pragma unroll
-        for (int q = 0; q < kNQ; ++q) {
-          out[q * 3 + 0] = carry[q].f;
-          out[q * 3 + 1] = carry[q].l;
-          out[q * 3 + 2] = carry[q].c;
-        }
+      seg = __reduce_max_sync(FULL, seg);
+      const int rep = seg + ((z - seg) % per);
+      if (rep != z) {
+        if (lane == 0) chunkres[(pre[c].chunk + ci) * (kNQ * 3) + 2] = -(long long)(rep - RI.z0) - 2;
+        continue;
       }
     }
-   }
+    if (ranges_c != c) {  // ranges and zone boundaries of this config (k_plan) -> warp smem, 32-bit
+      __syncwarp();
+      if (lane < 5) {
+        const RangeInfo& R = P.rng[lane];
+        RI32 r32;
+        r32.ra = (int)R.ra;
+        r32.rl = (int)R.rl;
+        for (int a = 0; a < 4; ++a) {
+          r32.iv[a][0] = (int)R.iv[a][0];
+          r32.iv[a][1] = (int)R.iv[a][1];
+        }
+        r32.nonempty = R.nonempty;
+        r32.pad = 0;
+        X.r[lane] = r32;
+      }
+      if (lane < 20) X.bnd[lane] = (int)P.bnd[lane];
+      __syncwarp();
+      ranges_c = c;
+    }
+    const int nb = P.nb;
+    const long long R0p = F.align + ((py * y0 + pz * z) << le);
+    const long long Bp = (R0p >> ll) << ll;
+    const int off0 = (int)(R0p - Bp);
+    const int pystep = (int)(py << le);
+    T32 pt[kNQ];
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) pt[q] = t32_empty();
+    for (int ys = y0; ys < y0 + ny; ys += kSegRows) {
+      const int nseg = y0 + ny - ys < kSegRows ? y0 + ny - ys : kSegRows;
+      const int nwd = (nseg + 31) >> 5;
+      for (int w = lane; w < nwd; w += 32) X.bm[w] = 0u;
+      __syncwarp();
+      if (lane == 0) atomicOr(&X.bm[0], 1u);
+      my_ops += (unsigned long long)(lane < ng ? 8 * (nb + 2) : 0);
+      for (int g = lane; g < ng; g += 32) {
+        const DGroup gr = K.g[g0 + g];
+        const int zz = z - gr.oz;
+        if (zz < lo2 || zz >= hi2) continue;
+        const int C = Gy * fdiv32(zz - lo2, fdz);
+        auto mark = [&](int yb) {
+          const int i = yb - ys;
+          if (i > 0 && i < nseg) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
+        };
+        mark(lo1 + gr.oy);
+        mark(hi1 + gr.oy);
+        for (int k = 0; k < nb; ++k) {
+          const int d = X.bnd[k] - C;
+          if (d > 0 && d < Gy) mark(lo1 + d * BF1 + gr.oy);
+        }
+      }
+      __syncwarp();
+      // compact the run starts (ascending) into X.rs
+      const int wpl = (nwd + 31) >> 5;
+      int cnt = 0;
+      for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(X.bm[w]);
+      int pos = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, pos, o);
+        if (lane >= o) pos += v;
+      }
+      const int nruns = __shfl_sync(FULL, pos, 31);
+      pos -= cnt;
+      for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
+        unsigned bits = X.bm[w];
+        while (bits) {
+          const int bt = __ffs(bits) - 1;
+          bits &= bits - 1;
+          X.rs[pos++] = (short)(w * 32 + bt);
+        }
+      }
+      if (lane == 0) X.rs[nruns] = (short)nseg;
+      __syncwarp();
+      for (int rb = 0; rb < nruns; rb += 32) {
+        T32 t[kNQ];
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q) t[q] = t32_empty();
+        const int j = rb + lane;
+        if (j < nruns) {
+          const int y = ys + X.rs[j];
+          const int run = X.rs[j + 1] - X.rs[j];
+          my_ops += (unsigned long long)(30 * ng + 72 * run);
+          unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
+          for (int g = 0; g < ng; ++g) {
+            const DGroup gr = K.g[g0 + g];
+            const int zz = z - gr.oz, yy = y - gr.oy;
+            if (zz < lo2 || zz >= hi2 || yy < lo1 || yy >= hi1) continue;
+            const int r = fdiv32(yy - lo1, fdy) + Gy * fdiv32(zz - lo2, fdz);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+              const int ty = classify32(X.r[q], r);
+              if (ty >= 0) {
+                const unsigned long long bit = 1ull << (ty * 16 + gr.run);
+                if (gr.kind) mS[q] |= bit;
+                else mL[q] |= bit;
+              }
+            }
+          }
+          const int R0 = off0 + (y - y0) * pystep;
+          const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
+          if (noS) {
+            row_emit32<0, 2, -1>(t, X, F, mL[0], 0, 0ull, 0, R0, pystep, run, le, ls, ll);
+          } else if (noL) {
+            row_emit32<1, 2, -1>(t, X, F, mS[0], 0, 0ull, 0, R0, pystep, run, le, ls, ll);
+          } else {
+            row_emit32<0, -1, -1>(t, X, F, mL[0], 0, 0ull, 0, R0, pystep, run, le, ls, ll);
+            row_emit32<1, -1, -1>(t, X, F, mS[0], 0, 0ull, 0, R0, pystep, run, le, ls, ll);
+            row_emit32<-1, 2, -1>(t, X, F, mL[0] | mS[0], 0, 0ull, 0, R0, pystep, run, le, ls, ll);
+          }
+          if (!noL) {
+            row_emit32<3, 4, -1>(t, X, F, mL[1] | mS[1], 1, 0ull, 1, R0, pystep, run, le, ls, ll);
+            row_emit32<5, 6, -1>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0, pystep, run, le, ls, ll);
+            row_emit32<7, -1, -1>(t, X, F, mL[3], 3, mS[1], 1, R0, pystep, run, le, ls, ll);
+            row_emit32<8, -1, -1>(t, X, F, mL[4], 4, mS[2], 2, R0, pystep, run, le, ls, ll);
+          } else {
+            row_emit32<3, 4, 7>(t, X, F, mL[1] | mS[1], 1, 0ull, 1, R0, pystep, run, le, ls, ll);
+            row_emit32<5, 6, 8>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0, pystep, run, le, ls, ll);
+          }
+        }
+        warp_ordered_reduce32<kNQ>(t);
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q)
+          pt[q] = t32_combine(pt[q], T32{__shfl_sync(FULL, t[q].f, 0), __shfl_sync(FULL, t[q].l, 0),
+                                         __shfl_sync(FULL, t[q].c, 0)});
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
+      const long long bs = Bp >> ls, bl = Bp >> ll;
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        const long long b = (q == 2 || q == 4 || q == 6) ? bl : bs;
+        out[q * 3 + 0] = pt[q].c ? pt[q].f + b : 0;
+        out[q * 3 + 1] = pt[q].c ? pt[q].l + b : 0;
+        out[q * 3 + 2] = pt[q].c;
+      }
+    }
   }
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) my_rows += __shfl_down_sync(FULL, my_rows, o);
-  if (lane == 0 && my_rows) atomicAdd(work + K_ROWS, my_rows);
+  for (int o = 16; o >= 1; o >>= 1) my_ops += __shfl_down_sync(FULL, my_ops, o);
+  if (lane == 0 && my_ops) atomicAdd(work + K_ROWS, my_ops);
 }
 
 // Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
