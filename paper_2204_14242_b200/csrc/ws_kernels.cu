@@ -42,6 +42,11 @@ __device__ __forceinline__ long long shfl64(long long v, int src) {
   int hi = __shfl_sync(FULL, (int)(v >> 32), src);
   return ((long long)hi << 32) | (unsigned int)lo;
 }
+__device__ __forceinline__ long long shfl64_up(long long v, int d) {
+  int lo = __shfl_up_sync(FULL, (int)(v & 0xffffffffll), d);
+  int hi = __shfl_up_sync(FULL, (int)(v >> 32), d);
+  return ((long long)hi << 32) | (unsigned int)lo;
+}
 __device__ __forceinline__ long long shfl64_down(long long v, int d) {
   int lo = __shfl_down_sync(FULL, (int)(v & 0xffffffffll), d);
   int hi = __shfl_down_sync(FULL, (int)(v >> 32), d);
@@ -314,35 +319,46 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   const long long Rw = M >> K.f[0].lg_elem, Rs = (long long)G.g.line_bytes >> K.f[0].lg_elem;
   P.wcls_R = (same && Rw >= 1 && Rw <= 64 && P.nwarps <= 32) ? (int)Rw : 0;
   P.scls_R = (same && Rs >= 1 && Rs <= 64) ? (int)Rs : 0;
-  // k_rows ranges and zone boundaries
+  for (int d = 0; d < 3; ++d) P.cls_pitch[d] = K.f[0].pitch[d];
+  P.cls_lg_elem = K.f[0].lg_elem;
+  P.status = WS_OK;
+}
+
+// k_rows range q of a plan: 0 = wave, 1 = L_y, 2 = L_z, 3 = L_y + wave, 4 = L_z + wave
+__device__ void plan_range(DPlan& P, int q) {
+  long long a, b;
+  if (q == 0) { a = P.s; b = P.s + P.W; }
+  else if (q == 1) { a = P.Ly0; b = P.s; }
+  else if (q == 2) { a = P.Lz0; b = P.s; }
+  else if (q == 3) { a = P.Ly0; b = P.s + P.W; }
+  else { a = P.Lz0; b = P.s + P.W; }
+  RangeInfo& R = P.rng[q];
+  R.nonempty = a < b;
+  R.pad = 0;
+  const long long Gx = P.G[0], lx = P.lo[0], hx = P.hi[0], bf = P.BF[0];
+  long long xa = 0, xl = Gx;
+  if (a < b) {
+    R.ra = a / Gx;
+    xa = a % Gx;
+    R.rl = (b - 1) / Gx;
+    xl = (b - 1) % Gx + 1;
+  } else {
+    R.ra = R.rl = 0;
+  }
+  const long long xs_a = lx + xa * bf;
+  long long xe_l = lx + xl * bf;
+  if (xe_l > hx) xe_l = hx;
+  R.iv[0][0] = lx;   R.iv[0][1] = hx;
+  R.iv[1][0] = xs_a; R.iv[1][1] = hx;
+  R.iv[2][0] = lx;   R.iv[2][1] = xe_l;
+  R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
+}
+
+// sorted distinct block rows where some range's classification zone starts
+__device__ void plan_boundaries(DPlan& P) {
   P.nb = 0;
   for (int q = 0; q < 5; ++q) {
-    long long a, b;
-    if (q == 0) { a = P.s; b = P.s + P.W; }
-    else if (q == 1) { a = P.Ly0; b = P.s; }
-    else if (q == 2) { a = P.Lz0; b = P.s; }
-    else if (q == 3) { a = P.Ly0; b = P.s + P.W; }
-    else { a = P.Lz0; b = P.s + P.W; }
-    RangeInfo& R = P.rng[q];
-    R.nonempty = a < b;
-    R.pad = 0;
-    const long long Gx = P.G[0], lx = P.lo[0], hx = P.hi[0], bf = P.BF[0];
-    long long xa = 0, xl = Gx;
-    if (a < b) {
-      R.ra = a / Gx;
-      xa = a % Gx;
-      R.rl = (b - 1) / Gx;
-      xl = (b - 1) % Gx + 1;
-    } else {
-      R.ra = R.rl = 0;
-    }
-    const long long xs_a = lx + xa * bf;
-    long long xe_l = lx + xl * bf;
-    if (xe_l > hx) xe_l = hx;
-    R.iv[0][0] = lx;   R.iv[0][1] = hx;
-    R.iv[1][0] = xs_a; R.iv[1][1] = hx;
-    R.iv[2][0] = lx;   R.iv[2][1] = xe_l;
-    R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
+    const RangeInfo& R = P.rng[q];
     if (!R.nonempty) continue;
     const long long cand[4] = {R.ra, R.ra + 1, R.rl, R.rl + 1};
     for (int k = 0; k < 4; ++k) {
@@ -355,9 +371,6 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
       ++P.nb;
     }
   }
-  for (int d = 0; d < 3; ++d) P.cls_pitch[d] = K.f[0].pitch[d];
-  P.cls_lg_elem = K.f[0].lg_elem;
-  P.status = WS_OK;
 }
 
 __device__ __forceinline__ void decode_kappa(int q, const int* f, int& kx, int& ky, int& kz) {
@@ -388,6 +401,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     if (tid == 0) plans[c] = P;
     return;
   }
+  if (tid < 5) plan_range(P, tid);
+  __syncthreads();
+  if (tid == 0) plan_boundaries(P);
   const DKernel& K = ks[P.kid];
   const int fc = P.fcube;
   const int np = K.n_acc * fc;
@@ -539,8 +555,8 @@ __device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
 __global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
                                                unsigned long long* __restrict__ work,
                                                unsigned long long* __restrict__ lists) {
-  __shared__ long long s[kNPrefix][1024];
-  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ long long s_w[32][kNPrefix];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 16) work[tid] = 0ull;
   if (tid < 4) lists[tid] = 0ull;
   const int seg = (n + nt - 1) / nt;
@@ -553,21 +569,37 @@ __global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, 
 #pragma unroll
     for (int j = 0; j < kNPrefix; ++j) a[j] += plan_count(P, j);
   }
+  // block exclusive scan of the per-thread sums: warp inclusive scans, then the warp totals
+  long long inc[kNPrefix];
 #pragma unroll
-  for (int j = 0; j < kNPrefix; ++j) s[j][tid] = a[j];
+  for (int j = 0; j < kNPrefix; ++j) {
+    long long v = a[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = shfl64_up(v, o);
+      if (lane >= o) v += u;
+    }
+    inc[j] = v;
+    if (lane == 31) s_w[wid][j] = v;
+  }
   __syncthreads();
-  if (tid < kNPrefix) {
-    long long run = 0;
-    for (int i = 0; i < nt; ++i) {
-      long long v = s[tid][i];
-      s[tid][i] = run;
-      run += v;
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < kNPrefix; ++j) {
+      long long v = lane < (nt >> 5) ? s_w[lane][j] : 0;
+      const long long own = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long u = shfl64_up(v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane < (nt >> 5)) s_w[lane][j] = v - own;  // exclusive warp offsets
     }
   }
   __syncthreads();
   long long r[kNPrefix];
 #pragma unroll
-  for (int j = 0; j < kNPrefix; ++j) r[j] = s[j][tid];
+  for (int j = 0; j < kNPrefix; ++j) r[j] = s_w[wid][j] + inc[j] - a[j];
   for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
     pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5]};
     const DPlan& P = plans[c];
@@ -747,8 +779,11 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
     bool direct = false;
     unsigned long long key = ~0ull;
     long long B = 0;
+    // one search per warp (lanes hold consecutive items), then each lane advances
+    int c0 = find_config<0>(pre, n, base);
     if (have) {
-      c = find_config<0>(pre, n, item);
+      c = c0;
+      while (c + 1 < n && pre[c + 1].warp <= item) ++c;
       const DPlan& P = plans[c];
       const long long wi = item - pre[c].warp;
       B = P.s + wi / P.nwarps;
@@ -956,391 +991,6 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
   }
 }
 
-constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
-constexpr int kSegRowsS = 1024;  // rows of a plane per SM-set run segment
-
-// Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
-// dispatch, Q9) by one CTA.  Row (y,z) of field phi holds element x iff some member box
-// contains (x - ox, y - oy, z - oz) for a load offset o.  Per z-plane: if every
-// (group, member) z-membership equals that of plane z - per, the plane is the translate of
-// that plane by whole lines (derived); otherwise a warp computes it, lanes taking rows
-// (per row: compares against the member boxes into a candidate mask, union, triple), with an
-// ordered warp reduction.  Thread 0 folds the plane triples in z order.
-struct SmWarp {
-  unsigned bm[kSegRowsS / 32];
-  short rs[kSegRowsS + 2];
-};
-
-__device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
-                          SmBox* mb, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */, SmWarp* sw,
-                          unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwp = blockDim.x >> 5;
-  const int ls = G.lg_sector, ll = G.lg_line;
-  const int nm = (int)(kj < kMaxMembers ? kj : kMaxMembers);
-  sum_s = sum_l = 0;
-  units = 0;
-  __syncthreads();
-  if (tid < nm) {
-    const long long Bm = S0 + (long long)tid * nsm;
-    const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
-    long long lo[3], hi[3];
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = P.lo[d] + bc[d] * P.BF[d];
-      hi[d] = lo[d] + P.BF[d];
-      if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
-    }
-    mb[tid] = SmBox{lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]};
-  }
-  __syncthreads();
-  long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
-  for (int m = 0; m < nm; ++m) {
-    ylo = min(ylo, mb[m].y0);
-    yhi = max(yhi, mb[m].y1);
-    zlo = min(zlo, mb[m].z0);
-    zhi = max(zhi, mb[m].z1);
-  }
-  for (int fi = 0; fi < K.n_fields; ++fi) {
-    const DField& F = K.f[fi];
-    if (!(F.kinds & 1)) continue;
-    const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
-    const int le = F.lg_elem;
-    long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
-    if (y0 < 0) y0 = 0;
-    if (z0 < 0) z0 = 0;
-    if (y1 > F.ext[1]) y1 = F.ext[1];
-    if (z1 > F.ext[2]) z1 = F.ext[2];
-    if (y1 <= y0 || z1 <= z0) continue;
-    const long long ny = y1 - y0;
-    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
-    const long long pbytes = pz << le, pystep = py << le;
-    const int per = plane_period(pz, le, ll);
-    const int npairs = ng * nm;
-    Tri cs_all = tri_empty(), cl_all = tri_empty();
-    for (long long zs = z0; zs < z1; zs += kMaxPlanes) {
-      const int np = (int)(z1 - zs < kMaxPlanes ? z1 - zs : kMaxPlanes);
-      // (a) derived planes (relative to plane z - per of the whole box)
-      for (int p = wid; p < np; p += nwp) {
-        const long long z = zs + p;
-        bool same = per > 0 && z - per >= zs;  // derive only within this segment
-        if (same) {
-          for (int k = lane; k < npairs; k += 32) {
-            const DGroup gr = K.g[g0 + k / nm];
-            if (gr.kind != 0) continue;
-            const SmBox& bx = mb[k % nm];
-            const long long za = z - gr.oz, zb = za - per;
-            same = same && ((za >= bx.z0 && za < bx.z1) == (zb >= bx.z0 && zb < bx.z1));
-          }
-        }
-        same = __all_sync(FULL, same);
-        if (lane == 0) pder[p] = same ? 1 : 0;
-      }
-      __syncthreads();
-      // (b) computed planes: one warp per plane.  A row's candidates change only where some
-      //     y - oy crosses a member's y edge: lanes mark these breakpoints, then take one run
-      //     each (candidates of its first row, union, closed-form run triple).
-      for (int p = wid; p < np; p += nwp) {
-        if (pder[p]) continue;
-        const long long z = zs + p;
-        SmWarp& Wp = sw[wid];
-        Tri ps = tri_empty(), pl = tri_empty();
-        for (long long ys = y0; ys < y1; ys += kSegRowsS) {
-          const int nseg = (int)(y1 - ys < kSegRowsS ? y1 - ys : kSegRowsS);
-          const int nwd = (nseg + 31) >> 5;
-          for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
-          __syncwarp();
-          if (lane == 0) atomicOr(&Wp.bm[0], 1u);
-          for (int k = lane; k < npairs; k += 32) {
-            const DGroup gr = K.g[g0 + k / nm];
-            if (gr.kind != 0) continue;
-            const SmBox& bx = mb[k % nm];
-            const long long zz = z - gr.oz;
-            if (zz < bx.z0 || zz >= bx.z1) continue;
-            const long long e0 = bx.y0 + gr.oy - ys, e1 = bx.y1 + gr.oy - ys;
-            if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
-            if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
-          }
-          __syncwarp();
-          const int wpl = (nwd + 31) >> 5;
-          int cnt = 0;
-          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(Wp.bm[w]);
-          int pos = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL, pos, o);
-            if (lane >= o) pos += v;
-          }
-          const int nruns = __shfl_sync(FULL, pos, 31);
-          pos -= cnt;
-          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
-            unsigned bits = Wp.bm[w];
-            while (bits) {
-              const int bt = __ffs(bits) - 1;
-              bits &= bits - 1;
-              Wp.rs[pos++] = (short)(w * 32 + bt);
-            }
-          }
-          if (lane == 0) Wp.rs[nruns] = (short)nseg;
-          __syncwarp();
-          for (int rb = 0; rb < nruns; rb += 32) {
-            Tri t[2] = {tri_empty(), tri_empty()};
-            const int j = rb + lane;
-            if (j < nruns) {
-              const long long y = ys + Wp.rs[j];
-              const int run = Wp.rs[j + 1] - Wp.rs[j];
-              const long long R0f = align + ((py * y + pz * z) << le);
-              unsigned long long mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              for (int g = 0; g < ng; ++g) {
-                const DGroup gr = K.g[g0 + g];
-                if (gr.kind != 0) continue;
-                const long long yy = y - gr.oy, zz = z - gr.oz;
-#pragma unroll 4
-                for (int m = 0; m < nm; ++m) {
-                  const SmBox& bx = mb[m];
-                  if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
-                    mk[m >> 2] |= 1ull << ((m & 3) * 16 + gr.run);
-                }
-              }
-              auto gen = [&](auto&& cb) {
-                for (int w = 0; w < ((nm + 3) >> 2); ++w) {
-                  unsigned long long q = mk[w];
-                  while (q) {
-                    const int bb = __ffsll((long long)q) - 1;
-                    q &= q - 1;
-                    const SmBox& bx = mb[w * 4 + (bb >> 4)];
-                    cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
-                  }
-                }
-              };
-              long long mn_s = LLONG_MAX, mx_s = LLONG_MIN, mn_e = LLONG_MAX, mx_e = LLONG_MIN;
-              gen([&](long long xs, long long xe) {
-                mn_s = xs < mn_s ? xs : mn_s;
-                mx_s = xs > mx_s ? xs : mx_s;
-                mn_e = xe < mn_e ? xe : mn_e;
-                mx_e = xe > mx_e ? xe : mx_e;
-              });
-              if (mn_s != LLONG_MAX) {
-                if (mx_s <= mn_e) {
-                  const long long a0 = R0f + (mn_s << le), a1 = R0f + ((mx_e - 1) << le);
-                  auto rs_ = [&](int r) {
-                    const long long s0 = (a0 + r * pystep) >> ls, s1 = (a1 + r * pystep) >> ls;
-                    return Tri{s0, s1, s1 - s0 + 1};
-                  };
-                  auto rl_ = [&](int r) {
-                    const long long s0 = (a0 + r * pystep) >> ll, s1 = (a1 + r * pystep) >> ll;
-                    return Tri{s0, s1, s1 - s0 + 1};
-                  };
-                  t[0] = run_triple(rs_, pystep, run, ls);
-                  t[1] = run_triple(rl_, pystep, run, ll);
-                } else {
-                  auto rs_ = [&](int r) {
-                    Tri x = tri_empty();
-                    row_union(gen, R0f + r * pystep, le, ls, ll, &x, nullptr);
-                    return x;
-                  };
-                  auto rl_ = [&](int r) {
-                    Tri x = tri_empty();
-                    row_union(gen, R0f + r * pystep, le, ls, ll, nullptr, &x);
-                    return x;
-                  };
-                  t[0] = run_triple(rs_, pystep, run, ls);
-                  t[1] = run_triple(rl_, pystep, run, ll);
-                }
-              }
-            }
-            warp_ordered_reduce<2>(t);
-            ps = tri_combine(ps, Tri{shfl64(t[0].f, 0), shfl64(t[0].l, 0), shfl64(t[0].c, 0)});
-            pl = tri_combine(pl, Tri{shfl64(t[1].f, 0), shfl64(t[1].l, 0), shfl64(t[1].c, 0)});
-          }
-          __syncwarp();
-        }
-        if (lane == 0) {
-          pt[2 * p] = ps;
-          pt[2 * p + 1] = pl;
-          units += (unsigned long long)ny;
-        }
-      }
-      __syncthreads();
-      // (c) ordered fold with derivation (plane z - per is resolved before z)
-      if (tid == 0) {
-        for (int p = 0; p < np; ++p) {
-          if (pder[p]) {
-            const int q = p - per;  // >= 0: derived planes have their source in this segment
-            const Tri a = pt[2 * q], b = pt[2 * q + 1];
-            const long long dsh = (long long)per * pbytes;
-            pt[2 * p] = a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty();
-            pt[2 * p + 1] = b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty();
-          }
-          cs_all = tri_combine(cs_all, pt[2 * p]);
-          cl_all = tri_combine(cl_all, pt[2 * p + 1]);
-        }
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      sum_s += (unsigned long long)cs_all.c;
-      sum_l += (unsigned long long)cl_all.c;
-    }
-  }
-}
-
-// Pass 1 (one thread per SM set): single-block sets go to their translation class: clip
-// pattern of the block x residue of its first cell's address mod line_bytes (identical
-// active-cell boxes that are translates by a multiple of the line size have identical
-// sector and line counts).  Multi-block sets are appended to the direct list.
-__global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
-                                               const DGpu* __restrict__ gs, unsigned int* __restrict__ scnt,
-                                               unsigned long long* __restrict__ srep,
-                                               unsigned long long* __restrict__ lists,
-                                               unsigned long long* __restrict__ slist,
-                                               unsigned long long* __restrict__ dlist) {
-  const long long total = pre[n].set;
-  for (long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x; item < total;
-       item += (long long)gridDim.x * blockDim.x) {
-    const int c = find_config<2>(pre, n, item);
-    const DPlan& P = plans[c];
-    const long long j = item - pre[c].set;
-    const long long nsm = gs[P.gid].g.n_sm;
-    const long long S0 = P.s + j;
-    const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-    if (P.scls_R > 0 && kj == 1) {
-      const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
-      long long pl = 0;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-      const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
-      const long long gslot = (long long)c * kSSlots + slot;
-      if (atomicAdd(scnt + gslot, 1u) == 0u) {
-        srep[gslot] = (unsigned long long)S0;
-        slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
-      }
-    } else {
-      dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
-    }
-  }
-}
-
-// Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
-// directly evaluated multi-block SM sets.
-__global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
-                                                const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
-                                                const unsigned int* __restrict__ scnt,
-                                                const unsigned long long* __restrict__ srep,
-                                                const unsigned long long* __restrict__ lists,
-                                                const unsigned long long* __restrict__ slist,
-                                                const unsigned long long* __restrict__ dlist,
-                                                unsigned long long* __restrict__ work) {
-  __shared__ SmBox s_mb[kMaxMembers];
-  __shared__ Tri s_pt[2 * kMaxPlanes];
-  __shared__ unsigned char s_der[kMaxPlanes];
-  __shared__ SmWarp s_sw[8];
-  __shared__ DGroup s_g[kMaxAcc];
-  __shared__ int s_ng;
-  __shared__ long long s_box[4];
-  __shared__ Tri s_red[(kRowThreads / 32) * 2];
-  const long long ncls = (long long)lists[1];
-  const long long total = ncls + (long long)lists[2];
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const bool cls = item < ncls;
-    const unsigned long long ent = cls ? slist[item] : dlist[item - ncls];
-    const int c = (int)(ent >> 32);
-    const unsigned low = (unsigned)(ent & 0xffffffffu);
-    const DPlan& P = plans[c];
-    const DGpu& G = gs[P.gid];
-    const long long nsm = G.g.n_sm;
-    unsigned long long mult = 1;
-    long long S0, kj;
-    if (cls) {
-      const long long gslot = (long long)c * kSSlots + low;
-      mult = scnt[gslot];
-      S0 = (long long)srep[gslot];
-      kj = 1;
-    } else {
-      S0 = P.s + low;
-      kj = (P.W - (long long)low + nsm - 1) / nsm;
-    }
-    unsigned long long ss, sl, un;
-    if (kj == 1) {  // one block: small box, flat rows over the whole CTA
-      smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
-      if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
-    } else {        // several blocks: plane derivation + runs
-      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_pt, s_der, s_sw, ss, sl, un);
-      // every warp's lane 0 counted its planes' rows
-      if ((threadIdx.x & 31) == 0 && un) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
-    }
-    if (threadIdx.x == 0) {
-      unsigned long long* a = acc + (long long)c * A_N;
-      atomicAdd(a + A_SM_SEC, ss * mult);
-      atomicAdd(a + A_SM_LIN, sl * mult);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ a5 + a6: wave and layer sets
-// ranges: 0 = wave [s, s+W), 1 = L_y [Ly0, s), 2 = L_z [Lz0, s), 3 = L_y + wave, 4 = L_z + wave
-
-__device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
-  if (!R.nonempty || r < R.ra || r > R.rl) return -1;
-  if (R.ra == R.rl) return 3;
-  if (r == R.ra) return 1;
-  if (r == R.rl) return 2;
-  return 0;
-}
-
-// Cached union of one row: a single component [x0, x1) (x0 >= x1: empty) or `multi`.
-struct UC {
-  long long x0, x1;
-  int single;
-};
-
-template <class Gen>
-__device__ __forceinline__ void row_union_c(const Gen& gen, long long R0, int le, int ls, int ll, Tri* ts, Tri* tl,
-                                            Tri* ts2, UC& uc) {
-  const long long INF = LLONG_MAX;
-  long long start = INF, mx_s = LLONG_MIN, mn_e = INF, mx_e = LLONG_MIN;
-  gen([&](long long xs, long long xe) {
-    start = xs < start ? xs : start;
-    mx_s = xs > mx_s ? xs : mx_s;
-    mn_e = xe < mn_e ? xe : mn_e;
-    mx_e = xe > mx_e ? xe : mx_e;
-  });
-  if (start == INF) {
-    uc = UC{0, 0, 1};
-    return;
-  }
-  if (mx_s <= mn_e) {
-    uc = UC{start, mx_e, 1};
-    const long long a0 = R0 + (start << le), a1 = R0 + ((mx_e - 1) << le);
-    if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
-    if (ts2) tri_add(*ts2, a0 >> ls, a1 >> ls);
-    if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
-    return;
-  }
-  uc.single = 0;
-  row_union(gen, R0, le, ls, ll, ts, tl, ts2);
-}
-
-template <class Gen>
-__device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, long long R0, int le, int ls, int ll,
-                                                 Tri* ts, Tri* tl, Tri* ts2, UC& uc) {
-  if (first) {
-    row_union_c(gen, R0, le, ls, ll, ts, tl, ts2, uc);
-  } else if (uc.single) {
-    if (uc.x0 < uc.x1) {
-      const long long a0 = R0 + (uc.x0 << le), a1 = R0 + ((uc.x1 - 1) << le);
-      if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
-      if (ts2) tri_add(*ts2, a0 >> ls, a1 >> ls);
-      if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
-    }
-  } else {
-    row_union(gen, R0, le, ls, ll, ts, tl, ts2);
-  }
-}
-
-constexpr int kRowWarps = 8;
-
-constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
-constexpr int kRunMax = 256;    // runs are split every kRunMax rows (lane work balance)
-
 // ---- 32-bit plane-relative arithmetic for k_rows ---------------------------------------------
 // Every address of one z-plane of a field is R0p + rel with R0p the address of the plane's first
 // box row and 0 <= rel < 2^31 (describe-time limit: pitch[2] * elem_bytes < 2^31).  Sectors and
@@ -1428,6 +1078,419 @@ __device__ __forceinline__ T32 run_triple32(const RowFn& row, int step, int run,
   return acc;
 }
 
+template <int NQ>
+__device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const T32 x{__shfl_down_sync(FULL, t[q].f, o), __shfl_down_sync(FULL, t[q].l, o),
+                  __shfl_down_sync(FULL, t[q].c, o)};
+      if (lane + o < 32) t[q] = t32_combine(t[q], x);
+    }
+  }
+}
+
+struct SmBox32 {
+  int x0, x1, y0, y1, z0, z1;
+};
+
+constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
+constexpr int kSegRowsS = 1024;  // rows of a plane per SM-set run segment
+
+// Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
+// dispatch, Q9) by one CTA.  Row (y,z) of field phi holds element x iff some member box
+// contains (x - ox, y - oy, z - oz) for a load offset o.  Per z-plane: if every
+// (group, member) z-membership equals that of plane z - per, the plane is the translate of
+// that plane by whole lines (derived); otherwise a warp computes it, lanes taking rows
+// (per row: compares against the member boxes into a candidate mask, union, triple), with an
+// ordered warp reduction.  Thread 0 folds the plane triples in z order.
+struct SmWarp {
+  unsigned bm[kSegRowsS / 32];
+  short rs[kSegRowsS + 2];
+};
+
+__device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
+                          SmBox* mb, SmBox32* mb32, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */,
+                          SmWarp* sw,
+                          unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwp = blockDim.x >> 5;
+  const int ls = G.lg_sector, ll = G.lg_line;
+  const int nm = (int)(kj < kMaxMembers ? kj : kMaxMembers);
+  sum_s = sum_l = 0;
+  units = 0;
+  __syncthreads();
+  if (tid < nm) {
+    const long long Bm = S0 + (long long)tid * nsm;
+    const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+    long long lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = P.lo[d] + bc[d] * P.BF[d];
+      hi[d] = lo[d] + P.BF[d];
+      if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
+    }
+    mb[tid] = SmBox{lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]};
+    mb32[tid] = SmBox32{(int)lo[0], (int)hi[0], (int)lo[1], (int)hi[1], (int)lo[2], (int)hi[2]};
+  }
+  __syncthreads();
+  long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
+  for (int m = 0; m < nm; ++m) {
+    ylo = min(ylo, mb[m].y0);
+    yhi = max(yhi, mb[m].y1);
+    zlo = min(zlo, mb[m].z0);
+    zhi = max(zhi, mb[m].z1);
+  }
+  for (int fi = 0; fi < K.n_fields; ++fi) {
+    const DField& F = K.f[fi];
+    if (!(F.kinds & 1)) continue;
+    const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
+    const int le = F.lg_elem;
+    long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
+    if (y0 < 0) y0 = 0;
+    if (z0 < 0) z0 = 0;
+    if (y1 > F.ext[1]) y1 = F.ext[1];
+    if (z1 > F.ext[2]) z1 = F.ext[2];
+    if (y1 <= y0 || z1 <= z0) continue;
+    const long long ny = y1 - y0;
+    const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
+    const long long pbytes = pz << le, pystep = py << le;
+    const int per = plane_period(pz, le, ll);
+    const int npairs = ng * nm;
+    Tri cs_all = tri_empty(), cl_all = tri_empty();
+    for (long long zs = z0; zs < z1; zs += kMaxPlanes) {
+      const int np = (int)(z1 - zs < kMaxPlanes ? z1 - zs : kMaxPlanes);
+      // (a) derived planes (relative to plane z - per of the whole box)
+      for (int p = wid; p < np; p += nwp) {
+        const long long z = zs + p;
+        bool same = per > 0 && z - per >= zs;  // derive only within this segment
+        if (same) {
+          for (int k = lane; k < npairs; k += 32) {
+            const DGroup gr = K.g[g0 + k / nm];
+            if (gr.kind != 0) continue;
+            const SmBox& bx = mb[k % nm];
+            const long long za = z - gr.oz, zb = za - per;
+            same = same && ((za >= bx.z0 && za < bx.z1) == (zb >= bx.z0 && zb < bx.z1));
+          }
+        }
+        same = __all_sync(FULL, same);
+        if (lane == 0) pder[p] = same ? 1 : 0;
+      }
+      __syncthreads();
+      // (b) computed planes: one warp per plane.  A row's candidates change only where some
+      //     y - oy crosses a member's y edge: lanes mark these breakpoints, then take one run
+      //     each (candidates of its first row, union, closed-form run triple), in 32-bit
+      //     plane-relative arithmetic (see k_rows).
+      for (int p = wid; p < np; p += nwp) {
+        if (pder[p]) continue;
+        const int z = (int)(zs + p);
+        SmWarp& Wp = sw[wid];
+        const long long R0p = align + ((py * y0 + pz * (long long)z) << le);
+        const long long Bp = (R0p >> ll) << ll;
+        const int off0 = (int)(R0p - Bp), step = (int)pystep;
+        T32 ps = t32_empty(), pl = t32_empty();
+        for (int ys = 0; ys < (int)ny; ys += kSegRowsS) {
+          const int nseg = (int)ny - ys < kSegRowsS ? (int)ny - ys : kSegRowsS;
+          const int nwd = (nseg + 31) >> 5;
+          for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
+          __syncwarp();
+          if (lane == 0) atomicOr(&Wp.bm[0], 1u);
+          for (int k = lane; k < npairs; k += 32) {
+            const DGroup gr = K.g[g0 + k / nm];
+            if (gr.kind != 0) continue;
+            const SmBox32& bx = mb32[k % nm];
+            const int zz = z - gr.oz;
+            if (zz < bx.z0 || zz >= bx.z1) continue;
+            const int e0 = bx.y0 + gr.oy - (int)y0 - ys, e1 = bx.y1 + gr.oy - (int)y0 - ys;
+            if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
+            if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
+          }
+          __syncwarp();
+          const int wpl = (nwd + 31) >> 5;
+          int cnt = 0;
+          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(Wp.bm[w]);
+          int pos = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, pos, o);
+            if (lane >= o) pos += v;
+          }
+          const int nruns = __shfl_sync(FULL, pos, 31);
+          pos -= cnt;
+          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
+            unsigned bits = Wp.bm[w];
+            while (bits) {
+              const int bt = __ffs(bits) - 1;
+              bits &= bits - 1;
+              Wp.rs[pos++] = (short)(w * 32 + bt);
+            }
+          }
+          if (lane == 0) Wp.rs[nruns] = (short)nseg;
+          __syncwarp();
+          for (int rb = 0; rb < nruns; rb += 32) {
+            T32 ts = t32_empty(), tl = t32_empty();
+            const int j = rb + lane;
+            if (j < nruns) {
+              const int yr = ys + Wp.rs[j];  // row index inside the box
+              const int y = (int)y0 + yr;
+              const int run = Wp.rs[j + 1] - Wp.rs[j];
+              const int R0 = off0 + yr * step;
+              unsigned long long mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+              for (int g = 0; g < ng; ++g) {
+                const DGroup gr = K.g[g0 + g];
+                if (gr.kind != 0) continue;
+                const int yy = y - gr.oy, zz = z - gr.oz;
+#pragma unroll 4
+                for (int m = 0; m < nm; ++m) {
+                  const SmBox32& bx = mb32[m];
+                  if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
+                    mk[m >> 2] |= 1ull << ((m & 3) * 16 + gr.run);
+                }
+              }
+              auto gen = [&](auto&& cb) {
+                for (int w = 0; w < ((nm + 3) >> 2); ++w) {
+                  unsigned long long q = mk[w];
+                  while (q) {
+                    const int bb = __ffsll((long long)q) - 1;
+                    q &= q - 1;
+                    const SmBox32& bx = mb32[w * 4 + (bb >> 4)];
+                    cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
+                  }
+                }
+              };
+              const int INF = 0x7fffffff;
+              int mn_s = INF, mx_s = -INF, mn_e = INF, mx_e = -INF;
+              gen([&](int xs, int xe) {
+                mn_s = xs < mn_s ? xs : mn_s;
+                mx_s = xs > mx_s ? xs : mx_s;
+                mn_e = xe < mn_e ? xe : mn_e;
+                mx_e = xe > mx_e ? xe : mx_e;
+              });
+              if (mn_s != INF) {
+                if (mx_s <= mn_e) {
+                  const int a0 = R0 + (mn_s << le), a1 = R0 + ((mx_e - 1) << le);
+                  ts = run_triple32([&](int r) {
+                    const int s0 = (a0 + r * step) >> ls, s1 = (a1 + r * step) >> ls;
+                    return T32{s0, s1, s1 - s0 + 1};
+                  }, step, run, ls);
+                  tl = run_triple32([&](int r) {
+                    const int s0 = (a0 + r * step) >> ll, s1 = (a1 + r * step) >> ll;
+                    return T32{s0, s1, s1 - s0 + 1};
+                  }, step, run, ll);
+                } else {
+                  ts = run_triple32([&](int r) {
+                    T32 x = t32_empty();
+                    row_union32(gen, R0 + r * step, le, ls, x);
+                    return x;
+                  }, step, run, ls);
+                  tl = run_triple32([&](int r) {
+                    T32 x = t32_empty();
+                    row_union32(gen, R0 + r * step, le, ll, x);
+                    return x;
+                  }, step, run, ll);
+                }
+              }
+            }
+            T32 tt[2] = {ts, tl};
+            warp_ordered_reduce32<2>(tt);
+            ps = t32_combine(ps, T32{__shfl_sync(FULL, tt[0].f, 0), __shfl_sync(FULL, tt[0].l, 0), __shfl_sync(FULL, tt[0].c, 0)});
+            pl = t32_combine(pl, T32{__shfl_sync(FULL, tt[1].f, 0), __shfl_sync(FULL, tt[1].l, 0), __shfl_sync(FULL, tt[1].c, 0)});
+          }
+          __syncwarp();
+        }
+        if (lane == 0) {
+          const long long bs = Bp >> ls, bl = Bp >> ll;
+          pt[2 * p] = ps.c ? Tri{ps.f + bs, ps.l + bs, ps.c} : tri_empty();
+          pt[2 * p + 1] = pl.c ? Tri{pl.f + bl, pl.l + bl, pl.c} : tri_empty();
+          units += (unsigned long long)ny;
+        }
+      }
+      __syncthreads();
+      // (c) ordered fold with derivation (plane z - per is resolved before z)
+      if (tid == 0) {
+        for (int p = 0; p < np; ++p) {
+          if (pder[p]) {
+            const int q = p - per;  // >= 0: derived planes have their source in this segment
+            const Tri a = pt[2 * q], b = pt[2 * q + 1];
+            const long long dsh = (long long)per * pbytes;
+            pt[2 * p] = a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty();
+            pt[2 * p + 1] = b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty();
+          }
+          cs_all = tri_combine(cs_all, pt[2 * p]);
+          cl_all = tri_combine(cl_all, pt[2 * p + 1]);
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      sum_s += (unsigned long long)cs_all.c;
+      sum_l += (unsigned long long)cl_all.c;
+    }
+  }
+}
+
+// Pass 1 (one thread per SM set): single-block sets go to their translation class: clip
+// pattern of the block x residue of its first cell's address mod line_bytes (identical
+// active-cell boxes that are translates by a multiple of the line size have identical
+// sector and line counts).  Multi-block sets are appended to the direct list.
+__global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                               const DGpu* __restrict__ gs, unsigned int* __restrict__ scnt,
+                                               unsigned long long* __restrict__ srep,
+                                               unsigned long long* __restrict__ lists,
+                                               unsigned long long* __restrict__ slist,
+                                               unsigned long long* __restrict__ dlist) {
+  const long long total = pre[n].set;
+  for (long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x; item < total;
+       item += (long long)gridDim.x * blockDim.x) {
+    const int c = find_config<2>(pre, n, item);
+    const DPlan& P = plans[c];
+    const long long j = item - pre[c].set;
+    const long long nsm = gs[P.gid].g.n_sm;
+    const long long S0 = P.s + j;
+    const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
+    if (P.scls_R > 0 && kj == 1) {
+      const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
+      long long pl = 0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+      const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+      const long long gslot = (long long)c * kSSlots + slot;
+      if (atomicAdd(scnt + gslot, 1u) == 0u) {
+        srep[gslot] = (unsigned long long)S0;
+        slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
+      }
+    } else {
+      dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
+    }
+  }
+}
+
+// Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
+// directly evaluated multi-block SM sets.
+__global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                                const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
+                                                const unsigned int* __restrict__ scnt,
+                                                const unsigned long long* __restrict__ srep,
+                                                const unsigned long long* __restrict__ lists,
+                                                const unsigned long long* __restrict__ slist,
+                                                const unsigned long long* __restrict__ dlist,
+                                                unsigned long long* __restrict__ work) {
+  __shared__ SmBox s_mb[kMaxMembers];
+  __shared__ SmBox32 s_mb32[kMaxMembers];
+  __shared__ Tri s_pt[2 * kMaxPlanes];
+  __shared__ unsigned char s_der[kMaxPlanes];
+  __shared__ SmWarp s_sw[8];
+  __shared__ DGroup s_g[kMaxAcc];
+  __shared__ int s_ng;
+  __shared__ long long s_box[4];
+  __shared__ Tri s_red[(kRowThreads / 32) * 2];
+  const long long ncls = (long long)lists[1];
+  const long long total = ncls + (long long)lists[2];
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+    const bool cls = item < ncls;
+    const unsigned long long ent = cls ? slist[item] : dlist[item - ncls];
+    const int c = (int)(ent >> 32);
+    const unsigned low = (unsigned)(ent & 0xffffffffu);
+    const DPlan& P = plans[c];
+    const DGpu& G = gs[P.gid];
+    const long long nsm = G.g.n_sm;
+    unsigned long long mult = 1;
+    long long S0, kj;
+    if (cls) {
+      const long long gslot = (long long)c * kSSlots + low;
+      mult = scnt[gslot];
+      S0 = (long long)srep[gslot];
+      kj = 1;
+    } else {
+      S0 = P.s + low;
+      kj = (P.W - (long long)low + nsm - 1) / nsm;
+    }
+    unsigned long long ss, sl, un;
+    int n_ld = 0;
+    for (int f = 0; f < ks[P.kid].n_fields; ++f) n_ld += ks[P.kid].f[f].kinds & 1;
+    // one block and many load fields (LBM: one offset each): flat rows over the whole CTA;
+    // otherwise plane derivation + lane-per-run unions
+    if (kj == 1 && n_ld > 4) {
+      smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
+      if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
+    } else {        // several blocks: plane derivation + runs
+      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_mb32, s_pt, s_der, s_sw, ss, sl, un);
+      // every warp's lane 0 counted its planes' rows
+      if ((threadIdx.x & 31) == 0 && un) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
+    }
+    if (threadIdx.x == 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      atomicAdd(a + A_SM_SEC, ss * mult);
+      atomicAdd(a + A_SM_LIN, sl * mult);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a5 + a6: wave and layer sets
+// ranges: 0 = wave [s, s+W), 1 = L_y [Ly0, s), 2 = L_z [Lz0, s), 3 = L_y + wave, 4 = L_z + wave
+
+__device__ __forceinline__ int classify(const RangeInfo& R, long long r) {
+  if (!R.nonempty || r < R.ra || r > R.rl) return -1;
+  if (R.ra == R.rl) return 3;
+  if (r == R.ra) return 1;
+  if (r == R.rl) return 2;
+  return 0;
+}
+
+// Cached union of one row: a single component [x0, x1) (x0 >= x1: empty) or `multi`.
+struct UC {
+  long long x0, x1;
+  int single;
+};
+
+template <class Gen>
+__device__ __forceinline__ void row_union_c(const Gen& gen, long long R0, int le, int ls, int ll, Tri* ts, Tri* tl,
+                                            Tri* ts2, UC& uc) {
+  const long long INF = LLONG_MAX;
+  long long start = INF, mx_s = LLONG_MIN, mn_e = INF, mx_e = LLONG_MIN;
+  gen([&](long long xs, long long xe) {
+    start = xs < start ? xs : start;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  if (start == INF) {
+    uc = UC{0, 0, 1};
+    return;
+  }
+  if (mx_s <= mn_e) {
+    uc = UC{start, mx_e, 1};
+    const long long a0 = R0 + (start << le), a1 = R0 + ((mx_e - 1) << le);
+    if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
+    if (ts2) tri_add(*ts2, a0 >> ls, a1 >> ls);
+    if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
+    return;
+  }
+  uc.single = 0;
+  row_union(gen, R0, le, ls, ll, ts, tl, ts2);
+}
+
+template <class Gen>
+__device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, long long R0, int le, int ls, int ll,
+                                                 Tri* ts, Tri* tl, Tri* ts2, UC& uc) {
+  if (first) {
+    row_union_c(gen, R0, le, ls, ll, ts, tl, ts2, uc);
+  } else if (uc.single) {
+    if (uc.x0 < uc.x1) {
+      const long long a0 = R0 + (uc.x0 << le), a1 = R0 + ((uc.x1 - 1) << le);
+      if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
+      if (ts2) tri_add(*ts2, a0 >> ls, a1 >> ls);
+      if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
+    }
+  } else {
+    row_union(gen, R0, le, ls, ll, ts, tl, ts2);
+  }
+}
+
+constexpr int kRowWarps = 8;
+
+constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
+
 struct RI32 {
   int ra, rl;
   int iv[4][2];
@@ -1449,20 +1512,6 @@ struct WarpRowCtx {
   unsigned bm[kSegRows / 32];  // run-start bitmap of the current segment
   short rs[kSegRows + 2];      // run starts (ascending) + end
 };
-
-template <int NQ>
-__device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const T32 x{__shfl_down_sync(FULL, t[q].f, o), __shfl_down_sync(FULL, t[q].l, o),
-                  __shfl_down_sync(FULL, t[q].c, o)};
-      if (lane + o < 32) t[q] = t32_combine(t[q], x);
-    }
-  }
-}
 
 // Union of the candidates (range q1, mask m1) u (range q2, mask m2) over `run` consecutive rows
 // (row 0 at plane offset R0, rows `step` bytes apart), appended to the compile-time targets
