@@ -87,7 +87,7 @@ struct DPlan {
   // translation classes: 0 = disabled
   int32_t wcls_R, scls_R;        // residue slots per warp index / per SM set
   int64_t cls_pitch[3];          // the common pitch of every field when classes are enabled
-  int32_t cls_lg_elem, pad2;
+  int32_t cls_lg_elem, wpow2;    // wpow2: power-of-two block dims and T % 32 == 0
   int64_t n_warp_items, n_wclass_items, n_set_items, n_sclass_items, n_chunks, n_fields;
   uint64_t addr_evals;
   FDiv fd_BF[3];                 // division by BF[d] (cell -> block coordinate)

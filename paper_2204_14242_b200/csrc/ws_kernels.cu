@@ -321,6 +321,8 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   P.scls_R = (same && Rs >= 1 && Rs <= 64) ? (int)Rs : 0;
   for (int d = 0; d < 3; ++d) P.cls_pitch[d] = K.f[0].pitch[d];
   P.cls_lg_elem = K.f[0].lg_elem;
+  P.wpow2 = (T % 32 == 0) && !(cf.block[0] & (cf.block[0] - 1)) && !(cf.block[1] & (cf.block[1] - 1)) &&
+            !(cf.block[2] & (cf.block[2] - 1));
   P.status = WS_OK;
 }
 
@@ -779,6 +781,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
     bool direct = false;
     unsigned long long key = ~0ull;
     long long B = 0;
+    int wrep_w = 0;
     // one search per warp (lanes hold consecutive items), then each lane advances
     int c0 = find_config<0>(pre, n, base);
     if (have) {
@@ -788,6 +791,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
       const long long wi = item - pre[c].warp;
       B = P.s + wi / P.nwarps;
       const int w = (int)(wi % P.nwarps);
+      wrep_w = w;
       if (P.wcls_R > 0) {
         const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
         const int t0 = w * 32;
@@ -796,7 +800,11 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
 #pragma unroll
         for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d]);
         const int res = (int)(pl & (P.wcls_R - 1));  // (pl * elem) mod M, in elements
-        const unsigned slot = (unsigned)(((w * 64 + res) << 3) | clip_pattern(P, bc));
+        const int pat = clip_pattern(P, bc);
+        // power-of-two blocks: every warp covers an aligned sub-box with the same relative lane
+        // pattern, so in an unclipped block the warp index does not matter
+        const int wk = (P.wpow2 && pat == 0) ? 0 : w;
+        const unsigned slot = (unsigned)(((wk * 64 + res) << 3) | pat);
         key = ((unsigned long long)c << 32) | slot;
         my_units += 32;
       } else {
@@ -810,7 +818,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
       const unsigned slot = (unsigned)(key & 0xffffffffu);
       const long long gslot = (long long)cc * kWSlots + slot;
       if (atomicAdd(wcnt + gslot, (unsigned)__popc(peers)) == 0u) {
-        wrep[gslot] = (unsigned long long)B;
+        wrep[gslot] = ((unsigned long long)B << 5) | (unsigned long long)wrep_w;
         const unsigned long long idx = atomicAdd(lists + 0, 1ull);
         wlist[idx] = key;
       }
@@ -858,8 +866,8 @@ __global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans,
     const DPlan& P = plans[c];
     const long long gslot = (long long)c * kWSlots + slot;
     const unsigned int cnt = wcnt[gslot];
-    const long long B = (long long)wrep[gslot];
-    const int w = (int)(slot >> 9);
+    const long long B = (long long)(wrep[gslot] >> 5);
+    const int w = (int)(wrep[gslot] & 31ull);
     const Lane L = lane_setup(P, B, w, lane);
     long long lup, wf, rl, rs;
     eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)c * kMaxInstr, L, lane, lup, wf, rl, rs);
