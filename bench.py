@@ -227,7 +227,6 @@ def run_native(args, rank, world, local):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    ctx.profile_enable(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -242,9 +241,16 @@ def run_native(args, rank, world, local):
     t_wall1 = time.time()
     if world > 1:
         dist.barrier()
+    ms_total = sum(a.elapsed_time(b) for a, b in evs)
+    # per-kernel durations (CUDA events on each kernel's own stream) from a separate pass of
+    # the same steps: event recording disables the graph replay of the timed loop
+    ctx.profile_enable(True)
+    for i in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
     ctx.profile_enable(False)
     prof = ctx.profile_read()
-    ms_total = sum(a.elapsed_time(b) for a, b in evs)
     time.sleep(0.2)
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)

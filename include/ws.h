@@ -59,7 +59,7 @@ ws_status ws_set_stream(ws_ctx* ctx, void* cuda_stream);
  * (P:157-161 with the unknown base pointer replaced by the alignment).
  * Requirements: pitch[0] == 1, pitch[1] >= extent[0], pitch[2] >= pitch[1]*extent[1]
  * (rows and planes never overlap); elem_bytes in {1,2,4,8,16,32}; one z-plane
- * (pitch[2] * elem_bytes) smaller than 2 GiB (WS_ELIMIT).  */
+ * (pitch[2] * elem_bytes) at most 2 GiB - 16 KiB (WS_ELIMIT).  */
 typedef struct {
   int64_t extent[3];
   int64_t pitch[3];
@@ -88,7 +88,7 @@ typedef struct {
 
 /* Deep-copies the description.  Errors: WS_EINVAL (counts, layout, elem,
  * empty domain), WS_EBOUNDS (dom +- offsets leaves a field), WS_ELIMIT (a
- * field has more than 16 distinct x-offset runs, or a z-plane >= 2 GiB).
+ * field has more than 16 distinct x-offset runs, or a z-plane > 2 GiB - 16 KiB).
  * *kernel_id receives a new id. */
 ws_status ws_describe_kernel(ws_ctx* ctx, const ws_kernel* k, uint32_t* kernel_id);
 
@@ -98,7 +98,7 @@ typedef struct {
   uint32_t n_sm;
   uint32_t max_thr_sm, max_blk_sm, max_thr_blk, regs_sm;   /* occupancy limits (Q10) */
   uint32_t sector_bytes;       /* 32  (power of two, >= every elem_bytes used)  */
-  uint32_t line_bytes;         /* 128 (power of two, multiple of sector_bytes)   */
+  uint32_t line_bytes;         /* 128 (power of two, multiple of sector_bytes, <= 4096) */
   uint32_t n_banks;            /* 16  (power of two)                            */
   uint32_t bank_bytes;         /* 8   (power of two)                            */
   uint32_t half_warp;          /* 16  (power of two dividing 32)                */
@@ -109,7 +109,8 @@ typedef struct {
   double hit_abc[4][3];        /* R(O) = a exp(-b exp(-c O)) for L1, L2-over-y, L2-over-z, L2-store */
 } ws_gpu;
 
-/* Deep-copies.  Errors: WS_EINVAL (zero / non-power-of-two geometry, ...). */
+/* Deep-copies.  Errors: WS_EINVAL (zero / non-power-of-two geometry, ...),
+ * WS_ELIMIT (line_bytes > 4096). */
 ws_status ws_describe_gpu(ws_ctx* ctx, const ws_gpu* g, uint32_t* gpu_id);
 
 /* ------------------------------------------------------------------ configurations */

@@ -48,6 +48,22 @@ struct ws_ctx {
   // aux streams + fork/join events for the concurrent worker chains
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+  // CUDA graph of the whole estimate launch sequence, captured on `cap` and replayed on
+  // `stream` while the launch arguments (key) are unchanged
+  struct GKey {
+    const void *cfgs, *out, *scratch, *dk, *dg;
+    size_t n;
+    int nk, ng;
+    bool operator==(const GKey& o) const {
+      return cfgs == o.cfgs && out == o.out && scratch == o.scratch && dk == o.dk && dg == o.dg && n == o.n &&
+             nk == o.nk && ng == o.ng;
+    }
+  };
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  GKey gkey{};
+  uint32_t g_launches = 0;
+  bool graphs = true;
   // 2 events (start, end) per kernel kind, kinds [first_kind, first_kind + nk)
   cudaEvent_t* take_events(int first_kind, int nk) {
     Rec r;
@@ -179,13 +195,15 @@ ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out) {
   if (!c) return WS_ENOMEM;
   c->device = cuda_device;
   c->stream = (cudaStream_t)cuda_stream;
+  c->graphs = !(getenv("WS_GRAPH") && getenv("WS_GRAPH")[0] == '0');
   cudaDeviceGetAttribute(&c->n_sm_dev, cudaDevAttrMultiProcessorCount, cuda_device);
   if (c->n_sm_dev <= 0) c->n_sm_dev = 148;
   if (cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->join[0], cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->join[1], cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->join[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) {
     ws_destroy(c);
     return WS_ECUDA;
   }
@@ -208,6 +226,8 @@ void ws_destroy(ws_ctx* c) {
     if (c->join[i]) cudaEventDestroy(c->join[i]);
   }
   if (c->fork) cudaEventDestroy(c->fork);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->cap) cudaStreamDestroy(c->cap);
   delete c;
 }
 
@@ -298,8 +318,9 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
       if (F.extent[d] < 1) return fail(c, WS_EINVAL, "field extent < 1");
     if (F.pitch[0] != 1 || F.pitch[1] < F.extent[0] || F.pitch[2] < F.pitch[1] * F.extent[1])
       return fail(c, WS_EINVAL, "layout: need pitch[0]==1, pitch[1]>=extent[0], pitch[2]>=pitch[1]*extent[1]");
-    if ((F.pitch[2] * (int64_t)F.elem_bytes) >= (int64_t(1) << 31) || F.extent[2] >= (int64_t(1) << 31))
-      return fail(c, WS_ELIMIT, "a z-plane of a field must be smaller than 2 GiB");
+    // plane-relative 32-bit unit arithmetic adds < 2 lines (<= 8 KiB) to in-plane offsets
+    if ((F.pitch[2] * (int64_t)F.elem_bytes) > (int64_t(1) << 31) - (int64_t(1) << 14) || F.extent[2] >= (int64_t(1) << 31))
+      return fail(c, WS_ELIMIT, "a z-plane of a field must be at most 2 GiB - 16 KiB");
     for (int d = 0; d < 3; ++d) {
       G.ext[d] = F.extent[d];
       G.pitch[d] = F.pitch[d];
@@ -400,6 +421,7 @@ ws_status ws_describe_gpu(ws_ctx* c, const ws_gpu* g, uint32_t* id) {
   if (D.lg_sector < 0 || D.lg_line < 0 || D.lg_line < D.lg_sector || D.lg_bank < 0 || D.lg_hw < 0 || g->half_warp > 32 ||
       D.lg_nbanks < 0 || g->n_banks > 256)
     return fail(c, WS_EINVAL, "sector/line/bank/half-warp geometry must be powers of two (line >= sector, half_warp <= 32)");
+  if (g->line_bytes > 4096) return fail(c, WS_ELIMIT, "line_bytes must be <= 4096");
   if (g->pair_window_bytes < 1 || g->l2_sections < 1 || g->l1_bytes < 1 || g->l2_bytes < 1)
     return fail(c, WS_EINVAL, "cache sizes / window must be >= 1");
   if (!(g->clock_hz > 0) || !(g->dram_bw > 0) || !(g->l2_bw > 0)) return fail(c, WS_EINVAL, "rates must be > 0");
@@ -430,6 +452,37 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   st.fork = c->fork;
   st.join[0] = c->join[0];
   st.join[1] = c->join[1];
+  // graph replay unless profiling (per-kernel events), serial diagnostics, or the caller's
+  // stream is itself being captured (then the launches become part of the caller's graph)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (c->graphs && !ev && !serial && cs == cudaStreamCaptureStatusNone) {
+    const ws_ctx::GKey key{d_cfgs, d_out, c->scratch, c->dk, c->dg, n, (int)c->hk.size(), (int)c->hg.size()};
+    if (!c->gexec || !(key == c->gkey)) {
+      if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+      st.main = c->cap;
+      cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
+      launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st, c->n_sm_dev,
+                      &c->g_launches, nullptr);
+      cudaGraph_t g = nullptr;
+      e = cudaStreamEndCapture(c->cap, &g);
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&c->gexec, g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        c->gexec = nullptr;
+        return cuda_fail(c, e, "graph instantiate");
+      }
+      c->gkey = key;
+    }
+    cudaError_t e = cudaGraphLaunch(c->gexec, c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "graph launch");
+    c->last_launches = c->g_launches;
+    return WS_OK;
+  }
   int e = launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st,
                           c->n_sm_dev, &c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "launch");

@@ -5,7 +5,7 @@ import numpy as np, torch
 import workloads as W
 from paper_2204_14242_b200 import Context, config_array, result_dicts
 
-def run(name, k, g, cfgs, reps=5):
+def run(name, k, g, cfgs, reps=20):
     ctx = Context(0, torch.cuda.current_stream().cuda_stream)
     kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
     a = config_array(kid, gid, cfgs)
@@ -15,15 +15,21 @@ def run(name, k, g, cfgs, reps=5):
     for _ in range(2):
         ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
     torch.cuda.synchronize()
-    ctx.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
         ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
     e1.record(); torch.cuda.synchronize()
-    prof = ctx.profile_read()
     tot = e0.elapsed_time(e1) / reps
-    print(f"{name}: n={n} step {tot:.3f} ms -> {n/tot*1e3:.0f} configs/s")
+    ctx.profile_enable(True)
+    e0.record()
+    for _ in range(reps):
+        ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
+    e1.record(); torch.cuda.synchronize()
+    ctx.profile_enable(False)
+    prof = ctx.profile_read()
+    totp = e0.elapsed_time(e1) / reps
+    print(f"{name}: n={n} step {tot:.3f} ms (profiled {totp:.3f}) -> {n/tot*1e3:.0f} configs/s")
     for kname, (ms, cnt) in prof.items():
         if cnt: print(f"   {kname:8s} {ms/cnt:9.4f} ms")
 
@@ -31,4 +37,4 @@ run("configs1 K25 512^3 A100 168", W.k25(512), W.gpu_a100(), W.space_stencil_pap
 run("configs2 LBM15 256^3 A100 49", W.lbm15(256), W.gpu_a100(), W.space_lbm())
 run("configs2 LBM27 256^3 A100 49", W.lbm27(256), W.gpu_a100(), W.space_lbm())
 run("configs0 K7 64^3 V100 16", W.k7(64), W.gpu_v100(), W.space_k7())
-run("extended K25 512^3 A100", W.k25(512), W.gpu_a100(), W.space_extended(), reps=2)
+run("extended K25 512^3 A100", W.k25(512), W.gpu_a100(), W.space_extended(), reps=3)

@@ -147,6 +147,16 @@ def test_describe_errors(ctx):
     g["sector_bytes"] = 24
     with pytest.raises(WSError):
         ctx.describe_gpu(g)
+    g = W.gpu_v100()
+    g["line_bytes"] = 8192                       # 32-bit plane-relative unit arithmetic limit
+    with pytest.raises(WSError) as e:
+        ctx.describe_gpu(g)
+    assert e.value.status == 2
+    big = W.k7(8)                                # z-plane of 2 GiB (pitch[2] * 8 B = 2^31)
+    big["fields"][0] = dict(big["fields"][0], extent=(1 << 14, 1 << 14, 4), pitch=(1, 1 << 14, 1 << 28))
+    with pytest.raises(WSError) as e:
+        ctx.describe_kernel(big)
+    assert e.value.status == 2
 
 
 # ----------------------------------------------------------------- full size (bench launch configuration)
