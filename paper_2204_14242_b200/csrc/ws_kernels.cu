@@ -230,6 +230,35 @@ __device__ __forceinline__ int find_config(const DPrefix* pre, int n, long long 
   return lo;
 }
 
+template <int MEMBER>
+__device__ __forceinline__ long long prefix_member(const DPrefix& p) {
+  return MEMBER == 0   ? p.warp
+         : MEMBER == 1 ? p.wclass
+         : MEMBER == 2 ? p.set
+         : MEMBER == 3 ? p.sclass
+         : MEMBER == 4 ? p.chunk
+                       : p.fold;
+}
+
+// find_config by the whole warp (item warp-uniform): 32-ary search, one load round per
+// factor 32 of n, starting from the hint c when item still lies in config c.
+template <int MEMBER>
+__device__ __forceinline__ int find_config_warp(const DPrefix* pre, int n, long long item, int hint) {
+  const int lane = threadIdx.x & 31;
+  if (hint >= 0 && item >= prefix_member<MEMBER>(pre[hint]) && item < prefix_member<MEMBER>(pre[hint + 1]))
+    return hint;
+  int lo = 0, hi = n - 1;  // invariant: member(pre[lo]) <= item
+  while (hi > lo) {
+    const int stride = (hi - lo + 32) >> 5;
+    const int idx = lo + lane * stride;
+    const bool le = idx <= hi && prefix_member<MEMBER>(pre[idx]) <= item;
+    const unsigned b = __ballot_sync(FULL, le);
+    lo += (31 - __clz(b)) * stride;
+    hi = min(hi, lo + stride - 1);
+  }
+  return lo;
+}
+
 // ------------------------------------------------------------------ a1: plan
 __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, const DGpu* gs, int ng, DPlan& P) {
   P = DPlan();
@@ -1086,11 +1115,13 @@ __device__ __forceinline__ T32 run_triple32(const RowFn& row, int step, int run,
   return acc;
 }
 
+// lanes [0, cnt) hold data (lanes >= cnt empty): steps with offset >= cnt are no-ops
 template <int NQ>
-__device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ]) {
+__device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ], int cnt = 32) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
+    if (o >= cnt) break;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const T32 x{__shfl_down_sync(FULL, t[q].f, o), __shfl_down_sync(FULL, t[q].l, o),
@@ -1300,9 +1331,11 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
               }
             }
             T32 tt[2] = {ts, tl};
-            warp_ordered_reduce32<2>(tt);
-            ps = t32_combine(ps, T32{__shfl_sync(FULL, tt[0].f, 0), __shfl_sync(FULL, tt[0].l, 0), __shfl_sync(FULL, tt[0].c, 0)});
-            pl = t32_combine(pl, T32{__shfl_sync(FULL, tt[1].f, 0), __shfl_sync(FULL, tt[1].l, 0), __shfl_sync(FULL, tt[1].c, 0)});
+            warp_ordered_reduce32<2>(tt, nruns - rb);
+            if (lane == 0) {  // ps, pl: lane 0 only
+              ps = t32_combine(ps, tt[0]);
+              pl = t32_combine(pl, tt[1]);
+            }
           }
           __syncwarp();
         }
@@ -1522,12 +1555,15 @@ struct WarpRowCtx {
 };
 
 // Union of the candidates (range q1, mask m1) u (range q2, mask m2) over `run` consecutive rows
-// (row 0 at plane offset R0, rows `step` bytes apart), appended to the compile-time targets
-// t[TS] (sectors), t[TL] (lines), t[TS2] (sectors again); -1 = none.
-template <int TS, int TL, int TS2>
-__device__ __forceinline__ void row_emit32(T32 (&t)[kNQ], const WarpRowCtx& X, const DField& F, unsigned long long m1,
-                                           int q1, unsigned long long m2, int q2, int R0, int step, int run, int le,
-                                           int ls, int ll) {
+// (row 0 at plane offset R0, rows `step` bytes apart): sector triple (if want_s) and line
+// triple (if want_l).  One out-of-line copy (instruction-cache footprint); the callers fold
+// the triples into their compile-time targets.
+struct T32x2 {
+  T32 s, l;
+};
+__device__ __noinline__ T32x2 row_emit32(const WarpRowCtx& X, const DField& F, unsigned long long m1, int q1,
+                                         unsigned long long m2, int q2, int R0, int step, int run, int le, int ls,
+                                         int ll, bool want_s, bool want_l) {
   auto gen = [&](auto&& cb) {
     unsigned long long m = m1;
     while (m) {
@@ -1552,37 +1588,46 @@ __device__ __forceinline__ void row_emit32(T32 (&t)[kNQ], const WarpRowCtx& X, c
     mn_e = xe < mn_e ? xe : mn_e;
     mx_e = xe > mx_e ? xe : mx_e;
   });
-  if (mn_s == INF) return;
-  T32 ts = t32_empty(), tl = t32_empty();
+  T32x2 o{t32_empty(), t32_empty()};
+  if (mn_s == INF) return o;
   if (mx_s <= mn_e) {  // one interval per row
     const int a0 = R0 + (mn_s << le), a1 = R0 + ((mx_e - 1) << le);
-    if (TS >= 0 || TS2 >= 0)
-      ts = run_triple32([&](int r) {
+    if (want_s)
+      o.s = run_triple32([&](int r) {
         const int s0 = (a0 + r * step) >> ls, s1 = (a1 + r * step) >> ls;
         return T32{s0, s1, s1 - s0 + 1};
       }, step, run, ls);
-    if (TL >= 0)
-      tl = run_triple32([&](int r) {
+    if (want_l)
+      o.l = run_triple32([&](int r) {
         const int s0 = (a0 + r * step) >> ll, s1 = (a1 + r * step) >> ll;
         return T32{s0, s1, s1 - s0 + 1};
       }, step, run, ll);
   } else {  // several intervals per row (the same components in every row of the run)
-    if (TS >= 0 || TS2 >= 0)
-      ts = run_triple32([&](int r) {
+    if (want_s)
+      o.s = run_triple32([&](int r) {
         T32 x = t32_empty();
         row_union32(gen, R0 + r * step, le, ls, x);
         return x;
       }, step, run, ls);
-    if (TL >= 0)
-      tl = run_triple32([&](int r) {
+    if (want_l)
+      o.l = run_triple32([&](int r) {
         T32 x = t32_empty();
         row_union32(gen, R0 + r * step, le, ll, x);
         return x;
       }, step, run, ll);
   }
-  if (TS >= 0) t[TS >= 0 ? TS : 0] = t32_combine(t[TS >= 0 ? TS : 0], ts);
-  if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = t32_combine(t[TS2 >= 0 ? TS2 : 0], ts);
-  if (TL >= 0) t[TL >= 0 ? TL : 0] = t32_combine(t[TL >= 0 ? TL : 0], tl);
+  return o;
+}
+
+// compile-time targets t[TS] (sectors), t[TL] (lines), t[TS2] (sectors again); -1 = none
+template <int TS, int TL, int TS2>
+__device__ __forceinline__ void row_emit32(T32 (&t)[kNQ], const WarpRowCtx& X, const DField& F, unsigned long long m1,
+                                           int q1, unsigned long long m2, int q2, int R0, int step, int run, int le,
+                                           int ls, int ll) {
+  const T32x2 o = row_emit32(X, F, m1, q1, m2, q2, R0, step, run, le, ls, ll, TS >= 0 || TS2 >= 0, TL >= 0);
+  if (TS >= 0) t[TS >= 0 ? TS : 0] = t32_combine(t[TS >= 0 ? TS : 0], o.s);
+  if (TS2 >= 0) t[TS2 >= 0 ? TS2 : 0] = t32_combine(t[TS2 >= 0 ? TS2 : 0], o.s);
+  if (TL >= 0) t[TL >= 0 ? TL : 0] = t32_combine(t[TL >= 0 ? TL : 0], o.l);
 }
 
 __device__ __forceinline__ int fdiv32(int n, FDiv f) { return (int)((__umulhi((unsigned)n, f.m) + (unsigned)n) >> f.l); }
@@ -1612,8 +1657,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
   const long long nwg = (long long)gridDim.x * kRowWarps;
   unsigned long long my_ops = 0;
   int ranges_c = -1;
+  int c = -1;
   for (long long item = (long long)blockIdx.x * kRowWarps + wid; item < total; item += nwg) {
-    const int c = find_config<4>(pre, n, item);
+    c = find_config_warp<4>(pre, n, item, c);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
@@ -1773,11 +1819,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
             row_emit32<5, 6, 8>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0, pystep, run, le, ls, ll);
           }
         }
-        warp_ordered_reduce32<kNQ>(t);
+        warp_ordered_reduce32<kNQ>(t, nruns - rb);
+        if (lane == 0)  // pt: lane 0 only
 #pragma unroll
-        for (int q = 0; q < kNQ; ++q)
-          pt[q] = t32_combine(pt[q], T32{__shfl_sync(FULL, t[q].f, 0), __shfl_sync(FULL, t[q].l, 0),
-                                         __shfl_sync(FULL, t[q].c, 0)});
+          for (int q = 0; q < kNQ; ++q) pt[q] = t32_combine(pt[q], t[q]);
       }
       __syncwarp();
     }
@@ -1806,10 +1851,10 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
                                               const DRowInfo* __restrict__ rowinfo,
                                               const long long* __restrict__ chunkres,
                                               unsigned long long* __restrict__ acc) {
+  __shared__ Tri s_red[(256 / 32) * kNQ];
   const long long total = pre[n].fold;
-  const int lane = threadIdx.x & 31;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nw) {
+  const int tid = threadIdx.x;
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {  // one CTA per (config, field)
     const int c = find_config<5>(pre, n, item);
     const int fi = (int)(item - pre[c].fold);
     const DPlan& P = plans[c];
@@ -1819,12 +1864,12 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
     const long long pbytes = F.pitch[2] << F.lg_elem;
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
-    const long long per_l = (nch + 31) / 32;
+    const long long per_l = (nch + blockDim.x - 1) / blockDim.x;
     const long long* base = chunkres + (pre[c].chunk + RI.chunk_begin) * (kNQ * 3);
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
-    for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
+    for (long long k = tid * per_l; k < nch && k < (tid + 1) * per_l; ++k) {
       long long src = k;
       const long long mk = base[k * (kNQ * 3) + 2];
       if (mk < 0) src = -mk - 2;  // derived plane: representative plane index
@@ -1837,15 +1882,8 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
         t[q] = tri_combine(t[q], cq ? Tri{in[q * 3] + d, in[q * 3 + 1] + d, cq} : tri_empty());
       }
     }
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-      for (int q = 0; q < kNQ; ++q) {
-        Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
-        if (lane + o < 32) t[q] = tri_combine(t[q], x);
-      }
-    }
-    if (lane == 0 && nch > 0) {
+    cta_ordered_reduce<kNQ>(t, s_red);
+    if (tid == 0 && nch > 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_WLD, (unsigned long long)t[0].c);
       atomicAdd(a + A_WST, (unsigned long long)t[1].c);
@@ -1995,7 +2033,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_rows<<<persist, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
   end(K_ROWS, b);
   beg(K_FOLD, b);
-  k_fold<<<n_sm_dev * 2, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
+  k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
   end(K_FOLD, b);
   beg(K_SMSET, a);
   k_smset<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, s.prefix, n, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
