@@ -1135,9 +1135,73 @@ struct SmBox32 {
   int x0, x1, y0, y1, z0, z1;
 };
 
+struct T32x2 {
+  T32 s, l;
+};
+
 constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
 constexpr int kSegRowsS = 1024;  // rows of a plane per SM-set run segment
 
+// One run of rows [y, y + run) of plane z (row y at plane offset R0): candidates of its first
+// row (member boxes x offset groups), their union, the run's sector and line triples.
+__device__ __noinline__ T32x2 smset_run(const SmBox32* mb, int nm, const DKernel& K, const DField& F, int g0, int ng,
+                                        int y, int z, int R0, int step, int run, int le, int ls, int ll) {
+  unsigned long long mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int g = 0; g < ng; ++g) {
+    const DGroup gr = K.g[g0 + g];
+    if (gr.kind != 0) continue;
+    const int yy = y - gr.oy, zz = z - gr.oz;
+#pragma unroll 4
+    for (int m = 0; m < nm; ++m) {
+      const SmBox32& bx = mb[m];
+      if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1) mk[m >> 2] |= 1ull << ((m & 3) * 16 + gr.run);
+    }
+  }
+  auto gen = [&](auto&& cb) {
+    for (int w = 0; w < ((nm + 3) >> 2); ++w) {
+      unsigned long long q = mk[w];
+      while (q) {
+        const int bb = __ffsll((long long)q) - 1;
+        q &= q - 1;
+        const SmBox32& bx = mb[w * 4 + (bb >> 4)];
+        cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
+      }
+    }
+  };
+  const int INF = 0x7fffffff;
+  int mn_s = INF, mx_s = -INF, mn_e = INF, mx_e = -INF;
+  gen([&](int xs, int xe) {
+    mn_s = xs < mn_s ? xs : mn_s;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  T32x2 o{t32_empty(), t32_empty()};
+  if (mn_s == INF) return o;
+  if (mx_s <= mn_e) {
+    const int a0 = R0 + (mn_s << le), a1 = R0 + ((mx_e - 1) << le);
+    o.s = run_triple32([&](int r) {
+      const int s0 = (a0 + r * step) >> ls, s1 = (a1 + r * step) >> ls;
+      return T32{s0, s1, s1 - s0 + 1};
+    }, step, run, ls);
+    o.l = run_triple32([&](int r) {
+      const int s0 = (a0 + r * step) >> ll, s1 = (a1 + r * step) >> ll;
+      return T32{s0, s1, s1 - s0 + 1};
+    }, step, run, ll);
+  } else {
+    o.s = run_triple32([&](int r) {
+      T32 x = t32_empty();
+      row_union32(gen, R0 + r * step, le, ls, x);
+      return x;
+    }, step, run, ls);
+    o.l = run_triple32([&](int r) {
+      T32 x = t32_empty();
+      row_union32(gen, R0 + r * step, le, ll, x);
+      return x;
+    }, step, run, ll);
+  }
+  return o;
+}
 // Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
 // dispatch, Q9) by one CTA.  Row (y,z) of field phi holds element x iff some member box
 // contains (x - ox, y - oy, z - oz) for a load offset o.  Per z-plane: if every
@@ -1216,149 +1280,118 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
         if (lane == 0) pder[p] = same ? 1 : 0;
       }
       __syncthreads();
-      // (b) computed planes: one warp per plane.  A row's candidates change only where some
-      //     y - oy crosses a member's y edge: lanes mark these breakpoints, then take one run
-      //     each (candidates of its first row, union, closed-form run triple), in 32-bit
-      //     plane-relative arithmetic (see k_rows).
-      for (int p = wid; p < np; p += nwp) {
-        if (pder[p]) continue;
-        const int z = (int)(zs + p);
-        SmWarp& Wp = sw[wid];
-        const long long R0p = align + ((py * y0 + pz * (long long)z) << le);
-        const long long Bp = (R0p >> ll) << ll;
-        const int off0 = (int)(R0p - Bp), step = (int)pystep;
-        T32 ps = t32_empty(), pl = t32_empty();
-        for (int ys = 0; ys < (int)ny; ys += kSegRowsS) {
-          const int nseg = (int)ny - ys < kSegRowsS ? (int)ny - ys : kSegRowsS;
-          const int nwd = (nseg + 31) >> 5;
-          for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
-          __syncwarp();
-          if (lane == 0) atomicOr(&Wp.bm[0], 1u);
-          for (int k = lane; k < npairs; k += 32) {
-            const DGroup gr = K.g[g0 + k / nm];
-            if (gr.kind != 0) continue;
-            const SmBox32& bx = mb32[k % nm];
-            const int zz = z - gr.oz;
-            if (zz < bx.z0 || zz >= bx.z1) continue;
-            const int e0 = bx.y0 + gr.oy - (int)y0 - ys, e1 = bx.y1 + gr.oy - (int)y0 - ys;
-            if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
-            if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
+      // (b) computed planes, dealt round-robin to the warps in order of their rank among the
+      //     computed planes (balanced): one warp per plane.  A row's candidates change only
+      //     where some y - oy crosses a member's y edge: lanes mark these breakpoints, then take
+      //     one run each (smset_run), in 32-bit plane-relative arithmetic (see k_rows).
+      int rank0 = 0;  // computed planes before the current 32-plane window
+      for (int pb = 0; pb < np; pb += 32) {
+        const int pw = pb + lane;
+        const unsigned cm = __ballot_sync(FULL, pw < np && !pder[pw]);
+        unsigned mine = 0;  // planes of this window whose rank % nwp == wid
+        {
+          unsigned q = cm;
+          int r = rank0;
+          while (q) {
+            const int b = __ffs(q) - 1;
+            q &= q - 1;
+            if (r % nwp == wid) mine |= 1u << b;
+            ++r;
           }
-          __syncwarp();
-          const int wpl = (nwd + 31) >> 5;
-          int cnt = 0;
-          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(Wp.bm[w]);
-          int pos = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL, pos, o);
-            if (lane >= o) pos += v;
-          }
-          const int nruns = __shfl_sync(FULL, pos, 31);
-          pos -= cnt;
-          for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
-            unsigned bits = Wp.bm[w];
-            while (bits) {
-              const int bt = __ffs(bits) - 1;
-              bits &= bits - 1;
-              Wp.rs[pos++] = (short)(w * 32 + bt);
-            }
-          }
-          if (lane == 0) Wp.rs[nruns] = (short)nseg;
-          __syncwarp();
-          for (int rb = 0; rb < nruns; rb += 32) {
-            T32 ts = t32_empty(), tl = t32_empty();
-            const int j = rb + lane;
-            if (j < nruns) {
-              const int yr = ys + Wp.rs[j];  // row index inside the box
-              const int y = (int)y0 + yr;
-              const int run = Wp.rs[j + 1] - Wp.rs[j];
-              const int R0 = off0 + yr * step;
-              unsigned long long mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-              for (int g = 0; g < ng; ++g) {
-                const DGroup gr = K.g[g0 + g];
-                if (gr.kind != 0) continue;
-                const int yy = y - gr.oy, zz = z - gr.oz;
-#pragma unroll 4
-                for (int m = 0; m < nm; ++m) {
-                  const SmBox32& bx = mb32[m];
-                  if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
-                    mk[m >> 2] |= 1ull << ((m & 3) * 16 + gr.run);
-                }
-              }
-              auto gen = [&](auto&& cb) {
-                for (int w = 0; w < ((nm + 3) >> 2); ++w) {
-                  unsigned long long q = mk[w];
-                  while (q) {
-                    const int bb = __ffsll((long long)q) - 1;
-                    q &= q - 1;
-                    const SmBox32& bx = mb32[w * 4 + (bb >> 4)];
-                    cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
-                  }
-                }
-              };
-              const int INF = 0x7fffffff;
-              int mn_s = INF, mx_s = -INF, mn_e = INF, mx_e = -INF;
-              gen([&](int xs, int xe) {
-                mn_s = xs < mn_s ? xs : mn_s;
-                mx_s = xs > mx_s ? xs : mx_s;
-                mn_e = xe < mn_e ? xe : mn_e;
-                mx_e = xe > mx_e ? xe : mx_e;
-              });
-              if (mn_s != INF) {
-                if (mx_s <= mn_e) {
-                  const int a0 = R0 + (mn_s << le), a1 = R0 + ((mx_e - 1) << le);
-                  ts = run_triple32([&](int r) {
-                    const int s0 = (a0 + r * step) >> ls, s1 = (a1 + r * step) >> ls;
-                    return T32{s0, s1, s1 - s0 + 1};
-                  }, step, run, ls);
-                  tl = run_triple32([&](int r) {
-                    const int s0 = (a0 + r * step) >> ll, s1 = (a1 + r * step) >> ll;
-                    return T32{s0, s1, s1 - s0 + 1};
-                  }, step, run, ll);
-                } else {
-                  ts = run_triple32([&](int r) {
-                    T32 x = t32_empty();
-                    row_union32(gen, R0 + r * step, le, ls, x);
-                    return x;
-                  }, step, run, ls);
-                  tl = run_triple32([&](int r) {
-                    T32 x = t32_empty();
-                    row_union32(gen, R0 + r * step, le, ll, x);
-                    return x;
-                  }, step, run, ll);
-                }
-              }
-            }
-            T32 tt[2] = {ts, tl};
-            warp_ordered_reduce32<2>(tt, nruns - rb);
-            if (lane == 0) {  // ps, pl: lane 0 only
-              ps = t32_combine(ps, tt[0]);
-              pl = t32_combine(pl, tt[1]);
-            }
-          }
-          __syncwarp();
         }
-        if (lane == 0) {
-          const long long bs = Bp >> ls, bl = Bp >> ll;
-          pt[2 * p] = ps.c ? Tri{ps.f + bs, ps.l + bs, ps.c} : tri_empty();
-          pt[2 * p + 1] = pl.c ? Tri{pl.f + bl, pl.l + bl, pl.c} : tri_empty();
-          units += (unsigned long long)ny;
+        rank0 += __popc(cm);
+        while (mine) {
+          const int p = pb + __ffs(mine) - 1;
+          mine &= mine - 1;
+          const int z = (int)(zs + p);
+          SmWarp& Wp = sw[wid];
+          const long long R0p = align + ((py * y0 + pz * (long long)z) << le);
+          const long long Bp = (R0p >> ll) << ll;
+          const int off0 = (int)(R0p - Bp), step = (int)pystep;
+          T32 ps = t32_empty(), pl = t32_empty();
+          for (int ys = 0; ys < (int)ny; ys += kSegRowsS) {
+            const int nseg = (int)ny - ys < kSegRowsS ? (int)ny - ys : kSegRowsS;
+            const int nwd = (nseg + 31) >> 5;
+            for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
+            __syncwarp();
+            if (lane == 0) atomicOr(&Wp.bm[0], 1u);
+            for (int k = lane; k < npairs; k += 32) {
+              const DGroup gr = K.g[g0 + k / nm];
+              if (gr.kind != 0) continue;
+              const SmBox32& bx = mb32[k % nm];
+              const int zz = z - gr.oz;
+              if (zz < bx.z0 || zz >= bx.z1) continue;
+              const int e0 = bx.y0 + gr.oy - (int)y0 - ys, e1 = bx.y1 + gr.oy - (int)y0 - ys;
+              if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
+              if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
+            }
+            __syncwarp();
+            const int wpl = (nwd + 31) >> 5;
+            int cnt = 0;
+            for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(Wp.bm[w]);
+            int pos = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int v = __shfl_up_sync(FULL, pos, o);
+              if (lane >= o) pos += v;
+            }
+            const int nruns = __shfl_sync(FULL, pos, 31);
+            pos -= cnt;
+            for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
+              unsigned bits = Wp.bm[w];
+              while (bits) {
+                const int bt = __ffs(bits) - 1;
+                bits &= bits - 1;
+                Wp.rs[pos++] = (short)(w * 32 + bt);
+              }
+            }
+            if (lane == 0) Wp.rs[nruns] = (short)nseg;
+            __syncwarp();
+            for (int rb = 0; rb < nruns; rb += 32) {
+              T32 tt[2] = {t32_empty(), t32_empty()};
+              const int j = rb + lane;
+              if (j < nruns) {
+                const int yr = ys + Wp.rs[j];  // row index inside the box
+                const T32x2 o = smset_run(mb32, nm, K, F, g0, ng, (int)y0 + yr, z, off0 + yr * step, step,
+                                          Wp.rs[j + 1] - Wp.rs[j], le, ls, ll);
+                tt[0] = o.s;
+                tt[1] = o.l;
+              }
+              warp_ordered_reduce32<2>(tt, nruns - rb);
+              if (lane == 0) {  // ps, pl: lane 0 only
+                ps = t32_combine(ps, tt[0]);
+                pl = t32_combine(pl, tt[1]);
+              }
+            }
+            __syncwarp();
+          }
+          if (lane == 0) {
+            const long long bs = Bp >> ls, bl = Bp >> ll;
+            pt[2 * p] = ps.c ? Tri{ps.f + bs, ps.l + bs, ps.c} : tri_empty();
+            pt[2 * p + 1] = pl.c ? Tri{pl.f + bl, pl.l + bl, pl.c} : tri_empty();
+            units += (unsigned long long)ny;
+          }
         }
       }
       __syncthreads();
-      // (c) ordered fold with derivation (plane z - per is resolved before z)
-      if (tid == 0) {
-        for (int p = 0; p < np; ++p) {
-          if (pder[p]) {
-            const int q = p - per;  // >= 0: derived planes have their source in this segment
-            const Tri a = pt[2 * q], b = pt[2 * q + 1];
-            const long long dsh = (long long)per * pbytes;
-            pt[2 * p] = a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty();
-            pt[2 * p + 1] = b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty();
-          }
-          cs_all = tri_combine(cs_all, pt[2 * p]);
-          cl_all = tri_combine(cl_all, pt[2 * p + 1]);
+      // (c) ordered fold, warp 0: a derived plane is its computed source plane (p - m*per, the
+      //     nearest non-derived one) translated by m*per planes; lanes take contiguous planes.
+      if (wid == 0) {
+        const int ppl = (np + 31) >> 5;
+        Tri ts = tri_empty(), tl = tri_empty();
+        for (int p = lane * ppl; p < np && p < (lane + 1) * ppl; ++p) {
+          int q = p;
+          while (pder[q]) q -= per;
+          const long long dsh = (long long)(p - q) * pbytes;
+          const Tri a = pt[2 * q], b = pt[2 * q + 1];
+          ts = tri_combine(ts, a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty());
+          tl = tri_combine(tl, b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty());
+        }
+        Tri t2[2] = {ts, tl};
+        warp_ordered_reduce<2>(t2);
+        if (lane == 0) {
+          cs_all = tri_combine(cs_all, t2[0]);
+          cl_all = tri_combine(cl_all, t2[1]);
         }
       }
       __syncthreads();
@@ -1550,6 +1583,7 @@ struct WarpRowCtx {
   RI32 r[5];
   int bnd[20];  // sorted distinct block rows where some range's classification zone starts
   int nb, pad;
+  T32 pt[kNQ];                 // the plane's triples (lane 0)
   unsigned bm[kSegRows / 32];  // run-start bitmap of the current segment
   short rs[kSegRows + 2];      // run starts (ascending) + end
 };
@@ -1558,9 +1592,6 @@ struct WarpRowCtx {
 // (row 0 at plane offset R0, rows `step` bytes apart): sector triple (if want_s) and line
 // triple (if want_l).  One out-of-line copy (instruction-cache footprint); the callers fold
 // the triples into their compile-time targets.
-struct T32x2 {
-  T32 s, l;
-};
 __device__ __noinline__ T32x2 row_emit32(const WarpRowCtx& X, const DField& F, unsigned long long m1, int q1,
                                          unsigned long long m2, int q2, int R0, int step, int run, int le, int ls,
                                          int ll, bool want_s, bool want_l) {
@@ -1724,9 +1755,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
     const long long Bp = (R0p >> ll) << ll;
     const int off0 = (int)(R0p - Bp);
     const int pystep = (int)(py << le);
-    T32 pt[kNQ];
-#pragma unroll
-    for (int q = 0; q < kNQ; ++q) pt[q] = t32_empty();
+    if (lane < kNQ) X.pt[lane] = t32_empty();
     for (int ys = y0; ys < y0 + ny; ys += kSegRows) {
       const int nseg = y0 + ny - ys < kSegRows ? y0 + ny - ys : kSegRows;
       const int nwd = (nseg + 31) >> 5;
@@ -1820,9 +1849,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
           }
         }
         warp_ordered_reduce32<kNQ>(t, nruns - rb);
-        if (lane == 0)  // pt: lane 0 only
+        if (lane == 0)  // plane triples: lane 0 only
 #pragma unroll
-          for (int q = 0; q < kNQ; ++q) pt[q] = t32_combine(pt[q], t[q]);
+          for (int q = 0; q < kNQ; ++q) X.pt[q] = t32_combine(X.pt[q], t[q]);
       }
       __syncwarp();
     }
@@ -1832,9 +1861,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) {
         const long long b = (q == 2 || q == 4 || q == 6) ? bl : bs;
-        out[q * 3 + 0] = pt[q].c ? pt[q].f + b : 0;
-        out[q * 3 + 1] = pt[q].c ? pt[q].l + b : 0;
-        out[q * 3 + 2] = pt[q].c;
+        const T32 v = X.pt[q];
+        out[q * 3 + 0] = v.c ? v.f + b : 0;
+        out[q * 3 + 1] = v.c ? v.l + b : 0;
+        out[q * 3 + 2] = v.c;
       }
     }
   }
