@@ -107,24 +107,46 @@ typedef struct {
   uint64_t l1_bytes, l2_bytes;
   double clock_hz, dram_bw, l2_bw;   /* Hz, bytes/s, bytes/s */
   double hit_abc[4][3];        /* R(O) = a exp(-b exp(-c O)) for L1, L2-over-y, L2-over-z, L2-store */
+  /* Outlook metrics: */
+  uint64_t page_bytes;         /* TLB page size (power of two >= line_bytes); 0 = wave_pages not counted */
+  double link_bw;              /* bytes/s of the link between L2 sections; 0 = not a limiter */
 } ws_gpu;
 
-/* Deep-copies.  Errors: WS_EINVAL (zero / non-power-of-two geometry, ...),
- * WS_ELIMIT (line_bytes > 4096). */
+/* Deep-copies.  Errors: WS_EINVAL (zero / non-power-of-two geometry, page_bytes not 0
+ * or a power of two >= line_bytes, link_bw < 0, ...), WS_ELIMIT (line_bytes > 4096,
+ * l2_sections > 8). */
 ws_status ws_describe_gpu(ws_ctx* ctx, const ws_gpu* g, uint32_t* gpu_id);
 
 /* ------------------------------------------------------------------ configurations */
+/* Model variants (bit flags of ws_config.variant).  0 = the
+ * model of DESIGN.md section 3. */
+enum {
+  /* Wave and layer-set footprints in the multidimensional address space: a
+   * sector is (field, z, y, floor(x * elem_bytes / sector_bytes)); rows never share a
+   * sector or line and the field alignment is not considered.  Warp and SM-set
+   * scopes keep linear addresses (explicit grid iteration). */
+  WS_VAR_MDIM = 1,
+  /* Warm-cache reuse from the directly preceding wave only (the V100 / SBAC model,
+   * P:583-587): both look-back sets become [max(0, s - W), s), so ov_z = ov_y and
+   * ly_lines = lz_lines; the model uses the L2-over-y curve for it. */
+  WS_VAR_PREV_WAVE = 2,
+  /* Effective L2 capacity from the estimated line duplication between L2 sections
+   * instead of l2_bytes / l2_sections: l2_bytes * U / (U + l2_dup_lines),
+   * U = distinct wave lines. */
+  WS_VAR_L2_DUP = 4
+};
+
 typedef struct {
   uint32_t kernel_id, gpu_id;
   uint32_t block[3];           /* threads per block (X,Y,Z)            */
   uint32_t fold[3];            /* thread folding factors; prod <= 64       */
   uint32_t blocks_per_sm;      /* 0 = derive the occupancy k (Q10)                */
-  uint32_t pad;
+  uint32_t variant;            /* WS_VAR_* bits; other bits -> status WS_EINVAL   */
 } ws_config;                   /* 40 bytes */
 
 typedef struct {
   int32_t status;              /* WS_OK or the per-config error                   */
-  uint32_t limiter;            /* 0 = L1, 1 = L2, 2 = DRAM                        */
+  uint32_t limiter;            /* 0 = L1, 1 = L2, 2 = DRAM, 3 = L2 section link   */
   uint32_t grid[3];            /* blocks per dimension                            */
   uint32_t k;                  /* resident blocks per SM                          */
   uint32_t wave_blocks;        /* W                                               */
@@ -148,7 +170,14 @@ typedef struct {
   double l1_cyc_per_lup, l2_ld_Bpl, l2_st_Bpl, dram_ld_Bpl, dram_st_Bpl;
   double t_l1, t_l2, t_dram;   /* seconds per lattice update                      */
   double t_pred;               /* seconds for the whole domain                    */
-} ws_result;                   /* 296 bytes */
+  /* Outlook metrics (NEXT-4), linear address space.  SM j belongs to L2 section
+   * floor(j * l2_sections / n_sm); wave block B runs on SM (B - s) mod n_sm. */
+  uint64_t wave_pages;         /* distinct (field, address / page_bytes) of the wave */
+  uint64_t l2_dup_lines;       /* sum over sections of the section's lines - distinct wave lines   */
+  uint64_t l2_link_sectors;    /* sum over sections of the section's load sectors - distinct ones  */
+  double l2_eff_bytes;         /* L2 capacity the model used (l2_bytes / l2_sections or WS_VAR_L2_DUP) */
+  double t_link;               /* seconds per LUP on the section link (0 if link_bw == 0)          */
+} ws_result;                   /* 336 bytes */
 
 /* Host pointers; synchronous.  Copies cfgs to the device, runs the whole
  * device path, copies n results back. */

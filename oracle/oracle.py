@@ -39,11 +39,11 @@ class Gpu(C.Structure):
                 ("bank_bytes", I64), ("half_warp", I64), ("pair_window_bytes", I64),
                 ("l2_sections", I64), ("l1_bytes", I64), ("l2_bytes", I64),
                 ("clock_hz", C.c_double), ("dram_bw", C.c_double), ("l2_bw", C.c_double),
-                ("hit_abc", (C.c_double * 3) * 4)]
+                ("hit_abc", (C.c_double * 3) * 4), ("page_bytes", I64), ("link_bw", C.c_double)]
 
 
 class Config(C.Structure):
-    _fields_ = [("block", I64 * 3), ("fold", I64 * 3), ("blocks_per_sm", I64)]
+    _fields_ = [("block", I64 * 3), ("fold", I64 * 3), ("blocks_per_sm", I64), ("variant", I64)]
 
 
 INT_FIELDS = ["status", "limiter", "grid", "k", "wave_blocks", "n_smsets", "wave_first_block",
@@ -53,12 +53,15 @@ INT_FIELDS = ["status", "limiter", "grid", "k", "wave_blocks", "n_smsets", "wave
 FP_FIELDS = ["O_l1", "R_l1", "O_y", "R_y", "O_z", "R_z", "O_st", "R_st",
              "l1_cyc_per_lup", "l2_ld_Bpl", "l2_st_Bpl", "dram_ld_Bpl", "dram_st_Bpl",
              "t_l1", "t_l2", "t_dram", "t_pred"]
+INT_FIELDS2 = ["wave_pages", "l2_dup_lines", "l2_link_sectors"]   # NEXT-4
+FP_FIELDS2 = ["l2_eff_bytes", "t_link"]
 
 
 class Result(C.Structure):
     _fields_ = ([("status", I64), ("limiter", I64), ("grid", I64 * 3)] +
                 [(n, I64) for n in INT_FIELDS[3:]] +
-                [(n, C.c_double) for n in FP_FIELDS] + [("addr_evals", I64)])
+                [(n, C.c_double) for n in FP_FIELDS] + [("addr_evals", I64)] +
+                [(n, I64) for n in INT_FIELDS2] + [(n, C.c_double) for n in FP_FIELDS2])
 
 
 def build(force=False):
@@ -133,15 +136,19 @@ def make_gpu(g):
     for i in range(4):
         for j in range(3):
             G.hit_abc[i][j] = g["hit_abc"][i][j]
+    G.page_bytes = int(g.get("page_bytes", 0))
+    G.link_bw = float(g.get("link_bw", 0.0))
     return G
 
 
 def make_config(c):
-    b, f, k = c
+    # (block, fold, blocks_per_sm[, variant])
+    b, f, k = c[:3]
     X = Config()
     X.block[:] = list(b)
     X.fold[:] = list(f)
     X.blocks_per_sm = k
+    X.variant = c[3] if len(c) > 3 else 0
     return X
 
 
@@ -153,6 +160,10 @@ def result_dict(R):
     for n in FP_FIELDS:
         d[n] = float(getattr(R, n))
     d["addr_evals"] = int(R.addr_evals)
+    for n in INT_FIELDS2:
+        d[n] = int(getattr(R, n))
+    for n in FP_FIELDS2:
+        d[n] = float(getattr(R, n))
     return d
 
 

@@ -119,6 +119,7 @@ struct Instr {
 struct Plan {
   V3 b, f, lo, hi, G;
   int64_t T, N, k, W, s, n_sets, Ly0, Lz0;
+  bool mdim;  // multidimensional address space for the wave / layer-set footprints
   std::vector<Instr> instr;
 };
 
@@ -177,6 +178,8 @@ int64_t make_plan(const wso_kernel& K, const wso_gpu& g, const wso_config& c, Pl
   p.N = p.G[0] * p.G[1] * p.G[2];
   // Resident blocks per SM (Q10): threads, blocks and registers,
   // allocated at warp granularity.
+  if (c.variant < 0 || c.variant > 7) return WSO_EINVAL;
+  p.mdim = (c.variant & WSO_VAR_MDIM) != 0;
   if (c.blocks_per_sm > 0) {
     p.k = c.blocks_per_sm;
   } else {
@@ -195,6 +198,9 @@ int64_t make_plan(const wso_kernel& K, const wso_gpu& g, const wso_config& c, Pl
   // row / z-neighbour block layer (Q13).
   p.Ly0 = std::max(int64_t(0), p.s - p.G[0]);
   p.Lz0 = std::max(int64_t(0), p.s - p.G[0] * p.G[1]);
+  // Variant (NEXT-3): the V100 / SBAC model looks back exactly one wave:
+  // both look-back sets become the directly preceding wave [s - W, s).
+  if (c.variant & WSO_VAR_PREV_WAVE) p.Ly0 = p.Lz0 = std::max(int64_t(0), p.s - p.W);
   // O3: instruction table
   for (int64_t fi = 0; fi < K.n_fields; ++fi)
     for (int64_t st = 0; st < 2; ++st) {
@@ -227,21 +233,36 @@ int64_t make_plan(const wso_kernel& K, const wso_gpu& g, const wso_config& c, Pl
   return WSO_OK;
 }
 
-size_t intersection_size(const std::set<Key>& a, const std::set<Key>& b) {
-  std::vector<Key> out;
+// Footprint key of the wave / layer-set scopes: (field, z, y, x-sector).  Linear address
+// space: (field, 0, 0, A div sector_bytes).  Multidimensional address space:
+// two addresses are distinct when their tuples differ; the innermost dimension keeps the
+// floor division by the fetch granularity, the array alignment is not considered
+// ("the alignment of arrays cannot be considered").
+typedef std::array<int64_t, 4> K4;
+K4 scope_key(const wso_kernel& K, const wso_gpu& g, const Plan& p, const V3& base, const Instr& I) {
+  if (!p.mdim) return K4{I.field, 0, 0, floordiv(instr_address(K, base, I), g.sector_bytes)};
+  V3 cell{base[0] + I.r[0], base[1] + I.r[1], base[2] + I.r[2]};
+  return K4{I.field, cell[2], cell[1], floordiv(cell[0] * K.fields[I.field].elem_bytes, g.sector_bytes)};
+}
+// sector key -> line key (128 / 32 = 4 sectors per line, floor(floor(a/32)/4) = floor(a/128))
+K4 line_of(const K4& k, int64_t sec_per_line) { return K4{k[0], k[1], k[2], floordiv(k[3], sec_per_line)}; }
+
+template <class S>
+size_t intersection_size(const S& a, const S& b) {
+  std::vector<typename S::value_type> out;
   std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
   return out.size();
 }
 
 // F_L: every sector touched by any instruction (loads and stores) of the
 // blocks [B0, B1) (Q15: L2 is write-back, stored data can be hit).
-std::set<Key> layer_footprint(const wso_kernel& K, const wso_gpu& g, const Plan& p, int64_t B0, int64_t B1) {
-  std::set<Key> F;
+std::set<K4> layer_footprint(const wso_kernel& K, const wso_gpu& g, const Plan& p, int64_t B0, int64_t B1) {
+  std::set<K4> F;
   for (int64_t B = B0; B < B1; ++B)
     for (int64_t t = 0; t < p.T; ++t) {
       V3 base = base_cell(p, B, t);
       for (const Instr& I : p.instr)
-        if (issues(p, base, I)) F.insert(Key(I.field, floordiv(instr_address(K, base, I), g.sector_bytes)));
+        if (issues(p, base, I)) F.insert(scope_key(K, g, p, base, I));
     }
   return F;
 }
@@ -262,10 +283,17 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
   // ------------------------------------------------------------ O5-O7 over the wave
   int64_t wf = 0, req_ld = 0, req_st = 0, lup = 0;
   std::vector<std::set<Key>> SMsec(p.n_sets), SMlin(p.n_sets);
-  std::set<Key> WLD, WST, WLIN;
+  std::set<K4> WLD, WST, WLIN;
+  // NEXT-4: TLB pages of the wave and the per-L2-section footprints
+  // (P:322-329), always in the linear (physical) address space.  SM j is
+  // attached to section floor(j * S / n_sm); block B runs on SM (B - s) mod n_sm (Q9).
+  const int64_t S = g.l2_sections;
+  std::set<Key> PAGES;
+  std::vector<std::set<Key>> SECld(S), SEClin(S);
   const int64_t n_warps = ceildiv(p.T, 32);
   for (int64_t B = p.s; B < p.s + p.W; ++B) {
     const int64_t j = (B - p.s) % g.n_sm;  // round-robin SM assignment (Q9)
+    const int64_t sec = j * S / g.n_sm;      // L2 section of that SM
     for (int64_t t = 0; t < p.T; ++t) {   // active cells = lattice updates of the wave
       V3 base = base_cell(p, B, t);
       for (int64_t kz = 0; kz < p.f[2]; ++kz)
@@ -302,11 +330,21 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
           if (!I.is_store) {
             SMsec[j].insert(ks);  // L1: SM-resident set (Q8)
             SMlin[j].insert(kl);  // 128 B allocation granularity (Q18: loads only)
-            WLD.insert(ks);       // wave load footprint
-          } else {
-            WST.insert(ks);       // wave store footprint
+            SECld[sec].insert(ks);
           }
-          WLIN.insert(kl);
+          SEClin[sec].insert(kl);
+          if (g.page_bytes > 0) PAGES.insert(Key(I.field, floordiv(a, g.page_bytes)));
+        }
+        // wave scope keys (linear or multidimensional address space)
+        for (int64_t lane = 0; lane < 32; ++lane) {
+          int64_t t = w * 32 + lane;
+          if (t >= p.T) break;
+          V3 base = base_cell(p, B, t);
+          if (!issues(p, base, I)) continue;
+          K4 k4 = scope_key(K, g, p, base, I);
+          if (!I.is_store) WLD.insert(k4);  // wave load footprint
+          else WST.insert(k4);              // wave store footprint
+          WLIN.insert(line_of(k4, sec_per_line));
         }
       }
     }
@@ -318,11 +356,25 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
   }
 
   // ------------------------------------------------------------ O8 layer sets
-  std::set<Key> Fy = layer_footprint(K, g, p, p.Ly0, p.s);
-  std::set<Key> Fz = layer_footprint(K, g, p, p.Lz0, p.s);
-  std::set<Key> Fy_lines, Fz_lines;
-  for (const Key& k : Fy) Fy_lines.insert(Key(k.first, floordiv(k.second, sec_per_line)));
-  for (const Key& k : Fz) Fz_lines.insert(Key(k.first, floordiv(k.second, sec_per_line)));
+  std::set<K4> Fy = layer_footprint(K, g, p, p.Ly0, p.s);
+  std::set<K4> Fz = layer_footprint(K, g, p, p.Lz0, p.s);
+  std::set<K4> Fy_lines, Fz_lines;
+  for (const K4& k : Fy) Fy_lines.insert(line_of(k, sec_per_line));
+  for (const K4& k : Fz) Fz_lines.insert(line_of(k, sec_per_line));
+
+  // NEXT-4: duplication = copies beyond the first of a line held by several sections;
+  // link volume = load sectors fetched by more than one section (one far-section copy each).
+  std::set<Key> Uld, Ulin;
+  int64_t sum_ld = 0, sum_lin = 0;
+  for (int64_t i = 0; i < S; ++i) {
+    sum_ld += (int64_t)SECld[i].size();
+    sum_lin += (int64_t)SEClin[i].size();
+    Uld.insert(SECld[i].begin(), SECld[i].end());
+    Ulin.insert(SEClin[i].begin(), SEClin[i].end());
+  }
+  r.wave_pages = (int64_t)PAGES.size();
+  r.l2_dup_lines = sum_lin - (int64_t)Ulin.size();
+  r.l2_link_sectors = sum_ld - (int64_t)Uld.size();
 
   r.lup_wave = lup;
   r.l1_wavefronts = wf;
@@ -352,6 +404,11 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
   double l1l2_st = (double)req_st;  // write-through
   // L2 level: effective capacity of one section (Q31)
   double l2eff = (double)g.l2_bytes / (double)g.l2_sections;
+  // Variant (NEXT-4): instead of assuming full duplication (capacity / S),
+  // the capacity holds |Ulin| + dup line copies for |Ulin| distinct lines.
+  if ((c.variant & WSO_VAR_L2_DUP) && !Ulin.empty())
+    l2eff = (double)g.l2_bytes * (double)Ulin.size() / (double)(Ulin.size() + r.l2_dup_lines);
+  r.l2_eff_bytes = l2eff;
   r.O_y = (double)Fy_lines.size() * LB / l2eff;
   r.O_z = (double)Fz_lines.size() * LB / l2eff;
   r.R_y = hit_rate(g.hit_abc[1], r.O_y);
@@ -374,9 +431,11 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
   r.t_l1 = (double)wf / (n * (double)g.n_sm * g.clock_hz);
   r.t_l2 = SB * (l2l1_ld + l1l2_st) / (n * g.l2_bw);
   r.t_dram = SB * (dram_ld + dram_st) / (n * g.dram_bw);
-  double t = std::max(r.t_l1, std::max(r.t_l2, r.t_dram));
-  // limiter: argmax, ties resolved DRAM > L2 > L1 (Q29)
-  r.limiter = (r.t_dram >= t) ? 2 : (r.t_l2 >= t) ? 1 : 0;
+  // inter-section link as an additional L2 limiter, when its bandwidth is given
+  r.t_link = g.link_bw > 0 ? SB * (double)r.l2_link_sectors / (n * g.link_bw) : 0.0;
+  double t = std::max(std::max(r.t_l1, r.t_link), std::max(r.t_l2, r.t_dram));
+  // limiter: argmax, ties resolved DRAM > L2 > link > L1 (Q29)
+  r.limiter = (r.t_dram >= t) ? 2 : (r.t_l2 >= t) ? 1 : (r.t_link >= t) ? 3 : 0;
   double cells = 1.0;
   for (int d = 0; d < 3; ++d) cells *= (double)(p.hi[d] - p.lo[d]);
   r.t_pred = t * cells;

@@ -47,10 +47,20 @@ typedef struct {
   int64_t l1_bytes, l2_bytes;
   double  clock_hz, dram_bw, l2_bw;
   double  hit_abc[4][3];          /* L1, L2-over-y, L2-over-z, L2-store */
+  int64_t page_bytes;             /* TLB page size; 0 = pages not counted */
+  double  link_bw;                /* L2 inter-section link bytes/s; 0 = no link limiter */
 } wso_gpu;
+
+/* model variants, bit flags of wso_config.variant */
+enum {
+  WSO_VAR_MDIM = 1,       /* multidimensional address space for wave + layer sets */
+  WSO_VAR_PREV_WAVE = 2,  /* warm reuse from the directly preceding wave only (SBAC) */
+  WSO_VAR_L2_DUP = 4      /* L2 capacity from the estimated line duplication */
+};
 
 typedef struct {
   int64_t block[3], fold[3], blocks_per_sm;
+  int64_t variant;                /* WSO_VAR_* bits */
 } wso_config;
 
 typedef struct {
@@ -62,6 +72,10 @@ typedef struct {
   double  l1_cyc_per_lup, l2_ld_Bpl, l2_st_Bpl, dram_ld_Bpl, dram_st_Bpl;
   double  t_l1, t_l2, t_dram, t_pred;
   int64_t addr_evals;             /* (thread, instruction) evaluations done   */
+  int64_t wave_pages;             /* TLB pages touched by the wave (0 if page_bytes == 0) */
+  int64_t l2_dup_lines;           /* sum over L2 sections of section lines - distinct wave lines */
+  int64_t l2_link_sectors;        /* sum over sections of section load sectors - distinct ones */
+  double  l2_eff_bytes, t_link;   /* effective L2 capacity used by the model; link time per LUP */
 } wso_result;
 
 /* status codes (same meaning as the ABI's, defined independently) */

@@ -1,6 +1,6 @@
 """Multi-GPU plumbing: configurations are independent, so a sweep is
 sharded over ranks (one process per GPU) and the only exchange is one all-gather of
-the fixed-size result records (296 B, include/ws.h `ws_result`) over NCCL; every rank
+the fixed-size result records (336 B, include/ws.h `ws_result`) over NCCL; every rank
 then ranks the gathered set with the library's `ws_rank_async` and holds identical bytes.
 
 This module holds host logic only (shard assignment, padding, gather, reordering);
@@ -13,7 +13,7 @@ import heapq
 import torch
 import torch.distributed as dist
 
-RECORD_BYTES = 296
+RECORD_BYTES = 336
 
 
 def proxy_cost(config) -> float:
@@ -70,7 +70,7 @@ def estimate_sharded(ctx, cfg_records, group=None, k_top: int = 10):
     """Shard a batch of ws_config records (numpy CONFIG_DTYPE) over the ranks of `group`,
     estimate locally on this rank's GPU, all-gather, rank the full set on every rank.
 
-    Returns (results uint8 tensor (n, 296) on this rank's GPU, top-k indices tensor)."""
+    Returns (results uint8 tensor (n, 336) on this rank's GPU, top-k indices tensor)."""
     from .ws import CONFIG_DTYPE, RESULT_DTYPE
     import numpy as np
     world = dist.get_world_size(group) if dist.is_initialized() else 1

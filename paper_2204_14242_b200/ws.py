@@ -37,12 +37,12 @@ class ws_gpu(C.Structure):
                 ("sector_bytes", U32), ("line_bytes", U32), ("n_banks", U32), ("bank_bytes", U32),
                 ("half_warp", U32), ("pair_window_bytes", U32), ("l2_sections", U32),
                 ("l1_bytes", U64), ("l2_bytes", U64), ("clock_hz", F64), ("dram_bw", F64), ("l2_bw", F64),
-                ("hit_abc", (F64 * 3) * 4)]
+                ("hit_abc", (F64 * 3) * 4), ("page_bytes", U64), ("link_bw", F64)]
 
 
 class ws_config(C.Structure):
     _fields_ = [("kernel_id", U32), ("gpu_id", U32), ("block", U32 * 3), ("fold", U32 * 3),
-                ("blocks_per_sm", U32), ("pad", U32)]
+                ("blocks_per_sm", U32), ("variant", U32)]
 
 
 RESULT_U64 = ["wave_first_block", "lup_wave", "l1_wavefronts", "l1_req_ld_sectors", "l1_req_st_sectors",
@@ -50,15 +50,19 @@ RESULT_U64 = ["wave_first_block", "lup_wave", "l1_wavefronts", "l1_req_ld_sector
               "lz_lines", "ov_y", "ov_z", "addr_evals"]
 RESULT_F64 = ["O_l1", "R_l1", "O_y", "R_y", "O_z", "R_z", "O_st", "R_st", "l1_cyc_per_lup", "l2_ld_Bpl",
               "l2_st_Bpl", "dram_ld_Bpl", "dram_st_Bpl", "t_l1", "t_l2", "t_dram", "t_pred"]
+RESULT_U64_2 = ["wave_pages", "l2_dup_lines", "l2_link_sectors"]   # NEXT-4 outlook metrics
+RESULT_F64_2 = ["l2_eff_bytes", "t_link"]
+WS_VAR_MDIM, WS_VAR_PREV_WAVE, WS_VAR_L2_DUP = 1, 2, 4
 
 
 class ws_result(C.Structure):
     _fields_ = ([("status", I32), ("limiter", U32), ("grid", U32 * 3), ("k", U32), ("wave_blocks", U32),
                  ("n_smsets", U32), ("n_instr", U32), ("rank", U32)] +
-                [(n, U64) for n in RESULT_U64] + [(n, F64) for n in RESULT_F64])
+                [(n, U64) for n in RESULT_U64] + [(n, F64) for n in RESULT_F64] +
+                [(n, U64) for n in RESULT_U64_2] + [(n, F64) for n in RESULT_F64_2])
 
 
-assert C.sizeof(ws_config) == 40 and C.sizeof(ws_result) == 296
+assert C.sizeof(ws_config) == 40 and C.sizeof(ws_result) == 336
 
 CONFIG_DTYPE = np.dtype(ws_config)
 RESULT_DTYPE = np.dtype(ws_result)
@@ -145,14 +149,18 @@ def gpu_struct(g):
     for i in range(4):
         for j in range(3):
             G.hit_abc[i][j] = g["hit_abc"][i][j]
+    G.page_bytes = int(g.get("page_bytes", 0))
+    G.link_bw = float(g.get("link_bw", 0.0))
     return G
 
 
 def config_array(kernel_id, gpu_id, configs):
-    """configs: iterable of (block, fold, blocks_per_sm) -> numpy ws_config records."""
+    """configs: iterable of (block, fold, blocks_per_sm[, variant]) -> numpy ws_config records."""
     configs = list(configs)
     a = np.zeros(len(configs), dtype=CONFIG_DTYPE)
-    for i, (b, f, kov) in enumerate(configs):
+    for i, c in enumerate(configs):
+        b, f, kov = c[:3]
+        a[i]["variant"] = c[3] if len(c) > 3 else 0
         a[i]["kernel_id"], a[i]["gpu_id"] = kernel_id, gpu_id
         a[i]["block"] = b
         a[i]["fold"] = f
@@ -168,8 +176,10 @@ def result_dicts(res):
              "n_instr": int(r["n_instr"]), "rank": int(r["rank"])}
         for n in RESULT_U64:
             d[n] = int(r[n])
-        for n in RESULT_F64:
+        for n in RESULT_F64 + RESULT_F64_2:
             d[n] = float(r[n])
+        for n in RESULT_U64_2:
+            d[n] = int(r[n])
         out.append(d)
     return out
 

@@ -20,7 +20,7 @@ kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
 a = config_array(kid, gid, space)
 n = len(a)
 dc = torch.from_numpy(a.view(np.uint8)).cuda()
-do = torch.empty(n * 296, dtype=torch.uint8, device="cuda")
+do = torch.empty(n * 336, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
     torch.cuda.synchronize()

@@ -11,7 +11,7 @@ def run(name, k, g, cfgs, reps=20):
     a = config_array(kid, gid, cfgs)
     n = len(a)
     dc = torch.from_numpy(a.view(np.uint8)).cuda()
-    do = torch.empty(n * 296, dtype=torch.uint8, device="cuda")
+    do = torch.empty(n * 336, dtype=torch.uint8, device="cuda")
     for _ in range(2):
         ctx.estimate_async(dc.data_ptr(), n, do.data_ptr())
     torch.cuda.synchronize()

@@ -23,7 +23,8 @@ import numpy as np
 
 
 def geometry(kernel, gpu, cfg):
-    (bx, by, bz), (fx, fy, fz), kov = cfg
+    (bx, by, bz), (fx, fy, fz), kov = cfg[:3]
+    variant = cfg[3] if len(cfg) > 3 else 0
     lo = np.array(kernel["dom_lo"], dtype=np.int64)
     hi = np.array(kernel["dom_hi"], dtype=np.int64)
     b = np.array([bx, by, bz], dtype=np.int64)
@@ -42,8 +43,10 @@ def geometry(kernel, gpu, cfg):
     cx, cy, cz = G[0] // 2, G[1] // 2, G[2] // 2
     centre = int(cx + G[0] * (cy + G[1] * cz))
     s = min(max(centre - W // 2, 0), N - W)
-    return dict(lo=lo, hi=hi, b=b, f=f, T=T, G=G, N=N, k=k, W=W, s=s,
-                Ly=(max(0, s - int(G[0])), s), Lz=(max(0, s - int(G[0] * G[1])), s))
+    Ly, Lz = (max(0, s - int(G[0])), s), (max(0, s - int(G[0] * G[1])), s)
+    if variant & 2:   # previous wave only (SBAC)
+        Ly = Lz = (max(0, s - W), s)
+    return dict(lo=lo, hi=hi, b=b, f=f, T=T, G=G, N=N, k=k, W=W, s=s, Ly=Ly, Lz=Lz, variant=variant)
 
 
 def block_cells(geo, blocks):
@@ -80,6 +83,19 @@ def footprint(kernel, cells, kinds, shift):
     return keys
 
 
+def footprint_md(kernel, cells, kinds, shift):
+    """Multidimensional address space: (field, z, y, (x * elem) >> shift)."""
+    keys = set()
+    for fi, fld in enumerate(kernel["fields"]):
+        offs = [o for (f, st, o) in kernel["accesses"] if f == fi and st in kinds]
+        if not offs or len(cells) == 0:
+            continue
+        allc = np.concatenate([cells + np.array(o, dtype=np.int64) for o in offs])
+        xs = (allc[:, 0] * fld["elem"]) >> shift
+        keys.update((fi, int(z), int(y), int(x)) for x, y, z in zip(xs, allc[:, 1], allc[:, 2]))
+    return keys
+
+
 def set_counts(kernel, gpu, cfg):
     """Union scopes a4-a6 by cell enumeration (the oracle does (thread, instr))."""
     geo = geometry(kernel, gpu, cfg)
@@ -88,22 +104,38 @@ def set_counts(kernel, gpu, cfg):
     s, W, nsm = geo["s"], geo["W"], gpu["n_sm"]
     wave = list(range(s, s + W))
     wcells = block_cells(geo, wave)
-    WLD = footprint(kernel, wcells, (0,), ls)
-    WST = footprint(kernel, wcells, (1,), ls)
-    WLIN = footprint(kernel, wcells, (0, 1), ll)
+    md = bool(geo["variant"] & 1)
+    fp = footprint_md if md else footprint
+    WLD = fp(kernel, wcells, (0,), ls)
+    WST = fp(kernel, wcells, (1,), ls)
+    WLIN = fp(kernel, wcells, (0, 1), ll)
     sm_sec = sm_lin = 0
     for j in range(min(nsm, W)):
         cells = block_cells(geo, wave[j::nsm])
         sm_sec += len(footprint(kernel, cells, (0,), ls))
         sm_lin += len(footprint(kernel, cells, (0,), ll))
-    FY = footprint(kernel, block_cells(geo, range(*geo["Ly"])), (0, 1), ls)
-    FZ = footprint(kernel, block_cells(geo, range(*geo["Lz"])), (0, 1), ls)
+    FY = fp(kernel, block_cells(geo, range(*geo["Ly"])), (0, 1), ls)
+    FZ = fp(kernel, block_cells(geo, range(*geo["Lz"])), (0, 1), ls)
     d = ll - ls
+    # NEXT-4 (linear address space): TLB pages of the wave; per-L2-section footprints with SM j
+    # in section j*S//n_sm and block s+i on SM i % n_sm
+    pb = int(gpu.get("page_bytes", 0))
+    pages = len(footprint(kernel, wcells, (0, 1), int(np.log2(pb)))) if pb else 0
+    S = gpu["l2_sections"]
+    sec_ld, sec_lin = [set() for _ in range(S)], [set() for _ in range(S)]
+    for i, B in enumerate(wave):
+        sec = (i % nsm) * S // nsm
+        cells = block_cells(geo, [B])
+        sec_ld[sec] |= footprint(kernel, cells, (0,), ls)
+        sec_lin[sec] |= footprint(kernel, cells, (0, 1), ll)
+    dup = sum(len(x) for x in sec_lin) - len(set().union(*sec_lin))
+    link = sum(len(x) for x in sec_ld) - len(set().union(*sec_ld))
     return dict(lup_wave=len(wcells), sm_ld_sectors=sm_sec, sm_ld_lines=sm_lin,
                 wave_ld_sectors=len(WLD), wave_st_sectors=len(WST), wave_lines=len(WLIN),
-                ly_lines=len({(f, v >> d) for f, v in FY}), lz_lines=len({(f, v >> d) for f, v in FZ}),
+                ly_lines=len({v[:-1] + (v[-1] >> d,) for v in FY}), lz_lines=len({v[:-1] + (v[-1] >> d,) for v in FZ}),
                 ov_y=len(WLD & FY), ov_z=len(WLD & FZ), k=geo["k"], wave_blocks=W,
-                wave_first_block=s, grid=tuple(int(g) for g in geo["G"]))
+                wave_first_block=s, grid=tuple(int(g) for g in geo["G"]),
+                wave_pages=pages, l2_dup_lines=dup, l2_link_sectors=link)
 
 
 # ------------------------------------------------------------- per-thread traces

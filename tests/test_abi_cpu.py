@@ -30,11 +30,11 @@ def test_struct_layouts():
     import ctypes as C
     from paper_2204_14242_b200 import ws
     assert C.sizeof(ws.ws_config) == 40
-    assert C.sizeof(ws.ws_result) == 296
+    assert C.sizeof(ws.ws_result) == 336
     assert C.sizeof(ws.ws_field) == 64
     assert C.sizeof(ws.ws_access) == 20
     src = open(os.path.join(ROOT, "include", "ws.h")).read()
-    assert "/* 296 bytes */" in src and "/* 40 bytes */" in src
+    assert "/* 336 bytes */" in src and "/* 40 bytes */" in src
 
 
 def test_sm100a_cubin_present():

@@ -383,3 +383,138 @@ def test_invariants_random(seed):
     for key in ["l1_wavefronts", "l1_req_ld_sectors", "l1_req_st_sectors", "sm_ld_lines", "wave_ld_sectors",
                 "wave_st_sectors", "ly_lines", "lz_lines", "ov_y", "ov_z", "t_pred"]:
         assert r3[key] == r[key]
+
+
+# --------------------------------------------------------------------- NEXT-3 / NEXT-4 variants
+VAR_MDIM, VAR_PREV_WAVE, VAR_L2_DUP = 1, 2, 4
+
+
+def _plain_kernel(ext, accesses, align=0, elem=8, dom_lo=(0, 0, 0), dom_hi=None):
+    ex, ey, ez = ext
+    f = {"extent": ext, "pitch": (1, ex, ex * ey), "align": align, "elem": elem}
+    nf = 1 + max(a[0] for a in accesses)
+    return {"fields": [dict(f) for _ in range(nf)], "accesses": accesses, "dom_lo": dom_lo,
+            "dom_hi": dom_hi or ext, "regs": 0, "flops": 0.0}
+
+
+def test_mdim_paper_example():
+    """P:527-532 + P:557-562: A[tidx][tidy+1] over a 256x2 thread block maps to the 2D address
+    (ax = floor(tidx*8/32), ay = tidy+1): 64 x 2 = 128 distinct sectors in the multidimensional
+    address space, whatever the alignment.  The linear space with the -1-element
+    alignment of P:540 shares one sector between the two rows: 2 * 65 - 1 = 129."""
+    k = _plain_kernel((256, 4, 1), [(0, 0, (0, 1, 0))], align=-8, dom_hi=(256, 2, 1))
+    g = dict(W.gpu_a100(), n_sm=1)
+    c = ((256, 2, 1), (1, 1, 1), 1)
+    md = O.estimate(k, g, c + (VAR_MDIM,))
+    lin = O.estimate(k, g, c)
+    assert md["wave_ld_sectors"] == 128 and md["wave_lines"] == 2 * 16
+    assert lin["wave_ld_sectors"] == 129
+    # the warp / SM-set scopes keep linear addresses (explicit grid iteration, P:399-503)
+    for key in ("l1_req_ld_sectors", "l1_wavefronts", "sm_ld_sectors", "sm_ld_lines"):
+        assert md[key] == lin[key], key
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_mdim_alignment_invariance_and_line_rows(seed):
+    """Multidimensional counts ignore the alignment; with line-multiple rows and a
+    line-aligned base, the two address spaces count the same sets (no row shares a line)."""
+    k = W.stencil_star(24, 10, 12, 1 + seed % 2, regs=0)   # rows of 26 / 28 doubles
+    g = dict(W.gpu_a100(), n_sm=4)
+    c = ((8, 2, 2), (1, 1 + seed % 2, 1), 1, VAR_MDIM)
+    r0 = O.estimate(k, g, c)
+    keys = ["wave_ld_sectors", "wave_st_sectors", "wave_lines", "ly_lines", "lz_lines", "ov_y", "ov_z"]
+    for shift in (8, 24, 64 + 16 * seed):
+        k2 = dict(k, fields=[dict(f, align=f["align"] + shift) for f in k["fields"]])
+        r2 = O.estimate(k2, g, c)
+        for key in keys:
+            assert r2[key] == r0[key], (shift, key)
+    # pad the rows to 32 doubles = 2 lines: linear == multidimensional
+    kp = dict(k, fields=[dict(f, pitch=(1, 32, 32 * f["extent"][1])) for f in k["fields"]])
+    a, b = O.estimate(kp, g, c[:3]), O.estimate(kp, g, c)
+    for key in keys:
+        assert a[key] == b[key], key
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8, 16])
+def test_prev_wave_series(d):
+    """P:583-587 (SBAC, V100): reuse only from the directly preceding wave.  A wave of 16 full
+    rows, d planes deep, in the middle of a block layer: the previous wave holds exactly its
+    y-neighbour rows, so with R = 1 the DRAM load is the P:993 series 8(d+8)/d B/Lup (+ the
+    64/XS x-halo), independent of the z curve."""
+    k = W.stencil_star(XS, 64, 64, 4, regs=0)
+    g = W.gpu_a100()
+    g["n_sm"] = 16
+    g["hit_abc"][1] = [1.0, 0.0, 0.0]
+    g["hit_abc"][2] = [0.0, 0.0, 0.0]
+    r = O.estimate(k, g, ((XS, 1, 1), (1, 1, d), 1, VAR_PREV_WAVE))
+    assert r["ov_y"] == r["ov_z"] and r["ly_lines"] == r["lz_lines"]
+    assert r["dram_ld_Bpl"] == pytest.approx(8 * (d + 8) / d + 64 / XS, rel=1e-12)
+
+
+def test_prev_wave_lru_pin():
+    """Cold sectored LRU replaying the previous wave (loads + stores) then the wave's loads:
+    misses inside the wave = wave_ld_sectors - ov_y (exact at infinite capacity)."""
+    k = W.stencil_star(16, 8, 12, 4, regs=64)
+    g = dict(W.gpu_a100(), n_sm=4)
+    c = ((8, 2, 2), (1, 1, 1), 1, VAR_PREV_WAVE)
+    r = O.estimate(k, g, c)
+    geo = M.geometry(k, g, c)
+    s, Wb = geo["s"], geo["W"]
+    assert geo["Ly"] == (max(0, s - Wb), s)
+    cache = M.SectoredLRU(1 << 40)
+    M.replay_blocks(k, g, c, range(max(0, s - Wb), s), cache, kinds=(0, 1))
+    before = cache.misses
+    M.replay_blocks(k, g, c, range(s, s + Wb), cache, kinds=(0,))
+    assert cache.misses - before == r["wave_ld_sectors"] - r["ov_y"] > 0
+
+
+@pytest.mark.parametrize("align,pages_per_plane", [(0, 2), (8, 3)])
+def test_tlb_pages_hand_count(align, pages_per_plane):
+    """TLB pages accessed by the current wave.  Copy kernel B[c] = A[c] on
+    1024 x 64 x 64 doubles (8 KiB rows), 64 KiB pages, a wave of 16 rows x d planes at rows
+    24..39 of each plane = bytes [192 KiB, 320 KiB) of the plane: 2 pages per plane and field,
+    3 when the field starts 8 B past a page boundary."""
+    d = 4
+    k = _plain_kernel((1024, 64, 64), [(0, 0, (0, 0, 0)), (1, 1, (0, 0, 0))], align=align)
+    g = dict(W.gpu_a100(), n_sm=16, page_bytes=64 * 1024)
+    r = O.estimate(k, g, ((1024, 1, 1), (1, 1, d), 1))
+    assert r["wave_first_block"] % 64 == 24
+    assert r["wave_pages"] == 2 * d * pages_per_plane
+    assert O.estimate(k, dict(g, page_bytes=0), ((1024, 1, 1), (1, 1, d), 1))["wave_pages"] == 0
+
+
+def test_l2_sections_duplication_and_link_hand_count():
+    """4 SMs in 2 L2 sections (SMs 0,1 | 2,3), a wave of 4 one-row
+    blocks; a 3-point y stencil loads rows y-1..y+1.  Section 0 (rows y0, y0+1) and section 1
+    (rows y0+2, y0+3) both load rows y0+1, y0+2: 2 rows x 64 sectors cross the link and
+    2 rows x 16 lines are held twice; the stored rows are disjoint."""
+    k = _plain_kernel((256, 32, 1), [(0, 0, (0, -1, 0)), (0, 0, (0, 0, 0)), (0, 0, (0, 1, 0)),
+                                      (1, 1, (0, 0, 0))], dom_lo=(0, 1, 0), dom_hi=(256, 31, 1))
+    g = dict(W.gpu_a100(), n_sm=4, l2_sections=2, link_bw=1e12)
+    c = ((256, 1, 1), (1, 1, 1), 1)
+    r = O.estimate(k, g, c)
+    assert r["l2_link_sectors"] == 128 and r["l2_dup_lines"] == 32
+    n = r["lup_wave"]
+    assert n == 4 * 256
+    assert r["t_link"] == pytest.approx(32 * 128 / (n * 1e12), rel=1e-15)
+    assert r["l2_eff_bytes"] == g["l2_bytes"] / 2                 # default: full duplication (P:326)
+    rd = O.estimate(k, g, c + (VAR_L2_DUP,))
+    U = 6 * 16 + 4 * 16                                            # distinct lines: 6 load rows + 4 store rows
+    assert rd["l2_eff_bytes"] == pytest.approx(g["l2_bytes"] * U / (U + 32), rel=1e-15)
+    r1 = O.estimate(k, dict(g, l2_sections=1), c + (VAR_L2_DUP,))
+    assert r1["l2_dup_lines"] == r1["l2_link_sectors"] == 0 and r1["l2_eff_bytes"] == g["l2_bytes"]
+    # link-limited once the link is slow enough; limiter code 3
+    rs = O.estimate(k, dict(g, link_bw=1e6), c)
+    assert rs["limiter"] == 3 and rs["t_pred"] == pytest.approx(rs["t_link"] * 256 * 30, rel=1e-12)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 4, 7])
+@pytest.mark.parametrize("case", range(len(SMALL_CASES)))
+def test_oracle_vs_independent_variants(case, variant):
+    k, g, c = SMALL_CASES[case]
+    g = dict(g, page_bytes=1024, l2_sections=3 if case % 2 else 2)
+    c = c + (variant,)
+    r = O.estimate(k, g, c)
+    m = M.set_counts(k, g, c)
+    for key, v in m.items():
+        assert r[key] == v, key

@@ -73,8 +73,13 @@ def gpu_b200_like(hbm_gbs=6546.2):
     (l2_sections=2 by analogy with the A100 split), DRAM bandwidth
     = the measured copy bandwidth from MEASURED_PEAKS.json.  The L2 bandwidth
     is a nominal 12 TB/s (hypothetical parameter, not measured)."""
-    return _gpu("B200-like", 148, 1.965e9, 256 * KiB, 126 * 1000 * 1000, 2,
-                hbm_gbs * 1e9, 12e12)
+    g = _gpu("B200-like", 148, 1.965e9, 256 * KiB, 126 * 1000 * 1000, 2,
+             hbm_gbs * 1e9, 12e12)
+    # outlook metrics (NEXT-4, hypothetical parameters): 2 MiB GPU pages; the die-to-die
+    # link between the two L2 halves at a nominal 10 TB/s
+    g["page_bytes"] = 2 * MiB
+    g["link_bw"] = 10e12
+    return g
 
 
 def gpu_hypothetical(l1_kib, l2_eff_mib, n_sm):
@@ -261,6 +266,10 @@ def random_gpu(seed):
              500e9 + rng.random() * 1e12, 2000e9 + rng.random() * 2e12,
              max_thr_sm=rng.choice([512, 1024, 2048]), max_blk_sm=rng.choice([2, 4, 8, 32]))
     g["pair_window_bytes"] = rng.choice([256, 512, 1024])
+    # outlook metrics (NEXT-4): TLB page size, L2 section count and link bandwidth
+    g["page_bytes"] = rng.choice([0, 512, 4096, 65536])
+    g["l2_sections"] = rng.choice([g["l2_sections"], g["l2_sections"], 3, 4])
+    g["link_bw"] = rng.choice([0.0, 0.0, 1e11 + rng.random() * 1e12])
     return g
 
 
@@ -272,4 +281,5 @@ def random_config(seed):
             break
     f = (rng.choice([1, 1, 2]), rng.choice([1, 1, 2, 3]), rng.choice([1, 1, 2]))
     k = rng.choice([0, 0, 0, 1, 2])
-    return (b, f, k)
+    variant = rng.choice([0, 0, 1, 2, 3, 4, 5, 6, 7])   # WS_VAR_* bits (NEXT-3 / NEXT-4)
+    return (b, f, k, variant)
