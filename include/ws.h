@@ -114,7 +114,7 @@ typedef struct {
 
 /* Deep-copies.  Errors: WS_EINVAL (zero / non-power-of-two geometry, page_bytes not 0
  * or a power of two >= line_bytes, link_bw < 0, ...), WS_ELIMIT (line_bytes > 4096,
- * l2_sections > 8). */
+ * l2_sections > 4). */
 ws_status ws_describe_gpu(ws_ctx* ctx, const ws_gpu* g, uint32_t* gpu_id);
 
 /* ------------------------------------------------------------------ configurations */
@@ -175,6 +175,7 @@ typedef struct {
   uint64_t wave_pages;         /* distinct (field, address / page_bytes) of the wave */
   uint64_t l2_dup_lines;       /* sum over sections of the section's lines - distinct wave lines   */
   uint64_t l2_link_sectors;    /* sum over sections of the section's load sectors - distinct ones  */
+                               /* (both 0 unless l2_sections > 1 and (link_bw > 0 or WS_VAR_L2_DUP)) */
   double l2_eff_bytes;         /* L2 capacity the model used (l2_bytes / l2_sections or WS_VAR_L2_DUP) */
   double t_link;               /* seconds per LUP on the section link (0 if link_bw == 0)          */
 } ws_result;                   /* 336 bytes */

@@ -373,8 +373,10 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
     Ulin.insert(SEClin[i].begin(), SEClin[i].end());
   }
   r.wave_pages = (int64_t)PAGES.size();
-  r.l2_dup_lines = sum_lin - (int64_t)Ulin.size();
-  r.l2_link_sectors = sum_ld - (int64_t)Uld.size();
+  // reported on request (ABI): several sections and the link limiter or WSO_VAR_L2_DUP
+  const bool want_sect = S > 1 && (g.link_bw > 0 || (c.variant & WSO_VAR_L2_DUP));
+  r.l2_dup_lines = want_sect ? sum_lin - (int64_t)Ulin.size() : 0;
+  r.l2_link_sectors = want_sect ? sum_ld - (int64_t)Uld.size() : 0;
 
   r.lup_wave = lup;
   r.l1_wavefronts = wf;

@@ -145,6 +145,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   const size_t o_scnt = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned int));
   const size_t o_srep = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
   const size_t o_work = off;    off = align_up(off + 16 * sizeof(unsigned long long));
+  static_assert(K_NKINDS <= 16, "work slots");
   const size_t o_lists = off;   off = align_up(off + 4 * sizeof(unsigned long long));
   const size_t o_wlist = off;   off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
   const size_t o_slist = off;   off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
@@ -241,8 +242,8 @@ ws_status ws_set_stream(ws_ctx* c, void* s) {
 
 uint32_t ws_last_launch_count(const ws_ctx* c) { return c ? c->last_launches : 0; }
 
-static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_scan", "k_warp", "k_wclass", "k_smset",
-                                           "k_sclass", "k_rows", "k_fold", "k_model",  "k_rank"};
+static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_scan", "k_warp", "k_wclass", "k_smset", "k_sclass",
+                                           "k_rows",   "k_fold", "k_sect", "k_model",  "k_rank"};
 
 const char* ws_kernel_name(uint32_t i) { return i < (uint32_t)K_NKINDS ? kKindNames[i] : nullptr; }
 
@@ -425,6 +426,11 @@ ws_status ws_describe_gpu(ws_ctx* c, const ws_gpu* g, uint32_t* id) {
   if (g->pair_window_bytes < 1 || g->l2_sections < 1 || g->l1_bytes < 1 || g->l2_bytes < 1)
     return fail(c, WS_EINVAL, "cache sizes / window must be >= 1");
   if (!(g->clock_hz > 0) || !(g->dram_bw > 0) || !(g->l2_bw > 0)) return fail(c, WS_EINVAL, "rates must be > 0");
+  if (!(g->link_bw >= 0) || g->link_bw > 1e30) return fail(c, WS_EINVAL, "link_bw must be >= 0 and finite");
+  D.lg_page = g->page_bytes ? lg2(g->page_bytes) : -1;
+  if (g->page_bytes && (D.lg_page < 0 || g->page_bytes < g->line_bytes || D.lg_page > 40))
+    return fail(c, WS_EINVAL, "page_bytes must be 0 or a power of two >= line_bytes (<= 2^40)");
+  if (g->l2_sections > (uint32_t)kMaxSections) return fail(c, WS_ELIMIT, "l2_sections must be <= 4");
   c->hg.push_back(D);
   c->dirty = true;
   *id = (uint32_t)(c->hg.size() - 1);

@@ -46,8 +46,9 @@ struct DKernel {
 
 struct DGpu {
   ws_gpu g;
-  int32_t lg_sector, lg_line, lg_bank, lg_hw, lg_nbanks, pad;
+  int32_t lg_sector, lg_line, lg_bank, lg_hw, lg_nbanks, lg_page;  // lg_page: -1 = no pages
 };
+constexpr int kMaxSections = 4;    // L2 sections (k_sect keeps 2 triples per section)
 
 // One per-thread instruction after fold dedupe:
 // address = C + (pitch . base) << lg_elem ; issued iff kmask & active_kappas != 0.
@@ -97,18 +98,24 @@ struct DPlan {
   RangeInfo rng[5];
   int64_t bnd[20];
   int32_t nb, pad3;
+  // model variants (ws_config.variant) and the outlook metrics (NEXT-3 / NEXT-4)
+  int32_t variant, mdim;         // mdim: wave / layer-set footprints in the multidimensional space
+  int32_t want_pages, want_sect; // k_sect: TLB pages / L2-section footprints wanted
+  int64_t n_sect_items;          // k_sect work items (fields) of this config
 };
 
 // per-config accumulator slots (u64, atomically added by the worker kernels)
 enum {
   A_LUP = 0, A_WF, A_REQ_LD, A_REQ_ST, A_SM_SEC, A_SM_LIN,
-  A_WLD, A_WST, A_WLIN, A_LY, A_LZ, A_OVY, A_OVZ, A_N = 16
+  A_WLD, A_WST, A_WLIN, A_LY, A_LZ, A_OVY, A_OVZ,
+  A_PAGES, A_SECLD, A_SECLIN, A_ULD, A_ULIN,   // k_sect (linear address space)
+  A_N = 24
 };
 
 struct DPrefix {
-  int64_t warp, wclass, set, sclass, chunk, fold;
+  int64_t warp, wclass, set, sclass, chunk, fold, sect;
 };
-constexpr int kNPrefix = 6;
+constexpr int kNPrefix = 7;
 constexpr int kWSlots = 32 * 64 * 8;  // per config: warp index (<32) x residue (<64) x clip pattern (<8)
 constexpr int kSSlots = 64 * 8;       // per config: residue (<64) x clip pattern (<8)
 
@@ -133,8 +140,8 @@ struct Scratch {
 };
 
 // kernel kinds, in launch order (ws_kernel_name)
-enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_MODEL, K_RANK, K_NKINDS };
-constexpr int kEstimateKernels = 9;
+enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_SECT, K_MODEL, K_RANK, K_NKINDS };
+constexpr int kEstimateKernels = 10;
 
 // Streams and fork/join events of one context: the three worker chains (warp scope, SM-set
 // scope, row scope) run concurrently after k_scan.

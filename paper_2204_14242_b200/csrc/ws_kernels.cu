@@ -223,7 +223,8 @@ __device__ __forceinline__ int find_config(const DPrefix* pre, int n, long long 
                         : MEMBER == 2 ? pre[mid].set
                         : MEMBER == 3 ? pre[mid].sclass
                         : MEMBER == 4 ? pre[mid].chunk
-                                      : pre[mid].fold;
+                        : MEMBER == 5 ? pre[mid].fold
+                                      : pre[mid].sect;
     if (v <= item) lo = mid;
     else hi = mid - 1;
   }
@@ -237,7 +238,8 @@ __device__ __forceinline__ long long prefix_member(const DPrefix& p) {
          : MEMBER == 2 ? p.set
          : MEMBER == 3 ? p.sclass
          : MEMBER == 4 ? p.chunk
-                       : p.fold;
+         : MEMBER == 5 ? p.fold
+                       : p.sect;
 }
 
 // find_config by the whole warp (item warp-uniform): 32-ary search, one load round per
@@ -281,6 +283,21 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
       P.status = WS_EINVAL;
       return;
     }
+  if (cf.variant & ~7u) {  // unknown WS_VAR_* bits
+    P.status = WS_EINVAL;
+    return;
+  }
+  P.variant = (int)cf.variant;
+  P.mdim = (cf.variant & WS_VAR_MDIM) != 0;
+  if (P.mdim) {  // padded rows (whole lines) must keep a z-plane within the 32-bit plane arithmetic
+    for (int i = 0; i < K.n_fields; ++i) {
+      const long long rowb = (((K.f[i].ext[0] << K.f[i].lg_elem) + (1ll << G.lg_line) - 1) >> G.lg_line) << G.lg_line;
+      if (rowb * K.f[i].ext[1] > (1ll << 31) - (1ll << 14)) {
+        P.status = WS_ELIMIT;
+        return;
+      }
+    }
+  }
   const long long T = (long long)cf.block[0] * cf.block[1] * cf.block[2];
   if (T > (long long)G.g.max_thr_blk) {
     P.status = WS_ELIMIT;
@@ -330,6 +347,12 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   P.nsets = (long long)G.g.n_sm < P.W ? (long long)G.g.n_sm : P.W;
   P.Ly0 = s - P.G[0] > 0 ? s - P.G[0] : 0;
   P.Lz0 = s - P.G[0] * P.G[1] > 0 ? s - P.G[0] * P.G[1] : 0;
+  // WS_VAR_PREV_WAVE (V100 / SBAC model): both look-back sets are the preceding wave
+  if (cf.variant & WS_VAR_PREV_WAVE) P.Ly0 = P.Lz0 = s - P.W > 0 ? s - P.W : 0;
+  // NEXT-4 outlook metrics: TLB pages (page size given) and L2-section footprints (several
+  // sections and either the link limiter or the duplication-based capacity wanted)
+  P.want_pages = G.lg_page >= 0;
+  P.want_sect = G.g.l2_sections > 1 && (G.g.link_bw > 0 || (cf.variant & WS_VAR_L2_DUP));
   for (int d = 0; d < 3; ++d) {
     P.fd_BF[d] = make_fdiv((unsigned long long)P.BF[d]);
     const long long last = (K.hi[d] - K.lo[d]) - (P.G[d] - 1) * P.BF[d];
@@ -566,6 +589,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     Q.n_sclass_items = 0;
     Q.n_chunks = cb;
     Q.n_fields = K.n_fields;
+    Q.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
     Q.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
     plans[c] = Q;
   }
@@ -579,7 +603,8 @@ __device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
     case 2: return P.n_set_items;
     case 3: return P.n_sclass_items;
     case 4: return P.n_chunks;
-    default: return P.n_fields;
+    case 5: return P.n_fields;
+    default: return P.n_sect_items;
   }
 }
 
@@ -588,7 +613,7 @@ __global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, 
                                                unsigned long long* __restrict__ lists) {
   __shared__ long long s_w[32][kNPrefix];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < 16) work[tid] = 0ull;
+  if (tid < 16) work[tid] = 0ull;  // K_NKINDS <= 16
   if (tid < 4) lists[tid] = 0ull;
   const int seg = (n + nt - 1) / nt;
   long long a[kNPrefix];
@@ -632,13 +657,13 @@ __global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, 
 #pragma unroll
   for (int j = 0; j < kNPrefix; ++j) r[j] = s_w[wid][j] + inc[j] - a[j];
   for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
-    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5]};
+    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
     const DPlan& P = plans[c];
     if (P.status != WS_OK) continue;
 #pragma unroll
     for (int j = 0; j < kNPrefix; ++j) r[j] += plan_count(P, j);
   }
-  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5]};
+  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
 }
 
 // ------------------------------------------------------------------ a2 + a3: warp instructions
@@ -1500,6 +1525,26 @@ __global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans,
   }
 }
 
+// Row layout of field F seen by the wave / layer-set scopes: the field's own (linear address
+// space), or under WS_VAR_MDIM the multidimensional address space realised as a
+// virtual layout whose rows start on a line boundary and are padded to whole lines, with no
+// alignment: (z, y, floor(x * elem / sector)) tuples never share a sector or line across
+// rows, exactly the paper's "two multi dimensional addresses are distinct when their tuples
+// differ"; floor(x * elem / sector) is unchanged by a line-aligned row start.
+__device__ __forceinline__ void field_rows(const DField& F, const DPlan& P, int ll, long long& py, long long& pz,
+                                           long long& align) {
+  if (!P.mdim) {
+    py = F.pitch[1];
+    pz = F.pitch[2];
+    align = F.align;
+    return;
+  }
+  const long long rowb = (((F.ext[0] << F.lg_elem) + (1ll << ll) - 1) >> ll) << ll;
+  py = rowb >> F.lg_elem;
+  pz = py * F.ext[1];
+  align = 0;
+}
+
 // ------------------------------------------------------------------ a5 + a6: wave and layer sets
 // ranges: 0 = wave [s, s+W), 1 = L_y [Ly0, s), 2 = L_z [Lz0, s), 3 = L_y + wave, 4 = L_z + wave
 
@@ -1712,7 +1757,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
     const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
     const int y0 = (int)RI.y0, ny = (int)RI.ny;
     const int z = (int)(RI.z0 + (ci - RI.chunk_begin));  // one plane per chunk (ppc == 1)
-    const long long py = F.pitch[1], pz = F.pitch[2];
+    long long py, pz, falign;
+    field_rows(F, P, ll, py, pz, falign);
     const int per = plane_period(pz, le, ll);
     if (per > 0) {
       int seg = (int)RI.z0;
@@ -1751,7 +1797,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
       ranges_c = c;
     }
     const int nb = P.nb;
-    const long long R0p = F.align + ((py * y0 + pz * z) << le);
+    const long long R0p = falign + ((py * y0 + pz * z) << le);
     const long long Bp = (R0p >> ll) << ll;
     const int off0 = (int)(R0p - Bp);
     const int pystep = (int)(py << le);
@@ -1891,7 +1937,9 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
     const DField& F = ks[P.kid].f[fi];
     const DGpu& G = gs[P.gid];
     const int ls = G.lg_sector, ll = G.lg_line;
-    const long long pbytes = F.pitch[2] << F.lg_elem;
+    long long py, pz, falign;
+    field_rows(F, P, ll, py, pz, falign);
+    const long long pbytes = pz << F.lg_elem;
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
     const long long per_l = (nch + blockDim.x - 1) / blockDim.x;
@@ -1925,6 +1973,150 @@ __global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, c
       atomicAdd(a + A_OVZ, (unsigned long long)(t[0].c + t[5].c - t[8].c));
     }
   }
+}
+
+// ------------------------------------------------------------------ NEXT-4: pages + L2 sections
+// Union of the element intervals produced by gen(cb) in one address row (element 0 at byte
+// R0): appends the union's sectors (ts), lines (tl) and pages (tp) in increasing order.
+template <class Gen>
+__device__ __forceinline__ void row_union_p(const Gen& gen, long long R0, int le, int ls, int ll, int lp, Tri* ts,
+                                            Tri* tl, Tri* tp) {
+  const long long INF = LLONG_MAX;
+  long long start = INF;
+  gen([&](long long xs, long long xe) { start = xs < start ? xs : start; });
+  while (start != INF) {
+    long long end = start, nxt;
+    bool grew;
+    do {
+      grew = false;
+      nxt = INF;
+      gen([&](long long xs, long long xe) {
+        if (xs <= end) {
+          if (xe > end) {
+            end = xe;
+            grew = true;
+          }
+        } else if (xs < nxt) {
+          nxt = xs;
+        }
+      });
+    } while (grew);
+    const long long a0 = R0 + (start << le), a1 = R0 + ((end - 1) << le);
+    if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
+    if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
+    if (tp) tri_add(*tp, a0 >> lp, a1 >> lp);
+    start = nxt;
+  }
+}
+
+constexpr int kSectNQ = 2 * kMaxSections + 3;  // per section: load sectors, lines; union: load sectors, lines; pages
+
+// One CTA per (config, field) of the configs that want the outlook metrics.
+// Linear address space.  The wave's rows (y, z) are walked in address order, threads taking
+// contiguous row ranges; per row and offset group, the wave blocks of the group's block row
+// are split into pieces of one L2 section (SM j = (B - s) mod n_sm belongs to section
+// floor(j * S / n_sm)), each piece a cell x-interval shifted by the group's x-run.  Unions
+// per section and over all sections give ordered triples; an ordered CTA reduction gives the
+// field's counts.
+__global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                              const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                              unsigned long long* __restrict__ acc,
+                                              unsigned long long* __restrict__ work) {
+  __shared__ Tri s_red[(256 / 32) * kSectNQ];
+  const long long total = pre[n].sect;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  unsigned long long my_ops = 0;
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+    const int c = find_config<6>(pre, n, item);
+    const int fi = (int)(item - pre[c].sect);
+    const DPlan& P = plans[c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    const DField& F = K.f[fi];
+    const int le = F.lg_elem, ls = G.lg_sector, ll = G.lg_line, lp = G.lg_page >= 0 ? G.lg_page : ll;
+    const int S = (int)G.g.l2_sections;
+    const long long nsm = G.g.n_sm, s = P.s, Wb = P.W, Gx = P.G[0], Gy = P.G[1];
+    // cell box of the wave's block rows, then the field rows its accesses can touch
+    const long long rA = s / Gx, rB = (s + Wb - 1) / Gx;
+    const long long byA = rA % Gy, bzA = rA / Gy, byB = rB % Gy, bzB = rB / Gy;
+    long long ylo = P.lo[1], yhi = P.hi[1];
+    if (bzA == bzB) {
+      ylo = P.lo[1] + byA * P.BF[1];
+      yhi = P.lo[1] + (byB + 1) * P.BF[1];
+      if (yhi > P.hi[1]) yhi = P.hi[1];
+    }
+    long long zlo = P.lo[2] + bzA * P.BF[2], zhi = P.lo[2] + (bzB + 1) * P.BF[2];
+    if (zhi > P.hi[2]) zhi = P.hi[2];
+    long long y0 = ylo + F.oy_min, y1 = yhi + F.oy_max, z0 = zlo + F.oz_min, z1 = zhi + F.oz_max;
+    if (y0 < 0) y0 = 0;
+    if (z0 < 0) z0 = 0;
+    if (y1 > F.ext[1]) y1 = F.ext[1];
+    if (z1 > F.ext[2]) z1 = F.ext[2];
+    const long long ny = y1 > y0 ? y1 - y0 : 0, nz = z1 > z0 ? z1 - z0 : 0;
+    const long long nrows = (F.g_end > F.g_begin) ? ny * nz : 0;
+    const long long per = (nrows + nt - 1) / nt;
+    Tri t[kSectNQ];
+#pragma unroll
+    for (int q = 0; q < kSectNQ; ++q) t[q] = tri_empty();
+    for (long long ri = tid * per; ri < nrows && ri < (tid + 1) * per; ++ri) {
+      const long long z = z0 + ri / ny, y = y0 + ri % ny;
+      const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << le);
+      my_ops += (unsigned long long)(F.g_end - F.g_begin);
+      // intervals of (section sel or -1 = any, kind mask km: 1 = loads, 3 = loads + stores)
+      auto gen_for = [&](int sel, int km) {
+        return [&, sel, km](auto&& cb) {
+          for (int g = F.g_begin; g < F.g_end; ++g) {
+            const DGroup gr = K.g[g];
+            if (!((km >> gr.kind) & 1)) continue;
+            const long long yy = y - gr.oy, zz = z - gr.oz;
+            if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
+            const long long r = (yy - P.lo[1]) / P.BF[1] + Gy * ((zz - P.lo[2]) / P.BF[2]);
+            long long b0 = r * Gx > s ? r * Gx : s;
+            const long long b1 = (r + 1) * Gx < s + Wb ? (r + 1) * Gx : s + Wb;
+            while (b0 < b1) {
+              // piece of blocks on SMs of one section
+              const long long j = (b0 - s) % nsm;
+              const long long sec = j * S / nsm;
+              const long long jend = sec + 1 < S ? ((sec + 1) * nsm + S - 1) / S : nsm;
+              long long e = b0 + (jend - j);
+              if (e > b1) e = b1;
+              if (sel < 0 || sel == sec) {
+                const long long xs = P.lo[0] + (b0 - r * Gx) * P.BF[0];
+                long long xe = P.lo[0] + (e - r * Gx) * P.BF[0];
+                if (xe > P.hi[0]) xe = P.hi[0];
+                if (xs < xe) cb(xs + F.run_lo[gr.run], xe + F.run_hi[gr.run]);
+              }
+              b0 = e;
+            }
+          }
+        };
+      };
+      if (P.want_sect) {
+        for (int i = 0; i < S; ++i) {
+          row_union_p(gen_for(i, 1), R0, le, ls, ll, lp, &t[2 * i], nullptr, nullptr);
+          row_union_p(gen_for(i, 3), R0, le, ls, ll, lp, nullptr, &t[2 * i + 1], nullptr);
+        }
+        row_union_p(gen_for(-1, 1), R0, le, ls, ll, lp, &t[2 * kMaxSections], nullptr, nullptr);
+      }
+      row_union_p(gen_for(-1, 3), R0, le, ls, ll, lp, nullptr, &t[2 * kMaxSections + 1],
+                  P.want_pages ? &t[2 * kMaxSections + 2] : nullptr);
+    }
+    cta_ordered_reduce<kSectNQ>(t, s_red);
+    if (tid == 0 && nrows > 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      long long sld = 0, slin = 0;
+      for (int i = 0; i < kMaxSections; ++i) {
+        sld += t[2 * i].c;
+        slin += t[2 * i + 1].c;
+      }
+      atomicAdd(a + A_SECLD, (unsigned long long)sld);
+      atomicAdd(a + A_SECLIN, (unsigned long long)slin);
+      atomicAdd(a + A_ULD, (unsigned long long)t[2 * kMaxSections].c);
+      atomicAdd(a + A_ULIN, (unsigned long long)t[2 * kMaxSections + 1].c);
+      atomicAdd(a + A_PAGES, (unsigned long long)t[2 * kMaxSections + 2].c);
+    }
+  }
+  if (my_ops) atomicAdd(work + K_SECT, my_ops);
 }
 
 // ------------------------------------------------------------------ a7: model (FP64)
@@ -1976,7 +2168,15 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
   const double v_l2l1_ld = (double)R.sm_ld_sectors + (1.0 - R.R_l1) * red1;
   const double v_l1l2_st = (double)R.l1_req_st_sectors;
   // L2: split-L2 effective capacity; layer-set overlaps (Q13-Q16)
-  const double l2_eff = (double)G.g.l2_bytes / (double)G.g.l2_sections;
+  // NEXT-4 outlook metrics (k_sect, linear address space)
+  R.wave_pages = a[A_PAGES];
+  R.l2_dup_lines = P.want_sect ? a[A_SECLIN] - a[A_ULIN] : 0ull;
+  R.l2_link_sectors = P.want_sect ? a[A_SECLD] - a[A_ULD] : 0ull;
+  double l2_eff = (double)G.g.l2_bytes / (double)G.g.l2_sections;
+  // WS_VAR_L2_DUP: the capacity holds U + dup line copies for U distinct lines
+  if ((P.variant & WS_VAR_L2_DUP) && P.want_sect && a[A_ULIN] > 0)
+    l2_eff = (double)G.g.l2_bytes * (double)a[A_ULIN] / (double)(a[A_ULIN] + R.l2_dup_lines);
+  R.l2_eff_bytes = l2_eff;
   R.O_y = (double)R.ly_lines * line / l2_eff;
   R.O_z = (double)R.lz_lines * line / l2_eff;
   R.R_y = gompertz(G.g.hit_abc[1], R.O_y);
@@ -1996,8 +2196,10 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
   R.t_l1 = (double)R.l1_wavefronts / (lup * (double)G.g.n_sm * G.g.clock_hz);
   R.t_l2 = sector * (v_l2l1_ld + v_l1l2_st) / (lup * G.g.l2_bw);
   R.t_dram = sector * (v_dram_ld + v_dram_st) / (lup * G.g.dram_bw);
-  const double tm = fmax(R.t_l1, fmax(R.t_l2, R.t_dram));
-  R.limiter = R.t_dram >= tm ? 2u : (R.t_l2 >= tm ? 1u : 0u);
+  // the inter-section link as an additional L2 limiter
+  R.t_link = G.g.link_bw > 0 ? sector * (double)R.l2_link_sectors / (lup * G.g.link_bw) : 0.0;
+  const double tm = fmax(fmax(R.t_l1, R.t_link), fmax(R.t_l2, R.t_dram));
+  R.limiter = R.t_dram >= tm ? 2u : (R.t_l2 >= tm ? 1u : (R.t_link >= tm ? 3u : 0u));
   R.t_pred = tm * K.cells;
   out[c] = R;
 }
@@ -2078,6 +2280,9 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   beg(K_WCLASS, m);
   k_wclass<<<persist, 256, 0, m>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
   end(K_WCLASS, m);
+  beg(K_SECT, m);
+  k_sect<<<n_sm_dev * 2, 256, 0, m>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.work);
+  end(K_SECT, m);
   // join
   cudaEventRecord(st.join[0], a);
   cudaEventRecord(st.join[1], b);

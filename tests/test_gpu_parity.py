@@ -269,3 +269,61 @@ def test_full_size_b200_like_sampled(ctx):
     for j, i in enumerate(idx):
         errs += compare(g[i], o[j], f"b200[{i}] {cf[i]}")
     assert not errs, "\n".join(errs)
+
+
+# ----------------------------------------------------------------- NEXT-3 / NEXT-4 variants + outlook metrics
+def test_variants_paper_space_64(ctx):
+    """Every other configuration of the 168-config space on 64^3 with each WS_VAR_* combination
+    (multidimensional address space, previous-wave reuse, duplication-based L2 capacity), TLB
+    pages and the L2 section link limiter on."""
+    gp = dict(W.gpu_a100(), page_bytes=64 * 1024, link_bw=2e12)
+    cf = [c + (1 + i % 7,) for i, c in enumerate(W.space_stencil_paper()[::2])]
+    g, _ = assert_parity(ctx, W.k25(64), gp, cf, "var64")
+    assert any(r["l2_link_sectors"] > 0 for r in g) and all(r["wave_pages"] > 0 for r in g)
+
+
+def test_variants_lbm_and_sections(ctx):
+    """LBM15 (32 arrays) with 3 and 4 L2 sections, 4 KiB pages, every variant."""
+    for S in (3, 4):
+        gp = dict(W.gpu_a100(), n_sm=12, l2_sections=S, page_bytes=4096, link_bw=5e11)
+        cf = [c + (v,) for c in W.space_lbm()[::6] for v in (0, 5, 6)]
+        assert_parity(ctx, W.lbm15(20), gp, cf, f"lbmS{S}")
+
+
+def test_mdim_paper_example_gpu(ctx):
+    """P:557-562 through the GPU path: 128 multidimensional vs 129 linear sectors."""
+    k = {"fields": [{"extent": (256, 4, 1), "pitch": (1, 256, 1024), "align": -8, "elem": 8}],
+         "accesses": [(0, 0, (0, 1, 0))], "dom_lo": (0, 0, 0), "dom_hi": (256, 2, 1), "regs": 0, "flops": 0.0}
+    gp = dict(W.gpu_a100(), n_sm=1)
+    g, _ = assert_parity(ctx, k, gp, [((256, 2, 1), (1, 1, 1), 1, 1), ((256, 2, 1), (1, 1, 1), 1, 0)], "mdim")
+    assert g[0]["wave_ld_sectors"] == 128 and g[1]["wave_ld_sectors"] == 129
+
+
+def test_variant_errors(ctx):
+    from paper_2204_14242_b200 import WSError, config_array, result_dicts
+    kid, gid = ctx.describe_kernel(W.k7(8)), ctx.describe_gpu(W.gpu_v100())
+    r = result_dicts(ctx.estimate(config_array(kid, gid, [((32, 1, 1), (1, 1, 1), 0, 8)])))
+    assert r[0]["status"] == 1
+    for bad, st in [(dict(W.gpu_a100(), l2_sections=5), 2), (dict(W.gpu_a100(), page_bytes=100), 1),
+                    (dict(W.gpu_a100(), page_bytes=64), 1), (dict(W.gpu_a100(), link_bw=-1.0), 1)]:
+        with pytest.raises(WSError) as e:
+            ctx.describe_gpu(bad)
+        assert e.value.status == st
+
+
+def test_full_size_variants_sampled(ctx):
+    """configs[1] at 512^3 with variant bits 7 and the link limiter: whole space in one launch,
+    three configurations recomputed by the oracle."""
+    k, cf = W.k25(512), [c + (7,) for c in W.space_stencil_paper()]
+    gp = dict(W.gpu_a100(), page_bytes=2 * 1024 * 1024, link_bw=2e12)
+    g, _ = run_gpu(ctx, k, gp, cf)
+    idx = [i for i, c in enumerate(cf) if c[0] in ((512, 2, 1), (32, 32, 1)) and c[1] == (1, 1, 1)]
+    idx += [i for i, c in enumerate(cf) if c[0] == (64, 4, 4) and c[1] == (1, 1, 2)]
+    o = O.estimate_batch(k, gp, [cf[i] for i in idx], NT)
+    errs = []
+    for j, i in enumerate(idx):
+        errs += compare(g[i], o[j], f"fullvar[{i}] {cf[i]}")
+    assert not errs, "\n".join(errs)
+    for r in g:
+        assert r["ov_y"] == r["ov_z"] and r["wave_pages"] > 0
+        assert 0 < r["l2_eff_bytes"] <= gp["l2_bytes"]
