@@ -130,6 +130,8 @@ def set_counts(kernel, gpu, cfg):
         sec_lin[sec] |= footprint(kernel, cells, (0, 1), ll)
     dup = sum(len(x) for x in sec_lin) - len(set().union(*sec_lin))
     link = sum(len(x) for x in sec_ld) - len(set().union(*sec_ld))
+    if not (S > 1 and (gpu.get("link_bw", 0.0) > 0 or geo["variant"] & 4)):   # reported on request (ws.h)
+        dup = link = 0
     return dict(lup_wave=len(wcells), sm_ld_sectors=sm_sec, sm_ld_lines=sm_lin,
                 wave_ld_sectors=len(WLD), wave_st_sectors=len(WST), wave_lines=len(WLIN),
                 ly_lines=len({v[:-1] + (v[-1] >> d,) for v in FY}), lz_lines=len({v[:-1] + (v[-1] >> d,) for v in FZ}),
