@@ -214,3 +214,54 @@ def halfwarp_wavefronts(addrs, gpu):
 def hit_rate(abc, O):
     a = (C.c_double * 3)(*abc)
     return float(lib().wso_hit_rate(a, O))
+
+
+# ----------------------------------------------------------------- NEXT-1: simulated hit rates
+SIM_INT = ["status", "capacity_bytes", "l1_requests", "l1_compulsory", "l1_misses", "st_requests",
+           "st_compulsory", "st_misses", "ov_y", "y_resident", "ov_z_only", "z_resident"]
+SIM_FP = ["O_l1", "R_l1", "O_y", "R_y", "O_z", "R_z", "O_st", "R_st"]
+
+
+class SimResult(C.Structure):
+    _fields_ = [(n, I64) for n in SIM_INT] + [(n, C.c_double) for n in SIM_FP]
+
+
+def _sim_lib():
+    L = lib()
+    if not getattr(L, "_sim_ready", False):
+        L.wso_simulate_batch.argtypes = [C.POINTER(Kernel), C.POINTER(Gpu), C.POINTER(Config), I64,
+                                         C.POINTER(I64), I64, C.POINTER(SimResult), I64]
+        L.wso_simulate_batch.restype = None
+        L.wso_fit_gompertz.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), I64, C.POINTER(C.c_double)]
+        L.wso_fit_gompertz.restype = C.c_double
+        L._sim_ready = True
+    return L
+
+
+def simulate_batch(kernel, gpu, configs, capacities, n_threads=1):
+    """-> [[dict per capacity] per config]"""
+    K, G = make_kernel(kernel), make_gpu(gpu)
+    X = (Config * len(configs))(*[make_config(c) for c in configs])
+    caps = (I64 * len(capacities))(*capacities)
+    R = (SimResult * (len(configs) * len(capacities)))()
+    _sim_lib().wso_simulate_batch(C.byref(K), C.byref(G), X, len(configs), caps, len(capacities), R, n_threads)
+    out = []
+    for i in range(len(configs)):
+        row = []
+        for k in range(len(capacities)):
+            r = R[i * len(capacities) + k]
+            d = {n: int(getattr(r, n)) for n in SIM_INT}
+            d.update({n: float(getattr(r, n)) for n in SIM_FP})
+            row.append(d)
+        out.append(row)
+    return out
+
+
+def fit_gompertz(O, R):
+    """-> ((a, b, c), residual sum of squares)"""
+    n = len(O)
+    o = (C.c_double * n)(*O)
+    r = (C.c_double * n)(*R)
+    th = (C.c_double * 3)()
+    rss = _sim_lib().wso_fit_gompertz(o, r, n, th)
+    return (th[0], th[1], th[2]), float(rss)

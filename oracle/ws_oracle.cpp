@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cmath>
 #include <iterator>
+#include <list>
 #include <map>
 #include <set>
 #include <thread>
@@ -445,6 +446,259 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
   return WSO_OK;
 }
 
+// ================================================================ NEXT-1: simulated hit rates
+// replace the paper's counter-based curve fits by
+// (O, R) samples from a sectored, fully associative LRU simulator (SPEC cachesim-oracle,
+// S:507-555) replaying the configuration's own request streams, and a least-squares fit of
+// the Gompertz form ("coarse grid search ... followed by local refinement").
+//
+// Request stream of a block B: warps in order; per warp the instructions in canonical order
+// (field, kind [loads first], offset C = elem * (pitch . r)); per warp instruction its distinct
+// sectors in ascending order (the coalesced requests).  Every request updates LRU
+// recency; a request to a resident line with the sector invalid, or to an absent line, is a
+// miss (the line is allocated with that sector valid, evicting the least recently used line).
+
+struct SimReq {
+  Key sector;
+  bool is_store;
+};
+
+// Requests of blocks [B0, B1) in schedule order, only those of kind in `kinds` (bit mask).
+std::vector<SimReq> block_trace(const wso_kernel& K, const wso_gpu& g, const Plan& p, const std::vector<int64_t>& blocks,
+                                int kinds) {
+  std::vector<const Instr*> order;
+  for (const Instr& I : p.instr) order.push_back(&I);
+  auto offs = [&](const Instr* I) {
+    const wso_field& f = K.fields[I->field];
+    return f.elem_bytes * (f.pitch[0] * I->r[0] + f.pitch[1] * I->r[1] + f.pitch[2] * I->r[2]);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](const Instr* a, const Instr* b) {
+    if (a->field != b->field) return a->field < b->field;
+    if (a->is_store != b->is_store) return a->is_store < b->is_store;
+    return offs(a) < offs(b);
+  });
+  std::vector<SimReq> out;
+  const int64_t n_warps = ceildiv(p.T, 32);
+  for (int64_t B : blocks)
+    for (int64_t w = 0; w < n_warps; ++w)
+      for (const Instr* I : order) {
+        if (!((kinds >> I->is_store) & 1)) continue;
+        std::set<int64_t> secs;
+        for (int64_t lane = 0; lane < 32; ++lane) {
+          int64_t t = w * 32 + lane;
+          if (t >= p.T) break;
+          V3 base = base_cell(p, B, t);
+          if (issues(p, base, *I)) secs.insert(floordiv(instr_address(K, base, *I), g.sector_bytes));
+        }
+        for (int64_t sct : secs) out.push_back(SimReq{Key(I->field, sct), I->is_store != 0});
+      }
+  return out;
+}
+
+// Fully associative LRU cache over lines with per-sector valid bits.
+struct SimCache {
+  int64_t cap, spl;
+  std::list<Key> lru;  // front = most recently used line
+  std::map<Key, std::pair<std::list<Key>::iterator, std::set<int64_t>>> lines;
+  SimCache(int64_t cap_lines, int64_t sectors_per_line) : cap(std::max<int64_t>(1, cap_lines)), spl(sectors_per_line) {}
+  bool access(const Key& s) {  // returns hit
+    Key ln(s.first, floordiv(s.second, spl));
+    auto it = lines.find(ln);
+    if (it != lines.end()) {
+      lru.splice(lru.begin(), lru, it->second.first);
+      bool hit = it->second.second.count(s.second) > 0;
+      it->second.second.insert(s.second);
+      return hit;
+    }
+    lru.push_front(ln);
+    lines[ln] = std::make_pair(lru.begin(), std::set<int64_t>{s.second});
+    if ((int64_t)lines.size() > cap) {
+      lines.erase(lru.back());
+      lru.pop_back();
+    }
+    return false;
+  }
+  bool valid(const Key& s) const {
+    auto it = lines.find(Key(s.first, floordiv(s.second, spl)));
+    return it != lines.end() && it->second.second.count(s.second) > 0;
+  }
+};
+
+int64_t simulate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, const int64_t* caps, int64_t ncap,
+                 wso_sim_result* out) {
+  wso_result r;
+  int64_t st = estimate(K, g, c, r);
+  if (st == WSO_OK && (c.variant & WSO_VAR_MDIM)) st = WSO_EINVAL;  // the simulator replays linear addresses
+  if (st == WSO_OK && g.line_bytes / g.sector_bytes > 32) st = WSO_ELIMIT;
+  for (int64_t k = 0; k < ncap; ++k) {
+    out[k] = wso_sim_result();
+    out[k].status = st;
+    out[k].capacity_bytes = caps[k];
+    if (caps[k] < 1) out[k].status = WSO_EINVAL;
+  }
+  if (st != WSO_OK) return st;
+  Plan p;
+  wso_result tmp;
+  make_plan(K, g, c, p, tmp);
+  const int64_t spl = g.line_bytes / g.sector_bytes;
+  // ---- L1: each SM set's load requests through a fresh cache (Q8/Q9)
+  int64_t l1_req = 0;
+  std::vector<int64_t> l1_miss(ncap, 0);
+  for (int64_t j = 0; j < p.n_sets; ++j) {
+    std::vector<int64_t> blocks;
+    for (int64_t B = p.s + j; B < p.s + p.W; B += g.n_sm) blocks.push_back(B);
+    std::vector<SimReq> tr = block_trace(K, g, p, blocks, 1);
+    l1_req += (int64_t)tr.size();
+    for (int64_t k = 0; k < ncap; ++k) {
+      SimCache cache(caps[k] / g.line_bytes, spl);
+      for (const SimReq& q : tr) l1_miss[k] += cache.access(q.sector) ? 0 : 1;
+    }
+  }
+  // ---- stores: the wave's requests (loads and stores) in schedule order; misses among stores
+  std::vector<int64_t> wave;
+  for (int64_t B = p.s; B < p.s + p.W; ++B) wave.push_back(B);
+  std::vector<SimReq> wtr = block_trace(K, g, p, wave, 3);
+  int64_t st_req = 0, st_comp = 0;
+  std::set<Key> WLD, seen;
+  for (const SimReq& q : wtr) {
+    if (q.is_store) {
+      ++st_req;
+      if (!seen.count(q.sector)) ++st_comp;
+    } else {
+      WLD.insert(q.sector);
+    }
+    seen.insert(q.sector);
+  }
+  std::vector<int64_t> st_miss(ncap, 0);
+  for (int64_t k = 0; k < ncap; ++k) {
+    SimCache cache(caps[k] / g.line_bytes, spl);
+    for (const SimReq& q : wtr) {
+      bool hit = cache.access(q.sector);
+      if (q.is_store && !hit) ++st_miss[k];
+    }
+  }
+  // ---- layer sets: replay L_z = [Lz0, s) (loads + stores, Q15), then count the wave's
+  // overlap sectors still valid: those of F_Ly (touched by blocks >= Ly0) for the y curve,
+  // the rest of WLD n F_Lz for the z curve (Q16: hits = R_y ov_y + R_z (ov_z - ov_y)).
+  std::vector<int64_t> lz, ly;
+  for (int64_t B = p.Lz0; B < p.s; ++B) lz.push_back(B);
+  for (int64_t B = p.Ly0; B < p.s; ++B) ly.push_back(B);
+  std::vector<SimReq> ltr = block_trace(K, g, p, lz, 3);
+  std::set<Key> FY, FZ;
+  for (const SimReq& q : block_trace(K, g, p, ly, 3)) FY.insert(q.sector);
+  for (const SimReq& q : ltr) FZ.insert(q.sector);
+  std::vector<Key> ovy, ovz;
+  for (const Key& s : WLD)
+    if (FY.count(s)) ovy.push_back(s);
+    else if (FZ.count(s)) ovz.push_back(s);
+  std::vector<int64_t> yres(ncap, 0), zres(ncap, 0);
+  for (int64_t k = 0; k < ncap; ++k) {
+    SimCache cache(caps[k] / g.line_bytes, spl);
+    for (const SimReq& q : ltr) cache.access(q.sector);
+    for (const Key& s : ovy) yres[k] += cache.valid(s) ? 1 : 0;
+    for (const Key& s : ovz) zres[k] += cache.valid(s) ? 1 : 0;
+  }
+  // ---- samples: O as in the model (Eq. 4) at capacity C; R = hits / redundant requests
+  // (Eq. 3: R_hit = 1 - V_cap / V_red) or resident / potential reuse
+  const double LB = (double)g.line_bytes;
+  for (int64_t k = 0; k < ncap; ++k) {
+    if (out[k].status != WSO_OK) continue;
+    wso_sim_result& o = out[k];
+    const double C = (double)caps[k];
+    o.l1_requests = l1_req;
+    o.l1_compulsory = r.sm_ld_sectors;
+    o.l1_misses = l1_miss[k];
+    o.st_requests = st_req;
+    o.st_compulsory = st_comp;
+    o.st_misses = st_miss[k];
+    o.ov_y = (int64_t)ovy.size();
+    o.y_resident = yres[k];
+    o.ov_z_only = (int64_t)ovz.size();
+    o.z_resident = zres[k];
+    o.O_l1 = ((double)r.sm_ld_lines * LB / (double)p.n_sets) / C;
+    o.O_y = (double)r.ly_lines * LB / C;
+    o.O_z = (double)r.lz_lines * LB / C;
+    o.O_st = (double)r.wave_lines * LB / C;
+    o.R_l1 = l1_req > r.sm_ld_sectors ? (double)(l1_req - o.l1_misses) / (double)(l1_req - r.sm_ld_sectors) : 1.0;
+    o.R_st = st_req > st_comp ? (double)(st_req - o.st_misses) / (double)(st_req - st_comp) : 1.0;
+    o.R_y = o.ov_y > 0 ? (double)o.y_resident / (double)o.ov_y : 1.0;
+    o.R_z = o.ov_z_only > 0 ? (double)o.z_resident / (double)o.ov_z_only : 1.0;
+  }
+  return WSO_OK;
+}
+
+// Least-squares fit of R(O) = a exp(-b exp(-c O)) to n samples:
+// (1) grid search a in {0.5, 0.6, ..., 1.0}, b = exp(-8 + 0.5 j) (j = 0..22),
+//     c = -8 + 0.25 k (k = 0..31); first minimum of the residual sum of squares in (a, b, c) order;
+// (2) 200 Levenberg-Marquardt steps: (J^T J + lambda diag(J^T J)) d = -J^T res, Cramer's rule,
+//     a step is taken only if it lowers the RSS (lambda / 10, floor 1e-15), else lambda * 10.
+double fit_rss(const double* O, const double* R, int64_t n, const double th[3]) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double e = hit_rate(th, O[i]) - R[i];
+    s += e * e;
+  }
+  return s;
+}
+
+double fit_gompertz(const double* O, const double* R, int64_t n, double th[3]) {
+  double best = INFINITY;
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 23; ++j)
+      for (int k = 0; k < 32; ++k) {
+        double t[3] = {0.5 + 0.1 * i, std::exp(-8.0 + 0.5 * j), -8.0 + 0.25 * k};
+        double v = fit_rss(O, R, n, t);
+        if (v < best) {
+          best = v;
+          th[0] = t[0];
+          th[1] = t[1];
+          th[2] = t[2];
+        }
+      }
+  double lambda = 1e-3;
+  for (int it = 0; it < 200; ++it) {
+    double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, gv[3] = {0, 0, 0};
+    for (int64_t m = 0; m < n; ++m) {
+      const double E = std::exp(-th[2] * O[m]);
+      const double F = std::exp(-th[1] * E);
+      const double J[3] = {F, -th[0] * E * F, th[0] * F * th[1] * E * O[m]};
+      const double res = th[0] * F - R[m];
+      for (int a = 0; a < 3; ++a) {
+        gv[a] += J[a] * res;
+        for (int b = 0; b < 3; ++b) A[a][b] += J[a] * J[b];
+      }
+    }
+    double M[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) M[a][b] = A[a][b] + (a == b ? lambda * A[a][a] : 0.0);
+    const double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                       M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                       M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+    if (!(std::fabs(det) > 0.0)) break;
+    double d[3];
+    for (int col = 0; col < 3; ++col) {  // Cramer: replace column col by -g
+      double Mc[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Mc[a][b] = (b == col) ? -gv[a] : M[a][b];
+      d[col] = (Mc[0][0] * (Mc[1][1] * Mc[2][2] - Mc[1][2] * Mc[2][1]) -
+                Mc[0][1] * (Mc[1][0] * Mc[2][2] - Mc[1][2] * Mc[2][0]) +
+                Mc[0][2] * (Mc[1][0] * Mc[2][1] - Mc[1][1] * Mc[2][0])) / det;
+    }
+    double t2[3] = {th[0] + d[0], th[1] + d[1], th[2] + d[2]};
+    double v = fit_rss(O, R, n, t2);
+    if (v < best) {
+      best = v;
+      th[0] = t2[0];
+      th[1] = t2[1];
+      th[2] = t2[2];
+      lambda = std::max(lambda / 10.0, 1e-15);
+    } else {
+      lambda *= 10.0;
+    }
+  }
+  return best;
+}
+
 }  // namespace
 
 extern "C" {
@@ -493,5 +747,31 @@ int64_t wso_halfwarp_wavefronts(const int64_t* a, int64_t n, const wso_gpu* g) {
 }
 
 double wso_hit_rate(const double abc[3], double O) { return hit_rate(abc, O); }
+
+int64_t wso_simulate(const wso_kernel* k, const wso_gpu* g, const wso_config* c, const int64_t* caps, int64_t ncap,
+                     wso_sim_result* out) {
+  return simulate(*k, *g, *c, caps, ncap, out);
+}
+
+void wso_simulate_batch(const wso_kernel* k, const wso_gpu* g, const wso_config* c, int64_t n, const int64_t* caps,
+                        int64_t ncap, wso_sim_result* out, int64_t n_threads) {
+  if (n_threads < 1) n_threads = 1;
+  std::atomic<int64_t> next(0);
+  auto work = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      simulate(*k, *g, c[i], caps, ncap, out + i * ncap);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int64_t i = 1; i < n_threads; ++i) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
+
+double wso_fit_gompertz(const double* O, const double* R, int64_t n, double abc[3]) {
+  return fit_gompertz(O, R, n, abc);
+}
 
 }  // extern "C"

@@ -78,6 +78,16 @@ typedef struct {
   double  l2_eff_bytes, t_link;   /* effective L2 capacity used by the model; link time per LUP */
 } wso_result;
 
+/* NEXT-1: simulated hit-rate samples of one configuration at one cache capacity (see
+ * ws_oracle.cpp "NEXT-1" for the request streams and the cache). */
+typedef struct {
+  int64_t status, capacity_bytes;
+  int64_t l1_requests, l1_compulsory, l1_misses;   /* SM-set load request streams, summed over sets */
+  int64_t st_requests, st_compulsory, st_misses;   /* store requests of the wave stream */
+  int64_t ov_y, y_resident, ov_z_only, z_resident; /* wave load sectors of F_Ly / F_Lz minus F_Ly valid after L_z */
+  double  O_l1, R_l1, O_y, R_y, O_z, R_z, O_st, R_st;
+} wso_sim_result;
+
 /* status codes (same meaning as the ABI's, defined independently) */
 enum { WSO_OK = 0, WSO_EINVAL = 1, WSO_ELIMIT = 2, WSO_EBOUNDS = 3 };
 
@@ -99,6 +109,14 @@ int64_t wso_address(const wso_field* f, const int64_t cell[3]);                 
 int64_t wso_unique_sectors(const int64_t* addr, int64_t n, int64_t sector_bytes);      /* P:494-500 */
 int64_t wso_halfwarp_wavefronts(const int64_t* addr, int64_t n, const wso_gpu* g);    /* P:373-417 */
 double  wso_hit_rate(const double abc[3], double O);                                   /* P:690 */
+
+/* NEXT-1: LRU-simulated (O, R) samples at capacities caps[0..ncap) (out: ncap records per config),
+ * and the least-squares Gompertz fit (returns the residual sum of squares). */
+int64_t wso_simulate(const wso_kernel* k, const wso_gpu* g, const wso_config* c, const int64_t* caps,
+                     int64_t ncap, wso_sim_result* out);
+void    wso_simulate_batch(const wso_kernel* k, const wso_gpu* g, const wso_config* c, int64_t n,
+                           const int64_t* caps, int64_t ncap, wso_sim_result* out, int64_t n_threads);
+double  wso_fit_gompertz(const double* O, const double* R, int64_t n, double abc[3]);
 
 #ifdef __cplusplus
 }

@@ -244,3 +244,26 @@ def replay_blocks(kernel, gpu, cfg, blocks, cache, kinds=(0,), count_from=None):
                 if st in kinds:
                     cache.access((fi, a // SB))
     return cache.misses - (base_miss or 0)
+
+
+# ------------------------------------------------------------- NEXT-1 request streams
+def warp_requests(kernel, geo, B, kinds):
+    """Coalesced requests of block B: warps in order; per warp the instructions ordered by
+    (field, kind, elem * (pitch . r)); per instruction the distinct sectors of its issuing
+    lanes, ascending.  Built from the per-thread traces (thread_trace), grouped by instruction
+    identity (field, kind, cell - thread base)."""
+    T = geo["T"]
+    out = []
+    for w in range(-(-T // 32)):
+        per = {}
+        for t in range(32 * w, min(32 * w + 32, T)):
+            for (fi, st, rel, a) in thread_trace(kernel, geo, B, t):
+                if st in kinds:
+                    per.setdefault((fi, st, rel), set()).add(a // 32)
+        def key(item):
+            (fi, st, rel), _ = item
+            f = kernel["fields"][fi]
+            return (fi, st, f["elem"] * sum(p * r for p, r in zip(f["pitch"], rel)))
+        for (fi, st, rel), secs in sorted(per.items(), key=key):
+            out += [((fi, s), st) for s in sorted(secs)]
+    return out
