@@ -194,6 +194,43 @@ ws_status ws_estimate_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_r
 ws_status ws_rank(ws_ctx* ctx, ws_result* res, size_t n, size_t k, uint32_t* top_idx);
 ws_status ws_rank_async(ws_ctx* ctx, ws_result* d_res, size_t n, size_t k, uint32_t* d_top_idx);
 
+/* ------------------------------------------------------------------ NEXT-1: simulated hit rates
+ * (O, R) samples for the four hit-rate curves from a sectored,
+ * fully associative LRU cache (line_bytes lines, sector valid bits; SPEC cachesim-oracle
+ * S:507-555) replaying the configuration's own request streams, instead of the paper's
+ * hardware-counter measurements.  Request stream of a block: warps in order; per
+ * warp the instructions in canonical order (field, kind [loads first], offset elem*(pitch.r));
+ * per warp instruction its distinct sectors ascending.  Every request updates recency; a
+ * request whose sector is not valid (absent line or invalid sector) is a miss that validates it.
+ *   L1:    each SM set's load requests (blocks s+j, s+j+n_sm, ...) through its own cache;
+ *   store: the wave's requests (loads and stores, blocks s..s+W-1); misses among stores;
+ *   layer: the requests of L_z = [Lz0, s); afterwards the wave's load sectors of F_Ly (ov_y)
+ *          and of F_Lz minus F_Ly (ov_z_only) that are still valid.
+ * R = hits / (requests - compulsory) (Eq. 3) for L1 and stores, resident / overlap for y and z;
+ * O = the model's allocation (Eq. 4) over the capacity.  The GPU computes exact LRU stack
+ * distances once per stream and answers every capacity from them. */
+typedef struct {
+  int32_t status;              /* WS_OK; WS_EINVAL for WS_VAR_MDIM configs or capacity 0;
+                                  WS_ELIMIT: line_bytes/sector_bytes > 32 or a stream >= 2^31 */
+  uint32_t pad;
+  uint64_t capacity_bytes;
+  uint64_t l1_requests, l1_compulsory, l1_misses;
+  uint64_t st_requests, st_compulsory, st_misses;
+  uint64_t ov_y, y_resident, ov_z_only, z_resident;
+  double O_l1, R_l1, O_y, R_y, O_z, R_z, O_st, R_st;
+} ws_sim_result;               /* 160 bytes */
+
+/* Host arrays; synchronous.  out[i * n_cap + k] = configuration i at capacities[k];
+ * n_cap <= 64.  Device memory grows with the streams (about 40 B per request). */
+ws_status ws_simulate(ws_ctx* ctx, const ws_config* cfgs, size_t n, const uint64_t* capacities, uint32_t n_cap,
+                      ws_sim_result* out);
+
+/* Least-squares fit of R(O) = a exp(-b exp(-c O)) to n >= 3 samples, on the device:
+ * grid search a in {0.5,...,1.0}, b = exp(-8 + 0.5 j) (j < 23), c = -8 + 0.25 k (k < 32), then 200
+ * Levenberg-Marquardt steps (accepted only when the residual sum of squares drops).  Host
+ * arrays; abc receives (a, b, c), *rss the residual sum of squares. */
+ws_status ws_fit_gompertz(ws_ctx* ctx, const double* O, const double* R, size_t n, double abc[3], double* rss);
+
 /* Number of kernel launches the last ws_estimate[_async] / ws_rank[_async]
  * call enqueued (for the bench's gpu_launches count). */
 uint32_t ws_last_launch_count(const ws_ctx* ctx);

@@ -242,8 +242,9 @@ ws_status ws_set_stream(ws_ctx* c, void* s) {
 
 uint32_t ws_last_launch_count(const ws_ctx* c) { return c ? c->last_launches : 0; }
 
-static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_scan", "k_warp", "k_wclass", "k_smset", "k_sclass",
-                                           "k_rows",   "k_fold", "k_sect", "k_model",  "k_rank"};
+static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_scan",  "k_warp",  "k_wclass", "k_smset",
+                                           "k_sclass", "k_rows",  "k_fold",  "k_sect",   "k_model",
+                                           "k_rank",   "k_simgen", "k_simrun", "k_fit"};
 
 const char* ws_kernel_name(uint32_t i) { return i < (uint32_t)K_NKINDS ? kKindNames[i] : nullptr; }
 
@@ -557,6 +558,68 @@ ws_status ws_rank(ws_ctx* c, ws_result* res, size_t n, size_t k, uint32_t* top) 
   }
   cudaFree(buf);
   return s;
+}
+
+ws_status ws_simulate(ws_ctx* c, const ws_config* cfgs, size_t n, const uint64_t* caps, uint32_t n_cap,
+                      ws_sim_result* out) {
+  if (!c) return WS_EINVAL;
+  if (n == 0 || n_cap == 0) return WS_OK;
+  if (!cfgs || !caps || !out) return fail(c, WS_EINVAL, "null argument");
+  if (n_cap > (uint32_t)kSimMaxCaps) return fail(c, WS_ELIMIT, "at most 64 capacities per call");
+  if (n > (size_t)(1 << 20)) return fail(c, WS_ELIMIT, "batch larger than 2^20 configurations");
+  if (c->hk.empty() || c->hg.empty()) return fail(c, WS_EUNKNOWN_ID, "describe a kernel and a gpu first");
+  cudaSetDevice(c->device);
+  ws_status s = upload(c);
+  if (s != WS_OK) return s;
+  Scratch S;
+  if ((s = ensure_scratch(c, n, S)) != WS_OK) return s;
+  const size_t need = align_up(n * sizeof(ws_config)) + n * sizeof(ws_result);
+  cudaError_t e;
+  if (need > c->io_cap) {
+    if (c->io) cudaFree(c->io);
+    c->io = nullptr;
+    c->io_cap = 0;
+    if ((e = cudaMalloc(&c->io, need)) != cudaSuccess) return fail(c, WS_ENOMEM, "device io buffer");
+    c->io_cap = need;
+  }
+  ws_config* dc = (ws_config*)c->io;
+  ws_result* dr = (ws_result*)((char*)c->io + align_up(n * sizeof(ws_config)));
+  if ((e = cudaMemcpyAsync(dc, cfgs, n * sizeof(ws_config), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "H2D configs");
+  Streams st;
+  st.main = c->stream;
+  st.aux[0] = c->aux[0];
+  st.aux[1] = c->aux[1];
+  st.fork = c->fork;
+  st.join[0] = c->join[0];
+  st.join[1] = c->join[1];
+  cudaEvent_t* ev = nullptr;
+  if (c->profiling) {
+    ev = c->take_events(K_SIMGEN, 2);
+  }
+  const int rc = run_simulate(dc, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), c->hg, S, dr, st,
+                              c->n_sm_dev, caps, (int)n_cap, out, &c->last_launches, ev);
+  if (rc == -WS_ELIMIT) return fail(c, WS_ELIMIT, "a request stream of 2^31 or more requests");
+  if (rc == -WS_EINVAL) return fail(c, WS_EINVAL, "all configurations of a ws_simulate call need one line_bytes");
+  if (rc) return cuda_fail(c, (cudaError_t)rc, "simulate");
+  return WS_OK;
+}
+
+ws_status ws_fit_gompertz(ws_ctx* c, const double* O, const double* R, size_t n, double abc[3], double* rss) {
+  if (!c) return WS_EINVAL;
+  if (!O || !R || !abc) return fail(c, WS_EINVAL, "null argument");
+  if (n < 3 || n > (size_t)(1 << 20)) return fail(c, WS_EINVAL, "need 3 .. 2^20 samples");
+  cudaSetDevice(c->device);
+  cudaEvent_t* ev = c->profiling ? c->take_events(K_FIT, 1) : nullptr;
+  double out[4];
+  const int rc = run_fit(O, R, (int)n, out, c->stream, ev);
+  if (rc) return cuda_fail(c, (cudaError_t)rc, "fit");
+  abc[0] = out[0];
+  abc[1] = out[1];
+  abc[2] = out[2];
+  if (rss) *rss = out[3];
+  c->last_launches = 1;
+  return WS_OK;
 }
 
 }  // extern "C"

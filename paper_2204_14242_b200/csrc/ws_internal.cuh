@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "ws.h"
 
@@ -140,7 +141,8 @@ struct Scratch {
 };
 
 // kernel kinds, in launch order (ws_kernel_name)
-enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_SECT, K_MODEL, K_RANK, K_NKINDS };
+enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_SECT, K_MODEL, K_RANK,
+       K_SIMGEN, K_SIMRUN, K_FIT, K_NKINDS };
 constexpr int kEstimateKernels = 10;
 
 // Streams and fork/join events of one context: the three worker chains (warp scope, SM-set
@@ -153,8 +155,53 @@ struct Streams {
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                     const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
                     cudaEvent_t* ev);
+// ---------------------------------------------------------------- NEXT-1: simulated hit rates
+// Request encoding: bits 0..45 sector + 2^45, bit 46 store, bits 48..55 field.
+constexpr int kSimSecBits = 46;
+constexpr long long kSimSecBias = 1ll << 45;
+constexpr int kSimMaxCaps = 64;
+constexpr int kSimAcc = 8 + 4 * (kSimMaxCaps + 1);  // per-config u64 accumulators
+// per-config accumulator layout
+enum { SA_L1REQ = 0, SA_L1COMP, SA_STREQ, SA_STCOMP, SA_OVY, SA_OVZ, SA_L1H = 8 };
+// SA_L1H + b: L1 misses histogram; +65: store; +130: y resident; +195: z resident (b = 0..64)
+constexpr int kSimHist = kSimMaxCaps + 1;
+
+struct DSimTrace {
+  int64_t req_off, n, fen_off, slot_off, hcap, t_y, m_off;
+  int32_t config, type;  // type 0 = SM-set loads, 1 = wave, 2 = layer set L_z
+};
+
+struct SimScratch {
+  int64_t* item_pre;           // per config: exclusive prefix of block items (n + 1)
+  int64_t* trace_pre;          // per config: first trace index (n + 1)
+  int64_t* item_cnt;           // per block item: requests (then exclusive prefix, + total)
+  uint32_t* order;             // n * kMaxInstr: canonical instruction order
+  unsigned long long* req;     // requests
+  DSimTrace* traces;
+  int64_t n_traces;
+  uint32_t* fen;               // Fenwick trees
+  unsigned long long* keys;    // slot keys
+  uint32_t* last;              // slot: last access of the line
+  uint32_t* M;                 // slot x sector: max line distance since the sector's last access
+  uint32_t* SL;                // slot x sector: last access of the sector
+  unsigned long long* wld;     // per config WLD hash sets
+  int64_t* wld_off;            // per config (offset, capacity) pairs
+  unsigned long long* acc;     // n * kSimAcc
+  unsigned long long* lines;   // capacities in lines, ascending (n_cap)
+  unsigned long long* counter; // trace work counter
+};
+
 // ev: nullptr or 2 events (start, end)
 int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches,
                 cudaEvent_t* ev);
+
+// NEXT-1 (ws_kernels.cu): the whole ws_simulate device sequence (estimate, request streams,
+// stack-distance simulation, sample records) on st.main, synchronous; returns 0, a
+// cudaError_t, or -WS_ELIMIT / -WS_EINVAL.  ev: nullptr or 4 events (gen start/end, run start/end).
+int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
+                 const std::vector<DGpu>& hg, const Scratch& s, ws_result* d_est, const Streams& st, int n_sm_dev,
+                 const uint64_t* h_caps, int ncap, ws_sim_result* h_out, uint32_t* launches, cudaEvent_t* ev);
+// ws_fit_gompertz on the device; out = (a, b, c, rss).  ev: nullptr or 2 events.
+int run_fit(const double* h_O, const double* h_R, int n, double* h_out, cudaStream_t q, cudaEvent_t* ev);
 
 }  // namespace wsb

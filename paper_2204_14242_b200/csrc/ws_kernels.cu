@@ -27,8 +27,11 @@
 // sector); the (first, last, count) triple is a monoid under that rule.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstring>
+#include <vector>
 
 #include "ws_internal.cuh"
 
@@ -2302,6 +2305,796 @@ int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st
   if (ev) cudaEventRecord(ev[1], st);
   if (launches) *launches = 1;
   return check_launch();
+}
+
+
+// ================================================================== NEXT-1: simulated hit rates
+// SURVEY 8(f) NEXT-1 (include/ws.h ws_simulate): the configuration's request streams replayed
+// through a sectored, fully associative LRU cache, answered for every capacity at once from
+// exact LRU stack distances (Mattson): a line access at q hits a cache of L lines iff the
+// number of distinct other lines accessed since its previous access, dist(q), is < L; a
+// sector access i is valid iff no access of its line in (previous access of the sector, i]
+// missed, i.e. iff D_i = max of those dist(q) is < L (an eviction re-allocates the line with
+// only the requested sector valid).  One warp per stream, 32 requests per step: dist from a
+// Fenwick tree over "latest access of its line" markers (state before the step) corrected for
+// the step's own earlier lanes; D from per-(line, sector) running maxima.
+// simulated: estimate ok, linear address space, at most 32 sectors per line (valid bits)
+__device__ __forceinline__ int sim_status(const DPlan& P, const DGpu* gs) {
+  if (P.status != WS_OK) return P.status;
+  if (P.mdim) return WS_EINVAL;
+  if (gs[P.gid].lg_line - gs[P.gid].lg_sector > 5) return WS_ELIMIT;
+  return WS_OK;
+}
+__device__ __forceinline__ bool sim_ok(const DPlan& P, const DGpu* gs) { return sim_status(P, gs) == WS_OK; }
+
+__device__ __forceinline__ long long sim_items_of(const DPlan& P, const DGpu* gs) {
+  return sim_ok(P, gs) ? 2 * P.W + (P.s - P.Lz0) : 0;
+}
+__device__ __forceinline__ long long sim_traces_of(const DPlan& P, const DGpu* gs) { return sim_ok(P, gs) ? P.nsets + 2 : 0; }
+
+// canonical instruction order (field, kind, offset C): one CTA per configuration, rank sort
+__global__ void __launch_bounds__(256) k_sim_order(const DPlan* __restrict__ plans, const DGpu* __restrict__ gs,
+                                                   const DInstr* __restrict__ instr, uint32_t* __restrict__ order, int n) {
+  const int c = blockIdx.x;
+  const DPlan& P = plans[c];
+  if (!sim_ok(P, gs)) return;
+  const DInstr* tab = instr + (long long)c * kMaxInstr;
+  const int ni = P.n_instr;
+  for (int i = threadIdx.x; i < ni; i += blockDim.x) {
+    const DInstr e = tab[i];
+    int rank = 0;
+    for (int j = 0; j < ni; ++j) {
+      const DInstr f = tab[j];
+      rank += (f.field < e.field || (f.field == e.field && (f.kind < e.kind || (f.kind == e.kind && f.C < e.C)))) ? 1 : 0;
+    }
+    order[(long long)c * kMaxInstr + rank] = (uint32_t)i;
+  }
+}
+
+// exclusive prefix (single CTA) of per-config block items and streams
+__global__ void __launch_bounds__(1024) k_sim_cscan(const DPlan* __restrict__ plans, const DGpu* __restrict__ gs, int n,
+                                                    int64_t* __restrict__ ipre, int64_t* __restrict__ tpre) {
+  __shared__ long long s_a[1024], s_b[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int seg = (n + nt - 1) / nt;
+  long long a = 0, b = 0;
+  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
+    a += sim_items_of(plans[c], gs);
+    b += sim_traces_of(plans[c], gs);
+  }
+  s_a[tid] = a;
+  s_b[tid] = b;
+  __syncthreads();
+  if (tid == 0) {
+    long long ra = 0, rb = 0;
+    for (int i = 0; i < nt; ++i) {
+      const long long va = s_a[i], vb = s_b[i];
+      s_a[i] = ra;
+      s_b[i] = rb;
+      ra += va;
+      rb += vb;
+    }
+    ipre[n] = ra;
+    tpre[n] = rb;
+  }
+  __syncthreads();
+  a = s_a[tid];
+  b = s_b[tid];
+  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
+    ipre[c] = a;
+    tpre[c] = b;
+    a += sim_items_of(plans[c], gs);
+    b += sim_traces_of(plans[c], gs);
+  }
+}
+
+// exclusive prefix (single CTA) of v[0..m) in place; v[m] = total
+__global__ void __launch_bounds__(1024) k_sim_scan(int64_t* __restrict__ v, long long m) {
+  __shared__ long long s_a[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long seg = (m + nt - 1) / nt;
+  long long a = 0;
+  for (long long i = tid * seg; i < m && i < (tid + 1) * seg; ++i) a += v[i];
+  s_a[tid] = a;
+  __syncthreads();
+  if (tid == 0) {
+    long long r = 0;
+    for (int i = 0; i < nt; ++i) {
+      const long long x = s_a[i];
+      s_a[i] = r;
+      r += x;
+    }
+    v[m] = r;
+  }
+  __syncthreads();
+  a = s_a[tid];
+  for (long long i = tid * seg; i < m && i < (tid + 1) * seg; ++i) {
+    const long long x = v[i];
+    v[i] = a;
+    a += x;
+  }
+}
+
+__device__ __forceinline__ int find_c64(const int64_t* pre, int n, long long item) {
+  int lo = 0, hi = n - 1;  // largest c with pre[c] <= item
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// block item q of a configuration -> (stream tl, block B).  Items: the SM sets' blocks set by
+// set (set j: s + j + m * n_sm), then the wave's blocks, then L_z's blocks.
+__device__ __forceinline__ void sim_item(const DPlan& P, long long nsm, long long q, int& tl, long long& B) {
+  const long long W = P.W;
+  if (q < W) {
+    const long long h = W / nsm, r = W % nsm;
+    long long j, m;
+    if (q < r * (h + 1)) {
+      j = q / (h + 1);
+      m = q % (h + 1);
+    } else {
+      const long long q2 = q - r * (h + 1);
+      j = r + q2 / h;
+      m = q2 % h;
+    }
+    tl = (int)j;
+    B = P.s + j + m * nsm;
+  } else if (q < 2 * W) {
+    tl = (int)P.nsets;
+    B = P.s + (q - W);
+  } else {
+    tl = (int)P.nsets + 1;
+    B = P.Lz0 + (q - 2 * W);
+  }
+}
+// first block item of stream tl
+__device__ __forceinline__ long long sim_first_item(const DPlan& P, long long nsm, int tl) {
+  const long long W = P.W;
+  if (tl < P.nsets) {
+    const long long h = W / nsm, r = W % nsm;
+    return tl < r ? tl * (h + 1) : r * (h + 1) + (tl - r) * h;
+  }
+  return tl == P.nsets ? W : 2 * W;
+}
+
+__device__ __forceinline__ unsigned long long sim_encode(int field, long long sec, int kind) {
+  return ((unsigned long long)field << 48) | ((unsigned long long)kind << kSimSecBits) |
+         ((unsigned long long)(sec + kSimSecBias) & ((1ull << kSimSecBits) - 1ull));
+}
+
+// Requests of one block item (one warp per item): count (GEN = false) or write them.
+template <bool GEN>
+__global__ void __launch_bounds__(256) k_sim_warp(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                                  const DGpu* __restrict__ gs, const DInstr* __restrict__ instr,
+                                                  const uint32_t* __restrict__ order,
+                                                  const int64_t* __restrict__ ipre, int n, long long n_items,
+                                                  int64_t* __restrict__ cnt, unsigned long long* __restrict__ req) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const long long nwg = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long item = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < n_items; item += nwg) {
+    const int c = find_c64(ipre, n, item);
+    const DPlan& P = plans[c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    int tl;
+    long long B;
+    sim_item(P, (long long)G.g.n_sm, item - ipre[c], tl, B);
+    const int kinds = tl < P.nsets ? 1 : 3;
+    const DInstr* tab = instr + (long long)c * kMaxInstr;
+    const uint32_t* ord = order + (long long)c * kMaxInstr;
+    long long total = 0;
+    unsigned long long* out = GEN ? req + cnt[item] : nullptr;
+    for (int w = 0; w < P.nwarps; ++w) {
+      const Lane L = lane_setup(P, B, w, lane);
+      int cur_field = -1;
+      long long plane = 0;
+      for (int ii = 0; ii < P.n_instr; ++ii) {
+        const DInstr e = tab[ord[ii]];
+        if (!((kinds >> e.kind) & 1)) continue;
+        const bool iss = (e.kmask & L.act) != 0ull;
+        const unsigned m = __ballot_sync(FULL, iss);
+        if (m == 0u) continue;
+        if (e.field != cur_field) {
+          cur_field = e.field;
+          const DField& F = K.f[e.field];
+          plane = L.base[0] + F.pitch[1] * L.base[1] + F.pitch[2] * L.base[2];
+        }
+        const long long A = e.C + (plane << e.lg_elem);
+        const long long sec = A >> G.lg_sector;
+        const unsigned pm = m & lt_mask;
+        const long long psec = shfl64(sec, pm ? 31 - __clz(pm) : lane);
+        const bool us = iss && (pm == 0u || psec != sec);
+        const unsigned bm = __ballot_sync(FULL, us);
+        if (GEN && us) out[total + __popc(bm & lt_mask)] = sim_encode(e.field, sec, e.kind);
+        total += __popc(bm);
+      }
+    }
+    if (!GEN && lane == 0) cnt[item] = total;
+  }
+}
+
+// stream table: (config, type, request offset, length, L_y start)
+__global__ void k_sim_traces(const DPlan* __restrict__ plans, const DGpu* __restrict__ gs, int n,
+                             const int64_t* __restrict__ ipre, const int64_t* __restrict__ tpre,
+                             const int64_t* __restrict__ cnt, DSimTrace* __restrict__ tr) {
+  const int c = blockIdx.x;
+  const DPlan& P = plans[c];
+  if (!sim_ok(P, gs)) return;
+  const long long nsm = gs[P.gid].g.n_sm;
+  const int nt = (int)P.nsets + 2;
+  for (int tl = threadIdx.x; tl < nt; tl += blockDim.x) {
+    const long long a = ipre[c] + sim_first_item(P, nsm, tl);
+    const long long b = tl + 1 < nt ? ipre[c] + sim_first_item(P, nsm, tl + 1) : ipre[c] + sim_items_of(P, gs);
+    DSimTrace T;
+    T.req_off = cnt[a];
+    T.n = cnt[b] - cnt[a];
+    T.fen_off = T.slot_off = T.hcap = T.m_off = 0;
+    T.t_y = tl == nt - 1 ? cnt[a + (P.Ly0 - P.Lz0)] - cnt[a] : 0;
+    T.config = c;
+    T.type = tl < P.nsets ? 0 : (tl == P.nsets ? 1 : 2);
+    tr[tpre[c] + tl] = T;
+  }
+}
+
+__device__ __forceinline__ unsigned long long sim_hash(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+constexpr unsigned long long kEmpty = ~0ull;
+
+// the wave's load sectors (WLD) of each configuration into its hash set
+__global__ void k_sim_wld(const DSimTrace* __restrict__ tr, long long n_traces, const unsigned long long* __restrict__ req,
+                          unsigned long long* __restrict__ wld, const int64_t* __restrict__ wld_off) {
+  for (long long t = blockIdx.y; t < n_traces; t += gridDim.y) {
+    const DSimTrace T = tr[t];
+    if (T.type != 1) continue;
+    unsigned long long* H = wld + wld_off[2 * T.config];
+    const unsigned long long hm = (unsigned long long)wld_off[2 * T.config + 1] - 1ull;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (long long)gridDim.x * blockDim.x) {
+      const unsigned long long r = req[T.req_off + i];
+      if ((r >> kSimSecBits) & 1ull) continue;  // stores
+      unsigned long long h = sim_hash(r) & hm;
+      for (;;) {
+        const unsigned long long old = atomicCAS(&H[h], kEmpty, r);
+        if (old == kEmpty || old == r) break;
+        h = (h + 1) & hm;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool wld_has(const unsigned long long* H, unsigned long long hm, unsigned long long k) {
+  unsigned long long h = sim_hash(k) & hm;
+  for (;;) {
+    const unsigned long long v = H[h];
+    if (v == k) return true;
+    if (v == kEmpty) return false;
+    h = (h + 1) & hm;
+  }
+}
+
+// Fenwick tree over positions [0, n) (1-indexed storage, f[1..n])
+__device__ __forceinline__ uint32_t fen_prefix(const uint32_t* f, long long x) {  // sum over [0, x)
+  uint32_t s = 0;
+  for (long long y = x; y > 0; y -= y & -y) s += f[y];
+  return s;
+}
+__device__ __forceinline__ void fen_add(uint32_t* f, long long n, long long pos, uint32_t d) {
+  for (long long x = pos + 1; x <= n; x += x & -x) atomicAdd(&f[x], d);
+}
+__device__ __forceinline__ int cap_bin(const unsigned long long* lines, int ncap, uint32_t D) {
+  int b = 0;  // number of capacities (ascending, in lines) <= D
+  while (b < ncap && lines[b] <= (unsigned long long)D) ++b;
+  return b;
+}
+
+constexpr uint32_t kInf = 0xffffffffu;
+constexpr int kSimWarps = 4;
+
+__global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restrict__ plans,
+                                                             const DGpu* __restrict__ gs, SimScratch S, int ncap) {
+  __shared__ uint32_t s_dist[kSimWarps][32];
+  __shared__ int32_t s_sidx[kSimWarps][32], s_next[kSimWarps][32];
+  __shared__ long long s_p[kSimWarps][32];
+  __shared__ unsigned s_hist[kSimWarps][2][kSimHist];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u, gt = lane == 31 ? 0u : ~((2u << lane) - 1u);
+  for (;;) {
+    long long t = 0;
+    if (lane == 0) t = (long long)atomicAdd(S.counter, 1ull);
+    t = shfl64(t, 0);
+    if (t >= S.n_traces) break;
+    const DSimTrace T = S.traces[t];
+    const DPlan& P = plans[T.config];
+    const DGpu& G = gs[P.gid];
+    const int lspl = G.lg_line - G.lg_sector, spl = 1 << lspl;
+    const long long n = T.n;
+    uint32_t* f = S.fen + T.fen_off;
+    unsigned long long* keys = S.keys + T.slot_off;
+    uint32_t* lastv = S.last + T.slot_off;
+    uint32_t* Mv = S.M + T.m_off;
+    uint32_t* SLv = S.SL + T.m_off;
+    const unsigned long long hm = (unsigned long long)T.hcap - 1ull;
+    for (int b = lane; b < 2 * kSimHist; b += 32) s_hist[wid][b / kSimHist][b % kSimHist] = 0u;
+    unsigned long long comp = 0, counted_n = 0;
+    __syncwarp();
+    for (long long c0 = 0; c0 < n; c0 += 32) {
+      const long long i = c0 + lane;
+      const bool valid = i < n;
+      const unsigned long long r = valid ? S.req[T.req_off + i] : 0ull;
+      const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
+      const int is_st = (int)((r >> kSimSecBits) & 1ull);
+      const unsigned long long lkey = ((r >> 48) << 48) | (sb >> lspl);
+      const int sidx = (int)(sb & (unsigned long long)(spl - 1));
+      const unsigned m = __match_any_sync(FULL, valid ? lkey : ((1ull << 63) | (unsigned long long)lane));
+      const unsigned pl = m & lt, ngm = m & gt;
+      const int prev_lane = pl ? 31 - __clz(pl) : -1;
+      const int next_lane = ngm ? __ffs(ngm) - 1 : 32;
+      const bool leader = valid && prev_lane < 0;
+      long long slot = -1;
+      int existed = 0;
+      long long lastp = -1;
+      if (leader) {
+        unsigned long long h = sim_hash(lkey) & hm;
+        for (;;) {
+          const unsigned long long k = keys[h];
+          if (k == lkey) {
+            existed = 1;
+            break;
+          }
+          if (k == kEmpty) {
+            const unsigned long long old = atomicCAS(&keys[h], kEmpty, lkey);
+            if (old == kEmpty) break;
+            if (old == lkey) {
+              existed = 1;
+              break;
+            }
+          }
+          h = (h + 1) & hm;
+        }
+        slot = (long long)h;
+        if (existed) lastp = (long long)lastv[slot];
+      }
+      const int first = __ffs(m) - 1;
+      slot = shfl64(slot, first);
+      existed = __shfl_sync(FULL, existed, first);
+      // previous access of the line: an earlier lane of this step, or the stored last access
+      const long long p = prev_lane >= 0 ? c0 + prev_lane : lastp;
+      s_p[wid][lane] = (leader && lastp >= 0) ? lastp : -1;
+      s_next[wid][lane] = valid ? next_lane : -1;
+      const uint32_t Fc0 = fen_prefix(f, c0);
+      const uint32_t Fp = (leader && lastp >= 0) ? fen_prefix(f, lastp + 1) : 0u;
+      __syncwarp();
+      uint32_t dist = kInf;
+      if (valid && p >= 0) {
+        long long cnt = 0;
+        if (p >= c0) {  // previous access in this step: lines accessed strictly between
+          for (int j = prev_lane + 1; j < lane; ++j) cnt += s_next[wid][j] >= lane ? 1 : 0;
+        } else {  // markers of the state before the step in (p, c0), minus those moved by earlier lanes
+          cnt = (long long)Fc0 - (long long)Fp;
+          for (int j = 0; j < lane; ++j) {
+            const long long pj = s_p[wid][j];
+            cnt -= (pj > p) ? 1 : 0;
+            cnt += s_next[wid][j] >= lane ? 1 : 0;
+          }
+        }
+        dist = (uint32_t)cnt;
+      }
+      s_dist[wid][lane] = dist;
+      s_sidx[wid][lane] = valid ? sidx : -1;
+      __syncwarp();
+      // D: max line distance since the sector's previous access (its own access included)
+      uint32_t D = 0;
+      if (valid) {
+        uint32_t acc = existed ? Mv[slot * spl + sidx] : kInf;
+        for (int j = 0; j <= lane; ++j) {
+          if (!((m >> j) & 1u)) continue;
+          if (j < lane && s_sidx[wid][j] == sidx) acc = 0u;
+          else acc = max(acc, s_dist[wid][j]);
+        }
+        D = acc;
+        const bool counted = T.type == 0 || (T.type == 1 && is_st);
+        if (counted) {
+          atomicAdd(&s_hist[wid][0][cap_bin(S.lines, ncap, D)], 1u);
+          counted_n += 1;
+          comp += D == kInf ? 1ull : 0ull;
+        }
+      }
+      __syncwarp();
+      // write back the line state (last lane of each line) and move the markers
+      if (valid && next_lane == 32) {
+        for (int sg = 0; sg < spl; ++sg) {
+          uint32_t a2 = existed ? Mv[slot * spl + sg] : kInf;
+          uint32_t l2 = existed ? SLv[slot * spl + sg] : kInf;
+          for (unsigned mm = m; mm; mm &= mm - 1u) {
+            const int j = __ffs(mm) - 1;
+            if (s_sidx[wid][j] == sg) {
+              a2 = 0u;
+              l2 = (uint32_t)(c0 + j);
+            } else {
+              a2 = max(a2, s_dist[wid][j]);
+            }
+          }
+          Mv[slot * spl + sg] = a2;
+          SLv[slot * spl + sg] = l2;
+        }
+        lastv[slot] = (uint32_t)i;
+        fen_add(f, n, i, 1u);
+      }
+      if (leader && lastp >= 0) fen_add(f, n, lastp, 0xffffffffu);
+      __syncwarp();
+    }
+    // end state of L_z: the wave's overlap sectors still valid (y: touched by blocks >= Ly0)
+    unsigned long long ovy = 0, ovz = 0;
+    if (T.type == 2) {
+      const uint32_t total = fen_prefix(f, n);
+      const unsigned long long* H = S.wld + S.wld_off[2 * T.config];
+      const unsigned long long whm = (unsigned long long)S.wld_off[2 * T.config + 1] - 1ull;
+      for (long long sl = lane; sl < T.hcap; sl += 32) {
+        const unsigned long long k = keys[sl];
+        if (k == kEmpty) continue;
+        const uint32_t dend = total - fen_prefix(f, (long long)lastv[sl] + 1);
+        for (int sg = 0; sg < spl; ++sg) {
+          const uint32_t lastsec = SLv[sl * spl + sg];
+          if (lastsec == kInf) continue;
+          const unsigned long long skey = ((k >> 48) << 48) | (((k & ((1ull << 48) - 1ull)) << lspl) | (unsigned)sg);
+          if (!wld_has(H, whm, skey)) continue;
+          const uint32_t De = max(Mv[sl * spl + sg], dend);
+          const bool isy = (long long)lastsec >= T.t_y;
+          atomicAdd(&s_hist[wid][isy ? 0 : 1][cap_bin(S.lines, ncap, De)], 1u);
+          if (isy) ++ovy;
+          else ++ovz;
+        }
+      }
+    }
+    __syncwarp();
+    // per-configuration accumulators
+    unsigned long long* A = S.acc + (long long)T.config * kSimAcc;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      comp += __shfl_down_sync(FULL, comp, o);
+      counted_n += __shfl_down_sync(FULL, counted_n, o);
+      ovy += __shfl_down_sync(FULL, ovy, o);
+      ovz += __shfl_down_sync(FULL, ovz, o);
+    }
+    if (lane == 0) {
+      if (T.type == 0) {
+        atomicAdd(A + SA_L1REQ, counted_n);
+        atomicAdd(A + SA_L1COMP, comp);
+      } else if (T.type == 1) {
+        atomicAdd(A + SA_STREQ, counted_n);
+        atomicAdd(A + SA_STCOMP, comp);
+      } else {
+        atomicAdd(A + SA_OVY, ovy);
+        atomicAdd(A + SA_OVZ, ovz);
+      }
+    }
+    const int h0 = T.type == 0 ? SA_L1H : (T.type == 1 ? SA_L1H + kSimHist : SA_L1H + 2 * kSimHist);
+    for (int b = lane; b <= ncap; b += 32) {
+      if (s_hist[wid][0][b]) atomicAdd(A + h0 + b, (unsigned long long)s_hist[wid][0][b]);
+      if (T.type == 2 && s_hist[wid][1][b]) atomicAdd(A + SA_L1H + 3 * kSimHist + b, (unsigned long long)s_hist[wid][1][b]);
+    }
+    __syncwarp();
+  }
+}
+
+// sample records: one thread per (configuration, capacity)
+__global__ void k_sim_out(const DPlan* __restrict__ plans, const DGpu* __restrict__ gs, const ws_result* __restrict__ est,
+                          int n, const unsigned long long* __restrict__ acc, int ncap, const uint64_t* __restrict__ caps,
+                          const int* __restrict__ cap_rank, ws_sim_result* __restrict__ out) {
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (long long)n * ncap) return;
+  const int c = (int)(id / ncap), k = (int)(id % ncap);
+  ws_sim_result o;
+  memset(&o, 0, sizeof(o));
+  const DPlan& P = plans[c];
+  o.capacity_bytes = caps[k];
+  o.status = sim_status(P, gs);
+  if (o.status == WS_OK && caps[k] < 1) o.status = WS_EINVAL;
+  if (o.status != WS_OK) {
+    out[id] = o;
+    return;
+  }
+  const DGpu& G = gs[P.gid];
+  const ws_result& R = est[c];
+  const unsigned long long* A = acc + (long long)c * kSimAcc;
+  const int kr = cap_rank[k];  // position of this capacity in the ascending order
+  unsigned long long l1m = 0, stm = 0, yr = 0, zr = 0;
+  for (int b = 0; b <= ncap; ++b) {
+    if (b > kr) {
+      l1m += A[SA_L1H + b];
+      stm += A[SA_L1H + kSimHist + b];
+    } else {
+      yr += A[SA_L1H + 2 * kSimHist + b];
+      zr += A[SA_L1H + 3 * kSimHist + b];
+    }
+  }
+  o.l1_requests = A[SA_L1REQ];
+  o.l1_compulsory = A[SA_L1COMP];
+  o.l1_misses = l1m;
+  o.st_requests = A[SA_STREQ];
+  o.st_compulsory = A[SA_STCOMP];
+  o.st_misses = stm;
+  o.ov_y = A[SA_OVY];
+  o.y_resident = yr;
+  o.ov_z_only = A[SA_OVZ];
+  o.z_resident = zr;
+  const double LB = (double)G.g.line_bytes, C = (double)caps[k];
+  o.O_l1 = ((double)R.sm_ld_lines * LB / (double)P.nsets) / C;
+  o.O_y = (double)R.ly_lines * LB / C;
+  o.O_z = (double)R.lz_lines * LB / C;
+  o.O_st = (double)R.wave_lines * LB / C;
+  o.R_l1 = o.l1_requests > R.sm_ld_sectors
+               ? (double)(o.l1_requests - o.l1_misses) / (double)(o.l1_requests - R.sm_ld_sectors) : 1.0;
+  o.R_st = o.st_requests > o.st_compulsory
+               ? (double)(o.st_requests - o.st_misses) / (double)(o.st_requests - o.st_compulsory) : 1.0;
+  o.R_y = o.ov_y > 0 ? (double)o.y_resident / (double)o.ov_y : 1.0;
+  o.R_z = o.ov_z_only > 0 ? (double)o.z_resident / (double)o.ov_z_only : 1.0;
+  out[id] = o;
+}
+
+// Gompertz least squares (ws.h ws_fit_gompertz): grid search by the CTA, LM by thread 0
+// (sequential sums, the oracle's order).  out = (a, b, c, rss).
+__device__ __forceinline__ double gompertz_abc(double a, double b, double c, double O) { return a * exp(-b * exp(-c * O)); }
+
+__device__ double fit_rss_d(const double* O, const double* R, int n, double a, double b, double c) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double e = gompertz_abc(a, b, c, O[i]) - R[i];
+    s += e * e;
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(256) k_fit(const double* __restrict__ O, const double* __restrict__ R, int n,
+                                             double* __restrict__ out) {
+  __shared__ double s_v[256];
+  __shared__ int s_i[256];
+  const int tid = threadIdx.x;
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = 1 << 30;
+  for (int idx = tid; idx < 6 * 23 * 32; idx += blockDim.x) {
+    const int i = idx / (23 * 32), j = (idx / 32) % 23, k = idx % 32;
+    const double v = fit_rss_d(O, R, n, 0.5 + 0.1 * i, exp(-8.0 + 0.5 * j), -8.0 + 0.25 * k);
+    if (v < best) {  // ascending idx per thread: keeps the first minimum
+      best = v;
+      bi = idx;
+    }
+  }
+  s_v[tid] = best;
+  s_i[tid] = bi;
+  __syncthreads();
+  if (tid != 0) return;
+  for (int t = 1; t < (int)blockDim.x; ++t)
+    if (s_v[t] < best || (s_v[t] == best && s_i[t] < bi)) {
+      best = s_v[t];
+      bi = s_i[t];
+    }
+  double th[3] = {0.5 + 0.1 * (bi / (23 * 32)), exp(-8.0 + 0.5 * ((bi / 32) % 23)), -8.0 + 0.25 * (bi % 32)};
+  double lambda = 1e-3;
+  for (int it = 0; it < 200; ++it) {
+    double A[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, gv[3] = {0, 0, 0};
+    for (int m = 0; m < n; ++m) {
+      const double E = exp(-th[2] * O[m]);
+      const double F = exp(-th[1] * E);
+      const double J[3] = {F, -th[0] * E * F, th[0] * F * th[1] * E * O[m]};
+      const double res = th[0] * F - R[m];
+      for (int a = 0; a < 3; ++a) {
+        gv[a] += J[a] * res;
+        for (int b = 0; b < 3; ++b) A[a][b] += J[a] * J[b];
+      }
+    }
+    double Mx[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) Mx[a][b] = A[a][b] + (a == b ? lambda * A[a][a] : 0.0);
+    const double det = Mx[0][0] * (Mx[1][1] * Mx[2][2] - Mx[1][2] * Mx[2][1]) -
+                       Mx[0][1] * (Mx[1][0] * Mx[2][2] - Mx[1][2] * Mx[2][0]) +
+                       Mx[0][2] * (Mx[1][0] * Mx[2][1] - Mx[1][1] * Mx[2][0]);
+    if (!(fabs(det) > 0.0)) break;
+    double d[3];
+    for (int col = 0; col < 3; ++col) {
+      double Mc[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Mc[a][b] = (b == col) ? -gv[a] : Mx[a][b];
+      d[col] = (Mc[0][0] * (Mc[1][1] * Mc[2][2] - Mc[1][2] * Mc[2][1]) -
+                Mc[0][1] * (Mc[1][0] * Mc[2][2] - Mc[1][2] * Mc[2][0]) +
+                Mc[0][2] * (Mc[1][0] * Mc[2][1] - Mc[1][1] * Mc[2][0])) / det;
+    }
+    const double t2[3] = {th[0] + d[0], th[1] + d[1], th[2] + d[2]};
+    const double v = fit_rss_d(O, R, n, t2[0], t2[1], t2[2]);
+    if (v < best) {
+      best = v;
+      th[0] = t2[0];
+      th[1] = t2[1];
+      th[2] = t2[2];
+      lambda = fmax(lambda / 10.0, 1e-15);
+    } else {
+      lambda *= 10.0;
+    }
+  }
+  out[0] = th[0];
+  out[1] = th[1];
+  out[2] = th[2];
+  out[3] = best;
+}
+
+
+// ------------------------------------------------------------------ NEXT-1 host orchestration
+namespace {
+template <class T>
+int dmalloc(T** p, size_t count, std::vector<void*>& owned) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) return (int)e;
+  owned.push_back(*p);
+  return 0;
+}
+long long pow2_at_least(long long v) {
+  long long p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+}  // namespace
+
+int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
+                 const std::vector<DGpu>& hg, const Scratch& s, ws_result* d_est, const Streams& st, int n_sm_dev,
+                 const uint64_t* h_caps, int ncap, ws_sim_result* h_out, uint32_t* launches, cudaEvent_t* ev) {
+  std::vector<void*> owned;
+  auto cleanup = [&](int rc) {
+    cudaStreamSynchronize(st.main);
+    for (void* p : owned) cudaFree(p);
+    return rc;
+  };
+  cudaStream_t q = st.main;
+  uint32_t L = 0;
+  int rc = launch_estimate(d_cfgs, n, d_k, nk, d_g, ng, s, d_est, st, n_sm_dev, &L, nullptr);
+  if (rc) return cleanup(rc);
+  SimScratch S;
+  memset(&S, 0, sizeof(S));
+  uint64_t* d_caps;
+  int* d_rank;
+  if ((rc = dmalloc(&S.item_pre, n + 1, owned)) || (rc = dmalloc(&S.trace_pre, n + 1, owned)) ||
+      (rc = dmalloc(&S.order, (size_t)n * kMaxInstr, owned)) || (rc = dmalloc(&S.acc, (size_t)n * kSimAcc, owned)) ||
+      (rc = dmalloc(&S.lines, kSimMaxCaps, owned)) || (rc = dmalloc(&S.counter, 1, owned)) ||
+      (rc = dmalloc(&d_caps, kSimMaxCaps, owned)) || (rc = dmalloc(&d_rank, kSimMaxCaps, owned)))
+    return cleanup(rc);
+  k_sim_order<<<n, 256, 0, q>>>(s.plans, d_g, s.instr, S.order, n);
+  k_sim_cscan<<<1, 1024, 0, q>>>(s.plans, d_g, n, S.item_pre, S.trace_pre);
+  L += 2;
+  int64_t n_items = 0, n_traces = 0;
+  cudaMemcpyAsync(&n_items, S.item_pre + n, sizeof(int64_t), cudaMemcpyDeviceToHost, q);
+  cudaMemcpyAsync(&n_traces, S.trace_pre + n, sizeof(int64_t), cudaMemcpyDeviceToHost, q);
+  if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);
+  int64_t* d_cnt;
+  DSimTrace* d_tr;
+  if ((rc = dmalloc(&d_cnt, (size_t)n_items + 1, owned)) || (rc = dmalloc(&d_tr, (size_t)n_traces, owned)))
+    return cleanup(rc);
+  S.item_cnt = d_cnt;
+  const int grid = n_sm_dev * 8;
+  if (ev) cudaEventRecord(ev[0], q);
+  if (n_items > 0) {
+    k_sim_warp<false><<<grid, 256, 0, q>>>(s.plans, d_k, d_g, s.instr, S.order, S.item_pre, n, n_items, d_cnt, nullptr);
+    k_sim_scan<<<1, 1024, 0, q>>>(d_cnt, n_items);
+    k_sim_traces<<<n, 128, 0, q>>>(s.plans, d_g, n, S.item_pre, S.trace_pre, d_cnt, d_tr);
+    L += 3;
+  }
+  std::vector<DSimTrace> tr((size_t)n_traces);
+  std::vector<ws_result> est((size_t)n);
+  if (n_traces) cudaMemcpyAsync(tr.data(), d_tr, tr.size() * sizeof(DSimTrace), cudaMemcpyDeviceToHost, q);
+  cudaMemcpyAsync(est.data(), d_est, est.size() * sizeof(ws_result), cudaMemcpyDeviceToHost, q);
+  std::vector<ws_config> cf((size_t)n);
+  cudaMemcpyAsync(cf.data(), d_cfgs, cf.size() * sizeof(ws_config), cudaMemcpyDeviceToHost, q);
+  if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);
+  // ---- host sizing of the per-stream state
+  long long req_total = 0, fen_total = 0, slot_total = 0, m_total = 0;
+  for (DSimTrace& T : tr) {
+    if (T.n >= (1ll << 31) - 1) return cleanup(-WS_ELIMIT);
+    const DGpu& G = hg[cf[T.config].gpu_id];
+    const int spl = 1 << (G.lg_line - G.lg_sector);
+    long long bound = T.n;
+    if (T.type == 1) bound = std::min<long long>(bound, (long long)est[T.config].wave_lines);
+    if (T.type == 2) bound = std::min<long long>(bound, (long long)est[T.config].lz_lines);
+    T.hcap = pow2_at_least(std::max<long long>(2, 2 * bound));
+    T.fen_off = fen_total;
+    fen_total += T.n + 1;
+    T.slot_off = slot_total;
+    slot_total += T.hcap;
+    T.m_off = m_total;
+    m_total += T.hcap * spl;
+    req_total = std::max<long long>(req_total, T.req_off + T.n);
+  }
+  std::vector<int64_t> wld_off(2 * (size_t)n, 0);
+  long long wld_total = 0;
+  for (int c = 0; c < n; ++c) {
+    const long long cap = pow2_at_least(std::max<long long>(2, 2 * (long long)est[c].wave_ld_sectors));
+    wld_off[2 * c] = wld_total;
+    wld_off[2 * c + 1] = cap;
+    wld_total += cap;
+  }
+  std::sort(tr.begin(), tr.end(), [](const DSimTrace& a, const DSimTrace& b) { return a.n > b.n; });
+  // capacities: ascending, in lines (every GPU of the batch shares line_bytes? no: per record below)
+  std::vector<int> idx(ncap);
+  for (int k = 0; k < ncap; ++k) idx[k] = k;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return h_caps[a] < h_caps[b]; });
+  std::vector<int> rank(ncap);
+  std::vector<unsigned long long> lines(ncap);
+  int lb = -1;
+  for (const ws_config& c : cf)
+    if (c.gpu_id < hg.size()) {
+      if (lb >= 0 && lb != hg[c.gpu_id].lg_line) return cleanup(-WS_EINVAL);  // one line size per call
+      lb = hg[c.gpu_id].lg_line;
+    }
+  if (lb < 0) lb = 7;
+  for (int k = 0; k < ncap; ++k) {
+    rank[idx[k]] = k;
+    lines[k] = std::max<unsigned long long>(1ull, h_caps[idx[k]] >> lb);
+  }
+  if ((rc = dmalloc(&S.req, (size_t)req_total, owned)) || (rc = dmalloc(&S.fen, (size_t)fen_total, owned)) ||
+      (rc = dmalloc(&S.keys, (size_t)slot_total, owned)) || (rc = dmalloc(&S.last, (size_t)slot_total, owned)) ||
+      (rc = dmalloc(&S.M, (size_t)m_total, owned)) || (rc = dmalloc(&S.SL, (size_t)m_total, owned)) ||
+      (rc = dmalloc(&S.wld, (size_t)wld_total, owned)) || (rc = dmalloc(&S.wld_off, 2 * (size_t)n, owned)))
+    return cleanup(rc);
+  S.traces = d_tr;
+  S.n_traces = n_traces;
+  ws_sim_result* d_out;
+  if ((rc = dmalloc(&d_out, (size_t)n * ncap, owned))) return cleanup(rc);
+  cudaMemsetAsync(S.fen, 0, (size_t)fen_total * sizeof(uint32_t), q);
+  cudaMemsetAsync(S.keys, 0xff, (size_t)slot_total * sizeof(unsigned long long), q);
+  cudaMemsetAsync(S.wld, 0xff, (size_t)wld_total * sizeof(unsigned long long), q);
+  cudaMemsetAsync(S.acc, 0, (size_t)n * kSimAcc * sizeof(unsigned long long), q);
+  cudaMemsetAsync(S.counter, 0, sizeof(unsigned long long), q);
+  if (n_traces) cudaMemcpyAsync(d_tr, tr.data(), tr.size() * sizeof(DSimTrace), cudaMemcpyHostToDevice, q);
+  cudaMemcpyAsync(S.wld_off, wld_off.data(), wld_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, q);
+  cudaMemcpyAsync(S.lines, lines.data(), ncap * sizeof(unsigned long long), cudaMemcpyHostToDevice, q);
+  cudaMemcpyAsync(d_caps, h_caps, ncap * sizeof(uint64_t), cudaMemcpyHostToDevice, q);
+  cudaMemcpyAsync(d_rank, rank.data(), ncap * sizeof(int), cudaMemcpyHostToDevice, q);
+  if (n_items > 0) {
+    k_sim_warp<true><<<grid, 256, 0, q>>>(s.plans, d_k, d_g, s.instr, S.order, S.item_pre, n, n_items, d_cnt, S.req);
+    k_sim_wld<<<dim3(64, (unsigned)std::min<long long>(n_traces, 4096)), 256, 0, q>>>(d_tr, n_traces, S.req, S.wld,
+                                                                                   S.wld_off);
+    L += 2;
+  }
+  if (ev) {
+    cudaEventRecord(ev[1], q);
+    cudaEventRecord(ev[2], q);
+  }
+  if (n_traces) {
+    k_sim_run<<<n_sm_dev * 4, kSimWarps * 32, 0, q>>>(s.plans, d_g, S, ncap);
+    ++L;
+  }
+  if (ev) cudaEventRecord(ev[3], q);
+  k_sim_out<<<(unsigned)(((long long)n * ncap + 127) / 128), 128, 0, q>>>(s.plans, d_g, d_est, n, S.acc, ncap, d_caps,
+                                                                          d_rank, d_out);
+  ++L;
+  if ((rc = check_launch())) return cleanup(rc);
+  cudaMemcpyAsync(h_out, d_out, (size_t)n * ncap * sizeof(ws_sim_result), cudaMemcpyDeviceToHost, q);
+  if (launches) *launches = L;
+  return cleanup((int)cudaStreamSynchronize(q));
+}
+
+int run_fit(const double* h_O, const double* h_R, int n, double* h_out, cudaStream_t q, cudaEvent_t* ev) {
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, (2 * (size_t)n + 4) * sizeof(double));
+  if (e != cudaSuccess) return (int)e;
+  cudaMemcpyAsync(d, h_O, n * sizeof(double), cudaMemcpyHostToDevice, q);
+  cudaMemcpyAsync(d + n, h_R, n * sizeof(double), cudaMemcpyHostToDevice, q);
+  if (ev) cudaEventRecord(ev[0], q);
+  k_fit<<<1, 256, 0, q>>>(d, d + n, n, d + 2 * n);
+  if (ev) cudaEventRecord(ev[1], q);
+  int rc = check_launch();
+  cudaMemcpyAsync(h_out, d + 2 * n, 4 * sizeof(double), cudaMemcpyDeviceToHost, q);
+  cudaError_t e2 = cudaStreamSynchronize(q);
+  cudaFree(d);
+  return rc ? rc : (int)e2;
 }
 
 }  // namespace wsb

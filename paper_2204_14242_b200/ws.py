@@ -62,14 +62,24 @@ class ws_result(C.Structure):
                 [(n, U64) for n in RESULT_U64_2] + [(n, F64) for n in RESULT_F64_2])
 
 
-assert C.sizeof(ws_config) == 40 and C.sizeof(ws_result) == 336
+SIM_U64 = ["capacity_bytes", "l1_requests", "l1_compulsory", "l1_misses", "st_requests", "st_compulsory",
+           "st_misses", "ov_y", "y_resident", "ov_z_only", "z_resident"]
+SIM_F64 = ["O_l1", "R_l1", "O_y", "R_y", "O_z", "R_z", "O_st", "R_st"]
+
+
+class ws_sim_result(C.Structure):
+    _fields_ = [("status", I32), ("pad", U32)] + [(n, U64) for n in SIM_U64] + [(n, F64) for n in SIM_F64]
+
+
+assert C.sizeof(ws_config) == 40 and C.sizeof(ws_result) == 336 and C.sizeof(ws_sim_result) == 160
 
 CONFIG_DTYPE = np.dtype(ws_config)
 RESULT_DTYPE = np.dtype(ws_result)
 
 EXPORTS = ["ws_create", "ws_destroy", "ws_last_error", "ws_set_stream", "ws_describe_kernel", "ws_describe_gpu",
            "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count",
-           "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read"]
+           "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read", "ws_simulate",
+           "ws_fit_gompertz"]
 
 _lib = None
 
@@ -101,6 +111,8 @@ def load_library(path: str = LIB_PATH):
     L.ws_profile_enable.argtypes = [P, C.c_int]
     L.ws_profile_read.argtypes = [P, C.POINTER(F64), C.POINTER(U64), U32, C.POINTER(U32)]
     L.ws_work_read.argtypes = [P, C.POINTER(U64), U32]
+    L.ws_simulate.argtypes = [P, P, C.c_size_t, P, U32, P]
+    L.ws_fit_gompertz.argtypes = [P, P, P, C.c_size_t, P, P]
     L.ws_kernel_name.argtypes = [U32]
     L.ws_kernel_name.restype = C.c_char_p
     for n in EXPORTS:
@@ -267,3 +279,33 @@ class Context:
             out[nm.decode()] = int(u[i])
             i += 1
         return out
+
+    # ------------------------------------------------------------ NEXT-1: simulated hit rates
+    def simulate(self, cfgs: np.ndarray, capacities) -> list:
+        """Host configs (CONFIG_DTYPE) x capacities (bytes) -> [[dict per capacity] per config]."""
+        cfgs = np.ascontiguousarray(cfgs, dtype=CONFIG_DTYPE)
+        caps = np.ascontiguousarray(np.asarray(capacities, dtype=np.uint64))
+        out = (ws_sim_result * (len(cfgs) * len(caps)))()
+        self._check(self.L.ws_simulate(self.h, cfgs.ctypes.data, len(cfgs), caps.ctypes.data, len(caps),
+                                       C.addressof(out)))
+        rows = []
+        for i in range(len(cfgs)):
+            row = []
+            for k in range(len(caps)):
+                r = out[i * len(caps) + k]
+                d = {"status": int(r.status)}
+                d.update({n: int(getattr(r, n)) for n in SIM_U64})
+                d.update({n: float(getattr(r, n)) for n in SIM_F64})
+                row.append(d)
+            rows.append(row)
+        return rows
+
+    def fit_gompertz(self, O, R):
+        """Least-squares Gompertz fit on the device -> ((a, b, c), rss)."""
+        o = np.ascontiguousarray(np.asarray(O, dtype=np.float64))
+        r = np.ascontiguousarray(np.asarray(R, dtype=np.float64))
+        abc = np.zeros(3, dtype=np.float64)
+        rss = np.zeros(1, dtype=np.float64)
+        self._check(self.L.ws_fit_gompertz(self.h, o.ctypes.data, r.ctypes.data, len(o), abc.ctypes.data,
+                                           rss.ctypes.data))
+        return (float(abc[0]), float(abc[1]), float(abc[2])), float(rss[0])

@@ -34,7 +34,8 @@ def test_struct_layouts():
     assert C.sizeof(ws.ws_field) == 64
     assert C.sizeof(ws.ws_access) == 20
     src = open(os.path.join(ROOT, "include", "ws.h")).read()
-    assert "/* 336 bytes */" in src and "/* 40 bytes */" in src
+    assert "/* 336 bytes */" in src and "/* 40 bytes */" in src and "/* 160 bytes */" in src
+    assert C.sizeof(ws.ws_sim_result) == 160
 
 
 def test_sm100a_cubin_present():

@@ -327,3 +327,92 @@ def test_full_size_variants_sampled(ctx):
     for r in g:
         assert r["ov_y"] == r["ov_z"] and r["wave_pages"] > 0
         assert 0 < r["l2_eff_bytes"] <= gp["l2_bytes"]
+
+
+# ----------------------------------------------------------------- NEXT-1: simulated hit rates
+SIM_KEYS_INT = ["status", "capacity_bytes", "l1_requests", "l1_compulsory", "l1_misses", "st_requests",
+                "st_compulsory", "st_misses", "ov_y", "y_resident", "ov_z_only", "z_resident"]
+SIM_KEYS_FP = ["O_l1", "R_l1", "O_y", "R_y", "O_z", "R_z", "O_st", "R_st"]
+
+
+def sim_parity(ctx, kernel, gpu, configs, caps, label):
+    from paper_2204_14242_b200 import config_array
+    from parity_util import close
+    kid, gid = ctx.describe_kernel(kernel), ctx.describe_gpu(gpu)
+    g = ctx.simulate(config_array(kid, gid, configs), caps)
+    o = O.simulate_batch(kernel, gpu, configs, caps, NT)
+    errs = []
+    for i in range(len(configs)):
+        for k in range(len(caps)):
+            a, b = g[i][k], o[i][k]
+            for key in SIM_KEYS_INT:
+                if a[key] != b[key]:
+                    errs.append(f"{label}[{i},{k}] {configs[i]} cap {caps[k]} {key}: gpu {a[key]} oracle {b[key]}")
+            if b["status"] == 0:
+                for key in SIM_KEYS_FP:
+                    if not close(a[key], b[key]):
+                        errs.append(f"{label}[{i},{k}] {key}: gpu {a[key]!r} oracle {b[key]!r}")
+    assert not errs, "\n".join(errs[:40])
+    return g
+
+
+CAPS = [1 << 40, 1 << 20, 262144, 65536, 16384, 4096, 1024, 128]
+
+
+def test_sim_small_cases(ctx):
+    cases = [
+        (W.stencil_star(24, 12, 12, 4, regs=64), dict(W.gpu_a100(), n_sm=6),
+         [((8, 2, 2), (1, 1, 1), 1), ((16, 4, 1), (1, 1, 2), 0), ((4, 4, 4), (1, 2, 1), 2), ((32, 1, 1), (1, 1, 1), 1, 2)]),
+        (W.stencil_star(20, 10, 12, 1, regs=0), dict(W.gpu_a100(), n_sm=4), [((4, 4, 2), (1, 1, 2), 2)]),
+        (W.lbm15(8), dict(W.gpu_a100(), n_sm=3), [((4, 2, 2), (1, 1, 1), 1), ((8, 1, 1), (1, 1, 1), 0)]),
+    ]
+    for i, (k, gp, cf) in enumerate(cases):
+        sim_parity(ctx, k, gp, cf, CAPS, f"simsmall{i}")
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_sim_random(ctx, seed):
+    k, gp = W.random_kernel(seed, max_dom=12), W.random_gpu(seed)
+    cf = [W.random_config(seed * 10 + j) for j in range(3)]
+    sim_parity(ctx, k, gp, cf, [1 << 30, 8192, 2048, 512, 128], f"simrand{seed}")
+
+
+def test_sim_paper_space_48(ctx):
+    """Every 4th configuration of the 168-config 25pt space on 48^3 (A100 with 24 SMs), eight
+    capacities from 128 B to 1 TiB; then the device fit of the z-layer samples against the oracle's."""
+    k, gp = W.k25(48), dict(W.gpu_a100(), n_sm=24)
+    cf = W.space_stencil_paper()[::4]
+    g = sim_parity(ctx, k, gp, cf, CAPS, "sim48")
+    Os = [r["O_z"] for row in g for r in row if r["status"] == 0 and r["ov_z_only"] > 0]
+    Rs = [r["R_z"] for row in g for r in row if r["status"] == 0 and r["ov_z_only"] > 0]
+    (a, b, c), rss = ctx.fit_gompertz(Os, Rs)
+    (oa, ob, oc), orss = O.fit_gompertz(Os, Rs)
+    assert rss == pytest.approx(orss, rel=1e-6, abs=1e-12)
+    assert (a, b, c) == pytest.approx((oa, ob, oc), rel=1e-4)
+
+
+def test_fit_known_curves(ctx):
+    Os = [0.05 * i for i in range(60)]
+    for abc in ([1.0, 5.0, -2.0], [0.95, 0.02, -3.0], list(W.HIT_ABC_DEFAULT[2])):
+        Rs = [O.hit_rate(abc, o) for o in Os]
+        (a, b, c), rss = ctx.fit_gompertz(Os, Rs)
+        (oa, ob, oc), orss = O.fit_gompertz(Os, Rs)
+        assert (a, b, c) == pytest.approx((oa, ob, oc), rel=1e-6)
+        assert (a, b, c) == pytest.approx(tuple(abc), rel=1e-6)
+
+
+def test_sim_errors(ctx):
+    from paper_2204_14242_b200 import config_array
+    kid, gid = ctx.describe_kernel(W.k7(8)), ctx.describe_gpu(dict(W.gpu_v100(), n_sm=4))
+    r = ctx.simulate(config_array(kid, gid, [((32, 1, 1), (1, 1, 1), 0, 1), ((32, 1, 1), (1, 1, 1), 0)]), [0, 4096])
+    assert r[0][0]["status"] == 1 and r[0][1]["status"] == 1      # multidimensional variant
+    assert r[1][0]["status"] == 1 and r[1][1]["status"] == 0      # capacity 0
+
+
+def test_sim_full_size_sampled(ctx):
+    """25pt 512^3 A100 (BJ configs[1] size): three configurations through the whole simulation at
+    the A100's L1 and effective L2 capacities (and 1/4, 4x), against the oracle."""
+    k, gp = W.k25(512), W.gpu_a100()
+    cf = [((512, 2, 1), (1, 1, 1), 0), ((32, 32, 1), (1, 1, 1), 0), ((256, 4, 1), (1, 1, 1), 0)]
+    caps = [gp["l1_bytes"], gp["l2_bytes"] // 8, gp["l2_bytes"] // 2, 2 * gp["l2_bytes"]]
+    sim_parity(ctx, k, gp, cf, caps, "simfull")
