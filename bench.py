@@ -288,6 +288,9 @@ def run_native(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(kernel, gpu, space, os.cpu_count() or 1)
+    nxt = None
+    if rank == 0 and not args.no_next:
+        nxt = next_rows_measure(ctx, stream, args, world == 1 and not args.no_cpu_baseline)
 
     if rank == 0:
         line = {
@@ -313,10 +316,88 @@ def run_native(args, rank, world, local):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if nxt is not None:
+            line["next_rows"] = nxt
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def next_rows_measure(ctx, stream, args, cpu_baseline):
+    """SURVEY 8(f) rows beyond the headline path, measured on the same context (rank 0):
+    NEXT-3/4 -- the 168-config 512^3 space with every WS_VAR_* bit and the outlook metrics on
+    (B200-like parameters: TLB pages, section link); NEXT-1 -- LRU-simulated hit-rate samples
+    (ws_simulate) of the 168-config space at 40^3 x 8 capacities, device-timed per kernel, with
+    the plain CPU oracle timed on one configuration of it."""
+    import numpy as np
+    import torch
+    from paper_2204_14242_b200 import config_array
+    out = {}
+    # ---- NEXT-3/4: variants + outlook metrics through the same estimate path
+    k, g = W.k25(512), W.with_outlook(W.gpu_b200_like(peaks().get("hbm_gbs", 6546.2)))
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
+    cf = config_array(kid, gid, [c + (7,) for c in W.space_stencil_paper()])
+    n = len(cf)
+    d_cfg = torch.from_numpy(cf.view(np.uint8).copy()).cuda()
+    d_out = torch.empty(n * 336, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+    torch.cuda.synchronize()
+    steps = max(10, min(args.steps, 100))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ctx.profile_enable(True)
+    ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+    torch.cuda.synchronize()
+    ctx.profile_enable(False)
+    sect_ms = ctx.profile_read().get("k_sect", (0.0, 0))[0]
+    out["next3_4_variants"] = {
+        "workload": "3D-25pt r4 512^3, 168 configs, variant bits 7 (multidimensional space + previous-wave reuse "
+                    "+ duplication-based L2 capacity), B200-like parameters with 2 MiB pages and a 10 TB/s "
+                    "section link (k_sect active)",
+        "value": n / (ms / 1e3), "unit": "configs/s", "ms_per_step": ms, "k_sect_ms": sect_ms,
+        "data": "synthetic", "timing": "CUDA events on the context stream, graph replay, no L2 flush"}
+    # ---- NEXT-1: simulated hit-rate samples
+    k, g = W.k25(40), W.gpu_a100()
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
+    space = W.space_stencil_paper()
+    cf = config_array(kid, gid, space)
+    caps = [int(g["l2_bytes"] // 2 * 2 ** (e / 2)) for e in range(-12, 4, 2)]
+    ctx.simulate(cf[:4], caps)                      # warm-up
+    ctx.profile_enable(True)
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rows = ctx.simulate(cf, caps)
+    wall = (time.perf_counter() - t0) / reps
+    ctx.profile_enable(False)
+    prof = ctx.profile_read()
+    dev_ms = (prof.get("k_simgen", (0, 0))[0] + prof.get("k_simrun", (0, 0))[0]) / reps
+    req = sum(r[0]["l1_requests"] + r[0]["st_requests"] for r in rows)
+    sim = {"workload": f"3D-25pt r4 40^3, 168 configs x {len(caps)} capacities (A100 L2/2 x 2^-6..2^1.5), "
+                       "L1 / store / layer-set streams", "value": len(space) * len(caps) / (wall), "unit": "samples/s",
+           "wall_ms_per_call": wall * 1e3, "device_ms_per_call": dev_ms,
+           "kernel_ms_per_call": {k: v[0] / reps for k, v in prof.items() if v[1]},
+           "l1_plus_store_requests": req, "data": "synthetic",
+           "timing": "wall clock around the synchronous ws_simulate (includes sizing + allocation); device ms from "
+                     "CUDA events on the stream"}
+    if cpu_baseline:
+        from oracle import oracle as O
+        one = [space[i] for i in (0, len(space) // 2)]
+        t0 = time.perf_counter()
+        O.simulate_batch(k, g, one, caps, 2)
+        dt = time.perf_counter() - t0
+        sim["cpu_baseline"] = {"value": len(one) * len(caps) / dt, "unit": "samples/s", "cores": 2, "kind": "oracle",
+                               "sample": f"{len(one)} of the 168 configs x {len(caps)} capacities on 2 host threads "
+                                         f"({dt:.1f} s): direct LRU simulation per capacity"}
+    out["next1_simulate"] = sim
+    return out
 
 
 def e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb):
@@ -374,6 +455,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-1/3/4 measurements")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -2061,48 +2061,105 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
     Tri t[kSectNQ];
 #pragma unroll
     for (int q = 0; q < kSectNQ; ++q) t[q] = tri_empty();
+    // per row: each offset group's block row and its wave-block range, computed once (32-bit,
+    // multiply-high divisions), then the unions scan the cached list
+    int c_b0[kMaxAcc], c_b1[kMaxAcc], c_rx[kMaxAcc], c_g[kMaxAcc];
+    const int lo0 = (int)P.lo[0], hi0 = (int)P.hi[0], lo1 = (int)P.lo[1], hi1 = (int)P.hi[1];
+    const int lo2 = (int)P.lo[2], hi2 = (int)P.hi[2], BF0 = (int)P.BF[0];
+    const unsigned nsm32 = (unsigned)nsm, S32 = (unsigned)S;
+    const FDiv fd_nsm = make_fdiv((unsigned long long)nsm);
+    int a_sec[kMaxSections + 1];  // first SM index of each section: ceil(i * n_sm / S)
+#pragma unroll
+    for (int i = 0; i <= kMaxSections; ++i) a_sec[i] = i <= S ? (int)((i * nsm + S - 1) / S) : (int)nsm;
+    const int s32 = (int)s, e32 = (int)(s + Wb), Gx32 = (int)Gx, Gy32 = (int)Gy;
     for (long long ri = tid * per; ri < nrows && ri < (tid + 1) * per; ++ri) {
       const long long z = z0 + ri / ny, y = y0 + ri % ny;
       const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << le);
       my_ops += (unsigned long long)(F.g_end - F.g_begin);
+      int nc = 0;
+      for (int g = F.g_begin; g < F.g_end; ++g) {
+        const DGroup gr = K.g[g];
+        const int yy = (int)y - gr.oy, zz = (int)z - gr.oz;
+        if (yy < lo1 || yy >= hi1 || zz < lo2 || zz >= hi2) continue;
+        const int r = fdiv32(yy - lo1, P.fd_BF[1]) + Gy32 * fdiv32(zz - lo2, P.fd_BF[2]);
+        const int rx = r * Gx32;
+        const int b0 = rx > s32 ? rx : s32, b1 = rx + Gx32 < e32 ? rx + Gx32 : e32;
+        if (b0 >= b1) continue;
+        c_b0[nc] = b0;
+        c_b1[nc] = b1;
+        c_rx[nc] = rx;
+        c_g[nc] = g;
+        ++nc;
+      }
+      if (nc == 0) continue;
       // intervals of (section sel or -1 = any, kind mask km: 1 = loads, 3 = loads + stores)
+      auto pieces = [&](auto&& cb) {  // cb(section, kind, xs, xe)
+        for (int q = 0; q < nc; ++q) {
+          const DGroup gr = K.g[c_g[q]];
+          int b0 = c_b0[q];
+          const int b1 = c_b1[q], rx = c_rx[q];
+          while (b0 < b1) {  // pieces of blocks on the SMs of one section
+            const int x = b0 - s32;
+            const int j = x - (int)nsm32 * fdiv32(x, fd_nsm);
+            int sec = 0;
+#pragma unroll
+            for (int i = 1; i < kMaxSections; ++i) sec += (i < (int)S32 && a_sec[i] <= j) ? 1 : 0;
+            const int jend = a_sec[sec + 1];
+            int e = b0 + (jend - j);
+            if (e > b1) e = b1;
+            const int xs = lo0 + (b0 - rx) * BF0;
+            int xe = lo0 + (e - rx) * BF0;
+            if (xe > hi0) xe = hi0;
+            if (xs < xe) cb((int)sec, gr.kind, xs + F.run_lo[gr.run], xe + F.run_hi[gr.run]);
+            b0 = e;
+          }
+        }
+      };
       auto gen_for = [&](int sel, int km) {
         return [&, sel, km](auto&& cb) {
-          for (int g = F.g_begin; g < F.g_end; ++g) {
-            const DGroup gr = K.g[g];
-            if (!((km >> gr.kind) & 1)) continue;
-            const long long yy = y - gr.oy, zz = z - gr.oz;
-            if (yy < P.lo[1] || yy >= P.hi[1] || zz < P.lo[2] || zz >= P.hi[2]) continue;
-            const long long r = (yy - P.lo[1]) / P.BF[1] + Gy * ((zz - P.lo[2]) / P.BF[2]);
-            long long b0 = r * Gx > s ? r * Gx : s;
-            const long long b1 = (r + 1) * Gx < s + Wb ? (r + 1) * Gx : s + Wb;
-            while (b0 < b1) {
-              // piece of blocks on SMs of one section
-              const long long j = (b0 - s) % nsm;
-              const long long sec = j * S / nsm;
-              const long long jend = sec + 1 < S ? ((sec + 1) * nsm + S - 1) / S : nsm;
-              long long e = b0 + (jend - j);
-              if (e > b1) e = b1;
-              if (sel < 0 || sel == sec) {
-                const long long xs = P.lo[0] + (b0 - r * Gx) * P.BF[0];
-                long long xe = P.lo[0] + (e - r * Gx) * P.BF[0];
-                if (xe > P.hi[0]) xe = P.hi[0];
-                if (xs < xe) cb(xs + F.run_lo[gr.run], xe + F.run_hi[gr.run]);
-              }
-              b0 = e;
-            }
-          }
+          pieces([&](int sec, int kind, int xs, int xe) {
+            if (((km >> kind) & 1) && (sel < 0 || sel == sec)) cb((long long)xs, (long long)xe);
+          });
         };
       };
-      if (P.want_sect) {
-        for (int i = 0; i < S; ++i) {
-          row_union_p(gen_for(i, 1), R0, le, ls, ll, lp, &t[2 * i], nullptr, nullptr);
-          row_union_p(gen_for(i, 3), R0, le, ls, ll, lp, nullptr, &t[2 * i + 1], nullptr);
-        }
-        row_union_p(gen_for(-1, 1), R0, le, ls, ll, lp, &t[2 * kMaxSections], nullptr, nullptr);
+      // one scan: per target (section loads, section all, union loads, union all) the extreme
+      // starts / ends; a target whose max start <= min end is one interval (the common case)
+      constexpr int NT = 2 * kMaxSections + 2;
+      int mns[NT], mxs[NT], mne[NT], mxe[NT];
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        mns[q] = mne[q] = 0x7fffffff;
+        mxs[q] = mxe[q] = -0x7fffffff;
       }
-      row_union_p(gen_for(-1, 3), R0, le, ls, ll, lp, nullptr, &t[2 * kMaxSections + 1],
-                  P.want_pages ? &t[2 * kMaxSections + 2] : nullptr);
+      pieces([&](int sec, int kind, int xs, int xe) {
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          const bool hit = q < 2 * kMaxSections ? ((q >> 1) == sec && ((q & 1) || kind == 0))
+                                                : ((q & 1) || kind == 0);
+          if (hit) {
+            mns[q] = min(mns[q], xs);
+            mxs[q] = max(mxs[q], xs);
+            mne[q] = min(mne[q], xe);
+            mxe[q] = max(mxe[q], xe);
+          }
+        }
+      });
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const bool need = q == NT - 1 || (P.want_sect && (q >= 2 * kMaxSections || (q >> 1) < S));
+        if (!need || mns[q] == 0x7fffffff) continue;
+        Tri* ts = (q & 1) ? nullptr : &t[q];
+        Tri* tl = (q & 1) ? &t[q] : nullptr;
+        Tri* tp = (q == NT - 1 && P.want_pages) ? &t[2 * kMaxSections + 2] : nullptr;
+        if (mxs[q] <= mne[q]) {
+          const long long a0 = R0 + ((long long)mns[q] << le), a1 = R0 + ((long long)(mxe[q] - 1) << le);
+          if (ts) tri_add(*ts, a0 >> ls, a1 >> ls);
+          if (tl) tri_add(*tl, a0 >> ll, a1 >> ll);
+          if (tp) tri_add(*tp, a0 >> lp, a1 >> lp);
+        } else {
+          row_union_p(gen_for(q < 2 * kMaxSections ? (q >> 1) : -1, (q & 1) ? 3 : 1), R0, le, ls, ll, lp, ts, tl, tp);
+        }
+      }
     }
     cta_ordered_reduce<kSectNQ>(t, s_red);
     if (tid == 0 && nrows > 0) {
@@ -2581,16 +2638,20 @@ __device__ __forceinline__ bool wld_has(const unsigned long long* H, unsigned lo
   }
 }
 
-// Fenwick tree over positions [0, n) (1-indexed storage, f[1..n])
+// Fenwick tree over positions [0, n) (1-indexed storage, f[1..n]).  The prefix over [0, x)
+// visits the nodes (x >> b) << b for every set bit b of x: independent loads, issued together.
 __device__ __forceinline__ uint32_t fen_prefix(const uint32_t* f, long long x) {  // sum over [0, x)
   uint32_t s = 0;
-  for (long long y = x; y > 0; y -= y & -y) s += f[y];
+#pragma unroll
+  for (int b = 0; b < 31; ++b)
+    if ((x >> b) & 1) s += __ldcg(&f[(x >> b) << b]);
   return s;
 }
 __device__ __forceinline__ void fen_add(uint32_t* f, long long n, long long pos, uint32_t d) {
   for (long long x = pos + 1; x <= n; x += x & -x) atomicAdd(&f[x], d);
 }
 __device__ __forceinline__ int cap_bin(const unsigned long long* lines, int ncap, uint32_t D) {
+  if (D == 0xffffffffu) return ncap;  // compulsory: a miss at every capacity
   int b = 0;  // number of capacities (ascending, in lines) <= D
   while (b < ncap && lines[b] <= (unsigned long long)D) ++b;
   return b;
@@ -2601,12 +2662,12 @@ constexpr int kSimWarps = 4;
 
 __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restrict__ plans,
                                                              const DGpu* __restrict__ gs, SimScratch S, int ncap) {
-  __shared__ uint32_t s_dist[kSimWarps][32];
-  __shared__ int32_t s_sidx[kSimWarps][32], s_next[kSimWarps][32];
-  __shared__ long long s_p[kSimWarps][32];
   __shared__ unsigned s_hist[kSimWarps][2][kSimHist];
+  __shared__ unsigned long long s_lines[kSimMaxCaps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u, gt = lane == 31 ? 0u : ~((2u << lane) - 1u);
+  for (int k = threadIdx.x; k < ncap; k += blockDim.x) s_lines[k] = S.lines[k];
+  __syncthreads();
   for (;;) {
     long long t = 0;
     if (lane == 0) t = (long long)atomicAdd(S.counter, 1ull);
@@ -2626,10 +2687,12 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
     for (int b = lane; b < 2 * kSimHist; b += 32) s_hist[wid][b / kSimHist][b % kSimHist] = 0u;
     unsigned long long comp = 0, counted_n = 0;
     __syncwarp();
+    unsigned long long r_next = lane < n ? __ldcs(&S.req[T.req_off + lane]) : 0ull;
     for (long long c0 = 0; c0 < n; c0 += 32) {
       const long long i = c0 + lane;
       const bool valid = i < n;
-      const unsigned long long r = valid ? S.req[T.req_off + i] : 0ull;
+      const unsigned long long r = r_next;
+      r_next = (i + 32 < n) ? __ldcs(&S.req[T.req_off + i + 32]) : 0ull;  // prefetch the next step
       const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
       const int is_st = (int)((r >> kSimSecBits) & 1ull);
       const unsigned long long lkey = ((r >> 48) << 48) | (sb >> lspl);
@@ -2637,7 +2700,7 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
       const unsigned m = __match_any_sync(FULL, valid ? lkey : ((1ull << 63) | (unsigned long long)lane));
       const unsigned pl = m & lt, ngm = m & gt;
       const int prev_lane = pl ? 31 - __clz(pl) : -1;
-      const int next_lane = ngm ? __ffs(ngm) - 1 : 32;
+      const int next_lane = valid ? (ngm ? __ffs(ngm) - 1 : 32) : -1;
       const bool leader = valid && prev_lane < 0;
       long long slot = -1;
       int existed = 0;
@@ -2666,70 +2729,80 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
       const int first = __ffs(m) - 1;
       slot = shfl64(slot, first);
       existed = __shfl_sync(FULL, existed, first);
+      uint32_t msnap = (valid && existed) ? Mv[slot * spl + sidx] : kInf;
       // previous access of the line: an earlier lane of this step, or the stored last access
       const long long p = prev_lane >= 0 ? c0 + prev_lane : lastp;
-      s_p[wid][lane] = (leader && lastp >= 0) ? lastp : -1;
-      s_next[wid][lane] = valid ? next_lane : -1;
+      const long long psnap = (leader && lastp >= 0) ? lastp : -1;  // a marker of the state before the step
       const uint32_t Fc0 = fen_prefix(f, c0);
-      const uint32_t Fp = (leader && lastp >= 0) ? fen_prefix(f, lastp + 1) : 0u;
-      __syncwarp();
+      const uint32_t Fp = psnap >= 0 ? fen_prefix(f, psnap + 1) : 0u;
+      // pass 1 (uniform): markers moved / set by the step's earlier lanes
+      int sub = 0, add_all = 0, add_after_prev = 0;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const long long pj = shfl64(psnap, j);
+        const int nj = __shfl_sync(FULL, next_lane, j);
+        if (j < lane) {
+          sub += (pj > p) ? 1 : 0;                 // old marker in (p, c0) moved into the step
+          const int still = nj >= lane ? 1 : 0;    // lane j is the latest access of its line before me
+          add_all += still;
+          add_after_prev += (j > prev_lane) ? still : 0;
+        }
+      }
       uint32_t dist = kInf;
-      if (valid && p >= 0) {
-        long long cnt = 0;
-        if (p >= c0) {  // previous access in this step: lines accessed strictly between
-          for (int j = prev_lane + 1; j < lane; ++j) cnt += s_next[wid][j] >= lane ? 1 : 0;
-        } else {  // markers of the state before the step in (p, c0), minus those moved by earlier lanes
-          cnt = (long long)Fc0 - (long long)Fp;
-          for (int j = 0; j < lane; ++j) {
-            const long long pj = s_p[wid][j];
-            cnt -= (pj > p) ? 1 : 0;
-            cnt += s_next[wid][j] >= lane ? 1 : 0;
+      if (valid && p >= 0)
+        dist = p >= c0 ? (uint32_t)add_after_prev : (uint32_t)((long long)Fc0 - (long long)Fp - sub + add_all);
+      // pass 2 (uniform): D = max line distance since the sector's previous access (own access
+      // included); suffix maxima for the write-back
+      uint32_t acc = msnap, suf = 0u, lmax = 0u;
+      bool later_same = false;
+      unsigned amask = 0u;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t dj = __shfl_sync(FULL, dist, j);
+        const int sj = __shfl_sync(FULL, sidx, j);
+        if ((m >> j) & 1u) {
+          lmax = max(lmax, dj);
+          amask |= 1u << sj;
+          if (j < lane) {
+            if (sj == sidx) acc = 0u;
+            else acc = max(acc, dj);
+          } else if (j == lane) {
+            acc = max(acc, dj);
+          } else {
+            suf = max(suf, dj);
+            later_same |= sj == sidx;
           }
         }
-        dist = (uint32_t)cnt;
       }
-      s_dist[wid][lane] = dist;
-      s_sidx[wid][lane] = valid ? sidx : -1;
-      __syncwarp();
-      // D: max line distance since the sector's previous access (its own access included)
-      uint32_t D = 0;
       if (valid) {
-        uint32_t acc = existed ? Mv[slot * spl + sidx] : kInf;
-        for (int j = 0; j <= lane; ++j) {
-          if (!((m >> j) & 1u)) continue;
-          if (j < lane && s_sidx[wid][j] == sidx) acc = 0u;
-          else acc = max(acc, s_dist[wid][j]);
-        }
-        D = acc;
+        const uint32_t D = acc;
         const bool counted = T.type == 0 || (T.type == 1 && is_st);
         if (counted) {
-          atomicAdd(&s_hist[wid][0][cap_bin(S.lines, ncap, D)], 1u);
+          atomicAdd(&s_hist[wid][0][cap_bin(s_lines, ncap, D)], 1u);
           counted_n += 1;
           comp += D == kInf ? 1ull : 0ull;
         }
-      }
-      __syncwarp();
-      // write back the line state (last lane of each line) and move the markers
-      if (valid && next_lane == 32) {
-        for (int sg = 0; sg < spl; ++sg) {
-          uint32_t a2 = existed ? Mv[slot * spl + sg] : kInf;
-          uint32_t l2 = existed ? SLv[slot * spl + sg] : kInf;
-          for (unsigned mm = m; mm; mm &= mm - 1u) {
-            const int j = __ffs(mm) - 1;
-            if (s_sidx[wid][j] == sg) {
-              a2 = 0u;
-              l2 = (uint32_t)(c0 + j);
+        // the step's last access of each (line, sector): running max restarts at it
+        if (!later_same) {
+          Mv[slot * spl + sidx] = suf;
+          SLv[slot * spl + sidx] = (uint32_t)i;
+        }
+        if (next_lane == 32) {  // last lane of the line: sectors the step did not touch
+          for (int sg = 0; sg < spl; ++sg) {
+            if ((amask >> sg) & 1u) continue;
+            if (existed) {
+              const uint32_t a2 = Mv[slot * spl + sg];
+              Mv[slot * spl + sg] = max(a2, lmax);
             } else {
-              a2 = max(a2, s_dist[wid][j]);
+              Mv[slot * spl + sg] = kInf;
+              SLv[slot * spl + sg] = kInf;
             }
           }
-          Mv[slot * spl + sg] = a2;
-          SLv[slot * spl + sg] = l2;
+          lastv[slot] = (uint32_t)i;
+          fen_add(f, n, i, 1u);
         }
-        lastv[slot] = (uint32_t)i;
-        fen_add(f, n, i, 1u);
       }
-      if (leader && lastp >= 0) fen_add(f, n, lastp, 0xffffffffu);
+      if (psnap >= 0) fen_add(f, n, psnap, 0xffffffffu);
       __syncwarp();
     }
     // end state of L_z: the wave's overlap sectors still valid (y: touched by blocks >= Ly0)
@@ -2749,7 +2822,7 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
           if (!wld_has(H, whm, skey)) continue;
           const uint32_t De = max(Mv[sl * spl + sg], dend);
           const bool isy = (long long)lastsec >= T.t_y;
-          atomicAdd(&s_hist[wid][isy ? 0 : 1][cap_bin(S.lines, ncap, De)], 1u);
+          atomicAdd(&s_hist[wid][isy ? 0 : 1][cap_bin(s_lines, ncap, De)], 1u);
           if (isy) ++ovy;
           else ++ovz;
         }

@@ -252,7 +252,7 @@ def test_architecture_exploration_sampled(ctx):
     effective L2, SM count) at 128^3, every 7th configuration, plus LBM15 with folds."""
     k = W.k25(128)
     cf = W.space_stencil_paper()[::7]
-    for gp in [W.gpu_b200_like(), W.gpu_hypothetical(128, 20, 148), W.gpu_hypothetical(256, 64, 80)]:
+    for gp in [W.with_outlook(W.gpu_b200_like()), W.gpu_hypothetical(128, 20, 148), W.gpu_hypothetical(256, 64, 80)]:
         assert_parity(ctx, k, gp, cf, gp["name"])
     assert_parity(ctx, W.lbm15(48), dict(W.gpu_a100(), n_sm=24), W.space_lbm(folds=True)[::5], "lbm15folds")
 
@@ -260,7 +260,7 @@ def test_architecture_exploration_sampled(ctx):
 def test_full_size_b200_like_sampled(ctx):
     """configs[3] at full size: 25pt 512^3 on the B200-like parameters (148 SMs), whole space in
     one launch, three sampled configurations recomputed by the oracle."""
-    k, gp, cf = W.k25(512), W.gpu_b200_like(), W.space_stencil_paper()
+    k, gp, cf = W.k25(512), W.with_outlook(W.gpu_b200_like()), W.space_stencil_paper()
     g, _ = run_gpu(ctx, k, gp, cf)
     idx = [i for i, c in enumerate(cf) if c[0] in ((512, 2, 1), (128, 8, 1)) and c[1] == (1, 1, 1)]
     idx += [i for i, c in enumerate(cf) if c[0] == (32, 32, 1) and c[1] == (1, 2, 1)]

@@ -75,11 +75,13 @@ def gpu_b200_like(hbm_gbs=6546.2):
     is a nominal 12 TB/s (hypothetical parameter, not measured)."""
     g = _gpu("B200-like", 148, 1.965e9, 256 * KiB, 126 * 1000 * 1000, 2,
              hbm_gbs * 1e9, 12e12)
-    # outlook metrics (NEXT-4, hypothetical parameters): 2 MiB GPU pages; the die-to-die
-    # link between the two L2 halves at a nominal 10 TB/s
-    g["page_bytes"] = 2 * MiB
-    g["link_bw"] = 10e12
     return g
+
+
+def with_outlook(g, page_bytes=2 * MiB, link_bw=10e12):
+    """A parameter set with the NEXT-4 outlook metrics on (hypothetical B200 values): 2 MiB GPU
+    pages for the TLB metric; the die-to-die link between the two L2 halves at a nominal 10 TB/s."""
+    return dict(g, page_bytes=page_bytes, link_bw=link_bw)
 
 
 def gpu_hypothetical(l1_kib, l2_eff_mib, n_sm):
