@@ -231,6 +231,19 @@ ws_status ws_simulate(ws_ctx* ctx, const ws_config* cfgs, size_t n, const uint64
  * arrays; abc receives (a, b, c), *rss the residual sum of squares. */
 ws_status ws_fit_gompertz(ws_ctx* ctx, const double* O, const double* R, size_t n, double abc[3], double* rss);
 
+/* ------------------------------------------------------------------ NEXT-2: on-box validation
+ * The modelled workload itself: the 3D-25pt range-4 FP64 star stencil of
+ * P:751-764 as an sm_100a kernel, dst = w0 src + sum_k w_k (six neighbours at distance k),
+ * k = 1..4, over the domain [4, n+4)^3 of (n+8)^3 fields (x fastest, ghost 4, the K25
+ * description).  block = threads per block (X,Y,Z), fold = (1,1,1), (1,2,1) or (1,1,2)
+ * (thread folding P:754).  Runs `reps` launches on cuda_stream (a cudaStream_t) and writes the
+ * average device milliseconds per launch to *ms_avg (CUDA events, synchronises).  d_src /
+ * d_dst: device arrays of (n[0]+8)(n[1]+8)(n[2]+8) doubles owned by the caller.
+ * Errors: WS_EINVAL (null, fold not one of the three), WS_ELIMIT (block > 1024 threads or
+ * grid > 65535 in y/z), WS_ECUDA. */
+ws_status ws_validate_stencil25(void* cuda_stream, const double* d_src, double* d_dst, const int64_t n[3],
+                                const uint32_t block[3], const uint32_t fold[3], uint32_t reps, double* ms_avg);
+
 /* Number of kernel launches the last ws_estimate[_async] / ws_rank[_async]
  * call enqueued (for the bench's gpu_launches count). */
 uint32_t ws_last_launch_count(const ws_ctx* ctx);

@@ -7,7 +7,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libwsb200.so")
-SRCS = [os.path.join(PKG, "csrc", f) for f in ("ws_api.cu", "ws_kernels.cu")]
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("ws_api.cu", "ws_kernels.cu", "ws_validate.cu")]
 DEPS = SRCS + [os.path.join(PKG, "csrc", "ws_internal.cuh"), os.path.join(ROOT, "include", "ws.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -416,3 +416,45 @@ def test_sim_full_size_sampled(ctx):
     cf = [((512, 2, 1), (1, 1, 1), 0), ((32, 32, 1), (1, 1, 1), 0), ((256, 4, 1), (1, 1, 1), 0)]
     caps = [gp["l1_bytes"], gp["l2_bytes"] // 8, gp["l2_bytes"] // 2, 2 * gp["l2_bytes"]]
     sim_parity(ctx, k, gp, cf, caps, "simfull")
+
+
+# ----------------------------------------------------------------- NEXT-2: validation kernel
+def _st_run(ctx, n, block, fold, seed=0):
+    import torch
+    from oracle import stencil as ST
+    g = torch.Generator().manual_seed(seed)
+    src = torch.rand((n[2] + 8, n[1] + 8, n[0] + 8), dtype=torch.float64, generator=g)
+    d_src = src.cuda()
+    d_dst = torch.zeros_like(d_src)
+    ctx.validate_stencil25(d_src.data_ptr(), d_dst.data_ptr(), n, block, fold, reps=1)
+    torch.cuda.synchronize()
+    return src.numpy(), d_dst.cpu().numpy(), ST
+
+
+@pytest.mark.parametrize("fold", [(1, 1, 1), (1, 2, 1), (1, 1, 2)])
+def test_validation_stencil_small(ctx, fold):
+    """The NEXT-2 kernel against the plain numpy definition on ragged domains (partial blocks and
+    partially active folded threads): FP64 within 1e-13 (FMA contraction only)."""
+    for n, block in [((20, 12, 16), (8, 4, 2)), ((37, 11, 9), (16, 2, 4)), ((9, 9, 9), (32, 1, 1))]:
+        src, dst, ST = _st_run(ctx, n, block, fold)
+        ref = ST.stencil25(src, n)
+        assert np.allclose(dst, ref, rtol=1e-13, atol=1e-13), (n, block, fold)
+
+
+def test_validation_stencil_full_size_sampled(ctx):
+    """512^3 (the bench / validation size), (16,2,32) with 2z folding: 2000 sampled cells."""
+    import torch
+    from oracle import stencil as ST
+    n = (512, 512, 512)
+    d_src = torch.rand((520, 520, 520), dtype=torch.float64, device="cuda")
+    d_dst = torch.zeros_like(d_src)
+    ctx.validate_stencil25(d_src.data_ptr(), d_dst.data_ptr(), n, (16, 2, 32), (1, 1, 2), reps=1)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    pts = rng.integers(4, 516, size=(2000, 3))
+    src = d_src.cpu().numpy()
+    dst = d_dst.cpu().numpy()
+    for z, y, x in pts:
+        sub = src[z - 4:z + 5, y - 4:y + 5, x - 4:x + 5]
+        ref = ST.stencil25(np.pad(sub, 0), (1, 1, 1))[4, 4, 4]
+        assert abs(dst[z, y, x] - ref) <= 1e-13 * max(1.0, abs(ref))

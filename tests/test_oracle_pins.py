@@ -7,6 +7,8 @@ independent brute-force implementation (tests/indep_model.py).
 """
 import json
 import math
+
+import numpy as np
 import os
 
 import pytest
@@ -628,3 +630,28 @@ def test_fit_recovers_known_curve():
     sims = O.simulate_batch(k, g, [cfg], [1 << 20, 131072, 65536, 32768, 16384, 8192, 4096, 2048])[0]
     (a, b, c), rss = O.fit_gompertz([s["O_z"] for s in sims], [s["R_z"] for s in sims])
     assert c < 0 and O.hit_rate([a, b, c], 1.0) > O.hit_rate([a, b, c], 4.0)
+
+
+# --------------------------------------------------------------------- NEXT-2: validation stencil definition
+def test_stencil25_definition_pins():
+    """The plain stencil: a constant field maps to (w0 + 6 sum w_k) * const (the weights sum to
+    the discrete Laplacian's zero row sum up to w0 + 6 sum w_k); a delta at one cell spreads
+    exactly to its 25 star neighbours with the weights; ghost layers stay untouched."""
+    from oracle import stencil as ST
+    n = (12, 10, 9)
+    src = np.full((n[2] + 8, n[1] + 8, n[0] + 8), 2.0)
+    dst = ST.stencil25(src, n)
+    tot = ST.W[0] + 6 * sum(ST.W[1:])
+    assert np.allclose(dst[4:-4, 4:-4, 4:-4], 2.0 * tot, rtol=1e-14)
+    assert not dst[:4].any() and not dst[:, :, -4:].any()
+    src = np.zeros_like(src)
+    src[8, 9, 10] = 1.0                    # cell (x=10, y=9, z=8)
+    dst = ST.stencil25(src, n)
+    assert dst[8, 9, 10] == ST.W[0]
+    for k in range(1, 5):
+        for dz, dy, dx in ((0, 0, k), (0, k, 0), (k, 0, 0)):
+            for sgn in (-1, 1):
+                z, y, x = 8 + sgn * dz, 9 + sgn * dy, 10 + sgn * dx
+                if 4 <= z < n[2] + 4 and 4 <= y < n[1] + 4 and 4 <= x < n[0] + 4:
+                    assert dst[z, y, x] == ST.W[k]
+    assert np.count_nonzero(dst) <= 25
