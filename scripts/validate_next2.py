@@ -94,12 +94,18 @@ def spearman(a, b):
     return num / den if den else float("nan")
 
 
-def analyze(time_json, ncu_csv, prefix):
-    from paper_2204_14242_b200 import Context, config_array, result_dicts
+def b200_params():
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    return W.gpu_b200_like(pk.get("hbm_gbs", 6546.2))
+
+
+def analyze(time_json, ncu_csv, prefix, hit_abc=None, title_note="Hit-rate curves: SURVEY Q17 defaults (not calibrated to B200)."):
+    from paper_2204_14242_b200 import Context, config_array, result_dicts
     k = W.stencil_star(N, N, N, 4, regs=REGS)
-    g = W.gpu_b200_like(pk.get("hbm_gbs", 6546.2))
+    g = b200_params()
+    if hit_abc is not None:
+        g["hit_abc"] = [list(t) for t in hit_abc]
     ctx = Context(0)
     space = W.space_stencil_paper()
     pred = result_dicts(ctx.estimate(config_array(ctx.describe_kernel(k), ctx.describe_gpu(g), space)))
@@ -144,8 +150,7 @@ def analyze(time_json, ncu_csv, prefix):
     with open(prefix + ".md", "w") as f:
         f.write("# NEXT-2 on-box validation: 3D-25pt r4 512^3, 168 configs, B200 (measured) vs estimator (B200 parameters)\n\n")
         f.write("Per-level volumes per lattice update (ncu counters / 512^3) against the estimator's prediction; "
-                "GLup/s from CUDA events (5 launches each).  Hit-rate curves: SURVEY Q17 defaults (not calibrated "
-                "to B200).\n\n")
+                "GLup/s from CUDA events (5 launches each).  " + title_note + "\n\n")
         f.write("| quantity | median abs rel err | p90 abs rel err | Spearman (measured vs predicted) |\n|---|---|---|---|\n")
         for key in keys:
             s = summ[key]
@@ -157,6 +162,7 @@ def analyze(time_json, ncu_csv, prefix):
             f.write(f"| {r['block']} | {r['fold']} | {r['limiter']} | " +
                     " | ".join(f"{r[k][0]:.2f} / {r[k][1]:.2f}" for k in keys) + " |\n")
     print(json.dumps(summ, indent=1))
+    return summ
 
 
 if __name__ == "__main__":
