@@ -35,6 +35,19 @@
 
 #include "ws_internal.cuh"
 
+// minimum resident CTAs per SM of the two heaviest kernels (register budget; A/B-tunable)
+// (A/B on B200, BJ configs[1]: rows/sclass 2/1 -> 3/3 took the step from 0.283 to 0.207 ms,
+// k_fold 4 resident CTAs to 0.206 ms; scripts/ab.sh)
+#ifndef WS_ROWS_MINB
+#define WS_ROWS_MINB 3
+#endif
+#ifndef WS_SCLASS_MINB
+#define WS_SCLASS_MINB 3
+#endif
+#ifndef WS_FOLD_MINB
+#define WS_FOLD_MINB 4
+#endif
+
 namespace wsb {
 
 #define FULL 0xffffffffu
@@ -265,8 +278,8 @@ __device__ __forceinline__ int find_config_warp(const DPrefix* pre, int n, long 
 }
 
 // ------------------------------------------------------------------ a1: plan
+// P must be zeroed by the caller (k_plan zeroes its shared copy cooperatively)
 __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, const DGpu* gs, int ng, DPlan& P) {
-  P = DPlan();
   P.kid = (int)cf.kernel_id;
   P.gid = (int)cf.gpu_id;
   if (cf.kernel_id >= (uint32_t)nk || cf.gpu_id >= (uint32_t)ng) {
@@ -444,42 +457,68 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
   __shared__ DPlan P;
+  __shared__ DKernel sK;   // this configuration's kernel and GPU descriptors, staged once: the
+  __shared__ DGpu sG;      // serial plan work then reads shared memory, not dependent global loads
 
   __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
   __shared__ int s_part[128];
   __shared__ int s_total;
   if (tid < A_N) acc[(long long)c * A_N + tid] = 0ull;
-  if (tid == 0) {
-    ws_config cf = cfgs[c];
-    plan_geometry(cf, ks, nk, gs, ng, P);
+  static_assert(sizeof(DPlan) % 16 == 0 && sizeof(DKernel) % 16 == 0 && sizeof(DGpu) % 16 == 0, "uint4 copies");
+  constexpr int kPlanVec = (int)(sizeof(DPlan) / 16);
+  for (int i = tid; i < kPlanVec; i += blockDim.x) reinterpret_cast<uint4*>(&P)[i] = make_uint4(0u, 0u, 0u, 0u);
+  const ws_config cf = cfgs[c];
+  const bool ids_ok = cf.kernel_id < (uint32_t)nk && cf.gpu_id < (uint32_t)ng;
+  if (ids_ok) {
+    const uint4* srcK = reinterpret_cast<const uint4*>(ks + cf.kernel_id);
+    for (int i = tid; i < (int)(sizeof(DKernel) / 16); i += blockDim.x) reinterpret_cast<uint4*>(&sK)[i] = srcK[i];
+    const uint4* srcG = reinterpret_cast<const uint4*>(gs + cf.gpu_id);
+    for (int i = tid; i < (int)(sizeof(DGpu) / 16); i += blockDim.x) reinterpret_cast<uint4*>(&sG)[i] = srcG[i];
   }
   __syncthreads();
+  if (tid == 0) {
+    if (ids_ok) {
+      ws_config c0 = cf;
+      c0.kernel_id = c0.gpu_id = 0;
+      plan_geometry(c0, &sK, 1, &sG, 1, P);
+      P.kid = (int)cf.kernel_id;
+      P.gid = (int)cf.gpu_id;
+    } else {
+      plan_geometry(cf, ks, nk, gs, ng, P);  // sets WS_EUNKNOWN_ID
+    }
+  }
+  __syncthreads();
+  auto store_plan = [&]() {  // cooperative 16-byte copy of the shared plan
+    uint4* dst = reinterpret_cast<uint4*>(plans + c);
+    for (int i = tid; i < kPlanVec; i += blockDim.x) dst[i] = reinterpret_cast<const uint4*>(&P)[i];
+  };
   if (P.status != WS_OK) {
-    if (tid == 0) plans[c] = P;
+    store_plan();
     return;
   }
   if (tid < 5) plan_range(P, tid);
   __syncthreads();
   if (tid == 0) plan_boundaries(P);
-  const DKernel& K = ks[P.kid];
+  const DKernel& K = sK;
   const int fc = P.fcube;
   const int np = K.n_acc * fc;
   // ---- O3: fold-deduplicated instruction table.  Pair p = (access a, kappa q) gives
-  // instruction (field, kind, kappa + o_a); keep the first occurrence of each key.
+  // instruction (field, kind, kappa + o_a); keep the first occurrence of each key.  An earlier
+  // pair with the same key needs an earlier access a2 of the same field and kind with
+  // r - o_a2 inside the fold cube (for a2 == a only q2 == q gives the key).
+  __shared__ int s_kap[kMaxFoldCube][3];
+  for (int q = tid; q < fc; q += blockDim.x) decode_kappa(q, P.f, s_kap[q][0], s_kap[q][1], s_kap[q][2]);
+  __syncthreads();
   for (int p = tid; p < np; p += blockDim.x) {
-    const int a = p / fc, q = p % fc;
-    int kx, ky, kz;
-    decode_kappa(q, P.f, kx, ky, kz);
+    const int a = p / fc, q = p - a * fc;
     const ws_access A = K.acc[a];
-    const int rx = kx + A.off[0], ry = ky + A.off[1], rz = kz + A.off[2];
+    const int rx = s_kap[q][0] + A.off[0], ry = s_kap[q][1] + A.off[1], rz = s_kap[q][2] + A.off[2];
     unsigned char first = 1;
-    for (int p2 = 0; p2 < p && first; ++p2) {
-      const int a2 = p2 / fc, q2 = p2 % fc;
+    for (int a2 = 0; a2 < a && first; ++a2) {
       const ws_access B = K.acc[a2];
       if (B.field != A.field || B.is_store != A.is_store) continue;
-      int jx, jy, jz;
-      decode_kappa(q2, P.f, jx, jy, jz);
-      if (jx + B.off[0] == rx && jy + B.off[1] == ry && jz + B.off[2] == rz) first = 0;
+      const int dx = rx - B.off[0], dy = ry - B.off[1], dz = rz - B.off[2];
+      if (dx >= 0 && dx < P.f[0] && dy >= 0 && dy < P.f[1] && dz >= 0 && dz < P.f[2]) first = 0;
     }
     s_first[p] = first;
   }
@@ -501,28 +540,23 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   }
   __syncthreads();
   if (s_total > kMaxInstr) {
-    if (tid == 0) {
-      DPlan Q = P;
-      Q.status = WS_ELIMIT;
-      plans[c] = Q;
-    }
+    __syncthreads();
+    if (tid == 0) P.status = WS_ELIMIT;
+    __syncthreads();
+    store_plan();
     return;
   }
   {
     int pos = s_part[tid];
     for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) {
       if (!s_first[p]) continue;
-      const int a = p / fc, q = p % fc;
-      int kx, ky, kz;
-      decode_kappa(q, P.f, kx, ky, kz);
+      const int a = p / fc, q = p - a * fc;
       const ws_access A = K.acc[a];
-      const int r[3] = {kx + A.off[0], ky + A.off[1], kz + A.off[2]};
+      const int r[3] = {s_kap[q][0] + A.off[0], s_kap[q][1] + A.off[1], s_kap[q][2] + A.off[2]};
       // kappas whose folded cell uses this instruction: r - kappa2 is an access offset (Q27)
       unsigned long long km = 0;
       for (int q2 = 0; q2 < fc; ++q2) {
-        int jx, jy, jz;
-        decode_kappa(q2, P.f, jx, jy, jz);
-        const int o0 = r[0] - jx, o1 = r[1] - jy, o2 = r[2] - jz;
+        const int o0 = r[0] - s_kap[q2][0], o1 = r[1] - s_kap[q2][1], o2 = r[2] - s_kap[q2][2];
         for (int a2 = 0; a2 < K.n_acc; ++a2) {
           const ws_access B = K.acc[a2];
           if (B.field == A.field && B.is_store == A.is_store && B.off[0] == o0 && B.off[1] == o1 && B.off[2] == o2) {
@@ -584,18 +618,18 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
       ri.chunk_begin = cb;
       cb += ri.n_chunks;
     }
-    DPlan Q = P;
-    Q.n_instr = s_total;
-    Q.n_warp_items = P.W * P.nwarps;
-    Q.n_wclass_items = 0;
-    Q.n_set_items = P.nsets;
-    Q.n_sclass_items = 0;
-    Q.n_chunks = cb;
-    Q.n_fields = K.n_fields;
-    Q.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
-    Q.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
-    plans[c] = Q;
+    P.n_instr = s_total;
+    P.n_warp_items = P.W * P.nwarps;
+    P.n_wclass_items = 0;
+    P.n_set_items = P.nsets;
+    P.n_sclass_items = 0;
+    P.n_chunks = cb;
+    P.n_fields = K.n_fields;
+    P.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
+    P.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
   }
+  __syncthreads();
+  store_plan();
 }
 
 // ------------------------------------------------------------------ scan of work counts
@@ -1469,7 +1503,7 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
 
 // Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
 // directly evaluated multi-block SM sets.
-__global__ void __launch_bounds__(256) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+__global__ void __launch_bounds__(256, WS_SCLASS_MINB) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
                                                 const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
                                                 const unsigned int* __restrict__ scnt,
                                                 const unsigned long long* __restrict__ srep,
@@ -1722,7 +1756,7 @@ __device__ __forceinline__ int fdiv32(int n, FDiv f) { return (int)((__umulhi((u
 //    take one run each: masks of its first row, the <= 7 unions, the run's triple in closed form
 //    (rows of a run are translates).  An ordered warp reduction of the lanes' 9 triples gives the
 //    plane's contribution.  All of it in 32-bit plane-relative arithmetic.
-__global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restrict__ plans,
+__global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPlan* __restrict__ plans,
                                                             const DPrefix* __restrict__ pre, int n,
                                                             const DKernel* __restrict__ ks,
                                                             const DGpu* __restrict__ gs,
@@ -1925,7 +1959,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_rows(const DPlan* __restr
 // Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
 // plane (count slot = -(representative index) - 2) takes its representative's triple
 // translated by the plane distance (a multiple of the reuse period: whole lines).
-__global__ void __launch_bounds__(256) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+__global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                               const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                               const DRowInfo* __restrict__ rowinfo,
                                               const long long* __restrict__ chunkres,

@@ -34,6 +34,8 @@ def run(name, k, g, cfgs, reps=20):
         if cnt: print(f"   {kname:8s} {ms/cnt:9.4f} ms")
 
 run("configs1 K25 512^3 A100 168", W.k25(512), W.gpu_a100(), W.space_stencil_paper())
+if len(sys.argv) > 1 and sys.argv[1] == "configs1":
+    sys.exit(0)
 run("configs2 LBM15 256^3 A100 49", W.lbm15(256), W.gpu_a100(), W.space_lbm())
 run("configs2 LBM27 256^3 A100 49", W.lbm27(256), W.gpu_a100(), W.space_lbm())
 run("configs0 K7 64^3 V100 16", W.k7(64), W.gpu_v100(), W.space_k7())
