@@ -179,7 +179,7 @@ int64_t make_plan(const wso_kernel& K, const wso_gpu& g, const wso_config& c, Pl
   p.N = p.G[0] * p.G[1] * p.G[2];
   // Resident blocks per SM (Q10): threads, blocks and registers,
   // allocated at warp granularity.
-  if (c.variant < 0 || c.variant > 7) return WSO_EINVAL;
+  if (c.variant < 0 || c.variant > 15) return WSO_EINVAL;
   p.mdim = (c.variant & WSO_VAR_MDIM) != 0;
   if (c.blocks_per_sm > 0) {
     p.k = c.blocks_per_sm;
@@ -292,47 +292,58 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
   std::set<Key> PAGES;
   std::vector<std::set<Key>> SECld(S), SEClin(S);
   const int64_t n_warps = ceildiv(p.T, 32);
-  for (int64_t B = p.s; B < p.s + p.W; ++B) {
-    const int64_t j = (B - p.s) % g.n_sm;  // round-robin SM assignment (Q9)
-    const int64_t sec = j * S / g.n_sm;      // L2 section of that SM
-    for (int64_t t = 0; t < p.T; ++t) {   // active cells = lattice updates of the wave
+  // Variant (NEXT-3): L1 scopes from one representative block (the wave's middle
+  // block) standing for every wave block: no L1 sharing between co-resident blocks, volumes and
+  // cycles = W x the block's, lattice updates = W x the block's.
+  const bool rep = (c.variant & WSO_VAR_REP_BLOCK) != 0;
+  const int64_t B_rep = p.s + p.W / 2;
+  // a3 / a4 contributions of one warp instruction of block B (issuing lanes' addresses A)
+  auto lanes_of = [&](int64_t B, int64_t w, const Instr& I, int64_t h0, int64_t h1) {
+    std::vector<int64_t> A;
+    for (int64_t lane = h0; lane < h1; ++lane) {
+      int64_t t = w * 32 + lane;
+      if (t >= p.T) break;
+      V3 base = base_cell(p, B, t);
+      if (issues(p, base, I)) A.push_back(instr_address(K, base, I));
+    }
+    return A;
+  };
+  auto l1_instr = [&](int64_t B, int64_t w, const Instr& I, const std::vector<int64_t>& A, int64_t j) {
+    // warp instruction: unique sectors over issuing lanes (Q5);
+    // stores are written through and counted per instruction
+    if (I.is_store) req_st += unique_sectors(A, g.sector_bytes);
+    else req_ld += unique_sectors(A, g.sector_bytes);
+    // half-warps: wavefronts (Q6: loads and stores)
+    for (int64_t h = 0; h < 32 / g.half_warp; ++h)
+      wf += halfwarp_wavefronts(lanes_of(B, w, I, h * g.half_warp, (h + 1) * g.half_warp), g);
+    if (!I.is_store)
+      for (int64_t a : A) {
+        SMsec[j].insert(Key(I.field, floordiv(a, g.sector_bytes)));  // L1: SM-resident set (Q8)
+        SMlin[j].insert(Key(I.field, floordiv(a, g.line_bytes)));    // 128 B allocation (Q18)
+      }
+  };
+  auto block_lup = [&](int64_t B) {  // active cells = lattice updates of the block
+    int64_t n = 0;
+    for (int64_t t = 0; t < p.T; ++t) {
       V3 base = base_cell(p, B, t);
       for (int64_t kz = 0; kz < p.f[2]; ++kz)
         for (int64_t ky = 0; ky < p.f[1]; ++ky)
           for (int64_t kx = 0; kx < p.f[0]; ++kx)
-            if (active(p, V3{base[0] + kx, base[1] + ky, base[2] + kz})) ++lup;
+            if (active(p, V3{base[0] + kx, base[1] + ky, base[2] + kz})) ++n;
     }
+    return n;
+  };
+  for (int64_t B = p.s; B < p.s + p.W; ++B) {
+    const int64_t j = (B - p.s) % g.n_sm;  // round-robin SM assignment (Q9)
+    const int64_t sec = j * S / g.n_sm;      // L2 section of that SM
+    if (!rep) lup += block_lup(B);
     for (int64_t w = 0; w < n_warps; ++w) {
       for (const Instr& I : p.instr) {
-        // warp instruction: unique sectors over issuing lanes (Q5);
-        // stores are written through and counted per instruction
-        std::vector<int64_t> A;
-        for (int64_t lane = 0; lane < 32; ++lane) {
-          int64_t t = w * 32 + lane;
-          if (t >= p.T) break;
-          V3 base = base_cell(p, B, t);
-          if (issues(p, base, I)) A.push_back(instr_address(K, base, I));
-        }
-        if (I.is_store) req_st += unique_sectors(A, g.sector_bytes);
-        else req_ld += unique_sectors(A, g.sector_bytes);
-        // half-warps: wavefronts (Q6: loads and stores)
-        for (int64_t h = 0; h < 32 / g.half_warp; ++h) {
-          std::vector<int64_t> H;
-          for (int64_t lane = h * g.half_warp; lane < (h + 1) * g.half_warp; ++lane) {
-            int64_t t = w * 32 + lane;
-            if (t >= p.T) break;
-            V3 base = base_cell(p, B, t);
-            if (issues(p, base, I)) H.push_back(instr_address(K, base, I));
-          }
-          wf += halfwarp_wavefronts(H, g);
-        }
+        std::vector<int64_t> A = lanes_of(B, w, I, 0, 32);
+        if (!rep) l1_instr(B, w, I, A, j);
         for (int64_t a : A) {
           Key ks(I.field, floordiv(a, g.sector_bytes)), kl(I.field, floordiv(a, g.line_bytes));
-          if (!I.is_store) {
-            SMsec[j].insert(ks);  // L1: SM-resident set (Q8)
-            SMlin[j].insert(kl);  // 128 B allocation granularity (Q18: loads only)
-            SECld[sec].insert(ks);
-          }
+          if (!I.is_store) SECld[sec].insert(ks);
           SEClin[sec].insert(kl);
           if (g.page_bytes > 0) PAGES.insert(Key(I.field, floordiv(a, g.page_bytes)));
         }
@@ -350,10 +361,22 @@ int64_t estimate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, wso
       }
     }
   }
+  if (rep) {
+    lup = p.W * block_lup(B_rep);
+    for (int64_t w = 0; w < n_warps; ++w)
+      for (const Instr& I : p.instr) l1_instr(B_rep, w, I, lanes_of(B_rep, w, I, 0, 32), 0);
+    wf *= p.W;
+    req_ld *= p.W;
+    req_st *= p.W;
+  }
   int64_t sm_sec = 0, sm_lin = 0;
   for (int64_t j = 0; j < p.n_sets; ++j) {
     sm_sec += (int64_t)SMsec[j].size();
     sm_lin += (int64_t)SMlin[j].size();
+  }
+  if (rep) {  // W blocks, each with the representative block's footprint (no sharing)
+    sm_sec *= p.W;
+    sm_lin *= p.W;
   }
 
   // ------------------------------------------------------------ O8 layer sets

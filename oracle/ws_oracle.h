@@ -55,7 +55,8 @@ typedef struct {
 enum {
   WSO_VAR_MDIM = 1,       /* multidimensional address space for wave + layer sets */
   WSO_VAR_PREV_WAVE = 2,  /* warm reuse from the directly preceding wave only (SBAC) */
-  WSO_VAR_L2_DUP = 4      /* L2 capacity from the estimated line duplication */
+  WSO_VAR_L2_DUP = 4,     /* L2 capacity from the estimated line duplication */
+  WSO_VAR_REP_BLOCK = 8   /* L1 scopes from one representative block */
 };
 
 typedef struct {

@@ -104,16 +104,23 @@ def set_counts(kernel, gpu, cfg):
     s, W, nsm = geo["s"], geo["W"], gpu["n_sm"]
     wave = list(range(s, s + W))
     wcells = block_cells(geo, wave)
+    rep_mode = bool(geo["variant"] & 8)   # representative block
+    B_rep = s + W // 2
     md = bool(geo["variant"] & 1)
     fp = footprint_md if md else footprint
     WLD = fp(kernel, wcells, (0,), ls)
     WST = fp(kernel, wcells, (1,), ls)
     WLIN = fp(kernel, wcells, (0, 1), ll)
     sm_sec = sm_lin = 0
-    for j in range(min(nsm, W)):
-        cells = block_cells(geo, wave[j::nsm])
-        sm_sec += len(footprint(kernel, cells, (0,), ls))
-        sm_lin += len(footprint(kernel, cells, (0,), ll))
+    if rep_mode:
+        cells = block_cells(geo, [B_rep])
+        sm_sec = W * len(footprint(kernel, cells, (0,), ls))
+        sm_lin = W * len(footprint(kernel, cells, (0,), ll))
+    else:
+        for j in range(min(nsm, W)):
+            cells = block_cells(geo, wave[j::nsm])
+            sm_sec += len(footprint(kernel, cells, (0,), ls))
+            sm_lin += len(footprint(kernel, cells, (0,), ll))
     FY = fp(kernel, block_cells(geo, range(*geo["Ly"])), (0, 1), ls)
     FZ = fp(kernel, block_cells(geo, range(*geo["Lz"])), (0, 1), ls)
     d = ll - ls
@@ -132,7 +139,8 @@ def set_counts(kernel, gpu, cfg):
     link = sum(len(x) for x in sec_ld) - len(set().union(*sec_ld))
     if not (S > 1 and (gpu.get("link_bw", 0.0) > 0 or geo["variant"] & 4)):   # reported on request (ws.h)
         dup = link = 0
-    return dict(lup_wave=len(wcells), sm_ld_sectors=sm_sec, sm_ld_lines=sm_lin,
+    lup = W * len(block_cells(geo, [B_rep])) if rep_mode else len(wcells)
+    return dict(lup_wave=lup, sm_ld_sectors=sm_sec, sm_ld_lines=sm_lin,
                 wave_ld_sectors=len(WLD), wave_st_sectors=len(WST), wave_lines=len(WLIN),
                 ly_lines=len({v[:-1] + (v[-1] >> d,) for v in FY}), lz_lines=len({v[:-1] + (v[-1] >> d,) for v in FZ}),
                 ov_y=len(WLD & FY), ov_z=len(WLD & FZ), k=geo["k"], wave_blocks=W,
@@ -175,7 +183,9 @@ def l1_counts(kernel, gpu, cfg):
                           gpu["half_warp"], gpu["pair_window_bytes"])
     req = [0, 0]
     wf = 0
-    for B in range(geo["s"], geo["s"] + geo["W"]):
+    rep_mode = bool(geo["variant"] & 8)
+    blocks = [geo["s"] + geo["W"] // 2] if rep_mode else range(geo["s"], geo["s"] + geo["W"])
+    for B in blocks:
         for w in range(-(-T // 32)):
             lanes = [t for t in range(32 * w, min(32 * w + 32, T))]
             # instruction key: (field, kind, relative cell) -> lane -> addr
@@ -200,7 +210,8 @@ def l1_counts(kernel, gpu, cfg):
                         for u in c:
                             cnt[u % NB] += 1
                         wf += max(cnt)
-    return dict(l1_wavefronts=wf, l1_req_ld_sectors=req[0], l1_req_st_sectors=req[1])
+    m = geo["W"] if rep_mode else 1
+    return dict(l1_wavefronts=m * wf, l1_req_ld_sectors=m * req[0], l1_req_st_sectors=m * req[1])
 
 
 class SectoredLRU:

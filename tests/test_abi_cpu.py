@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _header_functions():
     src = open(os.path.join(ROOT, "include", "ws.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ws_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ws_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_builds_and_exports_header_symbols():

@@ -369,8 +369,10 @@ def test_invariants_random(seed):
     if r["status"] != 0:
         return
     assert r["sm_ld_lines"] <= r["sm_ld_sectors"] <= 4 * r["sm_ld_lines"]
-    assert r["wave_ld_sectors"] <= r["sm_ld_sectors"] <= r["l1_req_ld_sectors"]
-    assert r["wave_st_sectors"] <= r["l1_req_st_sectors"]
+    assert r["sm_ld_sectors"] <= r["l1_req_ld_sectors"]
+    if not (len(c) > 3 and c[3] & 8):   # the representative block need not bound the wave
+        assert r["wave_ld_sectors"] <= r["sm_ld_sectors"]
+        assert r["wave_st_sectors"] <= r["l1_req_st_sectors"]
     assert r["ov_y"] <= r["ov_z"] <= r["wave_ld_sectors"]
     assert r["ly_lines"] <= r["lz_lines"]
     # shifting every field by 128 B changes nothing (sectors/lines/banks are 128 B periodic)
@@ -388,7 +390,7 @@ def test_invariants_random(seed):
 
 
 # --------------------------------------------------------------------- NEXT-3 / NEXT-4 variants
-VAR_MDIM, VAR_PREV_WAVE, VAR_L2_DUP = 1, 2, 4
+VAR_MDIM, VAR_PREV_WAVE, VAR_L2_DUP, VAR_REP_BLOCK = 1, 2, 4, 8
 
 
 def _plain_kernel(ext, accesses, align=0, elem=8, dom_lo=(0, 0, 0), dom_hi=None):
@@ -510,7 +512,7 @@ def test_l2_sections_duplication_and_link_hand_count():
     assert rs["limiter"] == 3 and rs["t_pred"] == pytest.approx(rs["t_link"] * 256 * 30, rel=1e-12)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 4, 7])
+@pytest.mark.parametrize("variant", [1, 2, 4, 7, 8, 15])
 @pytest.mark.parametrize("case", range(len(SMALL_CASES)))
 def test_oracle_vs_independent_variants(case, variant):
     k, g, c = SMALL_CASES[case]
@@ -520,6 +522,36 @@ def test_oracle_vs_independent_variants(case, variant):
     m = M.set_counts(k, g, c)
     for key, v in m.items():
         assert r[key] == v, key
+    if variant & VAR_REP_BLOCK:
+        for key, v in M.l1_counts(k, g, c).items():
+            assert r[key] == v, key
+
+
+@pytest.mark.parametrize("k_res", [1, 2])
+def test_rep_block_equals_exact_on_translation_invariant_grid(k_res):
+    """one representative block stands for the wave.  On a grid whose blocks are all
+    unclipped translates by whole lines (rows of 128 doubles = 8 lines, 16-wide blocks, aligned
+    base), every block has the same warp statistics and footprint, so with one block per SM set
+    the representative-block variant reproduces the exact per-SM-set counts; with two blocks per
+    set it can only over-count (co-resident blocks share nothing under the variant)."""
+    n = 128
+    ext = (n + 2, 34, 34)
+    fld = {"extent": ext, "pitch": (1, 128 * 2, 128 * 2 * 34), "align": 8 * 127, "elem": 8}
+    k = {"fields": [dict(fld), dict(fld)], "accesses": [(0, 0, (0, 0, 0)), (0, 0, (1, 0, 0)), (0, 0, (-1, 0, 0)),
+                                                        (0, 0, (0, 1, 0)), (0, 0, (0, -1, 0)), (0, 0, (0, 0, 1)),
+                                                        (0, 0, (0, 0, -1)), (1, 1, (0, 0, 0))],
+         "dom_lo": (1, 1, 1), "dom_hi": (n + 1, 33, 33), "regs": 0, "flops": 7.0}
+    g = dict(W.gpu_a100(), n_sm=4)
+    c = ((16, 4, 2), (1, 1, 1), k_res)
+    exact, rep = O.estimate(k, g, c), O.estimate(k, g, c + (VAR_REP_BLOCK,))
+    for key in ("lup_wave", "l1_wavefronts", "l1_req_ld_sectors", "l1_req_st_sectors"):
+        assert rep[key] == exact[key], key
+    if k_res == 1:
+        assert rep["sm_ld_sectors"] == exact["sm_ld_sectors"] and rep["sm_ld_lines"] == exact["sm_ld_lines"]
+    else:
+        assert rep["sm_ld_sectors"] >= exact["sm_ld_sectors"] and rep["sm_ld_lines"] >= exact["sm_ld_lines"]
+    for key in ("wave_ld_sectors", "wave_lines", "lz_lines", "ov_z"):   # wave scopes untouched
+        assert rep[key] == exact[key], key
 
 
 # --------------------------------------------------------------------- NEXT-1: simulated hit rates

@@ -283,5 +283,5 @@ def random_config(seed):
             break
     f = (rng.choice([1, 1, 2]), rng.choice([1, 1, 2, 3]), rng.choice([1, 1, 2]))
     k = rng.choice([0, 0, 0, 1, 2])
-    variant = rng.choice([0, 0, 1, 2, 3, 4, 5, 6, 7])   # WS_VAR_* bits (NEXT-3 / NEXT-4)
+    variant = rng.choice([0, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 15])   # WS_VAR_* bits (NEXT-3 / NEXT-4)
     return (b, f, k, variant)
