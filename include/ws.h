@@ -133,7 +133,12 @@ enum {
   /* Effective L2 capacity from the estimated line duplication between L2 sections
    * instead of l2_bytes / l2_sections: l2_bytes * U / (U + l2_dup_lines),
    * U = distinct wave lines. */
-  WS_VAR_L2_DUP = 4
+  WS_VAR_L2_DUP = 4,
+  /* L1 scopes (warp instructions, SM sets) from one representative block, the wave's middle
+   * block s + W/2, standing for all W wave blocks (per-block footprint, no
+   * L1 sharing between co-resident blocks): l1_wavefronts, l1_req_*_sectors, sm_ld_*,
+   * lup_wave = W x the block's.  Wave / layer-set scopes are unchanged. */
+  WS_VAR_REP_BLOCK = 8
 };
 
 typedef struct {

@@ -565,13 +565,16 @@ int64_t simulate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, con
   make_plan(K, g, c, p, tmp);
   const int64_t spl = g.line_bytes / g.sector_bytes;
   // ---- L1: each SM set's load requests through a fresh cache (Q8/Q9)
-  int64_t l1_req = 0;
+  int64_t l1_req = 0, l1_comp = 0;
   std::vector<int64_t> l1_miss(ncap, 0);
   for (int64_t j = 0; j < p.n_sets; ++j) {
     std::vector<int64_t> blocks;
     for (int64_t B = p.s + j; B < p.s + p.W; B += g.n_sm) blocks.push_back(B);
     std::vector<SimReq> tr = block_trace(K, g, p, blocks, 1);
     l1_req += (int64_t)tr.size();
+    std::set<Key> distinct;
+    for (const SimReq& q : tr) distinct.insert(q.sector);
+    l1_comp += (int64_t)distinct.size();  // compulsory misses of the stream
     for (int64_t k = 0; k < ncap; ++k) {
       SimCache cache(caps[k] / g.line_bytes, spl);
       for (const SimReq& q : tr) l1_miss[k] += cache.access(q.sector) ? 0 : 1;
@@ -629,7 +632,7 @@ int64_t simulate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, con
     wso_sim_result& o = out[k];
     const double C = (double)caps[k];
     o.l1_requests = l1_req;
-    o.l1_compulsory = r.sm_ld_sectors;
+    o.l1_compulsory = l1_comp;  // = sm_ld_sectors of the estimate unless WSO_VAR_REP_BLOCK
     o.l1_misses = l1_miss[k];
     o.st_requests = st_req;
     o.st_compulsory = st_comp;
@@ -642,7 +645,7 @@ int64_t simulate(const wso_kernel& K, const wso_gpu& g, const wso_config& c, con
     o.O_y = (double)r.ly_lines * LB / C;
     o.O_z = (double)r.lz_lines * LB / C;
     o.O_st = (double)r.wave_lines * LB / C;
-    o.R_l1 = l1_req > r.sm_ld_sectors ? (double)(l1_req - o.l1_misses) / (double)(l1_req - r.sm_ld_sectors) : 1.0;
+    o.R_l1 = l1_req > l1_comp ? (double)(l1_req - o.l1_misses) / (double)(l1_req - l1_comp) : 1.0;
     o.R_st = st_req > st_comp ? (double)(st_req - o.st_misses) / (double)(st_req - st_comp) : 1.0;
     o.R_y = o.ov_y > 0 ? (double)o.y_resident / (double)o.ov_y : 1.0;
     o.R_z = o.ov_z_only > 0 ? (double)o.z_resident / (double)o.ov_z_only : 1.0;

@@ -103,6 +103,7 @@ struct DPlan {
   int32_t variant, mdim;         // mdim: wave / layer-set footprints in the multidimensional space
   int32_t want_pages, want_sect; // k_sect: TLB pages / L2-section footprints wanted
   int64_t n_sect_items;          // k_sect work items (fields) of this config
+  int64_t rep_B, rep_mult;       // WS_VAR_REP_BLOCK: the representative block and W (0 = off)
 };
 
 // per-config accumulator slots (u64, atomically added by the worker kernels)

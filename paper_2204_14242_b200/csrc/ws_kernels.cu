@@ -299,7 +299,7 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
       P.status = WS_EINVAL;
       return;
     }
-  if (cf.variant & ~7u) {  // unknown WS_VAR_* bits
+  if (cf.variant & ~15u) {  // unknown WS_VAR_* bits
     P.status = WS_EINVAL;
     return;
   }
@@ -367,6 +367,11 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   if (cf.variant & WS_VAR_PREV_WAVE) P.Ly0 = P.Lz0 = s - P.W > 0 ? s - P.W : 0;
   // NEXT-4 outlook metrics: TLB pages (page size given) and L2-section footprints (several
   // sections and either the link limiter or the duplication-based capacity wanted)
+  // WS_VAR_REP_BLOCK: the wave's middle block stands for all W blocks in the L1 scopes
+  if (cf.variant & WS_VAR_REP_BLOCK) {
+    P.rep_B = s + P.W / 2;
+    P.rep_mult = P.W;
+  }
   P.want_pages = G.lg_page >= 0;
   P.want_sect = G.g.l2_sections > 1 && (G.g.link_bw > 0 || (cf.variant & WS_VAR_L2_DUP));
   for (int d = 0; d < 3; ++d) {
@@ -385,7 +390,7 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
   const long long M = (long long)G.g.sector_bytes > (long long)G.g.bank_bytes ? (long long)G.g.sector_bytes
                                                                               : (long long)G.g.bank_bytes;
   const long long Rw = M >> K.f[0].lg_elem, Rs = (long long)G.g.line_bytes >> K.f[0].lg_elem;
-  P.wcls_R = (same && Rw >= 1 && Rw <= 64 && P.nwarps <= 32) ? (int)Rw : 0;
+  P.wcls_R = (same && Rw >= 1 && Rw <= 64 && P.nwarps <= 32 && !P.rep_mult) ? (int)Rw : 0;
   P.scls_R = (same && Rs >= 1 && Rs <= 64) ? (int)Rs : 0;
   for (int d = 0; d < 3; ++d) P.cls_pitch[d] = K.f[0].pitch[d];
   P.cls_lg_elem = K.f[0].lg_elem;
@@ -619,9 +624,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
       cb += ri.n_chunks;
     }
     P.n_instr = s_total;
-    P.n_warp_items = P.W * P.nwarps;
+    P.n_warp_items = (P.rep_mult ? 1 : P.W) * P.nwarps;
     P.n_wclass_items = 0;
-    P.n_set_items = P.nsets;
+    P.n_set_items = P.rep_mult ? 1 : P.nsets;
     P.n_sclass_items = 0;
     P.n_chunks = cb;
     P.n_fields = K.n_fields;
@@ -922,11 +927,11 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
       const int cc = __shfl_sync(FULL, c, src);
       const DPlan& P = plans[cc];
       const long long wi = it - pre[cc].warp;
-      const Lane L = lane_setup(P, P.s + wi / P.nwarps, (int)(wi % P.nwarps), lane);
+      const Lane L = lane_setup(P, P.rep_mult ? P.rep_B : P.s + wi / P.nwarps, (int)(wi % P.nwarps), lane);
       long long lup, wf, rl, rs;
       eval_warp(P, ks[P.kid], gs[P.gid], instr + (long long)cc * kMaxInstr, L, lane, lup, wf, rl, rs);
       if (lane == 0) {
-        add_warp_stats(acc + (long long)cc * A_N, 1, lup, wf, rl, rs);
+        add_warp_stats(acc + (long long)cc * A_N, P.rep_mult ? P.rep_mult : 1, lup, wf, rl, rs);
         my_units += 32ull * (unsigned long long)P.n_instr;
       }
     }
@@ -1484,7 +1489,7 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
     const long long nsm = gs[P.gid].g.n_sm;
     const long long S0 = P.s + j;
     const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-    if (P.scls_R > 0 && kj == 1) {
+    if (P.scls_R > 0 && kj == 1 && !P.rep_mult) {
       const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
       long long pl = 0;
 #pragma unroll
@@ -1537,6 +1542,10 @@ __global__ void __launch_bounds__(256, WS_SCLASS_MINB) k_sclass(const DPlan* __r
       mult = scnt[gslot];
       S0 = (long long)srep[gslot];
       kj = 1;
+    } else if (P.rep_mult) {  // WS_VAR_REP_BLOCK: one block, counted for every wave block
+      S0 = P.rep_B;
+      kj = 1;
+      mult = (unsigned long long)P.rep_mult;
     } else {
       S0 = P.s + low;
       kj = (P.W - (long long)low + nsm - 1) / nsm;
@@ -2939,8 +2948,8 @@ __global__ void k_sim_out(const DPlan* __restrict__ plans, const DGpu* __restric
   o.O_y = (double)R.ly_lines * LB / C;
   o.O_z = (double)R.lz_lines * LB / C;
   o.O_st = (double)R.wave_lines * LB / C;
-  o.R_l1 = o.l1_requests > R.sm_ld_sectors
-               ? (double)(o.l1_requests - o.l1_misses) / (double)(o.l1_requests - R.sm_ld_sectors) : 1.0;
+  o.R_l1 = o.l1_requests > o.l1_compulsory
+               ? (double)(o.l1_requests - o.l1_misses) / (double)(o.l1_requests - o.l1_compulsory) : 1.0;
   o.R_st = o.st_requests > o.st_compulsory
                ? (double)(o.st_requests - o.st_misses) / (double)(o.st_requests - o.st_compulsory) : 1.0;
   o.R_y = o.ov_y > 0 ? (double)o.y_resident / (double)o.ov_y : 1.0;

@@ -52,7 +52,7 @@ RESULT_F64 = ["O_l1", "R_l1", "O_y", "R_y", "O_z", "R_z", "O_st", "R_st", "l1_cy
               "l2_st_Bpl", "dram_ld_Bpl", "dram_st_Bpl", "t_l1", "t_l2", "t_dram", "t_pred"]
 RESULT_U64_2 = ["wave_pages", "l2_dup_lines", "l2_link_sectors"]   # NEXT-4 outlook metrics
 RESULT_F64_2 = ["l2_eff_bytes", "t_link"]
-WS_VAR_MDIM, WS_VAR_PREV_WAVE, WS_VAR_L2_DUP = 1, 2, 4
+WS_VAR_MDIM, WS_VAR_PREV_WAVE, WS_VAR_L2_DUP, WS_VAR_REP_BLOCK = 1, 2, 4, 8
 
 
 class ws_result(C.Structure):

@@ -277,7 +277,7 @@ def test_variants_paper_space_64(ctx):
     (multidimensional address space, previous-wave reuse, duplication-based L2 capacity), TLB
     pages and the L2 section link limiter on."""
     gp = dict(W.gpu_a100(), page_bytes=64 * 1024, link_bw=2e12)
-    cf = [c + (1 + i % 7,) for i, c in enumerate(W.space_stencil_paper()[::2])]
+    cf = [c + (1 + i % 15,) for i, c in enumerate(W.space_stencil_paper()[::2])]
     g, _ = assert_parity(ctx, W.k25(64), gp, cf, "var64")
     assert any(r["l2_link_sectors"] > 0 for r in g) and all(r["wave_pages"] > 0 for r in g)
 
@@ -286,7 +286,7 @@ def test_variants_lbm_and_sections(ctx):
     """LBM15 (32 arrays) with 3 and 4 L2 sections, 4 KiB pages, every variant."""
     for S in (3, 4):
         gp = dict(W.gpu_a100(), n_sm=12, l2_sections=S, page_bytes=4096, link_bw=5e11)
-        cf = [c + (v,) for c in W.space_lbm()[::6] for v in (0, 5, 6)]
+        cf = [c + (v,) for c in W.space_lbm()[::6] for v in (0, 5, 6, 8, 14)]
         assert_parity(ctx, W.lbm15(20), gp, cf, f"lbmS{S}")
 
 
@@ -302,7 +302,7 @@ def test_mdim_paper_example_gpu(ctx):
 def test_variant_errors(ctx):
     from paper_2204_14242_b200 import WSError, config_array, result_dicts
     kid, gid = ctx.describe_kernel(W.k7(8)), ctx.describe_gpu(W.gpu_v100())
-    r = result_dicts(ctx.estimate(config_array(kid, gid, [((32, 1, 1), (1, 1, 1), 0, 8)])))
+    r = result_dicts(ctx.estimate(config_array(kid, gid, [((32, 1, 1), (1, 1, 1), 0, 16)])))
     assert r[0]["status"] == 1
     for bad, st in [(dict(W.gpu_a100(), l2_sections=5), 2), (dict(W.gpu_a100(), page_bytes=100), 1),
                     (dict(W.gpu_a100(), page_bytes=64), 1), (dict(W.gpu_a100(), link_bw=-1.0), 1)]:
@@ -314,7 +314,7 @@ def test_variant_errors(ctx):
 def test_full_size_variants_sampled(ctx):
     """configs[1] at 512^3 with variant bits 7 and the link limiter: whole space in one launch,
     three configurations recomputed by the oracle."""
-    k, cf = W.k25(512), [c + (7,) for c in W.space_stencil_paper()]
+    k, cf = W.k25(512), [c + (15,) for c in W.space_stencil_paper()]
     gp = dict(W.gpu_a100(), page_bytes=2 * 1024 * 1024, link_bw=2e12)
     g, _ = run_gpu(ctx, k, gp, cf)
     idx = [i for i, c in enumerate(cf) if c[0] in ((512, 2, 1), (32, 32, 1)) and c[1] == (1, 1, 1)]
