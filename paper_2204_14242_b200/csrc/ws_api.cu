@@ -265,6 +265,10 @@ ws_status ws_profile_read(ws_ctx* c, double* ms, uint64_t* launches, uint32_t ca
       float t = 0.f;
       cudaError_t e = cudaEventSynchronize(r.ev[2 * i + 1]);
       if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.ev[2 * i], r.ev[2 * i + 1]);
+      if (e == cudaErrorInvalidResourceHandle) {  // kind not launched by this call (events never recorded)
+        cudaGetLastError();
+        continue;
+      }
       if (e != cudaSuccess) st = cuda_fail(c, e, "profile read");
       acc[r.first_kind + i] += t;
       cnt[r.first_kind + i] += 1;
