@@ -284,6 +284,19 @@ def run_native(args, rank, world, local):
     except Exception:
         pass
     share = {k: round(v[0] / sum(x[0] for x in kern.values()), 4) for k, v in kern.items()}
+    # executed instruction mix (with row spans the roofline is recomputed for the
+    # executed mix): the committed ncu capture's warp instructions per launch of the dominant
+    # kernel over its live launch time, against the issue peak (148 SMs x 4 SMSPs x 1/clk)
+    warp_inst = None
+    try:
+        warp_inst = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom + ":warp_inst")
+    except Exception:
+        pass
+    issue_peak = 148 * 4 * sm_max * 1e6
+    executed = ({"warp_inst_per_launch": warp_inst, "issue_rate_per_s": warp_inst / (dom_ms / 1e3),
+                 "issue_peak_per_s": issue_peak, "issue_frac": warp_inst / (dom_ms / 1e3) / issue_peak,
+                 "source": "profiles/ncu_traffic.json (ncu --set full, smsp__inst_executed.sum)"}
+                if warp_inst and dom_ms > 0 else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -307,7 +320,8 @@ def run_native(args, rank, world, local):
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "units_per_launch": units, "ops_per_unit": OPS_PER_UNIT.get(dom),
                          "avg_launch_ms": dom_ms,
-                         "peak_note": f"148 SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (issue-limited int lane-ops)"},
+                         "peak_note": f"148 SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (issue-limited int lane-ops)",
+                         "executed": executed},
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
             "kernel_share": share,
             "e2e": e2e,

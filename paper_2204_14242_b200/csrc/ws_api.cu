@@ -134,6 +134,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   for (int64_t v : c->chunk_bound) cb = std::max(cb, v);
   const size_t max_chunks = n * (size_t)cb;
   size_t off = 0;
+  const size_t o_pdone = off;   off = align_up(off + sizeof(unsigned int));  // fixed offset: survives re-layouts
   const size_t o_plans = off;   off = align_up(off + n * sizeof(DPlan));
   const size_t o_instr = off;   off = align_up(off + n * (size_t)kMaxInstr * sizeof(DInstr));
   const size_t o_row = off;     off = align_up(off + n * (size_t)kMaxFields * sizeof(DRowInfo));
@@ -159,6 +160,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
     cudaError_t e = cudaMalloc(&c->scratch, off);
     if (e != cudaSuccess) return fail(c, WS_ENOMEM, std::string("device scratch: ") + cudaGetErrorString(e));
     c->scratch_cap = off;
+    cudaMemset(c->scratch, 0, off);  // counters (k_plan's plan_done) start at 0
   }
   char* b = (char*)c->scratch;
   s.plans = (DPlan*)(b + o_plans);
@@ -177,6 +179,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   s.wlist = (unsigned long long*)(b + o_wlist);
   s.slist = (unsigned long long*)(b + o_slist);
   s.dlist = (unsigned long long*)(b + o_dlist);
+  s.plan_done = (unsigned int*)(b + o_pdone);
   c->last_work = s.work;
   return WS_OK;
 }

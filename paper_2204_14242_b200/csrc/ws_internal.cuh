@@ -139,6 +139,7 @@ struct Scratch {
   unsigned long long* wlist;  // n * kWSlots entries (config << 32 | slot)
   unsigned long long* slist;  // n * kSSlots entries
   unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm entries
+  unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
 };
 
 // kernel kinds, in launch order (ws_kernel_name)

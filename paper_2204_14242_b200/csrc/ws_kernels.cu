@@ -454,11 +454,91 @@ __device__ __forceinline__ void decode_kappa(int q, const int* f, int& kx, int& 
   kz = q / (f[0] * f[1]);
 }
 
+__device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
+  switch (j) {
+    case 0: return P.n_warp_items;
+    case 1: return P.n_wclass_items;
+    case 2: return P.n_set_items;
+    case 3: return P.n_sclass_items;
+    case 4: return P.n_chunks;
+    case 5: return P.n_fields;
+    default: return P.n_sect_items;
+  }
+}
+
+// exclusive prefix of the per-config work counts (one CTA of any size); zeroes the work and
+// list counters of the call
+__device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
+                          unsigned long long* __restrict__ work, unsigned long long* __restrict__ lists) {
+  __shared__ long long s_w[32][kNPrefix];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < 16) work[tid] = 0ull;  // K_NKINDS <= 16
+  if (tid < 4) lists[tid] = 0ull;
+  const int seg = (n + nt - 1) / nt;
+  long long a[kNPrefix];
+#pragma unroll
+  for (int j = 0; j < kNPrefix; ++j) a[j] = 0;
+  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
+    const DPlan& P = plans[c];
+    if (P.status != WS_OK) continue;
+#pragma unroll
+    for (int j = 0; j < kNPrefix; ++j) a[j] += plan_count(P, j);
+  }
+  // block exclusive scan of the per-thread sums: warp inclusive scans, then the warp totals
+  long long inc[kNPrefix];
+#pragma unroll
+  for (int j = 0; j < kNPrefix; ++j) {
+    long long v = a[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = shfl64_up(v, o);
+      if (lane >= o) v += u;
+    }
+    inc[j] = v;
+    if (lane == 31) s_w[wid][j] = v;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < kNPrefix; ++j) {
+      long long v = lane < (nt >> 5) ? s_w[lane][j] : 0;
+      const long long own = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long u = shfl64_up(v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane < (nt >> 5)) s_w[lane][j] = v - own;  // exclusive warp offsets
+    }
+  }
+  __syncthreads();
+  long long r[kNPrefix];
+#pragma unroll
+  for (int j = 0; j < kNPrefix; ++j) r[j] = s_w[wid][j] + inc[j] - a[j];
+  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
+    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
+    const DPlan& P = plans[c];
+    if (P.status != WS_OK) continue;
+#pragma unroll
+    for (int j = 0; j < kNPrefix; ++j) r[j] += plan_count(P, j);
+  }
+  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
+}
+
+__global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
+                                               unsigned long long* __restrict__ work,
+                                               unsigned long long* __restrict__ lists) {
+  scan_body(plans, n, pre, work, lists);
+}
+
 __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs, int n,
                                               const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
                                               int ng, DPlan* __restrict__ plans, DInstr* __restrict__ instr,
                                               DRowInfo* __restrict__ rowinfo, unsigned long long* __restrict__ acc,
-                                              unsigned int* __restrict__ wcnt, unsigned int* __restrict__ scnt) {
+                                              unsigned int* __restrict__ wcnt, unsigned int* __restrict__ scnt,
+                                              unsigned int* __restrict__ plan_done, DPrefix* __restrict__ pre,
+                                              unsigned long long* __restrict__ work,
+                                              unsigned long long* __restrict__ lists) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
   __shared__ DPlan P;
@@ -493,9 +573,21 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     }
   }
   __syncthreads();
-  auto store_plan = [&]() {  // cooperative 16-byte copy of the shared plan
-    uint4* dst = reinterpret_cast<uint4*>(plans + c);
+  __shared__ int s_last;
+  auto store_plan = [&]() {  // cooperative 16-byte copy of the shared plan; the last CTA to finish
+    uint4* dst = reinterpret_cast<uint4*>(plans + c);  // scans the work counts of every config
     for (int i = tid; i < kPlanVec; i += blockDim.x) dst[i] = reinterpret_cast<const uint4*>(&P)[i];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(plan_done, 1u) == (unsigned)(n - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      scan_body(plans, n, pre, work, lists);
+      if (tid == 0) *plan_done = 0u;  // reset for the next call (graph replay)
+    }
   };
   if (P.status != WS_OK) {
     store_plan();
@@ -638,75 +730,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
 }
 
 // ------------------------------------------------------------------ scan of work counts
-__device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
-  switch (j) {
-    case 0: return P.n_warp_items;
-    case 1: return P.n_wclass_items;
-    case 2: return P.n_set_items;
-    case 3: return P.n_sclass_items;
-    case 4: return P.n_chunks;
-    case 5: return P.n_fields;
-    default: return P.n_sect_items;
-  }
-}
 
-__global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
-                                               unsigned long long* __restrict__ work,
-                                               unsigned long long* __restrict__ lists) {
-  __shared__ long long s_w[32][kNPrefix];
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < 16) work[tid] = 0ull;  // K_NKINDS <= 16
-  if (tid < 4) lists[tid] = 0ull;
-  const int seg = (n + nt - 1) / nt;
-  long long a[kNPrefix];
-#pragma unroll
-  for (int j = 0; j < kNPrefix; ++j) a[j] = 0;
-  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
-    const DPlan& P = plans[c];
-    if (P.status != WS_OK) continue;
-#pragma unroll
-    for (int j = 0; j < kNPrefix; ++j) a[j] += plan_count(P, j);
-  }
-  // block exclusive scan of the per-thread sums: warp inclusive scans, then the warp totals
-  long long inc[kNPrefix];
-#pragma unroll
-  for (int j = 0; j < kNPrefix; ++j) {
-    long long v = a[j];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long u = shfl64_up(v, o);
-      if (lane >= o) v += u;
-    }
-    inc[j] = v;
-    if (lane == 31) s_w[wid][j] = v;
-  }
-  __syncthreads();
-  if (wid == 0) {
-#pragma unroll
-    for (int j = 0; j < kNPrefix; ++j) {
-      long long v = lane < (nt >> 5) ? s_w[lane][j] : 0;
-      const long long own = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long u = shfl64_up(v, o);
-        if (lane >= o) v += u;
-      }
-      if (lane < (nt >> 5)) s_w[lane][j] = v - own;  // exclusive warp offsets
-    }
-  }
-  __syncthreads();
-  long long r[kNPrefix];
-#pragma unroll
-  for (int j = 0; j < kNPrefix; ++j) r[j] = s_w[wid][j] + inc[j] - a[j];
-  for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
-    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
-    const DPlan& P = plans[c];
-    if (P.status != WS_OK) continue;
-#pragma unroll
-    for (int j = 0; j < kNPrefix; ++j) r[j] += plan_count(P, j);
-  }
-  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
-}
 
 // ------------------------------------------------------------------ a2 + a3: warp instructions
 struct Lane {
@@ -2355,11 +2379,9 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), m);
   cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), m);
   beg(K_PLAN, m);
-  k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt);
+  k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
+                           s.plan_done, s.prefix, s.work, s.lists);  // its last CTA does the scan (k_scan)
   end(K_PLAN, m);
-  beg(K_SCAN, m);
-  k_scan<<<1, 1024, 0, m>>>(s.plans, n, s.prefix, s.work, s.lists);
-  end(K_SCAN, m);
   // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on main
   cudaEventRecord(st.fork, m);
   cudaStreamWaitEvent(a, st.fork, 0);

@@ -74,6 +74,9 @@ def main(rep, md_out, traffic_out):
         rd, wr = acc[name]["DRAM read MB"], acc[name]["DRAM write MB"]
         if rd and wr:
             traffic[name] = sum(rd) / len(rd) + sum(wr) / len(wr)
+        wi = acc[name]["warp inst"]
+        if wi:
+            traffic[name + ":warp_inst"] = sum(wi) / len(wi)
         lines.append(f"| {name} | {n} | " + " | ".join(cells) + " |")
     with open(md_out, "w") as f:
         f.write("\n".join(lines) + "\n")
