@@ -8,5 +8,5 @@ python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 cat gpurun_out/bench.json
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(rows|sclass|wclass|fold|smset|plan|warp)" -s 12 -c 6 -o gpurun_out/full python scripts/ncu_target.py > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(rows|sclass|wclass|fold|smset|plan|warp)" -s 14 -c 7 -o gpurun_out/full python scripts/ncu_target.py > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
