@@ -377,6 +377,27 @@ def next_rows_measure(ctx, stream, args, cpu_baseline):
                     "section link (k_sect active)",
         "value": n / (ms / 1e3), "unit": "configs/s", "ms_per_step": ms, "k_sect_ms": sect_ms,
         "data": "synthetic", "timing": "CUDA events on the context stream, graph replay, no L2 flush"}
+    # ---- the extended throughput space: 1890 configs (power-of-two shapes with
+    # 64..1024 threads x (fy, fz) in {1,2,4}^2) of the same 512^3 stencil, A100 parameters
+    k, g = W.k25(512), W.gpu_a100()
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
+    cf = config_array(kid, gid, W.space_extended())
+    n = len(cf)
+    d_cfg = torch.from_numpy(cf.view(np.uint8).copy()).cuda()
+    d_out = torch.empty(n * 336, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+    torch.cuda.synchronize()
+    steps_x = 10
+    e0.record(stream)
+    for _ in range(steps_x):
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps_x
+    out["extended_space"] = {"workload": f"3D-25pt r4 512^3, extended space (SURVEY Q34), {n} configs, A100 parameters",
+                             "value": n / (ms / 1e3), "unit": "configs/s", "ms_per_step": ms, "data": "synthetic",
+                             "timing": "CUDA events on the context stream, graph replay, no L2 flush"}
     # ---- NEXT-1: simulated hit-rate samples
     k, g = W.k25(40), W.gpu_a100()
     kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
