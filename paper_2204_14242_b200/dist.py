@@ -20,7 +20,7 @@ def proxy_cost(config) -> float:
     """Scheduling heuristic (not part of any result): the work of a configuration grows with
     the depth of its block layer (the L_z layer set spans one block layer) plus the
     halo; (block, fold, k) as in workloads."""
-    (bx, by, bz), (fx, fy, fz), _ = config
+    (bx, by, bz), (fx, fy, fz) = config[0], config[1]   # (block, fold, k[, variant])
     return float(bz * fz + 8)
 
 
