@@ -249,6 +249,16 @@ ws_status ws_fit_gompertz(ws_ctx* ctx, const double* O, const double* R, size_t 
 ws_status ws_validate_stencil25(void* cuda_stream, const double* d_src, double* d_dst, const int64_t n[3],
                                 const uint32_t block[3], const uint32_t fold[3], uint32_t reps, double* ms_avg);
 
+/* The paper's second workload (the estimator's LBM15 description) as an
+ * sm_100a kernel: D3Q15 pull (PDF q loaded at cell - c_q from d_src + q * array, stored at the
+ * cell to d_dst + q * array), phase field d_phi loaded at the cell and its 6 neighbours, FD
+ * result stored to d_fd; FP64; arrays of (n[0]+2)(n[1]+2)(n[2]+2) doubles (ghost 1, fzyx: the 15
+ * PDFs of d_src / d_dst consecutive), domain [1, n+1)^3; velocities in workloads.D3Q15 order.
+ * block = threads per block; reps launches; average device ms in *ms_avg.  Errors as
+ * ws_validate_stencil25. */
+ws_status ws_validate_lbm15(void* cuda_stream, const double* d_src, double* d_dst, const double* d_phi, double* d_fd,
+                            const int64_t n[3], const uint32_t block[3], uint32_t reps, double* ms_avg);
+
 /* Number of kernel launches the last ws_estimate[_async] / ws_rank[_async]
  * call enqueued (for the bench's gpu_launches count). */
 uint32_t ws_last_launch_count(const ws_ctx* ctx);

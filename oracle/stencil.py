@@ -24,3 +24,38 @@ def stencil25(src, n):
         v = v + W[k] * acc
     dst[c] = v
     return dst
+
+
+# D3Q15 in the estimator's order (workloads.D3Q15): rest, 6 faces, 8 corners
+Q15 = [(0, 0, 0), (1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)] + \
+      [(x, y, z) for x in (-1, 1) for y in (-1, 1) for z in (-1, 1)]
+
+
+def lbm15(src, phi, n):
+    """Plain definition of the LBM15 validation kernel: per cell of the
+    domain [1, n+1)^3 of (n+2)^3 arrays, pull f_q = src_q(cell - c_q); rho, j = sum f_q (1, c_q);
+    lap = 7-point Laplacian of phi; omega = 1.2 + 0.1 phi; feq_q = w_q (rho + 3 c_q.j) + w_q 0.05 lap;
+    dst_q = f_q + omega (feq_q - f_q); fd = lap.  src: (15, nz+2, ny+2, nx+2); phi: (nz+2, ny+2, nx+2).
+    Returns (dst, fd) with ghost layers zero."""
+    nx, ny, nz = n
+    dom = (slice(1, nz + 1), slice(1, ny + 1), slice(1, nx + 1))
+
+    def sh(a, dx, dy, dz):   # a(cell + (dx, dy, dz)) over the domain
+        return a[1 + dz:nz + 1 + dz, 1 + dy:ny + 1 + dy, 1 + dx:nx + 1 + dx]
+    f = [sh(src[q], -c[0], -c[1], -c[2]) for q, c in enumerate(Q15)]
+    rho = sum(f)
+    jx = sum(c[0] * f[q] for q, c in enumerate(Q15))
+    jy = sum(c[1] * f[q] for q, c in enumerate(Q15))
+    jz = sum(c[2] * f[q] for q, c in enumerate(Q15))
+    p0 = phi[dom]
+    lap = sh(phi, 1, 0, 0) + sh(phi, -1, 0, 0) + sh(phi, 0, 1, 0) + sh(phi, 0, -1, 0) + \
+        sh(phi, 0, 0, 1) + sh(phi, 0, 0, -1) - 6.0 * p0
+    omega, g = 1.2 + 0.1 * p0, 0.05 * lap
+    dst = np.zeros_like(src)
+    for q, c in enumerate(Q15):
+        w = 2.0 / 9.0 if q == 0 else (1.0 / 9.0 if q < 7 else 1.0 / 72.0)
+        feq = w * (rho + 3.0 * (c[0] * jx + c[1] * jy + c[2] * jz)) + w * g
+        dst[q][dom] = f[q] + omega * (feq - f[q])
+    fd = np.zeros_like(phi)
+    fd[dom] = lap
+    return dst, fd

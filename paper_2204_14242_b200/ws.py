@@ -79,7 +79,7 @@ RESULT_DTYPE = np.dtype(ws_result)
 EXPORTS = ["ws_create", "ws_destroy", "ws_last_error", "ws_set_stream", "ws_describe_kernel", "ws_describe_gpu",
            "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count",
            "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read", "ws_simulate",
-           "ws_fit_gompertz", "ws_validate_stencil25"]
+           "ws_fit_gompertz", "ws_validate_stencil25", "ws_validate_lbm15"]
 
 _lib = None
 
@@ -114,6 +114,7 @@ def load_library(path: str = LIB_PATH):
     L.ws_simulate.argtypes = [P, P, C.c_size_t, P, U32, P]
     L.ws_fit_gompertz.argtypes = [P, P, P, C.c_size_t, P, P]
     L.ws_validate_stencil25.argtypes = [P, P, P, P, P, P, U32, P]
+    L.ws_validate_lbm15.argtypes = [P, P, P, P, P, P, P, U32, P]
     L.ws_kernel_name.argtypes = [U32]
     L.ws_kernel_name.restype = C.c_char_p
     for n in EXPORTS:
@@ -322,4 +323,16 @@ class Context:
                                           int(reps), C.byref(ms))
         if st != WS_OK:
             raise WSError(st, "ws_validate_stencil25 failed")
+        return ms.value
+
+    def validate_lbm15(self, d_src: int, d_dst: int, d_phi: int, d_fd: int, n, block, reps: int = 1,
+                       stream: int = 0) -> float:
+        """Run the LBM15 validation kernel (device pointers) `reps` times; average device ms."""
+        nn = (C.c_int64 * 3)(*n)
+        bb = (U32 * 3)(*block)
+        ms = F64()
+        st = self.L.ws_validate_lbm15(C.c_void_p(stream or 0), C.c_void_p(d_src), C.c_void_p(d_dst),
+                                      C.c_void_p(d_phi), C.c_void_p(d_fd), nn, bb, int(reps), C.byref(ms))
+        if st != WS_OK:
+            raise WSError(st, "ws_validate_lbm15 failed")
         return ms.value

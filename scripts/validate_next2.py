@@ -31,6 +31,10 @@ import workloads as W  # noqa: E402
 
 N = 512
 REGS = 32   # registers/thread of k_st25 (cuobjdump --dump-resource-usage)
+LBM = os.environ.get("WS_VALIDATE", "k25") == "lbm15"
+if LBM:
+    N = 256
+    REGS = 128   # k_lbm15: __launch_bounds__(512, 1) -> 128 registers ("at most 512 threads")
 METRICS = ["gpu__time_duration.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
            "l1tex__data_pipe_lsu_wavefronts.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
            "lts__t_sectors_srcunit_tex_op_write.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]
@@ -38,24 +42,47 @@ METRICS = ["gpu__time_duration.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld
 
 def fields():
     import torch
+    if LBM:
+        shp = (N + 2, N + 2, N + 2)
+        src = torch.rand((15,) + shp, dtype=torch.float64, device="cuda")
+        phi = torch.rand(shp, dtype=torch.float64, device="cuda")
+        return src, torch.zeros_like(src), phi, torch.zeros_like(phi)
     src = torch.rand((N + 8, N + 8, N + 8), dtype=torch.float64, device="cuda")
     return src, torch.zeros_like(src)
+
+
+def space():
+    return W.space_lbm() if LBM else W.space_stencil_paper()
+
+
+def kernel_desc():
+    if LBM:
+        k = W.lbm15(N)
+        k["regs"] = REGS
+        return k
+    return W.stencil_star(N, N, N, 4, regs=REGS)
+
+
+def launch(ctx, fl, b, f, reps):
+    if LBM:
+        return ctx.validate_lbm15(fl[0].data_ptr(), fl[1].data_ptr(), fl[2].data_ptr(), fl[3].data_ptr(),
+                                  (N, N, N), b, reps=reps)
+    return ctx.validate_stencil25(fl[0].data_ptr(), fl[1].data_ptr(), (N, N, N), b, f, reps=reps)
 
 
 def run(mode, out=None):
     import torch
     from paper_2204_14242_b200 import Context
     ctx = Context(0)
-    src, dst = fields()
-    space = W.space_stencil_paper()
+    fl = fields()
     res = []
-    for (b, f, _k) in space:
+    for (b, f, _k) in space():
         if mode == "time":
-            ctx.validate_stencil25(src.data_ptr(), dst.data_ptr(), (N, N, N), b, f, reps=1)
-            ms = ctx.validate_stencil25(src.data_ptr(), dst.data_ptr(), (N, N, N), b, f, reps=5)
+            launch(ctx, fl, b, f, 1)
+            ms = launch(ctx, fl, b, f, 5)
             res.append({"block": b, "fold": f, "ms": ms, "glups": N ** 3 / (ms / 1e3) / 1e9})
         else:
-            ctx.validate_stencil25(src.data_ptr(), dst.data_ptr(), (N, N, N), b, f, reps=1)
+            launch(ctx, fl, b, f, 1)
     torch.cuda.synchronize()
     if mode == "time":
         json.dump(res, open(out, "w"), indent=0)
@@ -68,7 +95,7 @@ def parse_ncu(path):
     iid, iname, ival, ikern = h.index("ID"), h.index("Metric Name"), h.index("Metric Value"), h.index("Kernel Name")
     by = {}
     for r in rows[start + 1:]:
-        if len(r) <= ival or "k_st25" not in r[ikern]:
+        if len(r) <= ival or ("k_st25" not in r[ikern] and "k_lbm15" not in r[ikern]):
             continue
         by.setdefault(int(r[iid]), {})[r[iname]] = float(r[ival].replace(",", ""))
     return [by[k] for k in sorted(by)]
@@ -102,19 +129,19 @@ def b200_params():
 
 def analyze(time_json, ncu_csv, prefix, hit_abc=None, title_note="Hit-rate curves: SURVEY Q17 defaults (not calibrated to B200)."):
     from paper_2204_14242_b200 import Context, config_array, result_dicts
-    k = W.stencil_star(N, N, N, 4, regs=REGS)
+    k = kernel_desc()
     g = b200_params()
     if hit_abc is not None:
         g["hit_abc"] = [list(t) for t in hit_abc]
     ctx = Context(0)
-    space = W.space_stencil_paper()
-    pred = result_dicts(ctx.estimate(config_array(ctx.describe_kernel(k), ctx.describe_gpu(g), space)))
+    sp = space()
+    pred = result_dicts(ctx.estimate(config_array(ctx.describe_kernel(k), ctx.describe_gpu(g), sp)))
     tm = json.load(open(time_json))
     meas = parse_ncu(ncu_csv)
-    assert len(meas) == len(space) == len(tm), (len(meas), len(space), len(tm))
+    assert len(meas) == len(sp) == len(tm), (len(meas), len(sp), len(tm))
     lup = float(N ** 3)
     rows = []
-    for c, p, t, m in zip(space, pred, tm, meas):
+    for c, p, t, m in zip(sp, pred, tm, meas):
         rows.append({
             "block": c[0], "fold": c[1], "limiter": ["L1", "L2", "DRAM", "link"][p["limiter"]],
             "l1_sec_Bpl": (32 * m["l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"] / lup,
@@ -148,7 +175,9 @@ def analyze(time_json, ncu_csv, prefix, hit_abc=None, title_note="Hit-rate curve
     }
     json.dump({"summary": summ, "rows": rows, "gpu": g["name"], "regs": REGS}, open(prefix + ".json", "w"), indent=0)
     with open(prefix + ".md", "w") as f:
-        f.write("# NEXT-2 on-box validation: 3D-25pt r4 512^3, 168 configs, B200 (measured) vs estimator (B200 parameters)\n\n")
+        f.write(("# NEXT-2 on-box validation: LBM15 (D3Q15 pull + 7pt phase field) 256^3, 49 configs" if LBM else
+                 "# NEXT-2 on-box validation: 3D-25pt r4 512^3, 168 configs") +
+                ", B200 (measured) vs estimator (B200 parameters)\n\n")
         f.write("Per-level volumes per lattice update (ncu counters / 512^3) against the estimator's prediction; "
                 "GLup/s from CUDA events (5 launches each).  " + title_note + "\n\n")
         f.write("| quantity | median abs rel err | p90 abs rel err | Spearman (measured vs predicted) |\n|---|---|---|---|\n")

@@ -458,3 +458,21 @@ def test_validation_stencil_full_size_sampled(ctx):
         sub = src[z - 4:z + 5, y - 4:y + 5, x - 4:x + 5]
         ref = ST.stencil25(np.pad(sub, 0), (1, 1, 1))[4, 4, 4]
         assert abs(dst[z, y, x] - ref) <= 1e-13 * max(1.0, abs(ref))
+
+
+def test_validation_lbm15_small(ctx):
+    """The LBM15 validation kernel against the plain numpy definition (ragged blocks)."""
+    import torch
+    from oracle import stencil as ST
+    for n, block in [((10, 8, 6), (4, 2, 2)), ((13, 7, 5), (8, 4, 1)), ((6, 6, 6), (1, 8, 8))]:
+        g = torch.Generator().manual_seed(sum(n))
+        shp = (n[2] + 2, n[1] + 2, n[0] + 2)
+        src = torch.rand((15,) + shp, dtype=torch.float64, generator=g)
+        phi = torch.rand(shp, dtype=torch.float64, generator=g)
+        d_src, d_phi = src.cuda(), phi.cuda()
+        d_dst, d_fd = torch.zeros_like(d_src), torch.zeros_like(d_phi)
+        ctx.validate_lbm15(d_src.data_ptr(), d_dst.data_ptr(), d_phi.data_ptr(), d_fd.data_ptr(), n, block)
+        torch.cuda.synchronize()
+        dst, fd = ST.lbm15(src.numpy(), phi.numpy(), n)
+        assert np.allclose(d_dst.cpu().numpy(), dst, rtol=1e-12, atol=1e-12), (n, block)
+        assert np.allclose(d_fd.cpu().numpy(), fd, rtol=1e-12, atol=1e-12), (n, block)

@@ -687,3 +687,28 @@ def test_stencil25_definition_pins():
                 if 4 <= z < n[2] + 4 and 4 <= y < n[1] + 4 and 4 <= x < n[0] + 4:
                     assert dst[z, y, x] == ST.W[k]
     assert np.count_nonzero(dst) <= 25
+
+
+def test_lbm15_definition_pins():
+    """The plain LBM15 update: the weights sum to 1 (2/9 + 6/9 + 8/72), so a uniform state
+    (f_q = w_q rho0, constant phi) is a fixed point (feq = f), the streaming pull moves a single
+    population exactly by c_q, and the FD result is the 7-point Laplacian."""
+    from oracle import stencil as ST
+    n = (6, 5, 4)
+    w = [2.0 / 9.0] + [1.0 / 9.0] * 6 + [1.0 / 72.0] * 8
+    assert abs(sum(w) - 1.0) < 1e-15
+    src = np.stack([np.full((n[2] + 2, n[1] + 2, n[0] + 2), wq * 1.7) for wq in w])
+    phi = np.zeros((n[2] + 2, n[1] + 2, n[0] + 2))
+    dst, fd = ST.lbm15(src, phi, n)
+    assert np.allclose(dst[:, 1:-1, 1:-1, 1:-1], src[:, 1:-1, 1:-1, 1:-1], rtol=1e-14)
+    assert not fd.any()
+    src = np.zeros_like(src)
+    src[8, 2, 2, 2] = 1.0                       # population q=8, c = (-1,-1,1) at cell (2,2,2)
+    dst, _ = ST.lbm15(src, phi, n)
+    c = ST.Q15[8]
+    z, y, x = 2 + c[2], 2 + c[1], 2 + c[0]      # pulled from cell - c: lands at cell + c
+    om = 1.2
+    assert dst[8, z, y, x] == pytest.approx(1.0 + om * (1.0 / 72.0 * (1.0 + 3.0 * 3.0) - 1.0), rel=1e-14)
+    phi[3, 3, 3] = 1.0
+    _, fd = ST.lbm15(np.zeros_like(src), phi, n)
+    assert fd[3, 3, 3] == -6.0 and fd[3, 3, 4] == 1.0 and fd[2, 3, 3] == 1.0
