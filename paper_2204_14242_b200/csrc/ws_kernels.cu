@@ -2798,13 +2798,17 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
       // previous access of the line: an earlier lane of this step, or the stored last access
       const long long p = prev_lane >= 0 ? c0 + prev_lane : lastp;
       const long long psnap = (leader && lastp >= 0) ? lastp : -1;  // a marker of the state before the step
-      const uint32_t Fc0 = fen_prefix(f, c0);
+      // prefix over [0, c0) (the same for every lane): one tree node per set bit of c0, one lane each
+      uint32_t fpart = 0u;
+      if (lane < 31 && ((c0 >> lane) & 1)) fpart = __ldcg(&f[(c0 >> lane) << lane]);
+      const uint32_t Fc0 = __reduce_add_sync(FULL, fpart);
       const uint32_t Fp = psnap >= 0 ? fen_prefix(f, psnap + 1) : 0u;
       // pass 1 (uniform): markers moved / set by the step's earlier lanes
       int sub = 0, add_all = 0, add_after_prev = 0;
 #pragma unroll 8
+      const int psnap32 = (int)psnap;  // positions < 2^31 (ws_simulate limit)
       for (int j = 0; j < 32; ++j) {
-        const long long pj = shfl64(psnap, j);
+        const long long pj = __shfl_sync(FULL, psnap32, j);
         const int nj = __shfl_sync(FULL, next_lane, j);
         if (j < lane) {
           sub += (pj > p) ? 1 : 0;                 // old marker in (p, c0) moved into the step
@@ -2864,7 +2868,23 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
             }
           }
           lastv[slot] = (uint32_t)i;
-          fen_add(f, n, i, 1u);
+        }
+      }
+      // the step's new markers (last access of each line in the step): the tree nodes inside the
+      // step (c0 + 1 .. c0 + 31; untouched so far) are written directly, the node c0 + 32 and its
+      // ancestors (which cover the whole step) get the step's total
+      {
+        const unsigned newm = __ballot_sync(FULL, valid && next_lane == 32);
+        const int j1 = lane + 1;
+        if (lane < 31 && c0 + j1 <= n) {
+          const int lb = j1 & -j1;
+          const unsigned msk = (lb >= 32 ? 0xffffffffu : ((1u << lb) - 1u)) << (j1 - lb);
+          f[c0 + j1] = (uint32_t)__popc(newm & msk);
+        }
+        if (lane == 0 && c0 + 32 <= n) {
+          const uint32_t tot = (uint32_t)__popc(newm);
+          if (tot)
+            for (long long x = c0 + 32; x <= n; x += x & -x) atomicAdd(&f[x], tot);
         }
       }
       if (psnap >= 0) fen_add(f, n, psnap, 0xffffffffu);
