@@ -1499,6 +1499,7 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
 // active-cell boxes that are translates by a multiple of the line size have identical
 // sector and line counts).  Multi-block sets are appended to the direct list.
 __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                               const DKernel* __restrict__ ks,
                                                const DGpu* __restrict__ gs, unsigned int* __restrict__ scnt,
                                                unsigned long long* __restrict__ srep,
                                                unsigned long long* __restrict__ lists,
@@ -1513,16 +1514,74 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
     const long long nsm = gs[P.gid].g.n_sm;
     const long long S0 = P.s + j;
     const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-    if (P.scls_R > 0 && kj == 1 && !P.rep_mult) {
-      const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
-      long long pl = 0;
+    // A multi-block set whose members' load footprints cannot share a line is the disjoint union
+    // of its members' footprints: every member is then counted like a single-block set, in its
+    // translation class (members are n_sm blocks apart, usually far apart in the grid).  Two
+    // members' footprints (block box + the field's load-offset extremes) share no line when they
+    // are >= 2 planes apart in z, or >= 2 rows apart in y without touching the field's first or
+    // last row (rows / planes of >= one line), or >= one line of elements apart in x unless one
+    // reaches a row end and the other a row start (wrap-around adjacency of consecutive rows).
+    // Otherwise the set is evaluated directly.
+    bool split = false;
+    if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult) {
+      const DKernel& K = ks[P.kid];
+      const long long lb = gs[P.gid].g.line_bytes;
+      split = true;
+      long long box[32][6];
+      for (long long m = 0; m < kj; ++m) {
+        const long long Bm = S0 + m * nsm;
+        const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+        for (int d = 0; d < 3; ++d) {
+          box[m][2 * d] = P.lo[d] + bc[d] * P.BF[d];
+          long long hi = box[m][2 * d] + P.BF[d];
+          box[m][2 * d + 1] = (hi > P.hi[d] ? P.hi[d] : hi) - 1;
+        }
+      }
+      for (int fi = 0; fi < K.n_fields && split; ++fi) {
+        const DField& F = K.f[fi];
+        if (!(F.kinds & 1)) continue;
+        int xlo = 0x7fffffff, xhi = -0x7fffffff;
+        for (int r = 0; r < F.n_runs; ++r) {
+          xlo = min(xlo, F.run_lo[r]);
+          xhi = max(xhi, F.run_hi[r]);
+        }
+        const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
+        const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
+        for (long long a1 = 0; a1 < kj && split; ++a1)
+          for (long long b1 = a1 + 1; b1 < kj && split; ++b1) {
+            const long long ax0 = box[a1][0] + xlo, ax1 = box[a1][1] + xhi, bx0 = box[b1][0] + xlo, bx1 = box[b1][1] + xhi;
+            const long long ay0 = box[a1][2] + F.ld_oy_min, ay1 = box[a1][3] + F.ld_oy_max;
+            const long long by0 = box[b1][2] + F.ld_oy_min, by1 = box[b1][3] + F.ld_oy_max;
+            const long long az0 = box[a1][4] + F.ld_oz_min, az1 = box[a1][5] + F.ld_oz_max;
+            const long long bz0 = box[b1][4] + F.ld_oz_min, bz1 = box[b1][5] + F.ld_oz_max;
+            // rows >= 2 apart share no line within a plane; across consecutive planes only if a box
+            // reaches the field's first / last row (p2 >= p1 * ext1), hence the y-ends condition
+            const bool y_inner = min(ay0, by0) >= 1 && max(ay1, by1) <= F.ext[1] - 2;
+            const bool sep_y = rows_ok && y_inner && (ay1 + 2 <= by0 || by1 + 2 <= ay0);
+            const bool sep_z = planes_ok && (az1 + 2 <= bz0 || bz1 + 2 <= az0);
+            // consecutive rows in memory can share a line only between a box reaching the row end and
+            // one reaching the row start
+            const bool a_end = ax1 > F.pitch[1] - 1 - D, a_start = ax0 < D;
+            const bool b_end = bx1 > F.pitch[1] - 1 - D, b_start = bx0 < D;
+            const bool wrap = (a_end && b_start) || (b_end && a_start);
+            const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
+            if (!(sep_y || sep_z || sep_x)) split = false;
+          }
+      }
+    }
+    if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
+      for (long long m = 0; m < kj; ++m) {
+        const long long Bm = S0 + m * nsm;
+        const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+        long long pl = 0;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-      const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
-      const long long gslot = (long long)c * kSSlots + slot;
-      if (atomicAdd(scnt + gslot, 1u) == 0u) {
-        srep[gslot] = (unsigned long long)S0;
-        slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
+        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+        const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+        const long long gslot = (long long)c * kSSlots + slot;
+        if (atomicAdd(scnt + gslot, 1u) == 0u) {
+          srep[gslot] = (unsigned long long)Bm;
+          slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
+        }
       }
     } else {
       dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
@@ -2393,7 +2452,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
   end(K_FOLD, b);
   beg(K_SMSET, a);
-  k_smset<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, s.prefix, n, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
+  k_smset<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
   end(K_SMSET, a);
   beg(K_SCLASS, a);
   k_sclass<<<persist, 256, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);

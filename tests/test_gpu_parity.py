@@ -476,3 +476,13 @@ def test_validation_lbm15_small(ctx):
         dst, fd = ST.lbm15(src.numpy(), phi.numpy(), n)
         assert np.allclose(d_dst.cpu().numpy(), dst, rtol=1e-12, atol=1e-12), (n, block)
         assert np.allclose(d_fd.cpu().numpy(), fd, rtol=1e-12, atol=1e-12), (n, block)
+
+
+def test_extended_space_multiblock_sets(ctx):
+    """The extended space with 64-512-thread blocks: several blocks per SM
+    (k = 2..16), so multi-block SM sets whose members are split into translation classes
+    when their footprints cannot share a line (k_smset) -- every configuration against the
+    oracle on 48^3 and a ragged 40x36x44 domain."""
+    sp = [c for c in W.space_extended() if c[0][0] * c[0][1] * c[0][2] <= 512][::9]
+    for k in (W.k25(48), W.stencil_star(40, 36, 44, 4, regs=64)):
+        assert_parity(ctx, k, dict(W.gpu_a100(), n_sm=24), sp, "ext")
