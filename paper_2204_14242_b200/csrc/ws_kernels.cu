@@ -920,12 +920,30 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
 #pragma unroll
         for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d]);
         const int res = (int)(pl & (P.wcls_R - 1));  // (pl * elem) mod M, in elements
-        const int pat = clip_pattern(P, bc);
+        int pat = clip_pattern(P, bc);
         // power-of-two blocks: every warp covers an aligned sub-box with the same relative lane
-        // pattern, so in an unclipped block the warp index does not matter
+        // pattern, so in an unclipped block the warp index does not matter; in a clipped block a
+        // warp whose every folded cell is inside the domain is such a warp too, and a warp with
+        // no active cell contributes nothing
+        bool skip = false;
+        if (P.wpow2 && pat != 0) {
+          long long ext[3];  // thread extent of the warp's aligned sub-box
+          ext[0] = P.b[0] < 32 ? P.b[0] : 32;
+          ext[1] = P.b[0] >= 32 ? 1 : (P.b[0] * P.b[1] >= 32 ? 32 / P.b[0] : P.b[1]);
+          ext[2] = 32 / (ext[0] * ext[1]);
+          bool full = true, none = false;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const long long c0 = P.lo[d] + (bc[d] * P.b[d] + tc[d]) * P.f[d];
+            if (c0 + ext[d] * P.f[d] > P.hi[d]) full = false;
+            if (c0 >= P.hi[d]) none = true;
+          }
+          if (none) skip = true;
+          else if (full) pat = 0;
+        }
         const int wk = (P.wpow2 && pat == 0) ? 0 : w;
         const unsigned slot = (unsigned)(((wk * 64 + res) << 3) | pat);
-        key = ((unsigned long long)c << 32) | slot;
+        if (!skip) key = ((unsigned long long)c << 32) | slot;
         my_units += 32;
       } else {
         direct = true;
