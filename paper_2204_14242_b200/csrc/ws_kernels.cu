@@ -2882,8 +2882,8 @@ __global__ void __launch_bounds__(kSimWarps * 32) k_sim_run(const DPlan* __restr
       const uint32_t Fp = psnap >= 0 ? fen_prefix(f, psnap + 1) : 0u;
       // pass 1 (uniform): markers moved / set by the step's earlier lanes
       int sub = 0, add_all = 0, add_after_prev = 0;
-#pragma unroll 8
       const int psnap32 = (int)psnap;  // positions < 2^31 (ws_simulate limit)
+#pragma unroll 8
       for (int j = 0; j < 32; ++j) {
         const long long pj = __shfl_sync(FULL, psnap32, j);
         const int nj = __shfl_sync(FULL, next_lane, j);
