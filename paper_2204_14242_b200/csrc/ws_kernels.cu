@@ -1753,7 +1753,10 @@ __device__ __forceinline__ void row_union_cached(const Gen& gen, bool first, lon
   }
 }
 
-constexpr int kRowWarps = 8;
+#ifndef WS_ROW_WARPS
+#define WS_ROW_WARPS 8
+#endif
+constexpr int kRowWarps = WS_ROW_WARPS;
 
 constexpr int kSegRows = 1024;  // rows of a plane handled per k_rows segment
 
@@ -2451,7 +2454,16 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     if (ev) cudaEventRecord(ev[2 * kind + 1], q);
     ++L;
   };
-  const int persist = n_sm_dev * 8;
+#ifndef WS_PERSIST
+#define WS_PERSIST 8
+#endif
+#ifndef WS_PERSIST_ROWS
+#define WS_PERSIST_ROWS 8
+#endif
+#ifndef WS_PERSIST_SCLASS
+#define WS_PERSIST_SCLASS 8
+#endif
+  const int persist = n_sm_dev * WS_PERSIST;
   cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
   cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), m);
   cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), m);
@@ -2464,7 +2476,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   cudaStreamWaitEvent(a, st.fork, 0);
   cudaStreamWaitEvent(b, st.fork, 0);
   beg(K_ROWS, b);
-  k_rows<<<persist, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
+  k_rows<<<n_sm_dev * WS_PERSIST_ROWS, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
   end(K_ROWS, b);
   beg(K_FOLD, b);
   k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
@@ -2473,7 +2485,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_smset<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
   end(K_SMSET, a);
   beg(K_SCLASS, a);
-  k_sclass<<<persist, 256, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
+  k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, 256, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
   end(K_SCLASS, a);
   beg(K_WARP, m);
   k_warp<<<persist, 256, 0, m>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
