@@ -3174,6 +3174,337 @@ __global__ void __launch_bounds__(256) k_fit(const double* __restrict__ O, const
 }
 
 
+
+// ================================================================== NEXT-1: long streams in parallel
+// A stream of n >= kLongStream requests is not replayed by one warp but computed offline, fully
+// parallel (same exact results): dense line ids (hash), a stable radix sort of the requests by
+// line (time order kept inside each line), previous access p(i) of every request's line, the LRU
+// stack distance dist(i) = #{j < i : p(j) <= p(i)} - p(i) - 1 (the distinct lines accessed in
+// (p(i), i) are the accesses j there whose own previous access is <= p(i), and every j <= p(i)
+// has p(j) < j) counted with a wavelet matrix over p(j) + 1, then one thread per line walks its
+// accesses in time order with the per-sector running maxima D (as the warp path), histogramming
+// the counted requests and, for the layer stream, the end state of the overlap sectors.
+constexpr long long kLongStream = 1 << 18;
+constexpr int kScanB = 1024;  // elements per block of the device-wide scans
+
+__global__ void __launch_bounds__(256) k_ps_reduce(const uint32_t* __restrict__ in, long long m, uint32_t* __restrict__ bsum) {
+  const long long b0 = (long long)blockIdx.x * kScanB;
+  uint32_t v = 0;
+  for (int r = 0; r < kScanB / 256; ++r) {
+    const long long i = b0 + r * 256 + threadIdx.x;
+    if (i < m) v += in[i];
+  }
+  v = __reduce_add_sync(FULL, v);
+  __shared__ uint32_t s[8];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += s[w];
+    bsum[blockIdx.x] = t;
+  }
+}
+// single CTA: exclusive scan of nb block sums (in place), total to *total
+__global__ void __launch_bounds__(1024) k_ps_bsum(uint32_t* __restrict__ bsum, long long nb, uint32_t* __restrict__ total) {
+  __shared__ unsigned long long s[1024];
+  const int tid = threadIdx.x;
+  const long long seg = (nb + 1023) / 1024;
+  unsigned long long a = 0;
+  for (long long i = tid * seg; i < nb && i < (tid + 1) * seg; ++i) a += bsum[i];
+  s[tid] = a;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long r = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const unsigned long long x = s[i];
+      s[i] = r;
+      r += x;
+    }
+    *total = (uint32_t)r;
+  }
+  __syncthreads();
+  a = s[tid];
+  for (long long i = tid * seg; i < nb && i < (tid + 1) * seg; ++i) {
+    const uint32_t x = bsum[i];
+    bsum[i] = (uint32_t)a;
+    a += x;
+  }
+}
+// exclusive scan of io[0..m) given the scanned block sums
+__global__ void __launch_bounds__(256) k_ps_apply(uint32_t* __restrict__ io, long long m, const uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t s_w[8];
+  __shared__ uint32_t s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long b0 = (long long)blockIdx.x * kScanB;
+  if (threadIdx.x == 0) s_base = bsum[blockIdx.x];
+  __syncthreads();
+  for (int r = 0; r < kScanB / 256; ++r) {
+    const long long i = b0 + r * 256 + threadIdx.x;
+    const uint32_t v = i < m ? io[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    uint32_t wb = 0, tot = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t t = s_w[w];
+      if (w < wid) wb += t;
+      tot += t;
+    }
+    if (i < m) io[i] = s_base + wb + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += tot;
+    __syncthreads();
+  }
+}
+
+// dense line ids: phase 1 insert the line keys, phase 2 (after a scan of the occupancy flags)
+// look them up; ids follow slot order (deterministic)
+__global__ void k_pl_insert(const unsigned long long* __restrict__ req, long long n, int lspl,
+                            unsigned long long* __restrict__ H, unsigned long long hm) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long r = req[i];
+    const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
+    const unsigned long long lkey = ((r >> 48) << 48) | (sb >> lspl);
+    unsigned long long h = sim_hash(lkey) & hm;
+    for (;;) {
+      const unsigned long long old = atomicCAS(&H[h], kEmpty, lkey);
+      if (old == kEmpty || old == lkey) break;
+      h = (h + 1) & hm;
+    }
+  }
+}
+__global__ void k_pl_occ(const unsigned long long* __restrict__ H, long long hcap, uint32_t* __restrict__ occ) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hcap; i += (long long)gridDim.x * blockDim.x)
+    occ[i] = H[i] != kEmpty ? 1u : 0u;
+}
+__global__ void k_pl_ids(const unsigned long long* __restrict__ req, long long n, int lspl, int spl,
+                         const unsigned long long* __restrict__ H, unsigned long long hm, const uint32_t* __restrict__ occ,
+                         uint32_t* __restrict__ key, uint32_t* __restrict__ val, unsigned char* __restrict__ sidx) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long r = req[i];
+    const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
+    const unsigned long long lkey = ((r >> 48) << 48) | (sb >> lspl);
+    unsigned long long h = sim_hash(lkey) & hm;
+    while (H[h] != lkey) h = (h + 1) & hm;
+    key[i] = occ[h];            // exclusive prefix of the occupancy = dense id
+    val[i] = (uint32_t)i;
+    sidx[i] = (unsigned char)(sb & (unsigned long long)(spl - 1));
+  }
+}
+
+// stable LSD radix pass on 8 bits of key (tiles of 2048 = 256 threads x 8 rounds)
+constexpr int kRsTile = 2048;
+__global__ void __launch_bounds__(256) k_rs_hist(const uint32_t* __restrict__ key, long long n, int shift,
+                                                 uint32_t* __restrict__ hist, long long ntiles) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const long long t0 = (long long)blockIdx.x * kRsTile;
+  for (int r = 0; r < kRsTile / 256; ++r) {
+    const long long i = t0 + r * 256 + threadIdx.x;
+    if (i < n) atomicAdd(&h[(key[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(long long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];   // digit-major
+}
+__global__ void __launch_bounds__(256) k_rs_scatter(const uint32_t* __restrict__ key, const uint32_t* __restrict__ val,
+                                                    long long n, int shift, const uint32_t* __restrict__ off,
+                                                    long long ntiles, uint32_t* __restrict__ key2,
+                                                    uint32_t* __restrict__ val2) {
+  __shared__ uint32_t run[256];           // elements of each digit already placed from this tile
+  __shared__ uint32_t wc[8][256];         // per-warp digit counts of the current round
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  run[tid] = off[(long long)tid * ntiles + blockIdx.x];
+  const long long t0 = (long long)blockIdx.x * kRsTile;
+  for (int r = 0; r < kRsTile / 256; ++r) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) wc[w][tid] = 0u;
+    __syncthreads();
+    const long long i = t0 + r * 256 + tid;
+    const bool ok = i < n;
+    const uint32_t k = ok ? key[i] : 0u, v = ok ? val[i] : 0u;
+    const uint32_t d = (k >> shift) & 255u;
+    const unsigned peers = __match_any_sync(FULL, ok ? d : 0x100u + (unsigned)lane);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (ok && rank == 0) wc[wid][d] = (uint32_t)__popc(peers);
+    __syncthreads();
+    uint32_t before = 0;  // same digit in earlier warps of this round
+    for (int w = 0; w < wid; ++w) before += wc[w][d];
+    if (ok) {
+      const uint32_t pos = run[d] + before + (uint32_t)rank;
+      key2[pos] = k;
+      val2[pos] = v;
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += wc[w][tid];
+    run[tid] += tot;
+    __syncthreads();
+  }
+}
+
+// previous access of the line, last-access flags, line starts; V = prev + 1 for the wavelet matrix
+__global__ void k_pl_prev(const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sval, long long n,
+                          uint32_t* __restrict__ V, uint32_t* __restrict__ islast, uint32_t* __restrict__ lstart) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const uint32_t i = sval[k], l = skey[k];
+    const bool first = k == 0 || skey[k - 1] != l;
+    const bool last = k + 1 == n || skey[k + 1] != l;
+    V[i] = first ? 0u : sval[k - 1] + 1u;
+    islast[i] = last ? 1u : 0u;
+    if (first) lstart[l] = (uint32_t)k;
+  }
+}
+// one wavelet-matrix level: the bit of every value (64-bit words, one ballot pair per warp) and
+// the zero flags for the scan
+__global__ void k_wm_bits(const uint32_t* __restrict__ cur, long long n, int bit, unsigned long long* __restrict__ words,
+                          uint32_t* __restrict__ zf) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (n + 63) / 64;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long i0 = w * 64 + lane, i1 = i0 + 32;
+    const uint32_t b0 = i0 < n ? (cur[i0] >> bit) & 1u : 0u, b1 = i1 < n ? (cur[i1] >> bit) & 1u : 0u;
+    if (i0 < n) zf[i0] = 1u - b0;
+    if (i1 < n) zf[i1] = 1u - b1;
+    const unsigned lo = __ballot_sync(FULL, b0), hi = __ballot_sync(FULL, b1);
+    if (lane == 0) words[w] = ((unsigned long long)hi << 32) | lo;
+  }
+}
+__global__ void k_wm_next(const uint32_t* __restrict__ cur, long long n, int bit, const uint32_t* __restrict__ zpos,
+                          const uint32_t* __restrict__ Z, uint32_t* __restrict__ nxt, uint32_t* __restrict__ rdir) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const uint32_t v = cur[j];
+    const uint32_t zp = zpos[j];
+    nxt[((v >> bit) & 1u) ? *Z + (uint32_t)j - zp : zp] = v;
+    if ((j & 63) == 0) rdir[j >> 6] = zp;   // zeros before this word
+  }
+}
+__device__ __forceinline__ uint32_t wm_rank0(const unsigned long long* words, const uint32_t* rdir, long long pos) {
+  const long long w = pos >> 6;
+  const int r = (int)(pos & 63);
+  if (r == 0) return rdir[w];
+  return rdir[w] + (uint32_t)__popcll(~words[w] & ((1ull << r) - 1ull));
+}
+// dist(i) = #{j < i : V[j] < p(i) + 2} - p(i) - 1 (kInf for a line's first access)
+__global__ void k_pl_dist(const uint32_t* __restrict__ V, long long n, int LV, const unsigned long long* __restrict__ words,
+                          const uint32_t* __restrict__ rdir, const uint32_t* __restrict__ Zs, long long wstride,
+                          uint32_t* __restrict__ dist) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t v = V[i];
+    if (v == 0u) {
+      dist[i] = kInf;
+      continue;
+    }
+    const uint32_t p = v - 1u, x = p + 2u;
+    long long a = 0, b = i;
+    uint32_t cnt = 0;
+    for (int lev = 0; lev < LV; ++lev) {
+      const int bit = LV - 1 - lev;
+      const unsigned long long* W = words + (long long)lev * wstride;
+      const uint32_t* R = rdir + (long long)lev * wstride;
+      const uint32_t ra = wm_rank0(W, R, a), rb = wm_rank0(W, R, b);
+      if ((x >> bit) & 1u) {
+        cnt += rb - ra;
+        a = Zs[lev] + (a - ra);
+        b = Zs[lev] + (b - rb);
+      } else {
+        a = ra;
+        b = rb;
+      }
+    }
+    dist[i] = cnt - p - 1u;
+  }
+}
+// one thread per line: walk its accesses in time order (per-sector running maxima), histogram the
+// counted requests; the layer stream's end state of the overlap sectors
+__global__ void __launch_bounds__(128) k_pl_lines(const uint32_t* __restrict__ sval, const uint32_t* __restrict__ lstart,
+                                                  long long U, long long n, const unsigned char* __restrict__ sidx,
+                                                  const uint32_t* __restrict__ dist, const unsigned long long* __restrict__ req,
+                                                  const uint32_t* __restrict__ cntlast, uint32_t Ulines, int spl, int lspl,
+                                                  int type, long long t_y, const unsigned long long* __restrict__ H,
+                                                  unsigned long long whm, const unsigned long long* __restrict__ lines,
+                                                  int ncap, unsigned long long* __restrict__ A) {
+  __shared__ unsigned s_h[2][kSimHist];
+  __shared__ unsigned long long s_c[4];  // counted, compulsory, ovy, ovz
+  for (int b = threadIdx.x; b < 2 * kSimHist; b += blockDim.x) s_h[b / kSimHist][b % kSimHist] = 0u;
+  if (threadIdx.x < 4) s_c[threadIdx.x] = 0ull;
+  __syncthreads();
+  const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < U) {
+    const long long k0 = lstart[l], k1 = l + 1 < U ? (long long)lstart[l + 1] : n;
+    uint32_t M[32], SL[32];
+    for (int s = 0; s < spl; ++s) {
+      M[s] = kInf;
+      SL[s] = kInf;
+    }
+    unsigned long long cnt = 0, comp = 0;
+    uint32_t lasti = 0;
+    for (long long k = k0; k < k1; ++k) {
+      const uint32_t i = sval[k];
+      const int s = sidx[i];
+      const uint32_t d = dist[i];
+      const uint32_t D = max(M[s], d);
+      for (int s2 = 0; s2 < spl; ++s2) M[s2] = max(M[s2], d);
+      M[s] = 0u;
+      SL[s] = i;
+      lasti = i;
+      const bool st = (req[i] >> kSimSecBits) & 1ull;
+      if (type == 0 || (type == 1 && st)) {
+        atomicAdd(&s_h[0][cap_bin(lines, ncap, D)], 1u);
+        ++cnt;
+        comp += D == kInf ? 1ull : 0ull;
+      }
+    }
+    if (cnt) {
+      atomicAdd(&s_c[0], cnt);
+      atomicAdd(&s_c[1], comp);
+    }
+    if (type == 2) {
+      const uint32_t dend = Ulines - cntlast[lasti] - 1u;  // lines whose last access is after this line's
+      const unsigned long long r = req[lasti];
+      const unsigned long long lkey = ((r >> 48) << 48) | ((r & ((1ull << kSimSecBits) - 1ull)) >> lspl);
+      unsigned long long oy = 0, oz = 0;
+      for (int s = 0; s < spl; ++s) {
+        if (SL[s] == kInf) continue;
+        const unsigned long long skey = ((lkey >> 48) << 48) | (((lkey & ((1ull << 48) - 1ull)) << lspl) | (unsigned)s);
+        if (!wld_has(H, whm, skey)) continue;
+        const uint32_t De = max(M[s], dend);
+        const bool isy = (long long)SL[s] >= t_y;
+        atomicAdd(&s_h[isy ? 0 : 1][cap_bin(lines, ncap, De)], 1u);
+        if (isy) ++oy;
+        else ++oz;
+      }
+      if (oy) atomicAdd(&s_c[2], oy);
+      if (oz) atomicAdd(&s_c[3], oz);
+    }
+  }
+  __syncthreads();
+  const int h0 = type == 0 ? SA_L1H : (type == 1 ? SA_L1H + kSimHist : SA_L1H + 2 * kSimHist);
+  for (int b = threadIdx.x; b <= ncap; b += blockDim.x) {
+    if (s_h[0][b]) atomicAdd(A + h0 + b, (unsigned long long)s_h[0][b]);
+    if (type == 2 && s_h[1][b]) atomicAdd(A + SA_L1H + 3 * kSimHist + b, (unsigned long long)s_h[1][b]);
+  }
+  if (threadIdx.x == 0) {
+    if (type == 0) {
+      atomicAdd(A + SA_L1REQ, s_c[0]);
+      atomicAdd(A + SA_L1COMP, s_c[1]);
+    } else if (type == 1) {
+      atomicAdd(A + SA_STREQ, s_c[0]);
+      atomicAdd(A + SA_STCOMP, s_c[1]);
+    } else {
+      atomicAdd(A + SA_OVY, s_c[2]);
+      atomicAdd(A + SA_OVZ, s_c[3]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ NEXT-1 host orchestration
 namespace {
 template <class T>
@@ -3243,6 +3574,13 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);
   // ---- host sizing of the per-stream state
   long long req_total = 0, fen_total = 0, slot_total = 0, m_total = 0;
+  // streams of >= kLongStream requests take the parallel offline path (WS_SIM_PAR: "0" = never,
+  // "all" = every stream; both paths are exact and give identical counts)
+  const char* par_env = getenv("WS_SIM_PAR");
+  const long long long_th = par_env && par_env[0] == '0' ? LLONG_MAX
+                            : (par_env && par_env[0] == 'a' ? 0 : kLongStream);
+  std::vector<DSimTrace> longs;
+  const std::vector<DSimTrace> all_tr = tr;  // every stream (the WLD sets need the wave streams)
   for (DSimTrace& T : tr) {
     if (T.n >= (1ll << 31) - 1) return cleanup(-WS_ELIMIT);
     const DGpu& G = hg[cf[T.config].gpu_id];
@@ -3251,14 +3589,20 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     if (T.type == 1) bound = std::min<long long>(bound, (long long)est[T.config].wave_lines);
     if (T.type == 2) bound = std::min<long long>(bound, (long long)est[T.config].lz_lines);
     T.hcap = pow2_at_least(std::max<long long>(2, 2 * bound));
+    req_total = std::max<long long>(req_total, T.req_off + T.n);
+    if (T.n >= long_th && T.n > 0) {
+      longs.push_back(T);
+      T.n = -1;  // marked: removed from the warp path below
+      continue;
+    }
     T.fen_off = fen_total;
     fen_total += T.n + 1;
     T.slot_off = slot_total;
     slot_total += T.hcap;
     T.m_off = m_total;
     m_total += T.hcap * spl;
-    req_total = std::max<long long>(req_total, T.req_off + T.n);
   }
+  tr.erase(std::remove_if(tr.begin(), tr.end(), [](const DSimTrace& T) { return T.n < 0; }), tr.end());
   std::vector<int64_t> wld_off(2 * (size_t)n, 0);
   long long wld_total = 0;
   for (int c = 0; c < n; ++c) {
@@ -3299,7 +3643,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   cudaMemsetAsync(S.wld, 0xff, (size_t)wld_total * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.acc, 0, (size_t)n * kSimAcc * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.counter, 0, sizeof(unsigned long long), q);
-  if (n_traces) cudaMemcpyAsync(d_tr, tr.data(), tr.size() * sizeof(DSimTrace), cudaMemcpyHostToDevice, q);
+  if (n_traces) cudaMemcpyAsync(d_tr, all_tr.data(), all_tr.size() * sizeof(DSimTrace), cudaMemcpyHostToDevice, q);
   cudaMemcpyAsync(S.wld_off, wld_off.data(), wld_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, q);
   cudaMemcpyAsync(S.lines, lines.data(), ncap * sizeof(unsigned long long), cudaMemcpyHostToDevice, q);
   cudaMemcpyAsync(d_caps, h_caps, ncap * sizeof(uint64_t), cudaMemcpyHostToDevice, q);
@@ -3314,9 +3658,95 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     cudaEventRecord(ev[1], q);
     cudaEventRecord(ev[2], q);
   }
-  if (n_traces) {
+  // warp path: the short streams
+  S.n_traces = (int64_t)tr.size();
+  if (!tr.empty()) {
+    cudaMemcpyAsync(d_tr, tr.data(), tr.size() * sizeof(DSimTrace), cudaMemcpyHostToDevice, q);
     k_sim_run<<<n_sm_dev * 4, kSimWarps * 32, 0, q>>>(s.plans, d_g, S, ncap);
     ++L;
+  }
+  // parallel path: the long streams, one after the other with device-wide kernels
+  if (!longs.empty()) {
+    long long nmax = 0, hmax = 0;
+    for (const DSimTrace& T : longs) {
+      nmax = std::max<long long>(nmax, T.n);
+      hmax = std::max<long long>(hmax, T.hcap);
+    }
+    const long long nwmax = (nmax + 63) / 64 + 1;
+    int LVmax = 1;
+    while ((1ll << LVmax) <= nmax) ++LVmax;
+    unsigned long long *H, *words;
+    uint32_t *occ, *key, *val, *key2, *val2, *V, *cur, *nxt, *zf, *bsum, *tot, *rdir, *Zs, *dist, *isl, *lst, *hist;
+    unsigned char* sidx;
+    const long long ntmax = (nmax + kRsTile - 1) / kRsTile;
+    const long long nbmax = (std::max(std::max(nmax, hmax), 256 * ntmax) + kScanB - 1) / kScanB + 1;
+    if ((rc = dmalloc(&H, (size_t)hmax, owned)) || (rc = dmalloc(&occ, (size_t)hmax, owned)) ||
+        (rc = dmalloc(&key, (size_t)nmax, owned)) || (rc = dmalloc(&val, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&key2, (size_t)nmax, owned)) || (rc = dmalloc(&val2, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&V, (size_t)nmax, owned)) || (rc = dmalloc(&cur, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&nxt, (size_t)nmax, owned)) || (rc = dmalloc(&zf, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&bsum, (size_t)nbmax, owned)) || (rc = dmalloc(&tot, 8, owned)) ||
+        (rc = dmalloc(&words, (size_t)(LVmax * nwmax), owned)) || (rc = dmalloc(&rdir, (size_t)(LVmax * nwmax), owned)) ||
+        (rc = dmalloc(&Zs, (size_t)LVmax, owned)) || (rc = dmalloc(&dist, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&isl, (size_t)nmax, owned)) || (rc = dmalloc(&lst, (size_t)nmax + 1, owned)) ||
+        (rc = dmalloc(&hist, (size_t)(256 * ntmax), owned)) || (rc = dmalloc(&sidx, (size_t)nmax, owned)))
+      return cleanup(rc);
+    auto scan = [&](uint32_t* io, long long m, uint32_t* total) {
+      const long long nb = (m + kScanB - 1) / kScanB;
+      k_ps_reduce<<<(unsigned)nb, 256, 0, q>>>(io, m, bsum);
+      k_ps_bsum<<<1, 1024, 0, q>>>(bsum, nb, total);
+      k_ps_apply<<<(unsigned)nb, 256, 0, q>>>(io, m, bsum);
+    };
+    const unsigned gridN = (unsigned)(n_sm_dev * 8);
+    for (const DSimTrace& T : longs) {
+      const DGpu& G = hg[cf[T.config].gpu_id];
+      const int lspl = G.lg_line - G.lg_sector, spl = 1 << lspl;
+      const long long nn = T.n;
+      const unsigned long long* rq = S.req + T.req_off;
+      cudaMemsetAsync(H, 0xff, (size_t)T.hcap * sizeof(unsigned long long), q);
+      k_pl_insert<<<gridN, 256, 0, q>>>(rq, nn, lspl, H, (unsigned long long)T.hcap - 1ull);
+      k_pl_occ<<<gridN, 256, 0, q>>>(H, T.hcap, occ);
+      scan(occ, T.hcap, tot);
+      uint32_t U = 0;
+      cudaMemcpyAsync(&U, tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, q);
+      if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);
+      k_pl_ids<<<gridN, 256, 0, q>>>(rq, nn, lspl, spl, H, (unsigned long long)T.hcap - 1ull, occ, key, val, sidx);
+      // stable radix sort of (line id, position) by line id
+      int bits = 1;
+      while ((1ll << bits) < (long long)U) ++bits;
+      const long long ntiles = (nn + kRsTile - 1) / kRsTile;
+      uint32_t *ka = key, *va = val, *kb = key2, *vb = val2;
+      for (int sh = 0; sh < bits; sh += 8) {
+        k_rs_hist<<<(unsigned)ntiles, 256, 0, q>>>(ka, nn, sh, hist, ntiles);
+        scan(hist, 256 * ntiles, tot + 1);
+        k_rs_scatter<<<(unsigned)ntiles, 256, 0, q>>>(ka, va, nn, sh, hist, ntiles, kb, vb);
+        std::swap(ka, kb);
+        std::swap(va, vb);
+      }
+      k_pl_prev<<<gridN, 256, 0, q>>>(ka, va, nn, V, isl, lst);
+      // wavelet matrix over V = previous access + 1
+      int LV = 1;
+      while ((1ll << LV) <= nn) ++LV;
+      const long long nw = (nn + 63) / 64 + 1;
+      cudaMemcpyAsync(cur, V, (size_t)nn * sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
+      uint32_t *c1 = cur, *c2 = nxt;
+      for (int lev = 0; lev < LV; ++lev) {
+        const int bit = LV - 1 - lev;
+        k_wm_bits<<<gridN, 256, 0, q>>>(c1, nn, bit, words + (long long)lev * nw, zf);
+        scan(zf, nn, Zs + lev);
+        k_wm_next<<<gridN, 256, 0, q>>>(c1, nn, bit, zf, Zs + lev, c2, rdir + (long long)lev * nw);
+        cudaMemcpyAsync(rdir + (long long)lev * nw + (nw - 1), Zs + lev, sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
+        if ((nn & 63) == 0)
+          cudaMemcpyAsync(rdir + (long long)lev * nw + nn / 64, Zs + lev, sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
+        std::swap(c1, c2);
+      }
+      k_pl_dist<<<gridN, 256, 0, q>>>(V, nn, LV, words, rdir, Zs, nw, dist);
+      scan(isl, nn, tot + 2);  // exclusive prefix of the last-access flags
+      k_pl_lines<<<(unsigned)((U + 127) / 128), 128, 0, q>>>(
+          va, lst, (long long)U, nn, sidx, dist, rq, isl, U, spl, lspl, T.type, T.t_y, S.wld + wld_off[2 * T.config],
+          (unsigned long long)wld_off[2 * T.config + 1] - 1ull, S.lines, ncap, S.acc + (long long)T.config * kSimAcc);
+      if ((rc = check_launch())) return cleanup(rc);
+    }
   }
   if (ev) cudaEventRecord(ev[3], q);
   k_sim_out<<<(unsigned)(((long long)n * ncap + 127) / 128), 128, 0, q>>>(s.plans, d_g, d_est, n, S.acc, ncap, d_caps,

@@ -486,3 +486,24 @@ def test_extended_space_multiblock_sets(ctx):
     sp = [c for c in W.space_extended() if c[0][0] * c[0][1] * c[0][2] <= 512][::9]
     for k in (W.k25(48), W.stencil_star(40, 36, 44, 4, regs=64)):
         assert_parity(ctx, k, dict(W.gpu_a100(), n_sm=24), sp, "ext")
+
+
+@pytest.mark.parametrize("mode", ["all", "0"])
+def test_sim_parallel_path_matches_oracle(ctx, mode):
+    """The parallel offline path (wavelet-matrix stack distances) forced on every stream, and the
+    warp path forced on every stream, both against the oracle (WS_SIM_PAR)."""
+    os.environ["WS_SIM_PAR"] = mode
+    try:
+        cases = [
+            (W.stencil_star(24, 12, 12, 4, regs=64), dict(W.gpu_a100(), n_sm=6),
+             [((8, 2, 2), (1, 1, 1), 1), ((16, 4, 1), (1, 1, 2), 0), ((4, 4, 4), (1, 2, 1), 2)]),
+            (W.lbm15(8), dict(W.gpu_a100(), n_sm=3), [((4, 2, 2), (1, 1, 1), 1), ((8, 1, 1), (1, 1, 1), 0)]),
+        ]
+        for i, (k, gp, cf) in enumerate(cases):
+            sim_parity(ctx, k, gp, cf, CAPS, f"par{mode}{i}")
+        for seed in range(4):
+            k, gp = W.random_kernel(seed, max_dom=12), W.random_gpu(seed)
+            cf = [W.random_config(seed * 10 + j) for j in range(3)]
+            sim_parity(ctx, k, gp, cf, [1 << 30, 8192, 2048, 512, 128], f"par{mode}r{seed}")
+    finally:
+        os.environ.pop("WS_SIM_PAR", None)
