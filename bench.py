@@ -399,11 +399,11 @@ def next_rows_measure(ctx, stream, args, cpu_baseline):
                              "value": n / (ms / 1e3), "unit": "configs/s", "ms_per_step": ms, "data": "synthetic",
                              "timing": "CUDA events on the context stream, graph replay, no L2 flush"}
     # ---- NEXT-1: simulated hit-rate samples
-    k, g = W.k25(40), W.gpu_a100()
+    k, g = W.k25(128), W.gpu_a100()
     kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
     space = W.space_stencil_paper()
     cf = config_array(kid, gid, space)
-    caps = [int(g["l2_bytes"] // 2 * 2 ** (e / 2)) for e in range(-12, 4, 2)]
+    caps = [int(g["l2_bytes"] // 2 * 2 ** (e / 2)) for e in range(-24, 8)][::2]
     ctx.simulate(cf[:4], caps)                      # warm-up
     ctx.profile_enable(True)
     reps = 3
@@ -415,7 +415,7 @@ def next_rows_measure(ctx, stream, args, cpu_baseline):
     prof = ctx.profile_read()
     dev_ms = (prof.get("k_simgen", (0, 0))[0] + prof.get("k_simrun", (0, 0))[0]) / reps
     req = sum(r[0]["l1_requests"] + r[0]["st_requests"] for r in rows)
-    sim = {"workload": f"3D-25pt r4 40^3, 168 configs x {len(caps)} capacities (A100 L2/2 x 2^-6..2^1.5), "
+    sim = {"workload": f"3D-25pt r4 128^3, 168 configs x {len(caps)} capacities (A100 L2/2 x 2^-12..2^3), "
                        "L1 / store / layer-set streams", "value": len(space) * len(caps) / (wall), "unit": "samples/s",
            "wall_ms_per_call": wall * 1e3, "device_ms_per_call": dev_ms,
            "kernel_ms_per_call": {k: v[0] / reps for k, v in prof.items() if v[1]},
@@ -424,7 +424,7 @@ def next_rows_measure(ctx, stream, args, cpu_baseline):
                      "CUDA events on the stream"}
     if cpu_baseline:
         from oracle import oracle as O
-        one = [space[i] for i in (0, len(space) // 2)]
+        one = [c for c in space if c[0] in ((1024, 1, 1), (512, 2, 1)) and c[1] == (1, 1, 1)]
         t0 = time.perf_counter()
         O.simulate_batch(k, g, one, caps, 2)
         dt = time.perf_counter() - t0

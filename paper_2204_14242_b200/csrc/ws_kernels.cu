@@ -3595,14 +3595,12 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
       T.n = -1;  // marked: removed from the warp path below
       continue;
     }
-    T.fen_off = fen_total;
-    fen_total += T.n + 1;
-    T.slot_off = slot_total;
-    slot_total += T.hcap;
-    T.m_off = m_total;
-    m_total += T.hcap * spl;
+    T.m_off = spl;  // sectors per line (the offsets are assigned per batch below)
   }
   tr.erase(std::remove_if(tr.begin(), tr.end(), [](const DSimTrace& T) { return T.n < 0; }), tr.end());
+  // warp-path state in batches of bounded device memory (streams are independent)
+  const long long kBatchBytes = 8ll << 30;
+  std::vector<std::pair<size_t, size_t>> batches;  // [first, last) into tr (sorted by n below)
   std::vector<int64_t> wld_off(2 * (size_t)n, 0);
   long long wld_total = 0;
   for (int c = 0; c < n; ++c) {
@@ -3612,6 +3610,30 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     wld_total += cap;
   }
   std::sort(tr.begin(), tr.end(), [](const DSimTrace& a, const DSimTrace& b) { return a.n > b.n; });
+  {
+    size_t first = 0;
+    long long fen_b = 0, slot_b = 0, m_b = 0;
+    for (size_t t = 0; t < tr.size(); ++t) {
+      DSimTrace& T = tr[t];
+      const long long spl = T.m_off;
+      const long long bytes = (T.n + 1) * 4 + T.hcap * 12 + T.hcap * spl * 8;
+      if (t > first && (fen_b + T.n + 1) * 4 + slot_b * 12 + m_b * 8 + bytes > kBatchBytes) {
+        batches.push_back({first, t});
+        first = t;
+        fen_b = slot_b = m_b = 0;
+      }
+      T.fen_off = fen_b;
+      fen_b += T.n + 1;
+      T.slot_off = slot_b;
+      slot_b += T.hcap;
+      T.m_off = m_b;
+      m_b += T.hcap * spl;
+      fen_total = std::max(fen_total, fen_b);
+      slot_total = std::max(slot_total, slot_b);
+      m_total = std::max(m_total, m_b);
+    }
+    if (first < tr.size()) batches.push_back({first, tr.size()});
+  }
   // capacities: ascending, in lines (every GPU of the batch shares line_bytes? no: per record below)
   std::vector<int> idx(ncap);
   for (int k = 0; k < ncap; ++k) idx[k] = k;
@@ -3638,8 +3660,6 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   S.n_traces = n_traces;
   ws_sim_result* d_out;
   if ((rc = dmalloc(&d_out, (size_t)n * ncap, owned))) return cleanup(rc);
-  cudaMemsetAsync(S.fen, 0, (size_t)fen_total * sizeof(uint32_t), q);
-  cudaMemsetAsync(S.keys, 0xff, (size_t)slot_total * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.wld, 0xff, (size_t)wld_total * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.acc, 0, (size_t)n * kSimAcc * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.counter, 0, sizeof(unsigned long long), q);
@@ -3658,12 +3678,16 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     cudaEventRecord(ev[1], q);
     cudaEventRecord(ev[2], q);
   }
-  // warp path: the short streams
-  S.n_traces = (int64_t)tr.size();
-  if (!tr.empty()) {
-    cudaMemcpyAsync(d_tr, tr.data(), tr.size() * sizeof(DSimTrace), cudaMemcpyHostToDevice, q);
+  // warp path: the short streams, batch by batch
+  for (const auto& bt : batches) {
+    S.n_traces = (int64_t)(bt.second - bt.first);
+    cudaMemsetAsync(S.fen, 0, (size_t)fen_total * sizeof(uint32_t), q);
+    cudaMemsetAsync(S.keys, 0xff, (size_t)slot_total * sizeof(unsigned long long), q);
+    cudaMemsetAsync(S.counter, 0, sizeof(unsigned long long), q);
+    cudaMemcpyAsync(d_tr, tr.data() + bt.first, (size_t)S.n_traces * sizeof(DSimTrace), cudaMemcpyHostToDevice, q);
     k_sim_run<<<n_sm_dev * 4, kSimWarps * 32, 0, q>>>(s.plans, d_g, S, ncap);
     ++L;
+    if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);  // the host copy of tr is reused
   }
   // parallel path: the long streams, one after the other with device-wide kernels
   if (!longs.empty()) {

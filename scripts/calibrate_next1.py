@@ -22,14 +22,16 @@ sys.path.insert(0, os.path.join(ROOT, "scripts"))
 import workloads as W  # noqa: E402
 import validate_next2 as V  # noqa: E402
 
+NCAL = int(os.environ.get("WS_CAL_N", "128"))   # grid of the simulated calibration sweep
+
 
 def main(prefix):
     from paper_2204_14242_b200 import Context, config_array
     ctx = Context(0)
     g = V.b200_params()
-    k = W.stencil_star(128, 128, 128, 4, regs=V.REGS)
+    k = W.stencil_star(NCAL, NCAL, NCAL, 4, regs=V.REGS)
     space = W.space_stencil_paper()
-    caps = [1 << e for e in range(14, 26)]
+    caps = [1 << e for e in range(14, 26)] if NCAL <= 128 else [1 << e for e in range(16, 28)]
     cf = config_array(ctx.describe_kernel(k), ctx.describe_gpu(g), space)
     t0 = time.time()
     rows = ctx.simulate(cf, caps)
@@ -49,7 +51,7 @@ def main(prefix):
         fits.append(abc)
         info[name] = {"abc": abc, "samples": len(Os), "rss": rss,
                       "R_at_O": {o: W_hit(abc, o) for o in (0.5, 1.0, 2.0, 4.0)}}
-    out = {"workload": "25pt 168 configs at 128^3, B200 parameters, capacities 16 KiB..32 MiB (12)",
+    out = {"workload": f"25pt 168 configs at {NCAL}^3, B200 parameters, capacities {caps[0]}..{caps[-1]} B ({len(caps)})",
            "simulate_wall_s": sim_s, "curves": info}
     res = V.analyze(os.path.join(ROOT, "profiles", "r01_next2_times.json"),
                     os.path.join(ROOT, "profiles", "r01_next2_ncu.csv"), prefix + "_validation", hit_abc=fits,
