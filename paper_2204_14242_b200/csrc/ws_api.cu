@@ -42,6 +42,7 @@ struct ws_ctx {
   struct Rec {
     int first_kind, n;
     std::vector<cudaEvent_t> ev;
+    uint32_t skip = 0;  // kinds (bit i = first_kind + i) whose events this call never records
   };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> free_ev;
@@ -265,6 +266,7 @@ ws_status ws_profile_read(ws_ctx* c, double* ms, uint64_t* launches, uint32_t ca
   ws_status st = WS_OK;
   for (auto& r : c->pending) {
     for (int i = 0; i < r.n; ++i) {
+      if ((r.skip >> i) & 1u) continue;
       float t = 0.f;
       cudaError_t e = cudaEventSynchronize(r.ev[2 * i + 1]);
       if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.ev[2 * i], r.ev[2 * i + 1]);
@@ -457,6 +459,7 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   Scratch S;
   if ((s = ensure_scratch(c, n, S)) != WS_OK) return s;
   cudaEvent_t* ev = c->profiling ? c->take_events(K_PLAN, kEstimateKernels) : nullptr;
+  if (ev) c->pending.back().skip = 1u << (K_SCAN - K_PLAN);  // folded into k_plan
   Streams st;
   st.main = c->stream;
   // WS_SERIAL=1 (diagnostics): every chain on the context stream -> uncontended kernel times
