@@ -398,6 +398,26 @@ def next_rows_measure(ctx, stream, args, cpu_baseline):
     out["extended_space"] = {"workload": f"3D-25pt r4 512^3, extended space (SURVEY Q34), {n} configs, A100 parameters",
                              "value": n / (ms / 1e3), "unit": "configs/s", "ms_per_step": ms, "data": "synthetic",
                              "timing": "CUDA events on the context stream, graph replay, no L2 flush"}
+    # ---- BJ configs[2]: the LBM kernels (LBM15 = the paper's D3Q15 + phase field, LBM27 = D3Q27
+    # with the D3Q27 phase-field stencil), 256^3, the 49 shapes of 512 threads, A100 parameters
+    for name, kk in (("configs2_lbm15", W.lbm15(256)), ("configs2_lbm27", W.lbm27(256))):
+        kid, gid = ctx.describe_kernel(kk), ctx.describe_gpu(W.gpu_a100())
+        cf = config_array(kid, gid, W.space_lbm())
+        n = len(cf)
+        d_cfg = torch.from_numpy(cf.view(np.uint8).copy()).cuda()
+        d_out = torch.empty(n * 336, dtype=torch.uint8, device="cuda")
+        for _ in range(2):
+            ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(20):
+            ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        out[name] = {"workload": f"{name[9:].upper()} 256^3, 49 configs (P:730), A100 parameters", "value": n / (ms / 1e3),
+                     "unit": "configs/s", "ms_per_step": ms, "data": "synthetic",
+                     "timing": "CUDA events on the context stream, graph replay, no L2 flush"}
     # ---- NEXT-1: simulated hit-rate samples
     k, g = W.k25(128), W.gpu_a100()
     kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(g)
