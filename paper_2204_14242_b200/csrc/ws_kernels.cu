@@ -1884,6 +1884,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
   unsigned long long my_ops = 0;
   int ranges_c = -1;
   int c = -1;
+  int rra[5] = {0, 0, 0, 0, 0}, rrl[5] = {0, 0, 0, 0, 0};
   for (long long item = (long long)blockIdx.x * kRowWarps + wid; item < total; item += nwg) {
     c = find_config_warp<4>(pre, n, item, c);
     const DPlan& P = plans[c];
@@ -1945,6 +1946,11 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       if (lane < 20) X.bnd[lane] = (int)P.bnd[lane];
       __syncwarp();
       ranges_c = c;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {  // block-row span of each range in registers (empty: ra > rl)
+        rra[q] = P.rng[q].nonempty ? (int)P.rng[q].ra : 0x7fffffff;
+        rrl[q] = P.rng[q].nonempty ? (int)P.rng[q].rl : -0x7fffffff;
+      }
     }
     const int nb = P.nb;
     const long long R0p = falign + ((py * y0 + pz * z) << le);
@@ -2014,8 +2020,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
             if (zz < lo2 || zz >= hi2 || yy < lo1 || yy >= hi1) continue;
             const int r = fdiv32(yy - lo1, fdy) + Gy * fdiv32(zz - lo2, fdz);
 #pragma unroll
-            for (int q = 0; q < 5; ++q) {
-              const int ty = classify32(X.r[q], r);
+            for (int q = 0; q < 5; ++q) {  // classify32 from registers
+              const int ty = (r < rra[q] || r > rrl[q]) ? -1
+                             : (rra[q] == rrl[q] ? 3 : (r == rra[q] ? 1 : (r == rrl[q] ? 2 : 0)));
               if (ty >= 0) {
                 const unsigned long long bit = 1ull << (ty * 16 + gr.run);
                 if (gr.kind) mS[q] |= bit;
