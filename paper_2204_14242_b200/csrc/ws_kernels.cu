@@ -1483,22 +1483,23 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
         }
       }
       __syncthreads();
-      // (c) ordered fold, warp 0: a derived plane is its computed source plane (p - m*per, the
-      //     nearest non-derived one) translated by m*per planes; lanes take contiguous planes.
-      if (wid == 0) {
-        const int ppl = (np + 31) >> 5;
-        Tri ts = tri_empty(), tl = tri_empty();
-        for (int p = lane * ppl; p < np && p < (lane + 1) * ppl; ++p) {
+      // (c) ordered fold by the whole CTA: a derived plane is its computed source plane (p - m*per,
+      //     the nearest non-derived one) translated by m*per planes; threads take contiguous planes,
+      //     then an ordered CTA reduction
+      {
+        const int ppl = (np + (int)blockDim.x - 1) / (int)blockDim.x;
+        Tri t2[2] = {tri_empty(), tri_empty()};
+        for (int p = tid * ppl; p < np && p < (tid + 1) * ppl; ++p) {
           int q = p;
           while (pder[q]) q -= per;
           const long long dsh = (long long)(p - q) * pbytes;
           const Tri a = pt[2 * q], b = pt[2 * q + 1];
-          ts = tri_combine(ts, a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty());
-          tl = tri_combine(tl, b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty());
+          t2[0] = tri_combine(t2[0], a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty());
+          t2[1] = tri_combine(t2[1], b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty());
         }
-        Tri t2[2] = {ts, tl};
-        warp_ordered_reduce<2>(t2);
-        if (lane == 0) {
+        __shared__ Tri s_fold[(256 / 32) * 2];
+        cta_ordered_reduce<2>(t2, s_fold);
+        if (tid == 0) {
           cs_all = tri_combine(cs_all, t2[0]);
           cl_all = tri_combine(cl_all, t2[1]);
         }
