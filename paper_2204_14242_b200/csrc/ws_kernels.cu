@@ -1892,13 +1892,20 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
     const long long ci = item - pre[c].chunk;
-    int fi = 0;
-    for (int f2 = 0; f2 < K.n_fields; ++f2) {
-      const DRowInfo& r2 = rowinfo[(long long)c * kMaxFields + f2];
-      if (ci >= r2.chunk_begin && ci < r2.chunk_begin + r2.n_chunks) {
-        fi = f2;
-        break;
+    // the field whose chunk range holds ci: chunk_begin ascends with the field index (fields
+    // without chunks repeat their successor's begin), so the last field with begin <= ci and a
+    // nonempty range -- binary search for the last begin <= ci, then skip empty ranges backwards
+    int fi;
+    {
+      const DRowInfo* ri0 = rowinfo + (long long)c * kMaxFields;
+      int lo = 0, hi = K.n_fields - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ri0[mid].chunk_begin <= ci) lo = mid;
+        else hi = mid - 1;
       }
+      while (lo > 0 && !(ci < ri0[lo].chunk_begin + ri0[lo].n_chunks)) --lo;
+      fi = lo;
     }
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const DField& F = K.f[fi];
