@@ -2084,18 +2084,14 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
   if (lane == 0 && my_ops) atomicAdd(work + K_ROWS, my_ops);
 }
 
-// Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
-// plane (count slot = -(representative index) - 2) takes its representative's triple
-// translated by the plane distance (a multiple of the reuse period: whole lines).
-__global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
-                                              const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
-                                              const DRowInfo* __restrict__ rowinfo,
-                                              const long long* __restrict__ chunkres,
-                                              unsigned long long* __restrict__ acc) {
+// one CTA per (config, field): threads take contiguous planes, ordered CTA reduction
+__device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                         const DKernel* __restrict__ ks, const DGpu* __restrict__ gs, const DRowInfo* __restrict__ rowinfo,
+                         const long long* __restrict__ chunkres, unsigned long long* __restrict__ acc) {
   __shared__ Tri s_red[(256 / 32) * kNQ];
   const long long total = pre[n].fold;
   const int tid = threadIdx.x;
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {  // one CTA per (config, field)
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
     const int c = find_config<5>(pre, n, item);
     const int fi = (int)(item - pre[c].fold);
     const DPlan& P = plans[c];
@@ -2115,7 +2111,7 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
     for (long long k = tid * per_l; k < nch && k < (tid + 1) * per_l; ++k) {
       long long src = k;
       const long long mk = base[k * (kNQ * 3) + 2];
-      if (mk < 0) src = -mk - 2;  // derived plane: representative plane index
+      if (mk < 0) src = -mk - 2;
       const long long* in = base + src * (kNQ * 3);
       const long long dbytes = (k - src) * pbytes;
 #pragma unroll
@@ -2127,6 +2123,68 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
     }
     cta_ordered_reduce<kNQ>(t, s_red);
     if (tid == 0 && nch > 0) {
+      unsigned long long* a = acc + (long long)c * A_N;
+      atomicAdd(a + A_WLD, (unsigned long long)t[0].c);
+      atomicAdd(a + A_WST, (unsigned long long)t[1].c);
+      atomicAdd(a + A_WLIN, (unsigned long long)t[2].c);
+      atomicAdd(a + A_LY, (unsigned long long)t[4].c);
+      atomicAdd(a + A_LZ, (unsigned long long)t[6].c);
+      atomicAdd(a + A_OVY, (unsigned long long)(t[0].c + t[3].c - t[7].c));
+      atomicAdd(a + A_OVZ, (unsigned long long)(t[0].c + t[5].c - t[8].c));
+    }
+  }
+}
+
+// Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
+// plane (count slot = -(representative index) - 2) takes its representative's triple
+// translated by the plane distance (a multiple of the reuse period: whole lines).
+__global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+                                              const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                              const DRowInfo* __restrict__ rowinfo,
+                                              const long long* __restrict__ chunkres,
+                                              unsigned long long* __restrict__ acc) {
+  const long long total = pre[n].fold;
+  const int lane = threadIdx.x & 31;
+  // few items with many planes each (BJ configs[1]: 336 items x ~520 planes): one CTA per item;
+  // many items (LBM: 58 fields per config): one warp per item
+  if (total > 0 && pre[n].chunk / total > 256) {
+    fold_cta(plans, pre, n, ks, gs, rowinfo, chunkres, acc);
+    return;
+  }
+  const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
+  // one warp per (config, field): lanes take contiguous planes, ordered warp reduction
+  for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nwg) {
+    const int c = find_config<5>(pre, n, item);
+    const int fi = (int)(item - pre[c].fold);
+    const DPlan& P = plans[c];
+    const DField& F = ks[P.kid].f[fi];
+    const DGpu& G = gs[P.gid];
+    const int ls = G.lg_sector, ll = G.lg_line;
+    long long py, pz, falign;
+    field_rows(F, P, ll, py, pz, falign);
+    const long long pbytes = pz << F.lg_elem;
+    const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
+    const long long nch = RI.n_chunks;
+    const long long per_l = (nch + 31) / 32;
+    const long long* base = chunkres + (pre[c].chunk + RI.chunk_begin) * (kNQ * 3);
+    Tri t[kNQ];
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
+    for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
+      long long src = k;
+      const long long mk = base[k * (kNQ * 3) + 2];
+      if (mk < 0) src = -mk - 2;  // derived plane: representative plane index
+      const long long* in = base + src * (kNQ * 3);
+      const long long dbytes = (k - src) * pbytes;
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        const long long d = dbytes >> ((q == 2 || q == 4 || q == 6) ? ll : ls);
+        const long long cq = in[q * 3 + 2];
+        t[q] = tri_combine(t[q], cq ? Tri{in[q * 3] + d, in[q * 3 + 1] + d, cq} : tri_empty());
+      }
+    }
+    warp_ordered_reduce<kNQ>(t);
+    if (lane == 0 && nch > 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_WLD, (unsigned long long)t[0].c);
       atomicAdd(a + A_WST, (unsigned long long)t[1].c);
