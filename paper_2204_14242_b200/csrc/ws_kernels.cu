@@ -3498,14 +3498,18 @@ __global__ void k_pl_dist(const uint32_t* __restrict__ V, long long n, int LV, c
 // one thread per line: walk its accesses in time order (per-sector running maxima), histogram the
 // counted requests; the layer stream's end state of the overlap sectors
 __global__ void __launch_bounds__(128) k_pl_lines(const uint32_t* __restrict__ sval, const uint32_t* __restrict__ lstart,
-                                                  long long U, long long n, const unsigned char* __restrict__ sidx,
+                                                  const uint32_t* __restrict__ Uptr, long long n,
+                                                  const unsigned char* __restrict__ sidx,
                                                   const uint32_t* __restrict__ dist, const unsigned long long* __restrict__ req,
-                                                  const uint32_t* __restrict__ cntlast, uint32_t Ulines, int spl, int lspl,
+                                                  const uint32_t* __restrict__ cntlast, int spl, int lspl,
                                                   int type, long long t_y, const unsigned long long* __restrict__ H,
                                                   unsigned long long whm, const unsigned long long* __restrict__ lines,
                                                   int ncap, unsigned long long* __restrict__ A) {
   __shared__ unsigned s_h[2][kSimHist];
   __shared__ unsigned long long s_c[4];  // counted, compulsory, ovy, ovz
+  const long long U = *Uptr;
+  const uint32_t Ulines = (uint32_t)U;
+  if ((long long)blockIdx.x * blockDim.x >= U) return;  // grid sized by an upper bound of U
   for (int b = threadIdx.x; b < 2 * kSimHist; b += blockDim.x) s_h[b / kSimHist][b % kSimHist] = 0u;
   if (threadIdx.x < 4) s_c[threadIdx.x] = 0ull;
   __syncthreads();
@@ -3650,8 +3654,9 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   // streams of >= kLongStream requests take the parallel offline path (WS_SIM_PAR: "0" = never,
   // "all" = every stream; both paths are exact and give identical counts)
   const char* par_env = getenv("WS_SIM_PAR");
+  const char* th_env = getenv("WS_SIM_LONG");  // threshold override (requests), for tuning
   const long long long_th = par_env && par_env[0] == '0' ? LLONG_MAX
-                            : (par_env && par_env[0] == 'a' ? 0 : kLongStream);
+                            : (par_env && par_env[0] == 'a' ? 0 : (th_env ? atoll(th_env) : kLongStream));
   std::vector<DSimTrace> longs;
   const std::vector<DSimTrace> all_tr = tr;  // every stream (the WLD sets need the wave streams)
   for (DSimTrace& T : tr) {
@@ -3803,14 +3808,12 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
       cudaMemsetAsync(H, 0xff, (size_t)T.hcap * sizeof(unsigned long long), q);
       k_pl_insert<<<gridN, 256, 0, q>>>(rq, nn, lspl, H, (unsigned long long)T.hcap - 1ull);
       k_pl_occ<<<gridN, 256, 0, q>>>(H, T.hcap, occ);
-      scan(occ, T.hcap, tot);
-      uint32_t U = 0;
-      cudaMemcpyAsync(&U, tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, q);
-      if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);
+      scan(occ, T.hcap, tot);  // tot[0] = distinct lines U (stays on the device: no host sync)
+      const long long Ubound = T.hcap / 2;  // hcap >= 2 * (an upper bound of U)
       k_pl_ids<<<gridN, 256, 0, q>>>(rq, nn, lspl, spl, H, (unsigned long long)T.hcap - 1ull, occ, key, val, sidx);
       // stable radix sort of (line id, position) by line id
       int bits = 1;
-      while ((1ll << bits) < (long long)U) ++bits;
+      while ((1ll << bits) < Ubound) ++bits;
       const long long ntiles = (nn + kRsTile - 1) / kRsTile;
       uint32_t *ka = key, *va = val, *kb = key2, *vb = val2;
       for (int sh = 0; sh < bits; sh += 8) {
@@ -3839,8 +3842,8 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
       }
       k_pl_dist<<<gridN, 256, 0, q>>>(V, nn, LV, words, rdir, Zs, nw, dist);
       scan(isl, nn, tot + 2);  // exclusive prefix of the last-access flags
-      k_pl_lines<<<(unsigned)((U + 127) / 128), 128, 0, q>>>(
-          va, lst, (long long)U, nn, sidx, dist, rq, isl, U, spl, lspl, T.type, T.t_y, S.wld + wld_off[2 * T.config],
+      k_pl_lines<<<(unsigned)((Ubound + 127) / 128), 128, 0, q>>>(
+          va, lst, tot, nn, sidx, dist, rq, isl, spl, lspl, T.type, T.t_y, S.wld + wld_off[2 * T.config],
           (unsigned long long)wld_off[2 * T.config + 1] - 1ull, S.lines, ncap, S.acc + (long long)T.config * kSimAcc);
       if ((rc = check_launch())) return cleanup(rc);
     }
