@@ -3257,7 +3257,7 @@ __global__ void __launch_bounds__(256) k_fit(const double* __restrict__ O, const
 // has p(j) < j) counted with a wavelet matrix over p(j) + 1, then one thread per line walks its
 // accesses in time order with the per-sector running maxima D (as the warp path), histogramming
 // the counted requests and, for the layer stream, the end state of the overlap sectors.
-constexpr long long kLongStream = 1 << 18;
+constexpr long long kLongStream = 1 << 16;
 constexpr int kScanB = 1024;  // elements per block of the device-wide scans
 
 __global__ void __launch_bounds__(256) k_ps_reduce(const uint32_t* __restrict__ in, long long m, uint32_t* __restrict__ bsum) {
@@ -3436,27 +3436,32 @@ __global__ void k_pl_prev(const uint32_t* __restrict__ skey, const uint32_t* __r
 }
 // one wavelet-matrix level: the bit of every value (64-bit words, one ballot pair per warp) and
 // the zero flags for the scan
+// (the zeros of every word go to wz: their exclusive scan over the words is the rank directory)
 __global__ void k_wm_bits(const uint32_t* __restrict__ cur, long long n, int bit, unsigned long long* __restrict__ words,
-                          uint32_t* __restrict__ zf) {
+                          uint32_t* __restrict__ wz) {
   const int lane = threadIdx.x & 31;
   const long long nw = (n + 63) / 64;
   for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
        w += ((long long)gridDim.x * blockDim.x) >> 5) {
     const long long i0 = w * 64 + lane, i1 = i0 + 32;
     const uint32_t b0 = i0 < n ? (cur[i0] >> bit) & 1u : 0u, b1 = i1 < n ? (cur[i1] >> bit) & 1u : 0u;
-    if (i0 < n) zf[i0] = 1u - b0;
-    if (i1 < n) zf[i1] = 1u - b1;
+    const unsigned z0 = __ballot_sync(FULL, i0 < n && !b0), z1 = __ballot_sync(FULL, i1 < n && !b1);
     const unsigned lo = __ballot_sync(FULL, b0), hi = __ballot_sync(FULL, b1);
-    if (lane == 0) words[w] = ((unsigned long long)hi << 32) | lo;
+    if (lane == 0) {
+      words[w] = ((unsigned long long)hi << 32) | lo;
+      wz[w] = (uint32_t)(__popc(z0) + __popc(z1));
+    }
   }
 }
-__global__ void k_wm_next(const uint32_t* __restrict__ cur, long long n, int bit, const uint32_t* __restrict__ zpos,
-                          const uint32_t* __restrict__ Z, uint32_t* __restrict__ nxt, uint32_t* __restrict__ rdir) {
+__global__ void k_wm_next(const uint32_t* __restrict__ cur, long long n, int bit,
+                          const unsigned long long* __restrict__ words, const uint32_t* __restrict__ rdir,
+                          const uint32_t* __restrict__ Z, uint32_t* __restrict__ nxt) {
+  const uint32_t Zv = *Z;
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
     const uint32_t v = cur[j];
-    const uint32_t zp = zpos[j];
-    nxt[((v >> bit) & 1u) ? *Z + (uint32_t)j - zp : zp] = v;
-    if ((j & 63) == 0) rdir[j >> 6] = zp;   // zeros before this word
+    const int r = (int)(j & 63);
+    const uint32_t zp = rdir[j >> 6] + (r ? (uint32_t)__popcll(~words[j >> 6] & ((1ull << r) - 1ull)) : 0u);
+    nxt[((v >> bit) & 1u) ? Zv + (uint32_t)j - zp : zp] = v;
   }
 }
 __device__ __forceinline__ uint32_t wm_rank0(const unsigned long long* words, const uint32_t* rdir, long long pos) {
@@ -3582,6 +3587,174 @@ __global__ void __launch_bounds__(128) k_pl_lines(const uint32_t* __restrict__ s
   }
 }
 
+
+// ---- batched long streams: several long streams concatenated (positions are global; the stack
+// distance formula is invariant under the shift, and every quantity that must stay per stream --
+// line ids, the end state -- is keyed by the stream)
+struct DPB {
+  int64_t req_off, n, start, hoff, hcap, t_y_abs, wld_off, wld_cap;
+  int32_t type, config, spl, lspl;
+};
+
+__global__ void k_pb_gather(const unsigned long long* __restrict__ req, const DPB* __restrict__ pb,
+                            unsigned long long* __restrict__ cat, uint32_t* __restrict__ tid) {
+  const DPB T = pb[blockIdx.y];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (long long)gridDim.x * blockDim.x) {
+    cat[T.start + i] = req[T.req_off + i];
+    tid[T.start + i] = blockIdx.y;
+  }
+}
+__global__ void k_pb_insert(const unsigned long long* __restrict__ cat, const uint32_t* __restrict__ tid, long long n,
+                            const DPB* __restrict__ pb, unsigned long long* __restrict__ H) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const DPB& T = pb[tid[i]];
+    const unsigned long long r = cat[i];
+    const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
+    const unsigned long long lkey = ((r >> 48) << 48) | (sb >> T.lspl);
+    unsigned long long* R = H + T.hoff;
+    const unsigned long long hm = (unsigned long long)T.hcap - 1ull;
+    unsigned long long h = sim_hash(lkey) & hm;
+    for (;;) {
+      const unsigned long long old = atomicCAS(&R[h], kEmpty, lkey);
+      if (old == kEmpty || old == lkey) break;
+      h = (h + 1) & hm;
+    }
+  }
+}
+__global__ void k_pb_ids(const unsigned long long* __restrict__ cat, const uint32_t* __restrict__ tid, long long n,
+                         const DPB* __restrict__ pb, const unsigned long long* __restrict__ H,
+                         const uint32_t* __restrict__ occ, uint32_t* __restrict__ key, uint32_t* __restrict__ val,
+                         unsigned char* __restrict__ sidx) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const DPB& T = pb[tid[i]];
+    const unsigned long long r = cat[i];
+    const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
+    const unsigned long long lkey = ((r >> 48) << 48) | (sb >> T.lspl);
+    const unsigned long long* R = H + T.hoff;
+    const unsigned long long hm = (unsigned long long)T.hcap - 1ull;
+    unsigned long long h = sim_hash(lkey) & hm;
+    while (R[h] != lkey) h = (h + 1) & hm;
+    key[i] = occ[T.hoff + h];  // dense id, grouped by stream (regions in stream order)
+    val[i] = (uint32_t)i;
+    sidx[i] = (unsigned char)(sb & (unsigned long long)(T.spl - 1));
+  }
+}
+// one thread per line of the batch (ids grouped by stream): per-sector running maxima, the
+// counted requests' histograms, the layer stream's end state.  Histograms of the CTA's first
+// stream accumulate in shared memory, lines of other streams add to global memory directly.
+__global__ void __launch_bounds__(128) k_pb_lines(const uint32_t* __restrict__ sval, const uint32_t* __restrict__ lstart,
+                                                  const uint32_t* __restrict__ Uptr, long long n,
+                                                  const unsigned char* __restrict__ sidx, const uint32_t* __restrict__ dist,
+                                                  const unsigned long long* __restrict__ cat, const uint32_t* __restrict__ tid,
+                                                  const uint32_t* __restrict__ cntlast, const DPB* __restrict__ pb,
+                                                  const unsigned long long* __restrict__ wld,
+                                                  const unsigned long long* __restrict__ lines, int ncap,
+                                                  unsigned long long* __restrict__ acc) {
+  __shared__ unsigned s_h[2][kSimHist];
+  __shared__ unsigned long long s_c[4];
+  __shared__ int s_t;
+  const long long U = *Uptr;
+  if ((long long)blockIdx.x * blockDim.x >= U) return;
+  for (int b = threadIdx.x; b < 2 * kSimHist; b += blockDim.x) s_h[b / kSimHist][b % kSimHist] = 0u;
+  if (threadIdx.x < 4) s_c[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) s_t = (int)tid[sval[lstart[(long long)blockIdx.x * blockDim.x]]];
+  __syncthreads();
+  const int ct = s_t;
+  const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < U) {
+    const long long k0 = lstart[l], k1 = l + 1 < U ? (long long)lstart[l + 1] : n;
+    const int t = (int)tid[sval[k0]];
+    const DPB& T = pb[t];
+    const bool local = t == ct;
+    unsigned long long* A = acc + (long long)T.config * kSimAcc;
+    const int spl = T.spl, lspl = T.lspl, type = T.type;
+    const int h0 = type == 0 ? SA_L1H : (type == 1 ? SA_L1H + kSimHist : SA_L1H + 2 * kSimHist);
+    uint32_t M[32], SL[32];
+    for (int s = 0; s < spl; ++s) {
+      M[s] = kInf;
+      SL[s] = kInf;
+    }
+    unsigned long long cnt = 0, comp = 0;
+    uint32_t lasti = 0;
+    for (long long k = k0; k < k1; ++k) {
+      const uint32_t i = sval[k];
+      const int s = sidx[i];
+      const uint32_t d = dist[i];
+      const uint32_t D = max(M[s], d);
+      for (int s2 = 0; s2 < spl; ++s2) M[s2] = max(M[s2], d);
+      M[s] = 0u;
+      SL[s] = i;
+      lasti = i;
+      const bool st = (cat[i] >> kSimSecBits) & 1ull;
+      if (type == 0 || (type == 1 && st)) {
+        const int bin = cap_bin(lines, ncap, D);
+        if (local) atomicAdd(&s_h[0][bin], 1u);
+        else atomicAdd(A + h0 + bin, 1ull);
+        ++cnt;
+        comp += D == kInf ? 1ull : 0ull;
+      }
+    }
+    if (cnt) {
+      if (local) {
+        atomicAdd(&s_c[0], cnt);
+        atomicAdd(&s_c[1], comp);
+      } else {
+        atomicAdd(A + (type == 0 ? SA_L1REQ : SA_STREQ), cnt);
+        atomicAdd(A + (type == 0 ? SA_L1COMP : SA_STCOMP), comp);
+      }
+    }
+    if (type == 2) {
+      // lines of this stream whose last access is after this line's
+      const uint32_t dend = cntlast[T.start + T.n] - cntlast[lasti] - 1u;
+      const unsigned long long r = cat[lasti];
+      const unsigned long long lkey = ((r >> 48) << 48) | ((r & ((1ull << kSimSecBits) - 1ull)) >> lspl);
+      const unsigned long long* Hw = wld + T.wld_off;
+      const unsigned long long whm = (unsigned long long)T.wld_cap - 1ull;
+      unsigned long long oy = 0, oz = 0;
+      for (int s = 0; s < spl; ++s) {
+        if (SL[s] == kInf) continue;
+        const unsigned long long skey = ((lkey >> 48) << 48) | (((lkey & ((1ull << 48) - 1ull)) << lspl) | (unsigned)s);
+        if (!wld_has(Hw, whm, skey)) continue;
+        const uint32_t De = max(M[s], dend);
+        const bool isy = (long long)SL[s] >= T.t_y_abs;
+        const int bin = cap_bin(lines, ncap, De);
+        if (local) atomicAdd(&s_h[isy ? 0 : 1][bin], 1u);
+        else atomicAdd(A + SA_L1H + (isy ? 2 : 3) * kSimHist + bin, 1ull);
+        if (isy) ++oy;
+        else ++oz;
+      }
+      if (local) {
+        if (oy) atomicAdd(&s_c[2], oy);
+        if (oz) atomicAdd(&s_c[3], oz);
+      } else {
+        if (oy) atomicAdd(A + SA_OVY, oy);
+        if (oz) atomicAdd(A + SA_OVZ, oz);
+      }
+    }
+  }
+  __syncthreads();
+  const DPB& T = pb[ct];
+  unsigned long long* A = acc + (long long)T.config * kSimAcc;
+  const int type = T.type;
+  const int h0 = type == 0 ? SA_L1H : (type == 1 ? SA_L1H + kSimHist : SA_L1H + 2 * kSimHist);
+  for (int b = threadIdx.x; b <= ncap; b += blockDim.x) {
+    if (s_h[0][b]) atomicAdd(A + h0 + b, (unsigned long long)s_h[0][b]);
+    if (type == 2 && s_h[1][b]) atomicAdd(A + SA_L1H + 3 * kSimHist + b, (unsigned long long)s_h[1][b]);
+  }
+  if (threadIdx.x == 0) {
+    if (type == 0) {
+      if (s_c[0]) atomicAdd(A + SA_L1REQ, s_c[0]);
+      if (s_c[1]) atomicAdd(A + SA_L1COMP, s_c[1]);
+    } else if (type == 1) {
+      if (s_c[0]) atomicAdd(A + SA_STREQ, s_c[0]);
+      if (s_c[1]) atomicAdd(A + SA_STCOMP, s_c[1]);
+    } else {
+      if (s_c[2]) atomicAdd(A + SA_OVY, s_c[2]);
+      if (s_c[3]) atomicAdd(A + SA_OVZ, s_c[3]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ NEXT-1 host orchestration
 namespace {
 template <class T>
@@ -3677,7 +3850,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   }
   tr.erase(std::remove_if(tr.begin(), tr.end(), [](const DSimTrace& T) { return T.n < 0; }), tr.end());
   // warp-path state in batches of bounded device memory (streams are independent)
-  const long long kBatchBytes = 8ll << 30;
+  const long long kBatchBytes = 24ll << 30;
   std::vector<std::pair<size_t, size_t>> batches;  // [first, last) into tr (sorted by n below)
   std::vector<int64_t> wld_off(2 * (size_t)n, 0);
   long long wld_total = 0;
@@ -3767,21 +3940,43 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     ++L;
     if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);  // the host copy of tr is reused
   }
-  // parallel path: the long streams, one after the other with device-wide kernels
+  // parallel path: the long streams, concatenated in batches (positions < 2^31), device-wide kernels
   if (!longs.empty()) {
+    std::vector<std::pair<size_t, size_t>> pbat;
+    {
+      size_t first = 0;
+      long long tot_n = 0;
+      for (size_t t = 0; t < longs.size(); ++t) {
+        if (t > first && (tot_n + longs[t].n >= (1ll << 31) - 2 || t - first >= 4096)) {
+          pbat.push_back({first, t});
+          first = t;
+          tot_n = 0;
+        }
+        tot_n += longs[t].n;
+      }
+      pbat.push_back({first, longs.size()});
+    }
     long long nmax = 0, hmax = 0;
-    for (const DSimTrace& T : longs) {
-      nmax = std::max<long long>(nmax, T.n);
-      hmax = std::max<long long>(hmax, T.hcap);
+    size_t tmax = 0;
+    for (const auto& bt : pbat) {
+      long long nb = 0, hb = 0;
+      for (size_t t = bt.first; t < bt.second; ++t) {
+        nb += longs[t].n;
+        hb += longs[t].hcap;
+      }
+      nmax = std::max<long long>(nmax, nb);
+      hmax = std::max<long long>(hmax, hb);
+      tmax = std::max<size_t>(tmax, bt.second - bt.first);
     }
     const long long nwmax = (nmax + 63) / 64 + 1;
     int LVmax = 1;
     while ((1ll << LVmax) <= nmax) ++LVmax;
-    unsigned long long *H, *words;
-    uint32_t *occ, *key, *val, *key2, *val2, *V, *cur, *nxt, *zf, *bsum, *tot, *rdir, *Zs, *dist, *isl, *lst, *hist;
+    unsigned long long *H, *words, *cat;
+    uint32_t *occ, *key, *val, *key2, *val2, *V, *cur, *nxt, *zf, *bsum, *tot, *rdir, *Zs, *dist, *isl, *lst, *hist, *tidv;
     unsigned char* sidx;
+    DPB* d_pb;
     const long long ntmax = (nmax + kRsTile - 1) / kRsTile;
-    const long long nbmax = (std::max(std::max(nmax, hmax), 256 * ntmax) + kScanB - 1) / kScanB + 1;
+    const long long nbmax = (std::max(std::max(nmax + 1, hmax), 256 * ntmax) + kScanB - 1) / kScanB + 1;
     if ((rc = dmalloc(&H, (size_t)hmax, owned)) || (rc = dmalloc(&occ, (size_t)hmax, owned)) ||
         (rc = dmalloc(&key, (size_t)nmax, owned)) || (rc = dmalloc(&val, (size_t)nmax, owned)) ||
         (rc = dmalloc(&key2, (size_t)nmax, owned)) || (rc = dmalloc(&val2, (size_t)nmax, owned)) ||
@@ -3790,8 +3985,10 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
         (rc = dmalloc(&bsum, (size_t)nbmax, owned)) || (rc = dmalloc(&tot, 8, owned)) ||
         (rc = dmalloc(&words, (size_t)(LVmax * nwmax), owned)) || (rc = dmalloc(&rdir, (size_t)(LVmax * nwmax), owned)) ||
         (rc = dmalloc(&Zs, (size_t)LVmax, owned)) || (rc = dmalloc(&dist, (size_t)nmax, owned)) ||
-        (rc = dmalloc(&isl, (size_t)nmax, owned)) || (rc = dmalloc(&lst, (size_t)nmax + 1, owned)) ||
-        (rc = dmalloc(&hist, (size_t)(256 * ntmax), owned)) || (rc = dmalloc(&sidx, (size_t)nmax, owned)))
+        (rc = dmalloc(&isl, (size_t)nmax + 1, owned)) || (rc = dmalloc(&lst, (size_t)hmax + 1, owned)) ||
+        (rc = dmalloc(&hist, (size_t)(256 * ntmax), owned)) || (rc = dmalloc(&sidx, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&cat, (size_t)nmax, owned)) || (rc = dmalloc(&tidv, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&d_pb, tmax, owned)))
       return cleanup(rc);
     auto scan = [&](uint32_t* io, long long m, uint32_t* total) {
       const long long nb = (m + kScanB - 1) / kScanB;
@@ -3800,18 +3997,41 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
       k_ps_apply<<<(unsigned)nb, 256, 0, q>>>(io, m, bsum);
     };
     const unsigned gridN = (unsigned)(n_sm_dev * 8);
-    for (const DSimTrace& T : longs) {
-      const DGpu& G = hg[cf[T.config].gpu_id];
-      const int lspl = G.lg_line - G.lg_sector, spl = 1 << lspl;
-      const long long nn = T.n;
-      const unsigned long long* rq = S.req + T.req_off;
-      cudaMemsetAsync(H, 0xff, (size_t)T.hcap * sizeof(unsigned long long), q);
-      k_pl_insert<<<gridN, 256, 0, q>>>(rq, nn, lspl, H, (unsigned long long)T.hcap - 1ull);
-      k_pl_occ<<<gridN, 256, 0, q>>>(H, T.hcap, occ);
-      scan(occ, T.hcap, tot);  // tot[0] = distinct lines U (stays on the device: no host sync)
-      const long long Ubound = T.hcap / 2;  // hcap >= 2 * (an upper bound of U)
-      k_pl_ids<<<gridN, 256, 0, q>>>(rq, nn, lspl, spl, H, (unsigned long long)T.hcap - 1ull, occ, key, val, sidx);
-      // stable radix sort of (line id, position) by line id
+    for (const auto& bt : pbat) {
+      std::vector<DPB> hp;
+      long long nn = 0, hcap = 0, Ubound = 0, lmax = 0;
+      for (size_t t = bt.first; t < bt.second; ++t) {
+        const DSimTrace& T = longs[t];
+        const DGpu& G = hg[cf[T.config].gpu_id];
+        DPB P;
+        P.req_off = T.req_off;
+        P.n = T.n;
+        P.start = nn;
+        P.hoff = hcap;
+        P.hcap = T.hcap;
+        P.t_y_abs = nn + T.t_y;
+        P.wld_off = wld_off[2 * T.config];
+        P.wld_cap = wld_off[2 * T.config + 1];
+        P.type = T.type;
+        P.config = T.config;
+        P.lspl = G.lg_line - G.lg_sector;
+        P.spl = 1 << P.lspl;
+        hp.push_back(P);
+        nn += T.n;
+        hcap += T.hcap;
+        Ubound += T.hcap / 2;  // hcap >= 2 * (an upper bound of the stream's distinct lines)
+        lmax = std::max<long long>(lmax, T.n);
+      }
+      const int ntr = (int)hp.size();
+      // pageable host memory: the copy completes before the call returns, hp may go out of scope
+      cudaMemcpyAsync(d_pb, hp.data(), hp.size() * sizeof(DPB), cudaMemcpyHostToDevice, q);
+      k_pb_gather<<<dim3((unsigned)std::min<long long>((lmax + 255) / 256, 4096), (unsigned)ntr), 256, 0, q>>>(
+          S.req, d_pb, cat, tidv);
+      cudaMemsetAsync(H, 0xff, (size_t)hcap * sizeof(unsigned long long), q);
+      k_pb_insert<<<gridN, 256, 0, q>>>(cat, tidv, nn, d_pb, H);
+      k_pl_occ<<<gridN, 256, 0, q>>>(H, hcap, occ);
+      scan(occ, hcap, tot);  // tot[0] = distinct (stream, line) pairs U
+      k_pb_ids<<<gridN, 256, 0, q>>>(cat, tidv, nn, d_pb, H, occ, key, val, sidx);
       int bits = 1;
       while ((1ll << bits) < Ubound) ++bits;
       const long long ntiles = (nn + kRsTile - 1) / kRsTile;
@@ -3824,7 +4044,6 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
         std::swap(va, vb);
       }
       k_pl_prev<<<gridN, 256, 0, q>>>(ka, va, nn, V, isl, lst);
-      // wavelet matrix over V = previous access + 1
       int LV = 1;
       while ((1ll << LV) <= nn) ++LV;
       const long long nw = (nn + 63) / 64 + 1;
@@ -3832,20 +4051,19 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
       uint32_t *c1 = cur, *c2 = nxt;
       for (int lev = 0; lev < LV; ++lev) {
         const int bit = LV - 1 - lev;
-        k_wm_bits<<<gridN, 256, 0, q>>>(c1, nn, bit, words + (long long)lev * nw, zf);
-        scan(zf, nn, Zs + lev);
-        k_wm_next<<<gridN, 256, 0, q>>>(c1, nn, bit, zf, Zs + lev, c2, rdir + (long long)lev * nw);
-        cudaMemcpyAsync(rdir + (long long)lev * nw + (nw - 1), Zs + lev, sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
-        if ((nn & 63) == 0)
-          cudaMemcpyAsync(rdir + (long long)lev * nw + nn / 64, Zs + lev, sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
+        uint32_t* R = rdir + (long long)lev * nw;
+        k_wm_bits<<<gridN, 256, 0, q>>>(c1, nn, bit, words + (long long)lev * nw, R);
+        scan(R, nw - 1, Zs + lev);  // zeros before each word; Z = all zeros of the level
+        cudaMemcpyAsync(R + (nw - 1), Zs + lev, sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
+        k_wm_next<<<gridN, 256, 0, q>>>(c1, nn, bit, words + (long long)lev * nw, R, Zs + lev, c2);
         std::swap(c1, c2);
       }
       k_pl_dist<<<gridN, 256, 0, q>>>(V, nn, LV, words, rdir, Zs, nw, dist);
-      scan(isl, nn, tot + 2);  // exclusive prefix of the last-access flags
-      k_pl_lines<<<(unsigned)((Ubound + 127) / 128), 128, 0, q>>>(
-          va, lst, tot, nn, sidx, dist, rq, isl, spl, lspl, T.type, T.t_y, S.wld + wld_off[2 * T.config],
-          (unsigned long long)wld_off[2 * T.config + 1] - 1ull, S.lines, ncap, S.acc + (long long)T.config * kSimAcc);
+      scan(isl, nn, isl + nn);  // exclusive prefix of the last-access flags; isl[nn] = total
+      k_pb_lines<<<(unsigned)((Ubound + 127) / 128), 128, 0, q>>>(va, lst, tot, nn, sidx, dist, cat, tidv, isl, d_pb,
+                                                                   S.wld, S.lines, ncap, S.acc);
       if ((rc = check_launch())) return cleanup(rc);
+      if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);  // d_pb / buffers reused by the next batch
     }
   }
   if (ev) cudaEventRecord(ev[3], q);
