@@ -226,9 +226,13 @@ typedef struct {
 } ws_sim_result;               /* 160 bytes */
 
 /* Host arrays; synchronous.  out[i * n_cap + k] = configuration i at capacities[k];
- * n_cap <= 64.  Device memory grows with the streams (about 40 B per request). */
+ * n_cap <= 64.  Device memory grows with the streams (about 40 B per request); the context
+ * keeps these buffers for later calls (grow-only) until ws_sim_release or ws_destroy, and
+ * drops them after a failed call. */
 ws_status ws_simulate(ws_ctx* ctx, const ws_config* cfgs, size_t n, const uint64_t* capacities, uint32_t n_cap,
                       ws_sim_result* out);
+/* Free ws_simulate's kept device buffers (synchronises the context's stream). */
+ws_status ws_sim_release(ws_ctx* ctx);
 
 /* Least-squares fit of R(O) = a exp(-b exp(-c O)) to n >= 3 samples, on the device:
  * grid search a in {0.5,...,1.0}, b = exp(-8 + 0.5 j) (j < 23), c = -8 + 0.25 k (k < 32), then 200

@@ -34,6 +34,7 @@ struct ws_ctx {
   void* scratch = nullptr;
   size_t scratch_cap = 0;
   void* io = nullptr;  // host-path staging for configs + results
+  wsb::SimCache sim_cache;  // ws_simulate's device buffers (until ws_sim_release / ws_destroy)
   size_t io_cap = 0;
   uint32_t last_launches = 0;
   unsigned long long* last_work = nullptr;
@@ -223,6 +224,7 @@ void ws_destroy(ws_ctx* c) {
   if (c->dg) cudaFree(c->dg);
   if (c->scratch) cudaFree(c->scratch);
   if (c->io) cudaFree(c->io);
+  c->sim_cache.release();
   for (auto& r : c->pending)
     for (cudaEvent_t e : r.ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->free_ev) cudaEventDestroy(e);
@@ -608,11 +610,19 @@ ws_status ws_simulate(ws_ctx* c, const ws_config* cfgs, size_t n, const uint64_t
     ev = c->take_events(K_SIMGEN, 2);
   }
   const int rc = run_simulate(dc, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), c->hg, S, dr, st,
-                              c->n_sm_dev, caps, (int)n_cap, out, &c->last_launches, ev);
+                              c->n_sm_dev, caps, (int)n_cap, out, &c->last_launches, ev, c->sim_cache);
   if (rc == -WS_ELIMIT) return fail(c, WS_ELIMIT, "a request stream of 2^31 or more requests");
   if (rc == -WS_EINVAL) return fail(c, WS_EINVAL, "all configurations of a ws_simulate call need one line_bytes");
   if (rc) return cuda_fail(c, (cudaError_t)rc, "simulate");
   return WS_OK;
+}
+
+ws_status ws_sim_release(ws_ctx* c) {
+  if (!c) return WS_EINVAL;
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  c->sim_cache.release();
+  return e == cudaSuccess ? WS_OK : cuda_fail(c, e, "sim_release");
 }
 
 ws_status ws_fit_gompertz(ws_ctx* c, const double* O, const double* R, size_t n, double abc[3], double* rss) {

@@ -200,9 +200,22 @@ int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st
 // NEXT-1 (ws_kernels.cu): the whole ws_simulate device sequence (estimate, request streams,
 // stack-distance simulation, sample records) on st.main, synchronous; returns 0, a
 // cudaError_t, or -WS_ELIMIT / -WS_EINVAL.  ev: nullptr or 4 events (gen start/end, run start/end).
+// ws_simulate's device buffers, kept by the context between calls (grow-only, one slot per
+// allocation site in call order): cudaMalloc / cudaFree of tens of GB cost more than the kernels
+struct SimCache {
+  std::vector<void*> ptr;
+  std::vector<size_t> bytes;
+  void release() {
+    for (void* p : ptr)
+      if (p) cudaFree(p);
+    ptr.clear();
+    bytes.clear();
+  }
+};
 int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                  const std::vector<DGpu>& hg, const Scratch& s, ws_result* d_est, const Streams& st, int n_sm_dev,
-                 const uint64_t* h_caps, int ncap, ws_sim_result* h_out, uint32_t* launches, cudaEvent_t* ev);
+                 const uint64_t* h_caps, int ncap, ws_sim_result* h_out, uint32_t* launches, cudaEvent_t* ev,
+                 SimCache& cache);
 // ws_fit_gompertz on the device; out = (a, b, c, rss).  ev: nullptr or 2 events.
 int run_fit(const double* h_O, const double* h_R, int n, double* h_out, cudaStream_t q, cudaEvent_t* ev);
 

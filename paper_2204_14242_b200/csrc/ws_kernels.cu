@@ -31,6 +31,9 @@
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "ws_internal.cuh"
@@ -3337,37 +3340,9 @@ __global__ void __launch_bounds__(256) k_ps_apply(uint32_t* __restrict__ io, lon
 
 // dense line ids: phase 1 insert the line keys, phase 2 (after a scan of the occupancy flags)
 // look them up; ids follow slot order (deterministic)
-__global__ void k_pl_insert(const unsigned long long* __restrict__ req, long long n, int lspl,
-                            unsigned long long* __restrict__ H, unsigned long long hm) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long r = req[i];
-    const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
-    const unsigned long long lkey = ((r >> 48) << 48) | (sb >> lspl);
-    unsigned long long h = sim_hash(lkey) & hm;
-    for (;;) {
-      const unsigned long long old = atomicCAS(&H[h], kEmpty, lkey);
-      if (old == kEmpty || old == lkey) break;
-      h = (h + 1) & hm;
-    }
-  }
-}
 __global__ void k_pl_occ(const unsigned long long* __restrict__ H, long long hcap, uint32_t* __restrict__ occ) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hcap; i += (long long)gridDim.x * blockDim.x)
     occ[i] = H[i] != kEmpty ? 1u : 0u;
-}
-__global__ void k_pl_ids(const unsigned long long* __restrict__ req, long long n, int lspl, int spl,
-                         const unsigned long long* __restrict__ H, unsigned long long hm, const uint32_t* __restrict__ occ,
-                         uint32_t* __restrict__ key, uint32_t* __restrict__ val, unsigned char* __restrict__ sidx) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long r = req[i];
-    const unsigned long long sb = r & ((1ull << kSimSecBits) - 1ull);
-    const unsigned long long lkey = ((r >> 48) << 48) | (sb >> lspl);
-    unsigned long long h = sim_hash(lkey) & hm;
-    while (H[h] != lkey) h = (h + 1) & hm;
-    key[i] = occ[h];            // exclusive prefix of the occupancy = dense id
-    val[i] = (uint32_t)i;
-    sidx[i] = (unsigned char)(sb & (unsigned long long)(spl - 1));
-  }
 }
 
 // stable LSD radix pass on 8 bits of key (tiles of 2048 = 256 threads x 8 rounds)
@@ -3422,58 +3397,103 @@ __global__ void __launch_bounds__(256) k_rs_scatter(const uint32_t* __restrict__
   }
 }
 
-// previous access of the line, last-access flags, line starts; V = prev + 1 for the wavelet matrix
+// previous access of the line, last-access flags, line starts; V = prev + 1 for the wavelet matrix,
+// the last-access flag in bit 31 (positions < 2^31 - 2): one scattered store per access
 __global__ void k_pl_prev(const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sval, long long n,
-                          uint32_t* __restrict__ V, uint32_t* __restrict__ islast, uint32_t* __restrict__ lstart) {
+                          uint32_t* __restrict__ V, uint32_t* __restrict__ lstart) {
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
     const uint32_t i = sval[k], l = skey[k];
     const bool first = k == 0 || skey[k - 1] != l;
     const bool last = k + 1 == n || skey[k + 1] != l;
-    V[i] = first ? 0u : sval[k - 1] + 1u;
-    islast[i] = last ? 1u : 0u;
+    V[i] = (first ? 0u : sval[k - 1] + 1u) | (last ? 0x80000000u : 0u);
     if (first) lstart[l] = (uint32_t)k;
   }
 }
-// one wavelet-matrix level: the bit of every value (64-bit words, one ballot pair per warp) and
-// the zero flags for the scan
-// (the zeros of every word go to wz: their exclusive scan over the words is the rank directory)
-__global__ void k_wm_bits(const uint32_t* __restrict__ cur, long long n, int bit, unsigned long long* __restrict__ words,
+// split the flags off (coalesced)
+__global__ void k_pl_split(uint32_t* __restrict__ V, long long n, uint32_t* __restrict__ islast) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t v = V[i];
+    islast[i] = v >> 31;
+    V[i] = v & 0x7fffffffu;
+  }
+}
+// one wavelet-matrix level, one entry per 64 positions: {bit word, zeros before the word} (one
+// 16-byte load per rank query).  k_wm_bits writes the words and each word's zero count (wz);
+// the exclusive scan of wz is the rank directory, which k_wm_next stores next to the words while
+// it partitions the values stably by the bit (zeros first)
+__global__ void k_wm_bits(const uint32_t* __restrict__ cur, long long n, int bit, ulonglong2* __restrict__ wr,
                           uint32_t* __restrict__ wz) {
+  constexpr int kU = 4;  // words per warp iteration (loads in flight)
   const int lane = threadIdx.x & 31;
   const long long nw = (n + 63) / 64;
-  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
-       w += ((long long)gridDim.x * blockDim.x) >> 5) {
-    const long long i0 = w * 64 + lane, i1 = i0 + 32;
-    const uint32_t b0 = i0 < n ? (cur[i0] >> bit) & 1u : 0u, b1 = i1 < n ? (cur[i1] >> bit) & 1u : 0u;
-    const unsigned z0 = __ballot_sync(FULL, i0 < n && !b0), z1 = __ballot_sync(FULL, i1 < n && !b1);
-    const unsigned lo = __ballot_sync(FULL, b0), hi = __ballot_sync(FULL, b1);
-    if (lane == 0) {
-      words[w] = ((unsigned long long)hi << 32) | lo;
-      wz[w] = (uint32_t)(__popc(z0) + __popc(z1));
+  for (long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kU; w0 < nw;
+       w0 += (((long long)gridDim.x * blockDim.x) >> 5) * kU) {
+    uint32_t b[2 * kU];
+#pragma unroll
+    for (int u = 0; u < 2 * kU; ++u) {
+      const long long i = w0 * 64 + u * 32 + lane;
+      b[u] = i < n ? (cur[i] >> bit) & 1u : 2u;  // 2: past the end (neither bit)
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const unsigned lo = __ballot_sync(FULL, b[2 * u] == 1u), hi = __ballot_sync(FULL, b[2 * u + 1] == 1u);
+      const unsigned z0 = __ballot_sync(FULL, b[2 * u] == 0u), z1 = __ballot_sync(FULL, b[2 * u + 1] == 0u);
+      if (lane == u && w0 + u < nw) {
+        wr[w0 + u].x = ((unsigned long long)hi << 32) | lo;
+        wz[w0 + u] = (uint32_t)(__popc(z0) + __popc(z1));
+      }
     }
   }
 }
-__global__ void k_wm_next(const uint32_t* __restrict__ cur, long long n, int bit,
-                          const unsigned long long* __restrict__ words, const uint32_t* __restrict__ rdir,
+__global__ void k_wm_next(const uint32_t* __restrict__ cur, long long n, int bit, const uint32_t* __restrict__ wz,
                           const uint32_t* __restrict__ Z, uint32_t* __restrict__ nxt) {
+  constexpr int kU = 4;  // words per warp iteration; the word's bits come from ballots
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const uint32_t Zv = *Z;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
-    const uint32_t v = cur[j];
-    const int r = (int)(j & 63);
-    const uint32_t zp = rdir[j >> 6] + (r ? (uint32_t)__popcll(~words[j >> 6] & ((1ull << r) - 1ull)) : 0u);
-    nxt[((v >> bit) & 1u) ? Zv + (uint32_t)j - zp : zp] = v;
+  const long long nw = (n + 63) / 64;
+  for (long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kU; w0 < nw;
+       w0 += (((long long)gridDim.x * blockDim.x) >> 5) * kU) {
+    uint32_t v[2 * kU], zb[kU];
+#pragma unroll
+    for (int u = 0; u < 2 * kU; ++u) {
+      const long long i = w0 * 64 + u * 32 + lane;
+      v[u] = i < n ? cur[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) zb[u] = w0 + u < nw ? wz[w0 + u] : 0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long i0 = w0 * 64 + u * 64 + lane, i1 = i0 + 32;
+      const bool one0 = (v[2 * u] >> bit) & 1u, one1 = (v[2 * u + 1] >> bit) & 1u;
+      const unsigned z0 = __ballot_sync(FULL, i0 < n && !one0), z1 = __ballot_sync(FULL, i1 < n && !one1);
+      const uint32_t zp0 = zb[u] + (uint32_t)__popc(z0 & lt);                        // zeros before i0
+      const uint32_t zp1 = zb[u] + (uint32_t)__popc(z0) + (uint32_t)__popc(z1 & lt);  // zeros before i1
+      if (i0 < n) nxt[one0 ? Zv + (uint32_t)i0 - zp0 : zp0] = v[2 * u];
+      if (i1 < n) nxt[one1 ? Zv + (uint32_t)i1 - zp1 : zp1] = v[2 * u + 1];
+    }
   }
 }
-__device__ __forceinline__ uint32_t wm_rank0(const unsigned long long* words, const uint32_t* rdir, long long pos) {
-  const long long w = pos >> 6;
-  const int r = (int)(pos & 63);
-  if (r == 0) return rdir[w];
-  return rdir[w] + (uint32_t)__popcll(~words[w] & ((1ull << r) - 1ull));
+// the rank directory next to the words (a separate pass: stores into the entries while k_wm_next
+// reads their words would evict the words' L1 lines); the sentinel entry holds Z
+__global__ void k_wm_rank(ulonglong2* __restrict__ wr, long long nw, const uint32_t* __restrict__ wz,
+                          const uint32_t* __restrict__ Z) {
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (long long)gridDim.x * blockDim.x)
+    wr[w].y = w + 1 < nw ? wz[w] : *Z;
 }
-// dist(i) = #{j < i : V[j] < p(i) + 2} - p(i) - 1 (kInf for a line's first access)
-__global__ void k_pl_dist(const uint32_t* __restrict__ V, long long n, int LV, const unsigned long long* __restrict__ words,
-                          const uint32_t* __restrict__ rdir, const uint32_t* __restrict__ Zs, long long wstride,
-                          uint32_t* __restrict__ dist) {
+__device__ __forceinline__ uint32_t wm_rank0(const ulonglong2* wr, long long pos) {
+  const ulonglong2 e = wr[pos >> 6];
+  const int r = (int)(pos & 63);
+  return (uint32_t)e.y + (r ? (uint32_t)__popcll(~e.x & ((1ull << r) - 1ull)) : 0u);
+}
+// dist(i) = #{j < i : V[j] < p(i) + 2} - p(i) - 1 (kInf for a line's first access).  Only the
+// capacity bin of a distance is ever used (cap_bin of running maxima; cap_bin is monotone), so a
+// reuse window of i - p - 1 < lines[0] positions -- at most that many distinct lines, a hit at
+// every capacity -- stores the window length, an upper bound in the same bin, without a query.
+__global__ void k_pl_dist(const uint32_t* __restrict__ V, long long n, int LV, const ulonglong2* __restrict__ wr,
+                          const uint32_t* __restrict__ Zs, long long wstride,
+                          const unsigned long long* __restrict__ lines, uint32_t* __restrict__ dist) {
+  const unsigned long long l0 = lines[0];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const uint32_t v = V[i];
     if (v == 0u) {
@@ -3481,13 +3501,17 @@ __global__ void k_pl_dist(const uint32_t* __restrict__ V, long long n, int LV, c
       continue;
     }
     const uint32_t p = v - 1u, x = p + 2u;
+    const uint32_t win = (uint32_t)i - p - 1u;
+    if ((unsigned long long)win < l0) {
+      dist[i] = win;
+      continue;
+    }
     long long a = 0, b = i;
     uint32_t cnt = 0;
     for (int lev = 0; lev < LV; ++lev) {
       const int bit = LV - 1 - lev;
-      const unsigned long long* W = words + (long long)lev * wstride;
-      const uint32_t* R = rdir + (long long)lev * wstride;
-      const uint32_t ra = wm_rank0(W, R, a), rb = wm_rank0(W, R, b);
+      const ulonglong2* W = wr + (long long)lev * wstride;
+      const uint32_t ra = wm_rank0(W, a), rb = wm_rank0(W, b);
       if ((x >> bit) & 1u) {
         cnt += rb - ra;
         a = Zs[lev] + (a - ra);
@@ -3500,93 +3524,6 @@ __global__ void k_pl_dist(const uint32_t* __restrict__ V, long long n, int LV, c
     dist[i] = cnt - p - 1u;
   }
 }
-// one thread per line: walk its accesses in time order (per-sector running maxima), histogram the
-// counted requests; the layer stream's end state of the overlap sectors
-__global__ void __launch_bounds__(128) k_pl_lines(const uint32_t* __restrict__ sval, const uint32_t* __restrict__ lstart,
-                                                  const uint32_t* __restrict__ Uptr, long long n,
-                                                  const unsigned char* __restrict__ sidx,
-                                                  const uint32_t* __restrict__ dist, const unsigned long long* __restrict__ req,
-                                                  const uint32_t* __restrict__ cntlast, int spl, int lspl,
-                                                  int type, long long t_y, const unsigned long long* __restrict__ H,
-                                                  unsigned long long whm, const unsigned long long* __restrict__ lines,
-                                                  int ncap, unsigned long long* __restrict__ A) {
-  __shared__ unsigned s_h[2][kSimHist];
-  __shared__ unsigned long long s_c[4];  // counted, compulsory, ovy, ovz
-  const long long U = *Uptr;
-  const uint32_t Ulines = (uint32_t)U;
-  if ((long long)blockIdx.x * blockDim.x >= U) return;  // grid sized by an upper bound of U
-  for (int b = threadIdx.x; b < 2 * kSimHist; b += blockDim.x) s_h[b / kSimHist][b % kSimHist] = 0u;
-  if (threadIdx.x < 4) s_c[threadIdx.x] = 0ull;
-  __syncthreads();
-  const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (l < U) {
-    const long long k0 = lstart[l], k1 = l + 1 < U ? (long long)lstart[l + 1] : n;
-    uint32_t M[32], SL[32];
-    for (int s = 0; s < spl; ++s) {
-      M[s] = kInf;
-      SL[s] = kInf;
-    }
-    unsigned long long cnt = 0, comp = 0;
-    uint32_t lasti = 0;
-    for (long long k = k0; k < k1; ++k) {
-      const uint32_t i = sval[k];
-      const int s = sidx[i];
-      const uint32_t d = dist[i];
-      const uint32_t D = max(M[s], d);
-      for (int s2 = 0; s2 < spl; ++s2) M[s2] = max(M[s2], d);
-      M[s] = 0u;
-      SL[s] = i;
-      lasti = i;
-      const bool st = (req[i] >> kSimSecBits) & 1ull;
-      if (type == 0 || (type == 1 && st)) {
-        atomicAdd(&s_h[0][cap_bin(lines, ncap, D)], 1u);
-        ++cnt;
-        comp += D == kInf ? 1ull : 0ull;
-      }
-    }
-    if (cnt) {
-      atomicAdd(&s_c[0], cnt);
-      atomicAdd(&s_c[1], comp);
-    }
-    if (type == 2) {
-      const uint32_t dend = Ulines - cntlast[lasti] - 1u;  // lines whose last access is after this line's
-      const unsigned long long r = req[lasti];
-      const unsigned long long lkey = ((r >> 48) << 48) | ((r & ((1ull << kSimSecBits) - 1ull)) >> lspl);
-      unsigned long long oy = 0, oz = 0;
-      for (int s = 0; s < spl; ++s) {
-        if (SL[s] == kInf) continue;
-        const unsigned long long skey = ((lkey >> 48) << 48) | (((lkey & ((1ull << 48) - 1ull)) << lspl) | (unsigned)s);
-        if (!wld_has(H, whm, skey)) continue;
-        const uint32_t De = max(M[s], dend);
-        const bool isy = (long long)SL[s] >= t_y;
-        atomicAdd(&s_h[isy ? 0 : 1][cap_bin(lines, ncap, De)], 1u);
-        if (isy) ++oy;
-        else ++oz;
-      }
-      if (oy) atomicAdd(&s_c[2], oy);
-      if (oz) atomicAdd(&s_c[3], oz);
-    }
-  }
-  __syncthreads();
-  const int h0 = type == 0 ? SA_L1H : (type == 1 ? SA_L1H + kSimHist : SA_L1H + 2 * kSimHist);
-  for (int b = threadIdx.x; b <= ncap; b += blockDim.x) {
-    if (s_h[0][b]) atomicAdd(A + h0 + b, (unsigned long long)s_h[0][b]);
-    if (type == 2 && s_h[1][b]) atomicAdd(A + SA_L1H + 3 * kSimHist + b, (unsigned long long)s_h[1][b]);
-  }
-  if (threadIdx.x == 0) {
-    if (type == 0) {
-      atomicAdd(A + SA_L1REQ, s_c[0]);
-      atomicAdd(A + SA_L1COMP, s_c[1]);
-    } else if (type == 1) {
-      atomicAdd(A + SA_STREQ, s_c[0]);
-      atomicAdd(A + SA_STCOMP, s_c[1]);
-    } else {
-      atomicAdd(A + SA_OVY, s_c[2]);
-      atomicAdd(A + SA_OVZ, s_c[3]);
-    }
-  }
-}
-
 
 // ---- batched long streams: several long streams concatenated (positions are global; the stack
 // distance formula is invariant under the shift, and every quantity that must stay per stream --
@@ -3757,13 +3694,44 @@ __global__ void __launch_bounds__(128) k_pb_lines(const uint32_t* __restrict__ s
 
 // ------------------------------------------------------------------ NEXT-1 host orchestration
 namespace {
-template <class T>
-int dmalloc(T** p, size_t count, std::vector<void*>& owned) {
+// simulator scratch: the k-th allocation of a call reuses the cache's slot k when it is large
+// enough; otherwise the slot grows (slots not yet handed out are dropped first when memory is short)
+struct Owned {
+  SimCache* cache;
+  size_t next;
+};
+template <typename T>
+int dmalloc(T** p, size_t count, Owned& o) {
   *p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-  if (e != cudaSuccess) return (int)e;
-  owned.push_back(*p);
+  const size_t need = count * sizeof(T);
+  SimCache& C = *o.cache;
+  const size_t k = o.next++;
+  if (k >= C.ptr.size()) {
+    C.ptr.push_back(nullptr);
+    C.bytes.push_back(0);
+  }
+  if (C.bytes[k] < need) {
+    if (C.ptr[k]) cudaFree(C.ptr[k]);
+    C.ptr[k] = nullptr;
+    C.bytes[k] = 0;
+    cudaError_t e = cudaMalloc(&C.ptr[k], need);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      for (size_t j = k + 1; j < C.ptr.size(); ++j) {
+        if (C.ptr[j]) cudaFree(C.ptr[j]);
+        C.ptr[j] = nullptr;
+        C.bytes[j] = 0;
+      }
+      e = cudaMalloc(&C.ptr[k], need);
+    }
+    if (e != cudaSuccess) {
+      C.ptr[k] = nullptr;
+      return (int)e;
+    }
+    C.bytes[k] = need;
+  }
+  *p = (T*)C.ptr[k];
   return 0;
 }
 long long pow2_at_least(long long v) {
@@ -3775,14 +3743,25 @@ long long pow2_at_least(long long v) {
 
 int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                  const std::vector<DGpu>& hg, const Scratch& s, ws_result* d_est, const Streams& st, int n_sm_dev,
-                 const uint64_t* h_caps, int ncap, ws_sim_result* h_out, uint32_t* launches, cudaEvent_t* ev) {
-  std::vector<void*> owned;
+                 const uint64_t* h_caps, int ncap, ws_sim_result* h_out, uint32_t* launches, cudaEvent_t* ev,
+                 SimCache& cache) {
+  cudaStream_t q = st.main;
+  Owned owned{&cache, 0};
+  // WS_SIM_HOSTTIME=1: synchronise and print the elapsed host time at each phase (diagnostics)
+  static const bool htime = getenv("WS_SIM_HOSTTIME") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!htime) return;
+    cudaStreamSynchronize(q);
+    fprintf(stderr, "[ws_simulate] %-14s %9.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
   auto cleanup = [&](int rc) {
-    cudaStreamSynchronize(st.main);
-    for (void* p : owned) cudaFree(p);
+    cudaStreamSynchronize(q);
+    mark("end");
+    if (rc) cache.release();  // after an error nothing is kept
     return rc;
   };
-  cudaStream_t q = st.main;
   uint32_t L = 0;
   int rc = launch_estimate(d_cfgs, n, d_k, nk, d_g, ng, s, d_est, st, n_sm_dev, &L, nullptr);
   if (rc) return cleanup(rc);
@@ -3804,6 +3783,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);
   int64_t* d_cnt;
   DSimTrace* d_tr;
+  mark("estimate");
   if ((rc = dmalloc(&d_cnt, (size_t)n_items + 1, owned)) || (rc = dmalloc(&d_tr, (size_t)n_traces, owned)))
     return cleanup(rc);
   S.item_cnt = d_cnt;
@@ -3902,6 +3882,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     rank[idx[k]] = k;
     lines[k] = std::max<unsigned long long>(1ull, h_caps[idx[k]] >> lb);
   }
+  mark("sizing");
   if ((rc = dmalloc(&S.req, (size_t)req_total, owned)) || (rc = dmalloc(&S.fen, (size_t)fen_total, owned)) ||
       (rc = dmalloc(&S.keys, (size_t)slot_total, owned)) || (rc = dmalloc(&S.last, (size_t)slot_total, owned)) ||
       (rc = dmalloc(&S.M, (size_t)m_total, owned)) || (rc = dmalloc(&S.SL, (size_t)m_total, owned)) ||
@@ -3911,6 +3892,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   S.n_traces = n_traces;
   ws_sim_result* d_out;
   if ((rc = dmalloc(&d_out, (size_t)n * ncap, owned))) return cleanup(rc);
+  mark("alloc+gen");
   cudaMemsetAsync(S.wld, 0xff, (size_t)wld_total * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.acc, 0, (size_t)n * kSimAcc * sizeof(unsigned long long), q);
   cudaMemsetAsync(S.counter, 0, sizeof(unsigned long long), q);
@@ -3941,6 +3923,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     if ((rc = (int)cudaStreamSynchronize(q))) return cleanup(rc);  // the host copy of tr is reused
   }
   // parallel path: the long streams, concatenated in batches (positions < 2^31), device-wide kernels
+  mark("warp path");
   if (!longs.empty()) {
     std::vector<std::pair<size_t, size_t>> pbat;
     {
@@ -3971,8 +3954,9 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
     const long long nwmax = (nmax + 63) / 64 + 1;
     int LVmax = 1;
     while ((1ll << LVmax) <= nmax) ++LVmax;
-    unsigned long long *H, *words, *cat;
-    uint32_t *occ, *key, *val, *key2, *val2, *V, *cur, *nxt, *zf, *bsum, *tot, *rdir, *Zs, *dist, *isl, *lst, *hist, *tidv;
+    unsigned long long *H, *cat;
+    ulonglong2* wr;
+    uint32_t *occ, *key, *val, *key2, *val2, *V, *cur, *nxt, *wz, *bsum, *tot, *Zs, *dist, *isl, *lst, *hist, *tidv;
     unsigned char* sidx;
     DPB* d_pb;
     const long long ntmax = (nmax + kRsTile - 1) / kRsTile;
@@ -3981,15 +3965,16 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
         (rc = dmalloc(&key, (size_t)nmax, owned)) || (rc = dmalloc(&val, (size_t)nmax, owned)) ||
         (rc = dmalloc(&key2, (size_t)nmax, owned)) || (rc = dmalloc(&val2, (size_t)nmax, owned)) ||
         (rc = dmalloc(&V, (size_t)nmax, owned)) || (rc = dmalloc(&cur, (size_t)nmax, owned)) ||
-        (rc = dmalloc(&nxt, (size_t)nmax, owned)) || (rc = dmalloc(&zf, (size_t)nmax, owned)) ||
+        (rc = dmalloc(&nxt, (size_t)nmax, owned)) || (rc = dmalloc(&wz, (size_t)nwmax, owned)) ||
         (rc = dmalloc(&bsum, (size_t)nbmax, owned)) || (rc = dmalloc(&tot, 8, owned)) ||
-        (rc = dmalloc(&words, (size_t)(LVmax * nwmax), owned)) || (rc = dmalloc(&rdir, (size_t)(LVmax * nwmax), owned)) ||
+        (rc = dmalloc(&wr, (size_t)(LVmax * nwmax), owned)) ||
         (rc = dmalloc(&Zs, (size_t)LVmax, owned)) || (rc = dmalloc(&dist, (size_t)nmax, owned)) ||
         (rc = dmalloc(&isl, (size_t)nmax + 1, owned)) || (rc = dmalloc(&lst, (size_t)hmax + 1, owned)) ||
         (rc = dmalloc(&hist, (size_t)(256 * ntmax), owned)) || (rc = dmalloc(&sidx, (size_t)nmax, owned)) ||
         (rc = dmalloc(&cat, (size_t)nmax, owned)) || (rc = dmalloc(&tidv, (size_t)nmax, owned)) ||
         (rc = dmalloc(&d_pb, tmax, owned)))
       return cleanup(rc);
+    mark("long alloc");
     auto scan = [&](uint32_t* io, long long m, uint32_t* total) {
       const long long nb = (m + kScanB - 1) / kScanB;
       k_ps_reduce<<<(unsigned)nb, 256, 0, q>>>(io, m, bsum);
@@ -4043,22 +4028,23 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
         std::swap(ka, kb);
         std::swap(va, vb);
       }
-      k_pl_prev<<<gridN, 256, 0, q>>>(ka, va, nn, V, isl, lst);
+      k_pl_prev<<<gridN, 256, 0, q>>>(ka, va, nn, V, lst);
+      k_pl_split<<<gridN, 256, 0, q>>>(V, nn, isl);
       int LV = 1;
       while ((1ll << LV) <= nn) ++LV;
       const long long nw = (nn + 63) / 64 + 1;
-      cudaMemcpyAsync(cur, V, (size_t)nn * sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
-      uint32_t *c1 = cur, *c2 = nxt;
+      uint32_t *c1 = V, *c2 = cur;  // level 0 reads V (kept for k_pl_dist), then cur <-> nxt
       for (int lev = 0; lev < LV; ++lev) {
         const int bit = LV - 1 - lev;
-        uint32_t* R = rdir + (long long)lev * nw;
-        k_wm_bits<<<gridN, 256, 0, q>>>(c1, nn, bit, words + (long long)lev * nw, R);
-        scan(R, nw - 1, Zs + lev);  // zeros before each word; Z = all zeros of the level
-        cudaMemcpyAsync(R + (nw - 1), Zs + lev, sizeof(uint32_t), cudaMemcpyDeviceToDevice, q);
-        k_wm_next<<<gridN, 256, 0, q>>>(c1, nn, bit, words + (long long)lev * nw, R, Zs + lev, c2);
-        std::swap(c1, c2);
+        ulonglong2* Wl = wr + (long long)lev * nw;
+        k_wm_bits<<<gridN, 256, 0, q>>>(c1, nn, bit, Wl, wz);
+        scan(wz, nw - 1, Zs + lev);  // zeros before each word; Z = all zeros of the level
+        k_wm_next<<<gridN, 256, 0, q>>>(c1, nn, bit, wz, Zs + lev, c2);
+        k_wm_rank<<<gridN, 256, 0, q>>>(Wl, nw, wz, Zs + lev);
+        c1 = c2;
+        c2 = c2 == cur ? nxt : cur;
       }
-      k_pl_dist<<<gridN, 256, 0, q>>>(V, nn, LV, words, rdir, Zs, nw, dist);
+      k_pl_dist<<<gridN, 256, 0, q>>>(V, nn, LV, wr, Zs, nw, S.lines, dist);
       scan(isl, nn, isl + nn);  // exclusive prefix of the last-access flags; isl[nn] = total
       k_pb_lines<<<(unsigned)((Ubound + 127) / 128), 128, 0, q>>>(va, lst, tot, nn, sidx, dist, cat, tidv, isl, d_pb,
                                                                    S.wld, S.lines, ncap, S.acc);

@@ -79,7 +79,7 @@ RESULT_DTYPE = np.dtype(ws_result)
 EXPORTS = ["ws_create", "ws_destroy", "ws_last_error", "ws_set_stream", "ws_describe_kernel", "ws_describe_gpu",
            "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count",
            "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read", "ws_simulate",
-           "ws_fit_gompertz", "ws_validate_stencil25", "ws_validate_lbm15"]
+           "ws_sim_release", "ws_fit_gompertz", "ws_validate_stencil25", "ws_validate_lbm15"]
 
 _lib = None
 
@@ -112,6 +112,7 @@ def load_library(path: str = LIB_PATH):
     L.ws_profile_read.argtypes = [P, C.POINTER(F64), C.POINTER(U64), U32, C.POINTER(U32)]
     L.ws_work_read.argtypes = [P, C.POINTER(U64), U32]
     L.ws_simulate.argtypes = [P, P, C.c_size_t, P, U32, P]
+    L.ws_sim_release.argtypes = [P]
     L.ws_fit_gompertz.argtypes = [P, P, P, C.c_size_t, P, P]
     L.ws_validate_stencil25.argtypes = [P, P, P, P, P, P, U32, P]
     L.ws_validate_lbm15.argtypes = [P, P, P, P, P, P, P, U32, P]
@@ -301,6 +302,10 @@ class Context:
                 row.append(d)
             rows.append(row)
         return rows
+
+    def sim_release(self):
+        """Free the device buffers simulate() keeps between calls."""
+        self._check(self.L.ws_sim_release(self.h))
 
     def fit_gompertz(self, O, R):
         """Least-squares Gompertz fit on the device -> ((a, b, c), rss)."""

@@ -401,6 +401,24 @@ def test_fit_known_curves(ctx):
         assert (a, b, c) == pytest.approx(tuple(abc), rel=1e-6)
 
 
+def test_sim_buffer_cache(ctx):
+    """ws_simulate keeps its device buffers between calls (grow-only slots): a small call after a
+    large one, after a forced parallel-path call, and after ws_sim_release all match the oracle."""
+    small = (W.stencil_star(20, 10, 12, 1, regs=0), dict(W.gpu_a100(), n_sm=4), [((4, 4, 2), (1, 1, 2), 2)])
+    large = (W.k25(48), dict(W.gpu_a100(), n_sm=24), W.space_stencil_paper()[::21])
+    sim_parity(ctx, *large, CAPS, "cache-large")
+    sim_parity(ctx, *small, CAPS, "cache-small")
+    os.environ["WS_SIM_PAR"] = "all"
+    try:
+        sim_parity(ctx, *large, CAPS, "cache-large-par")
+    finally:
+        os.environ.pop("WS_SIM_PAR", None)
+    sim_parity(ctx, *small, CAPS, "cache-small2")
+    ctx.sim_release()
+    ctx.sim_release()
+    sim_parity(ctx, *small, CAPS, "cache-small3")
+
+
 def test_sim_errors(ctx):
     from paper_2204_14242_b200 import config_array
     kid, gid = ctx.describe_kernel(W.k7(8)), ctx.describe_gpu(dict(W.gpu_v100(), n_sm=4))
