@@ -1516,6 +1516,61 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
   }
 }
 
+// ---- translation groups of directly evaluated multi-block SM sets (k_smset)
+constexpr int kSetGrp = 1024;  // sets per config grouped in shared memory (more: no grouping)
+__device__ __forceinline__ void block_coord(const DPlan& P, long long B, long long* bc) {
+  bc[0] = B % P.G[0];
+  bc[1] = (B / P.G[0]) % P.G[1];
+  bc[2] = B / (P.G[0] * P.G[1]);
+}
+__device__ __forceinline__ bool set_unclipped(const DPlan& P, long long S0, long long kj, long long nsm) {
+  for (long long m = 0; m < kj; ++m) {
+    long long bc[3];
+    block_coord(P, S0 + m * nsm, bc);
+    if (clip_pattern(P, bc)) return false;
+  }
+  return true;
+}
+// line residue of the set's first block (translation by a multiple of a line keeps every count)
+__device__ __forceinline__ long long set_residue(const DPlan& P, long long S0) {
+  long long bc[3], pl = 0;
+  block_coord(P, S0, bc);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+  return pl & (P.scls_R - 1);
+}
+// hash of (member count, residue, members' block offsets from the first member); never 0
+__device__ __forceinline__ unsigned long long set_shape_key(const DPlan& P, long long S0, long long kj, long long nsm) {
+  long long b0[3];
+  block_coord(P, S0, b0);
+  unsigned long long h = 0x9e3779b97f4a7c15ull ^ ((unsigned long long)kj << 8) ^ (unsigned long long)set_residue(P, S0);
+  for (long long m = 1; m < kj; ++m) {
+    long long bc[3];
+    block_coord(P, S0 + m * nsm, bc);
+    for (int d = 0; d < 3; ++d) {
+      h ^= (unsigned long long)(bc[d] - b0[d]) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+      h *= 0xff51afd7ed558ccdull;
+    }
+  }
+  return h | 1ull;
+}
+// exact check: every member of set S1 is the same block translate of S0's member (same count)
+__device__ __forceinline__ bool set_translates(const DPlan& P, long long S0, long long S1, long long kj, long long nsm) {
+  if (set_residue(P, S0) != set_residue(P, S1)) return false;
+  long long a0[3], b0[3];
+  block_coord(P, S0, a0);
+  block_coord(P, S1, b0);
+  for (long long m = 1; m < kj; ++m) {
+    long long a[3], b[3];
+    block_coord(P, S0 + m * nsm, a);
+    block_coord(P, S1 + m * nsm, b);
+    for (int d = 0; d < 3; ++d)
+      if (a[d] - a0[d] != b[d] - b0[d]) return false;
+  }
+  return true;
+}
+
+
 // Pass 1 (one thread per SM set): single-block sets go to their translation class: clip
 // pattern of the block x residue of its first cell's address mod line_bytes (identical
 // active-cell boxes that are translates by a multiple of the line size have identical
@@ -1527,86 +1582,115 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
                                                unsigned long long* __restrict__ lists,
                                                unsigned long long* __restrict__ slist,
                                                unsigned long long* __restrict__ dlist) {
-  const long long total = pre[n].set;
-  for (long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x; item < total;
-       item += (long long)gridDim.x * blockDim.x) {
-    const int c = find_config<2>(pre, n, item);
+  __shared__ unsigned long long s_key[kSetGrp];  // directly evaluated sets: shape key (0: not grouped)
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const DPlan& P = plans[c];
-    const long long j = item - pre[c].set;
+    const long long nset = pre[c + 1].set - pre[c].set;
     const long long nsm = gs[P.gid].g.n_sm;
-    const long long S0 = P.s + j;
-    const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-    // A multi-block set whose members' load footprints cannot share a line is the disjoint union
-    // of its members' footprints: every member is then counted like a single-block set, in its
-    // translation class (members are n_sm blocks apart, usually far apart in the grid).  Two
-    // members' footprints (block box + the field's load-offset extremes) share no line when they
-    // are >= 2 planes apart in z, or >= 2 rows apart in y without touching the field's first or
-    // last row (rows / planes of >= one line), or >= one line of elements apart in x unless one
-    // reaches a row end and the other a row start (wrap-around adjacency of consecutive rows).
-    // Otherwise the set is evaluated directly.
-    bool split = false;
-    if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult) {
-      const DKernel& K = ks[P.kid];
-      const long long lb = gs[P.gid].g.line_bytes;
-      split = true;
-      long long box[32][6];
-      for (long long m = 0; m < kj; ++m) {
-        const long long Bm = S0 + m * nsm;
-        const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
-        for (int d = 0; d < 3; ++d) {
-          box[m][2 * d] = P.lo[d] + bc[d] * P.BF[d];
-          long long hi = box[m][2 * d] + P.BF[d];
-          box[m][2 * d + 1] = (hi > P.hi[d] ? P.hi[d] : hi) - 1;
+    const bool grp = nset <= kSetGrp && P.scls_R > 0 && !P.rep_mult;
+    for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
+      const long long S0 = P.s + j;
+      const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
+      // A multi-block set whose members' load footprints cannot share a line is the disjoint union
+      // of its members' footprints: every member is then counted like a single-block set, in its
+      // translation class (members are n_sm blocks apart, usually far apart in the grid).  Two
+      // members' footprints (block box + the field's load-offset extremes) share no line when they
+      // are >= 2 planes apart in z, or >= 2 rows apart in y without touching the field's first or
+      // last row (rows / planes of >= one line), or >= one line of elements apart in x unless one
+      // reaches a row end and the other a row start (wrap-around adjacency of consecutive rows).
+      // Otherwise the set is evaluated directly.
+      bool split = false;
+      if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult) {
+        const DKernel& K = ks[P.kid];
+        const long long lb = gs[P.gid].g.line_bytes;
+        split = true;
+        long long box[32][6];
+        for (long long m = 0; m < kj; ++m) {
+          const long long Bm = S0 + m * nsm;
+          const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+          for (int d = 0; d < 3; ++d) {
+            box[m][2 * d] = P.lo[d] + bc[d] * P.BF[d];
+            long long hi = box[m][2 * d] + P.BF[d];
+            box[m][2 * d + 1] = (hi > P.hi[d] ? P.hi[d] : hi) - 1;
+          }
+        }
+        for (int fi = 0; fi < K.n_fields && split; ++fi) {
+          const DField& F = K.f[fi];
+          if (!(F.kinds & 1)) continue;
+          int xlo = 0x7fffffff, xhi = -0x7fffffff;
+          for (int r = 0; r < F.n_runs; ++r) {
+            xlo = min(xlo, F.run_lo[r]);
+            xhi = max(xhi, F.run_hi[r]);
+          }
+          const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
+          const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
+          for (long long a1 = 0; a1 < kj && split; ++a1)
+            for (long long b1 = a1 + 1; b1 < kj && split; ++b1) {
+              const long long ax0 = box[a1][0] + xlo, ax1 = box[a1][1] + xhi, bx0 = box[b1][0] + xlo, bx1 = box[b1][1] + xhi;
+              const long long ay0 = box[a1][2] + F.ld_oy_min, ay1 = box[a1][3] + F.ld_oy_max;
+              const long long by0 = box[b1][2] + F.ld_oy_min, by1 = box[b1][3] + F.ld_oy_max;
+              const long long az0 = box[a1][4] + F.ld_oz_min, az1 = box[a1][5] + F.ld_oz_max;
+              const long long bz0 = box[b1][4] + F.ld_oz_min, bz1 = box[b1][5] + F.ld_oz_max;
+              // rows >= 2 apart share no line within a plane; across consecutive planes only if a box
+              // reaches the field's first / last row (p2 >= p1 * ext1), hence the y-ends condition
+              const bool y_inner = min(ay0, by0) >= 1 && max(ay1, by1) <= F.ext[1] - 2;
+              const bool sep_y = rows_ok && y_inner && (ay1 + 2 <= by0 || by1 + 2 <= ay0);
+              const bool sep_z = planes_ok && (az1 + 2 <= bz0 || bz1 + 2 <= az0);
+              // consecutive rows in memory can share a line only between a box reaching the row end and
+              // one reaching the row start
+              const bool a_end = ax1 > F.pitch[1] - 1 - D, a_start = ax0 < D;
+              const bool b_end = bx1 > F.pitch[1] - 1 - D, b_start = bx0 < D;
+              const bool wrap = (a_end && b_start) || (b_end && a_start);
+              const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
+              if (!(sep_y || sep_z || sep_x)) split = false;
+            }
         }
       }
-      for (int fi = 0; fi < K.n_fields && split; ++fi) {
-        const DField& F = K.f[fi];
-        if (!(F.kinds & 1)) continue;
-        int xlo = 0x7fffffff, xhi = -0x7fffffff;
-        for (int r = 0; r < F.n_runs; ++r) {
-          xlo = min(xlo, F.run_lo[r]);
-          xhi = max(xhi, F.run_hi[r]);
-        }
-        const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
-        const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
-        for (long long a1 = 0; a1 < kj && split; ++a1)
-          for (long long b1 = a1 + 1; b1 < kj && split; ++b1) {
-            const long long ax0 = box[a1][0] + xlo, ax1 = box[a1][1] + xhi, bx0 = box[b1][0] + xlo, bx1 = box[b1][1] + xhi;
-            const long long ay0 = box[a1][2] + F.ld_oy_min, ay1 = box[a1][3] + F.ld_oy_max;
-            const long long by0 = box[b1][2] + F.ld_oy_min, by1 = box[b1][3] + F.ld_oy_max;
-            const long long az0 = box[a1][4] + F.ld_oz_min, az1 = box[a1][5] + F.ld_oz_max;
-            const long long bz0 = box[b1][4] + F.ld_oz_min, bz1 = box[b1][5] + F.ld_oz_max;
-            // rows >= 2 apart share no line within a plane; across consecutive planes only if a box
-            // reaches the field's first / last row (p2 >= p1 * ext1), hence the y-ends condition
-            const bool y_inner = min(ay0, by0) >= 1 && max(ay1, by1) <= F.ext[1] - 2;
-            const bool sep_y = rows_ok && y_inner && (ay1 + 2 <= by0 || by1 + 2 <= ay0);
-            const bool sep_z = planes_ok && (az1 + 2 <= bz0 || bz1 + 2 <= az0);
-            // consecutive rows in memory can share a line only between a box reaching the row end and
-            // one reaching the row start
-            const bool a_end = ax1 > F.pitch[1] - 1 - D, a_start = ax0 < D;
-            const bool b_end = bx1 > F.pitch[1] - 1 - D, b_start = bx0 < D;
-            const bool wrap = (a_end && b_start) || (b_end && a_start);
-            const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
-            if (!(sep_y || sep_z || sep_x)) split = false;
+      if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
+        for (long long m = 0; m < kj; ++m) {
+          const long long Bm = S0 + m * nsm;
+          const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+          long long pl = 0;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+          const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+          const long long gslot = (long long)c * kSSlots + slot;
+          if (atomicAdd(scnt + gslot, 1u) == 0u) {
+            srep[gslot] = (unsigned long long)Bm;
+            slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
           }
+        }
+        if (grp) s_key[j] = 0ull;
+      } else if (grp && kj <= 32 && set_unclipped(P, S0, kj, nsm)) {
+        s_key[j] = set_shape_key(P, S0, kj, nsm);
+      } else {
+        if (grp) s_key[j] = 0ull;
+        dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
       }
     }
-    if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
-      for (long long m = 0; m < kj; ++m) {
-        const long long Bm = S0 + m * nsm;
-        const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
-        long long pl = 0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-        const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
-        const long long gslot = (long long)c * kSSlots + slot;
-        if (atomicAdd(scnt + gslot, 1u) == 0u) {
-          srep[gslot] = (unsigned long long)Bm;
-          slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
-        }
+    if (grp) {
+      // Multi-block sets evaluated directly, grouped by translation: two sets whose members are
+      // the same translate of each other (same count, unclipped, same line residue) have equal
+      // counts.  The smallest j of each group is evaluated, counted group-size times.
+      __syncthreads();
+      for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
+        const unsigned long long kj_key = s_key[j];
+        if (!kj_key) continue;
+        const long long kj = (P.W - j + nsm - 1) / nsm;
+        bool rep = true;
+        auto same = [&](long long i) {  // exact: same member count and the same translate
+          return s_key[i] == kj_key && (P.W - i + nsm - 1) / nsm == kj && set_translates(P, P.s + i, P.s + j, kj, nsm);
+        };
+        for (long long i = 0; i < j && rep; ++i)
+          if (same(i)) rep = false;
+        if (!rep) continue;
+        unsigned mult = 1;
+        for (long long i = j + 1; i < nset; ++i)
+          if (same(i)) ++mult;
+        dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | 0x80000000ull |
+                                            ((unsigned long long)(mult - 1) << 20) | (unsigned long long)j;
       }
-    } else {
-      dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
+      __syncthreads();
     }
   }
 }
@@ -1651,9 +1735,11 @@ __global__ void __launch_bounds__(256, WS_SCLASS_MINB) k_sclass(const DPlan* __r
       S0 = P.rep_B;
       kj = 1;
       mult = (unsigned long long)P.rep_mult;
-    } else {
-      S0 = P.s + low;
-      kj = (P.W - (long long)low + nsm - 1) / nsm;
+    } else {  // directly evaluated set j (grouped: bit 31, group size - 1 in bits 20..30)
+      const long long jj = (low & 0x80000000u) ? (long long)(low & 0xfffffu) : (long long)low;
+      if (low & 0x80000000u) mult = 1ull + ((low >> 20) & 0x7ffu);
+      S0 = P.s + jj;
+      kj = (P.W - jj + nsm - 1) / nsm;
     }
     unsigned long long ss, sl, un;
     int n_ld = 0;
