@@ -1523,10 +1523,36 @@ __device__ __forceinline__ void block_coord(const DPlan& P, long long B, long lo
   bc[1] = (B / P.G[0]) % P.G[1];
   bc[2] = B / (P.G[0] * P.G[1]);
 }
+// block-coordinate walk over a set's members (B -> B + nsm): adds and carries only
+struct MemberWalk {
+  long long ax, ay, az;  // nsm as (x, y, z) digits of the grid (az: whole grid planes)
+  __device__ __forceinline__ MemberWalk(const DPlan& P, long long nsm) {
+    ax = nsm % P.G[0];
+    ay = (nsm / P.G[0]) % P.G[1];
+    az = nsm / (P.G[0] * P.G[1]);
+  }
+  __device__ __forceinline__ void step(const DPlan& P, long long* bc) const {
+    bc[0] += ax;
+    long long cy = 0;
+    if (bc[0] >= P.G[0]) {
+      bc[0] -= P.G[0];
+      cy = 1;
+    }
+    bc[1] += ay + cy;
+    long long cz = 0;
+    if (bc[1] >= P.G[1]) {
+      bc[1] -= P.G[1];
+      cz = 1;
+    }
+    bc[2] += az + cz;
+  }
+};
 __device__ __forceinline__ bool set_unclipped(const DPlan& P, long long S0, long long kj, long long nsm) {
+  const MemberWalk mw(P, nsm);
+  long long bc[3];
+  block_coord(P, S0, bc);
   for (long long m = 0; m < kj; ++m) {
-    long long bc[3];
-    block_coord(P, S0 + m * nsm, bc);
+    if (m) mw.step(P, bc);
     if (clip_pattern(P, bc)) return false;
   }
   return true;
@@ -1541,12 +1567,13 @@ __device__ __forceinline__ long long set_residue(const DPlan& P, long long S0) {
 }
 // hash of (member count, residue, members' block offsets from the first member); never 0
 __device__ __forceinline__ unsigned long long set_shape_key(const DPlan& P, long long S0, long long kj, long long nsm) {
-  long long b0[3];
+  const MemberWalk mw(P, nsm);
+  long long b0[3], bc[3];
   block_coord(P, S0, b0);
+  bc[0] = b0[0], bc[1] = b0[1], bc[2] = b0[2];
   unsigned long long h = 0x9e3779b97f4a7c15ull ^ ((unsigned long long)kj << 8) ^ (unsigned long long)set_residue(P, S0);
   for (long long m = 1; m < kj; ++m) {
-    long long bc[3];
-    block_coord(P, S0 + m * nsm, bc);
+    mw.step(P, bc);
     for (int d = 0; d < 3; ++d) {
       h ^= (unsigned long long)(bc[d] - b0[d]) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
       h *= 0xff51afd7ed558ccdull;
@@ -1557,13 +1584,14 @@ __device__ __forceinline__ unsigned long long set_shape_key(const DPlan& P, long
 // exact check: every member of set S1 is the same block translate of S0's member (same count)
 __device__ __forceinline__ bool set_translates(const DPlan& P, long long S0, long long S1, long long kj, long long nsm) {
   if (set_residue(P, S0) != set_residue(P, S1)) return false;
-  long long a0[3], b0[3];
+  const MemberWalk mw(P, nsm);
+  long long a0[3], b0[3], a[3], b[3];
   block_coord(P, S0, a0);
   block_coord(P, S1, b0);
+  for (int d = 0; d < 3; ++d) a[d] = a0[d], b[d] = b0[d];
   for (long long m = 1; m < kj; ++m) {
-    long long a[3], b[3];
-    block_coord(P, S0 + m * nsm, a);
-    block_coord(P, S1 + m * nsm, b);
+    mw.step(P, a);
+    mw.step(P, b);
     for (int d = 0; d < 3; ++d)
       if (a[d] - a0[d] != b[d] - b0[d]) return false;
   }
@@ -1575,7 +1603,7 @@ __device__ __forceinline__ bool set_translates(const DPlan& P, long long S0, lon
 // pattern of the block x residue of its first cell's address mod line_bytes (identical
 // active-cell boxes that are translates by a multiple of the line size have identical
 // sector and line counts).  Multi-block sets are appended to the direct list.
-__global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+__global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                                const DKernel* __restrict__ ks,
                                                const DGpu* __restrict__ gs, unsigned int* __restrict__ scnt,
                                                unsigned long long* __restrict__ srep,
@@ -1583,6 +1611,8 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
                                                unsigned long long* __restrict__ slist,
                                                unsigned long long* __restrict__ dlist) {
   __shared__ unsigned long long s_key[kSetGrp];  // directly evaluated sets: shape key (0: not grouped)
+  __shared__ unsigned s_cnt[kSetGrp];            // group sizes (at the group's smallest member)
+  __shared__ short s_rep[kSetGrp];               // smallest member of the set's group
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const DPlan& P = plans[c];
     const long long nset = pre[c + 1].set - pre[c].set;
@@ -1673,20 +1703,27 @@ __global__ void __launch_bounds__(256) k_smset(const DPlan* __restrict__ plans, 
       // the same translate of each other (same count, unclipped, same line residue) have equal
       // counts.  The smallest j of each group is evaluated, counted group-size times.
       __syncthreads();
+      for (long long j = threadIdx.x; j < nset; j += blockDim.x) s_cnt[j] = 0u;
+      __syncthreads();
+      // every grouped set finds its group's smallest member (usually one verification) and
+      // counts itself there
       for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
         const unsigned long long kj_key = s_key[j];
         if (!kj_key) continue;
         const long long kj = (P.W - j + nsm - 1) / nsm;
-        bool rep = true;
-        auto same = [&](long long i) {  // exact: same member count and the same translate
-          return s_key[i] == kj_key && (P.W - i + nsm - 1) / nsm == kj && set_translates(P, P.s + i, P.s + j, kj, nsm);
-        };
-        for (long long i = 0; i < j && rep; ++i)
-          if (same(i)) rep = false;
-        if (!rep) continue;
-        unsigned mult = 1;
-        for (long long i = j + 1; i < nset; ++i)
-          if (same(i)) ++mult;
+        long long r = j;
+        for (long long i = 0; i < j; ++i)
+          if (s_key[i] == kj_key && (P.W - i + nsm - 1) / nsm == kj && set_translates(P, P.s + i, P.s + j, kj, nsm)) {
+            r = i;
+            break;
+          }
+        s_rep[j] = (short)r;
+        atomicAdd(&s_cnt[r], 1u);
+      }
+      __syncthreads();
+      for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
+        if (!s_key[j] || s_rep[j] != j) continue;
+        const unsigned mult = s_cnt[j];
         dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | 0x80000000ull |
                                             ((unsigned long long)(mult - 1) << 20) | (unsigned long long)j;
       }
@@ -1701,10 +1738,11 @@ __global__ void __launch_bounds__(256, WS_SCLASS_MINB) k_sclass(const DPlan* __r
                                                 const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
                                                 const unsigned int* __restrict__ scnt,
                                                 const unsigned long long* __restrict__ srep,
-                                                const unsigned long long* __restrict__ lists,
+                                                unsigned long long* __restrict__ lists,
                                                 const unsigned long long* __restrict__ slist,
                                                 const unsigned long long* __restrict__ dlist,
                                                 unsigned long long* __restrict__ work) {
+  __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ SmBox32 s_mb32[kMaxMembers];
   __shared__ Tri s_pt[2 * kMaxPlanes];
@@ -1714,11 +1752,18 @@ __global__ void __launch_bounds__(256, WS_SCLASS_MINB) k_sclass(const DPlan* __r
   __shared__ int s_ng;
   __shared__ long long s_box[4];
   __shared__ Tri s_red[(kRowThreads / 32) * 2];
-  const long long ncls = (long long)lists[1];
-  const long long total = ncls + (long long)lists[2];
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const bool cls = item < ncls;
-    const unsigned long long ent = cls ? slist[item] : dlist[item - ncls];
+  const long long ncls = (long long)lists[1], ndir = (long long)lists[2];
+  const long long total = ncls + ndir;
+  // dynamic scheduling (lists[3], zeroed by the plan's scan): the directly evaluated sets --
+  // the expensive, uneven entries -- first, then the single-block class representatives
+  for (;;) {
+    if (threadIdx.x == 0) s_item = (long long)atomicAdd(lists + 3, 1ull);
+    __syncthreads();
+    const long long item = s_item;
+    __syncthreads();  // s_item is rewritten by the next fetch
+    if (item >= total) break;
+    const bool cls = item >= ndir;
+    const unsigned long long ent = cls ? slist[item - ndir] : dlist[item];
     const int c = (int)(ent >> 32);
     const unsigned low = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
@@ -2644,7 +2689,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
   end(K_FOLD, b);
   beg(K_SMSET, a);
-  k_smset<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
+  k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
   end(K_SMSET, a);
   beg(K_SCLASS, a);
   k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, 256, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
