@@ -412,6 +412,25 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
     if (G.g_end > G.g_begin) chunks += G.ext[2];  // k_rows chunks are >= 1 z-plane each
   }
   D.n_groups = ng;
+  {
+    DLoadEnv& E = D.env;
+    E.spy = E.spz = 0;
+    E.oy_min = E.ext1_min = E.row_bytes_min = E.plane_bytes_min = INT64_MAX;
+    E.oy_max = INT64_MIN;
+    E.has_load = 0;
+    for (int fi = 0; fi < D.n_fields; ++fi) {
+      const DField& F = D.f[fi];
+      if (!(F.kinds & 1)) continue;
+      E.has_load = 1;
+      E.spy = std::max<int64_t>(E.spy, F.ld_oy_max - F.ld_oy_min);
+      E.spz = std::max<int64_t>(E.spz, F.ld_oz_max - F.ld_oz_min);
+      E.oy_min = std::min<int64_t>(E.oy_min, F.ld_oy_min);
+      E.oy_max = std::max<int64_t>(E.oy_max, F.ld_oy_max);
+      E.ext1_min = std::min<int64_t>(E.ext1_min, F.ext[1]);
+      E.row_bytes_min = std::min<int64_t>(E.row_bytes_min, F.pitch[1] << F.lg_elem);
+      E.plane_bytes_min = std::min<int64_t>(E.plane_bytes_min, F.pitch[2] << F.lg_elem);
+    }
+  }
   c->hk.push_back(D);
   c->chunk_bound.push_back(chunks);
   c->dirty = true;

@@ -36,9 +36,17 @@ struct DGroup {
   int32_t field, kind, oy, oz, run, pad;
 };
 
+// load-offset envelope over the load fields (k_smset's quick separation test)
+struct DLoadEnv {
+  int64_t spy, spz;                   // max over load fields of ld_oy/oz_max - ld_oy/oz_min
+  int64_t oy_min, oy_max, ext1_min;   // min / max load oy, min ext[1]
+  int64_t row_bytes_min, plane_bytes_min;
+  int32_t has_load, pad;
+};
 struct DKernel {
   int32_t n_fields, n_acc, n_groups, regs;
   int64_t lo[3], hi[3];
+  DLoadEnv env;
   double flops, cells;
   DField f[kMaxFields];
   ws_access acc[kMaxAcc];

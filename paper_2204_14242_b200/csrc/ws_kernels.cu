@@ -1523,6 +1523,17 @@ __device__ __forceinline__ void block_coord(const DPlan& P, long long B, long lo
   bc[1] = (B / P.G[0]) % P.G[1];
   bc[2] = B / (P.G[0] * P.G[1]);
 }
+// load-offset envelope of a kernel's load fields (k_smset's quick separation test)
+struct SetEnv {
+  long long spy, spz, oy_min, oy_max, ext1_min;
+  bool rows_ok, planes_ok;
+};
+__device__ __forceinline__ SetEnv set_env(const DKernel& K, long long lb) {
+  const DLoadEnv& E = K.env;  // precomputed by ws_describe_kernel
+  SetEnv e{E.spy, E.spz, E.oy_min, E.oy_max, E.ext1_min, E.has_load && E.row_bytes_min >= lb,
+           E.has_load && E.plane_bytes_min >= lb};
+  return e;
+}
 // block-coordinate walk over a set's members (B -> B + nsm): adds and carries only
 struct MemberWalk {
   long long ax, ay, az;  // nsm as (x, y, z) digits of the grid (az: whole grid planes)
@@ -1618,6 +1629,7 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
     const long long nset = pre[c + 1].set - pre[c].set;
     const long long nsm = gs[P.gid].g.n_sm;
     const bool grp = nset <= kSetGrp && P.scls_R > 0 && !P.rep_mult;
+    const SetEnv env = set_env(ks[P.kid], gs[P.gid].g.line_bytes);
     for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
       const long long S0 = P.s + j;
       const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
@@ -1635,27 +1647,38 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
         const long long lb = gs[P.gid].g.line_bytes;
         split = true;
         long long box[32][6];
+        const MemberWalk mw(P, nsm);
+        long long bc[3];
+        block_coord(P, S0, bc);
         for (long long m = 0; m < kj; ++m) {
-          const long long Bm = S0 + m * nsm;
-          const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+          if (m) mw.step(P, bc);
           for (int d = 0; d < 3; ++d) {
             box[m][2 * d] = P.lo[d] + bc[d] * P.BF[d];
             long long hi = box[m][2 * d] + P.BF[d];
             box[m][2 * d + 1] = (hi > P.hi[d] ? P.hi[d] : hi) - 1;
           }
         }
-        for (int fi = 0; fi < K.n_fields && split; ++fi) {
-          const DField& F = K.f[fi];
-          if (!(F.kinds & 1)) continue;
-          int xlo = 0x7fffffff, xhi = -0x7fffffff;
-          for (int r = 0; r < F.n_runs; ++r) {
-            xlo = min(xlo, F.run_lo[r]);
-            xhi = max(xhi, F.run_hi[r]);
-          }
-          const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
-          const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
-          for (long long a1 = 0; a1 < kj && split; ++a1)
-            for (long long b1 = a1 + 1; b1 < kj && split; ++b1) {
+        // pairs outer: a pair separated in z (or in y, away from the fields' first / last rows)
+        // by the load-offset envelope of all fields (one pitch for all fields under scls_R) is
+        // separated for every field; otherwise the fields are checked one by one
+        for (long long a1 = 0; a1 < kj && split; ++a1)
+          for (long long b1 = a1 + 1; b1 < kj && split; ++b1) {
+            if (env.planes_ok && (box[b1][4] - box[a1][5] >= 2 + env.spz || box[a1][4] - box[b1][5] >= 2 + env.spz))
+              continue;
+            if (env.rows_ok && min(box[a1][2], box[b1][2]) + env.oy_min >= 1 &&
+                max(box[a1][3], box[b1][3]) + env.oy_max <= env.ext1_min - 2 &&
+                (box[b1][2] - box[a1][3] >= 2 + env.spy || box[a1][2] - box[b1][3] >= 2 + env.spy))
+              continue;
+            for (int fi = 0; fi < K.n_fields && split; ++fi) {
+              const DField& F = K.f[fi];
+              if (!(F.kinds & 1)) continue;
+              int xlo = 0x7fffffff, xhi = -0x7fffffff;
+              for (int r = 0; r < F.n_runs; ++r) {
+                xlo = min(xlo, F.run_lo[r]);
+                xhi = max(xhi, F.run_hi[r]);
+              }
+              const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
+              const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
               const long long ax0 = box[a1][0] + xlo, ax1 = box[a1][1] + xhi, bx0 = box[b1][0] + xlo, bx1 = box[b1][1] + xhi;
               const long long ay0 = box[a1][2] + F.ld_oy_min, ay1 = box[a1][3] + F.ld_oy_max;
               const long long by0 = box[b1][2] + F.ld_oy_min, by1 = box[b1][3] + F.ld_oy_max;
@@ -1674,7 +1697,7 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
               const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
               if (!(sep_y || sep_z || sep_x)) split = false;
             }
-        }
+          }
       }
       if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
         for (long long m = 0; m < kj; ++m) {
