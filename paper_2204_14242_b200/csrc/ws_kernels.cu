@@ -2299,12 +2299,14 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
                                               const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                               const DRowInfo* __restrict__ rowinfo,
                                               const long long* __restrict__ chunkres,
-                                              unsigned long long* __restrict__ acc) {
+                                              unsigned long long* __restrict__ acc, int mode) {
   const long long total = pre[n].fold;
   const int lane = threadIdx.x & 31;
-  // few items with many planes each (BJ configs[1]: 336 items x ~520 planes): one CTA per item;
-  // many items (LBM: 58 fields per config): one warp per item
-  if (total > 0 && pre[n].chunk / total > 256) {
+  // items (config, field) <= CTAs (BJ configs[1]: 336 items x ~40 planes): one CTA per item (all
+  // items at once, 256 threads each); more items (LBM: 58 fields per config): one warp per item.
+  // (A/B on B200: 0.202 vs 0.212 ms per configs[1] step; LBM15 0.238 vs 0.284 ms the other way.)
+  // mode: 0 = that choice, 1 = CTA, 2 = warp (WS_FOLD_MODE, diagnostics)
+  if (mode == 1 || (mode == 0 && total <= gridDim.x)) {
     fold_cta(plans, pre, n, ks, gs, rowinfo, chunkres, acc);
     return;
   }
@@ -2709,7 +2711,8 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_rows<<<n_sm_dev * WS_PERSIST_ROWS, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
   end(K_ROWS, b);
   beg(K_FOLD, b);
-  k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc);
+  static const int fold_mode = getenv("WS_FOLD_MODE") ? atoi(getenv("WS_FOLD_MODE")) : 0;  // diagnostics
+  k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc, fold_mode);
   end(K_FOLD, b);
   beg(K_SMSET, a);
   k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
