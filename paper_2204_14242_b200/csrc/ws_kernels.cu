@@ -1403,12 +1403,12 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
         unsigned mine = 0;  // planes of this window whose rank % nwp == wid
         {
           unsigned q = cm;
-          int r = rank0;
+          int rm = rank0 % nwp;  // rank mod nwp, advanced incrementally
           while (q) {
             const int b = __ffs(q) - 1;
             q &= q - 1;
-            if (r % nwp == wid) mine |= 1u << b;
-            ++r;
+            if (rm == wid) mine |= 1u << b;
+            rm = rm + 1 == nwp ? 0 : rm + 1;
           }
         }
         rank0 += __popc(cm);
@@ -1489,8 +1489,11 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
       // (c) ordered fold by the whole CTA: a derived plane is its computed source plane (p - m*per,
       //     the nearest non-derived one) translated by m*per planes; threads take contiguous planes,
       //     then an ordered CTA reduction
-      {
-        const int ppl = (np + (int)blockDim.x - 1) / (int)blockDim.x;
+      // (few planes -- single blocks: warp 0 alone, no CTA barriers)
+      const bool one_warp = np <= 64;
+      if (!one_warp || wid == 0) {
+        const int nthr = one_warp ? 32 : (int)blockDim.x;
+        const int ppl = (np + nthr - 1) / nthr;
         Tri t2[2] = {tri_empty(), tri_empty()};
         for (int p = tid * ppl; p < np && p < (tid + 1) * ppl; ++p) {
           int q = p;
@@ -1500,8 +1503,12 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
           t2[0] = tri_combine(t2[0], a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty());
           t2[1] = tri_combine(t2[1], b.c ? Tri{b.f + (dsh >> ll), b.l + (dsh >> ll), b.c} : tri_empty());
         }
-        __shared__ Tri s_fold[(256 / 32) * 2];
-        cta_ordered_reduce<2>(t2, s_fold);
+        if (one_warp) {
+          warp_ordered_reduce<2>(t2);
+        } else {
+          __shared__ Tri s_fold[(256 / 32) * 2];
+          cta_ordered_reduce<2>(t2, s_fold);
+        }
         if (tid == 0) {
           cs_all = tri_combine(cs_all, t2[0]);
           cl_all = tri_combine(cl_all, t2[1]);
