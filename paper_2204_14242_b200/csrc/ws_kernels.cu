@@ -3994,7 +3994,7 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   }
   tr.erase(std::remove_if(tr.begin(), tr.end(), [](const DSimTrace& T) { return T.n < 0; }), tr.end());
   // warp-path state in batches of bounded device memory (streams are independent)
-  const long long kBatchBytes = 24ll << 30;
+  const long long kBatchBytes = 8ll << 30;
   std::vector<std::pair<size_t, size_t>> batches;  // [first, last) into tr (sorted by n below)
   std::vector<int64_t> wld_off(2 * (size_t)n, 0);
   long long wld_total = 0;
@@ -4091,15 +4091,24 @@ int run_simulate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, con
   if (!longs.empty()) {
     std::vector<std::pair<size_t, size_t>> pbat;
     {
+      // positions per batch: < 2^31, and within 85 % of the free device memory at ~72 bytes
+      // per position (request copy, ids, radix buffers, wavelet values and levels, distances,
+      // flags) plus the streams' hash tables
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const long long kPosBytes = 72;
+      const long long cap_mem = (long long)(0.85 * (double)free_b);
       size_t first = 0;
-      long long tot_n = 0;
+      long long tot_n = 0, tot_h = 0;
       for (size_t t = 0; t < longs.size(); ++t) {
-        if (t > first && (tot_n + longs[t].n >= (1ll << 31) - 2 || t - first >= 4096)) {
+        const long long n2 = tot_n + longs[t].n, h2 = tot_h + longs[t].hcap;
+        if (t > first && (n2 >= (1ll << 31) - 2 || t - first >= 4096 || n2 * kPosBytes + h2 * 12 > cap_mem)) {
           pbat.push_back({first, t});
           first = t;
-          tot_n = 0;
+          tot_n = tot_h = 0;
         }
         tot_n += longs[t].n;
+        tot_h += longs[t].hcap;
       }
       pbat.push_back({first, longs.size()});
     }
