@@ -436,6 +436,30 @@ def test_sim_full_size_sampled(ctx):
     sim_parity(ctx, k, gp, cf, caps, "simfull")
 
 
+def test_sim_full_space_512_properties(ctx):
+    """The whole 168-config space at 512^3 (the NEXT-1 calibration size; memory-bounded batches
+    of the parallel path) x 4 capacities: LRU inclusion (misses never grow with the capacity),
+    compulsory <= misses <= requests, residency <= overlap, hit rates in [0, 1]."""
+    from paper_2204_14242_b200 import config_array
+    k, gp = W.k25(512), W.gpu_a100()
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(gp)
+    caps = [gp["l1_bytes"], gp["l2_bytes"] // 8, gp["l2_bytes"] // 2, 2 * gp["l2_bytes"]]
+    rows = ctx.simulate(config_array(kid, gid, W.space_stencil_paper()), caps)
+    for i, row in enumerate(rows):
+        assert all(r["status"] == 0 for r in row), i
+        for key in ("l1", "st"):
+            m = [r[f"{key}_misses"] for r in row]
+            assert all(a >= b for a, b in zip(m, m[1:])), (i, key, m)
+            assert row[0][f"{key}_compulsory"] <= m[-1] and m[0] <= row[0][f"{key}_requests"], (i, key)
+        for a, b in zip(row, row[1:]):
+            assert b["y_resident"] >= a["y_resident"] and b["z_resident"] >= a["z_resident"], i
+        for r in row:
+            assert r["y_resident"] <= r["ov_y"] and r["z_resident"] <= r["ov_z_only"], i
+            for f in ("R_l1", "R_y", "R_z", "R_st"):
+                assert 0.0 <= r[f] <= 1.0 + 1e-12, (i, f, r[f])
+    ctx.sim_release()
+
+
 # ----------------------------------------------------------------- NEXT-2: validation kernel
 def _st_run(ctx, n, block, fold, seed=0):
     import torch
