@@ -47,6 +47,9 @@
 #ifndef WS_SCLASS_MINB
 #define WS_SCLASS_MINB 3
 #endif
+#ifndef WS_SCLASS_THREADS
+#define WS_SCLASS_THREADS 256  // threads per k_sclass CTA (<= 256: shared arrays sized for 8 warps)
+#endif
 #ifndef WS_FOLD_MINB
 #define WS_FOLD_MINB 4
 #endif
@@ -1085,7 +1088,7 @@ __device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long
     const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
     const int le = F.lg_elem;
     Tri carry_s = tri_empty(), carry_l = tri_empty();
-    for (long long base = 0; base < rows; base += (long long)kRowThreads * kRowsPerThread) {
+    for (long long base = 0; base < rows; base += (long long)blockDim.x * kRowsPerThread) {
       Tri t[2] = {tri_empty(), tri_empty()};
       for (int u = 0; u < kRowsPerThread; ++u) {
         const long long i = base + (long long)tid * kRowsPerThread + u;
@@ -1764,7 +1767,7 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
 
 // Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
 // directly evaluated multi-block SM sets.
-__global__ void __launch_bounds__(256, WS_SCLASS_MINB) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+__global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
                                                 const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
                                                 const unsigned int* __restrict__ scnt,
                                                 const unsigned long long* __restrict__ srep,
@@ -2725,7 +2728,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
   end(K_SMSET, a);
   beg(K_SCLASS, a);
-  k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, 256, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
+  k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
   end(K_SCLASS, a);
   beg(K_WARP, m);
   k_warp<<<persist, 256, 0, m>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
