@@ -547,6 +547,13 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
                                               unsigned long long* __restrict__ lists) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
+#ifdef WS_PLAN_CLOCK
+  long long clk[12];
+  int nclk = 0;
+#define PLAN_MARK() if (tid == 0) clk[nclk++] = clock64();
+#else
+#define PLAN_MARK()
+#endif
   __shared__ DPlan P;
   __shared__ DKernel sK;   // this configuration's kernel and GPU descriptors, staged once: the
   __shared__ DGpu sG;      // serial plan work then reads shared memory, not dependent global loads
@@ -558,6 +565,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   static_assert(sizeof(DPlan) % 16 == 0 && sizeof(DKernel) % 16 == 0 && sizeof(DGpu) % 16 == 0, "uint4 copies");
   constexpr int kPlanVec = (int)(sizeof(DPlan) / 16);
   for (int i = tid; i < kPlanVec; i += blockDim.x) reinterpret_cast<uint4*>(&P)[i] = make_uint4(0u, 0u, 0u, 0u);
+  PLAN_MARK()
   const ws_config cf = cfgs[c];
   const bool ids_ok = cf.kernel_id < (uint32_t)nk && cf.gpu_id < (uint32_t)ng;
   if (ids_ok) {
@@ -566,6 +574,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     const uint4* srcG = reinterpret_cast<const uint4*>(gs + cf.gpu_id);
     for (int i = tid; i < (int)(sizeof(DGpu) / 16); i += blockDim.x) reinterpret_cast<uint4*>(&sG)[i] = srcG[i];
   }
+  PLAN_MARK()
   __syncthreads();
   if (tid == 0) {
     if (ids_ok) {
@@ -579,6 +588,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     }
   }
   __syncthreads();
+  PLAN_MARK()
   __shared__ int s_last;
   auto store_plan = [&]() {  // cooperative 16-byte copy of the shared plan; the last CTA to finish
     uint4* dst = reinterpret_cast<uint4*>(plans + c);  // scans the work counts of every config
@@ -599,9 +609,11 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     store_plan();
     return;
   }
+  PLAN_MARK()
   if (tid < 5) plan_range(P, tid);
   __syncthreads();
   if (tid == 0) plan_boundaries(P);
+  PLAN_MARK()
   const DKernel& K = sK;
   const int fc = P.fcube;
   const int np = K.n_acc * fc;
@@ -626,20 +638,30 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     s_first[p] = first;
   }
   __syncthreads();
+  PLAN_MARK()
   // block-wide exclusive prefix of s_first (contiguous segments per thread)
   const int seg = (np + blockDim.x - 1) / blockDim.x;
   int mysum = 0;
   for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) mysum += s_first[p];
-  s_part[tid] = mysum;
-  __syncthreads();
-  if (tid == 0) {
-    int run = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      int v = s_part[i];
-      s_part[i] = run;
-      run += v;
+  {  // exclusive scan over the 128 threads: warp shuffles, then the 4 warp totals
+    const int lane = tid & 31, wid = tid >> 5;
+    int v = mysum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) v += u;
     }
-    s_total = run;
+    if (lane == 31) s_part[wid] = v;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int x = s_part[w];
+      if (w < wid) off += x;
+      tot += x;
+    }
+    __syncthreads();
+    s_part[tid] = off + v - mysum;
+    if (tid == 0) s_total = tot;
   }
   __syncthreads();
   if (s_total > kMaxInstr) {
@@ -680,6 +702,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
       ++pos;
     }
   }
+  PLAN_MARK()
   // ---- row boxes of the wave + layer-set footprint, per field
   for (int fi = tid; fi < K.n_fields; fi += blockDim.x) {
     const DField& F = K.f[fi];
@@ -732,7 +755,16 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     P.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
   }
   __syncthreads();
+  PLAN_MARK()
   store_plan();
+  PLAN_MARK()
+#ifdef WS_PLAN_CLOCK
+  if (tid == 0 && (c == 0 || c == n - 1 || s_last)) {
+    printf("PLANCLK c=%d last=%d", c, (int)s_last);
+    for (int i = 1; i < nclk; ++i) printf(" %lld", clk[i] - clk[i - 1]);
+    printf(" total %lld\n", clk[nclk - 1] - clk[0]);
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ scan of work counts
