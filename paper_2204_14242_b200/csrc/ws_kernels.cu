@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstddef>
 #include <cstdint>
 #include <cstring>
 #include <chrono>
@@ -569,8 +570,18 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   const ws_config cf = cfgs[c];
   const bool ids_ok = cf.kernel_id < (uint32_t)nk && cf.gpu_id < (uint32_t)ng;
   if (ids_ok) {
+    // only the used parts of the kernel descriptor (21 KB in full): header, fields, accesses,
+    // groups, each range widened to 16-byte units
     const uint4* srcK = reinterpret_cast<const uint4*>(ks + cf.kernel_id);
-    for (int i = tid; i < (int)(sizeof(DKernel) / 16); i += blockDim.x) reinterpret_cast<uint4*>(&sK)[i] = srcK[i];
+    uint4* dstK = reinterpret_cast<uint4*>(&sK);
+    const DKernel* hk = ks + cf.kernel_id;
+    const int nf = hk->n_fields, na = hk->n_acc, ngr = hk->n_groups;
+    const size_t rl[4] = {0, offsetof(DKernel, f), offsetof(DKernel, acc), offsetof(DKernel, g)};
+    const size_t rh[4] = {offsetof(DKernel, f), offsetof(DKernel, f) + nf * sizeof(DField),
+                          offsetof(DKernel, acc) + na * sizeof(ws_access), offsetof(DKernel, g) + ngr * sizeof(DGroup)};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      for (int i = (int)(rl[r] / 16) + tid; i < (int)((rh[r] + 15) / 16); i += blockDim.x) dstK[i] = srcK[i];
     const uint4* srcG = reinterpret_cast<const uint4*>(gs + cf.gpu_id);
     for (int i = tid; i < (int)(sizeof(DGpu) / 16); i += blockDim.x) reinterpret_cast<uint4*>(&sG)[i] = srcG[i];
   }
