@@ -2,7 +2,7 @@
 //
 //   k_plan   (a1)  one CTA per configuration: geometry, wave, SM sets, layer sets,
 //                  fold-deduplicated instruction table, row boxes, work counts.
-//   k_scan         exclusive prefix of the per-config work counts (one CTA).
+//   (scan)         exclusive prefix of the per-config work counts: k_plan's last CTA.
 //   k_warp   (a2+a3) one warp per (config, wave warp): addresses of every lane and
 //                  instruction, unique sectors per warp instruction (lanes are
 //                  address-sorted, so a shuffle against the previous issuing lane
@@ -532,11 +532,6 @@ __device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __res
   if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
 }
 
-__global__ void __launch_bounds__(1024) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
-                                               unsigned long long* __restrict__ work,
-                                               unsigned long long* __restrict__ lists) {
-  scan_body(plans, n, pre, work, lists);
-}
 
 __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs, int n,
                                               const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
