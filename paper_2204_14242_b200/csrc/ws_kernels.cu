@@ -2609,22 +2609,13 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
 // ------------------------------------------------------------------ a7: model (FP64)
 __device__ __forceinline__ double gompertz(const double* abc, double O) { return abc[0] * exp(-abc[1] * exp(-abc[2] * O)); }
 
-__global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, int n, const DKernel* __restrict__ ks,
-                                               const DGpu* __restrict__ gs, const unsigned long long* __restrict__ acc,
-                                               ws_result* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const DPlan& P = plans[c];
-  ws_result R;
+__device__ __noinline__ void model_one(const DPlan& P, const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                       const unsigned long long* a, ws_result& R) {
   memset(&R, 0, sizeof(R));
   R.status = P.status;
-  if (P.status != WS_OK) {
-    out[c] = R;
-    return;
-  }
+  if (P.status != WS_OK) return;
   const DKernel& K = ks[P.kid];
   const DGpu& G = gs[P.gid];
-  const unsigned long long* a = acc + (long long)c * A_N;
   for (int d = 0; d < 3; ++d) R.grid[d] = (uint32_t)P.G[d];
   R.k = (uint32_t)P.k;
   R.wave_blocks = (uint32_t)P.W;
@@ -2688,7 +2679,26 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
   const double tm = fmax(fmax(R.t_l1, R.t_link), fmax(R.t_l2, R.t_dram));
   R.limiter = R.t_dram >= tm ? 2u : (R.t_l2 >= tm ? 1u : (R.t_link >= tm ? 3u : 0u));
   R.t_pred = tm * K.cells;
-  out[c] = R;
+}
+
+// one warp per configuration: the accumulators in by the lanes, the model by lane 0, the
+// 336-byte record out by the lanes (coalesced)
+__global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, int n, const DKernel* __restrict__ ks,
+                                               const DGpu* __restrict__ gs, const unsigned long long* __restrict__ acc,
+                                               ws_result* __restrict__ out) {
+  static_assert(sizeof(ws_result) % 8 == 0 && A_N <= 32, "record copy / accumulator lanes");
+  __shared__ unsigned long long s_a[4][A_N];
+  __shared__ ws_result s_r[4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + w;
+  if (c >= n) return;
+  if (lane < A_N) s_a[w][lane] = acc[(long long)c * A_N + lane];
+  __syncwarp();
+  if (lane == 0) model_one(plans[c], ks, gs, s_a[w], s_r[w]);
+  __syncwarp();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s_r[w]);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(out + c);
+  for (int i = lane; i < (int)(sizeof(ws_result) / 8); i += 32) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------ a8: rank
@@ -2784,7 +2794,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   cudaStreamWaitEvent(m, st.join[0], 0);
   cudaStreamWaitEvent(m, st.join[1], 0);
   beg(K_MODEL, m);
-  k_model<<<(n + 127) / 128, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out);
+  k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out);
   end(K_MODEL, m);
   if (launches) *launches = L;
   return check_launch();
