@@ -550,9 +550,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
 #else
 #define PLAN_MARK()
 #endif
-  __shared__ DPlan P;
-  __shared__ DKernel sK;   // this configuration's kernel and GPU descriptors, staged once: the
-  __shared__ DGpu sG;      // serial plan work then reads shared memory, not dependent global loads
+  __shared__ __align__(16) DPlan P;
+  __shared__ __align__(16) DKernel sK;   // this configuration's kernel and GPU descriptors, staged once: the
+  __shared__ __align__(16) DGpu sG;      // serial plan work then reads shared memory, not dependent global loads
 
   __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
   __shared__ int s_part[128];
@@ -2609,13 +2609,12 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
 // ------------------------------------------------------------------ a7: model (FP64)
 __device__ __forceinline__ double gompertz(const double* abc, double O) { return abc[0] * exp(-abc[1] * exp(-abc[2] * O)); }
 
-__device__ __noinline__ void model_one(const DPlan& P, const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+__device__ __noinline__ void model_one(const DPlan& P, const DKernel* __restrict__ ks, const DGpu& G,
                                        const unsigned long long* a, ws_result& R) {
   memset(&R, 0, sizeof(R));
   R.status = P.status;
   if (P.status != WS_OK) return;
   const DKernel& K = ks[P.kid];
-  const DGpu& G = gs[P.gid];
   for (int d = 0; d < 3; ++d) R.grid[d] = (uint32_t)P.G[d];
   R.k = (uint32_t)P.k;
   R.wave_blocks = (uint32_t)P.W;
@@ -2689,12 +2688,26 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
   static_assert(sizeof(ws_result) % 8 == 0 && A_N <= 32, "record copy / accumulator lanes");
   __shared__ unsigned long long s_a[4][A_N];
   __shared__ ws_result s_r[4];
+  __shared__ __align__(16) DPlan s_p[4];  // plan and GPU descriptor staged by the lanes (one load round)
+  __shared__ __align__(16) DGpu s_gp[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + w;
   if (c >= n) return;
   if (lane < A_N) s_a[w][lane] = acc[(long long)c * A_N + lane];
+  {
+    const uint4* sp = reinterpret_cast<const uint4*>(plans + c);
+    uint4* dp = reinterpret_cast<uint4*>(&s_p[w]);
+    for (int i = lane; i < (int)(sizeof(DPlan) / 16); i += 32) dp[i] = sp[i];
+  }
   __syncwarp();
-  if (lane == 0) model_one(plans[c], ks, gs, s_a[w], s_r[w]);
+  {
+    const int gid = s_p[w].status == WS_OK ? s_p[w].gid : 0;
+    const uint4* sg = reinterpret_cast<const uint4*>(gs + gid);
+    uint4* dg = reinterpret_cast<uint4*>(&s_gp[w]);
+    for (int i = lane; i < (int)(sizeof(DGpu) / 16); i += 32) dg[i] = sg[i];
+  }
+  __syncwarp();
+  if (lane == 0) model_one(s_p[w], ks, s_gp[w], s_a[w], s_r[w]);
   __syncwarp();
   const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s_r[w]);
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(out + c);
