@@ -530,6 +530,14 @@ def test_extended_space_multiblock_sets(ctx):
         assert_parity(ctx, k, dict(W.gpu_a100(), n_sm=24), sp, "ext")
 
 
+def test_extended_space_grouped_sets_full_a100(ctx):
+    """Extended-space configurations with 64-256-thread blocks on 96^3 with the full A100 (108
+    SMs, k up to 16 blocks per SM): multi-block SM sets grouped by translation in k_smset (group
+    sizes > 1) and fetched dynamically by k_sclass -- every count against the oracle."""
+    sp = [c for c in W.space_extended() if c[0][0] * c[0][1] * c[0][2] <= 256][::60][:6]
+    assert_parity(ctx, W.k25(96), W.gpu_a100(), sp, "ext96")
+
+
 @pytest.mark.parametrize("mode", ["all", "0"])
 def test_sim_parallel_path_matches_oracle(ctx, mode):
     """The parallel offline path (wavelet-matrix stack distances) forced on every stream, and the
