@@ -147,6 +147,8 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   const size_t o_wrep = off;    off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
   const size_t o_scnt = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned int));
   const size_t o_srep = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
+  const size_t o_skey = off;    off = align_up(off + (size_t)kShareTab * sizeof(unsigned long long));
+  const size_t o_sval = off;    off = align_up(off + (size_t)kShareTab * 2 * sizeof(unsigned long long));
   const size_t o_work = off;    off = align_up(off + 16 * sizeof(unsigned long long));
   static_assert(K_NKINDS <= 16, "work slots");
   const size_t o_lists = off;   off = align_up(off + 4 * sizeof(unsigned long long));
@@ -176,6 +178,8 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   s.wrep = (unsigned long long*)(b + o_wrep);
   s.scnt = (unsigned int*)(b + o_scnt);
   s.srep = (unsigned long long*)(b + o_srep);
+  s.skey = (unsigned long long*)(b + o_skey);
+  s.sval = (unsigned long long*)(b + o_sval);
   s.work = (unsigned long long*)(b + o_work);
   s.lists = (unsigned long long*)(b + o_lists);
   s.wlist = (unsigned long long*)(b + o_wlist);

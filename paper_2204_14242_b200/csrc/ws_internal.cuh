@@ -128,6 +128,7 @@ struct DPrefix {
 constexpr int kNPrefix = 7;
 constexpr int kWSlots = 32 * 64 * 8;  // per config: warp index (<32) x residue (<64) x clip pattern (<8)
 constexpr int kSSlots = 64 * 8;       // per config: residue (<64) x clip pattern (<8)
+constexpr int kShareTab = 8192;       // SM-set classes shared across configurations (k_smset)
 
 // ---------------------------------------------------------------- launchers (ws_kernels.cu)
 struct Scratch {
@@ -142,6 +143,8 @@ struct Scratch {
   unsigned long long* wrep;   // n * kWSlots
   unsigned int* scnt;         // n * kSSlots
   unsigned long long* srep;   // n * kSSlots
+  unsigned long long* skey;   // kShareTab: cross-configuration class keys (~0 = empty)
+  unsigned long long* sval;   // kShareTab * 2: the owner's (sectors, lines)
   unsigned long long* work;   // K_NKINDS algorithmic work units of the last call (ws_work_read)
   unsigned long long* lists;  // [0] # warp classes, [1] # SM-set classes, [2] # direct SM sets (zeroed by k_scan)
   unsigned long long* wlist;  // n * kWSlots entries (config << 32 | slot)

@@ -1564,6 +1564,30 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
   }
 }
 
+// ---- single-block SM-set classes shared across configurations: the count of a class depends on
+// the kernel, the GPU's sector / line geometry, the block footprint BF (which fixes the clipped
+// extents) and the class slot (line residue, clip pattern) only, so configurations with the same
+// (kernel, GPU, BF) -- e.g. (32,2,1)+2y and (32,4,1) -- share it.  Key: kid 8 | gid 8 | BF 3 x 13
+// | slot 9 bits; 0 = not shareable.
+__device__ __forceinline__ unsigned long long share_key(const DPlan& P, unsigned slot) {
+  if (P.kid > 255 || P.gid > 255 || P.BF[0] >= 8192 || P.BF[1] >= 8192 || P.BF[2] >= 8192) return 0ull;
+  const unsigned long long k = ((unsigned long long)P.kid << 56) | ((unsigned long long)P.gid << 48) |
+                               ((unsigned long long)P.BF[0] << 35) | ((unsigned long long)P.BF[1] << 22) |
+                               ((unsigned long long)P.BF[2] << 9) | (unsigned long long)slot;
+  return k == ~0ull ? 0ull : k;
+}
+// owner (bit 30) or sharer (bit 31) of table entry t (bits 9..21) for a class slot; plain otherwise
+__device__ __forceinline__ unsigned share_claim(unsigned long long* skey, unsigned long long key, unsigned slot) {
+  if (!key) return slot;
+  unsigned t = (unsigned)((key * 0x9e3779b97f4a7c15ull) >> 51) & (kShareTab - 1);
+  for (int probe = 0; probe < 64; ++probe, t = (t + 1) & (kShareTab - 1)) {
+    const unsigned long long old = atomicCAS(skey + t, ~0ull, key);
+    if (old == ~0ull) return slot | (t << 9) | (1u << 30);
+    if (old == key) return slot | (t << 9) | (1u << 31);
+  }
+  return slot;  // table crowded: evaluate without sharing
+}
+
 // ---- translation groups of directly evaluated multi-block SM sets (k_smset)
 constexpr int kSetGrp = 1024;  // sets per config grouped in shared memory (more: no grouping)
 __device__ __forceinline__ void block_coord(const DPlan& P, long long B, long long* bc) {
@@ -1668,7 +1692,8 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
                                                unsigned long long* __restrict__ srep,
                                                unsigned long long* __restrict__ lists,
                                                unsigned long long* __restrict__ slist,
-                                               unsigned long long* __restrict__ dlist) {
+                                               unsigned long long* __restrict__ dlist,
+                                               unsigned long long* __restrict__ skey) {
   __shared__ unsigned long long s_key[kSetGrp];  // directly evaluated sets: shape key (0: not grouped)
   __shared__ unsigned s_cnt[kSetGrp];            // group sizes (at the group's smallest member)
   __shared__ short s_rep[kSetGrp];               // smallest member of the set's group
@@ -1758,7 +1783,8 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
           const long long gslot = (long long)c * kSSlots + slot;
           if (atomicAdd(scnt + gslot, 1u) == 0u) {
             srep[gslot] = (unsigned long long)Bm;
-            slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | slot;
+            const unsigned low = share_claim(skey, share_key(P, slot), slot);
+            slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | low;
           }
         }
         if (grp) s_key[j] = 0ull;
@@ -1812,7 +1838,8 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
                                                 unsigned long long* __restrict__ lists,
                                                 const unsigned long long* __restrict__ slist,
                                                 const unsigned long long* __restrict__ dlist,
-                                                unsigned long long* __restrict__ work) {
+                                                unsigned long long* __restrict__ work,
+                                                unsigned long long* __restrict__ sval) {
   __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ SmBox32 s_mb32[kMaxMembers];
@@ -1842,8 +1869,9 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     const long long nsm = G.g.n_sm;
     unsigned long long mult = 1;
     long long S0, kj;
+    if (cls && (low >> 31)) continue;  // shared class: k_sshare adds the owner's counts
     if (cls) {
-      const long long gslot = (long long)c * kSSlots + low;
+      const long long gslot = (long long)c * kSSlots + (low & 511u);
       mult = scnt[gslot];
       S0 = (long long)srep[gslot];
       kj = 1;
@@ -1874,7 +1902,32 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_SM_SEC, ss * mult);
       atomicAdd(a + A_SM_LIN, sl * mult);
+      if (cls && ((low >> 30) & 1u)) {  // owner of a shared class: publish the counts
+        const unsigned t = (low >> 9) & (kShareTab - 1);
+        sval[2 * t] = ss;
+        sval[2 * t + 1] = sl;
+      }
     }
+  }
+}
+
+// the shared classes' counts (owner evaluated in k_sclass) times each sharer's class size
+__global__ void __launch_bounds__(256) k_sshare(const unsigned long long* __restrict__ lists,
+                                                const unsigned long long* __restrict__ slist,
+                                                const unsigned int* __restrict__ scnt,
+                                                const unsigned long long* __restrict__ sval,
+                                                unsigned long long* __restrict__ acc) {
+  const long long ncls = (long long)lists[1];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ncls; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long ent = slist[i];
+    const unsigned low = (unsigned)(ent & 0xffffffffu);
+    if (!(low >> 31)) continue;
+    const int c = (int)(ent >> 32);
+    const unsigned t = (low >> 9) & (kShareTab - 1);
+    const unsigned long long mult = scnt[(long long)c * kSSlots + (low & 511u)];
+    unsigned long long* a = acc + (long long)c * A_N;
+    atomicAdd(a + A_SM_SEC, sval[2 * t] * mult);
+    atomicAdd(a + A_SM_LIN, sval[2 * t + 1] * mult);
   }
 }
 
@@ -2770,6 +2823,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
   cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), m);
   cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), m);
+  cudaMemsetAsync(s.skey, 0xff, (size_t)kShareTab * sizeof(unsigned long long), m);
   beg(K_PLAN, m);
   k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
                            s.plan_done, s.prefix, s.work, s.lists);  // its last CTA does the scan (k_scan)
@@ -2786,10 +2840,14 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc, fold_mode);
   end(K_FOLD, b);
   beg(K_SMSET, a);
-  k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist);
+  k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist,
+                                        s.skey);
   end(K_SMSET, a);
   beg(K_SCLASS, a);
-  k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists, s.slist, s.dlist, s.work);
+  k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
+                                                                     s.slist, s.dlist, s.work, s.sval);
+  k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
+  ++L;
   end(K_SCLASS, a);
   beg(K_WARP, m);
   k_warp<<<persist, 256, 0, m>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
