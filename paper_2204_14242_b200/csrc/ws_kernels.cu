@@ -8,8 +8,12 @@
 //                  address-sorted, so a shuffle against the previous issuing lane
 //                  dedupes), half-warp wavefronts (__match_any_sync bank histogram
 //                  per 1024 B cluster), lattice updates.
-//   k_smset  (a4)  one CTA per (config, SM-resident block set): unique load
-//                  sectors/lines of the set's footprint, row by row.
+//   k_smset  (a4)  one CTA per configuration: SM-resident block sets into translation
+//                  classes (per config, shared across configs with the same block
+//                  footprint) or translation groups of directly evaluated sets;
+//   k_sclass       one CTA per class representative / direct set: unique load
+//                  sectors/lines of the set's footprint, plane by plane; k_sshare
+//                  adds shared classes to their sharers.
 //   k_rows   (a5+a6) one CTA per (config, field, chunk of 1024 address rows):
 //                  unique sectors/lines of the wave, the layer sets and their unions,
 //                  row by row, as ordered (first, last, count) triples.
