@@ -147,6 +147,10 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   const size_t o_wrep = off;    off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
   const size_t o_scnt = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned int));
   const size_t o_srep = off;    off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
+  size_t max_fields = 1;
+  for (const DKernel& k : c->hk) max_fields = std::max<size_t>(max_fields, (size_t)k.n_fields);
+  const size_t o_spart = off;   off = align_up(off + n * max_fields * kSectSeg * (size_t)kSectPartBytes);
+  const size_t o_sdone = off;   off = align_up(off + n * max_fields * sizeof(unsigned int));
   const size_t o_skey = off;    off = align_up(off + (size_t)kShareTab * sizeof(unsigned long long));
   const size_t o_sval = off;    off = align_up(off + (size_t)kShareTab * 2 * sizeof(unsigned long long));
   const size_t o_work = off;    off = align_up(off + 16 * sizeof(unsigned long long));
@@ -179,6 +183,9 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   s.scnt = (unsigned int*)(b + o_scnt);
   s.srep = (unsigned long long*)(b + o_srep);
   s.skey = (unsigned long long*)(b + o_skey);
+  s.spart = (void*)(b + o_spart);
+  s.sdone = (unsigned int*)(b + o_sdone);
+  s.max_fields = (int32_t)max_fields;
   s.sval = (unsigned long long*)(b + o_sval);
   s.work = (unsigned long long*)(b + o_work);
   s.lists = (unsigned long long*)(b + o_lists);

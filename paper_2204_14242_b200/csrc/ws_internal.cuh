@@ -129,6 +129,8 @@ constexpr int kNPrefix = 7;
 constexpr int kWSlots = 32 * 64 * 8;  // per config: warp index (<32) x residue (<64) x clip pattern (<8)
 constexpr int kSSlots = 64 * 8;       // per config: residue (<64) x clip pattern (<8)
 constexpr int kShareTab = 8192;       // SM-set classes shared across configurations (k_smset)
+constexpr int kSectSeg = 8;           // k_sect: row segments (CTAs) per (config, field)
+constexpr int kSectPartBytes = 11 * 24;  // k_sect: one segment's partial triples (kSectNQ x Tri)
 
 // ---------------------------------------------------------------- launchers (ws_kernels.cu)
 struct Scratch {
@@ -145,6 +147,9 @@ struct Scratch {
   unsigned long long* srep;   // n * kSSlots
   unsigned long long* skey;   // kShareTab: cross-configuration class keys (~0 = empty)
   unsigned long long* sval;   // kShareTab * 2: the owner's (sectors, lines)
+  void* spart;                // k_sect: n * max_fields * kSectSeg partial triple sets
+  unsigned int* sdone;        // k_sect: n * max_fields finished segments
+  int32_t max_fields;
   unsigned long long* work;   // K_NKINDS algorithmic work units of the last call (ws_work_read)
   unsigned long long* lists;  // [0] # warp classes, [1] # SM-set classes, [2] # direct SM sets (zeroed by k_scan)
   unsigned long long* wlist;  // n * kWSlots entries (config << 32 | slot)

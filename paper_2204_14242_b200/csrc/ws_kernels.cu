@@ -52,6 +52,9 @@
 #ifndef WS_SCLASS_MINB
 #define WS_SCLASS_MINB 3
 #endif
+#ifndef WS_SECT_CTAS
+#define WS_SECT_CTAS 2  // k_sect CTAs per SM (launched even when no configuration wants outlook metrics)
+#endif
 #ifndef WS_SCLASS_THREADS
 #define WS_SCLASS_THREADS 256  // threads per k_sclass CTA (<= 256: shared arrays sized for 8 warps)
 #endif
@@ -544,7 +547,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
                                               unsigned int* __restrict__ wcnt, unsigned int* __restrict__ scnt,
                                               unsigned int* __restrict__ plan_done, DPrefix* __restrict__ pre,
                                               unsigned long long* __restrict__ work,
-                                              unsigned long long* __restrict__ lists) {
+                                              unsigned long long* __restrict__ lists,
+                                              unsigned long long* __restrict__ skey, unsigned int* __restrict__ sdone,
+                                              int max_fields) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
 #ifdef WS_PLAN_CLOCK
@@ -562,6 +567,16 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   __shared__ int s_part[128];
   __shared__ int s_total;
   if (tid < A_N) acc[(long long)c * A_N + tid] = 0ull;
+  // this configuration's class counters and k_sect counters, and a share of the cross-config
+  // class table: zeroed here instead of by memset nodes ahead of the graph's first kernel
+  {
+    uint4* wc = reinterpret_cast<uint4*>(wcnt + (long long)c * kWSlots);
+    for (int i = tid; i < kWSlots / 4; i += blockDim.x) wc[i] = make_uint4(0u, 0u, 0u, 0u);
+    uint4* sc = reinterpret_cast<uint4*>(scnt + (long long)c * kSSlots);
+    for (int i = tid; i < kSSlots / 4; i += blockDim.x) sc[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < max_fields; i += blockDim.x) sdone[(long long)c * max_fields + i] = 0u;
+    for (int i = c * blockDim.x + tid; i < kShareTab; i += n * blockDim.x) skey[i] = ~0ull;
+  }
   static_assert(sizeof(DPlan) % 16 == 0 && sizeof(DKernel) % 16 == 0 && sizeof(DGpu) % 16 == 0, "uint4 copies");
   constexpr int kPlanVec = (int)(sizeof(DPlan) / 16);
   for (int i = tid; i < kPlanVec; i += blockDim.x) reinterpret_cast<uint4*>(&P)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -1704,6 +1719,7 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
   for (int c = blockIdx.x; c < n; c += gridDim.x) {
     const DPlan& P = plans[c];
     const long long nset = pre[c + 1].set - pre[c].set;
+    if (nset <= 0) continue;  // failed configuration (its kid / gid may be out of range): no sets
     const long long nsm = gs[P.gid].g.n_sm;
     const bool grp = nset <= kSetGrp && P.scls_R > 0 && !P.rep_mult;
     const SetEnv env = set_env(ks[P.kid], gs[P.gid].g.line_bytes);
@@ -2497,6 +2513,7 @@ __device__ __forceinline__ void row_union_p(const Gen& gen, long long R0, int le
 }
 
 constexpr int kSectNQ = 2 * kMaxSections + 3;  // per section: load sectors, lines; union: load sectors, lines; pages
+static_assert(kSectNQ * sizeof(Tri) == kSectPartBytes, "k_sect partial size");
 
 // One CTA per (config, field) of the configs that want the outlook metrics.
 // Linear address space.  The wave's rows (y, z) are walked in address order, threads taking
@@ -2505,15 +2522,21 @@ constexpr int kSectNQ = 2 * kMaxSections + 3;  // per section: load sectors, lin
 // floor(j * S / n_sm)), each piece a cell x-interval shifted by the group's x-run.  Unions
 // per section and over all sections give ordered triples; an ordered CTA reduction gives the
 // field's counts.
+// One CTA per (config, field, row segment): kSectSeg segments of the field's rows; the CTA that
+// finishes an item's last segment folds the segments' partial triples in row order.
 __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                               const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                               unsigned long long* __restrict__ acc,
-                                              unsigned long long* __restrict__ work) {
+                                              unsigned long long* __restrict__ work, Tri* __restrict__ spart,
+                                              unsigned int* __restrict__ sdone, int max_fields) {
   __shared__ Tri s_red[(256 / 32) * kSectNQ];
-  const long long total = pre[n].sect;
+  __shared__ int s_last;
+  const long long total = pre[n].sect * kSectSeg;
   const int tid = threadIdx.x, nt = blockDim.x;
   unsigned long long my_ops = 0;
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+  for (long long it2 = blockIdx.x; it2 < total; it2 += gridDim.x) {
+    const long long item = it2 / kSectSeg;
+    const int seg = (int)(it2 % kSectSeg);
     const int c = find_config<6>(pre, n, item);
     const int fi = (int)(item - pre[c].sect);
     const DPlan& P = plans[c];
@@ -2541,7 +2564,8 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
     if (z1 > F.ext[2]) z1 = F.ext[2];
     const long long ny = y1 > y0 ? y1 - y0 : 0, nz = z1 > z0 ? z1 - z0 : 0;
     const long long nrows = (F.g_end > F.g_begin) ? ny * nz : 0;
-    const long long per = (nrows + nt - 1) / nt;
+    const long long r_begin = nrows * seg / kSectSeg, r_end = nrows * (seg + 1) / kSectSeg;
+    const long long per = (r_end - r_begin + nt - 1) / nt;
     Tri t[kSectNQ];
 #pragma unroll
     for (int q = 0; q < kSectNQ; ++q) t[q] = tri_empty();
@@ -2556,7 +2580,7 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
 #pragma unroll
     for (int i = 0; i <= kMaxSections; ++i) a_sec[i] = i <= S ? (int)((i * nsm + S - 1) / S) : (int)nsm;
     const int s32 = (int)s, e32 = (int)(s + Wb), Gx32 = (int)Gx, Gy32 = (int)Gy;
-    for (long long ri = tid * per; ri < nrows && ri < (tid + 1) * per; ++ri) {
+    for (long long ri = r_begin + tid * per; ri < r_end && ri < r_begin + (tid + 1) * per; ++ri) {
       const long long z = z0 + ri / ny, y = y0 + ri % ny;
       const long long R0 = F.align + ((F.pitch[1] * y + F.pitch[2] * z) << le);
       my_ops += (unsigned long long)(F.g_end - F.g_begin);
@@ -2646,7 +2670,30 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
       }
     }
     cta_ordered_reduce<kSectNQ>(t, s_red);
-    if (tid == 0 && nrows > 0) {
+    // publish this segment; the last segment of the item folds all of them in row order
+    const long long pslot = ((long long)c * max_fields + fi) * kSectSeg;
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < kSectNQ; ++q) spart[(pslot + seg) * kSectNQ + q] = t[q];
+      __threadfence();
+      s_last = atomicAdd(sdone + (long long)c * max_fields + fi, 1u) == (unsigned)(kSectSeg - 1);
+    }
+    __syncthreads();
+    const bool last = s_last;
+    __syncthreads();
+    if (tid == 0 && last) {
+      __threadfence();
+#pragma unroll
+      for (int q = 0; q < kSectNQ; ++q) {
+        Tri a = tri_empty();
+        for (int k = 0; k < kSectSeg; ++k) {
+          const long long* src = reinterpret_cast<const long long*>(spart + (pslot + k) * kSectNQ + q);
+          a = tri_combine(a, Tri{__ldcg(src), __ldcg(src + 1), __ldcg(src + 2)});
+        }
+        t[q] = a;
+      }
+    }
+    if (tid == 0 && last && nrows > 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       long long sld = 0, slin = 0;
       for (int i = 0; i < kMaxSections; ++i) {
@@ -2825,12 +2872,9 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
 #endif
   const int persist = n_sm_dev * WS_PERSIST;
   cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
-  cudaMemsetAsync(s.wcnt, 0, (size_t)n * kWSlots * sizeof(unsigned int), m);
-  cudaMemsetAsync(s.scnt, 0, (size_t)n * kSSlots * sizeof(unsigned int), m);
-  cudaMemsetAsync(s.skey, 0xff, (size_t)kShareTab * sizeof(unsigned long long), m);
   beg(K_PLAN, m);
   k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
-                           s.plan_done, s.prefix, s.work, s.lists);  // its last CTA does the scan (k_scan)
+                           s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields);  // its last CTA scans
   end(K_PLAN, m);
   // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on main
   cudaEventRecord(st.fork, m);
@@ -2861,7 +2905,8 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_wclass<<<persist, 256, 0, m>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
   end(K_WCLASS, m);
   beg(K_SECT, m);
-  k_sect<<<n_sm_dev * 2, 256, 0, m>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.work);
+  k_sect<<<n_sm_dev * WS_SECT_CTAS, 256, 0, m>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.work, (Tri*)s.spart, s.sdone,
+                                      s.max_fields);
   end(K_SECT, m);
   // join
   cudaEventRecord(st.join[0], a);
