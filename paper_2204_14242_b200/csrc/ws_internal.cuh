@@ -129,7 +129,10 @@ constexpr int kNPrefix = 7;
 constexpr int kWSlots = 32 * 64 * 8;  // per config: warp index (<32) x residue (<64) x clip pattern (<8)
 constexpr int kSSlots = 64 * 8;       // per config: residue (<64) x clip pattern (<8)
 constexpr int kShareTab = 8192;       // SM-set classes shared across configurations (k_smset)
-constexpr int kSectSeg = 8;           // k_sect: row segments (CTAs) per (config, field)
+#ifndef WS_SECT_SEG
+#define WS_SECT_SEG 8
+#endif
+constexpr int kSectSeg = WS_SECT_SEG;  // k_sect: row segments (CTAs) per (config, field)
 constexpr int kSectPartBytes = 11 * 24;  // k_sect: one segment's partial triples (kSectNQ x Tri)
 
 // ---------------------------------------------------------------- launchers (ws_kernels.cu)
