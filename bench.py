@@ -151,8 +151,16 @@ def run_reference(args, rank, world):
     plans = [O.plan(kernel, gpu, c) for c in cfgs]
     mean_evals = statistics.mean(p["addr_evals"] for p in plans if p["status"] == 0)
     shallow = [c for c in cfgs if c[0][2] == 1 and c[1] == (1, 1, 1)]
+    # one configuration runs on one host thread (the oracle parallelises over configurations):
+    # time one (the first warm-up step); a step is one wave of configurations over the host
+    # threads, or a single configuration when K such waves would take more than ~2 minutes
+    t0 = time.perf_counter()
+    O.estimate_batch(kernel, gpu, shallow[:1], 1)
+    t_one = time.perf_counter() - t0
     per_step = shallow[:max(1, min(len(shallow), threads))]
-    for _ in range(args.warmup):
+    if args.steps * t_one * 1.5 > 120.0:
+        per_step = shallow[:1]
+    for _ in range(max(0, args.warmup - 1)):
         O.estimate_batch(kernel, gpu, per_step[:1], 1)
     tot_dt, tot_ev, tot_n = 0.0, 0, 0
     for _ in range(args.steps):
@@ -506,12 +514,16 @@ def e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1500)  # timed region >= ~0.3 s: clock samples inside it
+    # native: 1500 timed steps (>= ~0.3 s: clock samples inside the timed region); reference
+    # arm (the slow CPU oracle, seconds per step): 3 unless given
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-1/3/4 measurements")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 3 if args.impl == "reference" else 1500
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
