@@ -13,7 +13,9 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "libwsoracle.so")
+# WSO_LIB: load another build of the oracle (scripts/oracle_mutations.py builds deliberately
+# broken copies to show that the pins in tests/test_oracle_pins.py catch each slip)
+LIB = os.environ.get("WSO_LIB") or os.path.join(HERE, "libwsoracle.so")
 SRC = os.path.join(HERE, "ws_oracle.cpp")
 
 I64 = C.c_int64
@@ -64,10 +66,13 @@ class Result(C.Structure):
                 [(n, I64) for n in INT_FIELDS2] + [(n, C.c_double) for n in FP_FIELDS2])
 
 
-def build(force=False):
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", LIB, SRC, "-lpthread"])
-    return LIB
+def build(force=False, src=SRC, out=None):
+    out = out or LIB
+    if out != LIB or force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        tmp = f"{out}.{os.getpid()}.tmp"        # build aside, then rename: a loaded copy stays valid
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I" + HERE, "-o", tmp, src, "-lpthread"])
+        os.replace(tmp, out)
+    return out
 
 
 _lib = None

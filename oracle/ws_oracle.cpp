@@ -91,6 +91,9 @@ int64_t check_kernel(const wso_kernel& K) {
   for (int64_t i = 0; i < K.n_fields; ++i) {
     const wso_field& f = K.fields[i];
     if (log2_exact(f.elem_bytes) < 0 || f.elem_bytes > 32) return WSO_EINVAL;
+    // elements never straddle a sector: the alignment is a multiple of the element size
+    // (WS_EINVAL otherwise; every sector count below keys an element by its first byte)
+    if (floormod(f.align_bytes, f.elem_bytes) != 0) return WSO_EINVAL;
     for (int d = 0; d < 3; ++d)
       if (f.extent[d] < 1) return WSO_EINVAL;
     // x contiguous, rows and planes disjoint (row-major, padding allowed)

@@ -712,3 +712,178 @@ def test_lbm15_definition_pins():
     phi[3, 3, 3] = 1.0
     _, fd = ST.lbm15(np.zeros_like(src), phi, n)
     assert fd[3, 3, 3] == -6.0 and fd[3, 3, 4] == 1.0 and fd[2, 3, 3] == 1.0
+
+
+# --------------------------------------------------------------------- a6 (O), a7 closed forms (round 2)
+# Each pin below is a value written out by hand from the definition of the term it checks (not
+# the oracle's formula retyped): scripts/oracle_mutations.py builds deliberately broken oracles
+# (a dropped factor, a swapped bandwidth, a wrong divisor, a dropped term) and records that
+# these tests fail for each one (profiles/r02_oracle_mutations.md).
+def _copy_kernel(X, Y, Z, loads=((0, 0, 0),), store=True, elem=8):
+    """dst[c] = f(src[c + o] for o in loads): dense, 0-aligned fields, no ghost layers in y/z."""
+    hx = max(max(abs(o[0]) for o in loads), 0)
+    ext = (X + 2 * hx, Y, Z)
+    fld = {"extent": ext, "pitch": (1, ext[0], ext[0] * ext[1]), "align": 0, "elem": elem}
+    acc = [(0, 0, o) for o in loads] + ([(1, 1, (0, 0, 0))] if store else [])
+    return {"name": "copy", "fields": [fld, dict(fld)] if store else [fld], "accesses": acc,
+            "dom_lo": (hx, 0, 0), "dom_hi": (hx + X, Y, Z), "regs": 0, "flops": 0.0}
+
+
+def _flat_gpu(n_sm=1, **kw):
+    g = W.gpu_a100()
+    g["n_sm"] = n_sm
+    g["hit_abc"] = [[1.0, 0.0, 0.0] for _ in range(4)]
+    g.update(kw)
+    return g
+
+
+def test_limiter_dram_floor_87_5_glups():
+    """S:468 / S:649-650 (P:262-281 limiters, Table tab:av100 P:313 1400 GB/s): a stencil at the
+    8 B/Lup load + 8 B/Lup store floor runs at 1400/16 = 87.5 GLup/s; load-only at 175 GLup/s.
+    Streaming copy, 128-wide rows (whole lines), no reuse possible -> exactly 8 + 8 B/Lup."""
+    X, Y, Z = 128, 16, 16
+    g = W.gpu_a100()
+    cells = X * Y * Z
+    r = O.estimate(_copy_kernel(X, Y, Z), g, ((128, 1, 1), (1, 1, 1), 0))
+    assert (r["dram_ld_Bpl"], r["dram_st_Bpl"]) == (8.0, 8.0)
+    assert r["limiter"] == 2
+    assert cells / r["t_pred"] == pytest.approx(87.5e9, rel=1e-12)
+    r = O.estimate(_copy_kernel(X, Y, Z, store=False), g, ((128, 1, 1), (1, 1, 1), 0))
+    assert r["dram_ld_Bpl"] == 8.0 and r["dram_st_Bpl"] == 0.0
+    assert cells / r["t_pred"] == pytest.approx(175e9, rel=1e-12)
+
+
+def test_limiter_l2_and_l1_absolute():
+    """L2 limiter = (L2<->L1 loads + stores) / L2 bandwidth: the copy moves 8 + 8 B/Lup
+    through L2 -> 5000e9 / 16 = 312.5 GLup/s (A100 L2 5000 GB/s) when DRAM is not the
+    bottleneck.  L1 limiter = cycles per LUP / (n_sm * clock): a half-warp instruction over 16
+    consecutive doubles is one wavefront, two instructions per LUP, 16 LUP per
+    half-warp -> 1/8 cycle per LUP -> 108 * 1.41e9 * 8 = 1.21824e12 LUP/s."""
+    X, Y, Z = 128, 16, 16
+    cells = X * Y * Z
+    g = dict(W.gpu_a100(), dram_bw=1e18)
+    r = O.estimate(_copy_kernel(X, Y, Z), g, ((128, 1, 1), (1, 1, 1), 0))
+    assert (r["l2_ld_Bpl"], r["l2_st_Bpl"]) == (8.0, 8.0)
+    assert r["limiter"] == 1
+    assert cells / r["t_pred"] == pytest.approx(312.5e9, rel=1e-12)
+    g = dict(W.gpu_a100(), dram_bw=1e18, l2_bw=1e18)
+    r = O.estimate(_copy_kernel(X, Y, Z), g, ((128, 1, 1), (1, 1, 1), 0))
+    assert r["l1_cyc_per_lup"] == 0.125 and r["limiter"] == 0
+    assert cells / r["t_pred"] == pytest.approx(108 * 1.41e9 * 8, rel=1e-12)
+
+
+def test_eq5_capacity_term_hand_count():
+    """Eq. 5 (P:695-698; S:388 "V_up=100, V_comp=60, R=.75 -> 10"): V_down = V_comp + (1-R)(V_up -
+    V_comp) at the L1 level.  One 32-thread block, 1D 3-point load src[x-1], src[x], src[x+1] on
+    doubles at x = 8..39 (addresses 56..327 B): the three warp instructions touch 9 + 8 + 9 = 26
+    sectors (V_up), their union is sectors 1..10 = 10 (V_comp).  With R_L1 = 0.75:
+    V_down = 10 + 0.25 * 16 = 14 sectors -> 14 * 32 / 32 LUP = 14 B/Lup."""
+    k = _copy_kernel(32, 1, 1, loads=((-1, 0, 0), (0, 0, 0), (1, 0, 0)), store=False)
+    k["fields"][0] = dict(k["fields"][0], extent=(48, 1, 1), pitch=(1, 48, 48))
+    k["dom_lo"], k["dom_hi"] = (8, 0, 0), (40, 1, 1)
+    g = _flat_gpu()
+    g["hit_abc"][0] = [0.75, 0.0, 0.0]
+    r = O.estimate(k, g, ((32, 1, 1), (1, 1, 1), 1))
+    assert (r["l1_req_ld_sectors"], r["sm_ld_sectors"], r["sm_ld_lines"]) == (26, 10, 3)
+    assert r["R_l1"] == 0.75
+    assert r["l2_ld_Bpl"] == pytest.approx(14.0, rel=1e-15)
+    g["hit_abc"][0] = [0.0, 0.0, 0.0]            # R = 0 -> V_up; R = 1 -> V_comp (S:389-390)
+    assert O.estimate(k, g, ((32, 1, 1), (1, 1, 1), 1))["l2_ld_Bpl"] == pytest.approx(26.0, rel=1e-15)
+    g["hit_abc"][0] = [1.0, 0.0, 0.0]
+    assert O.estimate(k, g, ((32, 1, 1), (1, 1, 1), 1))["l2_ld_Bpl"] == pytest.approx(10.0, rel=1e-15)
+
+
+def test_eq4_oversubscription_l1_hand_count():
+    """Eq. 4 (O = V_alloc / V_cache) at L1 with the SM set's 128 B line footprint (P:474-475,
+    Q8/Q18), averaged over the SM sets.  Two 32-thread blocks of the 3-point load at x = 8..71:
+    one SM with k = 2 holds both blocks: addresses 56..583 B -> lines 0..4 = 5 lines = 640 B;
+    L1 = 1280 B -> O = 0.5.  Two SMs, one block each: lines 0..2 and 2..4 -> 3 lines per set on
+    average = 384 B -> O = 0.3.  R_L1 = R(O) on the set's O."""
+    k = _copy_kernel(64, 1, 1, loads=((-1, 0, 0), (0, 0, 0), (1, 0, 0)), store=False)
+    k["fields"][0] = dict(k["fields"][0], extent=(80, 1, 1), pitch=(1, 80, 80))
+    k["dom_lo"], k["dom_hi"] = (8, 0, 0), (72, 1, 1)
+    abc = [1.0, 0.5, -2.0]
+    g = _flat_gpu(n_sm=1, l1_bytes=1280)
+    g["hit_abc"][0] = abc
+    r = O.estimate(k, g, ((32, 1, 1), (1, 1, 1), 2))
+    assert (r["n_smsets"], r["sm_ld_lines"]) == (1, 5)
+    assert r["O_l1"] == 0.5
+    assert r["R_l1"] == pytest.approx(math.exp(-0.5 * math.exp(1.0)), rel=1e-15)
+    g = _flat_gpu(n_sm=2, l1_bytes=1280)
+    r = O.estimate(k, g, ((32, 1, 1), (1, 1, 1), 1))
+    assert (r["n_smsets"], r["sm_ld_lines"]) == (2, 6)
+    assert r["O_l1"] == pytest.approx(0.3, rel=1e-15)
+
+
+def test_eq4_oversubscription_layer_sets_o_z_equals_one():
+    """SURVEY 8(c) "a6 (O)": O_z = 1 exactly when the z-layer set's line footprint equals the
+    effective L2 (split L2 = l2_bytes / sections, Q31).  Copy kernel on a
+    60 x 8 x 8 domain in rows padded to 64 doubles (512 B, line-aligned), one 64-thread block per
+    row (Gx = 1, Gy = 8): a row of 60 doubles is 15 sectors but 4 lines.  L_y = the previous row
+    (src + dst = 8 lines), L_z = the previous 8 rows = one z-layer (64 lines).  l2_bytes = 16 KiB
+    in 2 sections -> L2_eff = 8 KiB: O_y = 1024/8192 = 0.125, O_z = 8192/8192 = 1 (the sector
+    footprint would give 960/8192 and 7680/8192).  Store curve: O_st = wave lines /
+    L2_eff with the 2-block wave (2 rows x 2 fields x 4 lines = 16 lines)."""
+    k = _copy_kernel(60, 8, 8)
+    for f in k["fields"]:
+        f.update(extent=(64, 8, 8), pitch=(1, 64, 512))
+    g = _flat_gpu(n_sm=2, l2_bytes=16384, l2_sections=2)
+    r = O.estimate(k, g, ((64, 1, 1), (1, 1, 1), 1))
+    assert r["wave_blocks"] == 2 and r["wave_first_block"] >= 8
+    assert (r["ly_lines"], r["lz_lines"], r["wave_lines"]) == (8, 64, 16)
+    assert r["l2_eff_bytes"] == 8192.0
+    assert (r["O_y"], r["O_z"]) == (0.125, 1.0)
+    assert r["O_st"] == 16 * 128 / 8192
+    # the copy reads nothing twice: no overlap with either layer set
+    assert (r["ov_y"], r["ov_z"]) == (0, 0)
+
+
+def test_partial_store_readback_hand_count():
+    """P:519-521 (Q19): redundant partial stores (several warp instructions storing parts of one
+    sector) that miss in L2 are read back from DRAM: cap_st = (1 - R_st) * (req_st - wave_st).
+    Copy on a 4 x 16 domain of doubles, rows of 4 = exactly one sector, blocks (2,16,1): the two
+    blocks store the two halves of every row's sector -> 32 store-sector requests, 16 distinct;
+    loads likewise 16 distinct sectors.  R_st = 0.5 -> DRAM loads = 16 + 0.5 * 16 = 24 sectors
+    = 24 * 32 B / 64 LUP = 12 B/Lup (8 without the read-back), DRAM stores 8 B/Lup."""
+    k = _copy_kernel(4, 16, 1)
+    g = _flat_gpu(n_sm=2)
+    g["hit_abc"][3] = [0.5, 0.0, 0.0]
+    r = O.estimate(k, g, ((2, 16, 1), (1, 1, 1), 1))
+    assert (r["wave_blocks"], r["lup_wave"]) == (2, 64)
+    assert (r["l1_req_st_sectors"], r["wave_st_sectors"], r["wave_ld_sectors"]) == (32, 16, 16)
+    assert r["R_st"] == 0.5
+    assert r["dram_ld_Bpl"] == 12.0 and r["dram_st_Bpl"] == 8.0
+    # L1 -> L2 stores are written through per warp instruction (P:477): 32 sectors = 16 B/Lup;
+    # L2 -> L1 loads: each block's SM fetches the row sectors it reads: 2 x 16 sectors = 16 B/Lup
+    assert r["l2_st_Bpl"] == 16.0 and r["l2_ld_Bpl"] == 16.0
+    g["hit_abc"][3] = [1.0, 0.0, 0.0]
+    assert O.estimate(k, g, ((2, 16, 1), (1, 1, 1), 1))["dram_ld_Bpl"] == 8.0
+
+
+def test_alignment_must_be_element_multiple():
+    """align_bytes not a multiple of elem_bytes is WS_EINVAL (an element would
+    straddle two sectors); negative multiples are valid (P:540 uses -1 element)."""
+    k = W.k7(8)
+    k["fields"][0] = dict(k["fields"][0], align=4)
+    assert O.check_kernel(k) == 1
+    assert O.estimate(k, W.gpu_v100(), ((32, 1, 1), (1, 1, 1), 0))["status"] == 1
+    k["fields"][0] = dict(k["fields"][0], align=-8)
+    assert O.check_kernel(k) == 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_vs_independent_negative_alignment(seed):
+    """Negative alignments (P:540-545 uses -1 element): floor division of negative addresses in the
+    oracle vs Python's floor semantics in the independent model, every scope."""
+    import random
+    k, g, c = W.random_kernel(900 + seed, max_dom=8), W.random_gpu(seed), W.random_config(seed)
+    rng = random.Random(seed)
+    for f in k["fields"]:
+        f["align"] = -f["elem"] * rng.randint(1, 300)
+    r = O.estimate(k, g, c)
+    if r["status"] != 0:
+        pytest.skip("config rejected")
+    for key, v in M.set_counts(k, g, c).items():
+        assert r[key] == v, key
+    for key, v in M.l1_counts(k, g, c).items():
+        assert r[key] == v, key
