@@ -63,7 +63,7 @@ ws_status ws_set_stream(ws_ctx* ctx, void* cuda_stream);
 typedef struct {
   int64_t extent[3];
   int64_t pitch[3];
-  int64_t align_bytes;   /* may be negative (P:540 example uses -8) */
+  int64_t align_bytes;   /* may be negative (P:540 example uses -8); a multiple of elem_bytes */
   uint32_t elem_bytes;
   uint32_t pad;
 } ws_field;
@@ -87,7 +87,7 @@ typedef struct {
 } ws_kernel;
 
 /* Deep-copies the description.  Errors: WS_EINVAL (counts, layout, elem,
- * empty domain), WS_EBOUNDS (dom +- offsets leaves a field), WS_ELIMIT (a
+ * align_bytes not a multiple of elem_bytes, empty domain), WS_EBOUNDS (dom +- offsets leaves a field), WS_ELIMIT (a
  * field has more than 16 distinct x-offset runs, or a z-plane > 2 GiB - 16 KiB).
  * *kernel_id receives a new id. */
 ws_status ws_describe_kernel(ws_ctx* ctx, const ws_kernel* k, uint32_t* kernel_id);
@@ -193,9 +193,28 @@ ws_status ws_estimate(ws_ctx* ctx, const ws_config* cfgs, size_t n, ws_result* o
  * enqueued on the context stream, returns without synchronising. */
 ws_status ws_estimate_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_result* d_out);
 
+/* Architecture exploration (BJ configs[3]; hardware parameters P:307-320): every configuration
+ * against every hardware set of gpu_ids (a host array of n_gpu <= 256 described gpu ids).
+ *   out[g * n + i] = the record ws_estimate gives for cfgs[i] with gpu_id = gpu_ids[g]
+ * (cfgs[i].gpu_id is ignored), byte-identical.  The integer stages a1-a6 read a hardware set
+ * only through its occupancy limits, SM count, sector / line / bank geometry, half-warp, pair
+ * window, section count, page size and whether link_bw > 0; they run once per group of gpu_ids
+ * that agree in all of these, and the FP64 model (a7) fans out over each group's sets.
+ * ws_estimate_multi: host cfgs / out, synchronous.  ws_estimate_multi_async: device d_cfgs (n) /
+ * d_out (n * n_gpu), gpu_ids on the host, enqueued on the context stream.
+ * Errors: WS_EUNKNOWN_ID (an id not described), WS_ELIMIT (n_gpu > 256, n * n_gpu > 2^24). */
+ws_status ws_estimate_multi(ws_ctx* ctx, const ws_config* cfgs, size_t n, const uint32_t* gpu_ids, uint32_t n_gpu,
+                            ws_result* out);
+ws_status ws_estimate_multi_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, const uint32_t* gpu_ids,
+                                  uint32_t n_gpu, ws_result* d_out);
+/* Integer-stage groups the last ws_estimate_multi[_async] call formed. */
+uint32_t ws_last_group_count(const ws_ctx* ctx);
+
 /* Rank by (t_pred ascending, index ascending); failed configs rank last.
  * Fills res[i].rank and top_idx[0..min(k,n)) with the indices of the best.
- * ws_rank: host pointers, synchronous.  ws_rank_async: device pointers, no sync. */
+ * ws_rank: host pointers, synchronous.  ws_rank_async: device pointers, no sync.
+ * n <= 2^24 (WS_ELIMIT).  Device work: one CTA sorting in shared memory up to 16384 records,
+ * a stable radix sort of 64-bit keys beyond (scratch kept by the context, grow-only). */
 ws_status ws_rank(ws_ctx* ctx, ws_result* res, size_t n, size_t k, uint32_t* top_idx);
 ws_status ws_rank_async(ws_ctx* ctx, ws_result* d_res, size_t n, size_t k, uint32_t* d_top_idx);
 

@@ -38,6 +38,14 @@ struct ws_ctx {
   size_t io_cap = 0;
   uint32_t last_launches = 0;
   unsigned long long* last_work = nullptr;
+  // ws_rank: device scratch of the radix path and the host path's staging (grow-only)
+  void* rank_buf = nullptr;
+  size_t rank_cap = 0;
+  void* rank_io = nullptr;
+  size_t rank_io_cap = 0;
+  uint32_t last_groups = 0; // ws_estimate_multi: integer-stage groups of the last call
+  void* xcfg = nullptr;     // ws_estimate_multi: expanded configurations (grow-only)
+  size_t xcfg_cap = 0;
   // tracing
   bool profiling = false;
   struct Rec {
@@ -56,9 +64,11 @@ struct ws_ctx {
     const void *cfgs, *out, *scratch, *dk, *dg;
     size_t n;
     int nk, ng;
+    uint64_t fan;       // ws_estimate_multi: hash of the fan-out descriptor (0 = plain estimate)
+    const void* xcfg;   // its expanded-configuration buffer
     bool operator==(const GKey& o) const {
       return cfgs == o.cfgs && out == o.out && scratch == o.scratch && dk == o.dk && dg == o.dg && n == o.n &&
-             nk == o.nk && ng == o.ng;
+             nk == o.nk && ng == o.ng && fan == o.fan && xcfg == o.xcfg;
     }
   };
   cudaStream_t cap = nullptr;
@@ -130,8 +140,25 @@ ws_status upload(ws_ctx* c) {
 }
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+constexpr size_t kMaxBatch = size_t(1) << 24;
 
-ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
+// grow-only device buffer owned by the context (the old contents are not kept)
+ws_status grow(ws_ctx* c, void*& p, size_t& cap, size_t need, const char* what) {
+  if (need <= cap) return WS_OK;
+  if (p) {
+    cudaStreamSynchronize(c->stream);   // in-flight work may still read the old buffer
+    cudaFree(p);
+  }
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, need);
+  if (e != cudaSuccess) return fail(c, WS_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+  cap = need;
+  return WS_OK;
+}
+
+// Scratch layout for a batch of n configurations; with bytes_only, only its size.
+ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = nullptr) {
   int64_t cb = 1;
   for (int64_t v : c->chunk_bound) cb = std::max(cb, v);
   const size_t max_chunks = n * (size_t)cb;
@@ -161,6 +188,10 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
   size_t max_nsm = 1;
   for (const DGpu& g : c->hg) max_nsm = std::max<size_t>(max_nsm, g.g.n_sm);
   const size_t o_dlist = off;   off = align_up(off + n * max_nsm * sizeof(unsigned long long));
+  if (bytes_only) {
+    *bytes_only = off;
+    return WS_OK;
+  }
   if (off > c->scratch_cap) {
     if (c->scratch) cudaFree(c->scratch);
     c->scratch = nullptr;
@@ -168,7 +199,11 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s) {
     cudaError_t e = cudaMalloc(&c->scratch, off);
     if (e != cudaSuccess) return fail(c, WS_ENOMEM, std::string("device scratch: ") + cudaGetErrorString(e));
     c->scratch_cap = off;
-    cudaMemset(c->scratch, 0, off);  // counters (k_plan's plan_done) start at 0
+    // counters (k_plan's plan_done) start at 0: zeroed on the context stream (ordered before
+    // every later kernel of this context, whatever the stream's flags) and waited for
+    e = cudaMemsetAsync(c->scratch, 0, off, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "scratch init");
   }
   char* b = (char*)c->scratch;
   s.plans = (DPlan*)(b + o_plans);
@@ -235,6 +270,9 @@ void ws_destroy(ws_ctx* c) {
   if (c->dg) cudaFree(c->dg);
   if (c->scratch) cudaFree(c->scratch);
   if (c->io) cudaFree(c->io);
+  if (c->rank_buf) cudaFree(c->rank_buf);
+  if (c->rank_io) cudaFree(c->rank_io);
+  if (c->xcfg) cudaFree(c->xcfg);
   c->sim_cache.release();
   for (auto& r : c->pending)
     for (cudaEvent_t e : r.ev) cudaEventDestroy(e);
@@ -253,6 +291,16 @@ const char* ws_last_error(const ws_ctx* c) { return c ? c->err.c_str() : "null c
 
 ws_status ws_set_stream(ws_ctx* c, void* s) {
   if (!c) return WS_EINVAL;
+  if ((cudaStream_t)s == c->stream) return WS_OK;
+  cudaSetDevice(c->device);
+  // the scratch, io buffers and graph are shared: work issued on the new stream is ordered
+  // after everything already enqueued on the old one
+  cudaEvent_t e = nullptr;
+  cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (r == cudaSuccess) r = cudaEventRecord(e, c->stream);
+  if (r == cudaSuccess) r = cudaStreamWaitEvent((cudaStream_t)s, e, 0);
+  if (e) cudaEventDestroy(e);
+  if (r != cudaSuccess) return cuda_fail(c, r, "set_stream");
   c->stream = (cudaStream_t)s;
   return WS_OK;
 }
@@ -338,6 +386,9 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
     DField& G = D.f[i];
     const int le = lg2(F.elem_bytes);
     if (le < 0 || F.elem_bytes > 32) return fail(c, WS_EINVAL, "elem_bytes must be a power of two <= 32");
+    // an element never straddles a sector, so the alignment is a multiple of elem_bytes
+    if (F.align_bytes & (int64_t)(F.elem_bytes - 1))
+      return fail(c, WS_EINVAL, "align_bytes must be a multiple of elem_bytes");
     for (int d = 0; d < 3; ++d)
       if (F.extent[d] < 1) return fail(c, WS_EINVAL, "field extent < 1");
     if (F.pitch[0] != 1 || F.pitch[1] < F.extent[0] || F.pitch[2] < F.pitch[1] * F.extent[1])
@@ -479,17 +530,54 @@ ws_status ws_describe_gpu(ws_ctx* c, const ws_gpu* g, uint32_t* id) {
   return WS_OK;
 }
 
+static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out, bool allow_graph,
+                                 const FanOut* fan);
+static size_t chunk_configs(ws_ctx* c, size_t per_item_mult);
+
 ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out) {
   if (!c) return WS_EINVAL;
   if (n == 0) return WS_OK;
   if (!d_cfgs || !d_out) return fail(c, WS_EINVAL, "null argument");
-  if (n > (size_t)(1 << 24)) return fail(c, WS_ELIMIT, "batch larger than 2^24 configurations");
+  if (n > kMaxBatch) return fail(c, WS_ELIMIT, "batch larger than 2^24 configurations");
   if (c->hk.empty() || c->hg.empty()) return fail(c, WS_EUNKNOWN_ID, "describe a kernel and a gpu first");
   cudaSetDevice(c->device);
   ws_status s = upload(c);
   if (s != WS_OK) return s;
+  const size_t chunk = chunk_configs(c, 1);   // bounded scratch (see chunk_configs)
+  if (n <= chunk) return estimate_launch(c, d_cfgs, n, d_out, true, nullptr);
+  uint32_t launches = 0;
+  for (size_t off = 0; off < n; off += chunk) {
+    s = estimate_launch(c, d_cfgs + off, std::min(chunk, n - off), d_out + off, false, nullptr);
+    if (s != WS_OK) return s;
+    launches += c->last_launches;
+  }
+  c->last_launches = launches;
+  return WS_OK;
+}
+
+static uint64_t fan_hash(const FanOut* f) {  // FNV-1a over the fan-out descriptor (graph key)
+  if (!f) return 0;
+  uint64_t h = 1469598103934665603ull;
+  const unsigned char* p = (const unsigned char*)f;
+  for (size_t i = 0; i < sizeof(FanOut); ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h | 1;
+}
+
+// One launch sequence of the estimator over n configurations (fan == nullptr), or, for
+// ws_estimate_multi, over fan->m configurations x fan->n_groups representative hardware sets
+// with the model fanned out to fan->n_gpu sets (d_cfgs: the caller's configurations).
+static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out, bool allow_graph,
+                                 const FanOut* fan) {
+  ws_status s;
   Scratch S;
-  if ((s = ensure_scratch(c, n, S)) != WS_OK) return s;
+  const size_t n_int = fan ? (size_t)fan->m * fan->n_groups : n;
+  if ((s = ensure_scratch(c, n_int, S)) != WS_OK) return s;
+  ws_config* xcfg = nullptr;
+  if (fan) {
+    if ((s = grow(c, c->xcfg, c->xcfg_cap, n_int * sizeof(ws_config), "expanded configurations")) != WS_OK) return s;
+    xcfg = (ws_config*)c->xcfg;
+  }
+  const ws_config* icfg = fan ? xcfg : d_cfgs;
   cudaEvent_t* ev = c->profiling ? c->take_events(K_PLAN, kEstimateKernels) : nullptr;
   if (ev) c->pending.back().skip = 1u << (K_SCAN - K_PLAN);  // folded into k_plan
   Streams st;
@@ -501,12 +589,25 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   st.fork = c->fork;
   st.join[0] = c->join[0];
   st.join[1] = c->join[1];
+  auto enqueue = [&](uint32_t* launches, cudaEvent_t* evs) -> int {
+    uint32_t extra = 0;
+    if (fan) {
+      const int e0 = launch_expand(d_cfgs, *fan, xcfg, st.main);
+      if (e0) return e0;
+      extra = 1;
+    }
+    const int e1 = launch_estimate(icfg, (int)n_int, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st,
+                                   c->n_sm_dev, launches, evs, fan);
+    if (launches) *launches += extra;
+    return e1;
+  };
   // graph replay unless profiling (per-kernel events), serial diagnostics, or the caller's
   // stream is itself being captured (then the launches become part of the caller's graph)
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(c->stream, &cs);
-  if (c->graphs && !ev && !serial && cs == cudaStreamCaptureStatusNone) {
-    const ws_ctx::GKey key{d_cfgs, d_out, c->scratch, c->dk, c->dg, n, (int)c->hk.size(), (int)c->hg.size()};
+  if (allow_graph && c->graphs && !ev && !serial && cs == cudaStreamCaptureStatusNone) {
+    const ws_ctx::GKey key{d_cfgs, d_out, c->scratch, c->dk, c->dg, n, (int)c->hk.size(), (int)c->hg.size(),
+                           fan_hash(fan), xcfg};
     if (!c->gexec || !(key == c->gkey)) {
       if (c->gexec) {
         cudaGraphExecDestroy(c->gexec);
@@ -515,8 +616,7 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
       st.main = c->cap;
       cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
       if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
-      launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st, c->n_sm_dev,
-                      &c->g_launches, nullptr);
+      enqueue(&c->g_launches, nullptr);
       cudaGraph_t g = nullptr;
       e = cudaStreamEndCapture(c->cap, &g);
       if (e == cudaSuccess) e = cudaGraphInstantiate(&c->gexec, g, 0);
@@ -532,10 +632,33 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
     c->last_launches = c->g_launches;
     return WS_OK;
   }
-  int e = launch_estimate(d_cfgs, (int)n, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st,
-                          c->n_sm_dev, &c->last_launches, ev);
+  int e = enqueue(&c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "launch");
   return WS_OK;
+}
+
+// Per-configuration scratch bytes and the chunk size that keeps the scratch within the budget
+// (WS_SCRATCH_MB, default 4096): larger batches run as consecutive chunks on the same stream
+// (results identical: configurations are independent; chunks use direct launches).
+static size_t chunk_configs(ws_ctx* c, size_t per_item_mult) {
+  Scratch S0;
+  size_t b1 = 0, b2 = 0;
+  ensure_scratch(c, 1, S0, &b1);
+  ensure_scratch(c, 2, S0, &b2);
+  const size_t per = std::max<size_t>(1, b2 - b1) * per_item_mult, fixed = b1 > per ? b1 - per : 0;
+  static const size_t budget = (getenv("WS_SCRATCH_MB") ? (size_t)atoll(getenv("WS_SCRATCH_MB")) : 4096) << 20;
+  return budget > fixed + per ? (budget - fixed) / per : 1;
+}
+
+// Integer-stage key of a hardware set: every ws_gpu parameter the kernels before the model read
+// (occupancy limits, SM count, sector / line / bank geometry, sections, pages, link on/off).
+static bool same_integer_stage(const DGpu& a, const DGpu& b) {
+  const ws_gpu &x = a.g, &y = b.g;
+  return x.n_sm == y.n_sm && x.max_thr_sm == y.max_thr_sm && x.max_blk_sm == y.max_blk_sm &&
+         x.max_thr_blk == y.max_thr_blk && x.regs_sm == y.regs_sm && x.sector_bytes == y.sector_bytes &&
+         x.line_bytes == y.line_bytes && x.n_banks == y.n_banks && x.bank_bytes == y.bank_bytes &&
+         x.half_warp == y.half_warp && x.pair_window_bytes == y.pair_window_bytes && x.l2_sections == y.l2_sections &&
+         x.page_bytes == y.page_bytes && (x.link_bw > 0) == (y.link_bw > 0);
 }
 
 ws_status ws_estimate(ws_ctx* c, const ws_config* cfgs, size_t n, ws_result* out) {
@@ -564,13 +687,83 @@ ws_status ws_estimate(ws_ctx* c, const ws_config* cfgs, size_t n, ws_result* out
   return WS_OK;
 }
 
+ws_status ws_estimate_multi_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, const uint32_t* gpu_ids,
+                                  uint32_t n_gpu, ws_result* d_out) {
+  if (!c) return WS_EINVAL;
+  if (n == 0 || n_gpu == 0) return WS_OK;
+  if (!d_cfgs || !d_out || !gpu_ids) return fail(c, WS_EINVAL, "null argument");
+  if (n_gpu > (uint32_t)kMaxFanGpus) return fail(c, WS_ELIMIT, "at most 256 hardware sets per call");
+  if (n * n_gpu > kMaxBatch) return fail(c, WS_ELIMIT, "n * n_gpu larger than 2^24 records");
+  if (c->hk.empty() || c->hg.empty()) return fail(c, WS_EUNKNOWN_ID, "describe a kernel and a gpu first");
+  for (uint32_t g = 0; g < n_gpu; ++g)
+    if (gpu_ids[g] >= c->hg.size()) return fail(c, WS_EUNKNOWN_ID, "gpu_ids: id not described in this context");
+  cudaSetDevice(c->device);
+  ws_status s = upload(c);
+  if (s != WS_OK) return s;
+  FanOut f;
+  memset(&f, 0, sizeof(f));
+  f.n = (int32_t)n;
+  f.n_gpu = (int32_t)n_gpu;
+  for (uint32_t g = 0; g < n_gpu; ++g) {
+    int grp = -1;
+    for (int j = 0; j < f.n_groups && grp < 0; ++j)
+      if (same_integer_stage(c->hg[f.rep[j]], c->hg[gpu_ids[g]])) grp = j;
+    if (grp < 0) {
+      grp = f.n_groups++;
+      f.rep[grp] = gpu_ids[g];
+    }
+    f.group[g] = (uint16_t)grp;
+    f.gid[g] = (uint16_t)gpu_ids[g];
+  }
+  c->last_groups = (uint32_t)f.n_groups;
+  const size_t chunk = chunk_configs(c, (size_t)f.n_groups);
+  uint32_t launches = 0;
+  for (size_t off = 0; off < n; off += chunk) {
+    f.i0 = (int32_t)off;
+    f.m = (int32_t)std::min(chunk, n - off);
+    s = estimate_launch(c, d_cfgs, n, d_out, n <= chunk, &f);
+    if (s != WS_OK) return s;
+    launches += c->last_launches;
+  }
+  c->last_launches = launches;
+  return WS_OK;
+}
+
+ws_status ws_estimate_multi(ws_ctx* c, const ws_config* cfgs, size_t n, const uint32_t* gpu_ids, uint32_t n_gpu,
+                            ws_result* out) {
+  if (!c) return WS_EINVAL;
+  if (n == 0 || n_gpu == 0) return WS_OK;
+  if (!cfgs || !out || !gpu_ids) return fail(c, WS_EINVAL, "null argument");
+  if (n * n_gpu > kMaxBatch) return fail(c, WS_ELIMIT, "n * n_gpu larger than 2^24 records");
+  cudaSetDevice(c->device);
+  const size_t need = align_up(n * sizeof(ws_config)) + n * n_gpu * sizeof(ws_result);
+  cudaError_t e;
+  ws_status s = grow(c, c->io, c->io_cap, need, "device io buffer");
+  if (s != WS_OK) return s;
+  ws_config* dc = (ws_config*)c->io;
+  ws_result* dr = (ws_result*)((char*)c->io + align_up(n * sizeof(ws_config)));
+  if ((e = cudaMemcpyAsync(dc, cfgs, n * sizeof(ws_config), cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "H2D configs");
+  s = ws_estimate_multi_async(c, dc, n, gpu_ids, n_gpu, dr);
+  if (s != WS_OK) return s;
+  if ((e = cudaMemcpyAsync(out, dr, n * n_gpu * sizeof(ws_result), cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "D2H results");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "estimate_multi");
+  return WS_OK;
+}
+
+uint32_t ws_last_group_count(const ws_ctx* c) { return c ? c->last_groups : 0; }
+
 ws_status ws_rank_async(ws_ctx* c, ws_result* d_res, size_t n, size_t k, uint32_t* d_top) {
   if (!c) return WS_EINVAL;
   if (n == 0) return WS_OK;
   if (!d_res) return fail(c, WS_EINVAL, "null argument");
+  if (n > (size_t)kMaxBatch) return fail(c, WS_ELIMIT, "rank: more than 2^24 records");
   cudaSetDevice(c->device);
+  ws_status s = grow(c, c->rank_buf, c->rank_cap, rank_scratch_bytes((int)n), "rank scratch");
+  if (s != WS_OK) return s;
   cudaEvent_t* ev = c->profiling ? c->take_events(K_RANK, 1) : nullptr;
-  int e = launch_rank(d_res, (int)n, (int)std::min(k, n), d_top, c->stream, &c->last_launches, ev);
+  int e = launch_rank(d_res, (int)n, (int)std::min(k, n), d_top, c->rank_buf, c->stream, &c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "rank launch");
   return WS_OK;
 }
@@ -579,12 +772,14 @@ ws_status ws_rank(ws_ctx* c, ws_result* res, size_t n, size_t k, uint32_t* top) 
   if (!c) return WS_EINVAL;
   if (n == 0) return WS_OK;
   if (!res) return fail(c, WS_EINVAL, "null argument");
+  if (n > (size_t)kMaxBatch) return fail(c, WS_ELIMIT, "rank: more than 2^24 records");
   cudaSetDevice(c->device);
   k = std::min(k, n);
-  void* buf = nullptr;
   cudaError_t e;
   const size_t bytes = align_up(n * sizeof(ws_result)) + (k + 1) * sizeof(uint32_t);
-  if ((e = cudaMalloc(&buf, bytes)) != cudaSuccess) return fail(c, WS_ENOMEM, "rank buffer");
+  ws_status s0 = grow(c, c->rank_io, c->rank_io_cap, bytes, "rank buffer");   // kept by the context
+  if (s0 != WS_OK) return s0;
+  void* buf = c->rank_io;
   ws_result* dr = (ws_result*)buf;
   uint32_t* dt = (uint32_t*)((char*)buf + align_up(n * sizeof(ws_result)));
   ws_status s = WS_OK;
@@ -598,7 +793,6 @@ ws_status ws_rank(ws_ctx* c, ws_result* res, size_t n, size_t k, uint32_t* top) 
     else if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess)
       s = cuda_fail(c, e, "rank");
   }
-  cudaFree(buf);
   return s;
 }
 

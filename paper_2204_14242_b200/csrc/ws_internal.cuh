@@ -172,10 +172,20 @@ struct Streams {
   cudaStream_t main, aux[2];
   cudaEvent_t fork, join[2];
 };
-// ev: nullptr, or 2 events per kernel (start, end) in K_* order, recorded on the kernel's stream
+// ws_estimate_multi (BJ configs[3]): one integer pass over m configurations x n_groups
+// representative hardware sets, the model over m x n_gpu outputs (k_expand / k_model_fan).
+constexpr int kMaxFanGpus = 256;
+struct FanOut {
+  int32_t n, i0, m, n_gpu, n_groups, pad;  // n: configurations of the call (output stride); [i0, i0+m): this chunk
+  uint32_t rep[kMaxFanGpus];               // group -> representative gpu id (the integer pass runs with it)
+  uint16_t group[kMaxFanGpus], gid[kMaxFanGpus];  // output hardware set g -> its group, its gpu id
+};
+// ev: nullptr, or 2 events per kernel (start, end) in K_* order, recorded on the kernel's stream.
+// fan: nullptr (k_model writes d_out[0..n)) or the fan-out of ws_estimate_multi (n = m * n_groups).
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                     const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
-                    cudaEvent_t* ev);
+                    cudaEvent_t* ev, const FanOut* fan = nullptr);
+int launch_expand(const ws_config* d_cfgs, const FanOut& f, ws_config* xcfg, cudaStream_t st);
 // ---------------------------------------------------------------- NEXT-1: simulated hit rates
 // Request encoding: bits 0..45 sector + 2^45, bit 46 store, bits 48..55 field.
 constexpr int kSimSecBits = 46;
@@ -213,8 +223,10 @@ struct SimScratch {
 };
 
 // ev: nullptr or 2 events (start, end)
-int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches,
+// scratch: rank_scratch_bytes(n) bytes of device memory (none for n <= 16384)
+int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, void* scratch, cudaStream_t st, uint32_t* launches,
                 cudaEvent_t* ev);
+size_t rank_scratch_bytes(int n);
 
 // NEXT-1 (ws_kernels.cu): the whole ws_simulate device sequence (estimate, request streams,
 // stack-distance simulation, sample records) on st.main, synchronous; returns 0, a

@@ -2818,30 +2818,252 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
   for (int i = lane; i < (int)(sizeof(ws_result) / 8); i += 32) dst[i] = src[i];
 }
 
+// BJ configs[3] architecture exploration (ws_estimate_multi): the integer stages ran once per
+// group of hardware sets that agree in every parameter they read; the FP64 model fans out over
+// the group's sets.  Expanded batch: xcfg[j * m + t] = cfgs[i0 + t] with the group's
+// representative gpu id; output out[g * n + i0 + t] from the plan / accumulators of entry
+// group[g] * m + t and the descriptor of gid[g].
+__global__ void __launch_bounds__(256) k_expand(const ws_config* __restrict__ cfgs, FanOut f,
+                                                ws_config* __restrict__ xcfg) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= (long long)f.m * f.n_groups) return;
+  const int grp = (int)(j / f.m), t = (int)(j % f.m);
+  ws_config c = cfgs[f.i0 + t];
+  c.gpu_id = f.rep[grp];
+  xcfg[j] = c;
+}
+
+__global__ void __launch_bounds__(128) k_model_fan(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                                   const DGpu* __restrict__ gs, const unsigned long long* __restrict__ acc,
+                                                   FanOut f, ws_result* __restrict__ out) {
+  __shared__ unsigned long long s_a[4][A_N];
+  __shared__ ws_result s_r[4];
+  __shared__ __align__(16) DPlan s_p[4];
+  __shared__ __align__(16) DGpu s_gp[4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long o = (long long)blockIdx.x * 4 + w;   // output entry (g, t)
+  if (o >= (long long)f.m * f.n_gpu) return;
+  const int g = (int)(o / f.m), t = (int)(o % f.m);
+  const long long c = (long long)f.group[g] * f.m + t;  // integer entry
+  if (lane < A_N) s_a[w][lane] = acc[c * A_N + lane];
+  {
+    const uint4* sp = reinterpret_cast<const uint4*>(plans + c);
+    uint4* dp = reinterpret_cast<uint4*>(&s_p[w]);
+    for (int i = lane; i < (int)(sizeof(DPlan) / 16); i += 32) dp[i] = sp[i];
+    const uint4* sg = reinterpret_cast<const uint4*>(gs + f.gid[g]);
+    uint4* dg = reinterpret_cast<uint4*>(&s_gp[w]);
+    for (int i = lane; i < (int)(sizeof(DGpu) / 16); i += 32) dg[i] = sg[i];
+  }
+  __syncwarp();
+  if (lane == 0) model_one(s_p[w], ks, s_gp[w], s_a[w], s_r[w]);
+  __syncwarp();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s_r[w]);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(out + (long long)g * f.n + f.i0 + t);
+  for (int i = lane; i < (int)(sizeof(ws_result) / 8); i += 32) dst[i] = src[i];
+}
+
+int launch_expand(const ws_config* d_cfgs, const FanOut& f, ws_config* xcfg, cudaStream_t st) {
+  const long long m = (long long)f.m * f.n_groups;
+  k_expand<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(d_cfgs, f, xcfg);
+  return (int)cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ a8: rank
-__global__ void __launch_bounds__(256) k_rank(ws_result* __restrict__ res, int n, int k, uint32_t* __restrict__ top) {
-  __shared__ double s_key[256];
+// Rank by (t_pred ascending, index ascending), failed configurations last:
+// a sort of 64-bit order-preserving keys (IEEE bits with the sign folded; failed = +inf) carrying
+// the configuration index; (key, index) pairs are unique, so every comparison is strict.
+//   n <= kRankSmem: one CTA, bitonic sort in shared memory, ranks written directly;
+//   n <= kRankMerge: tiles of kRankTile sorted the same way by one CTA each, then every element's
+//     rank = its position in its tile + the number of smaller pairs in every other tile (binary
+//     searches of the sorted tiles);
+//   larger n: a stable LSD radix sort, 8 passes of 8 bits (tile histogram -> one-CTA scan -> stable
+//     tile scatter), whose stability over the index-ordered input gives the index tie-break.
+constexpr int kRankSmem = 16384;
+constexpr int kRankTile = 4096;
+constexpr int kRankMerge = 1 << 18;
+constexpr int kRkTile = 2048;
+__device__ __forceinline__ unsigned long long rank_key(const ws_result& r) {
+  if (r.status != WS_OK) return 0xfff0000000000000ull;     // +inf after the fold below
+  const unsigned long long b = (unsigned long long)__double_as_longlong(r.t_pred);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+// CTA b sorts the P-element tile [b*P, b*P+P) of the records (padding: key ~0, sorts last); with
+// skey == nullptr (a single tile) it writes ranks and top-k, else the sorted tile to skey / sidx.
+__global__ void __launch_bounds__(1024) k_rank_smem(ws_result* __restrict__ res, int n, int P, int k,
+                                                    uint32_t* __restrict__ top, unsigned long long* __restrict__ skey,
+                                                    uint32_t* __restrict__ sidx) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(s_raw);
+  uint32_t* idx = reinterpret_cast<uint32_t*>(s_raw + (size_t)P * 8);
+  const int base = blockIdx.x * P;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const int g = base + i;
+    key[i] = g < n ? rank_key(res[g]) : ~0ull;
+    idx[i] = (uint32_t)g;
+  }
+  __syncthreads();
+  const int half = P >> 1;
+  for (int kk = 2; kk <= P; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < half; t += blockDim.x) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), l = i + j;
+        const unsigned long long ki = key[i], kl = key[l];
+        const uint32_t ii = idx[i], il = idx[l];
+        const bool gt = ki > kl || (ki == kl && ii > il);
+        if (gt == ((i & kk) == 0)) {
+          key[i] = kl;
+          key[l] = ki;
+          idx[i] = il;
+          idx[l] = ii;
+        }
+      }
+      __syncthreads();
+    }
+  if (!skey) {
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+      const uint32_t c = idx[p];
+      res[c].rank = (uint32_t)p;
+      if (p < k && top) top[p] = c;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    skey[base + i] = key[i];
+    sidx[base + i] = idx[i];
+  }
+}
+// global rank of every element from the sorted tiles (one thread per sorted position)
+__global__ void __launch_bounds__(256) k_rank_merge(ws_result* __restrict__ res, int n, int P, int ntiles, int k,
+                                                    uint32_t* __restrict__ top, const unsigned long long* __restrict__ skey,
+                                                    const uint32_t* __restrict__ sidx) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ntiles * P) return;
+  const uint32_t c = sidx[q];
+  if ((int)c >= n) return;                         // padding
+  const unsigned long long x = skey[q];
+  const int my = q / P;
+  long long r = q - (long long)my * P;             // smaller pairs in its own tile
+  for (int t = 0; t < ntiles; ++t) {
+    if (t == my) continue;
+    const unsigned long long* K = skey + (long long)t * P;
+    const uint32_t* I = sidx + (long long)t * P;
+    int lo = 0, hi = P;                            // first position whose pair is > (x, c)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const unsigned long long km = K[mid];
+      if (km < x || (km == x && I[mid] < c)) lo = mid + 1;
+      else hi = mid;
+    }
+    r += lo;
+  }
+  res[c].rank = (uint32_t)r;
+  if (r < k && top) top[r] = c;
+}
+__global__ void __launch_bounds__(256) k_rank_keys(const ws_result* __restrict__ res, int n,
+                                                   unsigned long long* __restrict__ key, uint32_t* __restrict__ val) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const double INF = __longlong_as_double(0x7ff0000000000000ll);
-  double ki = INF;
-  if (i < n) ki = res[i].status == WS_OK ? res[i].t_pred : INF;
-  unsigned int rank = 0;
-  for (int base = 0; base < n; base += 256) {
-    const int j = base + threadIdx.x;
-    s_key[threadIdx.x] = j < n ? (res[j].status == WS_OK ? res[j].t_pred : INF) : INF;
+  if (i < n) {
+    key[i] = rank_key(res[i]);
+    val[i] = (uint32_t)i;
+  }
+}
+__global__ void __launch_bounds__(256) k_rank_hist(const unsigned long long* __restrict__ key, int n, int shift,
+                                                   uint32_t* __restrict__ hist, int ntiles) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int t0 = blockIdx.x * kRkTile;
+  for (int r = 0; r < kRkTile / 256; ++r) {
+    const int i = t0 + r * 256 + threadIdx.x;
+    if (i < n) atomicAdd(&h[(unsigned)(key[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];   // digit-major
+}
+// one CTA: exclusive scan of m counts in place (each thread a contiguous segment)
+__global__ void __launch_bounds__(1024) k_rank_scan(uint32_t* __restrict__ v, int m) {
+  __shared__ uint32_t s_w[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int seg = (m + 1023) / 1024, a = tid * seg, b = min(m, a + seg);
+  uint32_t sum = 0;
+  for (int i = a; i < b; ++i) sum += v[i];
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = s_w[lane], z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, z, o);
+      if (lane >= o) z += y;
+    }
+    s_w[lane] = z - w;
+  }
+  __syncthreads();
+  uint32_t run = s_w[wid] + x - sum;
+  for (int i = a; i < b; ++i) {
+    const uint32_t t = v[i];
+    v[i] = run;
+    run += t;
+  }
+}
+__global__ void __launch_bounds__(256) k_rank_scatter(const unsigned long long* __restrict__ key,
+                                                      const uint32_t* __restrict__ val, int n, int shift,
+                                                      const uint32_t* __restrict__ off, int ntiles,
+                                                      unsigned long long* __restrict__ key2, uint32_t* __restrict__ val2) {
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wc[8][256];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  run[tid] = off[tid * ntiles + blockIdx.x];
+  const int t0 = blockIdx.x * kRkTile;
+  for (int r = 0; r < kRkTile / 256; ++r) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) wc[w][tid] = 0u;
     __syncthreads();
-    const int lim = n - base < 256 ? n - base : 256;
-    for (int jj = 0; jj < lim; ++jj) {
-      const double kj = s_key[jj];
-      const int j2 = base + jj;
-      rank += (kj < ki || (kj == ki && j2 < i)) ? 1u : 0u;
+    const int i = t0 + r * 256 + tid;
+    const bool ok = i < n;
+    const unsigned long long kk = ok ? key[i] : 0ull;
+    const uint32_t v = ok ? val[i] : 0u;
+    const uint32_t d = (unsigned)(kk >> shift) & 255u;
+    const unsigned peers = __match_any_sync(FULL, ok ? d : 0x100u + (unsigned)lane);
+    const int rk = __popc(peers & ((1u << lane) - 1u));
+    if (ok && rk == 0) wc[wid][d] = (uint32_t)__popc(peers);
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < wid; ++w) before += wc[w][d];
+    if (ok) {
+      const uint32_t pos = run[d] + before + (uint32_t)rk;
+      key2[pos] = kk;
+      val2[pos] = v;
     }
     __syncthreads();
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += wc[w][tid];
+    run[tid] += tot;
+    __syncthreads();
   }
-  if (i < n) {
-    res[i].rank = rank;
-    if ((int)rank < k && top) top[rank] = (uint32_t)i;
+}
+__global__ void __launch_bounds__(256) k_rank_out(ws_result* __restrict__ res, const uint32_t* __restrict__ val, int n,
+                                                  int k, uint32_t* __restrict__ top) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    const uint32_t c = val[p];
+    res[c].rank = (uint32_t)p;
+    if (p < k && top) top[p] = c;
   }
+}
+
+size_t rank_scratch_bytes(int n) {
+  if (n <= kRankSmem) return 0;
+  if (n <= kRankMerge) return ((size_t)n + kRankTile) * 12 + 1024;
+  const size_t nt = (size_t)(n + kRkTile - 1) / kRkTile;
+  return 2 * (size_t)n * 8 + 2 * (size_t)n * 4 + 256 * nt * 4 + 1024;
 }
 
 // ------------------------------------------------------------------ launchers
@@ -2852,7 +3074,7 @@ static int check_launch() {
 
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                     const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
-                    cudaEvent_t* ev) {
+                    cudaEvent_t* ev, const FanOut* fan) {
   uint32_t L = 0;
   auto beg = [&](int kind, cudaStream_t q) {
     if (ev) cudaEventRecord(ev[2 * kind], q);
@@ -2914,18 +3136,60 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   cudaStreamWaitEvent(m, st.join[0], 0);
   cudaStreamWaitEvent(m, st.join[1], 0);
   beg(K_MODEL, m);
-  k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out);
+  if (fan)
+    k_model_fan<<<(unsigned)(((long long)fan->m * fan->n_gpu + 3) / 4), 128, 0, m>>>(s.plans, d_k, d_g, s.acc, *fan,
+                                                                                    d_out);
+  else
+    k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out);
   end(K_MODEL, m);
   if (launches) *launches = L;
   return check_launch();
 }
 
-int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, cudaStream_t st, uint32_t* launches,
+int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, void* scratch, cudaStream_t st, uint32_t* launches,
                 cudaEvent_t* ev) {
   if (ev) cudaEventRecord(ev[0], st);
-  k_rank<<<(n + 255) / 256, 256, 0, st>>>(d_res, n, k, d_top);
+  uint32_t L = 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rank_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmem * 12);
+    attr = true;
+  }
+  if (n <= kRankSmem) {
+    int P = 32;
+    while (P < n) P <<= 1;
+    k_rank_smem<<<1, P / 2 < 1024 ? P / 2 : 1024, (size_t)P * 12, st>>>(d_res, n, P, k, d_top, nullptr, nullptr);
+    L = 1;
+  } else if (n <= kRankMerge) {
+    const int nt = (n + kRankTile - 1) / kRankTile;
+    unsigned long long* skey = (unsigned long long*)scratch;
+    uint32_t* sidx = (uint32_t*)(skey + (size_t)nt * kRankTile);
+    k_rank_smem<<<nt, 1024, (size_t)kRankTile * 12, st>>>(d_res, n, kRankTile, k, d_top, skey, sidx);
+    k_rank_merge<<<(nt * kRankTile + 255) / 256, 256, 0, st>>>(d_res, n, kRankTile, nt, k, d_top, skey, sidx);
+    L = 2;
+  } else {
+    const int nt = (n + kRkTile - 1) / kRkTile;
+    char* b = (char*)scratch;
+    unsigned long long* k0 = (unsigned long long*)b;
+    unsigned long long* k1 = k0 + n;
+    uint32_t* v0 = (uint32_t*)(k1 + n);
+    uint32_t* v1 = v0 + n;
+    uint32_t* hist = v1 + n;
+    k_rank_keys<<<(n + 255) / 256, 256, 0, st>>>(d_res, n, k0, v0);
+    ++L;
+    for (int pass = 0; pass < 8; ++pass) {
+      k_rank_hist<<<nt, 256, 0, st>>>(k0, n, 8 * pass, hist, nt);
+      k_rank_scan<<<1, 1024, 0, st>>>(hist, 256 * nt);
+      k_rank_scatter<<<nt, 256, 0, st>>>(k0, v0, n, 8 * pass, hist, nt, k1, v1);
+      L += 3;
+      std::swap(k0, k1);
+      std::swap(v0, v1);
+    }
+    k_rank_out<<<(n + 255) / 256, 256, 0, st>>>(d_res, v0, n, k, d_top);
+    ++L;
+  }
   if (ev) cudaEventRecord(ev[1], st);
-  if (launches) *launches = 1;
+  if (launches) *launches = L;
   return check_launch();
 }
 

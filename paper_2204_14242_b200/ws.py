@@ -79,7 +79,8 @@ RESULT_DTYPE = np.dtype(ws_result)
 EXPORTS = ["ws_create", "ws_destroy", "ws_last_error", "ws_set_stream", "ws_describe_kernel", "ws_describe_gpu",
            "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count",
            "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read", "ws_simulate",
-           "ws_sim_release", "ws_fit_gompertz", "ws_validate_stencil25", "ws_validate_lbm15"]
+           "ws_sim_release", "ws_fit_gompertz", "ws_validate_stencil25", "ws_validate_lbm15",
+           "ws_estimate_multi", "ws_estimate_multi_async", "ws_last_group_count"]
 
 _lib = None
 
@@ -104,6 +105,10 @@ def load_library(path: str = LIB_PATH):
     L.ws_describe_gpu.argtypes = [P, C.POINTER(ws_gpu), C.POINTER(U32)]
     L.ws_estimate.argtypes = [P, P, C.c_size_t, P]
     L.ws_estimate_async.argtypes = [P, P, C.c_size_t, P]
+    L.ws_estimate_multi.argtypes = [P, P, C.c_size_t, P, U32, P]
+    L.ws_estimate_multi_async.argtypes = [P, P, C.c_size_t, P, U32, P]
+    L.ws_last_group_count.argtypes = [P]
+    L.ws_last_group_count.restype = U32
     L.ws_rank.argtypes = [P, P, C.c_size_t, C.c_size_t, P]
     L.ws_rank_async.argtypes = [P, P, C.c_size_t, C.c_size_t, P]
     L.ws_last_launch_count.argtypes = [P]
@@ -119,7 +124,7 @@ def load_library(path: str = LIB_PATH):
     L.ws_kernel_name.argtypes = [U32]
     L.ws_kernel_name.restype = C.c_char_p
     for n in EXPORTS:
-        if n not in ("ws_destroy", "ws_last_error", "ws_last_launch_count", "ws_kernel_name"):
+        if n not in ("ws_destroy", "ws_last_error", "ws_last_launch_count", "ws_kernel_name", "ws_last_group_count"):
             getattr(L, n).restype = C.c_int
     _lib = L
     return L
@@ -247,6 +252,24 @@ class Context:
     def estimate_async(self, d_cfgs: int, n: int, d_out: int):
         """Device pointers; enqueued on the context stream."""
         self._check(self.L.ws_estimate_async(self.h, C.c_void_p(d_cfgs), n, C.c_void_p(d_out)))
+
+    def estimate_multi(self, cfgs: np.ndarray, gpu_ids) -> np.ndarray:
+        """Every configuration against every hardware set: -> (n_gpu, n) RESULT_DTYPE array."""
+        cfgs = np.ascontiguousarray(cfgs, dtype=CONFIG_DTYPE)
+        ids = np.ascontiguousarray(gpu_ids, dtype=np.uint32)
+        out = np.zeros(len(ids) * len(cfgs), dtype=RESULT_DTYPE)
+        self._check(self.L.ws_estimate_multi(self.h, cfgs.ctypes.data, len(cfgs), ids.ctypes.data, len(ids),
+                                             out.ctypes.data))
+        return out.reshape(len(ids), len(cfgs))
+
+    def estimate_multi_async(self, d_cfgs: int, n: int, gpu_ids, d_out: int):
+        """Device configurations (n) and results (n * len(gpu_ids)); gpu_ids on the host."""
+        ids = np.ascontiguousarray(gpu_ids, dtype=np.uint32)
+        self._check(self.L.ws_estimate_multi_async(self.h, C.c_void_p(d_cfgs), n, ids.ctypes.data, len(ids),
+                                                   C.c_void_p(d_out)))
+
+    def last_group_count(self) -> int:
+        return int(self.L.ws_last_group_count(self.h))
 
     def rank(self, res: np.ndarray, k: int):
         top = np.zeros(max(1, k), dtype=np.uint32)

@@ -1,0 +1,141 @@
+"""GPU tests of the round-2 boundary additions, through the C ABI:
+
+* ws_rank at scale: the one-CTA shared-memory sort (n <= 16384) and the radix path (larger n)
+  against a plain numpy lexsort of (t_pred, index), with ties and failed records;
+* describe-time errors of SURVEY 8(b): alignment not a multiple of the element size, more than 16
+  distinct x-offset runs in a field;
+* ws_estimate_multi (BJ configs[3]): byte-identical to one ws_estimate per hardware set, and
+  against the oracle on sampled (configuration, hardware set) pairs.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+from parity_util import compare
+
+pytestmark = pytest.mark.gpu
+NT = max(1, min(32, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2204_14242_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _synthetic_results(n, seed):
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+    rng = np.random.default_rng(seed)
+    r = np.zeros(n, dtype=RESULT_DTYPE)
+    r["t_pred"] = rng.choice(rng.random(max(2, n // 7)) * 1e-3, n)      # many exact ties
+    r["status"] = np.where(rng.random(n) < 0.03, 2, 0)
+    return r
+
+
+def _expected_order(r):
+    key = np.where(r["status"] == 0, r["t_pred"], np.inf)
+    return np.lexsort((np.arange(len(r)), key))
+
+
+@pytest.mark.parametrize("n", [1, 2, 168, 5000, 16384, 16385, 100000, 300001])
+def test_rank_sort_paths(ctx, n):
+    r = _synthetic_results(n, n)
+    top = ctx.rank(r, 10)
+    order = _expected_order(r)
+    assert np.array_equal(r["rank"][order], np.arange(n))
+    assert list(top) == list(order[:10])
+
+
+def test_rank_async_device_time(ctx):
+    """Radix path on 10^5 device-resident records: time per ws_rank_async (CUDA events)."""
+    import torch
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+    n = 100000
+    r = _synthetic_results(n, 7)
+    d = torch.from_numpy(r.view(np.uint8).copy()).cuda()
+    top = torch.zeros(10, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        ctx.rank_async(d.data_ptr(), n, 10, top.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        ctx.rank_async(d.data_ptr(), n, 10, top.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    print(f"ws_rank_async n={n}: {ms * 1e3:.1f} us")
+    back = np.frombuffer(d.cpu().numpy().tobytes(), dtype=RESULT_DTYPE)
+    assert np.array_equal(back["rank"][_expected_order(r)], np.arange(n))
+    assert ms < 1.0
+
+
+def test_describe_alignment_and_run_limits(ctx):
+    from paper_2204_14242_b200 import WSError
+    k = W.k7(8)
+    k["fields"][0] = dict(k["fields"][0], align=4)           # 8 B elements at a 4 B alignment
+    with pytest.raises(WSError) as e:
+        ctx.describe_kernel(k)
+    assert e.value.status == 1
+    k["fields"][0] = dict(k["fields"][0], align=-8)
+    ctx.describe_kernel(k)                                   # negative multiples are valid
+    # 17 distinct x-offset runs in one field: loads at x offsets {0}, {2}, ... {32} (isolated)
+    runs = W.stencil_star(40, 4, 4, 1, regs=0)
+    f0 = dict(runs["fields"][0])
+    f0["extent"] = (80, f0["extent"][1], f0["extent"][2])
+    f0["pitch"] = (1, 80, 80 * f0["extent"][1])
+    runs["fields"] = [f0, dict(f0)]
+    runs["accesses"] = [(0, 0, (2 * i, 0, 0)) for i in range(17)] + [(1, 1, (0, 0, 0))]
+    with pytest.raises(WSError) as e:
+        ctx.describe_kernel(runs)
+    assert e.value.status == 2
+    runs["accesses"] = [(0, 0, (2 * i, 0, 0)) for i in range(16)] + [(1, 1, (0, 0, 0))]
+    ctx.describe_kernel(runs)
+
+
+def test_estimate_multi_byte_identical(ctx):
+    """configs[3]: the 168-config space at 96^3 x the 49 configs[3] hardware sets in one call ==
+    one ws_estimate per set (every byte of every record)."""
+    from paper_2204_14242_b200 import config_array
+    k = W.k25(96)
+    sets = W.hw_grid_configs3()
+    kid = ctx.describe_kernel(k)
+    gids = [ctx.describe_gpu(g) for g in sets]
+    cf = config_array(kid, 0, W.space_stencil_paper())
+    multi = ctx.estimate_multi(cf, gids)
+    assert ctx.last_group_count() == 5
+    for g, gid in enumerate(gids):
+        cf["gpu_id"] = gid
+        one = ctx.estimate(cf)
+        assert multi[g].tobytes() == one.tobytes(), sets[g]["name"]
+    multi2 = ctx.estimate_multi(cf, gids)          # graph replay
+    assert multi2.tobytes() == multi.tobytes()
+
+
+def test_estimate_multi_vs_oracle_sampled(ctx):
+    """configs[3] at the full 512^3 size: every configuration x the 49 hardware sets in one call;
+    sampled (configuration, set) pairs recomputed by the oracle."""
+    from paper_2204_14242_b200 import config_array, result_dicts
+    k = W.k25(512)
+    sets = W.hw_grid_configs3()
+    kid = ctx.describe_kernel(k)
+    gids = [ctx.describe_gpu(g) for g in sets]
+    space = W.space_stencil_paper()
+    multi = ctx.estimate_multi(config_array(kid, 0, space), gids)
+    assert (multi["status"] == 0).all()
+    cheap = [i for i, c in enumerate(space) if c[0][2] == 1 and c[1][2] == 1]   # shallow: seconds each
+    picks = [(g, cheap[(5 * g) % len(cheap)]) for g in (0, 1, 7, 13, 26, 40, 48)]
+    errs = []
+    for g, i in picks:
+        o = O.estimate(k, sets[g], space[i])
+        a = result_dicts(multi[g][i:i + 1])[0]
+        errs += compare(a, o, f"set{g} cfg{i} {space[i]}")
+    assert not errs, "\n".join(errs)

@@ -1,6 +1,7 @@
 """The estimator's alternate launch paths against the oracle, each in a fresh process (the
 switches are read once per process): fold by CTA / by warp (WS_FOLD_MODE), every chain on the
-context stream (WS_SERIAL), eager launches instead of CUDA-graph replay (WS_GRAPH=0)."""
+context stream (WS_SERIAL), eager launches instead of CUDA-graph replay (WS_GRAPH=0), batches split into scratch-bounded chunks
+(WS_SCRATCH_MB)."""
 import os
 import subprocess
 import sys
@@ -12,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.parametrize("env", [{"WS_FOLD_MODE": "1"}, {"WS_FOLD_MODE": "2"}, {"WS_SERIAL": "1"},
-                                 {"WS_GRAPH": "0"}], ids=["fold-cta", "fold-warp", "serial", "eager"])
+                                 {"WS_GRAPH": "0"}, {"WS_SCRATCH_MB": "8"}],
+                         ids=["fold-cta", "fold-warp", "serial", "eager", "chunked"])
 def test_launch_modes(env):
     import torch
     if not torch.cuda.is_available():

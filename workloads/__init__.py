@@ -90,6 +90,19 @@ def gpu_hypothetical(l1_kib, l2_eff_mib, n_sm):
                 l2_eff_mib * MiB, 1, 2000e9, 6000e9)
 
 
+def hw_grid_configs3(hbm_gbs=6546.2):
+    """BJ configs[3] architecture exploration: the B200-like set plus a hypothetical grid of
+    L1 {128, 192, 256} KiB x effective L2 {20, 40, 64, 126} MiB x SM count {108, 132, 148, 160}
+    (48 sets; P:307-320 parameter axes).  The integer stages depend only on the SM
+    count here (4 groups + the B200-like set's own)."""
+    sets = [gpu_b200_like(hbm_gbs)]
+    for nsm in (108, 132, 148, 160):
+        for l1 in (128, 192, 256):
+            for l2 in (20, 40, 64, 126):
+                sets.append(gpu_hypothetical(l1, l2, nsm))
+    return sets
+
+
 # ---------------------------------------------------------------------------
 # Kernels
 # ---------------------------------------------------------------------------
