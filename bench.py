@@ -9,12 +9,16 @@ layer-set scopes, model, ranking) over that batch.  At N GPUs every rank
 evaluates the same 168-config space on its own hardware parameter set
 (architecture exploration, BJ configs[3]: rank 0 = A100, then B200-like, V100
 and a hypothetical grid), the results are all-gathered over NCCL and every rank
-ranks the gathered set: per-GPU work is fixed -> "scaling": "weak".
+ranks the gathered set: per-GPU work is fixed -> "scaling": "weak".  The same run
+also measures BJ configs[3] with a fixed total (`configs3_strong`: 168 configs x 49
+hardware sets sharded by configuration over the ranks, one all-gather).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
 
-Rank 0 prints one JSON line.  `--impl reference` times the plain CPU oracle
-(oracle/) on the host cores instead (this tier's reference arm).
+`--gpus N` without a launcher starts N ranks itself (torch.distributed.run, one per
+GPU); under a launcher WORLD_SIZE must equal N.  Rank 0 prints one JSON line.
+`--impl reference` times the plain CPU oracle (oracle/) on the host cores instead
+(this tier's reference arm).
 """
 from __future__ import annotations
 
@@ -121,27 +125,77 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
+def host_info():
+    """CPU model, logical CPUs and RAM of the host the oracle runs on."""
+    model, mem = "unknown", 0
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        mem = int(open("/proc/meminfo").readline().split()[1]) // (1024 * 1024)
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count(), "ram_gib": mem}
+
+
+def stratified_sample(plans, cfgs, max_evals=1.0e8, stride=6):
+    """Configurations spread over the space's cost distribution: every `stride`-th configuration
+    in cost order among those the oracle finishes in about half a minute (<= max_evals address
+    evaluations, one host thread each) -- shallow and deep blocks, folded and unfolded."""
+    order = sorted(range(len(cfgs)), key=lambda i: plans[i]["addr_evals"])
+    ok = [i for i in order if plans[i]["status"] == 0 and plans[i]["addr_evals"] <= max_evals]
+    return [cfgs[i] for i in ok[::stride]]
+
+
+def full_space_timing():
+    """The measured single-thread oracle seconds of every configuration of configs[1] (written by
+    scripts/oracle_golden.py when it generated tests/golden/full_c1_k25_512_a100.json)."""
+    try:
+        doc = json.load(open(os.path.join(ROOT, "tests", "golden", "full_c1_k25_512_a100.json")))
+    except Exception:
+        return None
+    sec = doc.get("oracle_seconds") or []
+    if not sec:
+        return None
+    tot = sum(sec)
+    return {"configs": len(sec), "thread_seconds": tot, "configs_per_s_one_thread": len(sec) / tot,
+            "max_config_s": max(sec), "host": doc.get("host"),
+            "note": "measured: every configuration of the space once, one host thread each "
+                    "(scripts/oracle_golden.py), on the host named here (not the GPU box)"}
+
+
 def oracle_sample(kernel, gpu, cfgs, threads):
-    """Plain CPU oracle over a bounded sample of the workload, scaled to configs/s of the whole
-    space by the oracle's own work measure (addr_evals, the plain definition's address evaluations).
-    Sample: the shallow configurations (block z = 1, no z fold) -- about 1-3 s of CPU work each."""
+    """The plain CPU oracle on a bounded, stratified sample of the workload on all host threads,
+    extrapolated to configs/s of the whole space by the oracle's own work measure (addr_evals,
+    the plain definition's address evaluations): value = evals/s / mean evals per configuration."""
     from oracle import oracle as O
     plans = [O.plan(kernel, gpu, c) for c in cfgs]
     mean_evals = statistics.mean(p["addr_evals"] for p in plans if p["status"] == 0)
-    sample = [c for c in cfgs if c[0][2] == 1 and c[1] == (1, 1, 1)]
+    sample = stratified_sample(plans, cfgs)
     t0 = time.perf_counter()
     res = O.estimate_batch(kernel, gpu, sample, threads)
     dt = time.perf_counter() - t0
     ev = sum(r["addr_evals"] for r in res)
     rate = ev / dt
-    return {"value": rate / mean_evals, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": (f"{len(sample)} of {len(cfgs)} configs (block z=1, no fold) on {threads} host threads: "
-                       f"{dt:.2f} s wall, {ev:.3e} address evaluations -> {rate:.3e} evals/s, scaled by the "
-                       f"space's mean {mean_evals:.3e} evals/config"),
-            "sample_configs_per_s": len(sample) / dt, "evals_per_s": rate, "wall_s": dt}
+    out = {"value": rate / mean_evals, "unit": UNIT, "cores": min(threads, len(sample)), "kind": "oracle",
+           "estimated": True,
+           "sample": (f"{len(sample)} of {len(cfgs)} configs (stratified over the cost distribution, <= 1e8 "
+                      f"address evaluations each) on {min(threads, len(sample))} host threads: {dt:.2f} s wall, "
+                      f"{ev:.3e} address evaluations -> {rate:.3e} evals/s, extrapolated by the space's mean "
+                      f"{mean_evals:.3e} evals/config"),
+           "sample_configs_per_s": len(sample) / dt, "evals_per_s": rate, "wall_s": dt, "host": host_info()}
+    fs = full_space_timing()
+    if fs is not None:
+        out["full_space_measured"] = fs
+    return out
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the plain CPU oracle as it stands, on the host cores, on this arm's
+    configuration and metric.  Each step: one configuration per host thread, taken in turn from
+    the stratified sample of the space (cycled), timed; value = address evaluations per second
+    over the steps / the space's mean evaluations per configuration."""
     if rank != 0:
         return
     kernel, gpu, cfgs = W.k25(512), W.gpu_a100(), W.space_stencil_paper()
@@ -150,25 +204,26 @@ def run_reference(args, rank, world):
     O.build()
     plans = [O.plan(kernel, gpu, c) for c in cfgs]
     mean_evals = statistics.mean(p["addr_evals"] for p in plans if p["status"] == 0)
-    shallow = [c for c in cfgs if c[0][2] == 1 and c[1] == (1, 1, 1)]
-    # one configuration runs on one host thread (the oracle parallelises over configurations):
-    # time one (the first warm-up step); a step is one wave of configurations over the host
-    # threads, or a single configuration when K such waves would take more than ~2 minutes
-    t0 = time.perf_counter()
-    O.estimate_batch(kernel, gpu, shallow[:1], 1)
-    t_one = time.perf_counter() - t0
-    per_step = shallow[:max(1, min(len(shallow), threads))]
-    if args.steps * t_one * 1.5 > 120.0:
-        per_step = shallow[:1]
-    for _ in range(max(0, args.warmup - 1)):
-        O.estimate_batch(kernel, gpu, per_step[:1], 1)
+    # a step is bounded: configurations of <= 3e7 evaluations (~10 s on one thread)
+    sample = stratified_sample(plans, cfgs, max_evals=3e7, stride=2)
+    pos = 0
+
+    def take():
+        nonlocal pos
+        out = [sample[(pos + j) % len(sample)] for j in range(threads)]
+        pos += threads
+        return out
+
+    for _ in range(max(0, args.warmup)):
+        O.estimate_batch(kernel, gpu, take()[:1], 1)
     tot_dt, tot_ev, tot_n = 0.0, 0, 0
     for _ in range(args.steps):
+        batch = take()
         t0 = time.perf_counter()
-        res = O.estimate_batch(kernel, gpu, per_step, threads)
+        res = O.estimate_batch(kernel, gpu, batch, threads)
         tot_dt += time.perf_counter() - t0
         tot_ev += sum(r["addr_evals"] for r in res)
-        tot_n += len(per_step)
+        tot_n += len(batch)
     rate = tot_ev / tot_dt
     value = rate / mean_evals
     line = {
@@ -176,12 +231,17 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": len(cfgs), "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": (f"each step: {len(per_step)} shallow configs (block z=1, no fold) of the 168 on "
-                                    f"{threads} threads; throughput {rate:.3e} address evals/s scaled by the space's "
-                                    f"mean {mean_evals:.3e} evals/config")},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "estimated": True,
+                         "host": host_info(),
+                         "sample": (f"each step: {threads} configs (one per host thread) cycled from a stratified "
+                                    f"sample of {len(sample)} of the 168 (<= 3e7 evaluations each); throughput "
+                                    f"{rate:.3e} address evals/s extrapolated by the space's mean {mean_evals:.3e} "
+                                    f"evals/config")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    fs = full_space_timing()
+    if fs is not None:
+        line["cpu_baseline"]["full_space_measured"] = fs
     print(json.dumps(line), flush=True)
 
 
@@ -212,14 +272,12 @@ def run_native(args, rank, world, local):
     d_top = torch.empty(TOPK, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    from paper_2204_14242_b200 import dist as D
-    shards = [[r * n + j for j in range(n)] for r in range(world)]   # rank r: its hardware set
-
+    # rank r evaluates the space on hardware set r: the gathered buffer [r][i] is already in
+    # canonical order (equal shards), so a step is estimate -> one all-gather -> rank
     def step():
-        nonlocal gathered
         ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
         if world > 1:
-            gathered = D.gather_records(d_out.view(n, rb), shards).view(-1)
+            dist.all_gather_into_tensor(gathered, d_out)
         ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
 
     launches_per_step = None
@@ -306,6 +364,7 @@ def run_native(args, rank, world, local):
                  "source": "profiles/ncu_traffic.json (ncu --set full, smsp__inst_executed.sum)"}
                 if warp_inst and dom_ms > 0 else None)
 
+    strong = configs3_strong_measure(ctx, stream, args, rank, world, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(kernel, gpu, space, os.cpu_count() or 1)
@@ -340,10 +399,67 @@ def run_native(args, rank, world, local):
             line["cpu_baseline"] = cpu
         if nxt is not None:
             line["next_rows"] = nxt
+        line["configs3_strong"] = strong
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def configs3_strong_measure(ctx, stream, args, rank, world, dev):
+    """BJ configs[3] with a fixed total (strong scaling): the 168-config 3D-25pt 512^3 space x the
+    49 configs[3] hardware sets (workloads.hw_grid_configs3) = 8232 (configuration, hardware set)
+    estimates, sharded by configuration over the ranks (LPT on device-derived per-configuration
+    costs computed on rank 0 and broadcast), ws_estimate_multi per rank (integer stages once per
+    SM-count group, model fanned out), one all-gather, the canonical permutation, ws_rank of the
+    whole set on every rank.  Timed like the headline: barrier + synchronize around K steps,
+    CUDA events on the context stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2204_14242_b200 import config_array, dist as D
+    sets = W.hw_grid_configs3(peaks().get("hbm_gbs", 6546.2))
+    kid = ctx.describe_kernel(W.k25(512))
+    gids = [ctx.describe_gpu(g) for g in sets]
+    cf = config_array(kid, 0, W.space_stencil_paper())
+    costs = [D.device_costs(ctx, cf, gids) if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(costs, src=0)
+    sw = D.ShardedSweep(ctx, cf, gids, costs[0], device=dev)
+    for _ in range(max(3, args.warmup)):
+        sw.step()
+    torch.cuda.synchronize()
+    groups, launches = sw.est_groups, sw.est_launches
+    steps = max(20, min(args.steps, 200))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        sw.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    total = len(cf) * len(gids)
+    import numpy as np
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+    res = np.frombuffer(sw.result.cpu().numpy().tobytes(), dtype=RESULT_DTYPE)
+    assert (res["status"] == 0).all() and len(res) == total
+    loads = [sum(costs[0][i] for i in s) for s in sw.shards]
+    return {"workload": f"BJ configs[3]: 3D-25pt r4 512^3, 168 configs x {len(gids)} hardware sets (B200-like + "
+                        "hypothetical grid L1 x L2 x SM count), fixed total",
+            "value": total / (ms / 1e3), "unit": "configs/s", "metric_unit_note": "one config = one (configuration, "
+            "hardware set) estimate", "n_gpus": world, "scaling": "strong", "steps": steps, "ms_per_step": ms,
+            "integer_groups_per_rank": groups, "gpu_launches_per_step": launches + 1,
+            "shard_sizes": [len(s) for s in sw.shards],
+            "shard_cost_imbalance": max(loads) / (sum(loads) / len(loads)) if loads else None,
+            "timing": "barrier + synchronize around the K steps, CUDA events on the context stream, max over ranks; "
+                      "no L2 flush (working set of a step is re-read from HBM-resident descriptors)"}
 
 
 def next_rows_measure(ctx, stream, args, cpu_baseline):
@@ -524,9 +640,21 @@ def main():
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 3 if args.impl == "reference" else 1500
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start N ranks (one per GPU) ourselves
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: the launcher and the flag disagree")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -2943,18 +2943,33 @@ __global__ void __launch_bounds__(256) k_rank_merge(ws_result* __restrict__ res,
   const unsigned long long x = skey[q];
   const int my = q / P;
   long long r = q - (long long)my * P;             // smaller pairs in its own tile
-  for (int t = 0; t < ntiles; ++t) {
-    if (t == my) continue;
-    const unsigned long long* K = skey + (long long)t * P;
-    const uint32_t* I = sidx + (long long)t * P;
-    int lo = 0, hi = P;                            // first position whose pair is > (x, c)
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      const unsigned long long km = K[mid];
-      if (km < x || (km == x && I[mid] < c)) lo = mid + 1;
-      else hi = mid;
+  // branchless lower bounds (P a power of two) in 16 other tiles at once: each halving step issues
+  // 16 independent loads, so the latency chain is log2(P) steps per group of tiles
+  constexpr int kG = 16;
+  for (int t0 = 0; t0 < ntiles; t0 += kG) {
+    int pos[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) pos[u] = 0;
+    for (int step = P >> 1; step > 0; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int t = t0 + u;
+        if (t < ntiles && t != my) {
+          const long long o = (long long)t * P + pos[u] + step - 1;
+          const unsigned long long km = skey[o];
+          if (km < x || (km == x && sidx[o] < c)) pos[u] += step;
+        }
+      }
     }
-    r += lo;
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const int t = t0 + u;
+      if (t < ntiles && t != my) {   // pos = #pairs < (x, c) among the first P - 1; check the last
+        const long long o = (long long)t * P + P - 1;
+        const unsigned long long km = skey[o];
+        r += pos[u] + ((pos[u] == P - 1 && (km < x || (km == x && sidx[o] < c))) ? 1 : 0);
+      }
+    }
   }
   res[c].rank = (uint32_t)r;
   if (r < k && top) top[r] = c;

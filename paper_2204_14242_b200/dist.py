@@ -113,6 +113,7 @@ class ShardedSweep:
         self.result = torch.empty((self.H * self.n, RECORD_BYTES), dtype=torch.uint8, device=self.dev)
         self.top = torch.empty(max(1, k_top), dtype=torch.int32, device=self.dev)
         self.estimate = estimate
+        self.est_launches, self.est_groups = 0, 0
 
     def step(self):
         if self.n_local:
@@ -120,6 +121,8 @@ class ShardedSweep:
                 self.estimate(self.local_cfg, self.d_out[: self.H * self.n_local])
             else:
                 self.ctx.estimate_multi_async(self.d_cfg.data_ptr(), self.n_local, self.gpu_ids, self.d_out.data_ptr())
+                self.est_launches = self.ctx.last_launch_count()
+                self.est_groups = self.ctx.last_group_count()
         if self.world == 1:
             torch.index_select(self.d_out, 0, self.perm, out=self.result)
         elif self.backend == "nccl":
