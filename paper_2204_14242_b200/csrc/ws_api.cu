@@ -163,7 +163,10 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   for (int64_t v : c->chunk_bound) cb = std::max(cb, v);
   const size_t max_chunks = n * (size_t)cb;
   size_t off = 0;
-  const size_t o_pdone = off;   off = align_up(off + sizeof(unsigned int));  // fixed offset: survives re-layouts
+  // fixed offsets (survive re-layouts): plan_done, the call epoch, the a5/a6 sharing table
+  const size_t o_pdone = off;   off = align_up(off + sizeof(unsigned int));
+  const size_t o_epoch = off;   off = align_up(off + sizeof(unsigned long long));
+  const size_t o_rtab = off;    off = align_up(off + (size_t)kRowTab * 8 * sizeof(unsigned long long));
   const size_t o_plans = off;   off = align_up(off + n * sizeof(DPlan));
   const size_t o_instr = off;   off = align_up(off + n * (size_t)kMaxInstr * sizeof(DInstr));
   const size_t o_row = off;     off = align_up(off + n * (size_t)kMaxFields * sizeof(DRowInfo));
@@ -228,6 +231,8 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.slist = (unsigned long long*)(b + o_slist);
   s.dlist = (unsigned long long*)(b + o_dlist);
   s.plan_done = (unsigned int*)(b + o_pdone);
+  s.epoch = (unsigned long long*)(b + o_epoch);
+  s.rowtab = (unsigned long long*)(b + o_rtab);
   c->last_work = s.work;
   return WS_OK;
 }
@@ -250,8 +255,16 @@ ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out) {
   c->graphs = !(getenv("WS_GRAPH") && getenv("WS_GRAPH")[0] == '0');
   cudaDeviceGetAttribute(&c->n_sm_dev, cudaDevAttrMultiProcessorCount, cuda_device);
   if (c->n_sm_dev <= 0) c->n_sm_dev = 148;
-  if (cudaStreamCreateWithFlags(&c->aux[0], cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->aux[1], cudaStreamNonBlocking) != cudaSuccess ||
+  // stream priorities: the row chain (k_rows -> k_fold, the critical path) gets the highest, so
+  // its CTAs are scheduled first whenever the concurrent chains compete for SM slots
+  // (WS_PRIO=0 disables, diagnostics / A/B)
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  static const int prio_mode = getenv("WS_PRIO") ? atoi(getenv("WS_PRIO")) : 0;
+  const int p_rows = prio_mode >= 1 ? prio_hi : prio_lo;
+  const int p_set = prio_mode >= 2 ? (prio_hi + prio_lo) / 2 : prio_lo;
+  if (cudaStreamCreateWithPriority(&c->aux[0], cudaStreamNonBlocking, p_set) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->aux[1], cudaStreamNonBlocking, p_rows) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->join[0], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->join[1], cudaEventDisableTiming) != cudaSuccess ||

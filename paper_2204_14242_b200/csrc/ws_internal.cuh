@@ -112,7 +112,17 @@ struct DPlan {
   int32_t want_pages, want_sect; // k_sect: TLB pages / L2-section footprints wanted
   int64_t n_sect_items;          // k_sect work items (fields) of this config
   int64_t rep_B, rep_mult;       // WS_VAR_REP_BLOCK: the representative block and W (0 = off)
+  // a5/a6 sharing: configurations with identical wave / layer-set footprints (same kernel, sector
+  // and line geometry, block footprint BF, W, s, L_y, L_z, address space) have identical row-scope
+  // counts; the first to claim the key in the row table computes them, the others (row_owner !=
+  // own index) have no k_rows / k_fold work and k_model reads the owner's accumulators
+  int32_t row_owner, row_slot, pad4, pad5;
 };
+// row-sharing table (fixed offset in the scratch, survives re-layouts): entries of 8 u64 =
+// state ((epoch << 32) | ready bit 31 | busy bit 30 | owner) + 6 key words; epoch = call counter,
+// entries of other calls count as empty
+constexpr int kRowTab = 4096;
+constexpr int kRowTabProbe = 64;
 
 // per-config accumulator slots (u64, atomically added by the worker kernels)
 enum {
@@ -159,6 +169,8 @@ struct Scratch {
   unsigned long long* slist;  // n * kSSlots entries
   unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm entries
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
+  unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)
+  unsigned long long* rowtab; // kRowTab x 8 u64: a5/a6 sharing keys (see DPlan::row_owner)
 };
 
 // kernel kinds, in launch order (ws_kernel_name)

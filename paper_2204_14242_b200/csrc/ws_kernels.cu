@@ -462,6 +462,52 @@ __device__ void plan_boundaries(DPlan& P) {
   }
 }
 
+// a5/a6 sharing (DPlan::row_owner): claim this configuration's row-scope key in the row table, or
+// find the configuration of this call that claimed it first.  The row-scope counts depend only on
+// the kernel, the sector / line geometry, the address space, BF (with the domain: G, the block-row
+// map), W, s and the look-back starts (the five k_rows ranges).  One thread per configuration.
+__device__ void row_claim(DPlan& P, int c, const DGpu& G, unsigned long long cur_epoch,
+                          unsigned long long* __restrict__ tab) {
+  P.row_owner = c;
+  P.row_slot = -1;
+  unsigned long long key[6] = {
+      (unsigned long long)P.kid | ((unsigned long long)G.lg_sector << 32) | ((unsigned long long)G.lg_line << 40) |
+          ((unsigned long long)P.mdim << 48),
+      (unsigned long long)P.BF[0] | ((unsigned long long)P.BF[1] << 21) | ((unsigned long long)P.BF[2] << 42),
+      (unsigned long long)P.W, (unsigned long long)P.s, (unsigned long long)P.Ly0, (unsigned long long)P.Lz0};
+  unsigned long long h = 0x9e3779b97f4a7c15ull;
+  for (int i = 0; i < 6; ++i) h = (h ^ key[i]) * 0xff51afd7ed558ccdull, h ^= h >> 29;
+  const unsigned long long ep = cur_epoch << 32;
+  const unsigned long long READY = 1ull << 31, BUSY = 1ull << 30, OWNER = (1ull << 30) - 1ull;
+  for (int probe = 0; probe < kRowTabProbe; ++probe) {
+    unsigned long long* e = tab + ((h + probe) & (kRowTab - 1)) * 8;
+    unsigned long long st = *(volatile unsigned long long*)e;
+    if ((st >> 32) != cur_epoch) {  // empty for this call: try to claim it
+      const unsigned long long old = atomicCAS(e, st, ep | BUSY);
+      if (old == st) {
+        for (int i = 0; i < 6; ++i) e[1 + i] = key[i];
+        __threadfence();
+        atomicExch(e, ep | READY | (unsigned long long)c);
+        P.row_slot = (int)((h + probe) & (kRowTab - 1));
+        return;
+      }
+      st = old;
+      if ((st >> 32) != cur_epoch) {  // lost to a claimant of another epoch?  cannot happen; retry slot
+        --probe;
+        continue;
+      }
+    }
+    while (!(st & READY)) st = *(volatile unsigned long long*)e;  // being written by its claimant
+    __threadfence();
+    bool eq = true;
+    for (int i = 0; i < 6; ++i) eq = eq && ((volatile unsigned long long*)e)[1 + i] == key[i];
+    if (eq) {
+      P.row_owner = (int)(st & OWNER);
+      return;
+    }
+  }
+}
+
 __device__ __forceinline__ void decode_kappa(int q, const int* f, int& kx, int& ky, int& kz) {
   kx = q % f[0];
   ky = (q / f[0]) % f[1];
@@ -549,9 +595,11 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
                                               unsigned long long* __restrict__ work,
                                               unsigned long long* __restrict__ lists,
                                               unsigned long long* __restrict__ skey, unsigned int* __restrict__ sdone,
-                                              int max_fields) {
+                                              int max_fields, unsigned long long* __restrict__ epoch,
+                                              unsigned long long* __restrict__ rowtab) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
+  const unsigned long long cur_epoch = *(volatile unsigned long long*)epoch + 1ull;  // this call
 #ifdef WS_PLAN_CLOCK
   long long clk[12];
   int nclk = 0;
@@ -627,7 +675,10 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     if (s_last) {
       __threadfence();
       scan_body(plans, n, pre, work, lists);
-      if (tid == 0) *plan_done = 0u;  // reset for the next call (graph replay)
+      if (tid == 0) {
+        *plan_done = 0u;  // reset for the next call (graph replay)
+        *epoch = cur_epoch;  // every CTA of this call has read the epoch: the next call's is new
+      }
     }
   };
   if (P.status != WS_OK) {
@@ -637,7 +688,11 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   PLAN_MARK()
   if (tid < 5) plan_range(P, tid);
   __syncthreads();
-  if (tid == 0) plan_boundaries(P);
+  if (tid == 0) {
+    plan_boundaries(P);
+    row_claim(P, c, sG, cur_epoch, rowtab);
+  }
+  __syncthreads();
   PLAN_MARK()
   const DKernel& K = sK;
   const int fc = P.fcube;
@@ -756,7 +811,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     ri.nz = z1 > z0 ? z1 - z0 : 0;
     if (F.g_end == F.g_begin) ri.ny = ri.nz = 0;
     ri.ppc = 1;
-    ri.n_chunks = ri.ny > 0 ? ri.nz : 0;
+    ri.n_chunks = (ri.ny > 0 && P.row_owner == c) ? ri.nz : 0;   // sharers: the owner's rows
     ri.pad = 0;
     ri.chunk_begin = 0;
     rowinfo[(long long)c * kMaxFields + fi] = ri;
@@ -775,7 +830,7 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     P.n_set_items = P.rep_mult ? 1 : P.nsets;
     P.n_sclass_items = 0;
     P.n_chunks = cb;
-    P.n_fields = K.n_fields;
+    P.n_fields = P.row_owner == c ? K.n_fields : 0;   // k_fold items
     P.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
     P.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
   }
@@ -2784,6 +2839,14 @@ __device__ __noinline__ void model_one(const DPlan& P, const DKernel* __restrict
   R.t_pred = tm * K.cells;
 }
 
+// a5/a6 sharing: a configuration whose row scope another one computed (DPlan::row_owner) takes
+// the owner's wave / layer-set counts (the plan is already in shared memory; lanes A_WLD..A_OVZ)
+__device__ __forceinline__ void shared_row_counts(const DPlan& P, long long c, const unsigned long long* __restrict__ acc,
+                                                  unsigned long long* a, int lane) {
+  if (P.status == WS_OK && P.row_owner != c && lane >= A_WLD && lane <= A_OVZ)
+    a[lane] = acc[(long long)P.row_owner * A_N + lane];
+}
+
 // one warp per configuration: the accumulators in by the lanes, the model by lane 0, the
 // 336-byte record out by the lanes (coalesced)
 __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, int n, const DKernel* __restrict__ ks,
@@ -2810,6 +2873,7 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
     uint4* dg = reinterpret_cast<uint4*>(&s_gp[w]);
     for (int i = lane; i < (int)(sizeof(DGpu) / 16); i += 32) dg[i] = sg[i];
   }
+  shared_row_counts(s_p[w], c, acc, s_a[w], lane);
   __syncwarp();
   if (lane == 0) model_one(s_p[w], ks, s_gp[w], s_a[w], s_r[w]);
   __syncwarp();
@@ -2855,6 +2919,8 @@ __global__ void __launch_bounds__(128) k_model_fan(const DPlan* __restrict__ pla
     for (int i = lane; i < (int)(sizeof(DGpu) / 16); i += 32) dg[i] = sg[i];
   }
   __syncwarp();
+  shared_row_counts(s_p[w], c, acc, s_a[w], lane);
+  __syncwarp();
   if (lane == 0) model_one(s_p[w], ks, s_gp[w], s_a[w], s_r[w]);
   __syncwarp();
   const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s_r[w]);
@@ -2873,13 +2939,14 @@ int launch_expand(const ws_config* d_cfgs, const FanOut& f, ws_config* xcfg, cud
 // a sort of 64-bit order-preserving keys (IEEE bits with the sign folded; failed = +inf) carrying
 // the configuration index; (key, index) pairs are unique, so every comparison is strict.
 //   n <= kRankSmem: one CTA, bitonic sort in shared memory, ranks written directly;
-//   n <= kRankMerge: tiles of kRankTile sorted the same way by one CTA each, then every element's
+//   n <= kRankMerge: tiles of 2048 (n <= 2^15) or 4096 sorted the same way by one CTA each, then every element's
 //     rank = its position in its tile + the number of smaller pairs in every other tile (binary
 //     searches of the sorted tiles);
 //   larger n: a stable LSD radix sort, 8 passes of 8 bits (tile histogram -> one-CTA scan -> stable
 //     tile scatter), whose stability over the index-ordered input gives the index tie-break.
-constexpr int kRankSmem = 16384;
-constexpr int kRankTile = 4096;
+constexpr int kRankSmem = 2048;    // one CTA (1024 threads, one pair per thread per stage)
+constexpr int kRankTile = 4096;    // tile of the merge path (2048 below kRankSmall)
+constexpr int kRankSmall = 1 << 15;
 constexpr int kRankMerge = 1 << 18;
 constexpr int kRkTile = 2048;
 __device__ __forceinline__ unsigned long long rank_key(const ws_result& r) {
@@ -2943,9 +3010,11 @@ __global__ void __launch_bounds__(256) k_rank_merge(ws_result* __restrict__ res,
   const unsigned long long x = skey[q];
   const int my = q / P;
   long long r = q - (long long)my * P;             // smaller pairs in its own tile
-  // branchless lower bounds (P a power of two) in 16 other tiles at once: each halving step issues
-  // 16 independent loads, so the latency chain is log2(P) steps per group of tiles
-  constexpr int kG = 16;
+  // branchless lower bounds of the key alone (P a power of two) in 8 other tiles at once: each
+  // halving step issues 8 independent loads, so the latency chain is log2(P) steps per group of
+  // tiles.  Pairs of another tile smaller than (x, c): keys < x, plus keys == x with index < c
+  // (rare: a walk over the equal keys, which the tile holds in index order).
+  constexpr int kG = 8;
   for (int t0 = 0; t0 < ntiles; t0 += kG) {
     int pos[kG];
 #pragma unroll
@@ -2954,20 +3023,18 @@ __global__ void __launch_bounds__(256) k_rank_merge(ws_result* __restrict__ res,
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         const int t = t0 + u;
-        if (t < ntiles && t != my) {
-          const long long o = (long long)t * P + pos[u] + step - 1;
-          const unsigned long long km = skey[o];
-          if (km < x || (km == x && sidx[o] < c)) pos[u] += step;
-        }
+        if (t < ntiles && t != my && skey[(long long)t * P + pos[u] + step - 1] < x) pos[u] += step;
       }
     }
 #pragma unroll
     for (int u = 0; u < kG; ++u) {
       const int t = t0 + u;
-      if (t < ntiles && t != my) {   // pos = #pairs < (x, c) among the first P - 1; check the last
-        const long long o = (long long)t * P + P - 1;
-        const unsigned long long km = skey[o];
-        r += pos[u] + ((pos[u] == P - 1 && (km < x || (km == x && sidx[o] < c))) ? 1 : 0);
+      if (t < ntiles && t != my) {   // pos = #keys < x among the first P - 1
+        const unsigned long long* K = skey + (long long)t * P;
+        int p = pos[u];
+        if (p == P - 1 && K[p] < x) ++p;
+        while (p < P && K[p] == x && sidx[(long long)t * P + p] < c) ++p;
+        r += p;
       }
     }
   }
@@ -3111,7 +3178,8 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
   beg(K_PLAN, m);
   k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
-                           s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields);  // its last CTA scans
+                           s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields, s.epoch,
+                           s.rowtab);  // its last CTA scans
   end(K_PLAN, m);
   // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on main
   cudaEventRecord(st.fork, m);
@@ -3167,7 +3235,7 @@ int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, void* scratch, 
   uint32_t L = 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_rank_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmem * 12);
+    cudaFuncSetAttribute(k_rank_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankTile * 12);
     attr = true;
   }
   if (n <= kRankSmem) {
@@ -3176,11 +3244,12 @@ int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, void* scratch, 
     k_rank_smem<<<1, P / 2 < 1024 ? P / 2 : 1024, (size_t)P * 12, st>>>(d_res, n, P, k, d_top, nullptr, nullptr);
     L = 1;
   } else if (n <= kRankMerge) {
-    const int nt = (n + kRankTile - 1) / kRankTile;
+    const int P = n <= kRankSmall ? 2048 : kRankTile;
+    const int nt = (n + P - 1) / P;
     unsigned long long* skey = (unsigned long long*)scratch;
-    uint32_t* sidx = (uint32_t*)(skey + (size_t)nt * kRankTile);
-    k_rank_smem<<<nt, 1024, (size_t)kRankTile * 12, st>>>(d_res, n, kRankTile, k, d_top, skey, sidx);
-    k_rank_merge<<<(nt * kRankTile + 255) / 256, 256, 0, st>>>(d_res, n, kRankTile, nt, k, d_top, skey, sidx);
+    uint32_t* sidx = (uint32_t*)(skey + (size_t)nt * P);
+    k_rank_smem<<<nt, 1024, (size_t)P * 12, st>>>(d_res, n, P, k, d_top, skey, sidx);
+    k_rank_merge<<<(nt * P + 255) / 256, 256, 0, st>>>(d_res, n, P, nt, k, d_top, skey, sidx);
     L = 2;
   } else {
     const int nt = (n + kRkTile - 1) / kRkTile;

@@ -45,7 +45,7 @@ def _expected_order(r):
     return np.lexsort((np.arange(len(r)), key))
 
 
-@pytest.mark.parametrize("n", [1, 2, 168, 5000, 16384, 16385, 100000, 300001])
+@pytest.mark.parametrize("n", [1, 2, 168, 2048, 2049, 5000, 8232, 32768, 32769, 100000, 262144, 300001])
 def test_rank_sort_paths(ctx, n):
     r = _synthetic_results(n, n)
     top = ctx.rank(r, 10)
