@@ -2220,6 +2220,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
   int c = -1;
   int rra[5] = {0, 0, 0, 0, 0}, rrl[5] = {0, 0, 0, 0, 0};
   for (long long item = (long long)blockIdx.x * kRowWarps + wid; item < total; item += nwg) {
+#ifdef WS_ROWS_TRACE
+    const long long t_item0 = clock64();
+    int tr_runs = 0;
+#endif
     c = find_config_warp<4>(pre, n, item, c);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
@@ -2334,6 +2338,9 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
         if (lane >= o) pos += v;
       }
       const int nruns = __shfl_sync(FULL, pos, 31);
+#ifdef WS_ROWS_TRACE
+      tr_runs += nruns;
+#endif
       pos -= cnt;
       for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
         unsigned bits = X.bm[w];
@@ -2411,6 +2418,11 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
         out[q * 3 + 2] = v.c;
       }
     }
+#ifdef WS_ROWS_TRACE  // diagnostics build: the slow computed planes
+    if (lane == 0 && clock64() - t_item0 > WS_ROWS_TRACE)
+      printf("ROWITEM c=%d b=(%d,%d,%d) f=(%d,%d,%d) field=%d z=%d ny=%d runs=%d groups=%d cycles=%lld\n", c, P.b[0],
+             P.b[1], P.b[2], P.f[0], P.f[1], P.f[2], fi, z, ny, tr_runs, ng, clock64() - t_item0);
+#endif
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) my_ops += __shfl_down_sync(FULL, my_ops, o);
