@@ -191,6 +191,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   size_t max_nsm = 1;
   for (const DGpu& g : c->hg) max_nsm = std::max<size_t>(max_nsm, g.g.n_sm);
   const size_t o_dlist = off;   off = align_up(off + n * max_nsm * sizeof(unsigned long long));
+  const size_t o_clist = off;   off = align_up(off + max_chunks * sizeof(uint32_t));  // k_rows items per config
   if (bytes_only) {
     *bytes_only = off;
     return WS_OK;
@@ -231,6 +232,8 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.slist = (unsigned long long*)(b + o_slist);
   s.dlist = (unsigned long long*)(b + o_dlist);
   s.plan_done = (unsigned int*)(b + o_pdone);
+  s.clist = (uint32_t*)(b + o_clist);
+  s.clist_stride = (int64_t)cb;
   s.epoch = (unsigned long long*)(b + o_epoch);
   s.rowtab = (unsigned long long*)(b + o_rtab);
   c->last_work = s.work;
@@ -484,7 +487,8 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
       G.run_lo[q] = runs[q].first;
       G.run_hi[q] = runs[q].second;
     }
-    if (G.g_end > G.g_begin) chunks += G.ext[2];  // k_rows chunks are >= 1 z-plane each
+    // k_rows chunks: (z-plane, segment of kRowSeg rows) of the field's row box
+    if (G.g_end > G.g_begin) chunks += G.ext[2] * ((G.ext[1] + kRowSeg - 1) / kRowSeg);
   }
   D.n_groups = ng;
   {

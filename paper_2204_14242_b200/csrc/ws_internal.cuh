@@ -70,8 +70,15 @@ struct DInstr {
 // Row box (field-index rows (y,z), z-major) of the wave + layer-set footprint of one field.
 // A chunk is `ppc` consecutive z-planes of the box (k_rows: one warp per chunk).
 struct DRowInfo {
-  int64_t y0, ny, z0, nz, chunk_begin, n_chunks, ppc, pad;
+  int64_t y0, ny, z0, nz, chunk_begin, n_chunks, ppc, nseg;  // nseg: row segments per plane
 };
+// k_rows chunk = (plane, segment of kRowSeg rows).  A/B on B200 (configs[1], k_rows serial): 1024
+// rows (one segment for every plane of the paper's grids) 78 us, 256: 117 us, 128: 176 us, 64:
+// 286 us -- more, smaller items cost more per-item overhead than the runs they spread
+#ifndef WS_ROW_SEG
+#define WS_ROW_SEG 1024
+#endif
+constexpr int kRowSeg = WS_ROW_SEG;
 constexpr int kPlaneRows = 8192;   // target rows per k_rows chunk
 
 // One contiguous block-id range [a, b) seen per block row: first / last block row touched and the
@@ -117,6 +124,9 @@ struct DPlan {
   // counts; the first to claim the key in the row table computes them, the others (row_owner !=
   // own index) have no k_rows / k_fold work and k_model reads the owner's accumulators
   int32_t row_owner, row_slot, pad4, pad5;
+  // k_rows items: the chunks of computed planes only (derived planes -- translates of their zone
+  // segment's representative by whole lines -- are folded by k_fold from the representative)
+  int64_t n_ritems, pad6;
 };
 // row-sharing table (fixed offset in the scratch, survives re-layouts): entries of 8 u64 =
 // state ((epoch << 32) | ready bit 31 | busy bit 30 | owner) + 6 key words; epoch = call counter,
@@ -133,9 +143,9 @@ enum {
 };
 
 struct DPrefix {
-  int64_t warp, wclass, set, sclass, chunk, fold, sect;
+  int64_t warp, wclass, set, sclass, chunk, fold, sect, ritem;  // ritem: k_rows items (computed chunks)
 };
-constexpr int kNPrefix = 7;
+constexpr int kNPrefix = 8;
 constexpr int kWSlots = 32 * 64 * 8;  // per config: warp index (<32) x residue (<64) x clip pattern (<8)
 constexpr int kSSlots = 64 * 8;       // per config: residue (<64) x clip pattern (<8)
 constexpr int kShareTab = 8192;       // SM-set classes shared across configurations (k_smset)
@@ -171,6 +181,8 @@ struct Scratch {
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
   unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)
   unsigned long long* rowtab; // kRowTab x 8 u64: a5/a6 sharing keys (see DPlan::row_owner)
+  uint32_t* clist;            // per config (stride clist_stride): its computed chunks (k_rows items)
+  int64_t clist_stride;
 };
 
 // kernel kinds, in launch order (ws_kernel_name)

@@ -105,6 +105,46 @@ __device__ __forceinline__ int plane_period(long long pz, int le, int ll) {
   return need <= 4 ? (1 << need) : 0;
 }
 
+// Row layout of field F seen by the wave / layer-set scopes: the field's own (linear address
+// space), or under WS_VAR_MDIM the multidimensional address space (P:551-569) realised as a
+// virtual layout whose rows start on a line boundary and are padded to whole lines, with no
+// alignment: (z, y, floor(x * elem / sector)) tuples never share a sector or line across
+// rows, exactly the paper's "two multi dimensional addresses are distinct when their tuples
+// differ"; floor(x * elem / sector) is unchanged by a line-aligned row start.
+__device__ __forceinline__ void field_rows(const DField& F, const DPlan& P, int ll, long long& py, long long& pz,
+                                           long long& align) {
+  if (!P.mdim) {
+    py = F.pitch[1];
+    pz = F.pitch[2];
+    align = F.align;
+    return;
+  }
+  const long long rowb = (((F.ext[0] << F.lg_elem) + (1ll << ll) - 1) >> ll) << ll;
+  py = rowb >> F.lg_elem;
+  pz = py * F.ext[1];
+  align = 0;
+}
+
+// Plane derivation (k_plan, k_fold): a plane whose every offset group of the field falls in the
+// same block layer (or the same side outside the domain) as in the plane `per` before it has the
+// same row structure, translated by whole lines.  Returns the plane's representative: the start
+// of its zone segment (the largest zone start over the groups, at least the box start z0) plus
+// (z - start) mod per; the plane itself when per == 0 (no period within 16 planes).
+__device__ __forceinline__ int plane_rep(const DGroup* g, int ng, int z, int z0, int lo2, int hi2, int BF2, FDiv fdz,
+                                         int per) {
+  if (per <= 0) return z;
+  int seg = z0;
+  for (int i = 0; i < ng; ++i) {
+    const int oz = g[i].oz, zz = z - oz;
+    int st;
+    if (zz < lo2) st = -0x7fffffff;
+    else if (zz >= hi2) st = hi2 + oz;
+    else st = lo2 + (int)fdiv(zz - lo2, fdz) * BF2 + oz;
+    seg = st > seg ? st : seg;
+  }
+  return seg + ((z - seg) % per);
+}
+
 struct Tri {
   long long f, l, c;  // first, last, count; c == 0: empty
 };
@@ -254,7 +294,8 @@ __device__ __forceinline__ int find_config(const DPrefix* pre, int n, long long 
                         : MEMBER == 3 ? pre[mid].sclass
                         : MEMBER == 4 ? pre[mid].chunk
                         : MEMBER == 5 ? pre[mid].fold
-                                      : pre[mid].sect;
+                        : MEMBER == 6 ? pre[mid].sect
+                                      : pre[mid].ritem;
     if (v <= item) lo = mid;
     else hi = mid - 1;
   }
@@ -269,7 +310,8 @@ __device__ __forceinline__ long long prefix_member(const DPrefix& p) {
          : MEMBER == 3 ? p.sclass
          : MEMBER == 4 ? p.chunk
          : MEMBER == 5 ? p.fold
-                       : p.sect;
+         : MEMBER == 6 ? p.sect
+                       : p.ritem;
 }
 
 // find_config by the whole warp (item warp-uniform): 32-ary search, one load round per
@@ -522,7 +564,8 @@ __device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
     case 3: return P.n_sclass_items;
     case 4: return P.n_chunks;
     case 5: return P.n_fields;
-    default: return P.n_sect_items;
+    case 6: return P.n_sect_items;
+    default: return P.n_ritems;
   }
 }
 
@@ -576,13 +619,13 @@ __device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __res
 #pragma unroll
   for (int j = 0; j < kNPrefix; ++j) r[j] = s_w[wid][j] + inc[j] - a[j];
   for (int c = tid * seg; c < n && c < (tid + 1) * seg; ++c) {
-    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
+    pre[c] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
     const DPlan& P = plans[c];
     if (P.status != WS_OK) continue;
 #pragma unroll
     for (int j = 0; j < kNPrefix; ++j) r[j] += plan_count(P, j);
   }
-  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6]};
+  if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
 }
 
 
@@ -596,7 +639,8 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
                                               unsigned long long* __restrict__ lists,
                                               unsigned long long* __restrict__ skey, unsigned int* __restrict__ sdone,
                                               int max_fields, unsigned long long* __restrict__ epoch,
-                                              unsigned long long* __restrict__ rowtab) {
+                                              unsigned long long* __restrict__ rowtab, uint32_t* __restrict__ clist,
+                                              long long clist_stride) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
   const unsigned long long cur_epoch = *(volatile unsigned long long*)epoch + 1ull;  // this call
@@ -811,8 +855,8 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     ri.nz = z1 > z0 ? z1 - z0 : 0;
     if (F.g_end == F.g_begin) ri.ny = ri.nz = 0;
     ri.ppc = 1;
-    ri.n_chunks = (ri.ny > 0 && P.row_owner == c) ? ri.nz : 0;   // sharers: the owner's rows
-    ri.pad = 0;
+    ri.nseg = ri.ny > 0 ? (ri.ny + kRowSeg - 1) / kRowSeg : 1;
+    ri.n_chunks = (ri.ny > 0 && P.row_owner == c) ? ri.nz * ri.nseg : 0;   // sharers: the owner's rows
     ri.chunk_begin = 0;
     rowinfo[(long long)c * kMaxFields + fi] = ri;
   }
@@ -835,6 +879,34 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     P.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
   }
   __syncthreads();
+  // k_rows items: the chunks of computed planes (plane_rep(z) == z), listed per configuration;
+  // derived planes are folded from their representative by k_fold (same rule)
+  {
+    __shared__ int s_nri;
+    if (tid == 0) s_nri = 0;
+    __syncthreads();
+    const int ll = sG.lg_line;
+    uint32_t* cl = clist + (long long)c * clist_stride;
+    for (int fi = 0; fi < K.n_fields; ++fi) {
+      const DRowInfo ri = rowinfo[(long long)c * kMaxFields + fi];
+      if (ri.n_chunks == 0) continue;
+      const DField& F = K.f[fi];
+      long long py, pz, falign;
+      field_rows(F, P, ll, py, pz, falign);
+      const int per = plane_period(pz, F.lg_elem, ll);
+      for (int zi = tid; zi < (int)ri.nz; zi += blockDim.x) {
+        const int z = (int)ri.z0 + zi;
+        if (plane_rep(K.g + F.g_begin, F.g_end - F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
+                      P.fd_BF[2], per) != z)
+          continue;
+        const int at = atomicAdd(&s_nri, (int)ri.nseg);
+        for (int sg = 0; sg < (int)ri.nseg; ++sg) cl[at + sg] = (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) P.n_ritems = s_nri;
+    __syncthreads();
+  }
   PLAN_MARK()
   store_plan();
   PLAN_MARK()
@@ -2006,26 +2078,6 @@ __global__ void __launch_bounds__(256) k_sshare(const unsigned long long* __rest
   }
 }
 
-// Row layout of field F seen by the wave / layer-set scopes: the field's own (linear address
-// space), or under WS_VAR_MDIM the multidimensional address space (P:551-569) realised as a
-// virtual layout whose rows start on a line boundary and are padded to whole lines, with no
-// alignment: (z, y, floor(x * elem / sector)) tuples never share a sector or line across
-// rows, exactly the paper's "two multi dimensional addresses are distinct when their tuples
-// differ"; floor(x * elem / sector) is unchanged by a line-aligned row start.
-__device__ __forceinline__ void field_rows(const DField& F, const DPlan& P, int ll, long long& py, long long& pz,
-                                           long long& align) {
-  if (!P.mdim) {
-    py = F.pitch[1];
-    pz = F.pitch[2];
-    align = F.align;
-    return;
-  }
-  const long long rowb = (((F.ext[0] << F.lg_elem) + (1ll << ll) - 1) >> ll) << ll;
-  py = rowb >> F.lg_elem;
-  pz = py * F.ext[1];
-  align = 0;
-}
-
 // ------------------------------------------------------------------ a5 + a6: wave and layer sets
 // ranges: 0 = wave [s, s+W), 1 = L_y [Ly0, s), 2 = L_z [Lz0, s), 3 = L_y + wave, 4 = L_z + wave
 
@@ -2198,7 +2250,7 @@ __device__ unsigned long long g_rowtrace[kRowTrace][2];
 // diagnostics build: print the computed planes of the last k_rows launch, slowest first is left to
 // the reader (one line per computed plane with cycles > WS_ROWS_TRACE)
 __global__ void k_rowtrace_dump(const DPrefix* __restrict__ pre, int n) {
-  const long long total = pre[n].chunk < kRowTrace ? pre[n].chunk : kRowTrace;
+  const long long total = pre[n].ritem < kRowTrace ? pre[n].ritem : kRowTrace;
   for (long long i = 0; i < total; ++i) {
     const unsigned long long a = g_rowtrace[i][0], b = g_rowtrace[i][1];
     if ((b & 0xffffffffffull) > WS_ROWS_TRACE)
@@ -2226,11 +2278,12 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
                                                             const DGpu* __restrict__ gs,
                                                             const DRowInfo* __restrict__ rowinfo,
                                                             long long* __restrict__ chunkres,
-                                                            unsigned long long* __restrict__ work) {
+                                                            unsigned long long* __restrict__ work,
+                                                            const uint32_t* __restrict__ clist, long long clist_stride) {
   __shared__ WarpRowCtx s_ctx[kRowWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRowCtx& X = s_ctx[wid];
-  const long long total = pre[n].chunk;
+  const long long total = pre[n].ritem;   // computed chunks only (k_plan's per-config lists)
   const long long nwg = (long long)gridDim.x * kRowWarps;
   unsigned long long my_ops = 0;
   int ranges_c = -1;
@@ -2248,11 +2301,11 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const long long t_item0 = clock64();
     int tr_runs = 0;
 #endif
-    c = find_config_warp<4>(pre, n, item, c);
+    c = find_config_warp<7>(pre, n, item, c);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
-    const long long ci = item - pre[c].chunk;
+    const long long ci = clist[(long long)c * clist_stride + (item - pre[c].ritem)];
     // the field whose chunk range holds ci: chunk_begin ascends with the field index (fields
     // without chunks repeat their successor's begin), so the last field with begin <= ci and a
     // nonempty range -- binary search for the last begin <= ci, then skip empty ranges backwards
@@ -2273,30 +2326,15 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
     const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
     const int lo1 = (int)P.lo[1], hi1 = (int)P.hi[1], lo2 = (int)P.lo[2], hi2 = (int)P.hi[2];
-    const int Gy = (int)P.G[1], BF1 = (int)P.BF[1], BF2 = (int)P.BF[2];
+    const int Gy = (int)P.G[1], BF1 = (int)P.BF[1];
     const FDiv fdy = P.fd_BF[1], fdz = P.fd_BF[2];
     const int y0 = (int)RI.y0, ny = (int)RI.ny;
-    const int z = (int)(RI.z0 + (ci - RI.chunk_begin));  // one plane per chunk (ppc == 1)
+    // chunk = (plane, row segment of kRowSeg rows): a plane's runs spread over several warps
+    const int nsg = (int)RI.nseg, pci = (int)(ci - RI.chunk_begin);
+    const int z = (int)RI.z0 + pci / nsg, sg = pci % nsg;
+    const int ys0 = y0 + sg * kRowSeg, ys1 = ys0 + kRowSeg < y0 + ny ? ys0 + kRowSeg : y0 + ny;
     long long py, pz, falign;
     field_rows(F, P, ll, py, pz, falign);
-    const int per = plane_period(pz, le, ll);
-    if (per > 0) {
-      int seg = (int)RI.z0;
-      for (int g = lane; g < ng; g += 32) {
-        const int oz = K.g[g0 + g].oz, zz = z - oz;
-        int st;
-        if (zz < lo2) st = -0x7fffffff;
-        else if (zz >= hi2) st = hi2 + oz;
-        else st = lo2 + fdiv32(zz - lo2, fdz) * BF2 + oz;
-        seg = st > seg ? st : seg;
-      }
-      seg = __reduce_max_sync(FULL, seg);
-      const int rep = seg + ((z - seg) % per);
-      if (rep != z) {
-        if (lane == 0) chunkres[(pre[c].chunk + ci) * (kNQ * 3) + 2] = -(long long)(rep - RI.z0) - 2;
-        continue;
-      }
-    }
     if (ranges_c != c) {  // ranges and zone boundaries of this config (k_plan) -> warp smem, 32-bit
       __syncwarp();
       if (lane < 5) {
@@ -2327,8 +2365,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const int off0 = (int)(R0p - Bp);
     const int pystep = (int)(py << le);
     if (lane < kNQ) X.pt[lane] = t32_empty();
-    for (int ys = y0; ys < y0 + ny; ys += kSegRows) {
-      const int nseg = y0 + ny - ys < kSegRows ? y0 + ny - ys : kSegRows;
+    for (int ys = ys0; ys < ys1; ys += kSegRows) {
+      const int nseg = ys1 - ys < kSegRows ? ys1 - ys : kSegRows;
       const int nwd = (nseg + 31) >> 5;
       for (int w = lane; w < nwd; w += 32) X.bm[w] = 0u;
       __syncwarp();
@@ -2478,12 +2516,16 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restr
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
+    const DGroup* gk = ks[P.kid].g + F.g_begin;
+    const int ngk = F.g_end - F.g_begin, per = plane_period(pz, F.lg_elem, ll);
     for (long long k = tid * per_l; k < nch && k < (tid + 1) * per_l; ++k) {
-      long long src = k;
-      const long long mk = base[k * (kNQ * 3) + 2];
-      if (mk < 0) src = -mk - 2;
+      // derived plane: its representative's triple, translated (plane_rep, as in k_plan)
+      const long long pi = k / RI.nseg;
+      const int zr = plane_rep(gk, ngk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
+                               P.fd_BF[2], per);
+      const long long src = (zr - RI.z0) * RI.nseg + (k - pi * RI.nseg);
       const long long* in = base + src * (kNQ * 3);
-      const long long dbytes = (k - src) * pbytes;
+      const long long dbytes = ((k - src) / RI.nseg) * pbytes;   // same row segment, whole planes apart
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) {
         const long long d = dbytes >> ((q == 2 || q == 4 || q == 6) ? ll : ls);
@@ -2542,12 +2584,15 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
+    const DGroup* gk = ks[P.kid].g + F.g_begin;
+    const int ngk = F.g_end - F.g_begin, per = plane_period(pz, F.lg_elem, ll);
     for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
-      long long src = k;
-      const long long mk = base[k * (kNQ * 3) + 2];
-      if (mk < 0) src = -mk - 2;  // derived plane: representative plane index
+      const long long pi = k / RI.nseg;   // derived plane: its representative's triple, translated
+      const int zr = plane_rep(gk, ngk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
+                               P.fd_BF[2], per);
+      const long long src = (zr - RI.z0) * RI.nseg + (k - pi * RI.nseg);
       const long long* in = base + src * (kNQ * 3);
-      const long long dbytes = (k - src) * pbytes;
+      const long long dbytes = ((k - src) / RI.nseg) * pbytes;   // same row segment, whole planes apart
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) {
         const long long d = dbytes >> ((q == 2 || q == 4 || q == 6) ? ll : ls);
@@ -3216,14 +3261,15 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   beg(K_PLAN, m);
   k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
                            s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields, s.epoch,
-                           s.rowtab);  // its last CTA scans
+                           s.rowtab, s.clist, s.clist_stride);  // its last CTA scans
   end(K_PLAN, m);
   // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on main
   cudaEventRecord(st.fork, m);
   cudaStreamWaitEvent(a, st.fork, 0);
   cudaStreamWaitEvent(b, st.fork, 0);
   beg(K_ROWS, b);
-  k_rows<<<n_sm_dev * WS_PERSIST_ROWS, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work);
+  k_rows<<<n_sm_dev * WS_PERSIST_ROWS, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work,
+                                                             s.clist, s.clist_stride);
   end(K_ROWS, b);
 #ifdef WS_ROWS_TRACE
   k_rowtrace_dump<<<1, 1, 0, b>>>(s.prefix, n);
