@@ -323,7 +323,7 @@ ws_status ws_set_stream(ws_ctx* c, void* s) {
 
 uint32_t ws_last_launch_count(const ws_ctx* c) { return c ? c->last_launches : 0; }
 
-static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_scan",  "k_warp",  "k_wclass", "k_smset",
+static const char* kKindNames[K_NKINDS] = {"k_plan",   "k_instr", "k_warp",  "k_wclass", "k_smset",
                                            "k_sclass", "k_rows",  "k_fold",  "k_sect",   "k_model",
                                            "k_rank",   "k_simgen", "k_simrun", "k_fit"};
 
@@ -596,7 +596,6 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
   }
   const ws_config* icfg = fan ? xcfg : d_cfgs;
   cudaEvent_t* ev = c->profiling ? c->take_events(K_PLAN, kEstimateKernels) : nullptr;
-  if (ev) c->pending.back().skip = 1u << (K_SCAN - K_PLAN);  // folded into k_plan
   Streams st;
   st.main = c->stream;
   // WS_SERIAL=1 (diagnostics): every chain on the context stream -> uncontended kernel times

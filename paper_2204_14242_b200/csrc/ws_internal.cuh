@@ -123,7 +123,8 @@ struct DPlan {
   // and line geometry, block footprint BF, W, s, L_y, L_z, address space) have identical row-scope
   // counts; the first to claim the key in the row table computes them, the others (row_owner !=
   // own index) have no k_rows / k_fold work and k_model reads the owner's accumulators
-  int32_t row_owner, row_slot, pad4, pad5;
+  int32_t row_owner, row_slot;
+  int32_t istat, pad5;           // k_instr: WS_ELIMIT when the instruction table overflows (else 0)
   // k_rows items: the chunks of computed planes only (derived planes -- translates of their zone
   // segment's representative by whole lines -- are folded by k_fold from the representative)
   int64_t n_ritems, pad6;
@@ -186,7 +187,7 @@ struct Scratch {
 };
 
 // kernel kinds, in launch order (ws_kernel_name)
-enum { K_PLAN = 0, K_SCAN, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_SECT, K_MODEL, K_RANK,
+enum { K_PLAN = 0, K_INSTR, K_WARP, K_WCLASS, K_SMSET, K_SCLASS, K_ROWS, K_FOLD, K_SECT, K_MODEL, K_RANK,
        K_SIMGEN, K_SIMRUN, K_FIT, K_NKINDS };
 constexpr int kEstimateKernels = 10;
 

@@ -629,6 +629,131 @@ __device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __res
 }
 
 
+// a3 instruction table (O3), on the warp chain: k_plan's plan is complete; the row and SM-set
+// chains never read the table, n_instr or addr_evals, so they start without waiting for it.  One
+// CTA per configuration.  Pair p = (access a, kappa q) gives instruction (field, kind, kappa + o_a);
+// keep the first occurrence of each key.  An earlier pair with the same key needs an earlier access
+// a2 of the same field and kind with r - o_a2 inside the fold cube (for a2 == a only q2 == q gives
+// the key).  More than kMaxInstr instructions: istat = WS_ELIMIT (k_model reports it).
+__global__ void __launch_bounds__(128) k_instr(const DKernel* __restrict__ ks, DPlan* __restrict__ plans,
+                                               DInstr* __restrict__ instr, unsigned int* __restrict__ wcnt, int n) {
+  const int c = blockIdx.x, tid = threadIdx.x;
+  {  // this configuration's warp-class counters (k_warp)
+    uint4* wc = reinterpret_cast<uint4*>(wcnt + (long long)c * kWSlots);
+    for (int i = tid; i < kWSlots / 4; i += blockDim.x) wc[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
+  __shared__ int s_part[128];
+  __shared__ int s_total;
+  __shared__ ws_access s_acc[kMaxAcc];
+  __shared__ int s_f[3], s_fc, s_ok;
+  if (tid == 0) {
+    const DPlan& Pg = plans[c];
+    s_ok = Pg.status == WS_OK;
+    for (int d = 0; d < 3; ++d) s_f[d] = Pg.f[d];
+    s_fc = Pg.fcube;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const DPlan& PG = plans[c];
+  const DKernel& K = ks[PG.kid];
+  for (int i = tid; i < K.n_acc; i += blockDim.x) s_acc[i] = K.acc[i];
+  struct { int f[3]; } P{{s_f[0], s_f[1], s_f[2]}};
+  const int fc = s_fc;
+  const int np = K.n_acc * fc;
+  __syncthreads();
+  // ---- O3: fold-deduplicated instruction table.  Pair p = (access a, kappa q) gives
+  // instruction (field, kind, kappa + o_a); keep the first occurrence of each key.  An earlier
+  // pair with the same key needs an earlier access a2 of the same field and kind with
+  // r - o_a2 inside the fold cube (for a2 == a only q2 == q gives the key).
+  __shared__ int s_kap[kMaxFoldCube][3];
+  for (int q = tid; q < fc; q += blockDim.x) decode_kappa(q, P.f, s_kap[q][0], s_kap[q][1], s_kap[q][2]);
+  __syncthreads();
+  for (int p = tid; p < np; p += blockDim.x) {
+    const int a = p / fc, q = p - a * fc;
+    const ws_access A = s_acc[a];
+    const int rx = s_kap[q][0] + A.off[0], ry = s_kap[q][1] + A.off[1], rz = s_kap[q][2] + A.off[2];
+    unsigned char first = 1;
+    for (int a2 = 0; a2 < a && first; ++a2) {
+      const ws_access B = s_acc[a2];
+      if (B.field != A.field || B.is_store != A.is_store) continue;
+      const int dx = rx - B.off[0], dy = ry - B.off[1], dz = rz - B.off[2];
+      if (dx >= 0 && dx < P.f[0] && dy >= 0 && dy < P.f[1] && dz >= 0 && dz < P.f[2]) first = 0;
+    }
+    s_first[p] = first;
+  }
+  __syncthreads();
+  // block-wide exclusive prefix of s_first (contiguous segments per thread)
+  const int seg = (np + blockDim.x - 1) / blockDim.x;
+  int mysum = 0;
+  for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) mysum += s_first[p];
+  {  // exclusive scan over the 128 threads: warp shuffles, then the 4 warp totals
+    const int lane = tid & 31, wid = tid >> 5;
+    int v = mysum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) s_part[wid] = v;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      const int x = s_part[w];
+      if (w < wid) off += x;
+      tot += x;
+    }
+    __syncthreads();
+    s_part[tid] = off + v - mysum;
+    if (tid == 0) s_total = tot;
+  }
+  __syncthreads();
+  if (s_total > kMaxInstr) {   // the configuration fails (status WS_ELIMIT in k_model)
+    if (tid == 0) {
+      plans[c].istat = WS_ELIMIT;
+      plans[c].n_instr = 0;
+    }
+    return;
+  }
+  {
+    int pos = s_part[tid];
+    for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) {
+      if (!s_first[p]) continue;
+      const int a = p / fc, q = p - a * fc;
+      const ws_access A = s_acc[a];
+      const int r[3] = {s_kap[q][0] + A.off[0], s_kap[q][1] + A.off[1], s_kap[q][2] + A.off[2]};
+      // kappas whose folded cell uses this instruction: r - kappa2 is an access offset (Q27)
+      unsigned long long km = 0;
+      for (int q2 = 0; q2 < fc; ++q2) {
+        const int o0 = r[0] - s_kap[q2][0], o1 = r[1] - s_kap[q2][1], o2 = r[2] - s_kap[q2][2];
+        for (int a2 = 0; a2 < K.n_acc; ++a2) {
+          const ws_access B = s_acc[a2];
+          if (B.field == A.field && B.is_store == A.is_store && B.off[0] == o0 && B.off[1] == o1 && B.off[2] == o2) {
+            km |= 1ull << q2;
+            break;
+          }
+        }
+      }
+      const DField& F = K.f[A.field];
+      DInstr e;
+      e.C = F.align + ((r[0] * F.pitch[0] + r[1] * F.pitch[1] + r[2] * F.pitch[2]) << F.lg_elem);
+      e.kmask = km;
+      e.field = (int)A.field;
+      e.kind = (int)A.is_store;
+      e.lg_elem = F.lg_elem;
+      e.pad = 0;
+      instr[(long long)c * kMaxInstr + pos] = e;
+      ++pos;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    DPlan& Q = plans[c];
+    Q.n_instr = s_total;
+    Q.addr_evals = (unsigned long long)((Q.W + Q.s - Q.Lz0) * (long long)Q.T * s_total);
+  }
+}
+
 __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs, int n,
                                               const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
                                               int ng, DPlan* __restrict__ plans, DInstr* __restrict__ instr,
@@ -655,15 +780,11 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   __shared__ __align__(16) DKernel sK;   // this configuration's kernel and GPU descriptors, staged once: the
   __shared__ __align__(16) DGpu sG;      // serial plan work then reads shared memory, not dependent global loads
 
-  __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
-  __shared__ int s_part[128];
-  __shared__ int s_total;
   if (tid < A_N) acc[(long long)c * A_N + tid] = 0ull;
-  // this configuration's class counters and k_sect counters, and a share of the cross-config
-  // class table: zeroed here instead of by memset nodes ahead of the graph's first kernel
+  // this configuration's SM-set class counters and k_sect counters, and a share of the cross-config
+  // class table: zeroed here instead of by memset nodes ahead of the graph's first kernel (the
+  // warp-chain counters: k_instr)
   {
-    uint4* wc = reinterpret_cast<uint4*>(wcnt + (long long)c * kWSlots);
-    for (int i = tid; i < kWSlots / 4; i += blockDim.x) wc[i] = make_uint4(0u, 0u, 0u, 0u);
     uint4* sc = reinterpret_cast<uint4*>(scnt + (long long)c * kSSlots);
     for (int i = tid; i < kSSlots / 4; i += blockDim.x) sc[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int i = tid; i < max_fields; i += blockDim.x) sdone[(long long)c * max_fields + i] = 0u;
@@ -739,94 +860,6 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
   __syncthreads();
   PLAN_MARK()
   const DKernel& K = sK;
-  const int fc = P.fcube;
-  const int np = K.n_acc * fc;
-  // ---- O3: fold-deduplicated instruction table.  Pair p = (access a, kappa q) gives
-  // instruction (field, kind, kappa + o_a); keep the first occurrence of each key.  An earlier
-  // pair with the same key needs an earlier access a2 of the same field and kind with
-  // r - o_a2 inside the fold cube (for a2 == a only q2 == q gives the key).
-  __shared__ int s_kap[kMaxFoldCube][3];
-  for (int q = tid; q < fc; q += blockDim.x) decode_kappa(q, P.f, s_kap[q][0], s_kap[q][1], s_kap[q][2]);
-  __syncthreads();
-  for (int p = tid; p < np; p += blockDim.x) {
-    const int a = p / fc, q = p - a * fc;
-    const ws_access A = K.acc[a];
-    const int rx = s_kap[q][0] + A.off[0], ry = s_kap[q][1] + A.off[1], rz = s_kap[q][2] + A.off[2];
-    unsigned char first = 1;
-    for (int a2 = 0; a2 < a && first; ++a2) {
-      const ws_access B = K.acc[a2];
-      if (B.field != A.field || B.is_store != A.is_store) continue;
-      const int dx = rx - B.off[0], dy = ry - B.off[1], dz = rz - B.off[2];
-      if (dx >= 0 && dx < P.f[0] && dy >= 0 && dy < P.f[1] && dz >= 0 && dz < P.f[2]) first = 0;
-    }
-    s_first[p] = first;
-  }
-  __syncthreads();
-  PLAN_MARK()
-  // block-wide exclusive prefix of s_first (contiguous segments per thread)
-  const int seg = (np + blockDim.x - 1) / blockDim.x;
-  int mysum = 0;
-  for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) mysum += s_first[p];
-  {  // exclusive scan over the 128 threads: warp shuffles, then the 4 warp totals
-    const int lane = tid & 31, wid = tid >> 5;
-    int v = mysum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(FULL, v, o);
-      if (lane >= o) v += u;
-    }
-    if (lane == 31) s_part[wid] = v;
-    __syncthreads();
-    int off = 0, tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      const int x = s_part[w];
-      if (w < wid) off += x;
-      tot += x;
-    }
-    __syncthreads();
-    s_part[tid] = off + v - mysum;
-    if (tid == 0) s_total = tot;
-  }
-  __syncthreads();
-  if (s_total > kMaxInstr) {
-    __syncthreads();
-    if (tid == 0) P.status = WS_ELIMIT;
-    __syncthreads();
-    store_plan();
-    return;
-  }
-  {
-    int pos = s_part[tid];
-    for (int p = tid * seg; p < np && p < (tid + 1) * seg; ++p) {
-      if (!s_first[p]) continue;
-      const int a = p / fc, q = p - a * fc;
-      const ws_access A = K.acc[a];
-      const int r[3] = {s_kap[q][0] + A.off[0], s_kap[q][1] + A.off[1], s_kap[q][2] + A.off[2]};
-      // kappas whose folded cell uses this instruction: r - kappa2 is an access offset (Q27)
-      unsigned long long km = 0;
-      for (int q2 = 0; q2 < fc; ++q2) {
-        const int o0 = r[0] - s_kap[q2][0], o1 = r[1] - s_kap[q2][1], o2 = r[2] - s_kap[q2][2];
-        for (int a2 = 0; a2 < K.n_acc; ++a2) {
-          const ws_access B = K.acc[a2];
-          if (B.field == A.field && B.is_store == A.is_store && B.off[0] == o0 && B.off[1] == o1 && B.off[2] == o2) {
-            km |= 1ull << q2;
-            break;
-          }
-        }
-      }
-      const DField& F = K.f[A.field];
-      DInstr e;
-      e.C = F.align + ((r[0] * F.pitch[0] + r[1] * F.pitch[1] + r[2] * F.pitch[2]) << F.lg_elem);
-      e.kmask = km;
-      e.field = (int)A.field;
-      e.kind = (int)A.is_store;
-      e.lg_elem = F.lg_elem;
-      e.pad = 0;
-      instr[(long long)c * kMaxInstr + pos] = e;
-      ++pos;
-    }
-  }
-  PLAN_MARK()
   // ---- row boxes of the wave + layer-set footprint, per field
   for (int fi = tid; fi < K.n_fields; fi += blockDim.x) {
     const DField& F = K.f[fi];
@@ -868,7 +901,6 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
       ri.chunk_begin = cb;
       cb += ri.n_chunks;
     }
-    P.n_instr = s_total;
     P.n_warp_items = (P.rep_mult ? 1 : P.W) * P.nwarps;
     P.n_wclass_items = 0;
     P.n_set_items = P.rep_mult ? 1 : P.nsets;
@@ -876,7 +908,6 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     P.n_chunks = cb;
     P.n_fields = P.row_owner == c ? K.n_fields : 0;   // k_fold items
     P.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
-    P.addr_evals = (unsigned long long)((P.W + P.s - P.Lz0) * (long long)P.T * s_total);
   }
   __syncthreads();
   // k_rows items: the chunks of computed planes (plane_rep(z) == z), listed per configuration;
@@ -2853,8 +2884,8 @@ __device__ __forceinline__ double gompertz(const double* abc, double O) { return
 __device__ __noinline__ void model_one(const DPlan& P, const DKernel* __restrict__ ks, const DGpu& G,
                                        const unsigned long long* a, ws_result& R) {
   memset(&R, 0, sizeof(R));
-  R.status = P.status;
-  if (P.status != WS_OK) return;
+  R.status = P.status != WS_OK ? P.status : P.istat;   // istat: k_instr's instruction-table limit
+  if (R.status != WS_OK) return;
   const DKernel& K = ks[P.kid];
   for (int d = 0; d < 3; ++d) R.grid[d] = (uint32_t)P.G[d];
   R.k = (uint32_t)P.k;
@@ -3288,6 +3319,9 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
   ++L;
   end(K_SCLASS, a);
+  beg(K_INSTR, m);
+  k_instr<<<n, 128, 0, m>>>(d_k, s.plans, s.instr, s.wcnt, n);
+  end(K_INSTR, m);
   beg(K_WARP, m);
   k_warp<<<persist, 256, 0, m>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
                                  s.work);
@@ -3377,6 +3411,7 @@ int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, void* scratch, 
 // simulated: estimate ok, linear address space, at most 32 sectors per line (valid bits)
 __device__ __forceinline__ int sim_status(const DPlan& P, const DGpu* gs) {
   if (P.status != WS_OK) return P.status;
+  if (P.istat != WS_OK) return P.istat;
   if (P.mdim) return WS_EINVAL;
   if (gs[P.gid].lg_line - gs[P.gid].lg_sector > 5) return WS_ELIMIT;
   return WS_OK;
