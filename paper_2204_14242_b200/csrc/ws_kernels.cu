@@ -56,7 +56,7 @@
 #define WS_SECT_CTAS 2  // k_sect CTAs per SM (launched even when no configuration wants outlook metrics)
 #endif
 #ifndef WS_SCLASS_THREADS
-#define WS_SCLASS_THREADS 256  // threads per k_sclass CTA (<= 256: shared arrays sized for 8 warps)
+#define WS_SCLASS_THREADS 256  // threads per k_sclass CTA (<= 1024; shared arrays sized by it)
 #endif
 #ifndef WS_FOLD_MINB
 #define WS_FOLD_MINB 4
@@ -851,15 +851,15 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     return;
   }
   PLAN_MARK()
+  // the ranges (warp 0) and the row-table claim (warp 1, global atomics) overlap
   if (tid < 5) plan_range(P, tid);
-  __syncthreads();
-  if (tid == 0) {
-    plan_boundaries(P);
-    row_claim(P, c, sG, cur_epoch, rowtab);
-  }
+  if (tid == 32) row_claim(P, c, sG, cur_epoch, rowtab);
+  __syncwarp();
+  if (tid == 0) plan_boundaries(P);
   __syncthreads();
   PLAN_MARK()
   const DKernel& K = sK;
+  __shared__ DRowInfo s_ri[kMaxFields];   // row boxes staged here, written out once
   // ---- row boxes of the wave + layer-set footprint, per field
   for (int fi = tid; fi < K.n_fields; fi += blockDim.x) {
     const DField& F = K.f[fi];
@@ -891,15 +891,14 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     ri.nseg = ri.ny > 0 ? (ri.ny + kRowSeg - 1) / kRowSeg : 1;
     ri.n_chunks = (ri.ny > 0 && P.row_owner == c) ? ri.nz * ri.nseg : 0;   // sharers: the owner's rows
     ri.chunk_begin = 0;
-    rowinfo[(long long)c * kMaxFields + fi] = ri;
+    s_ri[fi] = ri;
   }
   __syncthreads();
   if (tid == 0) {
     long long cb = 0;
     for (int fi = 0; fi < K.n_fields; ++fi) {
-      DRowInfo& ri = rowinfo[(long long)c * kMaxFields + fi];
-      ri.chunk_begin = cb;
-      cb += ri.n_chunks;
+      s_ri[fi].chunk_begin = cb;
+      cb += s_ri[fi].n_chunks;
     }
     P.n_warp_items = (P.rep_mult ? 1 : P.W) * P.nwarps;
     P.n_wclass_items = 0;
@@ -918,8 +917,9 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     __syncthreads();
     const int ll = sG.lg_line;
     uint32_t* cl = clist + (long long)c * clist_stride;
+    for (int fi = tid; fi < K.n_fields; fi += blockDim.x) rowinfo[(long long)c * kMaxFields + fi] = s_ri[fi];
     for (int fi = 0; fi < K.n_fields; ++fi) {
-      const DRowInfo ri = rowinfo[(long long)c * kMaxFields + fi];
+      const DRowInfo ri = s_ri[fi];
       if (ri.n_chunks == 0) continue;
       const DField& F = K.f[fi];
       long long py, pz, falign;
@@ -1470,7 +1470,8 @@ struct T32x2 {
 };
 
 constexpr int kMaxPlanes = 256;   // planes per segment of the SM-set plane fold
-constexpr int kSegRowsS = 1024;  // rows of a plane per SM-set run segment
+// rows of a plane per SM-set run segment (per-warp shared arrays: fewer rows for wider CTAs)
+constexpr int kSegRowsS = WS_SCLASS_THREADS <= 256 ? 1024 : (WS_SCLASS_THREADS <= 512 ? 512 : 256);
 
 // One run of rows [y, y + run) of plane z (row y at plane offset R0): candidates of its first
 // row (member boxes x offset groups), their union, the run's sector and line triples.
@@ -1724,7 +1725,7 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
         if (one_warp) {
           warp_ordered_reduce<2>(t2);
         } else {
-          __shared__ Tri s_fold[(256 / 32) * 2];
+          __shared__ Tri s_fold[(WS_SCLASS_THREADS / 32) * 2];
           cta_ordered_reduce<2>(t2, s_fold);
         }
         if (tid == 0) {
@@ -2009,6 +2010,9 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
 
 // Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
 // directly evaluated multi-block SM sets.
+#ifdef WS_SCLASS_TRACE
+__device__ unsigned long long g_sctrace[65536][2];  // diagnostics build: per-item cycles
+#endif
 __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
                                                 const DGpu* __restrict__ gs, unsigned long long* __restrict__ acc,
                                                 const unsigned int* __restrict__ scnt,
@@ -2023,11 +2027,11 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
   __shared__ SmBox32 s_mb32[kMaxMembers];
   __shared__ Tri s_pt[2 * kMaxPlanes];
   __shared__ unsigned char s_der[kMaxPlanes];
-  __shared__ SmWarp s_sw[8];
+  __shared__ SmWarp s_sw[WS_SCLASS_THREADS / 32];
   __shared__ DGroup s_g[kMaxAcc];
   __shared__ int s_ng;
   __shared__ long long s_box[4];
-  __shared__ Tri s_red[(kRowThreads / 32) * 2];
+  __shared__ Tri s_red[(WS_SCLASS_THREADS / 32) * 2];
   const long long ncls = (long long)lists[1], ndir = (long long)lists[2];
   const long long total = ncls + ndir;
   // dynamic scheduling (lists[3], zeroed by the plan's scan): the directly evaluated sets --
@@ -2038,6 +2042,9 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     const long long item = s_item;
     __syncthreads();  // s_item is rewritten by the next fetch
     if (item >= total) break;
+#ifdef WS_SCLASS_TRACE
+    const long long t_item0 = clock64();
+#endif
     const bool cls = item >= ndir;
     const unsigned long long ent = cls ? slist[item - ndir] : dlist[item];
     const int c = (int)(ent >> 32);
@@ -2085,9 +2092,29 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
         sval[2 * t] = ss;
         sval[2 * t + 1] = sl;
       }
+#ifdef WS_SCLASS_TRACE
+      if (item < 65536) {
+        g_sctrace[item][0] = ((unsigned long long)c << 32) | ((unsigned long long)kj << 1) | (cls ? 1u : 0u);
+        g_sctrace[item][1] = (unsigned long long)(clock64() - t_item0) | ((unsigned long long)un << 40);
+      }
+#endif
     }
   }
 }
+#ifdef WS_SCLASS_TRACE
+__global__ void k_sctrace_dump(const unsigned long long* __restrict__ lists, const DPlan* __restrict__ plans) {
+  const long long total = (long long)lists[1] + (long long)lists[2];
+  for (long long i = 0; i < total && i < 65536; ++i) {
+    const unsigned long long a = g_sctrace[i][0], b = g_sctrace[i][1];
+    const int c = (int)(a >> 32);
+    if ((b & 0xffffffffffull) > WS_SCLASS_TRACE)
+      printf("SCITEM c=%d b=(%d,%d,%d) f=(%d,%d,%d) kj=%d cls=%d rows=%llu cycles=%llu\n", c, plans[c].b[0], plans[c].b[1],
+             plans[c].b[2], plans[c].f[0], plans[c].f[1], plans[c].f[2], (int)((a & 0xffffffffu) >> 1), (int)(a & 1),
+             b >> 40, b & 0xffffffffffull);
+    g_sctrace[i][1] = 0;
+  }
+}
+#endif
 
 // the shared classes' counts (owner evaluated in k_sclass) times each sharer's class size
 __global__ void __launch_bounds__(256) k_sshare(const unsigned long long* __restrict__ lists,
@@ -3317,6 +3344,9 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
                                                                      s.slist, s.dlist, s.work, s.sval);
   k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
+#ifdef WS_SCLASS_TRACE
+  k_sctrace_dump<<<1, 1, 0, a>>>(s.lists, s.plans);
+#endif
   ++L;
   end(K_SCLASS, a);
   beg(K_INSTR, m);
