@@ -190,7 +190,9 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   const size_t o_slist = off;   off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
   size_t max_nsm = 1;
   for (const DGpu& g : c->hg) max_nsm = std::max<size_t>(max_nsm, g.g.n_sm);
-  const size_t o_dlist = off;   off = align_up(off + n * max_nsm * sizeof(unsigned long long));
+  // direct SM-set items: one per set, or one per multi-member connected component (<= 16 per set)
+  const size_t o_dlist = off;   off = align_up(off + n * max_nsm * 16 * sizeof(unsigned long long));
+  const size_t o_dmask = off;   off = align_up(off + n * max_nsm * 16 * sizeof(unsigned int));
   const size_t o_clist = off;   off = align_up(off + max_chunks * sizeof(uint32_t));  // k_rows items per config
   if (bytes_only) {
     *bytes_only = off;
@@ -231,6 +233,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.wlist = (unsigned long long*)(b + o_wlist);
   s.slist = (unsigned long long*)(b + o_slist);
   s.dlist = (unsigned long long*)(b + o_dlist);
+  s.dmask = (unsigned int*)(b + o_dmask);
   s.plan_done = (unsigned int*)(b + o_pdone);
   s.clist = (uint32_t*)(b + o_clist);
   s.clist_stride = (int64_t)cb;

@@ -178,7 +178,8 @@ struct Scratch {
   unsigned long long* lists;  // [0] # warp classes, [1] # SM-set classes, [2] # direct SM sets (zeroed by k_scan)
   unsigned long long* wlist;  // n * kWSlots entries (config << 32 | slot)
   unsigned long long* slist;  // n * kSSlots entries
-  unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm entries
+  unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm * 16 entries
+  unsigned int* dmask;        // per dlist entry: member mask of a connected component (0 = the set)
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
   unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)
   unsigned long long* rowtab; // kRowTab x 8 u64: a5/a6 sharing keys (see DPlan::row_owner)

@@ -1545,18 +1545,22 @@ struct SmWarp {
   short rs[kSegRowsS + 2];
 };
 
+// msk: 0 = every member S0 + m * nsm (m < kj); else only the members m whose bit is set (one
+// connected component of the set, k_smset)
 __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
                           SmBox* mb, SmBox32* mb32, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */,
                           SmWarp* sw,
-                          unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
+                          unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units,
+                          unsigned msk = 0u) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwp = blockDim.x >> 5;
   const int ls = G.lg_sector, ll = G.lg_line;
-  const int nm = (int)(kj < kMaxMembers ? kj : kMaxMembers);
+  const int nm = msk ? __popc(msk) : (int)(kj < kMaxMembers ? kj : kMaxMembers);
   sum_s = sum_l = 0;
   units = 0;
   __syncthreads();
   if (tid < nm) {
-    const long long Bm = S0 + (long long)tid * nsm;
+    const long long mi = msk ? (long long)__fns(msk, 0, tid + 1) : (long long)tid;  // tid-th member
+    const long long Bm = S0 + mi * nsm;
     const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
     long long lo[3], hi[3];
     for (int d = 0; d < 3; ++d) {
@@ -1871,7 +1875,8 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
                                                unsigned long long* __restrict__ lists,
                                                unsigned long long* __restrict__ slist,
                                                unsigned long long* __restrict__ dlist,
-                                               unsigned long long* __restrict__ skey) {
+                                               unsigned long long* __restrict__ skey,
+                                               unsigned int* __restrict__ dmask) {
   __shared__ unsigned long long s_key[kSetGrp];  // directly evaluated sets: shape key (0: not grouped)
   __shared__ unsigned s_cnt[kSetGrp];            // group sizes (at the group's smallest member)
   __shared__ short s_rep[kSetGrp];               // smallest member of the set's group
@@ -1893,11 +1898,19 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
       // last row (rows / planes of >= one line), or >= one line of elements apart in x unless one
       // reaches a row end and the other a row start (wrap-around adjacency of consecutive rows).
       // Otherwise the set is evaluated directly.
+      // Members that cannot share a line with any member of another group form connected
+      // components (union of the non-separated pairs): the set's footprint is the disjoint union of
+      // its components' footprints.  All singletons: the set splits into single-block classes; one
+      // component: the set is evaluated directly (translation groups below); otherwise singletons
+      // join the classes and each larger component is a direct item of its own (member mask).
       bool split = false;
+      int par[32];
+      int ncomp = (int)kj;
       if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult) {
         const DKernel& K = ks[P.kid];
         const long long lb = gs[P.gid].g.line_bytes;
         split = true;
+        for (int m = 0; m < (int)kj; ++m) par[m] = m;
         long long box[32][6];
         const MemberWalk mw(P, nsm);
         long long bc[3];
@@ -1913,15 +1926,20 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
         // pairs outer: a pair separated in z (or in y, away from the fields' first / last rows)
         // by the load-offset envelope of all fields (one pitch for all fields under scls_R) is
         // separated for every field; otherwise the fields are checked one by one
-        for (long long a1 = 0; a1 < kj && split; ++a1)
-          for (long long b1 = a1 + 1; b1 < kj && split; ++b1) {
+        for (long long a1 = 0; a1 < kj && ncomp > 1; ++a1)
+          for (long long b1 = a1 + 1; b1 < kj && ncomp > 1; ++b1) {
             if (env.planes_ok && (box[b1][4] - box[a1][5] >= 2 + env.spz || box[a1][4] - box[b1][5] >= 2 + env.spz))
               continue;
             if (env.rows_ok && min(box[a1][2], box[b1][2]) + env.oy_min >= 1 &&
                 max(box[a1][3], box[b1][3]) + env.oy_max <= env.ext1_min - 2 &&
                 (box[b1][2] - box[a1][3] >= 2 + env.spy || box[a1][2] - box[b1][3] >= 2 + env.spy))
               continue;
-            for (int fi = 0; fi < K.n_fields && split; ++fi) {
+            int ra = (int)a1, rb = (int)b1;
+            while (par[ra] != ra) ra = par[ra];
+            while (par[rb] != rb) rb = par[rb];
+            if (ra == rb) continue;  // already connected
+            bool sep = true;
+            for (int fi = 0; fi < K.n_fields && sep; ++fi) {
               const DField& F = K.f[fi];
               if (!(F.kinds & 1)) continue;
               int xlo = 0x7fffffff, xhi = -0x7fffffff;
@@ -1947,23 +1965,49 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
               const bool b_end = bx1 > F.pitch[1] - 1 - D, b_start = bx0 < D;
               const bool wrap = (a_end && b_start) || (b_end && a_start);
               const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
-              if (!(sep_y || sep_z || sep_x)) split = false;
+              if (!(sep_y || sep_z || sep_x)) sep = false;
+            }
+            if (!sep) {  // union the two components
+              par[ra > rb ? ra : rb] = ra < rb ? ra : rb;
+              --ncomp;
             }
           }
+        split = ncomp == (int)kj;
       }
-      if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
-        for (long long m = 0; m < kj; ++m) {
-          const long long Bm = S0 + m * nsm;
-          const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
-          long long pl = 0;
+      auto claim_member = [&](long long m) {  // member m of the set joins its single-block class
+        const long long Bm = S0 + m * nsm;
+        const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+        long long pl = 0;
 #pragma unroll
-          for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-          const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
-          const long long gslot = (long long)c * kSSlots + slot;
-          if (atomicAdd(scnt + gslot, 1u) == 0u) {
-            srep[gslot] = (unsigned long long)Bm;
-            const unsigned low = share_claim(skey, share_key(P, slot), slot);
-            slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | low;
+        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+        const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+        const long long gslot = (long long)c * kSSlots + slot;
+        if (atomicAdd(scnt + gslot, 1u) == 0u) {
+          srep[gslot] = (unsigned long long)Bm;
+          const unsigned low = share_claim(skey, share_key(P, slot), slot);
+          slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | low;
+        }
+      };
+      if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
+        for (long long m = 0; m < kj; ++m) claim_member(m);
+        if (grp) s_key[j] = 0ull;
+      } else if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult && ncomp > 1) {
+        // several components: singletons -> classes, larger components -> direct items (mask)
+        unsigned cm[32];
+        for (int m = 0; m < (int)kj; ++m) cm[m] = 0u;
+        for (int m = 0; m < (int)kj; ++m) {
+          int r = m;
+          while (par[r] != r) r = par[r];
+          cm[r] |= 1u << m;
+        }
+        for (int r = 0; r < (int)kj; ++r) {
+          if (!cm[r]) continue;
+          if (__popc(cm[r]) == 1) {
+            claim_member(r);
+          } else {
+            const unsigned long long pos = atomicAdd(lists + 2, 1ull);
+            dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
+            dmask[pos] = cm[r];
           }
         }
         if (grp) s_key[j] = 0ull;
@@ -1971,7 +2015,9 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
         s_key[j] = set_shape_key(P, S0, kj, nsm);
       } else {
         if (grp) s_key[j] = 0ull;
-        dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | (unsigned long long)j;
+        const unsigned long long pos = atomicAdd(lists + 2, 1ull);
+        dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
+        dmask[pos] = 0u;
       }
     }
     if (grp) {
@@ -2000,8 +2046,10 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
       for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
         if (!s_key[j] || s_rep[j] != j) continue;
         const unsigned mult = s_cnt[j];
-        dlist[atomicAdd(lists + 2, 1ull)] = ((unsigned long long)c << 32) | 0x80000000ull |
-                                            ((unsigned long long)(mult - 1) << 20) | (unsigned long long)j;
+        const unsigned long long pos = atomicAdd(lists + 2, 1ull);
+        dlist[pos] = ((unsigned long long)c << 32) | 0x80000000ull | ((unsigned long long)(mult - 1) << 20) |
+                     (unsigned long long)j;
+        dmask[pos] = 0u;
       }
       __syncthreads();
     }
@@ -2021,7 +2069,8 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
                                                 const unsigned long long* __restrict__ slist,
                                                 const unsigned long long* __restrict__ dlist,
                                                 unsigned long long* __restrict__ work,
-                                                unsigned long long* __restrict__ sval) {
+                                                unsigned long long* __restrict__ sval,
+                                                const unsigned int* __restrict__ dmask) {
   __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ SmBox32 s_mb32[kMaxMembers];
@@ -2054,6 +2103,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     const long long nsm = G.g.n_sm;
     unsigned long long mult = 1;
     long long S0, kj;
+    unsigned msk = 0u;  // direct item of one connected component of a set (k_smset)
     if (cls && (low >> 31)) continue;  // shared class: k_sshare adds the owner's counts
     if (cls) {
       const long long gslot = (long long)c * kSSlots + (low & 511u);
@@ -2069,6 +2119,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
       if (low & 0x80000000u) mult = 1ull + ((low >> 20) & 0x7ffu);
       S0 = P.s + jj;
       kj = (P.W - jj + nsm - 1) / nsm;
+      msk = dmask[item];
     }
     unsigned long long ss, sl, un;
     int n_ld = 0;
@@ -2079,7 +2130,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
       smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
       if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     } else {        // several blocks: plane derivation + runs
-      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_mb32, s_pt, s_der, s_sw, ss, sl, un);
+      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_mb32, s_pt, s_der, s_sw, ss, sl, un, msk);
       // every warp's lane 0 counted its planes' rows
       if ((threadIdx.x & 31) == 0 && un) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     }
@@ -3338,11 +3389,11 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   end(K_FOLD, b);
   beg(K_SMSET, a);
   k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist,
-                                        s.skey);
+                                        s.skey, s.dmask);
   end(K_SMSET, a);
   beg(K_SCLASS, a);
   k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
-                                                                     s.slist, s.dlist, s.work, s.sval);
+                                                                     s.slist, s.dlist, s.work, s.sval, s.dmask);
   k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
 #ifdef WS_SCLASS_TRACE
   k_sctrace_dump<<<1, 1, 0, a>>>(s.lists, s.plans);
