@@ -193,6 +193,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   // direct SM-set items: one per set, or one per multi-member connected component (<= 16 per set)
   const size_t o_dlist = off;   off = align_up(off + n * max_nsm * 16 * sizeof(unsigned long long));
   const size_t o_dmask = off;   off = align_up(off + n * max_nsm * 16 * sizeof(unsigned int));
+  const size_t o_gkey = off;    off = align_up(off + n * max_nsm * sizeof(unsigned long long));
   const size_t o_clist = off;   off = align_up(off + max_chunks * sizeof(uint32_t));  // k_rows items per config
   if (bytes_only) {
     *bytes_only = off;
@@ -234,6 +235,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.slist = (unsigned long long*)(b + o_slist);
   s.dlist = (unsigned long long*)(b + o_dlist);
   s.dmask = (unsigned int*)(b + o_dmask);
+  s.gkey = (unsigned long long*)(b + o_gkey);
   s.plan_done = (unsigned int*)(b + o_pdone);
   s.clist = (uint32_t*)(b + o_clist);
   s.clist_stride = (int64_t)cb;

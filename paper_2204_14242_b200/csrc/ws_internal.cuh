@@ -180,6 +180,7 @@ struct Scratch {
   unsigned long long* slist;  // n * kSSlots entries
   unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm * 16 entries
   unsigned int* dmask;        // per dlist entry: member mask of a connected component (0 = the set)
+  unsigned long long* gkey;   // per SM set (pre.set order): k_spairs' translation-group key for k_smset
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
   unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)
   unsigned long long* rowtab; // kRowTab x 8 u64: a5/a6 sharing keys (see DPlan::row_owner)

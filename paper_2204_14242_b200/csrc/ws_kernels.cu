@@ -903,7 +903,8 @@ __global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs
     P.n_warp_items = (P.rep_mult ? 1 : P.W) * P.nwarps;
     P.n_wclass_items = 0;
     P.n_set_items = P.rep_mult ? 1 : P.nsets;
-    P.n_sclass_items = 0;
+    // k_spairs items: the sets j < nsets of >= 2 members, i.e. j < W - n_sm (members j + m * n_sm < W)
+    P.n_sclass_items = (P.scls_R > 0 && !P.rep_mult && P.W > P.nsets) ? min(P.nsets, P.W - P.nsets) : 0;
     P.n_chunks = cb;
     P.n_fields = P.row_owner == c ? K.n_fields : 0;   // k_fold items
     P.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
@@ -1864,11 +1865,81 @@ __device__ __forceinline__ bool set_translates(const DPlan& P, long long S0, lon
 }
 
 
+// Two members' load footprints (block box + the field's load-offset extremes) share no line when
+// they are >= 2 planes apart in z, or >= 2 rows apart in y without touching the field's first or
+// last row (rows / planes of >= one line), or >= one line of elements apart in x unless one reaches
+// a row end and the other a row start (wrap-around adjacency of consecutive rows).  The load-offset
+// envelope of all fields (one pitch for all fields under scls_R) decides most pairs at once.
+// Boxes: {x0, x1, y0, y1, z0, z1}, inclusive ends.
+__device__ bool set_pair_separated(const DKernel& K, const SetEnv& env, long long lb, const long long* A,
+                                   const long long* B) {
+  if (env.planes_ok && (B[4] - A[5] >= 2 + env.spz || A[4] - B[5] >= 2 + env.spz)) return true;
+  if (env.rows_ok && min(A[2], B[2]) + env.oy_min >= 1 && max(A[3], B[3]) + env.oy_max <= env.ext1_min - 2 &&
+      (B[2] - A[3] >= 2 + env.spy || A[2] - B[3] >= 2 + env.spy))
+    return true;
+  for (int fi = 0; fi < K.n_fields; ++fi) {
+    const DField& F = K.f[fi];
+    if (!(F.kinds & 1)) continue;
+    int xlo = 0x7fffffff, xhi = -0x7fffffff;
+    for (int r = 0; r < F.n_runs; ++r) {
+      xlo = min(xlo, F.run_lo[r]);
+      xhi = max(xhi, F.run_hi[r]);
+    }
+    const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
+    const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
+    const long long ax0 = A[0] + xlo, ax1 = A[1] + xhi, bx0 = B[0] + xlo, bx1 = B[1] + xhi;
+    const long long ay0 = A[2] + F.ld_oy_min, ay1 = A[3] + F.ld_oy_max;
+    const long long by0 = B[2] + F.ld_oy_min, by1 = B[3] + F.ld_oy_max;
+    const long long az0 = A[4] + F.ld_oz_min, az1 = A[5] + F.ld_oz_max;
+    const long long bz0 = B[4] + F.ld_oz_min, bz1 = B[5] + F.ld_oz_max;
+    // rows >= 2 apart share no line within a plane; across consecutive planes only if a box
+    // reaches the field's first / last row (p2 >= p1 * ext1), hence the y-ends condition
+    const bool y_inner = min(ay0, by0) >= 1 && max(ay1, by1) <= F.ext[1] - 2;
+    const bool sep_y = rows_ok && y_inner && (ay1 + 2 <= by0 || by1 + 2 <= ay0);
+    const bool sep_z = planes_ok && (az1 + 2 <= bz0 || bz1 + 2 <= az0);
+    // consecutive rows in memory can share a line only between a box reaching the row end and one
+    // reaching the row start
+    const bool a_end = ax1 > F.pitch[1] - 1 - D, a_start = ax0 < D;
+    const bool b_end = bx1 > F.pitch[1] - 1 - D, b_start = bx0 < D;
+    const bool wrap = (a_end && b_start) || (b_end && a_start);
+    const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
+    if (!(sep_y || sep_z || sep_x)) return false;
+  }
+  return true;
+}
+
+// block Bm of configuration c joins its single-block translation class (slot: line residue of its
+// first cell, clip pattern); the first member of a class claims it (and the cross-configuration
+// key).  Called by the whole warp (active lanes join): lanes of one slot are counted with one
+// atomic by their leader (__match_any_sync), not one per block.
+__device__ void smset_claim(const DPlan& P, int c, long long Bm, bool active, unsigned int* __restrict__ scnt,
+                            unsigned long long* __restrict__ srep, unsigned long long* __restrict__ skey,
+                            unsigned long long* __restrict__ slist, unsigned long long* __restrict__ lists) {
+  const int lane = threadIdx.x & 31;
+  unsigned slot = 0u;
+  if (active) {
+    const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
+    long long pl = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
+    slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
+  }
+  const unsigned peers = __match_any_sync(FULL, active ? slot : 0x80000000u + (unsigned)lane);
+  if (!active || lane != __ffs(peers) - 1) return;
+  const long long gslot = (long long)c * kSSlots + slot;
+  if (atomicAdd(scnt + gslot, (unsigned)__popc(peers)) == 0u) {
+    srep[gslot] = (unsigned long long)Bm;
+    const unsigned low = share_claim(skey, share_key(P, slot), slot);
+    slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | low;
+  }
+}
+
 // Pass 1 (one thread per SM set): single-block sets go to their translation class: clip
 // pattern of the block x residue of its first cell's address mod line_bytes (identical
 // active-cell boxes that are translates by a multiple of the line size have identical
 // sector and line counts).  Multi-block sets are appended to the direct list.
-__global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+constexpr int kSmsetThreads = 256;
+__global__ void __launch_bounds__(kSmsetThreads) k_smset(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
                                                const DKernel* __restrict__ ks,
                                                const DGpu* __restrict__ gs, unsigned int* __restrict__ scnt,
                                                unsigned long long* __restrict__ srep,
@@ -1876,7 +1947,8 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
                                                unsigned long long* __restrict__ slist,
                                                unsigned long long* __restrict__ dlist,
                                                unsigned long long* __restrict__ skey,
-                                               unsigned int* __restrict__ dmask) {
+                                               unsigned int* __restrict__ dmask,
+                                               const unsigned long long* __restrict__ gkey) {
   __shared__ unsigned long long s_key[kSetGrp];  // directly evaluated sets: shape key (0: not grouped)
   __shared__ unsigned s_cnt[kSetGrp];            // group sizes (at the group's smallest member)
   __shared__ short s_rep[kSetGrp];               // smallest member of the set's group
@@ -1887,129 +1959,27 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
     const long long nsm = gs[P.gid].g.n_sm;
     const bool grp = nset <= kSetGrp && P.scls_R > 0 && !P.rep_mult;
     const SetEnv env = set_env(ks[P.kid], gs[P.gid].g.line_bytes);
-    for (long long j = threadIdx.x; j < nset; j += blockDim.x) {
+    // A multi-block set whose members' load footprints cannot share a line is the disjoint union
+    // of its members' footprints: every member is then counted like a single-block set, in its
+    // translation class (members are n_sm blocks apart, usually far apart in the grid).  Members
+    // that cannot share a line with any member of another group form connected components (union
+    // of the non-separated pairs, set_pair_separated): the set's footprint is the disjoint union of
+    // its components' footprints.  All singletons: the set splits into single-block classes; one
+    // component: the set is evaluated directly (translation groups below); otherwise singletons
+    // join the classes and each larger component is a direct item of its own (member mask).
+    const bool pairs_on = P.scls_R > 0 && !P.rep_mult;
+    // (1) one thread per set (sets of 2..32 members were analysed by k_spairs)
+    for (long long j0 = threadIdx.x - (threadIdx.x & 31); j0 < nset; j0 += blockDim.x) {  // warp-uniform
+      const long long j = j0 + (threadIdx.x & 31);
       const long long S0 = P.s + j;
-      const long long kj = (P.W - j + nsm - 1) / nsm;  // members S0 + m*nsm, m < kj
-      // A multi-block set whose members' load footprints cannot share a line is the disjoint union
-      // of its members' footprints: every member is then counted like a single-block set, in its
-      // translation class (members are n_sm blocks apart, usually far apart in the grid).  Two
-      // members' footprints (block box + the field's load-offset extremes) share no line when they
-      // are >= 2 planes apart in z, or >= 2 rows apart in y without touching the field's first or
-      // last row (rows / planes of >= one line), or >= one line of elements apart in x unless one
-      // reaches a row end and the other a row start (wrap-around adjacency of consecutive rows).
-      // Otherwise the set is evaluated directly.
-      // Members that cannot share a line with any member of another group form connected
-      // components (union of the non-separated pairs): the set's footprint is the disjoint union of
-      // its components' footprints.  All singletons: the set splits into single-block classes; one
-      // component: the set is evaluated directly (translation groups below); otherwise singletons
-      // join the classes and each larger component is a direct item of its own (member mask).
-      bool split = false;
-      int par[32];
-      int ncomp = (int)kj;
-      if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult) {
-        const DKernel& K = ks[P.kid];
-        const long long lb = gs[P.gid].g.line_bytes;
-        split = true;
-        for (int m = 0; m < (int)kj; ++m) par[m] = m;
-        long long box[32][6];
-        const MemberWalk mw(P, nsm);
-        long long bc[3];
-        block_coord(P, S0, bc);
-        for (long long m = 0; m < kj; ++m) {
-          if (m) mw.step(P, bc);
-          for (int d = 0; d < 3; ++d) {
-            box[m][2 * d] = P.lo[d] + bc[d] * P.BF[d];
-            long long hi = box[m][2 * d] + P.BF[d];
-            box[m][2 * d + 1] = (hi > P.hi[d] ? P.hi[d] : hi) - 1;
-          }
-        }
-        // pairs outer: a pair separated in z (or in y, away from the fields' first / last rows)
-        // by the load-offset envelope of all fields (one pitch for all fields under scls_R) is
-        // separated for every field; otherwise the fields are checked one by one
-        for (long long a1 = 0; a1 < kj && ncomp > 1; ++a1)
-          for (long long b1 = a1 + 1; b1 < kj && ncomp > 1; ++b1) {
-            if (env.planes_ok && (box[b1][4] - box[a1][5] >= 2 + env.spz || box[a1][4] - box[b1][5] >= 2 + env.spz))
-              continue;
-            if (env.rows_ok && min(box[a1][2], box[b1][2]) + env.oy_min >= 1 &&
-                max(box[a1][3], box[b1][3]) + env.oy_max <= env.ext1_min - 2 &&
-                (box[b1][2] - box[a1][3] >= 2 + env.spy || box[a1][2] - box[b1][3] >= 2 + env.spy))
-              continue;
-            int ra = (int)a1, rb = (int)b1;
-            while (par[ra] != ra) ra = par[ra];
-            while (par[rb] != rb) rb = par[rb];
-            if (ra == rb) continue;  // already connected
-            bool sep = true;
-            for (int fi = 0; fi < K.n_fields && sep; ++fi) {
-              const DField& F = K.f[fi];
-              if (!(F.kinds & 1)) continue;
-              int xlo = 0x7fffffff, xhi = -0x7fffffff;
-              for (int r = 0; r < F.n_runs; ++r) {
-                xlo = min(xlo, F.run_lo[r]);
-                xhi = max(xhi, F.run_hi[r]);
-              }
-              const long long D = (lb >> F.lg_elem) + 1;  // elements per line, plus one
-              const bool rows_ok = (F.pitch[1] << F.lg_elem) >= lb, planes_ok = (F.pitch[2] << F.lg_elem) >= lb;
-              const long long ax0 = box[a1][0] + xlo, ax1 = box[a1][1] + xhi, bx0 = box[b1][0] + xlo, bx1 = box[b1][1] + xhi;
-              const long long ay0 = box[a1][2] + F.ld_oy_min, ay1 = box[a1][3] + F.ld_oy_max;
-              const long long by0 = box[b1][2] + F.ld_oy_min, by1 = box[b1][3] + F.ld_oy_max;
-              const long long az0 = box[a1][4] + F.ld_oz_min, az1 = box[a1][5] + F.ld_oz_max;
-              const long long bz0 = box[b1][4] + F.ld_oz_min, bz1 = box[b1][5] + F.ld_oz_max;
-              // rows >= 2 apart share no line within a plane; across consecutive planes only if a box
-              // reaches the field's first / last row (p2 >= p1 * ext1), hence the y-ends condition
-              const bool y_inner = min(ay0, by0) >= 1 && max(ay1, by1) <= F.ext[1] - 2;
-              const bool sep_y = rows_ok && y_inner && (ay1 + 2 <= by0 || by1 + 2 <= ay0);
-              const bool sep_z = planes_ok && (az1 + 2 <= bz0 || bz1 + 2 <= az0);
-              // consecutive rows in memory can share a line only between a box reaching the row end and
-              // one reaching the row start
-              const bool a_end = ax1 > F.pitch[1] - 1 - D, a_start = ax0 < D;
-              const bool b_end = bx1 > F.pitch[1] - 1 - D, b_start = bx0 < D;
-              const bool wrap = (a_end && b_start) || (b_end && a_start);
-              const bool sep_x = rows_ok && !wrap && (ax1 + D <= bx0 || bx1 + D <= ax0);
-              if (!(sep_y || sep_z || sep_x)) sep = false;
-            }
-            if (!sep) {  // union the two components
-              par[ra > rb ? ra : rb] = ra < rb ? ra : rb;
-              --ncomp;
-            }
-          }
-        split = ncomp == (int)kj;
+      const long long kj = j < nset ? (P.W - j + nsm - 1) / nsm : 0;  // members S0 + m*nsm, m < kj
+      smset_claim(P, c, S0, pairs_on && kj == 1, scnt, srep, skey, slist, lists);  // whole warp
+      if (j >= nset) continue;
+      if (pairs_on && kj > 1 && kj <= 32) {  // analysed by k_spairs: its translation-group key
+        if (grp) s_key[j] = gkey[pre[c].set + j];
+        continue;
       }
-      auto claim_member = [&](long long m) {  // member m of the set joins its single-block class
-        const long long Bm = S0 + m * nsm;
-        const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
-        long long pl = 0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) pl += P.cls_pitch[d] * (P.lo[d] + bc[d] * P.BF[d]);
-        const unsigned slot = (unsigned)(((pl & (P.scls_R - 1)) << 3) | clip_pattern(P, bc));
-        const long long gslot = (long long)c * kSSlots + slot;
-        if (atomicAdd(scnt + gslot, 1u) == 0u) {
-          srep[gslot] = (unsigned long long)Bm;
-          const unsigned low = share_claim(skey, share_key(P, slot), slot);
-          slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | low;
-        }
-      };
-      if (P.scls_R > 0 && (kj == 1 || split) && !P.rep_mult) {
-        for (long long m = 0; m < kj; ++m) claim_member(m);
-        if (grp) s_key[j] = 0ull;
-      } else if (P.scls_R > 0 && kj > 1 && kj <= 32 && !P.rep_mult && ncomp > 1) {
-        // several components: singletons -> classes, larger components -> direct items (mask)
-        unsigned cm[32];
-        for (int m = 0; m < (int)kj; ++m) cm[m] = 0u;
-        for (int m = 0; m < (int)kj; ++m) {
-          int r = m;
-          while (par[r] != r) r = par[r];
-          cm[r] |= 1u << m;
-        }
-        for (int r = 0; r < (int)kj; ++r) {
-          if (!cm[r]) continue;
-          if (__popc(cm[r]) == 1) {
-            claim_member(r);
-          } else {
-            const unsigned long long pos = atomicAdd(lists + 2, 1ull);
-            dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
-            dmask[pos] = cm[r];
-          }
-        }
+      if (pairs_on && kj == 1) {
         if (grp) s_key[j] = 0ull;
       } else if (grp && kj <= 32 && set_unclipped(P, S0, kj, nsm)) {
         s_key[j] = set_shape_key(P, S0, kj, nsm);
@@ -2020,6 +1990,7 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
         dmask[pos] = 0u;
       }
     }
+    __syncthreads();
     if (grp) {
       // Multi-block sets evaluated directly, grouped by translation: two sets whose members are
       // the same translate of each other (same count, unclipped, same line residue) have equal
@@ -2053,6 +2024,120 @@ __global__ void __launch_bounds__(128) k_smset(const DPlan* __restrict__ plans, 
       }
       __syncthreads();
     }
+  }
+}
+
+// SM sets of 2..32 members (k_smset's pair analysis), one warp per set over every configuration's
+// sets (items: the pre.set prefix): lanes test the member pairs (set_pair_separated), lane 0 unites
+// the connected components; all singletons -> the members' single-block classes, one component ->
+// the set as a whole (its translation-group key for k_smset in gkey, or a direct item), several ->
+// singletons to their classes, larger components to direct items with a member mask.
+__global__ void __launch_bounds__(kSmsetThreads) k_spairs(const DPlan* __restrict__ plans,
+                                                const DPrefix* __restrict__ pre, int n,
+                                                const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
+                                                unsigned int* __restrict__ scnt, unsigned long long* __restrict__ srep,
+                                                unsigned long long* __restrict__ lists,
+                                                unsigned long long* __restrict__ slist,
+                                                unsigned long long* __restrict__ dlist,
+                                                unsigned long long* __restrict__ skey, unsigned int* __restrict__ dmask,
+                                                unsigned long long* __restrict__ gkey) {
+  __shared__ long long s_mbox[kSmsetThreads / 32][32 * 6];  // member boxes of a warp's set
+  __shared__ unsigned s_adj[kSmsetThreads / 32][32];        // non-separated pairs, row a1 bit b1
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long total = pre[n].sclass;   // sets of >= 2 members only (k_plan's n_sclass_items)
+  const long long nwg = (long long)gridDim.x * (blockDim.x >> 5);
+  int c = -1;
+  for (long long item0 = (long long)blockIdx.x * (blockDim.x >> 5) + wid; item0 < total; item0 += nwg) {
+    c = find_config_warp<3>(pre, n, item0, c);
+    const DPlan& P = plans[c];
+    const long long j = item0 - pre[c].sclass;
+    const long long item = pre[c].set + j;  // the set's index in pre.set order (gkey)
+    const long long nsm = gs[P.gid].g.n_sm;
+    const long long kj = (P.W - j + nsm - 1) / nsm;
+    if (!(P.scls_R > 0 && !P.rep_mult) || kj <= 1 || kj > 32) continue;
+    const long long nset = pre[c + 1].set - pre[c].set;
+    const bool grp = nset <= kSetGrp;
+    const SetEnv env = set_env(ks[P.kid], gs[P.gid].g.line_bytes);
+    const DKernel& K = ks[P.kid];
+    const long long lb = gs[P.gid].g.line_bytes;
+    const long long S0 = P.s + j;
+    unsigned long long gk = 0ull;
+    {
+      {
+        long long* bx = s_mbox[wid];
+        if (lane < kj) {
+          long long bc[3];
+          block_coord(P, S0 + (long long)lane * nsm, bc);
+          for (int d = 0; d < 3; ++d) {
+            bx[lane * 6 + 2 * d] = P.lo[d] + bc[d] * P.BF[d];
+            const long long hi = bx[lane * 6 + 2 * d] + P.BF[d];
+            bx[lane * 6 + 2 * d + 1] = (hi > P.hi[d] ? P.hi[d] : hi) - 1;
+          }
+        }
+        s_adj[wid][lane] = 0u;
+        __syncwarp();
+        const int k = (int)kj, npair = k * (k - 1) / 2;
+        for (int p = lane; p < npair; p += 32) {
+          int a1 = 0, q = p;  // row-major triangular index -> (a1, b1), a1 < b1
+          while (q >= k - 1 - a1) {
+            q -= k - 1 - a1;
+            ++a1;
+          }
+          const int b1 = a1 + 1 + q;
+          if (!set_pair_separated(K, env, lb, bx + a1 * 6, bx + b1 * 6)) atomicOr(&s_adj[wid][a1], 1u << b1);
+        }
+        __syncwarp();
+        unsigned single = 0u;
+        if (lane == 0) {
+          int par[32];
+          for (int m = 0; m < k; ++m) par[m] = m;
+          for (int a1 = 0; a1 < k; ++a1) {
+            unsigned row = s_adj[wid][a1];
+            while (row) {
+              const int b1 = __ffs(row) - 1;
+              row &= row - 1;
+              int ra = a1, rb = b1;
+              while (par[ra] != ra) ra = par[ra];
+              while (par[rb] != rb) rb = par[rb];
+              if (ra != rb) par[ra > rb ? ra : rb] = ra < rb ? ra : rb;
+            }
+          }
+          unsigned cm[32];
+          for (int m = 0; m < k; ++m) cm[m] = 0u;
+          int ncomp = 0;
+          for (int m = 0; m < k; ++m) {
+            int r = m;
+            while (par[r] != r) r = par[r];
+            if (!cm[r]) ++ncomp;
+            cm[r] |= 1u << m;
+          }
+          if (ncomp == 1) {  // one component: the set as a whole (translation groups below)
+            if (grp && set_unclipped(P, S0, kj, nsm)) {
+              gk = set_shape_key(P, S0, kj, nsm);
+            } else {
+              const unsigned long long pos = atomicAdd(lists + 2, 1ull);
+              dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
+              dmask[pos] = 0u;
+            }
+          } else {
+            for (int r = 0; r < k; ++r) {
+              if (!cm[r]) continue;
+              if (__popc(cm[r]) == 1) {
+                single |= cm[r];
+              } else {
+                const unsigned long long pos = atomicAdd(lists + 2, 1ull);
+                dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
+                dmask[pos] = cm[r];
+              }
+            }
+          }
+        }
+        single = __shfl_sync(FULL, single, 0);
+        smset_claim(P, c, S0 + (long long)lane * nsm, (single >> lane) & 1u, scnt, srep, skey, slist, lists);
+        __syncwarp();
+      }
+    }
+    if (lane == 0) gkey[item] = gk;
   }
 }
 
@@ -3388,8 +3473,11 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc, fold_mode);
   end(K_FOLD, b);
   beg(K_SMSET, a);
-  k_smset<<<n_sm_dev * 8, 128, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist,
-                                        s.skey, s.dmask);
+  k_spairs<<<n_sm_dev * 4, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist,
+                                                  s.dlist, s.skey, s.dmask, s.gkey);
+  k_smset<<<n_sm_dev * 8, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist,
+                                        s.skey, s.dmask, s.gkey);
+  ++L;
   end(K_SMSET, a);
   beg(K_SCLASS, a);
   k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
