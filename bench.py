@@ -334,35 +334,46 @@ def run_native(args, rank, world, local):
     # ---- e2e through the public API with host buffers
     e2e = e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb)
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline: k_rows (the kernel VERDICT r01 names; the row chain's critical path), and
+    # the executed issue rate of every kernel against the MEASURED integer issue peak
     kern = {k: v for k, v in prof.items() if v[1] > 0}
-    dom = max(kern, key=lambda k: kern[k][0])
+    dom = "k_rows" if "k_rows" in kern else max(kern, key=lambda k: kern[k][0])
+    longest = max(kern, key=lambda k: kern[k][0] / kern[k][1])
     dom_ms = kern[dom][0] / kern[dom][1]
     pk = peaks()
     sm_max = pk.get("sm_max_mhz", 1965.0)
-    peak = alu_peak_gops(sm_max)
+    ipk = {}
+    try:
+        ipk = json.load(open(os.path.join(ROOT, "profiles", "r02_int_peak.json")))
+    except Exception:
+        pass
+    issue_peak_nominal = 148 * 4 * sm_max * 1e6
+    issue_peak = ipk.get("issue_peak_measured_warp_inst_per_s") or issue_peak_nominal
+    peak = issue_peak * 32 / 1e9          # lane-ops/s (Gop/s)
+    peak_note = (f"measured: {issue_peak:.4g} warp-instructions/s x 32 lanes (profiles/r02_int_peak.json, "
+                 f"scripts/int_peak.cu: integer ALU+FMA+SHFL mix at {ipk.get('issue_active_pct_mix_shfl', 0):.0f} % "
+                 f"issue-active; nominal 148 SMs x 4 SMSPs x 1/clk x {sm_max:.0f} MHz = {issue_peak_nominal:.4g})"
+                 if ipk else f"nominal: 148 SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (issue-limited int lane-ops)")
     units = work.get(dom, 0)
     ops = units * OPS_PER_UNIT.get(dom, 0)
     achieved = ops / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-    traffic = None
+    nt = {}
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom)
+        nt = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         pass
+    traffic = nt.get(dom)
     share = {k: round(v[0] / sum(x[0] for x in kern.values()), 4) for k, v in kern.items()}
     # executed instruction mix (with row spans the roofline is recomputed for the
-    # executed mix): the committed ncu capture's warp instructions per launch of the dominant
-    # kernel over its live launch time, against the issue peak (148 SMs x 4 SMSPs x 1/clk)
-    warp_inst = None
-    try:
-        warp_inst = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom + ":warp_inst")
-    except Exception:
-        pass
-    issue_peak = 148 * 4 * sm_max * 1e6
+    # executed mix): the committed ncu capture's warp instructions per launch over the kernel's
+    # live launch time in this run, against the measured issue peak
+    warp_inst = nt.get(dom + ":warp_inst")
     executed = ({"warp_inst_per_launch": warp_inst, "issue_rate_per_s": warp_inst / (dom_ms / 1e3),
                  "issue_peak_per_s": issue_peak, "issue_frac": warp_inst / (dom_ms / 1e3) / issue_peak,
                  "source": "profiles/ncu_traffic.json (ncu --set full, smsp__inst_executed.sum)"}
                 if warp_inst and dom_ms > 0 else None)
+    issue_by_kernel = {k: round(nt[k + ":warp_inst"] / (v[0] / v[1] / 1e3) / issue_peak, 4)
+                       for k, v in kern.items() if nt.get(k + ":warp_inst") and v[0] > 0}
 
     strong = configs3_strong_measure(ctx, stream, args, rank, world, dev)
     cpu = None
@@ -387,8 +398,10 @@ def run_native(args, rank, world, local):
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "units_per_launch": units, "ops_per_unit": OPS_PER_UNIT.get(dom),
                          "avg_launch_ms": dom_ms,
-                         "peak_note": f"148 SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (issue-limited int lane-ops)",
-                         "executed": executed},
+                         "peak_note": peak_note, "executed": executed,
+                         "kernel_choice": "k_rows: the kernel VERDICT r01 names (row chain, critical path); "
+                                          f"longest average launch this run: {longest}",
+                         "issue_frac_by_kernel": issue_by_kernel},
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
             "kernel_share": share,
             "e2e": e2e,
