@@ -1378,9 +1378,15 @@ __device__ __forceinline__ void t32_add(T32& t, int s0, int s1) {
   t.l = s1;
 }
 __device__ __forceinline__ T32 t32_combine(const T32& a, const T32& b) {
+#ifndef WS_T32_BRANCHY
+  // branch-free (selects): the lanes of a warp combine different triples without diverging
+  const bool ea = a.c == 0, eb = b.c == 0;
+  return T32{ea ? b.f : a.f, eb ? a.l : b.l, a.c + b.c - ((!ea && !eb && a.l == b.f) ? 1 : 0)};
+#else
   if (a.c == 0) return b;
   if (b.c == 0) return a;
   return T32{a.f, b.l, a.c + b.c - (a.l == b.f ? 1 : 0)};
+#endif
 }
 
 // union of the intervals [xs, xe) produced by gen, in the row starting at plane offset R
