@@ -159,10 +159,9 @@ __device__ __forceinline__ void tri_add(Tri& t, long long s0, long long s1) {
   }
   t.l = s1;
 }
-__device__ __forceinline__ Tri tri_combine(const Tri& a, const Tri& b) {
-  if (a.c == 0) return b;
-  if (b.c == 0) return a;
-  return Tri{a.f, b.l, a.c + b.c - (a.l == b.f ? 1 : 0)};
+__device__ __forceinline__ Tri tri_combine(const Tri& a, const Tri& b) {  // branch-free (selects)
+  const bool ea = a.c == 0, eb = b.c == 0;
+  return Tri{ea ? b.f : a.f, eb ? a.l : b.l, a.c + b.c - ((!ea && !eb && a.l == b.f) ? 1 : 0)};
 }
 
 // Ordered CTA reduction of NQ triples per thread (thread order = row order).
