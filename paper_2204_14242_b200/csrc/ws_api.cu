@@ -15,9 +15,18 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: ranges for nsys / ncu --nvtx (no cost without a tool)
+
 #include "ws_internal.cuh"
 
 using namespace wsb;
+
+namespace {
+struct NvtxRange {  // one NVTX range per ABI call
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct ws_ctx {
   int device = 0;
@@ -557,6 +566,7 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
 static size_t chunk_configs(ws_ctx* c, size_t per_item_mult);
 
 ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out) {
+  const NvtxRange range("ws_estimate_async");
   if (!c) return WS_EINVAL;
   if (n == 0) return WS_OK;
   if (!d_cfgs || !d_out) return fail(c, WS_EINVAL, "null argument");
@@ -710,6 +720,7 @@ ws_status ws_estimate(ws_ctx* c, const ws_config* cfgs, size_t n, ws_result* out
 
 ws_status ws_estimate_multi_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, const uint32_t* gpu_ids,
                                   uint32_t n_gpu, ws_result* d_out) {
+  const NvtxRange range("ws_estimate_multi_async");
   if (!c) return WS_EINVAL;
   if (n == 0 || n_gpu == 0) return WS_OK;
   if (!d_cfgs || !d_out || !gpu_ids) return fail(c, WS_EINVAL, "null argument");
@@ -776,6 +787,7 @@ ws_status ws_estimate_multi(ws_ctx* c, const ws_config* cfgs, size_t n, const ui
 uint32_t ws_last_group_count(const ws_ctx* c) { return c ? c->last_groups : 0; }
 
 ws_status ws_rank_async(ws_ctx* c, ws_result* d_res, size_t n, size_t k, uint32_t* d_top) {
+  const NvtxRange range("ws_rank_async");
   if (!c) return WS_EINVAL;
   if (n == 0) return WS_OK;
   if (!d_res) return fail(c, WS_EINVAL, "null argument");
@@ -819,6 +831,7 @@ ws_status ws_rank(ws_ctx* c, ws_result* res, size_t n, size_t k, uint32_t* top) 
 
 ws_status ws_simulate(ws_ctx* c, const ws_config* cfgs, size_t n, const uint64_t* caps, uint32_t n_cap,
                       ws_sim_result* out) {
+  const NvtxRange range("ws_simulate");
   if (!c) return WS_EINVAL;
   if (n == 0 || n_cap == 0) return WS_OK;
   if (!cfgs || !caps || !out) return fail(c, WS_EINVAL, "null argument");

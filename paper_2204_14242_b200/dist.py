@@ -123,6 +123,9 @@ class ShardedSweep:
                 self.ctx.estimate_multi_async(self.d_cfg.data_ptr(), self.n_local, self.gpu_ids, self.d_out.data_ptr())
                 self.est_launches = self.ctx.last_launch_count()
                 self.est_groups = self.ctx.last_group_count()
+        nvtx = torch.cuda.nvtx if self.dev.type == "cuda" else None
+        if nvtx:
+            nvtx.range_push("ShardedSweep.gather")
         if self.world == 1:
             torch.index_select(self.d_out, 0, self.perm, out=self.result)
         elif self.backend == "nccl":
@@ -132,6 +135,8 @@ class ShardedSweep:
             self.h_out.copy_(self.d_out)
             dist.all_gather_into_tensor(self.gathered, self.h_out, group=self.group)
             self.result.copy_(torch.index_select(self.gathered, 0, self.perm))
+        if nvtx:
+            nvtx.range_pop()
         if self.ctx is not None:
             self.ctx.rank_async(self.result.data_ptr(), self.H * self.n, self.k_top, self.top.data_ptr())
         return self.result
