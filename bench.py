@@ -10,7 +10,7 @@ evaluates the same 168-config space on its own hardware parameter set
 (architecture exploration, BJ configs[3]: rank 0 = A100, then B200-like, V100
 and a hypothetical grid), the results are all-gathered over NCCL and every rank
 ranks the gathered set: per-GPU work is fixed -> "scaling": "weak".  The same run
-also measures BJ configs[3] with a fixed total (`configs3_strong`: 168 configs x 49
+also measures BJ configs[3] with a fixed total (`configs3_strong`: 217 configs x 51
 hardware sets sharded by configuration over the ranks, one all-gather).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
@@ -420,9 +420,10 @@ def run_native(args, rank, world, local):
 
 
 def configs3_strong_measure(ctx, stream, args, rank, world, dev):
-    """BJ configs[3] with a fixed total (strong scaling): the 168-config 3D-25pt 512^3 space x the
-    49 configs[3] hardware sets (workloads.hw_grid_configs3) = 8232 (configuration, hardware set)
-    estimates, sharded by configuration over the ranks (LPT on device-derived per-configuration
+    """BJ configs[3] with a fixed total (strong scaling): configs[1] u configs[2] (the 168-config
+    3D-25pt 512^3 space and the 49 LBM15 256^3 configurations) x the 51 configs[3] hardware sets
+    (V100, A100, B200-like, 48 hypothetical; workloads.hw_grid_configs3) = 11067 (configuration,
+    hardware set) estimates, sharded by configuration over the ranks (LPT on device-derived per-configuration
     costs computed on rank 0 and broadcast), ws_estimate_multi per rank (integer stages once per
     SM-count group, model fanned out), one all-gather, the canonical permutation, ws_rank of the
     whole set on every rank.  Timed like the headline: barrier + synchronize around K steps,
@@ -431,9 +432,10 @@ def configs3_strong_measure(ctx, stream, args, rank, world, dev):
     import torch.distributed as dist
     from paper_2204_14242_b200 import config_array, dist as D
     sets = W.hw_grid_configs3(peaks().get("hbm_gbs", 6546.2))
-    kid = ctx.describe_kernel(W.k25(512))
+    import numpy as np
+    k25, klbm = ctx.describe_kernel(W.k25(512)), ctx.describe_kernel(W.lbm15(256))
     gids = [ctx.describe_gpu(g) for g in sets]
-    cf = config_array(kid, 0, W.space_stencil_paper())
+    cf = np.concatenate([config_array(k25, 0, W.space_stencil_paper()), config_array(klbm, 0, W.space_lbm())])
     costs = [D.device_costs(ctx, cf, gids) if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(costs, src=0)
@@ -464,8 +466,8 @@ def configs3_strong_measure(ctx, stream, args, rank, world, dev):
     res = np.frombuffer(sw.result.cpu().numpy().tobytes(), dtype=RESULT_DTYPE)
     assert (res["status"] == 0).all() and len(res) == total
     loads = [sum(costs[0][i] for i in s) for s in sw.shards]
-    return {"workload": f"BJ configs[3]: 3D-25pt r4 512^3, 168 configs x {len(gids)} hardware sets (B200-like + "
-                        "hypothetical grid L1 x L2 x SM count), fixed total",
+    return {"workload": f"BJ configs[3]: (3D-25pt r4 512^3, 168 configs) u (LBM15 256^3, 49 configs) x {len(gids)} "
+                        "hardware sets (V100, A100, B200-like + hypothetical grid L1 x L2 x SM count), fixed total",
             "value": total / (ms / 1e3), "unit": "configs/s", "metric_unit_note": "one config = one (configuration, "
             "hardware set) estimate", "n_gpus": world, "scaling": "strong", "steps": steps, "ms_per_step": ms,
             "integer_groups_per_rank": groups, "gpu_launches_per_step": launches + 1,

@@ -753,7 +753,10 @@ __global__ void __launch_bounds__(128) k_instr(const DKernel* __restrict__ ks, D
   }
 }
 
-__global__ void __launch_bounds__(128) k_plan(const ws_config* __restrict__ cfgs, int n,
+#ifndef WS_PLAN_THREADS
+#define WS_PLAN_THREADS 128
+#endif
+__global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __restrict__ cfgs, int n,
                                               const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
                                               int ng, DPlan* __restrict__ plans, DInstr* __restrict__ instr,
                                               DRowInfo* __restrict__ rowinfo, unsigned long long* __restrict__ acc,
@@ -3458,7 +3461,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   const int persist = n_sm_dev * WS_PERSIST;
   cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
   beg(K_PLAN, m);
-  k_plan<<<n, 128, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
+  k_plan<<<n, WS_PLAN_THREADS, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
                            s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields, s.epoch,
                            s.rowtab, s.clist, s.clist_stride);  // its last CTA scans
   end(K_PLAN, m);

@@ -1,6 +1,6 @@
 """Rank-count invariance of the sharded sweep with the real estimator (SURVEY §4 layer 4, §8(e)):
 two processes on one GPU (gloo over host copies) run `ShardedSweep` over the configs[3]-shaped
-space (168 configurations x the 49 configs[3] hardware sets, 3D-25pt at 64^3) with the device-
+space (168 configurations x the 51 configs[3] hardware sets, 3D-25pt at 64^3) with the device-
 derived cost plan broadcast from rank 0; the gathered, ranked records must be byte-identical to a
 single rank's `ws_estimate_multi` + `ws_rank` of the same space."""
 import os

@@ -102,16 +102,16 @@ def test_describe_alignment_and_run_limits(ctx):
 
 
 def test_estimate_multi_byte_identical(ctx):
-    """configs[3]: the 168-config space at 96^3 x the 49 configs[3] hardware sets in one call ==
-    one ws_estimate per set (every byte of every record)."""
+    """configs[3]: [1] u [2] (the 168-config 25pt space and the 49 LBM15 configurations, two
+    kernels in one batch) at small sizes x the 51 configs[3] hardware sets in one call == one
+    ws_estimate per set (every byte of every record); six integer-stage groups."""
     from paper_2204_14242_b200 import config_array
-    k = W.k25(96)
     sets = W.hw_grid_configs3()
-    kid = ctx.describe_kernel(k)
+    k1, k2 = ctx.describe_kernel(W.k25(96)), ctx.describe_kernel(W.lbm15(24))
     gids = [ctx.describe_gpu(g) for g in sets]
-    cf = config_array(kid, 0, W.space_stencil_paper())
+    cf = np.concatenate([config_array(k1, 0, W.space_stencil_paper()), config_array(k2, 0, W.space_lbm())])
     multi = ctx.estimate_multi(cf, gids)
-    assert ctx.last_group_count() == 5
+    assert ctx.last_group_count() == 6
     for g, gid in enumerate(gids):
         cf["gpu_id"] = gid
         one = ctx.estimate(cf)
@@ -121,21 +121,25 @@ def test_estimate_multi_byte_identical(ctx):
 
 
 def test_estimate_multi_vs_oracle_sampled(ctx):
-    """configs[3] at the full 512^3 size: every configuration x the 49 hardware sets in one call;
-    sampled (configuration, set) pairs recomputed by the oracle."""
+    """configs[3] at the full sizes: the 25pt 512^3 space and LBM15 256^3 x the 51 hardware sets in
+    one call; sampled (configuration, set) pairs recomputed by the oracle."""
     from paper_2204_14242_b200 import config_array, result_dicts
-    k = W.k25(512)
     sets = W.hw_grid_configs3()
-    kid = ctx.describe_kernel(k)
+    kern = [W.k25(512), W.lbm15(256)]
+    kids = [ctx.describe_kernel(k) for k in kern]
     gids = [ctx.describe_gpu(g) for g in sets]
-    space = W.space_stencil_paper()
-    multi = ctx.estimate_multi(config_array(kid, 0, space), gids)
+    s25, slbm = W.space_stencil_paper(), W.space_lbm()
+    cf = np.concatenate([config_array(kids[0], 0, s25), config_array(kids[1], 0, slbm)])
+    which = [(0, c) for c in s25] + [(1, c) for c in slbm]
+    multi = ctx.estimate_multi(cf, gids)
     assert (multi["status"] == 0).all()
-    cheap = [i for i, c in enumerate(space) if c[0][2] == 1 and c[1][2] == 1]   # shallow: seconds each
-    picks = [(g, cheap[(5 * g) % len(cheap)]) for g in (0, 1, 7, 13, 26, 40, 48)]
+    cheap = [i for i, (ki, c) in enumerate(which) if c[0][2] == 1 and c[1][2] == 1 and (ki == 0 or c[0][0] >= 64)]
+    picks = [(g, cheap[(5 * g) % len(cheap)]) for g in (0, 1, 2, 7, 13, 26, 40, 50)]
+    picks += [(2, len(s25) + 2), (30, len(s25) + 40)]      # LBM15 configurations
     errs = []
     for g, i in picks:
-        o = O.estimate(k, sets[g], space[i])
+        ki, c = which[i]
+        o = O.estimate(kern[ki], sets[g], c)
         a = result_dicts(multi[g][i:i + 1])[0]
-        errs += compare(a, o, f"set{g} cfg{i} {space[i]}")
+        errs += compare(a, o, f"set{g} cfg{i} {c}")
     assert not errs, "\n".join(errs)

@@ -91,14 +91,15 @@ def gpu_hypothetical(l1_kib, l2_eff_mib, n_sm):
 
 
 def hw_grid_configs3(hbm_gbs=6546.2):
-    """BJ configs[3] architecture exploration: the B200-like set plus a hypothetical grid of
-    L1 {128, 192, 256} KiB x effective L2 {20, 40, 64, 126} MiB x SM count {108, 132, 148, 160}
-    (48 sets; P:307-320 parameter axes).  The integer stages depend only on the SM
-    count here (4 groups + the B200-like set's own)."""
-    sets = [gpu_b200_like(hbm_gbs)]
-    for nsm in (108, 132, 148, 160):
+    """BJ configs[3] architecture exploration: V100, A100 (Table tab:av100,
+    P:307-320), the B200-like set and the hypothetical grid L1 {128, 192, 256} KiB x effective L2
+    {6, 20, 40, 64} MiB x SM count {80, 108, 132, 148} (48 sets) = 51 hardware sets.  The integer
+    stages read only the SM count, occupancy limits, cache geometry and L2 sections of a set: six
+    groups (V100 with the 80-SM sets, A100, B200-like, the 108 / 132 / 148-SM sets)."""
+    sets = [gpu_v100(), gpu_a100(), gpu_b200_like(hbm_gbs)]
+    for nsm in (80, 108, 132, 148):
         for l1 in (128, 192, 256):
-            for l2 in (20, 40, 64, 126):
+            for l2 in (6, 20, 40, 64):
                 sets.append(gpu_hypothetical(l1, l2, nsm))
     return sets
 
