@@ -194,7 +194,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   const size_t o_sval = off;    off = align_up(off + (size_t)kShareTab * 2 * sizeof(unsigned long long));
   const size_t o_work = off;    off = align_up(off + 16 * sizeof(unsigned long long));
   static_assert(K_NKINDS <= 16, "work slots");
-  const size_t o_lists = off;   off = align_up(off + 4 * sizeof(unsigned long long));
+  const size_t o_lists = off;   off = align_up(off + 8 * sizeof(unsigned long long));
   const size_t o_wlist = off;   off = align_up(off + n * (size_t)kWSlots * sizeof(unsigned long long));
   const size_t o_slist = off;   off = align_up(off + n * (size_t)kSSlots * sizeof(unsigned long long));
   size_t max_nsm = 1;
@@ -203,6 +203,11 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   const size_t o_dlist = off;   off = align_up(off + n * max_nsm * 16 * sizeof(unsigned long long));
   const size_t o_dmask = off;   off = align_up(off + n * max_nsm * 16 * sizeof(unsigned int));
   const size_t o_gkey = off;    off = align_up(off + n * max_nsm * sizeof(unsigned long long));
+  const size_t cdesc_cap = n * (size_t)kCDescPerConfig, cpool_cap = n * (size_t)kCPoolPerConfig;
+  const size_t o_cdesc = off;   off = align_up(off + cdesc_cap * sizeof(CDesc));
+  const size_t o_cpool = off;   off = align_up(off + cpool_cap * 2 * 24);   // Tri pairs (3 x i64 each)
+  const size_t o_citems = off;  off = align_up(off + cpool_cap * sizeof(uint32_t));
+  const size_t o_cfb = off;     off = align_up(off + n * (size_t)kSSlots);
   const size_t o_clist = off;   off = align_up(off + max_chunks * sizeof(uint32_t));  // k_rows items per config
   if (bytes_only) {
     *bytes_only = off;
@@ -245,6 +250,12 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.dlist = (unsigned long long*)(b + o_dlist);
   s.dmask = (unsigned int*)(b + o_dmask);
   s.gkey = (unsigned long long*)(b + o_gkey);
+  s.cdesc = (void*)(b + o_cdesc);
+  s.cpool = (void*)(b + o_cpool);
+  s.citems = (uint32_t*)(b + o_citems);
+  s.cfb = (unsigned char*)(b + o_cfb);
+  s.cdesc_cap = (int64_t)cdesc_cap;
+  s.cpool_cap = (int64_t)cpool_cap;
   s.plan_done = (unsigned int*)(b + o_pdone);
   s.clist = (uint32_t*)(b + o_clist);
   s.clist_stride = (int64_t)cb;

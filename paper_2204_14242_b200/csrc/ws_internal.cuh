@@ -135,6 +135,15 @@ struct DPlan {
 constexpr int kRowTab = 4096;
 constexpr int kRowTabProbe = 64;
 
+// single-block SM-set class by computed planes: one descriptor per (class entry, load field)
+struct CDesc {
+  int32_t entry, c, field, per;
+  int32_t z0, np, y0, ny;
+  long long S0, off;  // the class block, the descriptor's first plane in the pool
+};
+constexpr int kCPoolPerConfig = 2048;   // plane pool (Tri pairs) per configuration
+constexpr int kCDescPerConfig = 64;     // descriptors per configuration
+
 // per-config accumulator slots (u64, atomically added by the worker kernels)
 enum {
   A_LUP = 0, A_WF, A_REQ_LD, A_REQ_ST, A_SM_SEC, A_SM_LIN,
@@ -181,6 +190,12 @@ struct Scratch {
   unsigned long long* dlist;  // multi-block SM sets evaluated directly: n * max n_sm * 16 entries
   unsigned int* dmask;        // per dlist entry: member mask of a connected component (0 = the set)
   unsigned long long* gkey;   // per SM set (pre.set order): k_spairs' translation-group key for k_smset
+  // single-block SM-set classes by computed planes (k_cplan / k_cplanes / k_cfold)
+  void* cdesc;                // CDesc[cdesc_cap]
+  void* cpool;                // Tri pairs [cpool_cap]
+  uint32_t* citems;           // computed-plane items [cpool_cap]
+  unsigned char* cfb;         // per class entry: 1 = evaluated by k_sclass (CTA path)
+  int64_t cdesc_cap, cpool_cap;
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
   unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)
   unsigned long long* rowtab; // kRowTab x 8 u64: a5/a6 sharing keys (see DPlan::row_owner)

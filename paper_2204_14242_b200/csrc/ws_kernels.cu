@@ -575,7 +575,7 @@ __device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __res
   __shared__ long long s_w[32][kNPrefix];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 16) work[tid] = 0ull;  // K_NKINDS <= 16
-  if (tid < 4) lists[tid] = 0ull;
+  if (tid < 8) lists[tid] = 0ull;  // [0..3] class / direct counters, [4..6] the class-plane path
   const int seg = (n + nt - 1) / nt;
   long long a[kNPrefix];
 #pragma unroll
@@ -2149,6 +2149,288 @@ __global__ void __launch_bounds__(kSmsetThreads) k_spairs(const DPlan* __restric
   }
 }
 
+// ---- single-block SM-set classes by computed planes (the class representatives' footprints,
+// a4): one warp per (class, load field, computed plane) instead of one CTA per class.
+//   k_cplan : one warp per class entry: per load field the footprint box (block box + the
+//             field's load-offset extremes), plane derivation (a plane whose every (group,
+//             block) membership equals the plane `per` below it is its translate by whole
+//             lines), a descriptor, a slice of the plane pool (derived planes marked), and one
+//             item per computed plane.  Entries the pool cannot hold, and blocks of kernels with
+//             many load fields (LBM: flat rows, smset_eval), stay on the CTA path (k_sclass).
+//   k_cplanes: one warp per item: the plane's runs (smset_run with the one block), its sector and
+//             line triples into the pool.
+//   k_cfold : one warp per descriptor: ordered fold over the box's planes (derived planes
+//             translated from their source), counts x class size into the configuration's
+//             accumulators; owners of shared classes accumulate the published counts.
+
+__device__ __forceinline__ bool cplane_derived(const DKernel& K, const DField& F, const SmBox32& b, int z, int z0,
+                                               int per) {
+  if (per <= 0 || z - per < z0) return false;
+  for (int g = F.g_begin; g < F.g_end; ++g) {
+    const DGroup gr = K.g[g];
+    if (gr.kind != 0) continue;
+    const int za = z - gr.oz, zb = za - per;
+    if ((za >= b.z0 && za < b.z1) != (zb >= b.z0 && zb < b.z1)) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ SmBox32 block_box32(const DPlan& P, long long B) {
+  const long long bc[3] = {B % P.G[0], (B / P.G[0]) % P.G[1], B / (P.G[0] * P.G[1])};
+  long long lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = P.lo[d] + bc[d] * P.BF[d];
+    hi[d] = lo[d] + P.BF[d];
+    if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
+  }
+  return SmBox32{(int)lo[0], (int)hi[0], (int)lo[1], (int)hi[1], (int)lo[2], (int)hi[2]};
+}
+
+__global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                               const DGpu* __restrict__ gs, const unsigned long long* __restrict__ lists,
+                                               const unsigned long long* __restrict__ slist,
+                                               const unsigned long long* __restrict__ srep,
+                                               unsigned long long* __restrict__ sval, unsigned char* __restrict__ cfb,
+                                               CDesc* __restrict__ cdesc, Tri* __restrict__ cpool,
+                                               uint32_t* __restrict__ citems, unsigned long long* __restrict__ cctr,
+                                               long long desc_cap, long long pool_cap) {
+  const int lane = threadIdx.x & 31;
+  const long long ncls = (long long)lists[1];
+  const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ncls; e += nwg) {
+    const unsigned long long ent = slist[e];
+    const int c = (int)(ent >> 32);
+    const unsigned low = (unsigned)(ent & 0xffffffffu);
+    if (low >> 31) continue;  // sharer: k_sshare adds the owner's counts
+    const DPlan& P = plans[c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    int n_ld = 0;
+    for (int f = 0; f < K.n_fields; ++f) n_ld += K.f[f].kinds & 1;
+    if (n_ld > 4) {  // many load fields: the CTA path's flat rows
+      if (lane == 0) cfb[e] = 1;
+      continue;
+    }
+    const long long S0 = (long long)srep[(long long)c * kSSlots + (low & 511u)];
+    const SmBox32 b = block_box32(P, S0);
+    const int ll = G.lg_line;
+    // pass 1: descriptors and pool slices (lane 0), or the CTA path when they do not fit
+    bool fits = true;
+    long long dbase = 0, pbase = 0;
+    int ndesc = 0, nplanes = 0;
+    if (lane == 0) {
+      for (int fi = 0; fi < K.n_fields; ++fi) {
+        const DField& F = K.f[fi];
+        if (!(F.kinds & 1)) continue;
+        int y0 = b.y0 + F.ld_oy_min, y1 = b.y1 + F.ld_oy_max, z0 = b.z0 + F.ld_oz_min, z1 = b.z1 + F.ld_oz_max;
+        y0 = y0 < 0 ? 0 : y0;
+        z0 = z0 < 0 ? 0 : z0;
+        y1 = y1 > (int)F.ext[1] ? (int)F.ext[1] : y1;
+        z1 = z1 > (int)F.ext[2] ? (int)F.ext[2] : z1;
+        if (y1 <= y0 || z1 <= z0) continue;
+        ++ndesc;
+        nplanes += z1 - z0;
+        if (z1 - z0 > 4096) fits = false;   // item code: plane index in 12 bits
+      }
+      dbase = (long long)atomicAdd(cctr + 0, (unsigned long long)ndesc);
+      pbase = (long long)atomicAdd(cctr + 1, (unsigned long long)nplanes);
+      fits = fits && dbase + ndesc <= desc_cap && dbase + ndesc <= (1 << 20) && pbase + nplanes <= pool_cap;
+      cfb[e] = fits ? 0 : 1;
+      if (fits && ((low >> 30) & 1u)) {  // owner of a shared class: k_cfold accumulates the counts
+        const unsigned t = (low >> 9) & (kShareTab - 1);
+        sval[2 * t] = 0ull;
+        sval[2 * t + 1] = 0ull;
+      }
+    }
+    fits = __shfl_sync(FULL, fits, 0);
+    if (!fits) continue;
+    dbase = __shfl_sync(FULL, dbase, 0);
+    pbase = __shfl_sync(FULL, pbase, 0);
+    // pass 2: per load field, the descriptor, derived-plane marks and the computed-plane items
+    for (int fi = 0; fi < K.n_fields; ++fi) {
+      const DField& F = K.f[fi];
+      if (!(F.kinds & 1)) continue;
+      int y0 = b.y0 + F.ld_oy_min, y1 = b.y1 + F.ld_oy_max, z0 = b.z0 + F.ld_oz_min, z1 = b.z1 + F.ld_oz_max;
+      y0 = y0 < 0 ? 0 : y0;
+      z0 = z0 < 0 ? 0 : z0;
+      y1 = y1 > (int)F.ext[1] ? (int)F.ext[1] : y1;
+      z1 = z1 > (int)F.ext[2] ? (int)F.ext[2] : z1;
+      if (y1 <= y0 || z1 <= z0) continue;
+      const int per = plane_period(F.pitch[2], F.lg_elem, ll);
+      const int np = z1 - z0;
+      if (lane == 0) cdesc[dbase] = CDesc{(int)e, c, fi, per, z0, np, y0, y1 - y0, S0, pbase};
+      // windows of 32 planes (a multiple of per, a power of two <= 16): lane L's planes all have
+      // the residue L mod per, so its derived planes' source -- the last computed plane of that
+      // residue -- is carried across windows per lane
+      const unsigned same_res = per > 0 ? (0xffffffffu / ((1u << per) - 1u)) << (lane % per) : 0u;  // residue mask
+      int carry = -1;
+      for (int w0 = 0; w0 < np; w0 += 32) {
+        const int p = w0 + lane;
+        const bool in = p < np;
+        const bool der = in && cplane_derived(K, F, b, z0 + p, z0, per);
+        const unsigned m = __ballot_sync(FULL, in && !der);   // computed planes of the window
+        if (der) {
+          const unsigned below = m & same_res & ((lane ? (1u << lane) : 1u) - 1u);
+          const int src = below ? w0 + 31 - __clz(below) : carry;
+          cpool[2 * (pbase + p)].c = -2 - (long long)src;  // derived: its computed source plane
+        }
+        if (in && !der) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long at = 0;
+          if (lane == leader) at = atomicAdd(cctr + 2, (unsigned long long)__popc(m));
+          at = __shfl_sync(m, at, leader);
+          citems[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)dbase | ((uint32_t)p << 20);
+        }
+        const unsigned mr = m & same_res;
+        if (mr) carry = w0 + 31 - __clz(mr);
+      }
+      ++dbase;
+      pbase += np;
+    }
+  }
+}
+
+// one warp per item (descriptor 20 bits | plane 12 bits): the computed plane's runs
+__global__ void __launch_bounds__(256) k_cplanes(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                                 const DGpu* __restrict__ gs, const CDesc* __restrict__ cdesc,
+                                                 Tri* __restrict__ cpool, const uint32_t* __restrict__ citems,
+                                                 const unsigned long long* __restrict__ cctr,
+                                                 unsigned long long* __restrict__ work) {
+  __shared__ SmWarp s_sw[8];
+  __shared__ SmBox32 s_mb[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long total = (long long)cctr[2];
+  const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
+  unsigned long long units = 0;
+  for (long long it = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total; it += nwg) {
+    const uint32_t code = citems[it];
+    const CDesc D = cdesc[code & 0xfffffu];
+    const int p = (int)(code >> 20);
+    const DPlan& P = plans[D.c];
+    const DKernel& K = ks[P.kid];
+    const DGpu& G = gs[P.gid];
+    const DField& F = K.f[D.field];
+    const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
+    const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
+    if (lane == 0) s_mb[wid] = block_box32(P, D.S0);
+    __syncwarp();
+    SmWarp& Wp = s_sw[wid];
+    const int z = D.z0 + p, y0 = D.y0, ny = D.ny;
+    const long long py = F.pitch[1], pz = F.pitch[2];
+    const long long R0p = F.align + ((py * y0 + pz * (long long)z) << le);
+    const long long Bp = (R0p >> ll) << ll;
+    const int off0 = (int)(R0p - Bp), step = (int)(py << le);
+    T32 ps = t32_empty(), pl = t32_empty();
+    for (int ys = 0; ys < ny; ys += kSegRowsS) {
+      const int nseg = ny - ys < kSegRowsS ? ny - ys : kSegRowsS;
+      const int nwd = (nseg + 31) >> 5;
+      for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
+      __syncwarp();
+      if (lane == 0) atomicOr(&Wp.bm[0], 1u);
+      const SmBox32& bx = s_mb[wid];
+      for (int k = lane; k < ng; k += 32) {  // breakpoints: rows where a group's row enters / leaves the block
+        const DGroup gr = K.g[g0 + k];
+        if (gr.kind != 0) continue;
+        const int zz = z - gr.oz;
+        if (zz < bx.z0 || zz >= bx.z1) continue;
+        const int e0 = bx.y0 + gr.oy - y0 - ys, e1 = bx.y1 + gr.oy - y0 - ys;
+        if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
+        if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
+      }
+      __syncwarp();
+      const int wpl = (nwd + 31) >> 5;
+      int cnt = 0;
+      for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) cnt += __popc(Wp.bm[w]);
+      int pos = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, pos, o);
+        if (lane >= o) pos += v;
+      }
+      const int nruns = __shfl_sync(FULL, pos, 31);
+      pos -= cnt;
+      for (int w = lane * wpl; w < nwd && w < (lane + 1) * wpl; ++w) {
+        unsigned bits = Wp.bm[w];
+        while (bits) {
+          const int bt = __ffs(bits) - 1;
+          bits &= bits - 1;
+          Wp.rs[pos++] = (short)(w * 32 + bt);
+        }
+      }
+      if (lane == 0) Wp.rs[nruns] = (short)nseg;
+      __syncwarp();
+      for (int rb = 0; rb < nruns; rb += 32) {
+        T32 tt[2] = {t32_empty(), t32_empty()};
+        const int j = rb + lane;
+        if (j < nruns) {
+          const int yr = ys + Wp.rs[j];
+          const T32x2 o = smset_run(&bx, 1, K, F, g0, ng, y0 + yr, z, off0 + yr * step, step, Wp.rs[j + 1] - Wp.rs[j],
+                                    le, ls, ll);
+          tt[0] = o.s;
+          tt[1] = o.l;
+        }
+        warp_ordered_reduce32<2>(tt, nruns - rb);
+        if (lane == 0) {
+          ps = t32_combine(ps, tt[0]);
+          pl = t32_combine(pl, tt[1]);
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const long long bs = Bp >> ls, bl = Bp >> ll;
+      cpool[2 * (D.off + p)] = ps.c ? Tri{ps.f + bs, ps.l + bs, ps.c} : tri_empty();
+      cpool[2 * (D.off + p) + 1] = pl.c ? Tri{pl.f + bl, pl.l + bl, pl.c} : tri_empty();
+      units += (unsigned long long)ny;
+    }
+  }
+  if (lane == 0 && units) atomicAdd(work + K_SCLASS, units);
+}
+
+// one warp per descriptor: ordered fold of the box's planes, counts x class size
+__global__ void __launch_bounds__(256) k_cfold(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
+                                               const DGpu* __restrict__ gs, const unsigned long long* __restrict__ slist,
+                                               const unsigned int* __restrict__ scnt, const CDesc* __restrict__ cdesc,
+                                               const Tri* __restrict__ cpool, const unsigned long long* __restrict__ cctr,
+                                               unsigned long long* __restrict__ acc, unsigned long long* __restrict__ sval) {
+  const int lane = threadIdx.x & 31;
+  const long long total = (long long)cctr[0];
+  const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long d = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; d < total; d += nwg) {
+    const CDesc D = cdesc[d];
+    const DPlan& P = plans[D.c];
+    const DField& F = ks[P.kid].f[D.field];
+    const DGpu& G = gs[P.gid];
+    const int ls = G.lg_sector, ll = G.lg_line;
+    const long long pbytes = F.pitch[2] << F.lg_elem;
+    const int ppl = (D.np + 31) / 32;
+    Tri t[2] = {tri_empty(), tri_empty()};
+    for (int p = lane * ppl; p < D.np && p < (lane + 1) * ppl; ++p) {
+      int q = p;
+      const long long mk = cpool[2 * (D.off + p)].c;
+      if (mk < 0) q = (int)(-mk - 2);   // derived: its computed source plane (k_cplan)
+      const long long dsh = (long long)(p - q) * pbytes;
+      const Tri a = cpool[2 * (D.off + q)], bl = cpool[2 * (D.off + q) + 1];
+      t[0] = tri_combine(t[0], a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty());
+      t[1] = tri_combine(t[1], bl.c ? Tri{bl.f + (dsh >> ll), bl.l + (dsh >> ll), bl.c} : tri_empty());
+    }
+    warp_ordered_reduce<2>(t);
+    if (lane == 0) {
+      const unsigned long long ent = slist[D.entry];
+      const unsigned low = (unsigned)(ent & 0xffffffffu);
+      const unsigned long long mult = scnt[(long long)D.c * kSSlots + (low & 511u)];
+      unsigned long long* a = acc + (long long)D.c * A_N;
+      atomicAdd(a + A_SM_SEC, (unsigned long long)t[0].c * mult);
+      atomicAdd(a + A_SM_LIN, (unsigned long long)t[1].c * mult);
+      if ((low >> 30) & 1u) {  // owner of a shared class: the class's counts (over its load fields)
+        const unsigned tt = (low >> 9) & (kShareTab - 1);
+        atomicAdd(sval + 2 * tt, (unsigned long long)t[0].c);
+        atomicAdd(sval + 2 * tt + 1, (unsigned long long)t[1].c);
+      }
+    }
+  }
+}
+
 // Pass 2 (one CTA per entry): class representatives (counted class-size times), then the
 // directly evaluated multi-block SM sets.
 #ifdef WS_SCLASS_TRACE
@@ -2163,7 +2445,8 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
                                                 const unsigned long long* __restrict__ dlist,
                                                 unsigned long long* __restrict__ work,
                                                 unsigned long long* __restrict__ sval,
-                                                const unsigned int* __restrict__ dmask) {
+                                                const unsigned int* __restrict__ dmask,
+                                                const unsigned char* __restrict__ cfb) {
   __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ SmBox32 s_mb32[kMaxMembers];
@@ -2198,6 +2481,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     long long S0, kj;
     unsigned msk = 0u;  // direct item of one connected component of a set (k_smset)
     if (cls && (low >> 31)) continue;  // shared class: k_sshare adds the owner's counts
+    if (cls && cfb && !cfb[item - ndir]) continue;  // evaluated by k_cplan / k_cplanes / k_cfold
     if (cls) {
       const long long gslot = (long long)c * kSSlots + (low & 511u);
       mult = scnt[gslot];
@@ -3488,8 +3772,20 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   ++L;
   end(K_SMSET, a);
   beg(K_SCLASS, a);
+  static const bool cplanes = !(getenv("WS_CPLANES") && getenv("WS_CPLANES")[0] == '0');  // A/B, diagnostics
+  if (cplanes) {  // single-block classes by computed planes
+    CDesc* cd = (CDesc*)s.cdesc;
+    Tri* cp = (Tri*)s.cpool;
+    unsigned long long* cctr = s.lists + 4;  // descriptors, pool planes, items (zeroed with the lists)
+    k_cplan<<<n_sm_dev * 4, 256, 0, a>>>(s.plans, d_k, d_g, s.lists, s.slist, s.srep, s.sval, s.cfb, cd, cp, s.citems,
+                                         cctr, s.cdesc_cap, s.cpool_cap);
+    k_cplanes<<<n_sm_dev * 8, 256, 0, a>>>(s.plans, d_k, d_g, cd, cp, s.citems, cctr, s.work);
+    k_cfold<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, d_k, d_g, s.slist, s.scnt, cd, cp, cctr, s.acc, s.sval);
+    L += 3;
+  }
   k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
-                                                                     s.slist, s.dlist, s.work, s.sval, s.dmask);
+                                                                     s.slist, s.dlist, s.work, s.sval, s.dmask,
+                                                                     cplanes ? s.cfb : nullptr);
   k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
 #ifdef WS_SCLASS_TRACE
   k_sctrace_dump<<<1, 1, 0, a>>>(s.lists, s.plans);
