@@ -207,7 +207,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   const size_t o_cdesc = off;   off = align_up(off + cdesc_cap * sizeof(CDesc));
   const size_t o_cpool = off;   off = align_up(off + cpool_cap * 2 * 24);   // Tri pairs (3 x i64 each)
   const size_t o_citems = off;  off = align_up(off + cpool_cap * sizeof(uint32_t));
-  const size_t o_cfb = off;     off = align_up(off + n * (size_t)kSSlots);
+  const size_t o_cfb = off;     off = align_up(off + n * (size_t)kSSlots * sizeof(uint32_t));
   const size_t o_clist = off;   off = align_up(off + max_chunks * sizeof(uint32_t));  // k_rows items per config
   if (bytes_only) {
     *bytes_only = off;
@@ -253,7 +253,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.cdesc = (void*)(b + o_cdesc);
   s.cpool = (void*)(b + o_cpool);
   s.citems = (uint32_t*)(b + o_citems);
-  s.cfb = (unsigned char*)(b + o_cfb);
+  s.cfbl = (uint32_t*)(b + o_cfb);
   s.cdesc_cap = (int64_t)cdesc_cap;
   s.cpool_cap = (int64_t)cpool_cap;
   s.plan_done = (unsigned int*)(b + o_pdone);

@@ -140,6 +140,8 @@ struct CDesc {
   int32_t entry, c, field, per;
   int32_t z0, np, y0, ny;
   long long S0, off;  // the class block, the descriptor's first plane in the pool
+  int32_t box[6];     // the block's cell box x0, x1, y0, y1, z0, z1 (k_cplanes' member box)
+  int32_t pad[2];
 };
 constexpr int kCPoolPerConfig = 2048;   // plane pool (Tri pairs) per configuration
 constexpr int kCDescPerConfig = 64;     // descriptors per configuration
@@ -194,7 +196,7 @@ struct Scratch {
   void* cdesc;                // CDesc[cdesc_cap]
   void* cpool;                // Tri pairs [cpool_cap]
   uint32_t* citems;           // computed-plane items [cpool_cap]
-  unsigned char* cfb;         // per class entry: 1 = evaluated by k_sclass (CTA path)
+  uint32_t* cfbl;             // class entries k_cplan leaves to k_sclass (CTA path)
   int64_t cdesc_cap, cpool_cap;
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
   unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)

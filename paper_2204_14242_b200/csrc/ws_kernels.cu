@@ -2186,11 +2186,25 @@ __device__ __forceinline__ SmBox32 block_box32(const DPlan& P, long long B) {
   return SmBox32{(int)lo[0], (int)hi[0], (int)lo[1], (int)hi[1], (int)lo[2], (int)hi[2]};
 }
 
+// field fi's footprint box of block box b (rows y0..y1, planes z0..z1, clipped to the field)
+__device__ __forceinline__ bool cfield_box(const DField& F, const SmBox32& b, int& y0, int& y1, int& z0, int& z1) {
+  y0 = b.y0 + F.ld_oy_min;
+  y1 = b.y1 + F.ld_oy_max;
+  z0 = b.z0 + F.ld_oz_min;
+  z1 = b.z1 + F.ld_oz_max;
+  y0 = y0 < 0 ? 0 : y0;
+  z0 = z0 < 0 ? 0 : z0;
+  y1 = y1 > (int)F.ext[1] ? (int)F.ext[1] : y1;
+  z1 = z1 > (int)F.ext[2] ? (int)F.ext[2] : z1;
+  return y1 > y0 && z1 > z0 && (F.kinds & 1);
+}
+
+// cctr: [0] descriptors << 40 | pool planes (one atomic per class entry), [1] items, [2] CTA-path entries
 __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, const DKernel* __restrict__ ks,
                                                const DGpu* __restrict__ gs, const unsigned long long* __restrict__ lists,
                                                const unsigned long long* __restrict__ slist,
                                                const unsigned long long* __restrict__ srep,
-                                               unsigned long long* __restrict__ sval, unsigned char* __restrict__ cfb,
+                                               unsigned long long* __restrict__ sval, uint32_t* __restrict__ cfbl,
                                                CDesc* __restrict__ cdesc, Tri* __restrict__ cpool,
                                                uint32_t* __restrict__ citems, unsigned long long* __restrict__ cctr,
                                                long long desc_cap, long long pool_cap) {
@@ -2205,64 +2219,62 @@ __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, 
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
-    int n_ld = 0;
-    for (int f = 0; f < K.n_fields; ++f) n_ld += K.f[f].kinds & 1;
-    if (n_ld > 4) {  // many load fields: the CTA path's flat rows
-      if (lane == 0) cfb[e] = 1;
-      continue;
-    }
     const long long S0 = (long long)srep[(long long)c * kSSlots + (low & 511u)];
     const SmBox32 b = block_box32(P, S0);
     const int ll = G.lg_line;
-    // pass 1: descriptors and pool slices (lane 0), or the CTA path when they do not fit
+    // descriptors and pool planes of the entry: lanes over fields, one packed atomic
+    int ndesc = 0, nplanes = 0, n_ld = 0;
     bool fits = true;
-    long long dbase = 0, pbase = 0;
-    int ndesc = 0, nplanes = 0;
-    if (lane == 0) {
-      for (int fi = 0; fi < K.n_fields; ++fi) {
-        const DField& F = K.f[fi];
-        if (!(F.kinds & 1)) continue;
-        int y0 = b.y0 + F.ld_oy_min, y1 = b.y1 + F.ld_oy_max, z0 = b.z0 + F.ld_oz_min, z1 = b.z1 + F.ld_oz_max;
-        y0 = y0 < 0 ? 0 : y0;
-        z0 = z0 < 0 ? 0 : z0;
-        y1 = y1 > (int)F.ext[1] ? (int)F.ext[1] : y1;
-        z1 = z1 > (int)F.ext[2] ? (int)F.ext[2] : z1;
-        if (y1 <= y0 || z1 <= z0) continue;
-        ++ndesc;
-        nplanes += z1 - z0;
-        if (z1 - z0 > 4096) fits = false;   // item code: plane index in 12 bits
-      }
-      dbase = (long long)atomicAdd(cctr + 0, (unsigned long long)ndesc);
-      pbase = (long long)atomicAdd(cctr + 1, (unsigned long long)nplanes);
-      fits = fits && dbase + ndesc <= desc_cap && dbase + ndesc <= (1 << 20) && pbase + nplanes <= pool_cap;
-      cfb[e] = fits ? 0 : 1;
-      if (fits && ((low >> 30) & 1u)) {  // owner of a shared class: k_cfold accumulates the counts
-        const unsigned t = (low >> 9) & (kShareTab - 1);
-        sval[2 * t] = 0ull;
-        sval[2 * t + 1] = 0ull;
-      }
+    for (int fi = lane; fi < K.n_fields; fi += 32) {
+      const DField& F = K.f[fi];
+      n_ld += F.kinds & 1;
+      int y0, y1, z0, z1;
+      if (!cfield_box(F, b, y0, y1, z0, z1)) continue;
+      ++ndesc;
+      nplanes += z1 - z0;
+      if (z1 - z0 > 4096) fits = false;   // item code: plane index in 12 bits
     }
-    fits = __shfl_sync(FULL, fits, 0);
-    if (!fits) continue;
-    dbase = __shfl_sync(FULL, dbase, 0);
-    pbase = __shfl_sync(FULL, pbase, 0);
-    // pass 2: per load field, the descriptor, derived-plane marks and the computed-plane items
+    ndesc = __reduce_add_sync(FULL, ndesc);
+    nplanes = __reduce_add_sync(FULL, nplanes);
+    n_ld = __reduce_add_sync(FULL, n_ld);
+    fits = __all_sync(FULL, fits) && n_ld <= 4;   // many load fields: the CTA path's flat rows
+    unsigned long long base = 0;
+    if (fits && lane == 0) base = atomicAdd(cctr + 0, ((unsigned long long)ndesc << 40) | (unsigned long long)nplanes);
+    base = __shfl_sync(FULL, base, 0);
+    long long dbase = (long long)(base >> 40), pbase = (long long)(base & ((1ull << 40) - 1));
+    fits = fits && dbase + ndesc <= desc_cap && dbase + ndesc <= (1 << 20) && pbase + nplanes <= pool_cap;
+    if (!fits) {
+      if (lane == 0) cfbl[atomicAdd(cctr + 2, 1ull)] = (uint32_t)e;
+      continue;
+    }
+    if (lane == 0 && ((low >> 30) & 1u)) {  // owner of a shared class: k_cfold accumulates the counts
+      const unsigned t = (low >> 9) & (kShareTab - 1);
+      sval[2 * t] = 0ull;
+      sval[2 * t + 1] = 0ull;
+    }
+    // per load field: the descriptor, derived planes' sources, the computed-plane items
     for (int fi = 0; fi < K.n_fields; ++fi) {
       const DField& F = K.f[fi];
-      if (!(F.kinds & 1)) continue;
-      int y0 = b.y0 + F.ld_oy_min, y1 = b.y1 + F.ld_oy_max, z0 = b.z0 + F.ld_oz_min, z1 = b.z1 + F.ld_oz_max;
-      y0 = y0 < 0 ? 0 : y0;
-      z0 = z0 < 0 ? 0 : z0;
-      y1 = y1 > (int)F.ext[1] ? (int)F.ext[1] : y1;
-      z1 = z1 > (int)F.ext[2] ? (int)F.ext[2] : z1;
-      if (y1 <= y0 || z1 <= z0) continue;
+      int y0, y1, z0, z1;
+      if (!cfield_box(F, b, y0, y1, z0, z1)) continue;
       const int per = plane_period(F.pitch[2], F.lg_elem, ll);
       const int np = z1 - z0;
-      if (lane == 0) cdesc[dbase] = CDesc{(int)e, c, fi, per, z0, np, y0, y1 - y0, S0, pbase};
+      if (lane == 0) {
+        CDesc d{(int)e, c, fi, per, z0, np, y0, y1 - y0, S0, pbase, {b.x0, b.x1, b.y0, b.y1, b.z0, b.z1}, {0, 0}};
+        cdesc[dbase] = d;
+      }
       // windows of 32 planes (a multiple of per, a power of two <= 16): lane L's planes all have
       // the residue L mod per, so its derived planes' source -- the last computed plane of that
       // residue -- is carried across windows per lane
-      const unsigned same_res = per > 0 ? (0xffffffffu / ((1u << per) - 1u)) << (lane % per) : 0u;  // residue mask
+      const unsigned same_res = per > 0 ? (0xffffffffu / ((1u << per) - 1u)) << (lane % per) : 0u;
+      int ncomp = 0;
+      for (int w0 = 0; w0 < np; w0 += 32) {  // count the computed planes (one item atomic per field)
+        const int p = w0 + lane;
+        ncomp += __popc(__ballot_sync(FULL, p < np && !cplane_derived(K, F, b, z0 + p, z0, per)));
+      }
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(cctr + 1, (unsigned long long)ncomp);
+      at = __shfl_sync(FULL, at, 0);
       int carry = -1;
       for (int w0 = 0; w0 < np; w0 += 32) {
         const int p = w0 + lane;
@@ -2270,17 +2282,12 @@ __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, 
         const bool der = in && cplane_derived(K, F, b, z0 + p, z0, per);
         const unsigned m = __ballot_sync(FULL, in && !der);   // computed planes of the window
         if (der) {
-          const unsigned below = m & same_res & ((lane ? (1u << lane) : 1u) - 1u);
+          const unsigned below = m & same_res & ((1u << lane) - 1u);
           const int src = below ? w0 + 31 - __clz(below) : carry;
           cpool[2 * (pbase + p)].c = -2 - (long long)src;  // derived: its computed source plane
         }
-        if (in && !der) {
-          const int leader = __ffs(m) - 1;
-          unsigned long long at = 0;
-          if (lane == leader) at = atomicAdd(cctr + 2, (unsigned long long)__popc(m));
-          at = __shfl_sync(m, at, leader);
-          citems[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)dbase | ((uint32_t)p << 20);
-        }
+        if (in && !der) citems[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)dbase | ((uint32_t)p << 20);
+        at += __popc(m);
         const unsigned mr = m & same_res;
         if (mr) carry = w0 + 31 - __clz(mr);
       }
@@ -2299,7 +2306,7 @@ __global__ void __launch_bounds__(256) k_cplanes(const DPlan* __restrict__ plans
   __shared__ SmWarp s_sw[8];
   __shared__ SmBox32 s_mb[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long total = (long long)cctr[2];
+  const long long total = (long long)cctr[1];
   const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
   unsigned long long units = 0;
   for (long long it = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total; it += nwg) {
@@ -2312,7 +2319,7 @@ __global__ void __launch_bounds__(256) k_cplanes(const DPlan* __restrict__ plans
     const DField& F = K.f[D.field];
     const int ls = G.lg_sector, ll = G.lg_line, le = F.lg_elem;
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
-    if (lane == 0) s_mb[wid] = block_box32(P, D.S0);
+    if (lane == 0) s_mb[wid] = SmBox32{D.box[0], D.box[1], D.box[2], D.box[3], D.box[4], D.box[5]};
     __syncwarp();
     SmWarp& Wp = s_sw[wid];
     const int z = D.z0 + p, y0 = D.y0, ny = D.ny;
@@ -2394,7 +2401,7 @@ __global__ void __launch_bounds__(256) k_cfold(const DPlan* __restrict__ plans, 
                                                const Tri* __restrict__ cpool, const unsigned long long* __restrict__ cctr,
                                                unsigned long long* __restrict__ acc, unsigned long long* __restrict__ sval) {
   const int lane = threadIdx.x & 31;
-  const long long total = (long long)cctr[0];
+  const long long total = (long long)(cctr[0] >> 40);
   const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long d = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; d < total; d += nwg) {
     const CDesc D = cdesc[d];
@@ -2446,7 +2453,8 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
                                                 unsigned long long* __restrict__ work,
                                                 unsigned long long* __restrict__ sval,
                                                 const unsigned int* __restrict__ dmask,
-                                                const unsigned char* __restrict__ cfb) {
+                                                const uint32_t* __restrict__ cfbl,
+                                                const unsigned long long* __restrict__ cctr) {
   __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ SmBox32 s_mb32[kMaxMembers];
@@ -2457,8 +2465,10 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
   __shared__ int s_ng;
   __shared__ long long s_box[4];
   __shared__ Tri s_red[(WS_SCLASS_THREADS / 32) * 2];
-  const long long ncls = (long long)lists[1], ndir = (long long)lists[2];
+  // class entries: all of them, or (class-plane path) only those k_cplan left to the CTA path
+  const long long ncls = cfbl ? (long long)cctr[2] : (long long)lists[1], ndir = (long long)lists[2];
   const long long total = ncls + ndir;
+  if (total == 0) return;  // nothing for the CTA path (e.g. every SM set one block, classes by planes)
   // dynamic scheduling (lists[3], zeroed by the plan's scan): the directly evaluated sets --
   // the expensive, uneven entries -- first, then the single-block class representatives
   for (;;) {
@@ -2471,7 +2481,8 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     const long long t_item0 = clock64();
 #endif
     const bool cls = item >= ndir;
-    const unsigned long long ent = cls ? slist[item - ndir] : dlist[item];
+    const long long ce = cls ? (cfbl ? (long long)cfbl[item - ndir] : item - ndir) : 0;
+    const unsigned long long ent = cls ? slist[ce] : dlist[item];
     const int c = (int)(ent >> 32);
     const unsigned low = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
@@ -2481,7 +2492,6 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     long long S0, kj;
     unsigned msk = 0u;  // direct item of one connected component of a set (k_smset)
     if (cls && (low >> 31)) continue;  // shared class: k_sshare adds the owner's counts
-    if (cls && cfb && !cfb[item - ndir]) continue;  // evaluated by k_cplan / k_cplanes / k_cfold
     if (cls) {
       const long long gslot = (long long)c * kSSlots + (low & 511u);
       mult = scnt[gslot];
@@ -3777,7 +3787,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     CDesc* cd = (CDesc*)s.cdesc;
     Tri* cp = (Tri*)s.cpool;
     unsigned long long* cctr = s.lists + 4;  // descriptors, pool planes, items (zeroed with the lists)
-    k_cplan<<<n_sm_dev * 4, 256, 0, a>>>(s.plans, d_k, d_g, s.lists, s.slist, s.srep, s.sval, s.cfb, cd, cp, s.citems,
+    k_cplan<<<n_sm_dev * 4, 256, 0, a>>>(s.plans, d_k, d_g, s.lists, s.slist, s.srep, s.sval, s.cfbl, cd, cp, s.citems,
                                          cctr, s.cdesc_cap, s.cpool_cap);
     k_cplanes<<<n_sm_dev * 8, 256, 0, a>>>(s.plans, d_k, d_g, cd, cp, s.citems, cctr, s.work);
     k_cfold<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, d_k, d_g, s.slist, s.scnt, cd, cp, cctr, s.acc, s.sval);
@@ -3785,7 +3795,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   }
   k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
                                                                      s.slist, s.dlist, s.work, s.sval, s.dmask,
-                                                                     cplanes ? s.cfb : nullptr);
+                                                                     cplanes ? s.cfbl : nullptr, s.lists + 4);
   k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
 #ifdef WS_SCLASS_TRACE
   k_sctrace_dump<<<1, 1, 0, a>>>(s.lists, s.plans);
