@@ -66,6 +66,12 @@ namespace wsb {
 
 #define FULL 0xffffffffu
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-serialization
+// attribute starts while its predecessor in the stream finishes; griddepcontrol.wait blocks until
+// the predecessor grid has completed and its memory is visible (a no-op for ordinary launches),
+// launch_dependents lets this grid's own dependent start its prologue early.
+#define PDL_PROLOGUE() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ long long shfl64(long long v, int src) {
   int lo = __shfl_sync(FULL, (int)(v & 0xffffffffll), src);
@@ -636,6 +642,7 @@ __device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __res
 // the key).  More than kMaxInstr instructions: istat = WS_ELIMIT (k_model reports it).
 __global__ void __launch_bounds__(128) k_instr(const DKernel* __restrict__ ks, DPlan* __restrict__ plans,
                                                DInstr* __restrict__ instr, unsigned int* __restrict__ wcnt, int n) {
+  PDL_PROLOGUE();
   const int c = blockIdx.x, tid = threadIdx.x;
   {  // this configuration's warp-class counters (k_warp)
     uint4* wc = reinterpret_cast<uint4*>(wcnt + (long long)c * kWSlots);
@@ -1112,6 +1119,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
                                               unsigned long long* __restrict__ lists,
                                               unsigned long long* __restrict__ wlist,
                                               unsigned long long* __restrict__ work) {
+  PDL_PROLOGUE();
   const long long total = pre[n].warp;
   const int lane = threadIdx.x & 31;
   unsigned long long my_units = 0;
@@ -1217,6 +1225,7 @@ __global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans,
                                                 const unsigned long long* __restrict__ lists,
                                                 const unsigned long long* __restrict__ wlist,
                                                 unsigned long long* __restrict__ work) {
+  PDL_PROLOGUE();
   const long long total = (long long)lists[0];
   const int lane = threadIdx.x & 31;
   unsigned long long my_units = 0;
@@ -1957,6 +1966,7 @@ __global__ void __launch_bounds__(kSmsetThreads) k_smset(const DPlan* __restrict
                                                unsigned long long* __restrict__ skey,
                                                unsigned int* __restrict__ dmask,
                                                const unsigned long long* __restrict__ gkey) {
+  PDL_PROLOGUE();
   __shared__ unsigned long long s_key[kSetGrp];  // directly evaluated sets: shape key (0: not grouped)
   __shared__ unsigned s_cnt[kSetGrp];            // group sizes (at the group's smallest member)
   __shared__ short s_rep[kSetGrp];               // smallest member of the set's group
@@ -2049,6 +2059,7 @@ __global__ void __launch_bounds__(kSmsetThreads) k_spairs(const DPlan* __restric
                                                 unsigned long long* __restrict__ dlist,
                                                 unsigned long long* __restrict__ skey, unsigned int* __restrict__ dmask,
                                                 unsigned long long* __restrict__ gkey) {
+  PDL_PROLOGUE();
   __shared__ long long s_mbox[kSmsetThreads / 32][32 * 6];  // member boxes of a warp's set
   __shared__ unsigned s_adj[kSmsetThreads / 32][32];        // non-separated pairs, row a1 bit b1
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2208,6 +2219,7 @@ __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, 
                                                CDesc* __restrict__ cdesc, Tri* __restrict__ cpool,
                                                uint32_t* __restrict__ citems, unsigned long long* __restrict__ cctr,
                                                long long desc_cap, long long pool_cap) {
+  PDL_PROLOGUE();
   const int lane = threadIdx.x & 31;
   const long long ncls = (long long)lists[1];
   const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -2303,6 +2315,7 @@ __global__ void __launch_bounds__(256) k_cplanes(const DPlan* __restrict__ plans
                                                  Tri* __restrict__ cpool, const uint32_t* __restrict__ citems,
                                                  const unsigned long long* __restrict__ cctr,
                                                  unsigned long long* __restrict__ work) {
+  PDL_PROLOGUE();
   __shared__ SmWarp s_sw[8];
   __shared__ SmBox32 s_mb[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2400,6 +2413,7 @@ __global__ void __launch_bounds__(256) k_cfold(const DPlan* __restrict__ plans, 
                                                const unsigned int* __restrict__ scnt, const CDesc* __restrict__ cdesc,
                                                const Tri* __restrict__ cpool, const unsigned long long* __restrict__ cctr,
                                                unsigned long long* __restrict__ acc, unsigned long long* __restrict__ sval) {
+  PDL_PROLOGUE();
   const int lane = threadIdx.x & 31;
   const long long total = (long long)(cctr[0] >> 40);
   const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -2455,6 +2469,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
                                                 const unsigned int* __restrict__ dmask,
                                                 const uint32_t* __restrict__ cfbl,
                                                 const unsigned long long* __restrict__ cctr) {
+  PDL_PROLOGUE();
   __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
   __shared__ SmBox32 s_mb32[kMaxMembers];
@@ -2560,6 +2575,7 @@ __global__ void __launch_bounds__(256) k_sshare(const unsigned long long* __rest
                                                 const unsigned int* __restrict__ scnt,
                                                 const unsigned long long* __restrict__ sval,
                                                 unsigned long long* __restrict__ acc) {
+  PDL_PROLOGUE();
   const long long ncls = (long long)lists[1];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ncls; i += (long long)gridDim.x * blockDim.x) {
     const unsigned long long ent = slist[i];
@@ -2776,6 +2792,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
                                                             long long* __restrict__ chunkres,
                                                             unsigned long long* __restrict__ work,
                                                             const uint32_t* __restrict__ clist, long long clist_stride) {
+  PDL_PROLOGUE();
   __shared__ WarpRowCtx s_ctx[kRowWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRowCtx& X = s_ctx[wid];
@@ -3051,6 +3068,7 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
                                               const DRowInfo* __restrict__ rowinfo,
                                               const long long* __restrict__ chunkres,
                                               unsigned long long* __restrict__ acc, int mode) {
+  PDL_PROLOGUE();
   const long long total = pre[n].fold;
   const int lane = threadIdx.x & 31;
   // items (config, field) <= CTAs (BJ configs[1]: 336 items x ~40 planes): one CTA per item (all
@@ -3162,6 +3180,7 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
                                               unsigned long long* __restrict__ acc,
                                               unsigned long long* __restrict__ work, Tri* __restrict__ spart,
                                               unsigned int* __restrict__ sdone, int max_fields) {
+  PDL_PROLOGUE();
   __shared__ Tri s_red[(256 / 32) * kSectNQ];
   __shared__ int s_last;
   const long long total = pre[n].sect * kSectSeg;
@@ -3732,9 +3751,33 @@ static int check_launch() {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
+// launch `kern` on `q`, as a programmatic dependent of the stream's previous kernel when `pdl`
+template <typename... P, typename... A>
+static void launch_k(bool pdl, void (*kern)(P...), dim3 grid, dim3 block, cudaStream_t q, A... args) {
+  if (!pdl) {
+    kern<<<grid, block, 0, q>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = q;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                     const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
                     cudaEvent_t* ev, const FanOut* fan) {
+  // programmatic dependent launches along each chain (not while per-kernel events are recorded
+  // between the kernels; WS_PDL=0 disables, A/B)
+  static const bool pdl_env = !(getenv("WS_PDL") && getenv("WS_PDL")[0] == '0');
+  const bool pdl = pdl_env && !ev;
   uint32_t L = 0;
   auto beg = [&](int kind, cudaStream_t q) {
     if (ev) cudaEventRecord(ev[2 * kind], q);
@@ -3772,13 +3815,14 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
 #endif
   beg(K_FOLD, b);
   static const int fold_mode = getenv("WS_FOLD_MODE") ? atoi(getenv("WS_FOLD_MODE")) : 0;  // diagnostics
-  k_fold<<<n_sm_dev * 4, 256, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.acc, fold_mode);
+  launch_k(pdl, k_fold, n_sm_dev * 4, 256, b, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
+           (const DRowInfo*)s.rowinfo, (const long long*)s.chunkres, s.acc, (int)fold_mode);
   end(K_FOLD, b);
   beg(K_SMSET, a);
   k_spairs<<<n_sm_dev * 4, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist,
                                                   s.dlist, s.skey, s.dmask, s.gkey);
-  k_smset<<<n_sm_dev * 8, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist, s.dlist,
-                                        s.skey, s.dmask, s.gkey);
+  launch_k(pdl, k_smset, n_sm_dev * 8, kSmsetThreads, a, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
+           s.scnt, s.srep, s.lists, s.slist, s.dlist, s.skey, s.dmask, (const unsigned long long*)s.gkey);
   ++L;
   end(K_SMSET, a);
   beg(K_SCLASS, a);
@@ -3787,16 +3831,22 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     CDesc* cd = (CDesc*)s.cdesc;
     Tri* cp = (Tri*)s.cpool;
     unsigned long long* cctr = s.lists + 4;  // descriptors, pool planes, items (zeroed with the lists)
-    k_cplan<<<n_sm_dev * 4, 256, 0, a>>>(s.plans, d_k, d_g, s.lists, s.slist, s.srep, s.sval, s.cfbl, cd, cp, s.citems,
-                                         cctr, s.cdesc_cap, s.cpool_cap);
-    k_cplanes<<<n_sm_dev * 8, 256, 0, a>>>(s.plans, d_k, d_g, cd, cp, s.citems, cctr, s.work);
-    k_cfold<<<n_sm_dev * 2, 256, 0, a>>>(s.plans, d_k, d_g, s.slist, s.scnt, cd, cp, cctr, s.acc, s.sval);
+    launch_k(pdl, k_cplan, n_sm_dev * 4, 256, a, (const DPlan*)s.plans, d_k, d_g, (const unsigned long long*)s.lists,
+             (const unsigned long long*)s.slist, (const unsigned long long*)s.srep, s.sval, s.cfbl, cd, cp, s.citems,
+             cctr, (long long)s.cdesc_cap, (long long)s.cpool_cap);
+    launch_k(pdl, k_cplanes, n_sm_dev * 8, 256, a, (const DPlan*)s.plans, d_k, d_g, (const CDesc*)cd, cp,
+             (const uint32_t*)s.citems, (const unsigned long long*)cctr, s.work);
+    launch_k(pdl, k_cfold, n_sm_dev * 2, 256, a, (const DPlan*)s.plans, d_k, d_g, (const unsigned long long*)s.slist,
+             (const unsigned int*)s.scnt, (const CDesc*)cd, (const Tri*)cp, (const unsigned long long*)cctr, s.acc,
+             s.sval);
     L += 3;
   }
-  k_sclass<<<n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, 0, a>>>(s.plans, d_k, d_g, s.acc, s.scnt, s.srep, s.lists,
-                                                                     s.slist, s.dlist, s.work, s.sval, s.dmask,
-                                                                     cplanes ? s.cfbl : nullptr, s.lists + 4);
-  k_sshare<<<n_sm_dev, 256, 0, a>>>(s.lists, s.slist, s.scnt, s.sval, s.acc);
+  launch_k(pdl, k_sclass, n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, a, (const DPlan*)s.plans, d_k, d_g, s.acc,
+           (const unsigned int*)s.scnt, (const unsigned long long*)s.srep, s.lists, (const unsigned long long*)s.slist,
+           (const unsigned long long*)s.dlist, s.work, s.sval, (const unsigned int*)s.dmask,
+           (const uint32_t*)(cplanes ? s.cfbl : nullptr), (const unsigned long long*)(s.lists + 4));
+  launch_k(pdl, k_sshare, n_sm_dev, 256, a, (const unsigned long long*)s.lists, (const unsigned long long*)s.slist,
+           (const unsigned int*)s.scnt, (const unsigned long long*)s.sval, s.acc);
 #ifdef WS_SCLASS_TRACE
   k_sctrace_dump<<<1, 1, 0, a>>>(s.lists, s.plans);
 #endif
@@ -3806,15 +3856,17 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   k_instr<<<n, 128, 0, m>>>(d_k, s.plans, s.instr, s.wcnt, n);
   end(K_INSTR, m);
   beg(K_WARP, m);
-  k_warp<<<persist, 256, 0, m>>>(s.plans, s.prefix, n, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist,
-                                 s.work);
+  launch_k(pdl, k_warp, persist, 256, m, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, (const DInstr*)s.instr, d_k,
+           d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
   end(K_WARP, m);
   beg(K_WCLASS, m);
-  k_wclass<<<persist, 256, 0, m>>>(s.plans, s.instr, d_k, d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
+  launch_k(pdl, k_wclass, persist, 256, m, (const DPlan*)s.plans, (const DInstr*)s.instr, d_k, d_g, s.acc,
+           (const unsigned int*)s.wcnt, (const unsigned long long*)s.wrep, s.lists, (const unsigned long long*)s.wlist,
+           s.work);
   end(K_WCLASS, m);
   beg(K_SECT, m);
-  k_sect<<<n_sm_dev * WS_SECT_CTAS, 256, 0, m>>>(s.plans, s.prefix, n, d_k, d_g, s.acc, s.work, (Tri*)s.spart, s.sdone,
-                                      s.max_fields);
+  launch_k(pdl, k_sect, n_sm_dev * WS_SECT_CTAS, 256, m, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
+           s.acc, s.work, (Tri*)s.spart, s.sdone, (int)s.max_fields);
   end(K_SECT, m);
   // join
   cudaEventRecord(st.join[0], a);
