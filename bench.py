@@ -274,10 +274,14 @@ def run_native(args, rank, world, local):
 
     # rank r evaluates the space on hardware set r: the gathered buffer [r][i] is already in
     # canonical order (equal shards), so a step is estimate -> one all-gather -> rank
+    # one rank: ws_estimate_ranked_async (the model and the ranking fused into the chain's last
+    # kernel); several: estimate -> all-gather -> rank of the gathered set
     def step():
+        if world == 1:
+            ctx.estimate_ranked_async(d_cfg.data_ptr(), n, d_out.data_ptr(), TOPK, d_top.data_ptr())
+            return
         ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, d_out)
+        dist.all_gather_into_tensor(gathered, d_out)
         ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
 
     launches_per_step = None
@@ -285,9 +289,12 @@ def run_native(args, rank, world, local):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
-    est_launches = ctx.last_launch_count()
-    launches_per_step = est_launches + 1
+    if world == 1:
+        step()
+        launches_per_step = ctx.last_launch_count()
+    else:
+        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
+        launches_per_step = ctx.last_launch_count() + 1
     work = ctx.work_read()
 
     sampler = ClockSampler(local)
@@ -611,10 +618,12 @@ def e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb):
 
     def one():
         d_cfg.copy_(h_cfg, non_blocking=True)
-        ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
-        if world > 1:
+        if world == 1:
+            ctx.estimate_ranked_async(d_cfg.data_ptr(), n, d_out.data_ptr(), TOPK, d_top.data_ptr())
+        else:
+            ctx.estimate_async(d_cfg.data_ptr(), n, d_out.data_ptr())
             dist.all_gather_into_tensor(gathered, d_out)
-        ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
+            ctx.rank_async(gathered.data_ptr(), world * n, TOPK, d_top.data_ptr())
         h_res.copy_(gathered, non_blocking=True)
         h_top.copy_(d_top, non_blocking=True)
         stream.synchronize()
@@ -639,7 +648,8 @@ def e2e_measure(ctx, host_cfg, n, world, dev, stream, args, rb):
     assert (res["status"] == 0).all()
     return {"value": world * n * args.steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": int(h_cfg.numel()), "d2h_bytes_per_step": int(h_res.numel() + h_top.numel() * 4),
-            "api": "pinned host configs -> ws_estimate_async -> [all-gather] -> ws_rank_async -> pinned host results"}
+            "api": ("pinned host configs -> ws_estimate_ranked_async -> pinned host results" if world == 1 else
+                    "pinned host configs -> ws_estimate_async -> all-gather -> ws_rank_async -> pinned host results")}
 
 
 def main():

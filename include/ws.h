@@ -193,6 +193,16 @@ ws_status ws_estimate(ws_ctx* ctx, const ws_config* cfgs, size_t n, ws_result* o
  * enqueued on the context stream, returns without synchronising. */
 ws_status ws_estimate_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_result* d_out);
 
+/* One sweep step end to end on the device ("the best configurations are selected",
+ * P:1025-1046): ws_estimate_async of d_cfgs followed by ws_rank_async of d_out (d_top: k
+ * device uint32 indices, may be null), records and top-k byte-identical to those two calls.
+ * For n <= 1024 the FP64 model kernel (a7) also ranks (a8): its last CTA to finish sorts the
+ * batch's (t_pred, index) keys in shared memory, saving the rank launch and a kernel boundary
+ * on the critical path; larger batches call the two paths in turn.
+ * Device pointers, enqueued on the context stream; errors as ws_estimate_async / ws_rank_async. */
+ws_status ws_estimate_ranked_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_result* d_out, size_t k,
+                                   uint32_t* d_top_idx);
+
 /* Architecture exploration (BJ configs[3]; hardware parameters P:307-320): every configuration
  * against every hardware set of gpu_ids (a host array of n_gpu <= 256 described gpu ids).
  *   out[g * n + i] = the record ws_estimate gives for cfgs[i] with gpu_id = gpu_ids[g]
@@ -217,6 +227,14 @@ uint32_t ws_last_group_count(const ws_ctx* ctx);
  * a stable radix sort of 64-bit keys beyond (scratch kept by the context, grow-only). */
 ws_status ws_rank(ws_ctx* ctx, ws_result* res, size_t n, size_t k, uint32_t* top_idx);
 ws_status ws_rank_async(ws_ctx* ctx, ws_result* d_res, size_t n, size_t k, uint32_t* d_top_idx);
+
+/* Bounds checks (diagnostics; SURVEY 4 layer 5 in place of compute-sanitizer, which this GPU
+ * pool does not run): a library built with -DWS_CHECK checks every dynamically computed scratch
+ * index of the estimate chain against its capacity on the device and counts violations (no
+ * graphs in that build).  out[5] = {1 if this is a bounds-check build else 0, violations since
+ * the last read, first violation's source line, its index, its capacity}; reading resets them.
+ * Synchronises the context stream.  Ordinary builds: all zeros, WS_OK. */
+ws_status ws_check_read(ws_ctx* ctx, uint64_t* out);
 
 /* ------------------------------------------------------------------ NEXT-1: simulated hit rates
  * (O, R) samples for the four hit-rate curves from a sectored,

@@ -75,15 +75,20 @@ struct ws_ctx {
     int nk, ng;
     uint64_t fan;       // ws_estimate_multi: hash of the fan-out descriptor (0 = plain estimate)
     const void* xcfg;   // its expanded-configuration buffer
+    const void* top;    // ws_estimate_ranked_async: top-k buffer and k (rank_k = -1: no ranking tail)
+    long long rank_k;
     bool operator==(const GKey& o) const {
       return cfgs == o.cfgs && out == o.out && scratch == o.scratch && dk == o.dk && dg == o.dg && n == o.n &&
-             nk == o.nk && ng == o.ng && fan == o.fan && xcfg == o.xcfg;
+             nk == o.nk && ng == o.ng && fan == o.fan && xcfg == o.xcfg && top == o.top && rank_k == o.rank_k;
     }
   };
   cudaStream_t cap = nullptr;
   cudaGraphExec_t gexec = nullptr;
   GKey gkey{};
   uint32_t g_launches = 0;
+  int g_tail_done = 0;   // the captured graph's k_model also ranks (ws_estimate_ranked_async)
+  void* wclean_ptr = nullptr;   // warp-class counter region known to be zero (ensure_scratch)
+  size_t wclean_n = 0;
   bool graphs = true;
   // 2 events (start, end) per kernel kind, kinds [first_kind, first_kind + nk)
   cudaEvent_t* take_events(int first_kind, int nk) {
@@ -227,6 +232,14 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
     if (e != cudaSuccess) return cuda_fail(c, e, "scratch init");
   }
   char* b = (char*)c->scratch;
+  // the warp-class counters are self-cleaning (k_wclass zeroes every slot it consumes): zero the
+  // region only when this layout places it somewhere the previous call did not
+  if ((void*)(b + o_wcnt) != c->wclean_ptr || n > c->wclean_n) {
+    cudaError_t e = cudaMemsetAsync(b + o_wcnt, 0, n * (size_t)kWSlots * sizeof(unsigned int), c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "warp-class counters");
+    c->wclean_ptr = (void*)(b + o_wcnt);
+    c->wclean_n = n;
+  }
   s.plans = (DPlan*)(b + o_plans);
   s.instr = (DInstr*)(b + o_instr);
   s.rowinfo = (DRowInfo*)(b + o_row);
@@ -281,6 +294,9 @@ ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out) {
   c->device = cuda_device;
   c->stream = (cudaStream_t)cuda_stream;
   c->graphs = !(getenv("WS_GRAPH") && getenv("WS_GRAPH")[0] == '0');
+#ifdef WS_CHECK
+  c->graphs = false;   // the bounds-check build uploads each call's capacities before its launches
+#endif
   cudaDeviceGetAttribute(&c->n_sm_dev, cudaDevAttrMultiProcessorCount, cuda_device);
   if (c->n_sm_dev <= 0) c->n_sm_dev = 148;
   // stream priorities: the row chain (k_rows -> k_fold, the critical path) gets the highest, so
@@ -507,6 +523,9 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
       }
     }
     G.g_end = ng;
+    G.oz_mask = 0;
+    if (G.g_end > G.g_begin && G.oz_max - G.oz_min < 64)
+      for (int q = G.g_begin; q < G.g_end; ++q) G.oz_mask |= 1ull << (D.g[q].oz - G.oz_min);
     G.n_runs = (int)runs.size();
     for (size_t q = 0; q < runs.size(); ++q) {
       G.run_lo[q] = runs[q].first;
@@ -573,7 +592,7 @@ ws_status ws_describe_gpu(ws_ctx* c, const ws_gpu* g, uint32_t* id) {
 }
 
 static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out, bool allow_graph,
-                                 const FanOut* fan);
+                                 const FanOut* fan, TailRank* tail = nullptr);
 static size_t chunk_configs(ws_ctx* c, size_t per_item_mult);
 
 ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out) {
@@ -598,6 +617,31 @@ ws_status ws_estimate_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_res
   return WS_OK;
 }
 
+ws_status ws_estimate_ranked_async(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out, size_t k,
+                                   uint32_t* d_top) {
+  const NvtxRange range("ws_estimate_ranked_async");
+  if (!c) return WS_EINVAL;
+  if (n == 0) return WS_OK;
+  if (!d_cfgs || !d_out) return fail(c, WS_EINVAL, "null argument");
+  if (n > kMaxBatch) return fail(c, WS_ELIMIT, "batch larger than 2^24 configurations");
+  if (c->hk.empty() || c->hg.empty()) return fail(c, WS_EUNKNOWN_ID, "describe a kernel and a gpu first");
+  cudaSetDevice(c->device);
+  ws_status s = upload(c);
+  if (s != WS_OK) return s;
+  TailRank tail{(int)std::min(k, n), d_top, 0};
+  if (n <= (size_t)kTailMax && n <= chunk_configs(c, 1)) {
+    s = estimate_launch(c, d_cfgs, n, d_out, true, nullptr, &tail);
+    if (s != WS_OK || tail.done) return s;
+  } else {
+    s = ws_estimate_async(c, d_cfgs, n, d_out);
+    if (s != WS_OK) return s;
+  }
+  const uint32_t le = c->last_launches;
+  s = ws_rank_async(c, d_out, n, k, d_top);
+  c->last_launches += le;
+  return s;
+}
+
 static uint64_t fan_hash(const FanOut* f) {  // FNV-1a over the fan-out descriptor (graph key)
   if (!f) return 0;
   uint64_t h = 1469598103934665603ull;
@@ -610,7 +654,7 @@ static uint64_t fan_hash(const FanOut* f) {  // FNV-1a over the fan-out descript
 // ws_estimate_multi, over fan->m configurations x fan->n_groups representative hardware sets
 // with the model fanned out to fan->n_gpu sets (d_cfgs: the caller's configurations).
 static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, ws_result* d_out, bool allow_graph,
-                                 const FanOut* fan) {
+                                 const FanOut* fan, TailRank* tail) {
   ws_status s;
   Scratch S;
   const size_t n_int = fan ? (size_t)fan->m * fan->n_groups : n;
@@ -639,7 +683,7 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
       extra = 1;
     }
     const int e1 = launch_estimate(icfg, (int)n_int, c->dk, (int)c->hk.size(), c->dg, (int)c->hg.size(), S, d_out, st,
-                                   c->n_sm_dev, launches, evs, fan);
+                                   c->n_sm_dev, launches, evs, fan, tail);
     if (launches) *launches += extra;
     return e1;
   };
@@ -649,7 +693,8 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
   cudaStreamIsCapturing(c->stream, &cs);
   if (allow_graph && c->graphs && !ev && !serial && cs == cudaStreamCaptureStatusNone) {
     const ws_ctx::GKey key{d_cfgs, d_out, c->scratch, c->dk, c->dg, n, (int)c->hk.size(), (int)c->hg.size(),
-                           fan_hash(fan), xcfg};
+                           fan_hash(fan), xcfg, tail ? (const void*)tail->top : nullptr,
+                           tail ? (long long)tail->k : -1ll};
     if (!c->gexec || !(key == c->gkey)) {
       if (c->gexec) {
         cudaGraphExecDestroy(c->gexec);
@@ -668,7 +713,9 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
         return cuda_fail(c, e, "graph instantiate");
       }
       c->gkey = key;
+      c->g_tail_done = tail ? tail->done : 0;
     }
+    if (tail) tail->done = c->g_tail_done;
     cudaError_t e = cudaGraphLaunch(c->gexec, c->stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "graph launch");
     c->last_launches = c->g_launches;
@@ -809,6 +856,18 @@ ws_status ws_rank_async(ws_ctx* c, ws_result* d_res, size_t n, size_t k, uint32_
   cudaEvent_t* ev = c->profiling ? c->take_events(K_RANK, 1) : nullptr;
   int e = launch_rank(d_res, (int)n, (int)std::min(k, n), d_top, c->rank_buf, c->stream, &c->last_launches, ev);
   if (e) return cuda_fail(c, (cudaError_t)e, "rank launch");
+  return WS_OK;
+}
+
+ws_status ws_check_read(ws_ctx* c, uint64_t* out) {
+  if (!c || !out) return WS_EINVAL;
+  cudaSetDevice(c->device);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "check read");
+  unsigned long long h[5];
+  const int r = check_read(h);
+  if (r) return cuda_fail(c, (cudaError_t)r, "check read");
+  for (int i = 0; i < 5; ++i) out[i] = h[i];
   return WS_OK;
 }
 

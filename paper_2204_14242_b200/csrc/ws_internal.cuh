@@ -30,6 +30,7 @@ struct DField {
   int32_t oy_min, oy_max, oz_min, oz_max;  // over all groups of the field
   int32_t ld_oy_min, ld_oy_max, ld_oz_min, ld_oz_max;  // over load groups
   int32_t run_lo[kMaxRuns], run_hi[kMaxRuns];
+  uint64_t oz_mask;                // distinct oz of all groups: bit oz - oz_min (0 if oz_max - oz_min > 63)
 };
 
 struct DGroup {
@@ -226,9 +227,17 @@ struct FanOut {
 };
 // ev: nullptr, or 2 events per kernel (start, end) in K_* order, recorded on the kernel's stream.
 // fan: nullptr (k_model writes d_out[0..n)) or the fan-out of ws_estimate_multi (n = m * n_groups).
+// tail: nullptr, or the ranking of ws_estimate_ranked_async; for n <= kTailMax (no fan) the last
+// CTA of k_model ranks the batch and tail->done is set, else the caller ranks.
+constexpr int kTailMax = 1024;
+struct TailRank {
+  int k;
+  uint32_t* top;
+  int done;
+};
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                     const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
-                    cudaEvent_t* ev, const FanOut* fan = nullptr);
+                    cudaEvent_t* ev, const FanOut* fan = nullptr, TailRank* tail = nullptr);
 int launch_expand(const ws_config* d_cfgs, const FanOut& f, ws_config* xcfg, cudaStream_t st);
 // ---------------------------------------------------------------- NEXT-1: simulated hit rates
 // Request encoding: bits 0..45 sector + 2^45, bit 46 store, bits 48..55 field.
@@ -271,6 +280,9 @@ struct SimScratch {
 int launch_rank(ws_result* d_res, int n, int k, uint32_t* d_top, void* scratch, cudaStream_t st, uint32_t* launches,
                 cudaEvent_t* ev);
 size_t rank_scratch_bytes(int n);
+// WS_CHECK build: out[5] = {1, violations, first line, its index, its capacity} (and resets them);
+// ordinary build: zeros
+int check_read(unsigned long long* out);
 
 // NEXT-1 (ws_kernels.cu): the whole ws_simulate device sequence (estimate, request streams,
 // stack-distance simulation, sample records) on st.main, synchronous; returns 0, a

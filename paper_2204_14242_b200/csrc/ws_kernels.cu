@@ -71,6 +71,50 @@ namespace wsb {
 // the predecessor grid has completed and its memory is visible (a no-op for ordinary launches),
 // launch_dependents lets this grid's own dependent start its prologue early.
 #define PDL_PROLOGUE() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+
+// ------------------------------------------------------------------ bounds-check build (WS_CHECK)
+// The GPU pool's compute-sanitizer is closed, so a -DWS_CHECK build checks every dynamically
+// computed scratch index of the estimate chain against its capacity (WS_CHK) and records the
+// first violation (source line, index, capacity) and the count; ws_check_read returns them.
+#ifdef WS_CHECK
+struct CheckCaps {
+  long long max_chunks, clist_stride, wslots, sslots, cdesc, cpool, spart, rowinfo, instr;
+};
+__device__ CheckCaps g_caps;
+__device__ unsigned long long g_check[4];   // violations, first line, its index, its capacity
+__device__ __noinline__ void ws_check_fail(int line, long long i, long long cap) {
+  if (atomicAdd(&g_check[0], 1ull) == 0ull) {
+    g_check[1] = (unsigned long long)line;
+    g_check[2] = (unsigned long long)i;
+    g_check[3] = (unsigned long long)cap;
+  }
+}
+#define WS_CHK(i, cap)                                                       \
+  do {                                                                       \
+    const long long _wi = (long long)(i), _wc = (long long)(cap);            \
+    if (_wi < 0 || _wi >= _wc) ws_check_fail(__LINE__, _wi, _wc);           \
+  } while (0)
+#else
+#define WS_CHK(i, cap) \
+  do {                 \
+  } while (0)
+#endif
+
+int check_read(unsigned long long* out) {   // {is check build, violations, line, index, capacity}
+#ifdef WS_CHECK
+  unsigned long long h[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_check, sizeof(h));
+  if (e != cudaSuccess) return (int)e;
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_check, z, sizeof(z));
+  out[0] = 1;
+  for (int i = 0; i < 4; ++i) out[1 + i] = h[i];
+#else
+  for (int i = 0; i < 5; ++i) out[i] = 0;
+#endif
+  return 0;
+}
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ long long shfl64(long long v, int src) {
@@ -150,6 +194,25 @@ __device__ __forceinline__ int plane_rep(const DGroup* g, int ng, int z, int z0,
   }
   return seg + ((z - seg) % per);
 }
+// the same over the field's distinct oz values (DField::oz_mask: groups sharing an oz give the
+// same zone start), falling back to the group loop when the mask is unavailable
+__device__ __forceinline__ int plane_rep_f(const DField& F, const DGroup* g, int z, int z0, int lo2, int hi2, int BF2,
+                                           FDiv fdz, int per) {
+  if (per <= 0) return z;
+  unsigned long long m = F.oz_mask;
+  if (m == 0ull) return plane_rep(g, F.g_end - F.g_begin, z, z0, lo2, hi2, BF2, fdz, per);
+  int seg = z0;
+  while (m) {
+    const int oz = F.oz_min + __ffsll((long long)m) - 1, zz = z - oz;
+    m &= m - 1;
+    int st;
+    if (zz < lo2) st = -0x7fffffff;
+    else if (zz >= hi2) st = hi2 + oz;
+    else st = lo2 + (int)fdiv(zz - lo2, fdz) * BF2 + oz;
+    seg = st > seg ? st : seg;
+  }
+  return seg + ((z - seg) % per);
+}
 
 struct Tri {
   long long f, l, c;  // first, last, count; c == 0: empty
@@ -187,14 +250,17 @@ __device__ void cta_ordered_reduce(Tri (&t)[NQ], Tri* sm) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) sm[warp * NQ + q] = t[q];
   __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      Tri a = sm[q];
-      for (int w = 1; w < nw; ++w) a = tri_combine(a, sm[w * NQ + q]);
-      t[q] = a;
-    }
+  // the warps' partials in warp order, one triple slot per thread of warp 0 (NQ <= 32 in parallel)
+  if (threadIdx.x < NQ) {
+    const int q = threadIdx.x;
+    Tri a = sm[q];
+    for (int w = 1; w < nw; ++w) a = tri_combine(a, sm[w * NQ + q]);
+    sm[q] = a;
   }
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) t[q] = sm[q];
   __syncthreads();
 }
 
@@ -644,10 +710,8 @@ __global__ void __launch_bounds__(128) k_instr(const DKernel* __restrict__ ks, D
                                                DInstr* __restrict__ instr, unsigned int* __restrict__ wcnt, int n) {
   PDL_PROLOGUE();
   const int c = blockIdx.x, tid = threadIdx.x;
-  {  // this configuration's warp-class counters (k_warp)
-    uint4* wc = reinterpret_cast<uint4*>(wcnt + (long long)c * kWSlots);
-    for (int i = tid; i < kWSlots / 4; i += blockDim.x) wc[i] = make_uint4(0u, 0u, 0u, 0u);
-  }
+  // (the warp-class counters of k_warp are zero here: k_wclass returns every slot it reads to 0,
+  // and the host zeroes the region whenever the scratch layout moves it)
   __shared__ unsigned char s_first[kMaxAcc * kMaxFoldCube];
   __shared__ int s_part[128];
   __shared__ int s_total;
@@ -748,6 +812,8 @@ __global__ void __launch_bounds__(128) k_instr(const DKernel* __restrict__ ks, D
       e.kind = (int)A.is_store;
       e.lg_elem = F.lg_elem;
       e.pad = 0;
+      WS_CHK(pos, kMaxInstr);
+      WS_CHK((long long)c * kMaxInstr + pos, g_caps.instr);
       instr[(long long)c * kMaxInstr + pos] = e;
       ++pos;
     }
@@ -761,7 +827,7 @@ __global__ void __launch_bounds__(128) k_instr(const DKernel* __restrict__ ks, D
 }
 
 #ifndef WS_PLAN_THREADS
-#define WS_PLAN_THREADS 128
+#define WS_PLAN_THREADS 160   // 4 worker warps + the row-claim warp
 #endif
 __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __restrict__ cfgs, int n,
                                               const DKernel* __restrict__ ks, int nk, const DGpu* __restrict__ gs,
@@ -777,6 +843,9 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
                                               long long clist_stride) {
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
+  // k_rows (the row chain, a programmatic dependent on the same stream) may launch now: its CTAs
+  // wait in griddepcontrol.wait until this grid has completed, then start without a launch gap
+  PDL_TRIGGER();
   const unsigned long long cur_epoch = *(volatile unsigned long long*)epoch + 1ull;  // this call
 #ifdef WS_PLAN_CLOCK
   long long clk[12];
@@ -860,53 +929,99 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     return;
   }
   PLAN_MARK()
-  // the ranges (warp 0) and the row-table claim (warp 1, global atomics) overlap
-  if (tid < 5) plan_range(P, tid);
-  if (tid == 32) row_claim(P, c, sG, cur_epoch, rowtab);
-  __syncwarp();
-  if (tid == 0) plan_boundaries(P);
-  __syncthreads();
-  PLAN_MARK()
+  // warp kPlanWork/32 alone claims the row-table key (global atomics, a few dependent round trips);
+  // warps 0 .. kPlanWork/32-1 meanwhile compute the ranges, boundaries, row boxes and the computed-
+  // plane lists as if this configuration owned its row scope (named barrier 1), and the join below
+  // drops the lists of a sharer
+  constexpr int kPlanWork = WS_PLAN_THREADS - 32;
+  static_assert(kPlanWork >= 32 && kPlanWork % 32 == 0, "k_plan: worker warps + the claim warp");
+  const int ll = sG.lg_line;
   const DKernel& K = sK;
   __shared__ DRowInfo s_ri[kMaxFields];   // row boxes staged here, written out once
-  // ---- row boxes of the wave + layer-set footprint, per field
-  for (int fi = tid; fi < K.n_fields; fi += blockDim.x) {
-    const DField& F = K.f[fi];
-    const long long rA = P.Lz0 / P.G[0], rB = (P.s + P.W - 1) / P.G[0];
-    const long long byA = rA % P.G[1], bzA = rA / P.G[1], byB = rB % P.G[1], bzB = rB / P.G[1];
-    long long ylo, yhi;
-    if (bzA == bzB) {
-      ylo = P.lo[1] + byA * P.BF[1];
-      yhi = P.lo[1] + (byB + 1) * P.BF[1];
-      if (yhi > P.hi[1]) yhi = P.hi[1];
-    } else {
-      ylo = P.lo[1];
-      yhi = P.hi[1];
+  __shared__ int s_nri;
+  uint32_t* cl = clist + (long long)c * clist_stride;
+  if (tid >= kPlanWork) {
+    if (tid == kPlanWork) row_claim(P, c, sG, cur_epoch, rowtab);
+  } else {
+    auto wbar = [] { asm volatile("bar.sync 1, %0;" ::"r"(kPlanWork) : "memory"); };
+    if (tid < 5) plan_range(P, tid);
+    __syncwarp();
+    if (tid == 0) plan_boundaries(P);
+    // ---- row boxes of the wave + layer-set footprint, per field
+    for (int fi = tid; fi < K.n_fields; fi += kPlanWork) {
+      const DField& F = K.f[fi];
+      const long long rA = P.Lz0 / P.G[0], rB = (P.s + P.W - 1) / P.G[0];
+      const long long byA = rA % P.G[1], bzA = rA / P.G[1], byB = rB % P.G[1], bzB = rB / P.G[1];
+      long long ylo, yhi;
+      if (bzA == bzB) {
+        ylo = P.lo[1] + byA * P.BF[1];
+        yhi = P.lo[1] + (byB + 1) * P.BF[1];
+        if (yhi > P.hi[1]) yhi = P.hi[1];
+      } else {
+        ylo = P.lo[1];
+        yhi = P.hi[1];
+      }
+      long long zlo = P.lo[2] + bzA * P.BF[2], zhi = P.lo[2] + (bzB + 1) * P.BF[2];
+      if (zhi > P.hi[2]) zhi = P.hi[2];
+      long long y0 = ylo + F.oy_min, y1 = yhi + F.oy_max, z0 = zlo + F.oz_min, z1 = zhi + F.oz_max;
+      if (y0 < 0) y0 = 0;
+      if (z0 < 0) z0 = 0;
+      if (y1 > F.ext[1]) y1 = F.ext[1];
+      if (z1 > F.ext[2]) z1 = F.ext[2];
+      DRowInfo ri;
+      ri.y0 = y0;
+      ri.ny = y1 > y0 ? y1 - y0 : 0;
+      ri.z0 = z0;
+      ri.nz = z1 > z0 ? z1 - z0 : 0;
+      if (F.g_end == F.g_begin) ri.ny = ri.nz = 0;
+      ri.ppc = 1;
+      ri.nseg = ri.ny > 0 ? (ri.ny + kRowSeg - 1) / kRowSeg : 1;
+      ri.n_chunks = ri.ny > 0 ? ri.nz * ri.nseg : 0;   // as the owner (the join below drops a sharer's)
+      ri.chunk_begin = 0;
+      s_ri[fi] = ri;
     }
-    long long zlo = P.lo[2] + bzA * P.BF[2], zhi = P.lo[2] + (bzB + 1) * P.BF[2];
-    if (zhi > P.hi[2]) zhi = P.hi[2];
-    long long y0 = ylo + F.oy_min, y1 = yhi + F.oy_max, z0 = zlo + F.oz_min, z1 = zhi + F.oz_max;
-    if (y0 < 0) y0 = 0;
-    if (z0 < 0) z0 = 0;
-    if (y1 > F.ext[1]) y1 = F.ext[1];
-    if (z1 > F.ext[2]) z1 = F.ext[2];
-    DRowInfo ri;
-    ri.y0 = y0;
-    ri.ny = y1 > y0 ? y1 - y0 : 0;
-    ri.z0 = z0;
-    ri.nz = z1 > z0 ? z1 - z0 : 0;
-    if (F.g_end == F.g_begin) ri.ny = ri.nz = 0;
-    ri.ppc = 1;
-    ri.nseg = ri.ny > 0 ? (ri.ny + kRowSeg - 1) / kRowSeg : 1;
-    ri.n_chunks = (ri.ny > 0 && P.row_owner == c) ? ri.nz * ri.nseg : 0;   // sharers: the owner's rows
-    ri.chunk_begin = 0;
-    s_ri[fi] = ri;
+    wbar();
+    if (tid == 0) {
+      long long cb = 0;
+      for (int fi = 0; fi < K.n_fields; ++fi) {
+        s_ri[fi].chunk_begin = cb;
+        cb += s_ri[fi].n_chunks;
+      }
+      s_nri = 0;
+    }
+    wbar();
+    // k_rows items: the chunks of computed planes (plane_rep(z) == z), listed per configuration;
+    // derived planes are folded from their representative by k_fold (same rule)
+    for (int fi = 0; fi < K.n_fields; ++fi) {
+      const DRowInfo ri = s_ri[fi];
+      if (ri.n_chunks == 0) continue;
+      const DField& F = K.f[fi];
+      long long py, pz, falign;
+      field_rows(F, P, ll, py, pz, falign);
+      const int per = plane_period(pz, F.lg_elem, ll);
+      for (int zi = tid; zi < (int)ri.nz; zi += kPlanWork) {
+        const int z = (int)ri.z0 + zi;
+        if (plane_rep_f(F, K.g + F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2], P.fd_BF[2],
+                        per) != z)
+          continue;
+        const int at = atomicAdd(&s_nri, (int)ri.nseg);
+        for (int sg = 0; sg < (int)ri.nseg; ++sg) {
+          WS_CHK(at + sg, g_caps.clist_stride);
+          WS_CHK((long long)c * clist_stride + at + sg, g_caps.max_chunks);
+          cl[at + sg] = (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
+        }
+      }
+    }
   }
-  __syncthreads();
+  __syncthreads();   // join: the claim's row_owner, the workers' boxes and lists
   if (tid == 0) {
+    const bool owner = P.row_owner == c;
     long long cb = 0;
     for (int fi = 0; fi < K.n_fields; ++fi) {
-      s_ri[fi].chunk_begin = cb;
+      if (!owner) {   // sharer: the owner's rows (no k_rows / k_fold items)
+        s_ri[fi].n_chunks = 0;
+        s_ri[fi].chunk_begin = 0;
+      }
       cb += s_ri[fi].n_chunks;
     }
     P.n_warp_items = (P.rep_mult ? 1 : P.W) * P.nwarps;
@@ -915,39 +1030,12 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     // k_spairs items: the sets j < nsets of >= 2 members, i.e. j < W - n_sm (members j + m * n_sm < W)
     P.n_sclass_items = (P.scls_R > 0 && !P.rep_mult && P.W > P.nsets) ? min(P.nsets, P.W - P.nsets) : 0;
     P.n_chunks = cb;
-    P.n_fields = P.row_owner == c ? K.n_fields : 0;   // k_fold items
+    P.n_fields = owner ? K.n_fields : 0;   // k_fold items
     P.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
+    P.n_ritems = owner ? s_nri : 0;
   }
   __syncthreads();
-  // k_rows items: the chunks of computed planes (plane_rep(z) == z), listed per configuration;
-  // derived planes are folded from their representative by k_fold (same rule)
-  {
-    __shared__ int s_nri;
-    if (tid == 0) s_nri = 0;
-    __syncthreads();
-    const int ll = sG.lg_line;
-    uint32_t* cl = clist + (long long)c * clist_stride;
-    for (int fi = tid; fi < K.n_fields; fi += blockDim.x) rowinfo[(long long)c * kMaxFields + fi] = s_ri[fi];
-    for (int fi = 0; fi < K.n_fields; ++fi) {
-      const DRowInfo ri = s_ri[fi];
-      if (ri.n_chunks == 0) continue;
-      const DField& F = K.f[fi];
-      long long py, pz, falign;
-      field_rows(F, P, ll, py, pz, falign);
-      const int per = plane_period(pz, F.lg_elem, ll);
-      for (int zi = tid; zi < (int)ri.nz; zi += blockDim.x) {
-        const int z = (int)ri.z0 + zi;
-        if (plane_rep(K.g + F.g_begin, F.g_end - F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
-                      P.fd_BF[2], per) != z)
-          continue;
-        const int at = atomicAdd(&s_nri, (int)ri.nseg);
-        for (int sg = 0; sg < (int)ri.nseg; ++sg) cl[at + sg] = (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) P.n_ritems = s_nri;
-    __syncthreads();
-  }
+  for (int fi = tid; fi < K.n_fields; fi += blockDim.x) rowinfo[(long long)c * kMaxFields + fi] = s_ri[fi];
   PLAN_MARK()
   store_plan();
   PLAN_MARK()
@@ -1023,10 +1111,29 @@ __device__ void eval_warp(const DPlan& P, const DKernel& K, const DGpu& G, const
   int cur_field = -1;
   long long plane = 0;
   const int ni = P.n_instr;
-  DInstr e = tab[0];
+  // the instruction table in chunks of 32 entries, one per lane (one coalesced load round per
+  // chunk), broadcast by shuffles: no dependent global load per instruction
+  long long mC = 0;
+  unsigned long long mK = 0;
+  int mF = 0;
   for (int i = 0; i < ni; ++i) {
-    const DInstr cur = e;
-    if (i + 1 < ni) e = tab[i + 1];
+    if ((i & 31) == 0) {
+      if (i + lane < ni) {
+        const DInstr me = tab[i + lane];
+        mC = me.C;
+        mK = me.kmask;
+        mF = me.field | (me.kind << 8) | (me.lg_elem << 16);
+      }
+    }
+    DInstr cur;
+    cur.C = shfl64(mC, i & 31);
+    cur.kmask = (unsigned long long)shfl64((long long)mK, i & 31);
+    {
+      const int pk = __shfl_sync(FULL, mF, i & 31);
+      cur.field = pk & 255;
+      cur.kind = (pk >> 8) & 255;
+      cur.lg_elem = pk >> 16;
+    }
     const bool iss = (cur.kmask & L.act) != 0ull;
     const unsigned m = __ballot_sync(FULL, iss);
     if (m == 0u) continue;
@@ -1124,6 +1231,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
   const int lane = threadIdx.x & 31;
   unsigned long long my_units = 0;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  int c0 = -1;
   // each lane classifies one wave warp; warps of configs without classes are then
   // evaluated cooperatively by the whole warp
   for (long long base = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < total; base += nw * 32) {
@@ -1135,7 +1243,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
     long long B = 0;
     int wrep_w = 0;
     // one search per warp (lanes hold consecutive items), then each lane advances
-    int c0 = find_config<0>(pre, n, base);
+    c0 = find_config_warp<0>(pre, n, base, c0);
     if (have) {
       c = c0;
       while (c + 1 < n && pre[c + 1].warp <= item) ++c;
@@ -1187,9 +1295,12 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
       const int cc = (int)(key >> 32);
       const unsigned slot = (unsigned)(key & 0xffffffffu);
       const long long gslot = (long long)cc * kWSlots + slot;
+      WS_CHK(slot, kWSlots);
+      WS_CHK(gslot, g_caps.wslots);
       if (atomicAdd(wcnt + gslot, (unsigned)__popc(peers)) == 0u) {
         wrep[gslot] = ((unsigned long long)B << 5) | (unsigned long long)wrep_w;
         const unsigned long long idx = atomicAdd(lists + 0, 1ull);
+        WS_CHK(idx, g_caps.wslots);
         wlist[idx] = key;
       }
     }
@@ -1220,7 +1331,7 @@ __global__ void __launch_bounds__(256) k_warp(const DPlan* __restrict__ plans, c
 __global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans, const DInstr* __restrict__ instr,
                                                 const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                                 unsigned long long* __restrict__ acc,
-                                                const unsigned int* __restrict__ wcnt,
+                                                unsigned int* __restrict__ wcnt,
                                                 const unsigned long long* __restrict__ wrep,
                                                 const unsigned long long* __restrict__ lists,
                                                 const unsigned long long* __restrict__ wlist,
@@ -1236,7 +1347,12 @@ __global__ void __launch_bounds__(256) k_wclass(const DPlan* __restrict__ plans,
     const unsigned slot = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
     const long long gslot = (long long)c * kWSlots + slot;
-    const unsigned int cnt = wcnt[gslot];
+    WS_CHK(gslot, g_caps.wslots);
+    unsigned int cnt = 0;
+    if (lane == 0) {  // the class size; the slot returns to 0 for the next call (k_instr no longer zeroes)
+      cnt = wcnt[gslot];
+      wcnt[gslot] = 0u;
+    }
     const long long B = (long long)(wrep[gslot] >> 5);
     const int w = (int)(wrep[gslot] & 31ull);
     const Lane L = lane_setup(P, B, w, lane);
@@ -1947,7 +2063,11 @@ __device__ void smset_claim(const DPlan& P, int c, long long Bm, bool active, un
   if (atomicAdd(scnt + gslot, (unsigned)__popc(peers)) == 0u) {
     srep[gslot] = (unsigned long long)Bm;
     const unsigned low = share_claim(skey, share_key(P, slot), slot);
-    slist[atomicAdd(lists + 1, 1ull)] = ((unsigned long long)c << 32) | low;
+    {
+      const unsigned long long si = atomicAdd(lists + 1, 1ull);
+      WS_CHK(si, g_caps.sslots);
+      slist[si] = ((unsigned long long)c << 32) | low;
+    }
   }
 }
 
@@ -2256,7 +2376,11 @@ __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, 
     long long dbase = (long long)(base >> 40), pbase = (long long)(base & ((1ull << 40) - 1));
     fits = fits && dbase + ndesc <= desc_cap && dbase + ndesc <= (1 << 20) && pbase + nplanes <= pool_cap;
     if (!fits) {
-      if (lane == 0) cfbl[atomicAdd(cctr + 2, 1ull)] = (uint32_t)e;
+      if (lane == 0) {
+        const unsigned long long fb = atomicAdd(cctr + 2, 1ull);
+        WS_CHK(fb, g_caps.sslots);
+        cfbl[fb] = (uint32_t)e;
+      }
       continue;
     }
     if (lane == 0 && ((low >> 30) & 1u)) {  // owner of a shared class: k_cfold accumulates the counts
@@ -2273,16 +2397,42 @@ __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, 
       const int np = z1 - z0;
       if (lane == 0) {
         CDesc d{(int)e, c, fi, per, z0, np, y0, y1 - y0, S0, pbase, {b.x0, b.x1, b.y0, b.y1, b.z0, b.z1}, {0, 0}};
+        WS_CHK(dbase, g_caps.cdesc);
         cdesc[dbase] = d;
       }
       // windows of 32 planes (a multiple of per, a power of two <= 16): lane L's planes all have
       // the residue L mod per, so its derived planes' source -- the last computed plane of that
       // residue -- is carried across windows per lane
       const unsigned same_res = per > 0 ? (0xffffffffu / ((1u << per) - 1u)) << (lane % per) : 0u;
+      // cplane_derived in O(1): plane z is computed iff some load group's z - oz lies in
+      // [b.z0, b.z1) xor [b.z0 + per, b.z1 + per) = [L1, R1) u [L2, R2), i.e. iff the field's
+      // load-offset mask (bit oz - ld_oz_min, lanes over the groups) has a bit in one of two ranges
+      const int ozmin = F.ld_oz_min;
+      const bool fast = F.ld_oz_max - ozmin < 64;
+      unsigned long long ozm = 0;
+      for (int g = F.g_begin + lane; g < F.g_end; g += 32) {
+        const DGroup gr = K.g[g];
+        if (gr.kind == 0) ozm |= 1ull << ((gr.oz - ozmin) & 63);
+      }
+      ozm = (unsigned long long)__reduce_or_sync(FULL, (unsigned)ozm) |
+            ((unsigned long long)__reduce_or_sync(FULL, (unsigned)(ozm >> 32)) << 32);
+      const int L1 = b.z0, R1 = min(b.z1, b.z0 + per), L2 = max(b.z1, b.z0 + per), R2 = b.z1 + per;
+      auto any_bits = [&](int lo, int hi) {   // a bit of ozm in [lo, hi]
+        lo = max(lo, 0);
+        hi = min(hi, 63);
+        if (hi < lo) return false;
+        const int w = hi - lo + 1;
+        return ((ozm >> lo) & (w == 64 ? ~0ull : ((1ull << w) - 1ull))) != 0ull;
+      };
+      auto derived = [&](int z) {
+        if (!fast) return cplane_derived(K, F, b, z, z0, per);
+        if (per <= 0 || z - per < z0) return false;
+        return !(any_bits(z - R1 + 1 - ozmin, z - L1 - ozmin) || any_bits(z - R2 + 1 - ozmin, z - L2 - ozmin));
+      };
       int ncomp = 0;
       for (int w0 = 0; w0 < np; w0 += 32) {  // count the computed planes (one item atomic per field)
         const int p = w0 + lane;
-        ncomp += __popc(__ballot_sync(FULL, p < np && !cplane_derived(K, F, b, z0 + p, z0, per)));
+        ncomp += __popc(__ballot_sync(FULL, p < np && !derived(z0 + p)));
       }
       unsigned long long at = 0;
       if (lane == 0) at = atomicAdd(cctr + 1, (unsigned long long)ncomp);
@@ -2291,14 +2441,18 @@ __global__ void __launch_bounds__(256) k_cplan(const DPlan* __restrict__ plans, 
       for (int w0 = 0; w0 < np; w0 += 32) {
         const int p = w0 + lane;
         const bool in = p < np;
-        const bool der = in && cplane_derived(K, F, b, z0 + p, z0, per);
+        const bool der = in && derived(z0 + p);
         const unsigned m = __ballot_sync(FULL, in && !der);   // computed planes of the window
         if (der) {
           const unsigned below = m & same_res & ((1u << lane) - 1u);
           const int src = below ? w0 + 31 - __clz(below) : carry;
+          WS_CHK(pbase + p, g_caps.cpool);
           cpool[2 * (pbase + p)].c = -2 - (long long)src;  // derived: its computed source plane
         }
-        if (in && !der) citems[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)dbase | ((uint32_t)p << 20);
+        if (in && !der) {
+          WS_CHK(at + __popc(m & ((1u << lane) - 1u)), g_caps.cpool);
+          citems[at + __popc(m & ((1u << lane) - 1u))] = (uint32_t)dbase | ((uint32_t)p << 20);
+        }
         at += __popc(m);
         const unsigned mr = m & same_res;
         if (mr) carry = w0 + 31 - __clz(mr);
@@ -2399,6 +2553,7 @@ __global__ void __launch_bounds__(256) k_cplanes(const DPlan* __restrict__ plans
     }
     if (lane == 0) {
       const long long bs = Bp >> ls, bl = Bp >> ll;
+      WS_CHK(D.off + p, g_caps.cpool);
       cpool[2 * (D.off + p)] = ps.c ? Tri{ps.f + bs, ps.l + bs, ps.c} : tri_empty();
       cpool[2 * (D.off + p) + 1] = pl.c ? Tri{pl.f + bl, pl.l + bl, pl.c} : tri_empty();
       units += (unsigned long long)ny;
@@ -2431,6 +2586,7 @@ __global__ void __launch_bounds__(256) k_cfold(const DPlan* __restrict__ plans, 
       const long long mk = cpool[2 * (D.off + p)].c;
       if (mk < 0) q = (int)(-mk - 2);   // derived: its computed source plane (k_cplan)
       const long long dsh = (long long)(p - q) * pbytes;
+      WS_CHK(D.off + q, g_caps.cpool);
       const Tri a = cpool[2 * (D.off + q)], bl = cpool[2 * (D.off + q) + 1];
       t[0] = tri_combine(t[0], a.c ? Tri{a.f + (dsh >> ls), a.l + (dsh >> ls), a.c} : tri_empty());
       t[1] = tri_combine(t[1], bl.c ? Tri{bl.f + (dsh >> ll), bl.l + (dsh >> ll), bl.c} : tri_empty());
@@ -2818,6 +2974,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
+    WS_CHK(item - pre[c].ritem, g_caps.clist_stride);
     const long long ci = clist[(long long)c * clist_stride + (item - pre[c].ritem)];
     // the field whose chunk range holds ci: chunk_begin ascends with the field index (fields
     // without chunks repeat their successor's begin), so the last field with begin <= ci and a
@@ -2834,6 +2991,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       while (lo > 0 && !(ci < ri0[lo].chunk_begin + ri0[lo].n_chunks)) --lo;
       fi = lo;
     }
+    WS_CHK((long long)c * kMaxFields + fi, g_caps.rowinfo);
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const DField& F = K.f[fi];
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
@@ -2982,6 +3140,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       __syncwarp();
     }
     if (lane == 0) {
+      WS_CHK(pre[c].chunk + ci, g_caps.max_chunks);
       long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
       const long long bs = Bp >> ls, bl = Bp >> ll;
 #pragma unroll
@@ -3012,8 +3171,9 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restr
   __shared__ Tri s_red[(256 / 32) * kNQ];
   const long long total = pre[n].fold;
   const int tid = threadIdx.x;
+  int c = -1;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    const int c = find_config<5>(pre, n, item);
+    c = find_config_warp<5>(pre, n, item, c);   // 32-ary search by each warp (item CTA-uniform)
     const int fi = (int)(item - pre[c].fold);
     const DPlan& P = plans[c];
     const DField& F = ks[P.kid].f[fi];
@@ -3030,13 +3190,14 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restr
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
     const DGroup* gk = ks[P.kid].g + F.g_begin;
-    const int ngk = F.g_end - F.g_begin, per = plane_period(pz, F.lg_elem, ll);
+    const int per = plane_period(pz, F.lg_elem, ll);
     for (long long k = tid * per_l; k < nch && k < (tid + 1) * per_l; ++k) {
       // derived plane: its representative's triple, translated (plane_rep, as in k_plan)
       const long long pi = k / RI.nseg;
-      const int zr = plane_rep(gk, ngk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
+      const int zr = plane_rep_f(F, gk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
                                P.fd_BF[2], per);
       const long long src = (zr - RI.z0) * RI.nseg + (k - pi * RI.nseg);
+      WS_CHK(pre[c].chunk + RI.chunk_begin + src, g_caps.max_chunks);
       const long long* in = base + src * (kNQ * 3);
       const long long dbytes = ((k - src) / RI.nseg) * pbytes;   // same row segment, whole planes apart
 #pragma unroll
@@ -3081,8 +3242,9 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
   }
   const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
   // one warp per (config, field): lanes take contiguous planes, ordered warp reduction
+  int c = -1;
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nwg) {
-    const int c = find_config<5>(pre, n, item);
+    c = find_config_warp<5>(pre, n, item, c);
     const int fi = (int)(item - pre[c].fold);
     const DPlan& P = plans[c];
     const DField& F = ks[P.kid].f[fi];
@@ -3099,12 +3261,13 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
     const DGroup* gk = ks[P.kid].g + F.g_begin;
-    const int ngk = F.g_end - F.g_begin, per = plane_period(pz, F.lg_elem, ll);
+    const int per = plane_period(pz, F.lg_elem, ll);
     for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
       const long long pi = k / RI.nseg;   // derived plane: its representative's triple, translated
-      const int zr = plane_rep(gk, ngk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
+      const int zr = plane_rep_f(F, gk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
                                P.fd_BF[2], per);
       const long long src = (zr - RI.z0) * RI.nseg + (k - pi * RI.nseg);
+      WS_CHK(pre[c].chunk + RI.chunk_begin + src, g_caps.max_chunks);
       const long long* in = base + src * (kNQ * 3);
       const long long dbytes = ((k - src) / RI.nseg) * pbytes;   // same row segment, whole planes apart
 #pragma unroll
@@ -3186,10 +3349,11 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
   const long long total = pre[n].sect * kSectSeg;
   const int tid = threadIdx.x, nt = blockDim.x;
   unsigned long long my_ops = 0;
+  int c = -1;
   for (long long it2 = blockIdx.x; it2 < total; it2 += gridDim.x) {
     const long long item = it2 / kSectSeg;
     const int seg = (int)(it2 % kSectSeg);
-    const int c = find_config<6>(pre, n, item);
+    c = find_config_warp<6>(pre, n, item, c);
     const int fi = (int)(item - pre[c].sect);
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
@@ -3326,7 +3490,10 @@ __global__ void __launch_bounds__(256) k_sect(const DPlan* __restrict__ plans, c
     const long long pslot = ((long long)c * max_fields + fi) * kSectSeg;
     if (tid == 0) {
 #pragma unroll
-      for (int q = 0; q < kSectNQ; ++q) spart[(pslot + seg) * kSectNQ + q] = t[q];
+      for (int q = 0; q < kSectNQ; ++q) {
+        WS_CHK((pslot + seg) * kSectNQ + q, g_caps.spart);
+        spart[(pslot + seg) * kSectNQ + q] = t[q];
+      }
       __threadfence();
       s_last = atomicAdd(sdone + (long long)c * max_fields + fi, 1u) == (unsigned)(kSectSeg - 1);
     }
@@ -3444,11 +3611,22 @@ __device__ __forceinline__ void shared_row_counts(const DPlan& P, long long c, c
     a[lane] = acc[(long long)P.row_owner * A_N + lane];
 }
 
+// a8 rank key: 64-bit order-preserving (IEEE bits with the sign folded; failed configurations = +inf)
+__device__ __forceinline__ unsigned long long rank_key(const ws_result& r) {
+  if (r.status != WS_OK) return 0xfff0000000000000ull;     // +inf after the fold below
+  const unsigned long long b = (unsigned long long)__double_as_longlong(r.t_pred);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 // one warp per configuration: the accumulators in by the lanes, the model by lane 0, the
-// 336-byte record out by the lanes (coalesced)
+// 336-byte record out by the lanes (coalesced).  With rank_ctr (ws_estimate_ranked_async, n <=
+// kTailMax) the last CTA to finish (threadfence + counter, lists[7], zeroed by k_plan's scan)
+// also ranks the batch: keys of every record, bitonic sort of (key, index) in shared memory (the
+// k_rank_smem network), ranks and top-k -- no separate rank launch.
 __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, int n, const DKernel* __restrict__ ks,
                                                const DGpu* __restrict__ gs, const unsigned long long* __restrict__ acc,
-                                               ws_result* __restrict__ out) {
+                                               ws_result* __restrict__ out, int rank_k, uint32_t* __restrict__ top,
+                                               unsigned long long* __restrict__ rank_ctr) {
   static_assert(sizeof(ws_result) % 8 == 0 && A_N <= 32, "record copy / accumulator lanes");
   __shared__ unsigned long long s_a[4][A_N];
   __shared__ ws_result s_r[4];
@@ -3456,27 +3634,77 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
   __shared__ __align__(16) DGpu s_gp[4];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + w;
-  if (c >= n) return;
-  if (lane < A_N) s_a[w][lane] = acc[(long long)c * A_N + lane];
-  {
-    const uint4* sp = reinterpret_cast<const uint4*>(plans + c);
-    uint4* dp = reinterpret_cast<uint4*>(&s_p[w]);
-    for (int i = lane; i < (int)(sizeof(DPlan) / 16); i += 32) dp[i] = sp[i];
+  if (c < n) {
+    if (lane < A_N) s_a[w][lane] = acc[(long long)c * A_N + lane];
+    {
+      const uint4* sp = reinterpret_cast<const uint4*>(plans + c);
+      uint4* dp = reinterpret_cast<uint4*>(&s_p[w]);
+      for (int i = lane; i < (int)(sizeof(DPlan) / 16); i += 32) dp[i] = sp[i];
+    }
+    __syncwarp();
+    {
+      const int gid = s_p[w].status == WS_OK ? s_p[w].gid : 0;
+      const uint4* sg = reinterpret_cast<const uint4*>(gs + gid);
+      uint4* dg = reinterpret_cast<uint4*>(&s_gp[w]);
+      for (int i = lane; i < (int)(sizeof(DGpu) / 16); i += 32) dg[i] = sg[i];
+    }
+    shared_row_counts(s_p[w], c, acc, s_a[w], lane);
+    __syncwarp();
+    if (lane == 0) model_one(s_p[w], ks, s_gp[w], s_a[w], s_r[w]);
+    __syncwarp();
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s_r[w]);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(out + c);
+    for (int i = lane; i < (int)(sizeof(ws_result) / 8); i += 32) dst[i] = src[i];
   }
-  __syncwarp();
-  {
-    const int gid = s_p[w].status == WS_OK ? s_p[w].gid : 0;
-    const uint4* sg = reinterpret_cast<const uint4*>(gs + gid);
-    uint4* dg = reinterpret_cast<uint4*>(&s_gp[w]);
-    for (int i = lane; i < (int)(sizeof(DGpu) / 16); i += 32) dg[i] = sg[i];
+  if (!rank_ctr) return;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(rank_ctr, 1ull) == (unsigned long long)(gridDim.x - 1);
   }
-  shared_row_counts(s_p[w], c, acc, s_a[w], lane);
-  __syncwarp();
-  if (lane == 0) model_one(s_p[w], ks, s_gp[w], s_a[w], s_r[w]);
-  __syncwarp();
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s_r[w]);
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(out + c);
-  for (int i = lane; i < (int)(sizeof(ws_result) / 8); i += 32) dst[i] = src[i];
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ unsigned long long key[kTailMax];
+  __shared__ uint32_t idx[kTailMax];
+  int P = 32;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    if (i < n) {
+      const ws_result* r = out + i;   // other CTAs' records: through L2
+      ws_result t;
+      t.status = __ldcg(&r->status);
+      t.t_pred = __ldcg(&r->t_pred);
+      key[i] = rank_key(t);
+    } else {
+      key[i] = ~0ull;
+    }
+    idx[i] = (uint32_t)i;
+  }
+  __syncthreads();
+  const int half = P >> 1;
+  for (int kk = 2; kk <= P; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < half; t += blockDim.x) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), l = i + j;
+        const unsigned long long ki = key[i], kl = key[l];
+        const uint32_t ii = idx[i], il = idx[l];
+        const bool gt = ki > kl || (ki == kl && ii > il);
+        if (gt == ((i & kk) == 0)) {
+          key[i] = kl;
+          key[l] = ki;
+          idx[i] = il;
+          idx[l] = ii;
+        }
+      }
+      __syncthreads();
+    }
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const uint32_t cc = idx[p];
+    out[cc].rank = (uint32_t)p;
+    if (p < rank_k && top) top[p] = cc;
+  }
 }
 
 // BJ configs[3] architecture exploration (ws_estimate_multi): the integer stages ran once per
@@ -3546,11 +3774,6 @@ constexpr int kRankTile = 4096;    // tile of the merge path (2048 below kRankSm
 constexpr int kRankSmall = 1 << 15;
 constexpr int kRankMerge = 1 << 18;
 constexpr int kRkTile = 2048;
-__device__ __forceinline__ unsigned long long rank_key(const ws_result& r) {
-  if (r.status != WS_OK) return 0xfff0000000000000ull;     // +inf after the fold below
-  const unsigned long long b = (unsigned long long)__double_as_longlong(r.t_pred);
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
 // CTA b sorts the P-element tile [b*P, b*P+P) of the records (padding: key ~0, sorts last); with
 // skey == nullptr (a single tile) it writes ranks and top-k, else the sorted tile to skey / sidx.
 __global__ void __launch_bounds__(1024) k_rank_smem(ws_result* __restrict__ res, int n, int P, int k,
@@ -3773,7 +3996,7 @@ static void launch_k(bool pdl, void (*kern)(P...), dim3 grid, dim3 block, cudaSt
 
 int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, const DGpu* d_g, int ng,
                     const Scratch& s, ws_result* d_out, const Streams& st, int n_sm_dev, uint32_t* launches,
-                    cudaEvent_t* ev, const FanOut* fan) {
+                    cudaEvent_t* ev, const FanOut* fan, TailRank* tail) {
   // programmatic dependent launches along each chain (not while per-kernel events are recorded
   // between the kernels; WS_PDL=0 disables, A/B)
   static const bool pdl_env = !(getenv("WS_PDL") && getenv("WS_PDL")[0] == '0');
@@ -3795,33 +4018,62 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
 #ifndef WS_PERSIST_SCLASS
 #define WS_PERSIST_SCLASS 16  // A/B: 0.182 vs 0.184 ms (dynamic item fetch; more CTAs fill the SMs sooner)
 #endif
-  const int persist = n_sm_dev * WS_PERSIST;
+  // CTAs per SM of each chain's grid: build defaults, WS_GRID_<NAME> overrides at run time (A/B)
+  auto knob = [](const char* name, int def) {
+    const char* v = getenv(name);
+    return v && atoi(v) > 0 ? atoi(v) : def;
+  };
+  static const int g_warp = knob("WS_GRID_WARP", WS_PERSIST), g_rows = knob("WS_GRID_ROWS", WS_PERSIST_ROWS),
+                   g_sclass = knob("WS_GRID_SCLASS", WS_PERSIST_SCLASS), g_smset = knob("WS_GRID_SMSET", 8),
+                   g_cplan = knob("WS_GRID_CPLAN", 4), g_cplanes = knob("WS_GRID_CPLANES", 8),
+                   g_fold = knob("WS_GRID_FOLD", 4), g_cfold = knob("WS_GRID_CFOLD", 2);
+  const int persist = n_sm_dev * g_warp;
   cudaStream_t m = st.main, a = st.aux[0], b = st.aux[1];
+#ifdef WS_CHECK
+  {  // capacities of this call's scratch layout (the check build never captures graphs)
+    static CheckCaps hc;
+    hc = CheckCaps{(long long)s.max_chunks, (long long)s.clist_stride, (long long)n * kWSlots, (long long)n * kSSlots,
+                   (long long)s.cdesc_cap, (long long)s.cpool_cap, (long long)n * s.max_fields * kSectSeg * kSectNQ,
+                   (long long)n * kMaxFields, (long long)n * kMaxInstr};
+    cudaMemcpyToSymbolAsync(g_caps, &hc, sizeof(hc), 0, cudaMemcpyHostToDevice, m);
+    cudaStreamSynchronize(m);
+  }
+#endif
   beg(K_PLAN, m);
   k_plan<<<n, WS_PLAN_THREADS, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
                            s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields, s.epoch,
                            s.rowtab, s.clist, s.clist_stride);  // its last CTA scans
   end(K_PLAN, m);
-  // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on main
+  // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on the main stream.  WS_ROWMAIN=1
+  // swaps the row and warp chains so that k_rows is k_plan's programmatic dependent (its CTAs
+  // launch while k_plan runs): A/B on B200, configs[1] 0.125 vs 0.123 ms -- the early k_rows CTAs
+  // hold SM slots the other chains' first kernels need -- so off by default
+  static const bool rowmain = getenv("WS_ROWMAIN") && getenv("WS_ROWMAIN")[0] == '1';
   cudaEventRecord(st.fork, m);
   cudaStreamWaitEvent(a, st.fork, 0);
   cudaStreamWaitEvent(b, st.fork, 0);
-  beg(K_ROWS, b);
-  k_rows<<<n_sm_dev * WS_PERSIST_ROWS, kRowWarps * 32, 0, b>>>(s.plans, s.prefix, n, d_k, d_g, s.rowinfo, s.chunkres, s.work,
-                                                             s.clist, s.clist_stride);
-  end(K_ROWS, b);
+  {
+    const cudaStream_t r = rowmain ? m : b;
+    b = rowmain ? b : m;   // the warp chain's stream from here on
+    m = r;                 // ... and the row chain's (joins on the caller's stream below)
+  }
+  beg(K_ROWS, m);
+  launch_k(pdl && rowmain, k_rows, n_sm_dev * g_rows, kRowWarps * 32, m, (const DPlan*)s.plans,
+           (const DPrefix*)s.prefix, n, d_k, d_g, (const DRowInfo*)s.rowinfo, s.chunkres, s.work,
+           (const uint32_t*)s.clist, (long long)s.clist_stride);
+  end(K_ROWS, m);
 #ifdef WS_ROWS_TRACE
-  k_rowtrace_dump<<<1, 1, 0, b>>>(s.prefix, n);
+  k_rowtrace_dump<<<1, 1, 0, m>>>(s.prefix, n);
 #endif
-  beg(K_FOLD, b);
+  beg(K_FOLD, m);
   static const int fold_mode = getenv("WS_FOLD_MODE") ? atoi(getenv("WS_FOLD_MODE")) : 0;  // diagnostics
-  launch_k(pdl, k_fold, n_sm_dev * 4, 256, b, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
+  launch_k(pdl, k_fold, n_sm_dev * g_fold, 256, m, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
            (const DRowInfo*)s.rowinfo, (const long long*)s.chunkres, s.acc, (int)fold_mode);
-  end(K_FOLD, b);
+  end(K_FOLD, m);
   beg(K_SMSET, a);
   k_spairs<<<n_sm_dev * 4, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist,
                                                   s.dlist, s.skey, s.dmask, s.gkey);
-  launch_k(pdl, k_smset, n_sm_dev * 8, kSmsetThreads, a, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
+  launch_k(pdl, k_smset, n_sm_dev * g_smset, kSmsetThreads, a, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
            s.scnt, s.srep, s.lists, s.slist, s.dlist, s.skey, s.dmask, (const unsigned long long*)s.gkey);
   ++L;
   end(K_SMSET, a);
@@ -3831,17 +4083,17 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     CDesc* cd = (CDesc*)s.cdesc;
     Tri* cp = (Tri*)s.cpool;
     unsigned long long* cctr = s.lists + 4;  // descriptors, pool planes, items (zeroed with the lists)
-    launch_k(pdl, k_cplan, n_sm_dev * 4, 256, a, (const DPlan*)s.plans, d_k, d_g, (const unsigned long long*)s.lists,
+    launch_k(pdl, k_cplan, n_sm_dev * g_cplan, 256, a, (const DPlan*)s.plans, d_k, d_g, (const unsigned long long*)s.lists,
              (const unsigned long long*)s.slist, (const unsigned long long*)s.srep, s.sval, s.cfbl, cd, cp, s.citems,
              cctr, (long long)s.cdesc_cap, (long long)s.cpool_cap);
-    launch_k(pdl, k_cplanes, n_sm_dev * 8, 256, a, (const DPlan*)s.plans, d_k, d_g, (const CDesc*)cd, cp,
+    launch_k(pdl, k_cplanes, n_sm_dev * g_cplanes, 256, a, (const DPlan*)s.plans, d_k, d_g, (const CDesc*)cd, cp,
              (const uint32_t*)s.citems, (const unsigned long long*)cctr, s.work);
-    launch_k(pdl, k_cfold, n_sm_dev * 2, 256, a, (const DPlan*)s.plans, d_k, d_g, (const unsigned long long*)s.slist,
+    launch_k(pdl, k_cfold, n_sm_dev * g_cfold, 256, a, (const DPlan*)s.plans, d_k, d_g, (const unsigned long long*)s.slist,
              (const unsigned int*)s.scnt, (const CDesc*)cd, (const Tri*)cp, (const unsigned long long*)cctr, s.acc,
              s.sval);
     L += 3;
   }
-  launch_k(pdl, k_sclass, n_sm_dev * WS_PERSIST_SCLASS, WS_SCLASS_THREADS, a, (const DPlan*)s.plans, d_k, d_g, s.acc,
+  launch_k(pdl, k_sclass, n_sm_dev * g_sclass, WS_SCLASS_THREADS, a, (const DPlan*)s.plans, d_k, d_g, s.acc,
            (const unsigned int*)s.scnt, (const unsigned long long*)s.srep, s.lists, (const unsigned long long*)s.slist,
            (const unsigned long long*)s.dlist, s.work, s.sval, (const unsigned int*)s.dmask,
            (const uint32_t*)(cplanes ? s.cfbl : nullptr), (const unsigned long long*)(s.lists + 4));
@@ -3852,33 +4104,40 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
 #endif
   ++L;
   end(K_SCLASS, a);
-  beg(K_INSTR, m);
-  k_instr<<<n, 128, 0, m>>>(d_k, s.plans, s.instr, s.wcnt, n);
-  end(K_INSTR, m);
-  beg(K_WARP, m);
-  launch_k(pdl, k_warp, persist, 256, m, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, (const DInstr*)s.instr, d_k,
+  beg(K_INSTR, b);
+  k_instr<<<n, 128, 0, b>>>(d_k, s.plans, s.instr, s.wcnt, n);
+  end(K_INSTR, b);
+  beg(K_WARP, b);
+  launch_k(pdl, k_warp, persist, 256, b, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, (const DInstr*)s.instr, d_k,
            d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
-  end(K_WARP, m);
-  beg(K_WCLASS, m);
-  launch_k(pdl, k_wclass, persist, 256, m, (const DPlan*)s.plans, (const DInstr*)s.instr, d_k, d_g, s.acc,
-           (const unsigned int*)s.wcnt, (const unsigned long long*)s.wrep, s.lists, (const unsigned long long*)s.wlist,
+  end(K_WARP, b);
+  beg(K_WCLASS, b);
+  launch_k(pdl, k_wclass, persist, 256, b, (const DPlan*)s.plans, (const DInstr*)s.instr, d_k, d_g, s.acc,
+           s.wcnt, (const unsigned long long*)s.wrep, s.lists, (const unsigned long long*)s.wlist,
            s.work);
-  end(K_WCLASS, m);
-  beg(K_SECT, m);
-  launch_k(pdl, k_sect, n_sm_dev * WS_SECT_CTAS, 256, m, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
+  end(K_WCLASS, b);
+  beg(K_SECT, b);
+  launch_k(pdl, k_sect, n_sm_dev * WS_SECT_CTAS, 256, b, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
            s.acc, s.work, (Tri*)s.spart, s.sdone, (int)s.max_fields);
-  end(K_SECT, m);
+  end(K_SECT, b);
   // join
-  cudaEventRecord(st.join[0], a);
-  cudaEventRecord(st.join[1], b);
-  cudaStreamWaitEvent(m, st.join[0], 0);
-  cudaStreamWaitEvent(m, st.join[1], 0);
+  {  // join the other two chains into the caller's stream, which runs the model
+    const cudaStream_t other = m == st.main ? b : m;
+    m = st.main;
+    cudaEventRecord(st.join[0], a);
+    cudaEventRecord(st.join[1], other);
+    cudaStreamWaitEvent(m, st.join[0], 0);
+    cudaStreamWaitEvent(m, st.join[1], 0);
+  }
   beg(K_MODEL, m);
-  if (fan)
+  if (tail && !fan && n <= kTailMax) {   // ws_estimate_ranked_async: the model's last CTA ranks
+    k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out, tail->k, tail->top, s.lists + 7);
+    tail->done = 1;
+  } else if (fan)
     k_model_fan<<<(unsigned)(((long long)fan->m * fan->n_gpu + 3) / 4), 128, 0, m>>>(s.plans, d_k, d_g, s.acc, *fan,
                                                                                     d_out);
   else
-    k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out);
+    k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out, 0, nullptr, nullptr);
   end(K_MODEL, m);
   if (launches) *launches = L;
   return check_launch();

@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libwsb200.so")
+# WS_LIB selects another in-tree build of the same ABI (the bounds-check build libwsb200_check.so)
+LIB_PATH = os.environ.get("WS_LIB") or os.path.join(_PKG, "libwsb200.so")
 
 U32, I32, I64, U64, F64 = C.c_uint32, C.c_int32, C.c_int64, C.c_uint64, C.c_double
 
@@ -80,7 +81,7 @@ EXPORTS = ["ws_create", "ws_destroy", "ws_last_error", "ws_set_stream", "ws_desc
            "ws_estimate", "ws_estimate_async", "ws_rank", "ws_rank_async", "ws_last_launch_count",
            "ws_profile_enable", "ws_profile_read", "ws_kernel_name", "ws_work_read", "ws_simulate",
            "ws_sim_release", "ws_fit_gompertz", "ws_validate_stencil25", "ws_validate_lbm15",
-           "ws_estimate_multi", "ws_estimate_multi_async", "ws_last_group_count"]
+           "ws_estimate_multi", "ws_estimate_multi_async", "ws_last_group_count", "ws_estimate_ranked_async", "ws_check_read"]
 
 _lib = None
 
@@ -105,6 +106,8 @@ def load_library(path: str = LIB_PATH):
     L.ws_describe_gpu.argtypes = [P, C.POINTER(ws_gpu), C.POINTER(U32)]
     L.ws_estimate.argtypes = [P, P, C.c_size_t, P]
     L.ws_estimate_async.argtypes = [P, P, C.c_size_t, P]
+    L.ws_estimate_ranked_async.argtypes = [P, P, C.c_size_t, P, C.c_size_t, P]
+    L.ws_check_read.argtypes = [P, P]
     L.ws_estimate_multi.argtypes = [P, P, C.c_size_t, P, U32, P]
     L.ws_estimate_multi_async.argtypes = [P, P, C.c_size_t, P, U32, P]
     L.ws_last_group_count.argtypes = [P]
@@ -253,6 +256,11 @@ class Context:
         """Device pointers; enqueued on the context stream."""
         self._check(self.L.ws_estimate_async(self.h, C.c_void_p(d_cfgs), n, C.c_void_p(d_out)))
 
+    def estimate_ranked_async(self, d_cfgs: int, n: int, d_out: int, k: int, d_top: int | None):
+        """estimate_async + rank_async as one enqueue (model and ranking fused for n <= 1024)."""
+        self._check(self.L.ws_estimate_ranked_async(self.h, C.c_void_p(d_cfgs), n, C.c_void_p(d_out), k,
+                                                    C.c_void_p(d_top or 0)))
+
     def estimate_multi(self, cfgs: np.ndarray, gpu_ids) -> np.ndarray:
         """Every configuration against every hardware set: -> (n_gpu, n) RESULT_DTYPE array."""
         cfgs = np.ascontiguousarray(cfgs, dtype=CONFIG_DTYPE)
@@ -267,6 +275,12 @@ class Context:
         ids = np.ascontiguousarray(gpu_ids, dtype=np.uint32)
         self._check(self.L.ws_estimate_multi_async(self.h, C.c_void_p(d_cfgs), n, ids.ctypes.data, len(ids),
                                                    C.c_void_p(d_out)))
+
+    def check_read(self):
+        """Bounds-check build counters: (is_check_build, violations, line, index, capacity)."""
+        out = (C.c_uint64 * 5)()
+        self._check(self.L.ws_check_read(self.h, out))
+        return tuple(int(v) for v in out)
 
     def last_group_count(self) -> int:
         return int(self.L.ws_last_group_count(self.h))

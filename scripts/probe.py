@@ -33,10 +33,14 @@ def run(name, k, g, cfgs, reps=20):
     for kname, (ms, cnt) in prof.items():
         if cnt: print(f"   {kname:8s} {ms/cnt:9.4f} ms")
 
-run("configs1 K25 512^3 A100 168", W.k25(512), W.gpu_a100(), W.space_stencil_paper())
-if len(sys.argv) > 1 and sys.argv[1] == "configs1":
-    sys.exit(0)
-run("configs2 LBM15 256^3 A100 49", W.lbm15(256), W.gpu_a100(), W.space_lbm())
-run("configs2 LBM27 256^3 A100 49", W.lbm27(256), W.gpu_a100(), W.space_lbm())
-run("configs0 K7 64^3 V100 16", W.k7(64), W.gpu_v100(), W.space_k7())
-run("extended K25 512^3 A100", W.k25(512), W.gpu_a100(), W.space_extended(), reps=3)
+WORK = {
+    "configs1": ("configs1 K25 512^3 A100 168", lambda: (W.k25(512), W.gpu_a100(), W.space_stencil_paper()), 20),
+    "lbm15": ("configs2 LBM15 256^3 A100 49", lambda: (W.lbm15(256), W.gpu_a100(), W.space_lbm()), 20),
+    "lbm27": ("configs2 LBM27 256^3 A100 49", lambda: (W.lbm27(256), W.gpu_a100(), W.space_lbm()), 20),
+    "configs0": ("configs0 K7 64^3 V100 16", lambda: (W.k7(64), W.gpu_v100(), W.space_k7()), 20),
+    "extended": ("extended K25 512^3 A100", lambda: (W.k25(512), W.gpu_a100(), W.space_extended()), 3),
+}
+# python scripts/probe.py [name ...]  (default: all; "configs1" alone as before)
+for name in (sys.argv[1:] or list(WORK)):
+    label, mk, reps = WORK[name]
+    run(label, *mk(), reps=reps)

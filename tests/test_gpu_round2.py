@@ -143,3 +143,41 @@ def test_estimate_multi_vs_oracle_sampled(ctx):
         a = result_dicts(multi[g][i:i + 1])[0]
         errs += compare(a, o, f"set{g} cfg{i} {c}")
     assert not errs, "\n".join(errs)
+
+
+@pytest.mark.parametrize("case", ["c0_16", "c1_168", "ext_1024", "ext_1025", "one"])
+def test_estimate_ranked_byte_identical(ctx, case):
+    """ws_estimate_ranked_async (model + rank fused into one CTA for n <= 1024) = ws_estimate_async
+    followed by ws_rank_async, record bytes and top-k, over graph capture and replays."""
+    import torch
+    from paper_2204_14242_b200 import config_array
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+    k, space = {
+        "c0_16": (W.k25(64), W.space_stencil_paper()[::11]),
+        "c1_168": (W.k25(96), W.space_stencil_paper()),
+        "ext_1024": (W.k25(48), W.space_extended()[:1024]),
+        "ext_1025": (W.k25(48), W.space_extended()[:1025]),
+        "one": (W.k25(32), W.space_stencil_paper()[5:6]),
+    }[case]
+    kid, gid = ctx.describe_kernel(k), ctx.describe_gpu(W.gpu_a100())
+    a = config_array(kid, gid, space)
+    n, kt = len(a), min(10, len(a))
+    dc = torch.from_numpy(a.view(np.uint8).copy()).cuda()
+    ref = torch.zeros(n * RESULT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    rtop = torch.zeros(kt, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    ctx.estimate_async(dc.data_ptr(), n, ref.data_ptr())
+    ctx.rank_async(ref.data_ptr(), n, kt, rtop.data_ptr())
+    torch.cuda.synchronize()
+    out = torch.zeros_like(ref)
+    top = torch.zeros_like(rtop)
+    for rep in range(3):
+        out.zero_()
+        top.zero_()
+        torch.cuda.synchronize()
+        ctx.estimate_ranked_async(dc.data_ptr(), n, out.data_ptr(), kt, top.data_ptr())
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes(), (case, rep)
+        assert top.cpu().tolist() == rtop.cpu().tolist(), (case, rep)
+    r = np.frombuffer(ref.cpu().numpy().tobytes(), dtype=RESULT_DTYPE)
+    assert sorted(r["rank"].tolist()) == list(range(n))
