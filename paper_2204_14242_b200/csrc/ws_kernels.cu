@@ -981,35 +981,43 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
       s_ri[fi] = ri;
     }
     wbar();
+    __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' plane counts (fields with chunks)
     if (tid == 0) {
       long long cb = 0;
+      int zo = 0;
       for (int fi = 0; fi < K.n_fields; ++fi) {
         s_ri[fi].chunk_begin = cb;
         cb += s_ri[fi].n_chunks;
+        s_zoff[fi] = zo;
+        if (s_ri[fi].n_chunks > 0) zo += (int)s_ri[fi].nz;
       }
+      s_zoff[K.n_fields] = zo;
       s_nri = 0;
     }
     wbar();
     // k_rows items: the chunks of computed planes (plane_rep(z) == z), listed per configuration;
-    // derived planes are folded from their representative by k_fold (same rule)
-    for (int fi = 0; fi < K.n_fields; ++fi) {
-      const DRowInfo ri = s_ri[fi];
-      if (ri.n_chunks == 0) continue;
+    // derived planes are folded from their representative by k_fold (same rule).  The (field,
+    // plane) pairs of all fields are one flat range over the worker threads (LBM: many fields of
+    // few planes each).
+    const int nzt = s_zoff[K.n_fields];
+    int fi = 0;
+    for (int t = tid; t < nzt; t += kPlanWork) {
+      while (s_zoff[fi + 1] <= t) ++fi;   // t ascends per thread: the field index only advances
+      const DRowInfo& ri = s_ri[fi];
       const DField& F = K.f[fi];
       long long py, pz, falign;
       field_rows(F, P, ll, py, pz, falign);
       const int per = plane_period(pz, F.lg_elem, ll);
-      for (int zi = tid; zi < (int)ri.nz; zi += kPlanWork) {
-        const int z = (int)ri.z0 + zi;
-        if (plane_rep_f(F, K.g + F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2], P.fd_BF[2],
-                        per) != z)
-          continue;
-        const int at = atomicAdd(&s_nri, (int)ri.nseg);
-        for (int sg = 0; sg < (int)ri.nseg; ++sg) {
-          WS_CHK(at + sg, g_caps.clist_stride);
-          WS_CHK((long long)c * clist_stride + at + sg, g_caps.max_chunks);
-          cl[at + sg] = (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
-        }
+      const int zi = t - s_zoff[fi];
+      const int z = (int)ri.z0 + zi;
+      if (plane_rep_f(F, K.g + F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2], P.fd_BF[2],
+                      per) != z)
+        continue;
+      const int at = atomicAdd(&s_nri, (int)ri.nseg);
+      for (int sg = 0; sg < (int)ri.nseg; ++sg) {
+        WS_CHK(at + sg, g_caps.clist_stride);
+        WS_CHK((long long)c * clist_stride + at + sg, g_caps.max_chunks);
+        cl[at + sg] = (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
       }
     }
   }
@@ -1370,120 +1378,104 @@ struct SmBox {
 };
 constexpr int kMaxMembers = 32;
 
-// (flat-row variant, used for single-block class representatives: small boxes, no plane reuse)
-// Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
-// dispatch, Q9), row by row.  A row (y,z) of field phi holds element x iff some member's
-// box contains (x - ox, y - oy, z - oz) for a load offset o: per (row, offset group) the
-// member boxes are tested with compares only and the candidate intervals (member, x-run)
-// collected in a bitmask (<= 4 members) for the union.  Every thread of the CTA
-// participates; totals in thread 0.
-__device__ void smset_eval(const DPlan& P, const DKernel& K, const DGpu& G, long long S0, long long kj, long long nsm,
-                           DGroup* s_g, int* s_ng, long long* s_box, SmBox* s_mb, Tri* s_red,
-                           unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units) {
-  const int tid = threadIdx.x;
+// One block (single-block SM-set class of a kernel with many load fields, LBM): fields are
+// independent (they never alias), so each warp takes whole fields -- the field's footprint box
+// rows in contiguous lane chunks, per row the union of the load groups' x-intervals, an ordered
+// warp reduction of (sectors, lines) -- and the per-field counts add up (shared atomics).  No
+// CTA barrier per field (smset_eval's flat rows synchronise the CTA twice per field).
+__device__ void smset_eval_warps(const DPlan& P, const DKernel& K, const DGpu& G, long long S0,
+                                 unsigned long long* s_sum, unsigned long long& sum_s, unsigned long long& sum_l,
+                                 unsigned long long& units) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int lg_sec = G.lg_sector, lg_line = G.lg_line;
-  sum_s = sum_l = 0;
-  units = 0;
-  const int nm = (int)(kj < kMaxMembers ? kj : kMaxMembers);
-  __syncthreads();
-  for (int m = tid; m < nm; m += blockDim.x) {
-    const long long Bm = S0 + (long long)m * nsm;
-    const long long bc[3] = {Bm % P.G[0], (Bm / P.G[0]) % P.G[1], Bm / (P.G[0] * P.G[1])};
-    long long lo[3], hi[3];
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = P.lo[d] + bc[d] * P.BF[d];
-      hi[d] = lo[d] + P.BF[d];
-      if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
-    }
-    s_mb[m] = SmBox{lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]};
+  const long long bc[3] = {S0 % P.G[0], (S0 / P.G[0]) % P.G[1], S0 / (P.G[0] * P.G[1])};
+  long long lo[3], hi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = P.lo[d] + bc[d] * P.BF[d];
+    hi[d] = lo[d] + P.BF[d];
+    if (hi[d] > P.hi[d]) hi[d] = P.hi[d];
   }
-  for (int fi = 0; fi < K.n_fields; ++fi) {
+  if (threadIdx.x < 3) s_sum[threadIdx.x] = 0ull;
+  __syncthreads();
+  unsigned long long my_s = 0, my_l = 0, my_u = 0;
+  for (int fi = wid; fi < K.n_fields; fi += nw) {
     const DField& F = K.f[fi];
     if (!(F.kinds & 1)) continue;
-    __syncthreads();
-    if (tid == 0) {
-      int ng = 0;
-      for (int g = F.g_begin; g < F.g_end; ++g)
-        if (K.g[g].kind == 0) s_g[ng++] = K.g[g];
-      *s_ng = ng;
-      long long ylo = LLONG_MAX, yhi = LLONG_MIN, zlo = LLONG_MAX, zhi = LLONG_MIN;
-      for (int m = 0; m < nm; ++m) {
-        ylo = min(ylo, s_mb[m].y0);
-        yhi = max(yhi, s_mb[m].y1);
-        zlo = min(zlo, s_mb[m].z0);
-        zhi = max(zhi, s_mb[m].z1);
-      }
-      long long y0 = ylo + F.ld_oy_min, y1 = yhi + F.ld_oy_max, z0 = zlo + F.ld_oz_min, z1 = zhi + F.ld_oz_max;
-      if (y0 < 0) y0 = 0;
-      if (z0 < 0) z0 = 0;
-      if (y1 > F.ext[1]) y1 = F.ext[1];
-      if (z1 > F.ext[2]) z1 = F.ext[2];
-      s_box[0] = y0;
-      s_box[1] = y1 > y0 ? y1 - y0 : 0;
-      s_box[2] = z0;
-      s_box[3] = z1 > z0 ? z1 - z0 : 0;
-    }
-    __syncthreads();
-    const int ng = *s_ng;
-    const long long y0 = s_box[0], ny = s_box[1], z0 = s_box[2], nz = s_box[3];
-    const long long rows = ny * nz;
-    units += (unsigned long long)rows;
+    long long y0 = lo[1] + F.ld_oy_min, y1 = hi[1] + F.ld_oy_max, z0 = lo[2] + F.ld_oz_min, z1 = hi[2] + F.ld_oz_max;
+    if (y0 < 0) y0 = 0;
+    if (z0 < 0) z0 = 0;
+    if (y1 > F.ext[1]) y1 = F.ext[1];
+    if (z1 > F.ext[2]) z1 = F.ext[2];
+    const long long ny = y1 > y0 ? y1 - y0 : 0, nz = z1 > z0 ? z1 - z0 : 0, rows = ny * nz;
+    if (rows == 0) continue;
+    my_u += (unsigned long long)rows;
     const long long align = F.align, py = F.pitch[1], pz = F.pitch[2];
     const int le = F.lg_elem;
-    Tri carry_s = tri_empty(), carry_l = tri_empty();
-    for (long long base = 0; base < rows; base += (long long)blockDim.x * kRowsPerThread) {
-      Tri t[2] = {tri_empty(), tri_empty()};
-      for (int u = 0; u < kRowsPerThread; ++u) {
-        const long long i = base + (long long)tid * kRowsPerThread + u;
-        if (i >= rows) break;
-        const long long z = z0 + i / ny, y = y0 + i % ny;
-        const long long R0 = align + ((py * y + pz * z) << le);
-        if (nm <= 4) {
-          unsigned long long mk = 0;
-          for (int g = 0; g < ng; ++g) {
-            const DGroup gr = s_g[g];
-            const long long yy = y - gr.oy, zz = z - gr.oz;
-            for (int m = 0; m < nm; ++m) {
-              const SmBox& bx = s_mb[m];
-              if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1) mk |= 1ull << (m * 16 + gr.run);
-            }
+    const long long step = py << le;
+    // lanes take contiguous planes; in a plane the rows split into runs between the groups'
+    // y edges (lo1 + oy, hi1 + oy), the rows of a run have the same candidates and are
+    // translates by the row pitch: run_triple evaluates one period of them
+    const long long pper = (nz + 31) / 32;
+    Tri t[2] = {tri_empty(), tri_empty()};
+    for (long long z = z0 + lane * pper; z < z1 && z < z0 + (lane + 1) * pper; ++z) {
+      long long cur = y0;
+      while (cur < y1) {
+        unsigned mk = 0;   // runs whose group's cell row (y - oy, z - oz) lies in the block
+        long long nxt = y1;
+        for (int g = F.g_begin; g < F.g_end; ++g) {
+          const DGroup gr = K.g[g];
+          const long long zz = z - gr.oz;
+          if (gr.kind != 0 || zz < lo[2] || zz >= hi[2]) continue;
+          const long long ya = lo[1] + gr.oy, yb = hi[1] + gr.oy;
+          if (cur >= ya && cur < yb) {
+            mk |= 1u << gr.run;
+            nxt = yb < nxt ? yb : nxt;
+          } else if (ya > cur && ya < nxt) {
+            nxt = ya;
           }
-          auto gen = [&](auto&& cb) {
-            unsigned long long q = mk;
-            while (q) {
-              const int b = __ffsll((long long)q) - 1;
-              q &= q - 1;
-              const SmBox& bx = s_mb[b >> 4];
-              cb(bx.x0 + F.run_lo[b & 15], bx.x1 + F.run_hi[b & 15]);
-            }
-          };
-          row_union(gen, R0, le, lg_sec, lg_line, &t[0], &t[1]);
-        } else {
-          auto gen = [&](auto&& cb) {
-            for (int g = 0; g < ng; ++g) {
-              const DGroup gr = s_g[g];
-              const long long yy = y - gr.oy, zz = z - gr.oz;
-              for (int m = 0; m < nm; ++m) {
-                const SmBox& bx = s_mb[m];
-                if (yy >= bx.y0 && yy < bx.y1 && zz >= bx.z0 && zz < bx.z1)
-                  cb(bx.x0 + F.run_lo[gr.run], bx.x1 + F.run_hi[gr.run]);
-              }
-            }
-          };
-          row_union(gen, R0, le, lg_sec, lg_line, &t[0], &t[1]);
         }
-      }
-      cta_ordered_reduce<2>(t, s_red);
-      if (tid == 0) {
-        carry_s = tri_combine(carry_s, t[0]);
-        carry_l = tri_combine(carry_l, t[1]);
+        if (mk) {
+          const long long R0 = align + ((py * cur + pz * z) << le);
+          auto gen = [&](auto&& cb) {
+            unsigned q = mk;
+            while (q) {
+              const int b = __ffs(q) - 1;
+              q &= q - 1;
+              cb(lo[0] + F.run_lo[b], hi[0] + F.run_hi[b]);
+            }
+          };
+          const int run = (int)(nxt - cur);
+          t[0] = tri_combine(t[0], run_triple([&](int r) {
+            Tri x = tri_empty();
+            row_union(gen, R0 + r * step, le, lg_sec, lg_line, &x, nullptr);
+            return x;
+          }, step, run, lg_sec));
+          t[1] = tri_combine(t[1], run_triple([&](int r) {
+            Tri x = tri_empty();
+            row_union(gen, R0 + r * step, le, lg_sec, lg_line, nullptr, &x);
+            return x;
+          }, step, run, lg_line));
+        }
+        cur = nxt;
       }
     }
-    if (tid == 0) {
-      sum_s += (unsigned long long)carry_s.c;
-      sum_l += (unsigned long long)carry_l.c;
+    warp_ordered_reduce<2>(t);
+    if (lane == 0) {
+      my_s += (unsigned long long)t[0].c;
+      my_l += (unsigned long long)t[1].c;
     }
   }
+  if (lane == 0) {
+    if (my_s) atomicAdd(&s_sum[0], my_s);
+    if (my_l) atomicAdd(&s_sum[1], my_l);
+    if (my_u) atomicAdd(&s_sum[2], my_u);
+  }
+  __syncthreads();
+  sum_s = s_sum[0];
+  sum_l = s_sum[1];
+  units = s_sum[2];
+  __syncthreads();
 }
 
 // ---- 32-bit plane-relative arithmetic for k_rows ---------------------------------------------
@@ -1667,6 +1659,68 @@ __device__ __noinline__ T32x2 smset_run(const SmBox32* mb, int nm, const DKernel
   }
   return o;
 }
+// smset_run over the plane's active (group, member) pairs only (SmWarp::gm / gl): a member box
+// that the group's plane z - oz misses contributes nothing to any row of the plane
+__device__ __noinline__ T32x2 smset_run_g(const SmBox32* mb, int nm, const unsigned* gm, const unsigned char* gl,
+                                          int ngl, const DKernel& K, const DField& F, int g0, int y, int R0, int step,
+                                          int run, int le, int ls, int ll) {
+  unsigned long long mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < ngl; ++i) {
+    const DGroup gr = K.g[g0 + gl[i]];
+    const int yy = y - gr.oy;
+    unsigned q = gm[i];
+    while (q) {
+      const int m = __ffs(q) - 1;
+      q &= q - 1;
+      const SmBox32& bx = mb[m];
+      if (yy >= bx.y0 && yy < bx.y1) mk[m >> 2] |= 1ull << ((m & 3) * 16 + gr.run);
+    }
+  }
+  auto gen = [&](auto&& cb) {
+    for (int w = 0; w < ((nm + 3) >> 2); ++w) {
+      unsigned long long q = mk[w];
+      while (q) {
+        const int bb = __ffsll((long long)q) - 1;
+        q &= q - 1;
+        const SmBox32& bx = mb[w * 4 + (bb >> 4)];
+        cb(bx.x0 + F.run_lo[bb & 15], bx.x1 + F.run_hi[bb & 15]);
+      }
+    }
+  };
+  const int INF = 0x7fffffff;
+  int mn_s = INF, mx_s = -INF, mn_e = INF, mx_e = -INF;
+  gen([&](int xs, int xe) {
+    mn_s = xs < mn_s ? xs : mn_s;
+    mx_s = xs > mx_s ? xs : mx_s;
+    mn_e = xe < mn_e ? xe : mn_e;
+    mx_e = xe > mx_e ? xe : mx_e;
+  });
+  T32x2 o{t32_empty(), t32_empty()};
+  if (mn_s == INF) return o;
+  if (mx_s <= mn_e) {
+    const int a0 = R0 + (mn_s << le), a1 = R0 + ((mx_e - 1) << le);
+    o.s = run_triple32([&](int r) {
+      const int s0 = (a0 + r * step) >> ls, s1 = (a1 + r * step) >> ls;
+      return T32{s0, s1, s1 - s0 + 1};
+    }, step, run, ls);
+    o.l = run_triple32([&](int r) {
+      const int s0 = (a0 + r * step) >> ll, s1 = (a1 + r * step) >> ll;
+      return T32{s0, s1, s1 - s0 + 1};
+    }, step, run, ll);
+  } else {
+    o.s = run_triple32([&](int r) {
+      T32 x = t32_empty();
+      row_union32(gen, R0 + r * step, le, ls, x);
+      return x;
+    }, step, run, ls);
+    o.l = run_triple32([&](int r) {
+      T32 x = t32_empty();
+      row_union32(gen, R0 + r * step, le, ll, x);
+      return x;
+    }, step, run, ll);
+  }
+  return o;
+}
 // Unique load sectors / lines of the blocks {S0 + m*nsm : m < kj} (one SM set, round-robin
 // dispatch, Q9) by one CTA.  Row (y,z) of field phi holds element x iff some member box
 // contains (x - ox, y - oy, z - oz) for a load offset o.  Per z-plane: if every
@@ -1677,6 +1731,10 @@ __device__ __noinline__ T32x2 smset_run(const SmBox32* mb, int nm, const DKernel
 struct SmWarp {
   unsigned bm[kSegRowsS / 32];
   short rs[kSegRowsS + 2];
+  // the computed plane's active (load group, members) pairs: group gl[i] reaches the plane
+  // z - oz inside exactly the members of gm[i] (ngl entries)
+  unsigned gm[kMaxAcc];
+  unsigned char gl[kMaxAcc];
 };
 
 // msk: 0 = every member S0 + m * nsm (m < kj); else only the members m whose bit is set (one
@@ -1778,18 +1836,32 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
           const long long Bp = (R0p >> ll) << ll;
           const int off0 = (int)(R0p - Bp), step = (int)pystep;
           T32 ps = t32_empty(), pl = t32_empty();
+          // the plane's active (load group, members) pairs: one ballot over the members per group
+          int ngl = 0;
+          for (int g = 0; g < ng; ++g) {
+            const DGroup gr = K.g[g0 + g];
+            if (gr.kind != 0) continue;
+            const int zz = z - gr.oz;
+            const unsigned mm = __ballot_sync(FULL, lane < nm && zz >= mb32[lane].z0 && zz < mb32[lane].z1);
+            if (mm) {
+              if (lane == 0) {
+                Wp.gm[ngl] = mm;
+                Wp.gl[ngl] = (unsigned char)g;
+              }
+              ++ngl;
+            }
+          }
+          __syncwarp();
           for (int ys = 0; ys < (int)ny; ys += kSegRowsS) {
             const int nseg = (int)ny - ys < kSegRowsS ? (int)ny - ys : kSegRowsS;
             const int nwd = (nseg + 31) >> 5;
             for (int w = lane; w < nwd; w += 32) Wp.bm[w] = 0u;
             __syncwarp();
             if (lane == 0) atomicOr(&Wp.bm[0], 1u);
-            for (int k = lane; k < npairs; k += 32) {
-              const DGroup gr = K.g[g0 + k / nm];
-              if (gr.kind != 0) continue;
-              const SmBox32& bx = mb32[k % nm];
-              const int zz = z - gr.oz;
-              if (zz < bx.z0 || zz >= bx.z1) continue;
+            for (int i = 0; i < ngl; ++i) {   // lane m: member m's y edges shifted by the group's oy
+              if (!((Wp.gm[i] >> lane) & 1u)) continue;
+              const DGroup gr = K.g[g0 + Wp.gl[i]];
+              const SmBox32& bx = mb32[lane];
               const int e0 = bx.y0 + gr.oy - (int)y0 - ys, e1 = bx.y1 + gr.oy - (int)y0 - ys;
               if (e0 > 0 && e0 < nseg) atomicOr(&Wp.bm[e0 >> 5], 1u << (e0 & 31));
               if (e1 > 0 && e1 < nseg) atomicOr(&Wp.bm[e1 >> 5], 1u << (e1 & 31));
@@ -1821,8 +1893,8 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
               const int j = rb + lane;
               if (j < nruns) {
                 const int yr = ys + Wp.rs[j];  // row index inside the box
-                const T32x2 o = smset_run(mb32, nm, K, F, g0, ng, (int)y0 + yr, z, off0 + yr * step, step,
-                                          Wp.rs[j + 1] - Wp.rs[j], le, ls, ll);
+                const T32x2 o = smset_run_g(mb32, nm, Wp.gm, Wp.gl, ngl, K, F, g0, (int)y0 + yr, off0 + yr * step,
+                                            step, Wp.rs[j + 1] - Wp.rs[j], le, ls, ll);
                 tt[0] = o.s;
                 tt[1] = o.l;
               }
@@ -2632,10 +2704,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
   __shared__ Tri s_pt[2 * kMaxPlanes];
   __shared__ unsigned char s_der[kMaxPlanes];
   __shared__ SmWarp s_sw[WS_SCLASS_THREADS / 32];
-  __shared__ DGroup s_g[kMaxAcc];
-  __shared__ int s_ng;
-  __shared__ long long s_box[4];
-  __shared__ Tri s_red[(WS_SCLASS_THREADS / 32) * 2];
+  __shared__ unsigned long long s_wsum[3];
   // class entries: all of them, or (class-plane path) only those k_cplan left to the CTA path
   const long long ncls = cfbl ? (long long)cctr[2] : (long long)lists[1], ndir = (long long)lists[2];
   const long long total = ncls + ndir;
@@ -2685,7 +2754,7 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
     // one block and many load fields (LBM: one offset each): flat rows over the whole CTA;
     // otherwise plane derivation + lane-per-run unions
     if (kj == 1 && n_ld > 4) {
-      smset_eval(P, ks[P.kid], G, S0, kj, nsm, s_g, &s_ng, s_box, s_mb, s_red, ss, sl, un);
+      smset_eval_warps(P, ks[P.kid], G, S0, s_wsum, ss, sl, un);
       if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     } else {        // several blocks: plane derivation + runs
       smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_mb32, s_pt, s_der, s_sw, ss, sl, un, msk);
