@@ -66,7 +66,7 @@ struct ws_ctx {
   std::vector<cudaEvent_t> free_ev;
   // aux streams + fork/join events for the concurrent worker chains
   cudaStream_t aux[2] = {nullptr, nullptr};
-  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr}, scanned = nullptr;
   // CUDA graph of the whole estimate launch sequence, captured on `cap` and replayed on
   // `stream` while the launch arguments (key) are unchanged
   struct GKey {
@@ -180,6 +180,7 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   // fixed offsets (survive re-layouts): plan_done, the call epoch, the a5/a6 sharing table
   const size_t o_pdone = off;   off = align_up(off + sizeof(unsigned int));
   const size_t o_epoch = off;   off = align_up(off + sizeof(unsigned long long));
+  const size_t o_rctr = off;    off = align_up(off + 16 * sizeof(unsigned long long));
   const size_t o_rtab = off;    off = align_up(off + (size_t)kRowTab * 8 * sizeof(unsigned long long));
   const size_t o_plans = off;   off = align_up(off + n * sizeof(DPlan));
   const size_t o_instr = off;   off = align_up(off + n * (size_t)kMaxInstr * sizeof(DInstr));
@@ -214,6 +215,8 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   const size_t o_citems = off;  off = align_up(off + cpool_cap * sizeof(uint32_t));
   const size_t o_cfb = off;     off = align_up(off + n * (size_t)kSSlots * sizeof(uint32_t));
   const size_t o_clist = off;   off = align_up(off + max_chunks * sizeof(uint32_t));  // k_rows items per config
+  const size_t o_ritems = off;  off = align_up(off + max_chunks * sizeof(unsigned long long));
+  const size_t o_fitems = off;  off = align_up(off + n * max_fields * sizeof(uint32_t));
   if (bytes_only) {
     *bytes_only = off;
     return WS_OK;
@@ -273,6 +276,9 @@ ws_status ensure_scratch(ws_ctx* c, size_t n, Scratch& s, size_t* bytes_only = n
   s.clist = (uint32_t*)(b + o_clist);
   s.clist_stride = (int64_t)cb;
   s.epoch = (unsigned long long*)(b + o_epoch);
+  s.rctr = (unsigned long long*)(b + o_rctr);
+  s.ritems = (unsigned long long*)(b + o_ritems);
+  s.fitems = (uint32_t*)(b + o_fitems);
   s.rowtab = (unsigned long long*)(b + o_rtab);
   c->last_work = s.work;
   return WS_OK;
@@ -312,6 +318,7 @@ ws_status ws_create(int cuda_device, void* cuda_stream, ws_ctx** out) {
       cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->join[0], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->join[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->scanned, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) {
     ws_destroy(c);
     return WS_ECUDA;
@@ -339,6 +346,7 @@ void ws_destroy(ws_ctx* c) {
     if (c->join[i]) cudaEventDestroy(c->join[i]);
   }
   if (c->fork) cudaEventDestroy(c->fork);
+  if (c->scanned) cudaEventDestroy(c->scanned);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->cap) cudaStreamDestroy(c->cap);
   delete c;
@@ -675,6 +683,7 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
   st.fork = c->fork;
   st.join[0] = c->join[0];
   st.join[1] = c->join[1];
+  st.scanned = c->scanned;
   auto enqueue = [&](uint32_t* launches, cudaEvent_t* evs) -> int {
     uint32_t extra = 0;
     if (fan) {
@@ -933,6 +942,7 @@ ws_status ws_simulate(ws_ctx* c, const ws_config* cfgs, size_t n, const uint64_t
   st.fork = c->fork;
   st.join[0] = c->join[0];
   st.join[1] = c->join[1];
+  st.scanned = c->scanned;
   cudaEvent_t* ev = nullptr;
   if (c->profiling) {
     ev = c->take_events(K_SIMGEN, 2);

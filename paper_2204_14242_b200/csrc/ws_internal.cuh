@@ -128,7 +128,7 @@ struct DPlan {
   int32_t istat, pad5;           // k_instr: WS_ELIMIT when the instruction table overflows (else 0)
   // k_rows items: the chunks of computed planes only (derived planes -- translates of their zone
   // segment's representative by whole lines -- are folded by k_fold from the representative)
-  int64_t n_ritems, pad6;
+  int64_t n_ritems, chunk_base;  // chunk_base: this configuration's first slot in chunkres (owners)
 };
 // row-sharing table (fixed offset in the scratch, survives re-layouts): entries of 8 u64 =
 // state ((epoch << 32) | ready bit 31 | busy bit 30 | owner) + 6 key words; epoch = call counter,
@@ -202,8 +202,14 @@ struct Scratch {
   unsigned int* plan_done;    // k_plan CTAs finished (the last one scans; reset to 0 by it)
   unsigned long long* epoch;  // estimate calls so far (k_plan's last CTA increments it)
   unsigned long long* rowtab; // kRowTab x 8 u64: a5/a6 sharing keys (see DPlan::row_owner)
-  uint32_t* clist;            // per config (stride clist_stride): its computed chunks (k_rows items)
+  uint32_t* clist;            // per config (stride clist_stride): its computed chunks, fi << 26 | chunk
   int64_t clist_stride;
+  // the row chain's own work lists (no prefix scan): k_plan reserves each owner's ranges with atomics
+  // on the counters of the call's epoch parity; rctr[p * 4 + 0] row items, + 1 chunks, + 2 fold items,
+  // rctr[8] = p (written by k_plan)
+  unsigned long long* rctr;
+  unsigned long long* ritems;  // config << 32 | fi << 26 | chunk (max_chunks entries)
+  uint32_t* fitems;            // config << 6 | fi (n * max_fields entries)
 };
 
 // kernel kinds, in launch order (ws_kernel_name)
@@ -215,7 +221,7 @@ constexpr int kEstimateKernels = 10;
 // scope, row scope) run concurrently after k_scan.
 struct Streams {
   cudaStream_t main, aux[2];
-  cudaEvent_t fork, join[2];
+  cudaEvent_t fork, join[2], scanned;   // scanned: k_scan done (the warp chain waits for it)
 };
 // ws_estimate_multi (BJ configs[3]): one integer pass over m configurations x n_groups
 // representative hardware sets, the model over m x n_gpu outputs (k_expand / k_model_fan).

@@ -79,7 +79,7 @@ namespace wsb {
 // first violation (source line, index, capacity) and the count; ws_check_read returns them.
 #ifdef WS_CHECK
 struct CheckCaps {
-  long long max_chunks, clist_stride, wslots, sslots, cdesc, cpool, spart, rowinfo, instr;
+  long long max_chunks, clist_stride, wslots, sslots, cdesc, cpool, spart, rowinfo, instr, fitems;
 };
 __device__ CheckCaps g_caps;
 __device__ unsigned long long g_check[4];   // violations, first line, its index, its capacity
@@ -640,14 +640,10 @@ __device__ __forceinline__ long long plan_count(const DPlan& P, int j) {
   }
 }
 
-// exclusive prefix of the per-config work counts (one CTA of any size); zeroes the work and
-// list counters of the call
-__device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
-                          unsigned long long* __restrict__ work, unsigned long long* __restrict__ lists) {
+// exclusive prefix of the per-config work counts (one CTA of any size)
+__device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre) {
   __shared__ long long s_w[32][kNPrefix];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < 16) work[tid] = 0ull;  // K_NKINDS <= 16
-  if (tid < 8) lists[tid] = 0ull;  // [0..3] class / direct counters, [4..6] the class-plane path
   const int seg = (n + nt - 1) / nt;
   long long a[kNPrefix];
 #pragma unroll
@@ -699,6 +695,15 @@ __device__ void scan_body(const DPlan* __restrict__ plans, int n, DPrefix* __res
   if (tid == nt - 1) pre[n] = DPrefix{r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
 }
 
+
+// the work-count prefix of the warp and SM-set chains (one CTA, at the head of the SM-set chain;
+// the row chain has its own atomically reserved lists and does not wait for it); then the call's
+// epoch advances (every k_plan CTA of this call has read it)
+__global__ void __launch_bounds__(256) k_scan(const DPlan* __restrict__ plans, int n, DPrefix* __restrict__ pre,
+                                              unsigned long long* __restrict__ epoch) {
+  scan_body(plans, n, pre);
+  if (threadIdx.x == 0) *epoch = *epoch + 1ull;
+}
 
 // a3 instruction table (O3), on the warp chain: k_plan's plan is complete; the row and SM-set
 // chains never read the table, n_instr or addr_evals, so they start without waiting for it.  One
@@ -834,7 +839,8 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
                                               int ng, DPlan* __restrict__ plans, DInstr* __restrict__ instr,
                                               DRowInfo* __restrict__ rowinfo, unsigned long long* __restrict__ acc,
                                               unsigned int* __restrict__ wcnt, unsigned int* __restrict__ scnt,
-                                              unsigned int* __restrict__ plan_done, DPrefix* __restrict__ pre,
+                                              unsigned long long* __restrict__ rctr,
+                                              unsigned long long* __restrict__ ritems, uint32_t* __restrict__ fitems,
                                               unsigned long long* __restrict__ work,
                                               unsigned long long* __restrict__ lists,
                                               unsigned long long* __restrict__ skey, unsigned int* __restrict__ sdone,
@@ -847,6 +853,13 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
   // wait in griddepcontrol.wait until this grid has completed, then start without a launch gap
   PDL_TRIGGER();
   const unsigned long long cur_epoch = *(volatile unsigned long long*)epoch + 1ull;  // this call
+  const int par = (int)(cur_epoch & 1ull);   // the row chain's counters of this call: rctr[par * 4 ..]
+  if (c == 0 && tid < 16) {   // the call's counters (every consumer runs after this grid)
+    work[tid] = 0ull;         // K_NKINDS <= 16
+    if (tid < 8) lists[tid] = 0ull;                 // class / direct / class-plane / model counters
+    if (tid < 4) rctr[(par ^ 1) * 4 + tid] = 0ull;  // the next call's row-chain counters
+    if (tid == 8) rctr[8] = (unsigned long long)par;
+  }
 #ifdef WS_PLAN_CLOCK
   long long clk[12];
   int nclk = 0;
@@ -905,24 +918,9 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
   }
   __syncthreads();
   PLAN_MARK()
-  __shared__ int s_last;
-  auto store_plan = [&]() {  // cooperative 16-byte copy of the shared plan; the last CTA to finish
-    uint4* dst = reinterpret_cast<uint4*>(plans + c);  // scans the work counts of every config
+  auto store_plan = [&]() {  // cooperative 16-byte copy of the shared plan
+    uint4* dst = reinterpret_cast<uint4*>(plans + c);
     for (int i = tid; i < kPlanVec; i += blockDim.x) dst[i] = reinterpret_cast<const uint4*>(&P)[i];
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(plan_done, 1u) == (unsigned)(n - 1);
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      scan_body(plans, n, pre, work, lists);
-      if (tid == 0) {
-        *plan_done = 0u;  // reset for the next call (graph replay)
-        *epoch = cur_epoch;  // every CTA of this call has read the epoch: the next call's is new
-      }
-    }
   };
   if (P.status != WS_OK) {
     store_plan();
@@ -939,6 +937,7 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
   const DKernel& K = sK;
   __shared__ DRowInfo s_ri[kMaxFields];   // row boxes staged here, written out once
   __shared__ int s_nri;
+  __shared__ unsigned long long s_rb[2];   // reserved bases: row items, fold items
   uint32_t* cl = clist + (long long)c * clist_stride;
   if (tid >= kPlanWork) {
     if (tid == kPlanWork) row_claim(P, c, sG, cur_epoch, rowtab);
@@ -1017,7 +1016,7 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
       for (int sg = 0; sg < (int)ri.nseg; ++sg) {
         WS_CHK(at + sg, g_caps.clist_stride);
         WS_CHK((long long)c * clist_stride + at + sg, g_caps.max_chunks);
-        cl[at + sg] = (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
+        cl[at + sg] = ((uint32_t)fi << 26) | (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
       }
     }
   }
@@ -1041,15 +1040,27 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     P.n_fields = owner ? K.n_fields : 0;   // k_fold items
     P.n_sect_items = (P.want_pages || P.want_sect) ? K.n_fields : 0;
     P.n_ritems = owner ? s_nri : 0;
+    // the row chain's items: reserve this owner's ranges (row items, chunk slots, fold items)
+    s_rb[0] = owner ? atomicAdd(rctr + par * 4 + 0, (unsigned long long)P.n_ritems) : 0ull;
+    P.chunk_base = owner ? (long long)atomicAdd(rctr + par * 4 + 1, (unsigned long long)cb) : 0ll;
+    s_rb[1] = owner ? atomicAdd(rctr + par * 4 + 2, (unsigned long long)P.n_fields) : 0ull;
   }
   __syncthreads();
   for (int fi = tid; fi < K.n_fields; fi += blockDim.x) rowinfo[(long long)c * kMaxFields + fi] = s_ri[fi];
+  for (long long i = tid; i < P.n_ritems; i += blockDim.x) {
+    WS_CHK(s_rb[0] + i, g_caps.max_chunks);
+    ritems[s_rb[0] + i] = ((unsigned long long)c << 32) | (unsigned long long)cl[i];
+  }
+  for (int fi = tid; fi < (int)P.n_fields; fi += blockDim.x) {
+    WS_CHK(s_rb[1] + fi, g_caps.fitems);
+    fitems[s_rb[1] + fi] = ((uint32_t)c << 6) | (uint32_t)fi;
+  }
   PLAN_MARK()
   store_plan();
   PLAN_MARK()
 #ifdef WS_PLAN_CLOCK
-  if (tid == 0 && (c == 0 || c == n - 1 || s_last)) {
-    printf("PLANCLK c=%d last=%d", c, (int)s_last);
+  if (tid == 0 && (c == 0 || c == n - 1)) {
+    printf("PLANCLK c=%d", c);
     for (int i = 1; i < nclk; ++i) printf(" %lld", clk[i] - clk[i - 1]);
     printf(" total %lld\n", clk[nclk - 1] - clk[0]);
   }
@@ -2904,6 +2915,9 @@ struct WarpRowCtx {
   T32 pt[kNQ];                 // the plane's triples (lane 0)
   unsigned bm[kSegRows / 32];  // run-start bitmap of the current segment
   short rs[kSegRows + 2];      // run starts (ascending) + end
+  // the field's offset groups whose cell plane z - oz lies in the domain, per computed plane:
+  // x = Gy * block layer of z - oz (the block-row base), y = oy << 8 | run << 1 | kind
+  int2 gv[kMaxAcc];
 };
 
 // Union of the candidates (range q1, mask m1) u (range q2, mask m2) over `run` consecutive rows
@@ -2986,8 +3000,9 @@ constexpr long long kRowTrace = 1 << 17;
 __device__ unsigned long long g_rowtrace[kRowTrace][2];
 // diagnostics build: print the computed planes of the last k_rows launch, slowest first is left to
 // the reader (one line per computed plane with cycles > WS_ROWS_TRACE)
-__global__ void k_rowtrace_dump(const DPrefix* __restrict__ pre, int n) {
-  const long long total = pre[n].ritem < kRowTrace ? pre[n].ritem : kRowTrace;
+__global__ void k_rowtrace_dump(const unsigned long long* __restrict__ rctr) {
+  const long long nit = (long long)rctr[rctr[8] * 4 + 0];
+  const long long total = nit < kRowTrace ? nit : kRowTrace;
   for (long long i = 0; i < total; ++i) {
     const unsigned long long a = g_rowtrace[i][0], b = g_rowtrace[i][1];
     if ((b & 0xffffffffffull) > WS_ROWS_TRACE)
@@ -3010,18 +3025,19 @@ __global__ void k_rowtrace_dump(const DPrefix* __restrict__ pre, int n) {
 //    (rows of a run are translates).  An ordered warp reduction of the lanes' 9 triples gives the
 //    plane's contribution.  All of it in 32-bit plane-relative arithmetic.
 __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPlan* __restrict__ plans,
-                                                            const DPrefix* __restrict__ pre, int n,
                                                             const DKernel* __restrict__ ks,
                                                             const DGpu* __restrict__ gs,
                                                             const DRowInfo* __restrict__ rowinfo,
                                                             long long* __restrict__ chunkres,
                                                             unsigned long long* __restrict__ work,
-                                                            const uint32_t* __restrict__ clist, long long clist_stride) {
+                                                            const unsigned long long* __restrict__ rctr,
+                                                            const unsigned long long* __restrict__ ritems) {
   PDL_PROLOGUE();
   __shared__ WarpRowCtx s_ctx[kRowWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpRowCtx& X = s_ctx[wid];
-  const long long total = pre[n].ritem;   // computed chunks only (k_plan's per-config lists)
+  // computed chunks only: k_plan's reserved item list (config << 32 | field << 26 | chunk)
+  const long long total = (long long)rctr[rctr[8] * 4 + 0];
   const long long nwg = (long long)gridDim.x * kRowWarps;
   unsigned long long my_ops = 0;
   int ranges_c = -1;
@@ -3039,27 +3055,13 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const long long t_item0 = clock64();
     int tr_runs = 0;
 #endif
-    c = find_config_warp<7>(pre, n, item, c);
+    const unsigned long long ent = ritems[item];
+    c = (int)(ent >> 32);
+    const int fi = (int)((ent >> 26) & 63ull);
+    const long long ci = (long long)(ent & ((1ull << 26) - 1ull));
     const DPlan& P = plans[c];
     const DKernel& K = ks[P.kid];
     const DGpu& G = gs[P.gid];
-    WS_CHK(item - pre[c].ritem, g_caps.clist_stride);
-    const long long ci = clist[(long long)c * clist_stride + (item - pre[c].ritem)];
-    // the field whose chunk range holds ci: chunk_begin ascends with the field index (fields
-    // without chunks repeat their successor's begin), so the last field with begin <= ci and a
-    // nonempty range -- binary search for the last begin <= ci, then skip empty ranges backwards
-    int fi;
-    {
-      const DRowInfo* ri0 = rowinfo + (long long)c * kMaxFields;
-      int lo = 0, hi = K.n_fields - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (ri0[mid].chunk_begin <= ci) lo = mid;
-        else hi = mid - 1;
-      }
-      while (lo > 0 && !(ci < ri0[lo].chunk_begin + ri0[lo].n_chunks)) --lo;
-      fi = lo;
-    }
     WS_CHK((long long)c * kMaxFields + fi, g_caps.rowinfo);
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const DField& F = K.f[fi];
@@ -3105,6 +3107,23 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const int off0 = (int)(R0p - Bp);
     const int pystep = (int)(py << le);
     if (lane < kNQ) X.pt[lane] = t32_empty();
+    // this plane's valid groups and their block-row bases, once (lanes over the groups)
+    int ngv = 0;
+    for (int gb = 0; gb < ng; gb += 32) {
+      const int g = gb + lane;
+      bool v = false;
+      int2 e = make_int2(0, 0);
+      if (g < ng) {
+        const DGroup gr = K.g[g0 + g];
+        const int zz = z - gr.oz;
+        v = zz >= lo2 && zz < hi2;
+        if (v) e = make_int2(Gy * fdiv32(zz - lo2, fdz), (gr.oy << 8) | (gr.run << 1) | (gr.kind & 1));
+      }
+      const unsigned bal = __ballot_sync(FULL, v);
+      if (v) X.gv[ngv + __popc(bal & ((1u << lane) - 1u))] = e;
+      ngv += __popc(bal);
+    }
+    __syncwarp();
     for (int ys = ys0; ys < ys1; ys += kSegRows) {
       const int nseg = ys1 - ys < kSegRows ? ys1 - ys : kSegRows;
       const int nwd = (nseg + 31) >> 5;
@@ -3112,20 +3131,18 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       __syncwarp();
       if (lane == 0) atomicOr(&X.bm[0], 1u);
       my_ops += (unsigned long long)(lane < ng ? 8 * (nb + 2) : 0);
-      for (int g = lane; g < ng; g += 32) {
-        const DGroup gr = K.g[g0 + g];
-        const int zz = z - gr.oz;
-        if (zz < lo2 || zz >= hi2) continue;
-        const int C = Gy * fdiv32(zz - lo2, fdz);
+      for (int g = lane; g < ngv; g += 32) {
+        const int2 e = X.gv[g];
+        const int C = e.x, oy = e.y >> 8;
         auto mark = [&](int yb) {
           const int i = yb - ys;
           if (i > 0 && i < nseg) atomicOr(&X.bm[i >> 5], 1u << (i & 31));
         };
-        mark(lo1 + gr.oy);
-        mark(hi1 + gr.oy);
+        mark(lo1 + oy);
+        mark(hi1 + oy);
         for (int k = 0; k < nb; ++k) {
           const int d = X.bnd[k] - C;
-          if (d > 0 && d < Gy) mark(lo1 + d * BF1 + gr.oy);
+          if (d > 0 && d < Gy) mark(lo1 + d * BF1 + oy);
         }
       }
       __syncwarp();
@@ -3154,28 +3171,43 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       }
       if (lane == 0) X.rs[nruns] = (short)nseg;
       __syncwarp();
+#ifndef WS_ROWS_CONTIG   // 1: contiguous runs per lane, one reduction per segment (A/B on B200:
+#define WS_ROWS_CONTIG 0 // k_rows 63 vs 51 us serial -- the longer per-lane loop; rounds kept)
+#endif
+#if WS_ROWS_CONTIG
+      // lanes take contiguous runs (in row order): one ordered reduction per segment
+      const int rpl = (nruns + 31) >> 5, nact = (nruns + rpl - 1) / rpl;
+      {
+        T32 t[kNQ];
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q) t[q] = t32_empty();
+        for (int j = lane * rpl; j < nruns && j < (lane + 1) * rpl; ++j) {
+#else
+      // rounds of 32 runs, a run per lane, an ordered reduction per round
       for (int rb = 0; rb < nruns; rb += 32) {
+        const int nact = nruns - rb < 32 ? nruns - rb : 32;
         T32 t[kNQ];
 #pragma unroll
         for (int q = 0; q < kNQ; ++q) t[q] = t32_empty();
         const int j = rb + lane;
         if (j < nruns) {
+#endif
           const int y = ys + X.rs[j];
           const int run = X.rs[j + 1] - X.rs[j];
           my_ops += (unsigned long long)(30 * ng + 72 * run);
           unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
-          for (int g = 0; g < ng; ++g) {
-            const DGroup gr = K.g[g0 + g];
-            const int zz = z - gr.oz, yy = y - gr.oy;
-            if (zz < lo2 || zz >= hi2 || yy < lo1 || yy >= hi1) continue;
-            const int r = fdiv32(yy - lo1, fdy) + Gy * fdiv32(zz - lo2, fdz);
+          for (int g = 0; g < ngv; ++g) {
+            const int2 e = X.gv[g];
+            const int yy = y - (e.y >> 8);
+            if (yy < lo1 || yy >= hi1) continue;
+            const int r = fdiv32(yy - lo1, fdy) + e.x, grun = (e.y >> 1) & 15;
 #pragma unroll
             for (int q = 0; q < 5; ++q) {  // classify32 from registers
               const int ty = (r < rra[q] || r > rrl[q]) ? -1
                              : (rra[q] == rrl[q] ? 3 : (r == rra[q] ? 1 : (r == rrl[q] ? 2 : 0)));
               if (ty >= 0) {
-                const unsigned long long bit = 1ull << (ty * 16 + gr.run);
-                if (gr.kind) mS[q] |= bit;
+                const unsigned long long bit = 1ull << (ty * 16 + grun);
+                if (e.y & 1) mS[q] |= bit;
                 else mL[q] |= bit;
               }
             }
@@ -3201,7 +3233,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
             row_emit32<5, 6, 8>(t, X, F, mL[2] | mS[2], 2, 0ull, 2, R0, pystep, run, le, ls, ll);
           }
         }
-        warp_ordered_reduce32<kNQ>(t, nruns - rb);
+        warp_ordered_reduce32<kNQ>(t, nact);
         if (lane == 0)  // plane triples: lane 0 only
 #pragma unroll
           for (int q = 0; q < kNQ; ++q) X.pt[q] = t32_combine(X.pt[q], t[q]);
@@ -3209,8 +3241,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       __syncwarp();
     }
     if (lane == 0) {
-      WS_CHK(pre[c].chunk + ci, g_caps.max_chunks);
-      long long* out = chunkres + (pre[c].chunk + ci) * (kNQ * 3);
+      WS_CHK(P.chunk_base + ci, g_caps.max_chunks);
+      long long* out = chunkres + (P.chunk_base + ci) * (kNQ * 3);
       const long long bs = Bp >> ls, bl = Bp >> ll;
 #pragma unroll
       for (int q = 0; q < kNQ; ++q) {
@@ -3234,16 +3266,14 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
 }
 
 // one CTA per (config, field): threads take contiguous planes, ordered CTA reduction
-__device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+__device__ void fold_cta(const DPlan* __restrict__ plans, long long total, const uint32_t* __restrict__ fitems,
                          const DKernel* __restrict__ ks, const DGpu* __restrict__ gs, const DRowInfo* __restrict__ rowinfo,
                          const long long* __restrict__ chunkres, unsigned long long* __restrict__ acc) {
   __shared__ Tri s_red[(256 / 32) * kNQ];
-  const long long total = pre[n].fold;
   const int tid = threadIdx.x;
-  int c = -1;
   for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    c = find_config_warp<5>(pre, n, item, c);   // 32-ary search by each warp (item CTA-uniform)
-    const int fi = (int)(item - pre[c].fold);
+    const uint32_t ent = fitems[item];   // k_plan's reserved fold items: config << 6 | field
+    const int c = (int)(ent >> 6), fi = (int)(ent & 63u);
     const DPlan& P = plans[c];
     const DField& F = ks[P.kid].f[fi];
     const DGpu& G = gs[P.gid];
@@ -3254,7 +3284,7 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restr
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
     const long long per_l = (nch + blockDim.x - 1) / blockDim.x;
-    const long long* base = chunkres + (pre[c].chunk + RI.chunk_begin) * (kNQ * 3);
+    const long long* base = chunkres + (P.chunk_base + RI.chunk_begin) * (kNQ * 3);
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
@@ -3266,7 +3296,7 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restr
       const int zr = plane_rep_f(F, gk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
                                P.fd_BF[2], per);
       const long long src = (zr - RI.z0) * RI.nseg + (k - pi * RI.nseg);
-      WS_CHK(pre[c].chunk + RI.chunk_begin + src, g_caps.max_chunks);
+      WS_CHK(P.chunk_base + RI.chunk_begin + src, g_caps.max_chunks);
       const long long* in = base + src * (kNQ * 3);
       const long long dbytes = ((k - src) / RI.nseg) * pbytes;   // same row segment, whole planes apart
 #pragma unroll
@@ -3293,28 +3323,29 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, const DPrefix* __restr
 // Ordered fold of the plane triples of one (config, field); one warp per item.  A derived
 // plane (count slot = -(representative index) - 2) takes its representative's triple
 // translated by the plane distance (a multiple of the reuse period: whole lines).
-__global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restrict__ plans, const DPrefix* __restrict__ pre, int n,
+__global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restrict__ plans,
+                                              const unsigned long long* __restrict__ rctr,
+                                              const uint32_t* __restrict__ fitems,
                                               const DKernel* __restrict__ ks, const DGpu* __restrict__ gs,
                                               const DRowInfo* __restrict__ rowinfo,
                                               const long long* __restrict__ chunkres,
                                               unsigned long long* __restrict__ acc, int mode) {
   PDL_PROLOGUE();
-  const long long total = pre[n].fold;
+  const long long total = (long long)rctr[rctr[8] * 4 + 2];
   const int lane = threadIdx.x & 31;
   // items (config, field) <= CTAs (BJ configs[1]: 336 items x ~40 planes): one CTA per item (all
   // items at once, 256 threads each); more items (LBM: 58 fields per config): one warp per item.
   // (A/B on B200: 0.202 vs 0.212 ms per configs[1] step; LBM15 0.238 vs 0.284 ms the other way.)
   // mode: 0 = that choice, 1 = CTA, 2 = warp (WS_FOLD_MODE, diagnostics)
   if (mode == 1 || (mode == 0 && total <= gridDim.x)) {
-    fold_cta(plans, pre, n, ks, gs, rowinfo, chunkres, acc);
+    fold_cta(plans, total, fitems, ks, gs, rowinfo, chunkres, acc);
     return;
   }
   const long long nwg = ((long long)gridDim.x * blockDim.x) >> 5;
   // one warp per (config, field): lanes take contiguous planes, ordered warp reduction
-  int c = -1;
   for (long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < total; item += nwg) {
-    c = find_config_warp<5>(pre, n, item, c);
-    const int fi = (int)(item - pre[c].fold);
+    const uint32_t ent = fitems[item];
+    const int c = (int)(ent >> 6), fi = (int)(ent & 63u);
     const DPlan& P = plans[c];
     const DField& F = ks[P.kid].f[fi];
     const DGpu& G = gs[P.gid];
@@ -3325,7 +3356,7 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
     const DRowInfo RI = rowinfo[(long long)c * kMaxFields + fi];
     const long long nch = RI.n_chunks;
     const long long per_l = (nch + 31) / 32;
-    const long long* base = chunkres + (pre[c].chunk + RI.chunk_begin) * (kNQ * 3);
+    const long long* base = chunkres + (P.chunk_base + RI.chunk_begin) * (kNQ * 3);
     Tri t[kNQ];
 #pragma unroll
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
@@ -3336,7 +3367,7 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
       const int zr = plane_rep_f(F, gk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
                                P.fd_BF[2], per);
       const long long src = (zr - RI.z0) * RI.nseg + (k - pi * RI.nseg);
-      WS_CHK(pre[c].chunk + RI.chunk_begin + src, g_caps.max_chunks);
+      WS_CHK(P.chunk_base + RI.chunk_begin + src, g_caps.max_chunks);
       const long long* in = base + src * (kNQ * 3);
       const long long dbytes = ((k - src) / RI.nseg) * pbytes;   // same row segment, whole planes apart
 #pragma unroll
@@ -4103,15 +4134,15 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     static CheckCaps hc;
     hc = CheckCaps{(long long)s.max_chunks, (long long)s.clist_stride, (long long)n * kWSlots, (long long)n * kSSlots,
                    (long long)s.cdesc_cap, (long long)s.cpool_cap, (long long)n * s.max_fields * kSectSeg * kSectNQ,
-                   (long long)n * kMaxFields, (long long)n * kMaxInstr};
+                   (long long)n * kMaxFields, (long long)n * kMaxInstr, (long long)n * s.max_fields};
     cudaMemcpyToSymbolAsync(g_caps, &hc, sizeof(hc), 0, cudaMemcpyHostToDevice, m);
     cudaStreamSynchronize(m);
   }
 #endif
   beg(K_PLAN, m);
   k_plan<<<n, WS_PLAN_THREADS, 0, m>>>(d_cfgs, n, d_k, nk, d_g, ng, s.plans, s.instr, s.rowinfo, s.acc, s.wcnt, s.scnt,
-                           s.plan_done, s.prefix, s.work, s.lists, s.skey, s.sdone, s.max_fields, s.epoch,
-                           s.rowtab, s.clist, s.clist_stride);  // its last CTA scans
+                           s.rctr, s.ritems, s.fitems, s.work, s.lists, s.skey, s.sdone, s.max_fields, s.epoch,
+                           s.rowtab, s.clist, s.clist_stride);
   end(K_PLAN, m);
   // fork: SM-set chain on aux[0], row chain on aux[1], warp chain on the main stream.  WS_ROWMAIN=1
   // swaps the row and warp chains so that k_rows is k_plan's programmatic dependent (its CTAs
@@ -4127,19 +4158,23 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
     m = r;                 // ... and the row chain's (joins on the caller's stream below)
   }
   beg(K_ROWS, m);
-  launch_k(pdl && rowmain, k_rows, n_sm_dev * g_rows, kRowWarps * 32, m, (const DPlan*)s.plans,
-           (const DPrefix*)s.prefix, n, d_k, d_g, (const DRowInfo*)s.rowinfo, s.chunkres, s.work,
-           (const uint32_t*)s.clist, (long long)s.clist_stride);
+  launch_k(pdl && rowmain, k_rows, n_sm_dev * g_rows, kRowWarps * 32, m, (const DPlan*)s.plans, d_k, d_g,
+           (const DRowInfo*)s.rowinfo, s.chunkres, s.work, (const unsigned long long*)s.rctr,
+           (const unsigned long long*)s.ritems);
   end(K_ROWS, m);
 #ifdef WS_ROWS_TRACE
-  k_rowtrace_dump<<<1, 1, 0, m>>>(s.prefix, n);
+  k_rowtrace_dump<<<1, 1, 0, m>>>(s.rctr);
 #endif
   beg(K_FOLD, m);
   static const int fold_mode = getenv("WS_FOLD_MODE") ? atoi(getenv("WS_FOLD_MODE")) : 0;  // diagnostics
-  launch_k(pdl, k_fold, n_sm_dev * g_fold, 256, m, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
-           (const DRowInfo*)s.rowinfo, (const long long*)s.chunkres, s.acc, (int)fold_mode);
+  launch_k(pdl, k_fold, n_sm_dev * g_fold, 256, m, (const DPlan*)s.plans, (const unsigned long long*)s.rctr,
+           (const uint32_t*)s.fitems, d_k, d_g, (const DRowInfo*)s.rowinfo, (const long long*)s.chunkres, s.acc,
+           (int)fold_mode);
   end(K_FOLD, m);
   beg(K_SMSET, a);
+  // the work-count prefix for the SM-set and warp chains (the row chain does not need it)
+  k_scan<<<1, 256, 0, a>>>(s.plans, n, s.prefix, s.epoch);
+  cudaEventRecord(st.scanned, a);
   k_spairs<<<n_sm_dev * 4, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist,
                                                   s.dlist, s.skey, s.dmask, s.gkey);
   launch_k(pdl, k_smset, n_sm_dev * g_smset, kSmsetThreads, a, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, d_k, d_g,
@@ -4176,6 +4211,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   beg(K_INSTR, b);
   k_instr<<<n, 128, 0, b>>>(d_k, s.plans, s.instr, s.wcnt, n);
   end(K_INSTR, b);
+  cudaStreamWaitEvent(b, st.scanned, 0);
   beg(K_WARP, b);
   launch_k(pdl, k_warp, persist, 256, b, (const DPlan*)s.plans, (const DPrefix*)s.prefix, n, (const DInstr*)s.instr, d_k,
            d_g, s.acc, s.wcnt, s.wrep, s.lists, s.wlist, s.work);
