@@ -2298,42 +2298,42 @@ __global__ void __launch_bounds__(kSmsetThreads) k_spairs(const DPlan* __restric
         }
         s_adj[wid][lane] = 0u;
         __syncwarp();
-        const int k = (int)kj, npair = k * (k - 1) / 2;
-        for (int p = lane; p < npair; p += 32) {
-          int a1 = 0, q = p;  // row-major triangular index -> (a1, b1), a1 < b1
-          while (q >= k - 1 - a1) {
-            q -= k - 1 - a1;
-            ++a1;
-          }
-          const int b1 = a1 + 1 + q;
-          if (!set_pair_separated(K, env, lb, bx + a1 * 6, bx + b1 * 6)) atomicOr(&s_adj[wid][a1], 1u << b1);
-        }
-        __syncwarp();
-        unsigned single = 0u;
-        if (lane == 0) {
-          int par[32];
-          for (int m = 0; m < k; ++m) par[m] = m;
-          for (int a1 = 0; a1 < k; ++a1) {
-            unsigned row = s_adj[wid][a1];
-            while (row) {
-              const int b1 = __ffs(row) - 1;
-              row &= row - 1;
-              int ra = a1, rb = b1;
-              while (par[ra] != ra) ra = par[ra];
-              while (par[rb] != rb) rb = par[rb];
-              if (ra != rb) par[ra > rb ? ra : rb] = ra < rb ? ra : rb;
+        const int k = (int)kj;
+        // circulant pair assignment: lane a tests (a, a + d mod k) for d = 1 .. k/2, every unordered
+        // pair once (d = k/2 with k even: lanes < d only); the adjacency is kept symmetric
+        if (lane < k) {
+          unsigned row = 0u;
+          for (int d = 1; 2 * d <= k; ++d) {
+            if (2 * d == k && lane >= d) break;
+            const int b1 = lane + d < k ? lane + d : lane + d - k;
+            if (!set_pair_separated(K, env, lb, bx + lane * 6, bx + b1 * 6)) {
+              row |= 1u << b1;
+              atomicOr(&s_adj[wid][b1], 1u << lane);
             }
           }
-          unsigned cm[32];
-          for (int m = 0; m < k; ++m) cm[m] = 0u;
-          int ncomp = 0;
-          for (int m = 0; m < k; ++m) {
-            int r = m;
-            while (par[r] != r) r = par[r];
-            if (!cm[r]) ++ncomp;
-            cm[r] |= 1u << m;
+          atomicOr(&s_adj[wid][lane], row);
+        }
+        __syncwarp();
+        // connected components: transitive closure of adjacency | self by repeated squaring (paths
+        // of length <= 2^t after t rounds; stops when nothing changes)
+        unsigned comp = lane < k ? (s_adj[wid][lane] | (1u << lane)) : 0u;
+        for (int it = 0; it < 5; ++it) {
+          unsigned nc = comp;
+          for (int jj = 0; jj < k; ++jj) {
+            const unsigned cj = __shfl_sync(FULL, comp, jj);
+            if ((comp >> jj) & 1u) nc |= cj;
           }
-          if (ncomp == 1) {  // one component: the set as a whole (translation groups below)
+          const bool changed = nc != comp;
+          comp = nc;
+          if (!__any_sync(FULL, changed)) break;
+        }
+        const bool leader = lane < k && __ffs(comp) - 1 == lane;
+        const int ncomp = __popc(__ballot_sync(FULL, leader));
+        // singletons join the single-block classes; one component: the set as a whole (translation
+        // groups, k_smset); several: every larger component a direct item with its member mask
+        const unsigned single = ncomp > 1 ? __ballot_sync(FULL, lane < k && comp == (1u << lane)) : 0u;
+        if (ncomp == 1) {
+          if (lane == 0) {
             if (grp && set_unclipped(P, S0, kj, nsm)) {
               gk = set_shape_key(P, S0, kj, nsm);
             } else {
@@ -2341,20 +2341,12 @@ __global__ void __launch_bounds__(kSmsetThreads) k_spairs(const DPlan* __restric
               dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
               dmask[pos] = 0u;
             }
-          } else {
-            for (int r = 0; r < k; ++r) {
-              if (!cm[r]) continue;
-              if (__popc(cm[r]) == 1) {
-                single |= cm[r];
-              } else {
-                const unsigned long long pos = atomicAdd(lists + 2, 1ull);
-                dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
-                dmask[pos] = cm[r];
-              }
-            }
           }
+        } else if (leader && __popc(comp) > 1) {
+          const unsigned long long pos = atomicAdd(lists + 2, 1ull);
+          dlist[pos] = ((unsigned long long)c << 32) | (unsigned long long)j;
+          dmask[pos] = comp;
         }
-        single = __shfl_sync(FULL, single, 0);
         smset_claim(P, c, S0 + (long long)lane * nsm, (single >> lane) & 1u, scnt, srep, skey, slist, lists);
         __syncwarp();
       }
@@ -3306,7 +3298,37 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, long long total, const
         t[q] = tri_combine(t[q], cq ? Tri{in[q * 3] + d, in[q * 3 + 1] + d, cq} : tri_empty());
       }
     }
-    cta_ordered_reduce<kNQ>(t, s_red);
+    // the ordered CTA reduction in 32-bit item-relative indices when the item's span fits (half the
+    // shuffles of the 64-bit triples); only the counts leave the fold
+    const long long a0 = falign + ((py * RI.y0 + pz * RI.z0) << F.lg_elem);
+    if (((RI.nz * pbytes) >> ls) < (1ll << 29)) {
+      const long long bs = (a0 >> ls) - (1ll << 24), bl = (a0 >> ll) - (1ll << 24);
+      T32 u[kNQ];
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        const long long b = (q == 2 || q == 4 || q == 6) ? bl : bs;
+        u[q] = t[q].c ? T32{(int)(t[q].f - b), (int)(t[q].l - b), (int)t[q].c} : t32_empty();
+      }
+      warp_ordered_reduce32<kNQ>(u);
+      __shared__ T32 s_red32[(256 / 32) * kNQ];
+      const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q) s_red32[warp * kNQ + q] = u[q];
+      __syncthreads();
+      if (tid < kNQ) {
+        T32 a = s_red32[tid];
+        for (int w = 1; w < nw; ++w) a = t32_combine(a, s_red32[w * kNQ + tid]);
+        s_red32[tid] = a;
+      }
+      __syncthreads();
+      if (tid == 0)
+#pragma unroll
+        for (int q = 0; q < kNQ; ++q) t[q].c = s_red32[q].c;
+      __syncthreads();
+    } else {
+      cta_ordered_reduce<kNQ>(t, s_red);
+    }
     if (tid == 0 && nch > 0) {
       unsigned long long* a = acc + (long long)c * A_N;
       atomicAdd(a + A_WLD, (unsigned long long)t[0].c);
