@@ -549,10 +549,20 @@ ws_status ws_describe_kernel(ws_ctx* c, const ws_kernel* k, uint32_t* id) {
     E.oy_min = E.ext1_min = E.row_bytes_min = E.plane_bytes_min = INT64_MAX;
     E.oy_max = INT64_MIN;
     E.has_load = 0;
+    E.n_ld = 0;
+    E.max_lg_elem = 0;
+    E.same_layout = 1;
+    E.pad2 = E.pad3 = 0;
+    for (int fi = 0; fi < D.n_fields; ++fi) {
+      E.max_lg_elem = std::max(E.max_lg_elem, D.f[fi].lg_elem);
+      for (int d = 0; d < 3; ++d)
+        if (D.f[fi].pitch[d] != D.f[0].pitch[d] || D.f[fi].lg_elem != D.f[0].lg_elem) E.same_layout = 0;
+    }
     for (int fi = 0; fi < D.n_fields; ++fi) {
       const DField& F = D.f[fi];
       if (!(F.kinds & 1)) continue;
       E.has_load = 1;
+      E.n_ld++;
       E.spy = std::max<int64_t>(E.spy, F.ld_oy_max - F.ld_oy_min);
       E.spz = std::max<int64_t>(E.spz, F.ld_oz_max - F.ld_oz_min);
       E.oy_min = std::min<int64_t>(E.oy_min, F.ld_oy_min);

@@ -42,7 +42,9 @@ struct DLoadEnv {
   int64_t spy, spz;                   // max over load fields of ld_oy/oz_max - ld_oy/oz_min
   int64_t oy_min, oy_max, ext1_min;   // min / max load oy, min ext[1]
   int64_t row_bytes_min, plane_bytes_min;
-  int32_t has_load, pad;
+  int32_t has_load, n_ld;             // n_ld: fields with loads
+  int32_t max_lg_elem, same_layout;   // over all fields: largest lg_elem; one pitch and element size
+  int32_t pad2, pad3;
 };
 struct DKernel {
   int32_t n_fields, n_acc, n_groups, regs;

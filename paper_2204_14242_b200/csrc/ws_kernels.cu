@@ -214,6 +214,43 @@ __device__ __forceinline__ int plane_rep_f(const DField& F, const DGroup* g, int
   return seg + ((z - seg) % per);
 }
 
+// The zone segment of plane z and where it ends: seg = plane_rep's segment start (the largest zone
+// start over the field's distinct oz values, at least z0) and the next plane where some oz's zone
+// start changes (INT_MAX: none).  plane_rep(z) == z  <=>  z - seg < per, constant on [z, next).
+__device__ __forceinline__ int plane_seg(const DField& F, const DGroup* g, int z, int z0, int lo2, int hi2, int BF2,
+                                         FDiv fdz, int& seg) {
+  seg = z0;
+  int nxt = 0x7fffffff;
+  auto one = [&](int oz) {
+    const int zz = z - oz;
+    int st, nx;
+    if (zz < lo2) {
+      st = -0x7fffffff;
+      nx = lo2 + oz;
+    } else if (zz >= hi2) {
+      st = hi2 + oz;
+      nx = 0x7fffffff;
+    } else {
+      const int bl = lo2 + (int)fdiv(zz - lo2, fdz) * BF2;
+      st = bl + oz;
+      nx = (bl + BF2 < hi2 ? bl + BF2 : hi2) + oz;
+    }
+    seg = st > seg ? st : seg;
+    nxt = nx < nxt ? nx : nxt;
+  };
+  unsigned long long m = F.oz_mask;
+  if (m) {
+    while (m) {
+      const int oz = F.oz_min + __ffsll((long long)m) - 1;
+      m &= m - 1;
+      one(oz);
+    }
+  } else {
+    for (int i = 0; i < F.g_end - F.g_begin; ++i) one(g[i].oz);
+  }
+  return nxt;
+}
+
 struct Tri {
   long long f, l, c;  // first, last, count; c == 0: empty
 };
@@ -421,11 +458,10 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
       return;
     }
   }
-  for (int i = 0; i < K.n_fields; ++i)
-    if (K.f[i].lg_elem > G.lg_sector) {
-      P.status = WS_EINVAL;
-      return;
-    }
+  if (K.env.max_lg_elem > G.lg_sector) {   // an element wider than a sector (describe-time maximum)
+    P.status = WS_EINVAL;
+    return;
+  }
   if (cf.variant & ~15u) {  // unknown WS_VAR_* bits
     P.status = WS_EINVAL;
     return;
@@ -507,10 +543,7 @@ __device__ void plan_geometry(const ws_config& cf, const DKernel* ks, int nk, co
     P.part[d] = last < P.BF[d] ? last : 0;
   }
   // translation classes need one pitch and one element size for every field
-  bool same = true;
-  for (int i = 1; i < K.n_fields; ++i)
-    for (int d = 0; d < 3; ++d)
-      if (K.f[i].pitch[d] != K.f[0].pitch[d] || K.f[i].lg_elem != K.f[0].lg_elem) same = false;
+  const bool same = K.env.same_layout != 0;   // (computed at describe time)
   // sector counts are invariant under translation by multiples of sector_bytes; bank words
   // shift uniformly under multiples of bank_bytes, which only relabels the banks cyclically
   // (the max multiplicity and the cluster split are unchanged): M = lcm = max (powers of two)
@@ -556,23 +589,30 @@ __device__ void plan_range(DPlan& P, int q) {
   R.iv[3][0] = xs_a; R.iv[3][1] = xe_l;
 }
 
-// sorted distinct block rows where some range's classification zone starts
-__device__ void plan_boundaries(DPlan& P) {
-  P.nb = 0;
-  for (int q = 0; q < 5; ++q) {
-    const RangeInfo& R = P.rng[q];
-    if (!R.nonempty) continue;
-    const long long cand[4] = {R.ra, R.ra + 1, R.rl, R.rl + 1};
-    for (int k = 0; k < 4; ++k) {
-      const long long v = cand[k];
-      int pos = 0;
-      while (pos < P.nb && P.bnd[pos] < v) ++pos;
-      if (pos < P.nb && P.bnd[pos] == v) continue;
-      for (int m = P.nb; m > pos; --m) P.bnd[m] = P.bnd[m - 1];
-      P.bnd[pos] = v;
-      ++P.nb;
+// the sorted distinct block rows where some range's classification zone starts, by one warp: lane 4q + k holds candidate k of range q, the first lane of each
+// distinct value (match) writes it at its rank among the distinct values (shuffle count)
+__device__ void plan_boundaries_warp(DPlan& P, int lane) {
+  const unsigned long long INF = ~0ull;
+  unsigned long long v = INF;
+  if (lane < 20) {
+    const RangeInfo& R = P.rng[lane >> 2];
+    if (R.nonempty) {
+      const int k = lane & 3;
+      v = (unsigned long long)(k == 0 ? R.ra : (k == 1 ? R.ra + 1 : (k == 2 ? R.rl : R.rl + 1)));
     }
   }
+  const unsigned peers = __match_any_sync(FULL, v);
+  const bool first = v != INF && __ffs(peers) - 1 == lane;
+  int rank = 0;
+  for (int j = 0; j < 20; ++j) {
+    const unsigned long long vj = __shfl_sync(FULL, v, j);
+    const bool fj = __shfl_sync(FULL, first, j);
+    rank += (fj && vj < v) ? 1 : 0;
+  }
+  if (first) P.bnd[rank] = (long long)v;
+  const int nb = __popc(__ballot_sync(FULL, first));
+  if (lane == 0) P.nb = nb;
+  __syncwarp();
 }
 
 // a5/a6 sharing (DPlan::row_owner): claim this configuration's row-scope key in the row table, or
@@ -926,6 +966,9 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     store_plan();
     return;
   }
+  // the batch's split of directly evaluated SM sets by field (k_sclass): kernels with many load
+  // fields are evaluated one (set, field) per CTA item
+  if (tid == 0 && sK.env.n_ld > 4) atomicMax(rctr + par * 4 + 3, (unsigned long long)sK.n_fields);
   PLAN_MARK()
   // warp kPlanWork/32 alone claims the row-table key (global atomics, a few dependent round trips);
   // warps 0 .. kPlanWork/32-1 meanwhile compute the ranges, boundaries, row boxes and the computed-
@@ -939,13 +982,26 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
   __shared__ int s_nri;
   __shared__ unsigned long long s_rb[2];   // reserved bases: row items, fold items
   uint32_t* cl = clist + (long long)c * clist_stride;
+#ifdef WS_PLAN_CLOCK
+  __shared__ long long s_clk[4];   // phase start, claim end, workers end, join end
+  __shared__ unsigned long long s_wclk[4];   // workers: ranges+boundaries, row boxes, chunk prefix, listing
+  if (tid == 0) s_clk[0] = clock64();
+  if (tid < 4) s_wclk[tid] = 0ull;
+  __syncthreads();
+#endif
   if (tid >= kPlanWork) {
     if (tid == kPlanWork) row_claim(P, c, sG, cur_epoch, rowtab);
+#ifdef WS_PLAN_CLOCK
+    if (tid == kPlanWork) s_clk[1] = clock64();
+#endif
   } else {
     auto wbar = [] { asm volatile("bar.sync 1, %0;" ::"r"(kPlanWork) : "memory"); };
     if (tid < 5) plan_range(P, tid);
     __syncwarp();
-    if (tid == 0) plan_boundaries(P);
+    if (tid < 32) plan_boundaries_warp(P, tid);
+#ifdef WS_PLAN_CLOCK
+    if (tid == 0) atomicMax(&s_wclk[0], (unsigned long long)(clock64() - s_clk[0]));
+#endif
     // ---- row boxes of the wave + layer-set footprint, per field
     for (int fi = tid; fi < K.n_fields; fi += kPlanWork) {
       const DField& F = K.f[fi];
@@ -979,8 +1035,11 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
       ri.chunk_begin = 0;
       s_ri[fi] = ri;
     }
+#ifdef WS_PLAN_CLOCK
+    atomicMax(&s_wclk[1], (unsigned long long)(clock64() - s_clk[0]));
+#endif
     wbar();
-    __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' plane counts (fields with chunks)
+    __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' 8-plane chunk counts (fields with chunks)
     if (tid == 0) {
       long long cb = 0;
       int zo = 0;
@@ -988,16 +1047,20 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
         s_ri[fi].chunk_begin = cb;
         cb += s_ri[fi].n_chunks;
         s_zoff[fi] = zo;
-        if (s_ri[fi].n_chunks > 0) zo += (int)s_ri[fi].nz;
+        if (s_ri[fi].n_chunks > 0) zo += (int)((s_ri[fi].nz + 7) >> 3);
       }
       s_zoff[K.n_fields] = zo;
       s_nri = 0;
+#ifdef WS_PLAN_CLOCK
+      s_wclk[2] = (unsigned long long)(clock64() - s_clk[0]);
+#endif
     }
     wbar();
     // k_rows items: the chunks of computed planes (plane_rep(z) == z), listed per configuration;
     // derived planes are folded from their representative by k_fold (same rule).  The (field,
-    // plane) pairs of all fields are one flat range over the worker threads (LBM: many fields of
-    // few planes each).
+    // 8-plane window) pairs of all fields are one flat range over the worker threads; a window is
+    // walked by zone segments (plane_seg): the first `per` planes of a segment are computed, the
+    // rest of it is skipped at once (LBM, deep blocks: most planes are derived)
     const int nzt = s_zoff[K.n_fields];
     int fi = 0;
     for (int t = tid; t < nzt; t += kPlanWork) {
@@ -1007,19 +1070,42 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
       long long py, pz, falign;
       field_rows(F, P, ll, py, pz, falign);
       const int per = plane_period(pz, F.lg_elem, ll);
-      const int zi = t - s_zoff[fi];
-      const int z = (int)ri.z0 + zi;
-      if (plane_rep_f(F, K.g + F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2], P.fd_BF[2],
-                      per) != z)
-        continue;
-      const int at = atomicAdd(&s_nri, (int)ri.nseg);
-      for (int sg = 0; sg < (int)ri.nseg; ++sg) {
-        WS_CHK(at + sg, g_caps.clist_stride);
-        WS_CHK((long long)c * clist_stride + at + sg, g_caps.max_chunks);
-        cl[at + sg] = ((uint32_t)fi << 26) | (uint32_t)(ri.chunk_begin + (long long)zi * ri.nseg + sg);
+      const int zw = (int)ri.z0 + ((t - s_zoff[fi]) << 3), ze = min(zw + 8, (int)(ri.z0 + ri.nz));
+      unsigned cm = 0u;   // computed planes of the window (bit z - zw)
+      if (per <= 0) {
+        cm = (1u << (ze - zw)) - 1u;
+      } else {
+        for (int z = zw; z < ze;) {
+          int seg;
+          const int nb = plane_seg(F, K.g + F.g_begin, z, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
+                                   P.fd_BF[2], seg);
+          const int hi = nb < ze ? nb : ze;
+          const int ce = seg + per < hi ? seg + per : hi;   // computed planes [z, ce)
+          if (ce > z) cm |= ((1u << (ce - zw)) - 1u) & ~((1u << (z - zw)) - 1u);
+          z = hi;
+        }
+      }
+      if (cm == 0u) continue;
+      const int ncp = __popc(cm);
+      const int at = atomicAdd(&s_nri, ncp * (int)ri.nseg);
+      for (int i = 0; i < ncp; ++i) {
+        const int b = __fns(cm, 0, i + 1);
+        const long long zi = zw + b - ri.z0;
+        for (int sg = 0; sg < (int)ri.nseg; ++sg) {
+          const int slot = at + i * (int)ri.nseg + sg;
+          WS_CHK(slot, g_caps.clist_stride);
+          WS_CHK((long long)c * clist_stride + slot, g_caps.max_chunks);
+          cl[slot] = ((uint32_t)fi << 26) | (uint32_t)(ri.chunk_begin + zi * ri.nseg + sg);
+        }
       }
     }
+#ifdef WS_PLAN_CLOCK
+    atomicMax(&s_wclk[3], (unsigned long long)(clock64() - s_clk[0]));
+#endif
   }
+#ifdef WS_PLAN_CLOCK
+  if (tid == 0) s_clk[2] = clock64();
+#endif
   __syncthreads();   // join: the claim's row_owner, the workers' boxes and lists
   if (tid == 0) {
     const bool owner = P.row_owner == c;
@@ -1044,6 +1130,9 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     s_rb[0] = owner ? atomicAdd(rctr + par * 4 + 0, (unsigned long long)P.n_ritems) : 0ull;
     P.chunk_base = owner ? (long long)atomicAdd(rctr + par * 4 + 1, (unsigned long long)cb) : 0ll;
     s_rb[1] = owner ? atomicAdd(rctr + par * 4 + 2, (unsigned long long)P.n_fields) : 0ull;
+#ifdef WS_PLAN_CLOCK
+    s_clk[3] = clock64();
+#endif
   }
   __syncthreads();
   for (int fi = tid; fi < K.n_fields; fi += blockDim.x) rowinfo[(long long)c * kMaxFields + fi] = s_ri[fi];
@@ -1060,7 +1149,9 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
   PLAN_MARK()
 #ifdef WS_PLAN_CLOCK
   if (tid == 0 && (c == 0 || c == n - 1)) {
-    printf("PLANCLK c=%d", c);
+    printf("PLANCLK c=%d claim %lld workers %lld (ranges %llu boxes %llu prefix %llu list %llu) join %lld owner %d "
+           "nri %lld nf %d |", c, s_clk[1] - s_clk[0], s_clk[2] - s_clk[0], s_wclk[0], s_wclk[1], s_wclk[2], s_wclk[3],
+           s_clk[3] - s_clk[0], (int)(P.row_owner == c), (long long)P.n_ritems, K.n_fields);
     for (int i = 1; i < nclk; ++i) printf(" %lld", clk[i] - clk[i - 1]);
     printf(" total %lld\n", clk[nclk - 1] - clk[0]);
   }
@@ -1389,6 +1480,10 @@ struct SmBox {
 };
 constexpr int kMaxMembers = 32;
 
+struct SmBox32 {
+  int x0, x1, y0, y1, z0, z1;
+};
+
 // One block (single-block SM-set class of a kernel with many load fields, LBM): fields are
 // independent (they never alias), so each warp takes whole fields -- the field's footprint box
 // rows in contiguous lane chunks, per row the union of the load groups' x-intervals, an ordered
@@ -1598,9 +1693,6 @@ __device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ], int cnt = 32
   }
 }
 
-struct SmBox32 {
-  int x0, x1, y0, y1, z0, z1;
-};
 
 struct T32x2 {
   T32 s, l;
@@ -1754,7 +1846,7 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
                           SmBox* mb, SmBox32* mb32, Tri* pt /* 2*kMaxPlanes */, unsigned char* pder /* kMaxPlanes */,
                           SmWarp* sw,
                           unsigned long long& sum_s, unsigned long long& sum_l, unsigned long long& units,
-                          unsigned msk = 0u) {
+                          unsigned msk = 0u, int field_only = -1) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwp = blockDim.x >> 5;
   const int ls = G.lg_sector, ll = G.lg_line;
   const int nm = msk ? __popc(msk) : (int)(kj < kMaxMembers ? kj : kMaxMembers);
@@ -1782,7 +1874,7 @@ __device__ void smset_cta(const DPlan& P, const DKernel& K, const DGpu& G, long 
     zlo = min(zlo, mb[m].z0);
     zhi = max(zhi, mb[m].z1);
   }
-  for (int fi = 0; fi < K.n_fields; ++fi) {
+  for (int fi = field_only < 0 ? 0 : field_only; fi < (field_only < 0 ? K.n_fields : field_only + 1); ++fi) {
     const DField& F = K.f[fi];
     if (!(F.kinds & 1)) continue;
     const int g0 = F.g_begin, ng = F.g_end - F.g_begin;
@@ -2699,7 +2791,8 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
                                                 unsigned long long* __restrict__ sval,
                                                 const unsigned int* __restrict__ dmask,
                                                 const uint32_t* __restrict__ cfbl,
-                                                const unsigned long long* __restrict__ cctr) {
+                                                const unsigned long long* __restrict__ cctr,
+                                                const unsigned long long* __restrict__ rctr) {
   PDL_PROLOGUE();
   __shared__ long long s_item;
   __shared__ SmBox s_mb[kMaxMembers];
@@ -2710,7 +2803,11 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
   __shared__ unsigned long long s_wsum[3];
   // class entries: all of them, or (class-plane path) only those k_cplan left to the CTA path
   const long long ncls = cfbl ? (long long)cctr[2] : (long long)lists[1], ndir = (long long)lists[2];
-  const long long total = ncls + ndir;
+  // direct sets of kernels with many load fields split into (set, field) items: fs per set
+  // (k_plan's batch maximum; 1 when no such kernel is in the batch)
+  const unsigned long long fsr = rctr[rctr[8] * 4 + 3];
+  const long long fs = fsr > 1 ? (long long)fsr : 1;
+  const long long total = ncls + ndir * fs;
   if (total == 0) return;  // nothing for the CTA path (e.g. every SM set one block, classes by planes)
   // dynamic scheduling (lists[3], zeroed by the plan's scan): the directly evaluated sets --
   // the expensive, uneven entries -- first, then the single-block class representatives
@@ -2723,9 +2820,11 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
 #ifdef WS_SCLASS_TRACE
     const long long t_item0 = clock64();
 #endif
-    const bool cls = item >= ndir;
-    const long long ce = cls ? (cfbl ? (long long)cfbl[item - ndir] : item - ndir) : 0;
-    const unsigned long long ent = cls ? slist[ce] : dlist[item];
+    const bool cls = item >= ndir * fs;
+    const long long ce = cls ? (cfbl ? (long long)cfbl[item - ndir * fs] : item - ndir * fs) : 0;
+    const long long ditem = cls ? 0 : item / fs;
+    const int fsel = cls ? -1 : (int)(item - ditem * fs);
+    const unsigned long long ent = cls ? slist[ce] : dlist[ditem];
     const int c = (int)(ent >> 32);
     const unsigned low = (unsigned)(ent & 0xffffffffu);
     const DPlan& P = plans[c];
@@ -2749,18 +2848,29 @@ __global__ void __launch_bounds__(WS_SCLASS_THREADS, WS_SCLASS_MINB) k_sclass(co
       if (low & 0x80000000u) mult = 1ull + ((low >> 20) & 0x7ffu);
       S0 = P.s + jj;
       kj = (P.W - jj + nsm - 1) / nsm;
-      msk = dmask[item];
+      msk = dmask[ditem];
     }
     unsigned long long ss, sl, un;
-    int n_ld = 0;
-    for (int f = 0; f < ks[P.kid].n_fields; ++f) n_ld += ks[P.kid].f[f].kinds & 1;
-    // one block and many load fields (LBM: one offset each): flat rows over the whole CTA;
-    // otherwise plane derivation + lane-per-run unions
+    const int n_ld = ks[P.kid].env.n_ld;
+    int fonly = -1;   // (set, field) item of a many-field kernel's multi-block set; else the whole set
+    if (!cls && fs > 1) {
+      if (kj > 1 && n_ld > 4) {
+        if (fsel >= ks[P.kid].n_fields) continue;
+        fonly = fsel;
+      } else if (fsel != 0) {
+        continue;
+      }
+    }
+    // one block of a kernel with many load fields (LBM): warps over whole fields, row runs per
+    // plane (smset_eval_warps); otherwise the CTA's plane derivation + lane-per-run unions
+    // (smset_cta; a many-field kernel's multi-block set one field per item).  A/B on B200 (LBM15):
+    // multi-block LBM sets through a member-general smset_eval_warps made k_sclass 58 -> 85 us (a
+    // lane walks every (group, member) pair per row run, and the one-block case slowed too)
     if (kj == 1 && n_ld > 4) {
       smset_eval_warps(P, ks[P.kid], G, S0, s_wsum, ss, sl, un);
       if (threadIdx.x == 0) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     } else {        // several blocks: plane derivation + runs
-      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_mb32, s_pt, s_der, s_sw, ss, sl, un, msk);
+      smset_cta(P, ks[P.kid], G, S0, kj, nsm, s_mb, s_mb32, s_pt, s_der, s_sw, ss, sl, un, msk, fonly);
       // every warp's lane 0 counted its planes' rows
       if ((threadIdx.x & 31) == 0 && un) atomicAdd(work + (cls ? K_SCLASS : K_SMSET), un);
     }
@@ -4196,6 +4306,7 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   beg(K_SMSET, a);
   // the work-count prefix for the SM-set and warp chains (the row chain does not need it)
   k_scan<<<1, 256, 0, a>>>(s.plans, n, s.prefix, s.epoch);
+  ++L;
   cudaEventRecord(st.scanned, a);
   k_spairs<<<n_sm_dev * 4, kSmsetThreads, 0, a>>>(s.plans, s.prefix, n, d_k, d_g, s.scnt, s.srep, s.lists, s.slist,
                                                   s.dlist, s.skey, s.dmask, s.gkey);
@@ -4222,7 +4333,8 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   launch_k(pdl, k_sclass, n_sm_dev * g_sclass, WS_SCLASS_THREADS, a, (const DPlan*)s.plans, d_k, d_g, s.acc,
            (const unsigned int*)s.scnt, (const unsigned long long*)s.srep, s.lists, (const unsigned long long*)s.slist,
            (const unsigned long long*)s.dlist, s.work, s.sval, (const unsigned int*)s.dmask,
-           (const uint32_t*)(cplanes ? s.cfbl : nullptr), (const unsigned long long*)(s.lists + 4));
+           (const uint32_t*)(cplanes ? s.cfbl : nullptr), (const unsigned long long*)(s.lists + 4),
+           (const unsigned long long*)s.rctr);
   launch_k(pdl, k_sshare, n_sm_dev, 256, a, (const unsigned long long*)s.lists, (const unsigned long long*)s.slist,
            (const unsigned int*)s.scnt, (const unsigned long long*)s.sval, s.acc);
 #ifdef WS_SCLASS_TRACE

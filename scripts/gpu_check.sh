@@ -10,5 +10,5 @@ cat gpurun_out/bench.json
 python bench.py --impl reference > gpurun_out/bench_ref.json 2>gpurun_out/bench_ref.err
 cat gpurun_out/bench_ref.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-next > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(rows|sclass|wclass|fold|smset|plan|warp|model|cplan|cplanes|cfold|instr)" -s 24 -c 12 -o gpurun_out/full python scripts/ncu_target.py > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_(plan|rows|fold|scan|spairs|smset|cplan|cplanes|cfold|sclass|instr|warp|wclass|model)$" -s 28 -c 14 -o gpurun_out/full python scripts/ncu_target.py > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
