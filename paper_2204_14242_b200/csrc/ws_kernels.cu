@@ -1039,17 +1039,24 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     atomicMax(&s_wclk[1], (unsigned long long)(clock64() - s_clk[0]));
 #endif
     wbar();
-    __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' 8-plane chunk counts (fields with chunks)
+    __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' window counts (fields with chunks)
+    __shared__ int s_wsh;                    // window = 1 << s_wsh planes
     if (tid == 0) {
-      long long cb = 0;
+      long long cb = 0, npl = 0;
+      for (int fi = 0; fi < K.n_fields; ++fi)
+        if (s_ri[fi].n_chunks > 0) npl += s_ri[fi].nz;
+      // windows of 1-8 planes, about one per worker thread (the walk serialises a window's planes
+      // on one thread; many planes: 8-plane windows walked by zone segments)
+      const int wsh = npl <= kPlanWork ? 0 : (npl <= 2 * kPlanWork ? 1 : (npl <= 4 * kPlanWork ? 2 : 3));
       int zo = 0;
       for (int fi = 0; fi < K.n_fields; ++fi) {
         s_ri[fi].chunk_begin = cb;
         cb += s_ri[fi].n_chunks;
         s_zoff[fi] = zo;
-        if (s_ri[fi].n_chunks > 0) zo += (int)((s_ri[fi].nz + 7) >> 3);
+        if (s_ri[fi].n_chunks > 0) zo += (int)((s_ri[fi].nz + (1 << wsh) - 1) >> wsh);
       }
       s_zoff[K.n_fields] = zo;
+      s_wsh = wsh;
       s_nri = 0;
 #ifdef WS_PLAN_CLOCK
       s_wclk[2] = (unsigned long long)(clock64() - s_clk[0]);
@@ -1070,10 +1077,13 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
       long long py, pz, falign;
       field_rows(F, P, ll, py, pz, falign);
       const int per = plane_period(pz, F.lg_elem, ll);
-      const int zw = (int)ri.z0 + ((t - s_zoff[fi]) << 3), ze = min(zw + 8, (int)(ri.z0 + ri.nz));
+      const int zw = (int)ri.z0 + ((t - s_zoff[fi]) << s_wsh), ze = min(zw + (1 << s_wsh), (int)(ri.z0 + ri.nz));
       unsigned cm = 0u;   // computed planes of the window (bit z - zw)
       if (per <= 0) {
         cm = (1u << (ze - zw)) - 1u;
+      } else if (ze - zw == 1) {   // one plane: the direct test
+        cm = plane_rep_f(F, K.g + F.g_begin, zw, (int)ri.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2], P.fd_BF[2],
+                         per) == zw ? 1u : 0u;
       } else {
         for (int z = zw; z < ze;) {
           int seg;
