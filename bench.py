@@ -379,8 +379,15 @@ def run_native(args, rank, world, local):
                  "issue_peak_per_s": issue_peak, "issue_frac": warp_inst / (dom_ms / 1e3) / issue_peak,
                  "source": "profiles/ncu_traffic.json (ncu --set full, smsp__inst_executed.sum)"}
                 if warp_inst and dom_ms > 0 else None)
-    issue_by_kernel = {k: round(nt[k + ":warp_inst"] / (v[0] / v[1] / 1e3) / issue_peak, 4)
-                       for k, v in kern.items() if nt.get(k + ":warp_inst") and v[0] > 0}
+    # a profile bucket (CUDA events around a group of launches) against the warp instructions of
+    # every kernel in it
+    bucket = {"k_smset": ["k_scan", "k_spairs", "k_smset"],
+              "k_sclass": ["k_cplan", "k_cplanes", "k_cfold", "k_sclass", "k_sshare"]}
+    def bucket_inst(k):
+        parts = [nt.get(x + ":warp_inst") for x in bucket.get(k, [k])]
+        return sum(x for x in parts if x) if any(parts) else None
+    issue_by_kernel = {k: round(bucket_inst(k) / (v[0] / v[1] / 1e3) / issue_peak, 4)
+                       for k, v in kern.items() if bucket_inst(k) and v[0] > 0}
 
     strong = configs3_strong_measure(ctx, stream, args, rank, world, dev)
     cpu = None

@@ -981,6 +981,8 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
   __shared__ DRowInfo s_ri[kMaxFields];   // row boxes staged here, written out once
   __shared__ int s_nri;
   __shared__ unsigned long long s_rb[2];   // reserved bases: row items, fold items
+  __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' window counts (fields with chunks)
+  __shared__ int s_wsh;                    // listing window = 1 << s_wsh planes
   uint32_t* cl = clist + (long long)c * clist_stride;
 #ifdef WS_PLAN_CLOCK
   __shared__ long long s_clk[4];   // phase start, claim end, workers end, join end
@@ -1039,8 +1041,6 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
     atomicMax(&s_wclk[1], (unsigned long long)(clock64() - s_clk[0]));
 #endif
     wbar();
-    __shared__ int s_zoff[kMaxFields + 1];   // prefix of the fields' window counts (fields with chunks)
-    __shared__ int s_wsh;                    // window = 1 << s_wsh planes
     if (tid == 0) {
       long long cb = 0, npl = 0;
       for (int fi = 0; fi < K.n_fields; ++fi)
@@ -1160,8 +1160,10 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
 #ifdef WS_PLAN_CLOCK
   if (tid == 0 && (c == 0 || c == n - 1)) {
     printf("PLANCLK c=%d claim %lld workers %lld (ranges %llu boxes %llu prefix %llu list %llu) join %lld owner %d "
-           "nri %lld nf %d |", c, s_clk[1] - s_clk[0], s_clk[2] - s_clk[0], s_wclk[0], s_wclk[1], s_wclk[2], s_wclk[3],
-           s_clk[3] - s_clk[0], (int)(P.row_owner == c), (long long)P.n_ritems, K.n_fields);
+           "nri %lld nf %d b=(%d,%d,%d) f=(%d,%d,%d) nz0 %lld nseg0 %lld wsh %d nzt %d |", c, s_clk[1] - s_clk[0],
+           s_clk[2] - s_clk[0], s_wclk[0], s_wclk[1], s_wclk[2], s_wclk[3], s_clk[3] - s_clk[0],
+           (int)(P.row_owner == c), (long long)P.n_ritems, K.n_fields, P.b[0], P.b[1], P.b[2], P.f[0], P.f[1], P.f[2],
+           (long long)s_ri[0].nz, (long long)s_ri[0].nseg, s_wsh, s_zoff[K.n_fields]);
     for (int i = 1; i < nclk; ++i) printf(" %lld", clk[i] - clk[i - 1]);
     printf(" total %lld\n", clk[nclk - 1] - clk[0]);
   }
