@@ -270,19 +270,38 @@ __device__ __forceinline__ Tri tri_combine(const Tri& a, const Tri& b) {  // bra
   return Tri{ea ? b.f : a.f, eb ? a.l : b.l, a.c + b.c - ((!ea && !eb && a.l == b.f) ? 1 : 0)};
 }
 
+// Ordered warp reduction of NQ triples (lane order = address order), result in every lane.  The
+// fold of sorted element runs is associative with the only overlap between consecutive non-empty
+// triples (last == next first), so total count = sum of counts - #{consecutive non-empty pairs with
+// l_prev == f}, first = the first non-empty lane's f, last = the last non-empty lane's l: a ballot,
+// three shuffles and two sums per triple instead of a 5-level shuffle tree of whole triples.
+template <int NQ>
+__device__ __forceinline__ void warp_ordered_reduce(Tri (&t)[NQ]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const bool ne = t[q].c != 0;
+    const unsigned m = __ballot_sync(FULL, ne);
+    if (m == 0u) {
+      t[q] = tri_empty();
+      continue;
+    }
+    const unsigned below = m & lt;
+    const long long lprev = shfl64(t[q].l, below ? 31 - __clz(below) : lane);
+    long long c = t[q].c - ((ne && below && lprev == t[q].f) ? 1 : 0);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) c += shfl64_down(c, o);
+    t[q] = Tri{shfl64(t[q].f, __ffs(m) - 1), shfl64(t[q].l, 31 - __clz(m)), shfl64(c, 0)};
+  }
+}
+
 // Ordered CTA reduction of NQ triples per thread (thread order = row order).
 // Result valid in thread 0.  `sm` holds (blockDim/32)*NQ triples.
 template <int NQ>
 __device__ void cta_ordered_reduce(Tri (&t)[NQ], Tri* sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
-      if (lane + o < 32) t[q] = tri_combine(t[q], x);
-    }
-  }
+  warp_ordered_reduce<NQ>(t);
   if (lane == 0)
 #pragma unroll
     for (int q = 0; q < NQ; ++q) sm[warp * NQ + q] = t[q];
@@ -301,18 +320,6 @@ __device__ void cta_ordered_reduce(Tri (&t)[NQ], Tri* sm) {
   __syncthreads();
 }
 
-template <int NQ>
-__device__ __forceinline__ void warp_ordered_reduce(Tri (&t)[NQ]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      Tri x{shfl64_down(t[q].f, o), shfl64_down(t[q].l, o), shfl64_down(t[q].c, o)};
-      if (lane + o < 32) t[q] = tri_combine(t[q], x);
-    }
-  }
-}
 
 // Union of the element intervals produced by `gen` (each [xs, xe), xs < xe) in one
 // address row whose element 0 is at byte R0; appends the union's sectors/lines in
@@ -1692,16 +1699,24 @@ __device__ __forceinline__ T32 run_triple32(const RowFn& row, int step, int run,
 // lanes [0, cnt) hold data (lanes >= cnt empty): steps with offset >= cnt are no-ops
 template <int NQ>
 __device__ __forceinline__ void warp_ordered_reduce32(T32 (&t)[NQ], int cnt = 32) {
+  // as warp_ordered_reduce (sum of counts minus the consecutive-pair overlaps), 32-bit sums in one
+  // redux instruction each; cnt (lanes holding data) is no longer needed
+  (void)cnt;
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    if (o >= cnt) break;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const T32 x{__shfl_down_sync(FULL, t[q].f, o), __shfl_down_sync(FULL, t[q].l, o),
-                  __shfl_down_sync(FULL, t[q].c, o)};
-      if (lane + o < 32) t[q] = t32_combine(t[q], x);
+  for (int q = 0; q < NQ; ++q) {
+    const bool ne = t[q].c != 0;
+    const unsigned m = __ballot_sync(FULL, ne);
+    if (m == 0u) {
+      t[q] = t32_empty();
+      continue;
     }
+    const unsigned below = m & lt;
+    const int lprev = __shfl_sync(FULL, t[q].l, below ? 31 - __clz(below) : lane);
+    const unsigned dup = (ne && below && lprev == t[q].f) ? 1u : 0u;
+    const unsigned cs = __reduce_add_sync(FULL, (unsigned)t[q].c) - __reduce_add_sync(FULL, dup);
+    t[q] = T32{__shfl_sync(FULL, t[q].f, __ffs(m) - 1), __shfl_sync(FULL, t[q].l, 31 - __clz(m)), (int)cs};
   }
 }
 
