@@ -3171,7 +3171,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
   unsigned long long my_ops = 0;
   int ranges_c = -1;
   int c = -1;
+  // block-row span of each range: r in range q iff (unsigned)(r - rra[q]) <= rsp[q] (empty: rra far
+  // below every row, rsp 0); classification (r == rra) + 2 (r == rrl): 1 first, 2 last, 3 both, 0 inside
   int rra[5] = {0, 0, 0, 0, 0}, rrl[5] = {0, 0, 0, 0, 0};
+  unsigned rsp[5] = {0, 0, 0, 0, 0};
 #ifndef WS_ROWS_SPREAD
 #define WS_ROWS_SPREAD 0
 #endif
@@ -3225,9 +3228,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       __syncwarp();
       ranges_c = c;
 #pragma unroll
-      for (int q = 0; q < 5; ++q) {  // block-row span of each range in registers (empty: ra > rl)
-        rra[q] = P.rng[q].nonempty ? (int)P.rng[q].ra : 0x7fffffff;
-        rrl[q] = P.rng[q].nonempty ? (int)P.rng[q].rl : -0x7fffffff;
+      for (int q = 0; q < 5; ++q) {  // block-row span of each range in registers
+        rra[q] = P.rng[q].nonempty ? (int)P.rng[q].ra : -0x40000000;
+        rrl[q] = P.rng[q].nonempty ? (int)P.rng[q].rl : -0x40000000;
+        rsp[q] = P.rng[q].nonempty ? (unsigned)(P.rng[q].rl - P.rng[q].ra) : 0u;
       }
     }
     const int nb = P.nb;
@@ -3237,20 +3241,23 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
     const int pystep = (int)(py << le);
     if (lane < kNQ) X.pt[lane] = t32_empty();
     // this plane's valid groups and their block-row bases, once (lanes over the groups)
-    int ngv = 0;
-    for (int gb = 0; gb < ng; gb += 32) {
-      const int g = gb + lane;
-      bool v = false;
-      int2 e = make_int2(0, 0);
-      if (g < ng) {
-        const DGroup gr = K.g[g0 + g];
-        const int zz = z - gr.oz;
-        v = zz >= lo2 && zz < hi2;
-        if (v) e = make_int2(Gy * fdiv32(zz - lo2, fdz), (gr.oy << 8) | (gr.run << 1) | (gr.kind & 1));
+    int ngv = 0, ngl = 0;   // valid groups, loads first (ngl of them), then stores
+    for (int kind = 0; kind < 2; ++kind) {
+      for (int gb = 0; gb < ng; gb += 32) {
+        const int g = gb + lane;
+        bool v = false;
+        int2 e = make_int2(0, 0);
+        if (g < ng) {
+          const DGroup gr = K.g[g0 + g];
+          const int zz = z - gr.oz;
+          v = gr.kind == kind && zz >= lo2 && zz < hi2;
+          if (v) e = make_int2(Gy * fdiv32(zz - lo2, fdz), (gr.oy << 8) | (gr.run << 1) | (gr.kind & 1));
+        }
+        const unsigned bal = __ballot_sync(FULL, v);
+        if (v) X.gv[ngv + __popc(bal & ((1u << lane) - 1u))] = e;
+        ngv += __popc(bal);
       }
-      const unsigned bal = __ballot_sync(FULL, v);
-      if (v) X.gv[ngv + __popc(bal & ((1u << lane) - 1u))] = e;
-      ngv += __popc(bal);
+      if (kind == 0) ngl = ngv;
     }
     __syncwarp();
     for (int ys = ys0; ys < ys1; ys += kSegRows) {
@@ -3325,22 +3332,20 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
           const int run = X.rs[j + 1] - X.rs[j];
           my_ops += (unsigned long long)(30 * ng + 72 * run);
           unsigned long long mL[5] = {0, 0, 0, 0, 0}, mS[5] = {0, 0, 0, 0, 0};
-          for (int g = 0; g < ngv; ++g) {
+          auto classify = [&](int g, unsigned long long (&m)[5]) {
             const int2 e = X.gv[g];
             const int yy = y - (e.y >> 8);
-            if (yy < lo1 || yy >= hi1) continue;
-            const int r = fdiv32(yy - lo1, fdy) + e.x, grun = (e.y >> 1) & 15;
+            if (yy < lo1 || yy >= hi1) return;
+            const int r = fdiv32(yy - lo1, fdy) + e.x;
+            const unsigned long long b0 = 1ull << ((e.y >> 1) & 15);
 #pragma unroll
             for (int q = 0; q < 5; ++q) {  // classify32 from registers
-              const int ty = (r < rra[q] || r > rrl[q]) ? -1
-                             : (rra[q] == rrl[q] ? 3 : (r == rra[q] ? 1 : (r == rrl[q] ? 2 : 0)));
-              if (ty >= 0) {
-                const unsigned long long bit = 1ull << (ty * 16 + grun);
-                if (e.y & 1) mS[q] |= bit;
-                else mL[q] |= bit;
-              }
+              const int ty = (r == rra[q] ? 1 : 0) + (r == rrl[q] ? 2 : 0);
+              m[q] |= (unsigned)(r - rra[q]) <= rsp[q] ? b0 << (ty * 16) : 0ull;
             }
-          }
+          };
+          for (int g = 0; g < ngl; ++g) classify(g, mL);
+          for (int g = ngl; g < ngv; ++g) classify(g, mS);
           const int R0 = off0 + (y - y0) * pystep;
           const bool noS = mS[0] == 0ull, noL = mL[0] == 0ull;
           if (noS) {
