@@ -1052,9 +1052,11 @@ __global__ void __launch_bounds__(WS_PLAN_THREADS) k_plan(const ws_config* __res
       long long cb = 0, npl = 0;
       for (int fi = 0; fi < K.n_fields; ++fi)
         if (s_ri[fi].n_chunks > 0) npl += s_ri[fi].nz;
-      // windows of 1-8 planes, about one per worker thread (the walk serialises a window's planes
-      // on one thread; many planes: 8-plane windows walked by zone segments)
-      const int wsh = npl <= kPlanWork ? 0 : (npl <= 2 * kPlanWork ? 1 : (npl <= 4 * kPlanWork ? 2 : 3));
+      // up to 8 planes per worker thread: one-plane windows, the direct plane_rep test (clock
+      // probes: a window walk costs a thread more than 4-8 direct tests when the zone boundaries
+      // cluster, BJ configs[1] (1,16,64)+2z: 18k vs 9k cycles); more (LBM: 32 fields x ~260
+      // planes): 8-plane windows walked by zone segments (38k -> 10-20k cycles)
+      const int wsh = npl <= 8 * kPlanWork ? 0 : 3;
       int zo = 0;
       for (int fi = 0; fi < K.n_fields; ++fi) {
         s_ri[fi].chunk_begin = cb;
@@ -3947,6 +3949,21 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
     idx[i] = (uint32_t)i;
   }
   __syncthreads();
+  if (n <= 256) {
+    // small batch: each record's rank is the number of (key, index) pairs below its own -- one
+    // pass over the keys per thread, no sorting network (36 barrier-separated stages at n = 168)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long ki = key[i];
+      int r = 0;
+      for (int j = 0; j < n; ++j) {
+        const unsigned long long kj = key[j];
+        r += (kj < ki || (kj == ki && j < i)) ? 1 : 0;
+      }
+      out[i].rank = (uint32_t)r;
+      if (r < rank_k && top) top[r] = (uint32_t)i;
+    }
+    return;
+  }
   const int half = P >> 1;
   for (int kk = 2; kk <= P; kk <<= 1)
     for (int j = kk >> 1; j > 0; j >>= 1) {
