@@ -196,9 +196,10 @@ ws_status ws_estimate_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_r
 /* One sweep step end to end on the device ("the best configurations are selected",
  * P:1025-1046): ws_estimate_async of d_cfgs followed by ws_rank_async of d_out (d_top: k
  * device uint32 indices, may be null), records and top-k byte-identical to those two calls.
- * For n <= 1024 the FP64 model kernel (a7) also ranks (a8): its last CTA to finish sorts the
- * batch's (t_pred, index) keys in shared memory, saving the rank launch and a kernel boundary
- * on the critical path; larger batches call the two paths in turn.
+ * For n <= 1024 the FP64 model kernel (a7) also ranks (a8): its last CTA to finish ranks the
+ * batch's (t_pred, index) keys in shared memory (by counting for n <= 256, a sorting network
+ * above), saving the rank launch and a kernel boundary on the critical path; larger batches call
+ * the two paths in turn.
  * Device pointers, enqueued on the context stream; errors as ws_estimate_async / ws_rank_async. */
 ws_status ws_estimate_ranked_async(ws_ctx* ctx, const ws_config* d_cfgs, size_t n, ws_result* d_out, size_t k,
                                    uint32_t* d_top_idx);
@@ -223,8 +224,9 @@ uint32_t ws_last_group_count(const ws_ctx* ctx);
 /* Rank by (t_pred ascending, index ascending); failed configs rank last.
  * Fills res[i].rank and top_idx[0..min(k,n)) with the indices of the best.
  * ws_rank: host pointers, synchronous.  ws_rank_async: device pointers, no sync.
- * n <= 2^24 (WS_ELIMIT).  Device work: one CTA sorting in shared memory up to 16384 records,
- * a stable radix sort of 64-bit keys beyond (scratch kept by the context, grow-only). */
+ * n <= 2^24 (WS_ELIMIT).  Device work: one CTA sorting in shared memory up to 2048 records;
+ * up to 2^18: sorted tiles of 2048 / 4096 records and a binary-search merge-rank; beyond: a
+ * stable radix sort of 64-bit keys (scratch kept by the context, grow-only). */
 ws_status ws_rank(ws_ctx* ctx, ws_result* res, size_t n, size_t k, uint32_t* top_idx);
 ws_status ws_rank_async(ws_ctx* ctx, ws_result* d_res, size_t n, size_t k, uint32_t* d_top_idx);
 
