@@ -3376,18 +3376,15 @@ __global__ void __launch_bounds__(kRowWarps * 32, WS_ROWS_MINB) k_rows(const DPl
       }
       __syncwarp();
     }
-    if (lane == 0) {
+    if (lane < kNQ) {   // the plane's triples out, one per lane (X.pt written by lane 0 before the syncwarp)
+      const int q = lane;
       WS_CHK(P.chunk_base + ci, g_caps.max_chunks);
       long long* out = chunkres + (P.chunk_base + ci) * (kNQ * 3);
-      const long long bs = Bp >> ls, bl = Bp >> ll;
-#pragma unroll
-      for (int q = 0; q < kNQ; ++q) {
-        const long long b = (q == 2 || q == 4 || q == 6) ? bl : bs;
-        const T32 v = X.pt[q];
-        out[q * 3 + 0] = v.c ? v.f + b : 0;
-        out[q * 3 + 1] = v.c ? v.l + b : 0;
-        out[q * 3 + 2] = v.c;
-      }
+      const long long b = (q == 2 || q == 4 || q == 6) ? (Bp >> ll) : (Bp >> ls);
+      const T32 v = X.pt[q];
+      out[q * 3 + 0] = v.c ? v.f + b : 0;
+      out[q * 3 + 1] = v.c ? v.l + b : 0;
+      out[q * 3 + 2] = v.c;
     }
 #ifdef WS_ROWS_TRACE  // diagnostics build: per computed plane (config, field, z, runs, cycles)
     if (lane == 0 && item < kRowTrace) {
@@ -3426,6 +3423,7 @@ __device__ void fold_cta(const DPlan* __restrict__ plans, long long total, const
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
     const DGroup* gk = ks[P.kid].g + F.g_begin;
     const int per = plane_period(pz, F.lg_elem, ll);
+#pragma unroll 2   // two planes' loads in flight
     for (long long k = tid * per_l; k < nch && k < (tid + 1) * per_l; ++k) {
       // derived plane: its representative's triple, translated (plane_rep, as in k_plan)
       const long long pi = k / RI.nseg;
@@ -3528,6 +3526,7 @@ __global__ void __launch_bounds__(256, WS_FOLD_MINB) k_fold(const DPlan* __restr
     for (int q = 0; q < kNQ; ++q) t[q] = tri_empty();
     const DGroup* gk = ks[P.kid].g + F.g_begin;
     const int per = plane_period(pz, F.lg_elem, ll);
+#pragma unroll 2   // two planes' loads in flight
     for (long long k = lane * per_l; k < nch && k < (lane + 1) * per_l; ++k) {
       const long long pi = k / RI.nseg;   // derived plane: its representative's triple, translated
       const int zr = plane_rep_f(F, gk, (int)(RI.z0 + pi), (int)RI.z0, (int)P.lo[2], (int)P.hi[2], (int)P.BF[2],
