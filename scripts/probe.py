@@ -40,7 +40,8 @@ WORK = {
     "configs0": ("configs0 K7 64^3 V100 16", lambda: (W.k7(64), W.gpu_v100(), W.space_k7()), 20),
     "extended": ("extended K25 512^3 A100", lambda: (W.k25(512), W.gpu_a100(), W.space_extended()), 3),
 }
-# python scripts/probe.py [name ...]  (default: all; "configs1" alone as before)
-for name in (sys.argv[1:] or list(WORK)):
-    label, mk, reps = WORK[name]
-    run(label, *mk(), reps=reps)
+# python scripts/probe.py [name ...]  (default: all)
+if __name__ == "__main__":
+    for name in (sys.argv[1:] or list(WORK)):
+        label, mk, reps = WORK[name]
+        run(label, *mk(), reps=reps)
