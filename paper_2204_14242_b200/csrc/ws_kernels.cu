@@ -3893,6 +3893,7 @@ __global__ void __launch_bounds__(128) k_model(const DPlan* __restrict__ plans, 
                                                ws_result* __restrict__ out, int rank_k, uint32_t* __restrict__ top,
                                                unsigned long long* __restrict__ rank_ctr) {
   static_assert(sizeof(ws_result) % 8 == 0 && A_N <= 32, "record copy / accumulator lanes");
+  PDL_PROLOGUE();   // (WS_MODELPDL: k_fold's programmatic dependent; a no-op otherwise)
   __shared__ unsigned long long s_a[4][A_N];
   __shared__ ws_result s_r[4];
   __shared__ __align__(16) DPlan s_p[4];  // plan and GPU descriptor staged by the lanes (one load round)
@@ -4408,7 +4409,16 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
            s.acc, s.work, (Tri*)s.spart, s.sdone, (int)s.max_fields);
   end(K_SECT, b);
   // join
-  {  // join the other two chains into the caller's stream, which runs the model
+  // WS_MODELPDL=1 (A/B): the model runs on the row chain's stream as k_fold's programmatic dependent
+  // (after waiting for the other two chains), then the caller's stream joins it
+  static const bool model_pdl = getenv("WS_MODELPDL") && getenv("WS_MODELPDL")[0] == '1';
+  const bool mpdl = model_pdl && pdl && m != st.main && !fan;
+  if (mpdl) {
+    cudaEventRecord(st.join[0], a);
+    cudaEventRecord(st.join[1], b);
+    cudaStreamWaitEvent(m, st.join[0], 0);
+    cudaStreamWaitEvent(m, st.join[1], 0);
+  } else {  // join the other two chains into the caller's stream, which runs the model
     const cudaStream_t other = m == st.main ? b : m;
     m = st.main;
     cudaEventRecord(st.join[0], a);
@@ -4418,14 +4428,22 @@ int launch_estimate(const ws_config* d_cfgs, int n, const DKernel* d_k, int nk, 
   }
   beg(K_MODEL, m);
   if (tail && !fan && n <= kTailMax) {   // ws_estimate_ranked_async: the model's last CTA ranks
-    k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out, tail->k, tail->top, s.lists + 7);
+    launch_k(mpdl, k_model, (n + 3) / 4, 128, m, (const DPlan*)s.plans, n, d_k, d_g, (const unsigned long long*)s.acc,
+             d_out, tail->k, tail->top, s.lists + 7);
     tail->done = 1;
+  } else if (mpdl) {
+    launch_k(true, k_model, (n + 3) / 4, 128, m, (const DPlan*)s.plans, n, d_k, d_g, (const unsigned long long*)s.acc,
+             d_out, 0, (uint32_t*)nullptr, (unsigned long long*)nullptr);
   } else if (fan)
     k_model_fan<<<(unsigned)(((long long)fan->m * fan->n_gpu + 3) / 4), 128, 0, m>>>(s.plans, d_k, d_g, s.acc, *fan,
                                                                                     d_out);
   else
     k_model<<<(n + 3) / 4, 128, 0, m>>>(s.plans, n, d_k, d_g, s.acc, d_out, 0, nullptr, nullptr);
   end(K_MODEL, m);
+  if (mpdl) {   // the caller's stream waits for the model (on the row stream)
+    cudaEventRecord(st.fork, m);
+    cudaStreamWaitEvent(st.main, st.fork, 0);
+  }
   if (launches) *launches = L;
   return check_launch();
 }
