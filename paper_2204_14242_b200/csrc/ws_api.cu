@@ -83,10 +83,18 @@ struct ws_ctx {
     }
   };
   cudaStream_t cap = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  GKey gkey{};
-  uint32_t g_launches = 0;
-  int g_tail_done = 0;   // the captured graph's k_model also ranks (ws_estimate_ranked_async)
+  // captured estimate graphs, keyed by everything a capture bakes in (buffers, scratch, descriptor
+  // counts, fan-out, ranking): a few kept so that callers alternating buffers (double buffering)
+  // replay instead of re-capturing; round-robin replacement
+  struct GEntry {
+    cudaGraphExec_t exec = nullptr;
+    GKey key{};
+    uint32_t launches = 0;
+    int tail_done = 0;   // the captured graph's k_model also ranks (ws_estimate_ranked_async)
+  };
+  static constexpr int kGraphCache = 4;
+  GEntry gcache[kGraphCache];
+  int gnext = 0;
   void* wclean_ptr = nullptr;   // warp-class counter region known to be zero (ensure_scratch)
   size_t wclean_n = 0;
   bool graphs = true;
@@ -347,7 +355,8 @@ void ws_destroy(ws_ctx* c) {
   }
   if (c->fork) cudaEventDestroy(c->fork);
   if (c->scanned) cudaEventDestroy(c->scanned);
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  for (auto& ge : c->gcache)
+    if (ge.exec) cudaGraphExecDestroy(ge.exec);
   if (c->cap) cudaStreamDestroy(c->cap);
   delete c;
 }
@@ -714,30 +723,37 @@ static ws_status estimate_launch(ws_ctx* c, const ws_config* d_cfgs, size_t n, w
     const ws_ctx::GKey key{d_cfgs, d_out, c->scratch, c->dk, c->dg, n, (int)c->hk.size(), (int)c->hg.size(),
                            fan_hash(fan), xcfg, tail ? (const void*)tail->top : nullptr,
                            tail ? (long long)tail->k : -1ll};
-    if (!c->gexec || !(key == c->gkey)) {
-      if (c->gexec) {
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
+    int hit = -1;
+    for (int i = 0; i < ws_ctx::kGraphCache; ++i)
+      if (c->gcache[i].exec && c->gcache[i].key == key) hit = i;
+    if (hit < 0) {
+      hit = c->gnext;
+      c->gnext = (c->gnext + 1) % ws_ctx::kGraphCache;
+      ws_ctx::GEntry& ge = c->gcache[hit];
+      if (ge.exec) {
+        cudaGraphExecDestroy(ge.exec);
+        ge.exec = nullptr;
       }
       st.main = c->cap;
       cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
       if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
-      enqueue(&c->g_launches, nullptr);
+      enqueue(&ge.launches, nullptr);
       cudaGraph_t g = nullptr;
       e = cudaStreamEndCapture(c->cap, &g);
-      if (e == cudaSuccess) e = cudaGraphInstantiate(&c->gexec, g, 0);
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&ge.exec, g, 0);
       if (g) cudaGraphDestroy(g);
       if (e != cudaSuccess) {
-        c->gexec = nullptr;
+        ge.exec = nullptr;
         return cuda_fail(c, e, "graph instantiate");
       }
-      c->gkey = key;
-      c->g_tail_done = tail ? tail->done : 0;
+      ge.key = key;
+      ge.tail_done = tail ? tail->done : 0;
     }
-    if (tail) tail->done = c->g_tail_done;
-    cudaError_t e = cudaGraphLaunch(c->gexec, c->stream);
+    const ws_ctx::GEntry& ge = c->gcache[hit];
+    if (tail) tail->done = ge.tail_done;
+    cudaError_t e = cudaGraphLaunch(ge.exec, c->stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "graph launch");
-    c->last_launches = c->g_launches;
+    c->last_launches = ge.launches;
     return WS_OK;
   }
   int e = enqueue(&c->last_launches, ev);
