@@ -181,3 +181,26 @@ def test_estimate_ranked_byte_identical(ctx, case):
         assert top.cpu().tolist() == rtop.cpu().tolist(), (case, rep)
     r = np.frombuffer(ref.cpu().numpy().tobytes(), dtype=RESULT_DTYPE)
     assert sorted(r["rank"].tolist()) == list(range(n))
+
+
+def test_graph_cache_alternating_buffers(ctx):
+    """Double-buffered callers: ws_estimate_ranked_async alternating between two input / output
+    buffer pairs (the context keeps a captured graph per key) gives the same records every call."""
+    import torch
+    from paper_2204_14242_b200 import config_array
+    from paper_2204_14242_b200.ws import RESULT_DTYPE
+    kid, gid = ctx.describe_kernel(W.k25(80)), ctx.describe_gpu(W.gpu_a100())
+    a = config_array(kid, gid, W.space_stencil_paper()[::3])
+    n = len(a)
+    ref = ctx.estimate(a)
+    ctx.rank(ref, 5)
+    dc = [torch.from_numpy(a.view(np.uint8).copy()).cuda() for _ in range(2)]
+    do = [torch.zeros(n * RESULT_DTYPE.itemsize, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    tp = [torch.zeros(5, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for it in range(6):
+        b = it & 1
+        do[b].zero_()
+        torch.cuda.synchronize()
+        ctx.estimate_ranked_async(dc[b].data_ptr(), n, do[b].data_ptr(), 5, tp[b].data_ptr())
+        torch.cuda.synchronize()
+        assert do[b].cpu().numpy().tobytes() == ref.tobytes(), it
